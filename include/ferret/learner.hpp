@@ -1,0 +1,233 @@
+// ferret-b200 drop-in: the pipelined stream trainer.
+//
+// Public API of the reference's proj/include/ferret/learner.hpp that lies on
+// the hot path: kLearningRate/kReplayBuffer (:23-24), flatten/unflatten_into/
+// flatten_grads (:26-53), ReplayBuffer (:56-80), Compensator (:83-127),
+// TrainOutcome (:177-183), PipelineTrainOptions (:319-325), PipelineTrainer
+// (:330-520) and train_pipeline (:522-526).
+//
+// PipelineTrainer is a thin owner of a `ferret_trainer` handle: construction
+// uploads the net to the device, run() hands the event log and the stream to
+// ferret_trainer_run() (csrc/trainer.cpp), which replays the log with sm_100a
+// kernels, then reads the parameters and the normalizer back so the returned
+// TrainOutcome has the reference's shape. The reference trainer keys in-flight
+// state by (worker, item) and therefore never trains; this
+// implementation keys by item, which is the behaviour the reference intends.
+// B200Options::as_shipped = true reproduces the shipped no-op instead.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <vector>
+
+#include "ferret/b200_status.hpp"
+#include "ferret/compensate.hpp"
+#include "ferret/metrics.hpp"
+#include "ferret/net.hpp"
+#include "ferret/rng.hpp"
+#include "ferret/sim.hpp"
+#include "ferret/stream.hpp"
+#include "ferret/types.hpp"
+#include "ferret_b200.h"
+
+namespace ferret {
+
+inline constexpr double kLearningRate = 1e-3;
+inline constexpr std::size_t kReplayBuffer = 5000;
+
+inline ParamVec flatten(const DenseNet& net) {
+    ParamVec v;
+    v.reserve(net.n_params());
+    for (const DenseLayer& l : net.layers) {
+        v.insert(v.end(), l.W.begin(), l.W.end());
+        v.insert(v.end(), l.b.begin(), l.b.end());
+    }
+    return v;
+}
+
+inline void unflatten_into(DenseNet& net, const ParamVec& v) {
+    auto src = v.begin();
+    for (DenseLayer& l : net.layers) {
+        std::copy(src, src + static_cast<std::ptrdiff_t>(l.W.size()), l.W.begin());
+        src += static_cast<std::ptrdiff_t>(l.W.size());
+        std::copy(src, src + static_cast<std::ptrdiff_t>(l.b.size()), l.b.begin());
+        src += static_cast<std::ptrdiff_t>(l.b.size());
+    }
+}
+
+inline ParamVec flatten_grads(const Gradients& g) {
+    ParamVec v;
+    for (std::size_t k = 0; k < g.W.size(); ++k) {
+        v.insert(v.end(), g.W[k].begin(), g.W[k].end());
+        v.insert(v.end(), g.b[k].begin(), g.b[k].end());
+    }
+    return v;
+}
+
+// Reservoir of seen samples (reference learner.hpp:56-80); the device trainer
+// runs the same reservoir on item indices (csrc/trainer.cpp, ReplayIndex).
+class ReplayBuffer {
+  public:
+    ReplayBuffer(std::size_t capacity, std::uint64_t seed) : cap_(capacity), gen_(seed ^ 0xbf58476d1ce4e5b9ULL) {}
+
+    void add(const Sample& s) {
+        ++seen_;
+        if (pool_.size() < cap_) {
+            pool_.push_back(s);
+            return;
+        }
+        const std::uint64_t slot = gen_.below(seen_);
+        if (slot < cap_) pool_[static_cast<std::size_t>(slot)] = s;
+    }
+
+    bool empty() const { return pool_.empty(); }
+
+    const Sample& sample() { return pool_[static_cast<std::size_t>(gen_.below(pool_.size()))]; }
+
+  private:
+    std::size_t cap_;
+    Rng gen_;
+    std::uint64_t seen_ = 0;
+    std::vector<Sample> pool_;
+};
+
+// Per-policy compensation context over one flat parameter space
+// (reference learner.hpp:83-127); apply() runs on the device.
+class Compensator {
+  public:
+    Compensator(CompensationPolicy policy, std::size_t n_params, double lambda0 = 0.2, double eta_lambda = 1e-3,
+                double alpha = 0.99, double nu = 2e-6)
+        : policy_(policy), lambda0_(lambda0) {
+        if (policy_ == CompensationPolicy::iter_fisher)
+            state_ = CompensatorState::make(n_params, lambda0, eta_lambda, alpha, nu);
+        else if (policy_ == CompensationPolicy::gap)
+            mean_gap_.assign(n_params, 0.0);
+    }
+
+    ParamVec apply(const ParamVec& g, const std::vector<ParamVec>& chain) {
+        if (chain.empty()) throw std::invalid_argument("Compensator::apply: empty version chain");
+        if (policy_ == CompensationPolicy::none) return g;
+        std::vector<const double*> links;
+        for (const ParamVec& v : chain) links.push_back(v.data());
+        if (policy_ == CompensationPolicy::iter_fisher) {
+            const bool learn = state_.eta_lambda > 0.0;
+            return detail::device_compensate(static_cast<int>(policy_), g, links, state_.lambda.data(),
+                                             learn ? state_.v_r.data() : nullptr, learn ? state_.v_a.data() : nullptr,
+                                             nullptr, lambda0_, state_.alpha, state_.eta_lambda, state_.nu);
+        }
+        return detail::device_compensate(static_cast<int>(policy_), g, links, nullptr, nullptr, nullptr,
+                                         mean_gap_.empty() ? nullptr : mean_gap_.data(), lambda0_, 0.99, 0.0, 0.0);
+    }
+
+  private:
+    CompensationPolicy policy_;
+    double lambda0_;
+    CompensatorState state_;
+    ParamVec mean_gap_;
+};
+
+struct TrainOutcome {
+    std::vector<StepRecord> log;
+    DenseNet net;
+    RunningNormalizer normalizer;
+
+    double oacc() const { return online_accuracy(log); }
+};
+
+struct PipelineTrainOptions {
+    CompensationPolicy policy = CompensationPolicy::none;
+    double lr = kLearningRate;
+    double eta_lambda = 1e-3;
+    bool replay = false;
+    std::uint64_t replay_seed = 0;
+};
+
+// B200-side knobs with no reference counterpart (ABI-stable side struct).
+struct B200Options {
+    int precision = FERRET_PREC_FP32; // fp32 parity mode
+    int micro_batch = 1;              // 1 = reference semantics
+    int device = 0;
+    bool as_shipped = false;
+};
+
+class PipelineTrainer {
+  public:
+    PipelineTrainer(DenseNet net, const PartitionScheme& scheme, const PipelineTrainOptions& opt,
+                    const B200Options& b200 = B200Options{})
+        : net_(std::move(net)) {
+        net_.validate();
+        scheme.validate(net_.layers.size());
+        std::vector<uint64_t> in, out, bounds(scheme.bounds.begin(), scheme.bounds.end());
+        std::vector<int32_t> act;
+        for (const DenseLayer& l : net_.layers) {
+            in.push_back(l.in);
+            out.push_back(l.out);
+            act.push_back(static_cast<int32_t>(l.act));
+        }
+        const ParamVec params = flatten(net_);
+        const ferret_net_desc desc{static_cast<int32_t>(net_.layers.size()), in.data(), out.data(), act.data(),
+                                   params.data()};
+        ferret_train_opts o;
+        ferret_train_opts_default(&o);
+        o.policy = static_cast<int32_t>(opt.policy);
+        o.lr = opt.lr;
+        o.eta_lambda = opt.eta_lambda;
+        o.replay = opt.replay ? 1 : 0;
+        o.replay_seed = opt.replay_seed;
+        o.replay_capacity = kReplayBuffer;
+        o.precision = b200.precision;
+        o.micro_batch = b200.micro_batch;
+        o.device = b200.device;
+        o.as_shipped = b200.as_shipped ? 1 : 0;
+        ferret_trainer* raw = nullptr;
+        b200_check(ferret_trainer_create(&desc, bounds.data(), static_cast<int32_t>(bounds.size()), &o, &raw));
+        handle_.reset(raw);
+    }
+
+    TrainOutcome run(const SimTrace& trace, const DataStream& stream) {
+        std::vector<ferret_event> events;
+        events.reserve(trace.events.size());
+        for (const SimEvent& e : trace.events)
+            events.push_back(ferret_event{e.time, static_cast<int32_t>(e.kind), e.worker, e.stage, e.staleness, e.item,
+                                          e.version});
+        const std::size_t n = stream.items.size(), f = stream.n_features;
+        std::vector<double> features(n * f);
+        std::vector<uint64_t> labels(n);
+        for (std::size_t i = 0; i < n; ++i) {
+            std::copy(stream.items[i].features.begin(), stream.items[i].features.end(), features.begin() + i * f);
+            labels[i] = stream.items[i].label;
+        }
+        std::vector<ferret_step_record> raw_log(n);
+        b200_check(ferret_trainer_run(handle_.get(), events.data(), events.size(), features.data(), labels.data(), n, f,
+                                      raw_log.data()));
+        TrainOutcome res{std::vector<StepRecord>(n), net_, RunningNormalizer(f)};
+        for (std::size_t i = 0; i < n; ++i)
+            res.log[i] = StepRecord{raw_log[i].item, static_cast<StepOutcome>(raw_log[i].outcome),
+                                    static_cast<std::size_t>(raw_log[i].predicted),
+                                    static_cast<std::size_t>(raw_log[i].label)};
+        ParamVec params(net_.n_params());
+        b200_check(ferret_trainer_params(handle_.get(), params.data(), params.size()));
+        unflatten_into(res.net, params);
+        uint64_t count = 0;
+        std::vector<double> mean(f), m2(f);
+        b200_check(ferret_trainer_normalizer(handle_.get(), &count, mean.data(), m2.data(), f));
+        res.normalizer.restore(static_cast<std::size_t>(count), std::move(mean), std::move(m2));
+        return res;
+    }
+
+    ferret_trainer* handle() { return handle_.get(); }
+
+  private:
+    struct Release {
+        void operator()(ferret_trainer* t) const { ferret_trainer_destroy(t); }
+    };
+    DenseNet net_;
+    std::unique_ptr<ferret_trainer, Release> handle_;
+};
+
+inline TrainOutcome train_pipeline(DenseNet net, const PartitionScheme& scheme, const SimTrace& trace,
+                                   const DataStream& stream, const PipelineTrainOptions& opt) {
+    return PipelineTrainer(std::move(net), scheme, opt).run(trace, stream);
+}
+
+} // namespace ferret

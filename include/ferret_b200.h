@@ -1,0 +1,243 @@
+/* ferret-b200 C ABI — the boundary between the reference-shaped C++ API
+ * (the headers in include/ferret/, namespace ferret) and the sm_100a implementation in
+ * libferret_b200.so. Plain C types only: no torch, no STL, no CUDA types.
+ *
+ * Every entry point below replaces one reference interface; the citation is
+ * the reference file:line of the call it stands in for
+ * (reference root: proj/include/ferret/).
+ *
+ * Conventions
+ *   - Caller owns every input buffer (read-only; copied as needed) and every
+ *     output buffer (caller-allocated, sizes stated per function).
+ *   - Every function returns ferret_status; FERRET_OK == 0. On failure
+ *     ferret_last_error() returns the message (thread-local), and the status
+ *     maps 1:1 onto the exception type the reference throws
+ *     (types.hpp:13-25, compensate.hpp:17, learner.hpp:276, sim.hpp:396).
+ *   - A trainer is single-threaded like the reference's PipelineTrainer
+ *     (learner.hpp:330); one trainer per host thread.
+ *   - There is no CPU fallback: without a usable sm_100 device every
+ *     trainer/compute call returns FERRET_E_NO_DEVICE.
+ */
+#ifndef FERRET_B200_H
+#define FERRET_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define FERRET_API __attribute__((visibility("default")))
+#else
+#define FERRET_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    FERRET_OK = 0,
+    FERRET_E_SCHEMA = 1,       /* ferret::SchemaError            types.hpp:13 */
+    FERRET_E_BOUND = 2,        /* ferret::BoundError             types.hpp:18 */
+    FERRET_E_CONFIG = 3,       /* ferret::ConfigError            types.hpp:23 */
+    FERRET_E_INVALID_ARG = 4,  /* std::invalid_argument          compensate.hpp:17, net.hpp:159 */
+    FERRET_E_OUT_OF_RANGE = 5, /* std::out_of_range              learner.hpp:276, compensate.hpp:155 */
+    FERRET_E_LOGIC = 6,        /* std::logic_error               sim.hpp:396 */
+    FERRET_E_CUDA = 7,         /* CUDA runtime failure (no reference counterpart) */
+    FERRET_E_NO_DEVICE = 8     /* no sm_100 device visible (no reference counterpart) */
+} ferret_status;
+
+/* EventKind, sim.hpp:23 */
+enum { FERRET_EV_ARRIVAL = 0, FERRET_EV_DROP = 1, FERRET_EV_FORWARD = 2,
+       FERRET_EV_RECOMPUTE = 3, FERRET_EV_BACKWARD = 4, FERRET_EV_UPDATE = 5 };
+/* CompensationPolicy, compensate.hpp:20 */
+enum { FERRET_POLICY_NONE = 0, FERRET_POLICY_STEP = 1, FERRET_POLICY_GAP = 2,
+       FERRET_POLICY_FISHER = 3, FERRET_POLICY_ITER_FISHER = 4 };
+/* Activation, net.hpp:17 */
+enum { FERRET_ACT_RELU = 0, FERRET_ACT_IDENTITY = 1 };
+/* StepOutcome, metrics.hpp:15 */
+enum { FERRET_STEP_CORRECT = 0, FERRET_STEP_WRONG = 1, FERRET_STEP_DROPPED = 2 };
+/* arithmetic of the device path (no reference counterpart: the reference is fp64) */
+enum { FERRET_PREC_FP32 = 0, FERRET_PREC_BF16 = 1 };
+
+/* DenseNet, net.hpp:20-51. params in flatten() order (learner.hpp:26-34):
+ * per layer W (row-major out x in) then b. */
+typedef struct {
+    int32_t n_layers;
+    const uint64_t* in;
+    const uint64_t* out;
+    const int32_t* act;
+    const double* params;
+} ferret_net_desc;
+
+/* PipelineTrainOptions, learner.hpp:319-325, plus the Compensator constants
+ * (learner.hpp:85-86, compensate.hpp:59-64), the replay capacity
+ * (learner.hpp:24) and the B200-side knobs. Fill with
+ * ferret_train_opts_default() before editing. */
+typedef struct {
+    int32_t policy;            /* FERRET_POLICY_*; reference default none */
+    double lr;                 /* 1e-3 */
+    double eta_lambda;         /* 1e-3 */
+    double lambda0;            /* 0.2 */
+    double alpha;              /* 0.99 */
+    double nu;                 /* 2e-6 */
+    int32_t replay;            /* 0/1 */
+    uint64_t replay_seed;      /* 0 */
+    uint64_t replay_capacity;  /* 5000 */
+    int32_t precision;         /* FERRET_PREC_FP32 */
+    int32_t micro_batch;       /* stream samples per pipeline unit; 1 = reference semantics */
+    int32_t device;            /* CUDA ordinal of this stage group */
+    int32_t as_shipped;        /* 1: reproduce the reference's worker-keyed no-op trainer */
+} ferret_train_opts;
+
+/* SimEvent, sim.hpp:38-46 */
+typedef struct {
+    double time;
+    int32_t kind;
+    int32_t worker;
+    int32_t stage;
+    int32_t staleness;
+    int64_t item;
+    int64_t version;
+} ferret_event;
+
+/* StepRecord, metrics.hpp:18-23 */
+typedef struct {
+    int64_t item;
+    int32_t outcome;
+    int32_t _pad;
+    uint64_t predicted;
+    uint64_t label;
+} ferret_step_record;
+
+/* LayerProfile, types.hpp:35-40 */
+typedef struct {
+    double t_f;
+    double t_b;
+    uint64_t w;
+    uint64_t a;
+} ferret_layer_profile;
+
+/* StreamSpec, types.hpp:139-151 */
+typedef struct {
+    double t_d;
+    double decay_c;
+    double value;
+    double horizon;
+} ferret_stream_spec;
+
+FERRET_API const char* ferret_last_error(void);
+FERRET_API const char* ferret_version(void);
+/* 1 if an sm_100 device is visible and the kernels in this library load on it */
+FERRET_API int32_t ferret_device_available(void);
+
+FERRET_API void ferret_train_opts_default(ferret_train_opts* opts);
+
+/* ---------------- host tiers (bit-exact with the reference) ---------------- */
+
+/* make_dense_net, net.hpp:54-71; params_out sized ferret_net_param_count */
+FERRET_API size_t ferret_net_param_count(const uint64_t* widths, int32_t n_widths);
+FERRET_API ferret_status ferret_make_dense_net(const uint64_t* widths, int32_t n_widths, uint64_t seed,
+                                    int32_t hidden_act, double* params_out, size_t n_params);
+
+/* profile_from_net, net.hpp:263-274; layers_out has n_widths-1 entries */
+FERRET_API ferret_status ferret_profile_from_widths(const uint64_t* widths, int32_t n_widths,
+                                         double seconds_per_param, ferret_layer_profile* layers_out);
+
+/* synth_drift_stream, stream.hpp:43-87; features_out n*n_features (row-major), labels_out n */
+FERRET_API ferret_status ferret_synth_drift_stream(size_t n, size_t n_features, size_t n_classes, int32_t drift,
+                                        uint64_t seed, double rotate_rate, double noise,
+                                        double* features_out, uint64_t* labels_out);
+
+/* A schedule = plan (planner.hpp:192) or forced partition + default_config
+ * (planner.hpp:54), stage_stats (profile.hpp:167) and simulate (sim.hpp:401). */
+typedef struct ferret_schedule ferret_schedule;
+
+FERRET_API ferret_status ferret_schedule_plan(const ferret_layer_profile* layers, int32_t n_layers, double t_d,
+                                   const ferret_stream_spec* spec, uint64_t budget, int32_t max_stages,
+                                   size_t n_items, ferret_schedule** out);
+FERRET_API ferret_status ferret_schedule_forced(const ferret_layer_profile* layers, int32_t n_layers, double t_d,
+                                     const ferret_stream_spec* spec, const uint64_t* bounds,
+                                     int32_t n_bounds, int32_t recompute, size_t n_items,
+                                     ferret_schedule** out);
+/* number of bounds; copies min(n, cap) into out */
+FERRET_API int32_t ferret_schedule_bounds(const ferret_schedule* s, uint64_t* out, int32_t cap);
+FERRET_API size_t ferret_schedule_event_count(const ferret_schedule* s);
+FERRET_API ferret_status ferret_schedule_events(const ferret_schedule* s, ferret_event* out, size_t cap);
+/* write_plan (planner.hpp:219) / write_trace (sim.hpp:408) text; returns bytes
+ * needed incl. NUL, copies up to cap */
+FERRET_API size_t ferret_schedule_plan_text(const ferret_schedule* s, char* buf, size_t cap);
+FERRET_API size_t ferret_schedule_trace_text(const ferret_schedule* s, char* buf, size_t cap);
+FERRET_API void ferret_schedule_destroy(ferret_schedule* s);
+
+/* ---------------- hot path: PipelineTrainer on sm_100a ---------------- */
+
+typedef struct ferret_trainer ferret_trainer;
+
+/* PipelineTrainer(DenseNet, PartitionScheme, PipelineTrainOptions), learner.hpp:332-346 */
+FERRET_API ferret_status ferret_trainer_create(const ferret_net_desc* net, const uint64_t* bounds, int32_t n_bounds,
+                                    const ferret_train_opts* opts, ferret_trainer** out);
+
+/* PipelineTrainer::run(trace, stream), learner.hpp:348-363 — end to end:
+ * copies the host stream in, replays the event log on the device, copies the
+ * StepRecord log out (n_items entries). Synchronous. n_items counts stream
+ * samples (= trace items x micro_batch). */
+FERRET_API ferret_status ferret_trainer_run(ferret_trainer* t, const ferret_event* events, size_t n_events,
+                                 const double* features, const uint64_t* labels, size_t n_items,
+                                 size_t n_features, ferret_step_record* log_out);
+
+/* Split form of ferret_trainer_run for device-resident timing:
+ * load_stream (H2D) -> execute(chunk) (async on ferret_trainer_stream) ->
+ * fetch_log (D2H). execute() replays the event log over samples
+ * [chunk*n_chunk_items, (chunk+1)*n_chunk_items) of the loaded stream and
+ * continues training from the current state (normalizer included). */
+FERRET_API ferret_status ferret_trainer_load_stream(ferret_trainer* t, const double* features, const uint64_t* labels,
+                                         size_t n_items, size_t n_features);
+FERRET_API ferret_status ferret_trainer_set_schedule(ferret_trainer* t, const ferret_event* events, size_t n_events,
+                                          size_t n_chunk_items);
+FERRET_API ferret_status ferret_trainer_execute(ferret_trainer* t, size_t chunk);
+FERRET_API ferret_status ferret_trainer_fetch_log(ferret_trainer* t, size_t chunk, ferret_step_record* log_out);
+FERRET_API ferret_status ferret_trainer_sync(ferret_trainer* t);
+/* cudaStream_t the trainer launches on, as an opaque pointer (for CUDA-event timing) */
+FERRET_API void* ferret_trainer_stream(ferret_trainer* t);
+
+/* TrainOutcome::net (learner.hpp:177-181): current params, fp64, flatten() order */
+FERRET_API ferret_status ferret_trainer_params(ferret_trainer* t, double* out, size_t n);
+/* per-stage compensator state (compensate.hpp:55-58); any pointer may be NULL.
+ * mean_gap is the gap policy's running mean (learner.hpp:126). n = stage params */
+FERRET_API ferret_status ferret_trainer_comp_state(ferret_trainer* t, int32_t stage, double* lambda, double* v_r,
+                                        double* v_a, double* mean_gap, size_t n);
+/* TrainOutcome::normalizer (learner.hpp:180): count, mean[f], m2[f] */
+FERRET_API ferret_status ferret_trainer_normalizer(ferret_trainer* t, uint64_t* count, double* mean, double* m2,
+                                        size_t n_features);
+/* counters of the last execute/run: kernel launches, ring depth per stage, ... */
+typedef struct {
+    uint64_t kernel_launches;
+    uint64_t events;
+    uint64_t updates;
+    uint64_t replays;
+    uint64_t predicts;
+    int32_t ring_depth[16];
+    int32_t stash_slots;
+    double mean_tau[16];         /* mean trainer staleness per update, per stage */
+    uint64_t update_elems[16];   /* params touched by updates per stage */
+    uint64_t device_bytes;       /* HBM the trainer allocated */
+} ferret_trainer_stats;
+FERRET_API ferret_status ferret_trainer_get_stats(ferret_trainer* t, ferret_trainer_stats* out);
+FERRET_API void ferret_trainer_destroy(ferret_trainer* t);
+
+/* ---------------- unit entry: the fused compensation kernel ---------------- */
+
+/* One Compensator::apply (learner.hpp:97-120) on the device, fp32:
+ * chain = chain_len parameter versions oldest first (chain_len = tau + 1),
+ * state arrays updated in place (lambda/v_r/v_a for iter_fisher, mean_gap for gap;
+ * NULL where the policy has none). lambda0 is the fisher policy's fixed lambda. */
+FERRET_API ferret_status ferret_compensate(int32_t policy, const double* g, const double* const* chain,
+                                int32_t chain_len, double* lambda, double* v_r, double* v_a,
+                                double* mean_gap, size_t n, double lambda0, double alpha,
+                                double eta_lambda, double nu, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FERRET_B200_H */

@@ -1,0 +1,13 @@
+"""ferret-b200: B200-native pipelined stream training (Ferret, arXiv 2503.12053).
+
+The product is ``libferret_b200.so`` (C ABI in include/ferret_b200.h, C++
+drop-in headers in include/ferret/). This package is the Python mirror of the
+reference's API on top of it; see ``ferret.py``.
+"""
+from .ferret import (  # noqa: F401
+    EVENT_DTYPE, RECORD_DTYPE, PROFILE_DTYPE, NO_BUDGET, POLICIES,
+    BoundError, ConfigError, DeviceError, LogicError, SchemaError,
+    PipelineTrainOptions, PipelineTrainer, Schedule, StreamSpec,
+    compensate, device_available, lib, make_dense_net, online_accuracy, param_count,
+    profile_from_widths, synth_drift_stream, train_pipeline,
+)

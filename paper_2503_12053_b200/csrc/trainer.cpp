@@ -1,0 +1,1007 @@
+// ferret_trainer: PipelineTrainer (reference learner.hpp:330-526) on one B200.
+//
+// The reference interprets the simulator's event log one event at a time on
+// the host, copying whole nets per event. Here the log is compiled into a
+// sequence of sm_100a kernel launches whose device pointers are all resolved
+// on the host, in two passes over the log:
+//   1. a dry run on a copy of the host state sizes the HBM structures exactly:
+//      the per-stage version ring (depth = the longest live chain + 1, not the
+//      reference's leaky hold set, learner.hpp:419/507) and the stash slots
+//      (one per in-flight pipeline unit, freed at the unit's last use);
+//   2. the real pass launches the kernels on one CUDA stream in log order.
+// Everything the north star requires to be bit-exact (routing, schedule,
+// replay indices) is decided here on the host with the reference's own
+// arithmetic; the device only does fp32 math.
+//
+// HBM layout: per stage a ring of `depth` version slots
+// (fp32, per-layer W/b at 128-byte-aligned offsets), the compensator state
+// (lambda offset, v_r, v_a or mean_gap) of the same shape, the normalised
+// stream x[n][F], and the stash: per in-flight unit every layer's activation
+// and delta (B x width).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "common.hpp"
+#include "ferret/rng.hpp"
+#include "kernels.cuh"
+
+using fb200::fail;
+using fb200::guarded;
+
+namespace {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(FERRET_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+long long align_up(long long v, long long a) { return (v + a - 1) / a * a; }
+
+template <class T>
+T* dalloc(size_t n, size_t& counter) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    cuda_check(cudaMalloc(&p, n * sizeof(T)), "cudaMalloc");
+    counter += n * sizeof(T);
+    return static_cast<T*>(p);
+}
+
+void dfree(void* p) {
+    if (p) cudaFree(p);
+}
+
+// Reservoir over stream positions (reference ReplayBuffer, learner.hpp:56-80):
+// identical RNG draws; stores the sample's index instead of its features
+// because the normalised features of every sample stay resident in HBM.
+struct ReplayIndex {
+    uint64_t cap = 0;
+    ferret::Rng rng{0};
+    uint64_t seen = 0;
+    std::vector<long long> items;
+
+    ReplayIndex() = default;
+    ReplayIndex(uint64_t capacity, uint64_t seed) : cap(capacity), rng(seed ^ 0xbf58476d1ce4e5b9ULL) {}
+
+    void add(long long id) {
+        ++seen;
+        if (items.size() < cap) {
+            items.push_back(id);
+            return;
+        }
+        const uint64_t at = rng.below(seen);
+        if (at < cap) items[static_cast<size_t>(at)] = id;
+    }
+    bool empty() const { return items.empty(); }
+    long long sample() { return items[static_cast<size_t>(rng.below(items.size()))]; }
+};
+
+struct HostState {
+    std::vector<long long> current;  // per stage: version of the live parameters
+    ReplayIndex replay;
+    uint64_t norm_count = 0;
+};
+
+struct LayerDev {
+    int in = 0, out = 0, act = 0, stage = 0;
+    long long woff = 0, boff = 0;      // inside the stage slot
+    long long host_off = 0;            // in flatten() order of the whole net
+    long long act_off = 0, dlt_off = 0; // inside a stash slot
+};
+
+struct StageDev {
+    int lo = 0, hi = 0;
+    long long n_params = 0, slot_floats = 0, host_off = 0;
+    int total_rows = 0;
+    int depth = 0;
+    float* ring = nullptr;
+    float* lam_d = nullptr;
+    float* v_r = nullptr;
+    float* v_a = nullptr;
+    float* gap = nullptr;
+    fb200::UpdLayer* L_dev = nullptr;
+    float* slot(long long v) const { return ring + (v % depth) * slot_floats; }
+};
+
+// Schedule facts independent of the mutable state (computed once per log).
+struct Schedule {
+    std::vector<ferret_event> events;
+    size_t n_units = 0;
+    size_t chunk_items = 0;               // stream samples per execute()
+    std::vector<char> dropped;            // per unit
+    std::vector<char> has_bwd;            // per unit x stage
+    std::vector<long long> last_use;      // per unit: last event index touching its stash
+    std::vector<std::vector<size_t>> free_at; // per event index: units whose stash frees after it
+};
+
+struct PassResult {
+    std::vector<int> need_depth;
+    int need_slots = 0;
+};
+
+} // namespace
+
+struct ferret_trainer {
+    ferret_train_opts opt{};
+    int B = 1, P = 0, L = 0, F = 0, n_out = 0;
+    std::vector<LayerDev> layers;
+    std::vector<StageDev> stages;
+    std::vector<double> init_params;
+    cudaStream_t stream = nullptr;
+    size_t device_bytes = 0;
+
+    // stream resident in HBM
+    double* d_raw = nullptr;
+    float* d_x = nullptr;
+    int* d_pred = nullptr;
+    size_t n_loaded = 0;
+    std::vector<int> labels;
+    double* d_norm_mean = nullptr;
+    double* d_norm_m2 = nullptr;
+
+    // scratch
+    float* d_stash = nullptr;
+    long long stash_stride = 0;
+    int stash_slots = 0;
+    float* d_pred_buf = nullptr;  // 2 x B x max_width
+    long long pred_stride = 0;
+    float* d_replay = nullptr;    // one stash-shaped slot
+    float* d_partial = nullptr;
+    unsigned* d_counters = nullptr;
+
+    HostState hs;
+    Schedule sched;
+    bool have_schedule = false;
+
+    ferret_trainer_stats stats{};
+    uint64_t launches = 0;
+
+    ~ferret_trainer() {
+        cudaSetDevice(opt.device);
+        if (stream) cudaStreamSynchronize(stream);
+        for (StageDev& s : stages) {
+            dfree(s.ring);
+            dfree(s.lam_d);
+            dfree(s.v_r);
+            dfree(s.v_a);
+            dfree(s.gap);
+            dfree(s.L_dev);
+        }
+        dfree(d_raw);
+        dfree(d_x);
+        dfree(d_pred);
+        dfree(d_norm_mean);
+        dfree(d_norm_m2);
+        dfree(d_stash);
+        dfree(d_pred_buf);
+        dfree(d_replay);
+        dfree(d_partial);
+        dfree(d_counters);
+        if (stream) cudaStreamDestroy(stream);
+    }
+
+    // ------------------------------------------------------------------ setup
+    void build(const ferret_net_desc& net, const uint64_t* bounds, int32_t n_bounds) {
+        L = net.n_layers;
+        if (L <= 0) fail(FERRET_E_CONFIG, "net needs at least one layer");
+        if (n_bounds < 2 || bounds[0] != 0 || bounds[n_bounds - 1] != static_cast<uint64_t>(L))
+            fail(FERRET_E_CONFIG, "partition bounds must run from 0 to the layer count");
+        for (int32_t i = 1; i < n_bounds; ++i)
+            if (bounds[i] <= bounds[i - 1]) fail(FERRET_E_CONFIG, "partition bounds must be strictly increasing");
+        P = n_bounds - 1;
+        if (P > 16) fail(FERRET_E_CONFIG, "at most 16 stages per trainer");
+        B = opt.micro_batch;
+        if (B < 1 || B > fb200::kMaxBatch) fail(FERRET_E_CONFIG, "micro_batch must lie in [1, 16]");
+        if (opt.policy < 0 || opt.policy > 4) fail(FERRET_E_CONFIG, "unknown compensation policy");
+        if (opt.precision != FERRET_PREC_FP32) fail(FERRET_E_CONFIG, "only the fp32 parity precision is built");
+        layers.resize(static_cast<size_t>(L));
+        long long host_off = 0;
+        for (int l = 0; l < L; ++l) {
+            LayerDev& ld = layers[static_cast<size_t>(l)];
+            ld.in = static_cast<int>(net.in[l]);
+            ld.out = static_cast<int>(net.out[l]);
+            ld.act = net.act[l];
+            if (l > 0 && net.in[l] != net.out[l - 1])
+                fail(FERRET_E_CONFIG, "layer " + std::to_string(l) + ": input width mismatch");
+            ld.host_off = host_off;
+            host_off += static_cast<long long>(ld.in) * ld.out + ld.out;
+        }
+        F = layers.front().in;
+        n_out = layers.back().out;
+        init_params.assign(net.params, net.params + host_off);
+        // stash layout (per unit): activation + delta of every layer, B x out each
+        long long cursor = 0;
+        int max_width = F;
+        for (LayerDev& ld : layers) {
+            ld.act_off = align_up(cursor, 32);
+            cursor = ld.act_off + static_cast<long long>(B) * ld.out;
+            ld.dlt_off = align_up(cursor, 32);
+            cursor = ld.dlt_off + static_cast<long long>(B) * ld.out;
+            max_width = std::max(max_width, ld.out);
+        }
+        stash_stride = align_up(cursor, 64);
+        pred_stride = align_up(static_cast<long long>(B) * max_width, 64);
+        // stages
+        stages.resize(static_cast<size_t>(P));
+        hs.current.assign(static_cast<size_t>(P), 0);
+        size_t max_partial = 1, max_tiles = 1;
+        for (int j = 0; j < P; ++j) {
+            StageDev& s = stages[static_cast<size_t>(j)];
+            s.lo = static_cast<int>(bounds[j]);
+            s.hi = static_cast<int>(bounds[j + 1]);
+            if (s.hi - s.lo > fb200::kMaxStageLayers) fail(FERRET_E_CONFIG, "at most 16 layers per stage");
+            s.host_off = layers[static_cast<size_t>(s.lo)].host_off;
+            long long c = 0;
+            std::vector<fb200::UpdLayer> tab;
+            for (int l = s.lo; l < s.hi; ++l) {
+                LayerDev& ld = layers[static_cast<size_t>(l)];
+                ld.stage = j;
+                ld.woff = align_up(c, 32);
+                c = ld.woff + static_cast<long long>(ld.in) * ld.out;
+                ld.boff = align_up(c, 32);
+                c = ld.boff + ld.out;
+                s.n_params += static_cast<long long>(ld.in) * ld.out + ld.out;
+                fb200::UpdLayer ul{};
+                ul.in = ld.in;
+                ul.out = ld.out;
+                ul.woff = ld.woff;
+                ul.boff = ld.boff;
+                ul.row0 = s.total_rows;
+                ul.xin_off = l == 0 ? -1 : layers[static_cast<size_t>(l - 1)].act_off;
+                ul.dlt_off = ld.dlt_off;
+                tab.push_back(ul);
+                s.total_rows += ld.out;
+                if (l > 0) {
+                    max_partial = std::max(max_partial, static_cast<size_t>(fb200::bwd_row_splits(ld.in, ld.out)) *
+                                                            static_cast<size_t>(B) * static_cast<size_t>(ld.in));
+                    max_tiles = std::max(max_tiles, static_cast<size_t>(fb200::bwd_col_tiles(ld.in)));
+                }
+            }
+            s.slot_floats = align_up(c, 64);
+            s.L_dev = dalloc<fb200::UpdLayer>(tab.size(), device_bytes);
+            cuda_check(cudaMemcpy(s.L_dev, tab.data(), tab.size() * sizeof(fb200::UpdLayer), cudaMemcpyHostToDevice),
+                       "upload layer table");
+            const size_t n = static_cast<size_t>(s.slot_floats);
+            if (opt.policy == FERRET_POLICY_ITER_FISHER) {
+                s.lam_d = dalloc<float>(n, device_bytes);
+                cuda_check(cudaMemset(s.lam_d, 0, n * sizeof(float)), "memset");
+                if (opt.eta_lambda > 0.0) {
+                    s.v_r = dalloc<float>(n, device_bytes);
+                    s.v_a = dalloc<float>(n, device_bytes);
+                    cuda_check(cudaMemset(s.v_r, 0, n * sizeof(float)), "memset");
+                    cuda_check(cudaMemset(s.v_a, 0, n * sizeof(float)), "memset");
+                }
+            } else if (opt.policy == FERRET_POLICY_GAP) {
+                s.gap = dalloc<float>(n, device_bytes);
+                cuda_check(cudaMemset(s.gap, 0, n * sizeof(float)), "memset");
+            }
+            grow_ring(s, 2);
+        }
+        upload_initial_params();
+        d_pred_buf = dalloc<float>(static_cast<size_t>(2 * pred_stride), device_bytes);
+        d_replay = dalloc<float>(static_cast<size_t>(stash_stride), device_bytes);
+        d_partial = dalloc<float>(max_partial, device_bytes);
+        d_counters = dalloc<unsigned>(max_tiles, device_bytes);
+        cuda_check(cudaMemset(d_counters, 0, max_tiles * sizeof(unsigned)), "memset");
+        d_norm_mean = dalloc<double>(static_cast<size_t>(F), device_bytes);
+        d_norm_m2 = dalloc<double>(static_cast<size_t>(F), device_bytes);
+        cuda_check(cudaMemset(d_norm_mean, 0, static_cast<size_t>(F) * sizeof(double)), "memset");
+        cuda_check(cudaMemset(d_norm_m2, 0, static_cast<size_t>(F) * sizeof(double)), "memset");
+        hs.replay = ReplayIndex(opt.replay_capacity, opt.replay_seed);
+    }
+
+    void upload_initial_params() {
+        for (StageDev& s : stages) {
+            std::vector<float> slot(static_cast<size_t>(s.slot_floats), 0.f);
+            for (int l = s.lo; l < s.hi; ++l) {
+                const LayerDev& ld = layers[static_cast<size_t>(l)];
+                const double* src = init_params.data() + ld.host_off;
+                const long long nw = static_cast<long long>(ld.in) * ld.out;
+                for (long long i = 0; i < nw; ++i) slot[static_cast<size_t>(ld.woff + i)] = static_cast<float>(src[i]);
+                for (int r = 0; r < ld.out; ++r)
+                    slot[static_cast<size_t>(ld.boff + r)] = static_cast<float>(src[nw + r]);
+            }
+            cuda_check(cudaMemcpy(s.slot(0), slot.data(), slot.size() * sizeof(float), cudaMemcpyHostToDevice),
+                       "upload params");
+        }
+    }
+
+    // Grow a stage ring to `depth` slots, keeping the live version.
+    void grow_ring(StageDev& s, int depth) {
+        if (depth <= s.depth) return;
+        float* fresh = dalloc<float>(static_cast<size_t>(depth) * static_cast<size_t>(s.slot_floats), device_bytes);
+        if (s.ring) {
+            const long long v = hs.current[static_cast<size_t>(&s - stages.data())];
+            cuda_check(cudaStreamSynchronize(stream), "sync");
+            cuda_check(cudaMemcpy(fresh + (v % depth) * s.slot_floats, s.slot(v),
+                                  static_cast<size_t>(s.slot_floats) * sizeof(float), cudaMemcpyDeviceToDevice),
+                       "ring copy");
+            cudaFree(s.ring);
+            device_bytes -= static_cast<size_t>(s.depth) * static_cast<size_t>(s.slot_floats) * sizeof(float);
+        }
+        s.ring = fresh;
+        s.depth = depth;
+    }
+
+    void ensure_stash(int slots) {
+        if (slots <= stash_slots) return;
+        cuda_check(cudaStreamSynchronize(stream), "sync");
+        if (d_stash) {
+            cudaFree(d_stash);
+            device_bytes -= static_cast<size_t>(stash_slots) * static_cast<size_t>(stash_stride) * sizeof(float);
+        }
+        d_stash = dalloc<float>(static_cast<size_t>(slots) * static_cast<size_t>(stash_stride), device_bytes);
+        stash_slots = slots;
+    }
+
+    // ---------------------------------------------------------------- stream
+    void load_stream(const double* features, const uint64_t* lab, size_t n, size_t f) {
+        if (static_cast<int>(f) != F) fail(FERRET_E_INVALID_ARG, "stream feature width does not match the net input");
+        cuda_check(cudaStreamSynchronize(stream), "sync");
+        if (n > n_loaded) {
+            dfree(d_raw);
+            dfree(d_x);
+            dfree(d_pred);
+            d_raw = dalloc<double>(n * f, device_bytes);
+            d_x = dalloc<float>(n * f, device_bytes);
+            d_pred = dalloc<int>(n, device_bytes);
+        }
+        n_loaded = n;
+        labels.resize(n);
+        for (size_t i = 0; i < n; ++i) {
+            if (lab[i] >= static_cast<uint64_t>(n_out)) fail(FERRET_E_INVALID_ARG, "forward_backward: label out of range");
+            labels[i] = static_cast<int>(lab[i]);
+        }
+        cuda_check(cudaMemcpyAsync(d_raw, features, n * f * sizeof(double), cudaMemcpyHostToDevice, stream), "H2D stream");
+    }
+
+    void set_schedule(const ferret_event* ev, size_t n_ev, size_t chunk_items) {
+        Schedule s;
+        s.events.assign(ev, ev + n_ev);
+        // arrivals: units 0..n-1 in order (sim.hpp:171-173 pushes them by time)
+        long long expect = 0;
+        for (const ferret_event& e : s.events) {
+            if (e.kind == FERRET_EV_ARRIVAL) {
+                if (e.item != expect) fail(FERRET_E_INVALID_ARG, "event log: arrivals must cover items 0..n-1 in order");
+                ++expect;
+            }
+        }
+        s.n_units = static_cast<size_t>(expect);
+        s.chunk_items = chunk_items ? chunk_items : s.n_units * static_cast<size_t>(B);
+        if (s.n_units * static_cast<size_t>(B) > s.chunk_items)
+            fail(FERRET_E_INVALID_ARG, "event log covers more samples than one chunk");
+        s.dropped.assign(s.n_units, 0);
+        s.has_bwd.assign(s.n_units * static_cast<size_t>(P), 0);
+        s.last_use.assign(s.n_units, -1);
+        std::map<std::pair<int, int>, std::vector<long long>> open;  // (worker, stage) -> units awaiting update
+        for (size_t i = 0; i < s.events.size(); ++i) {
+            const ferret_event& e = s.events[i];
+            const bool staged = e.kind == FERRET_EV_FORWARD || e.kind == FERRET_EV_BACKWARD || e.kind == FERRET_EV_UPDATE;
+            if (staged && (e.stage < 0 || e.stage >= P))
+                fail(FERRET_E_INVALID_ARG, "event log: stage out of range for this partition");
+            if (e.kind != FERRET_EV_UPDATE && e.kind != FERRET_EV_ARRIVAL && e.kind != FERRET_EV_DROP &&
+                e.kind != FERRET_EV_FORWARD && e.kind != FERRET_EV_BACKWARD && e.kind != FERRET_EV_RECOMPUTE)
+                fail(FERRET_E_INVALID_ARG, "event log: unknown event kind");
+            if (e.kind != FERRET_EV_UPDATE && (e.item < 0 || static_cast<size_t>(e.item) >= s.n_units))
+                fail(FERRET_E_INVALID_ARG, "event log: item out of range");
+            const size_t u = static_cast<size_t>(e.item);
+            switch (e.kind) {
+                case FERRET_EV_DROP: s.dropped[u] = 1; break;
+                case FERRET_EV_ARRIVAL:
+                case FERRET_EV_FORWARD: s.last_use[u] = static_cast<long long>(i); break;
+                case FERRET_EV_BACKWARD:
+                    s.last_use[u] = static_cast<long long>(i);
+                    s.has_bwd[u * static_cast<size_t>(P) + static_cast<size_t>(e.stage)] = 1;
+                    open[{e.worker, e.stage}].push_back(static_cast<long long>(u));
+                    break;
+                case FERRET_EV_UPDATE: {
+                    auto it = open.find({e.worker, e.stage});
+                    if (it == open.end()) break;
+                    for (long long uu : it->second) s.last_use[static_cast<size_t>(uu)] = static_cast<long long>(i);
+                    it->second.clear();
+                    break;
+                }
+                default: break;
+            }
+        }
+        s.free_at.assign(s.events.size(), {});
+        for (size_t u = 0; u < s.n_units; ++u)
+            if (!s.dropped[u] && s.last_use[u] >= 0) s.free_at[static_cast<size_t>(s.last_use[u])].push_back(u);
+        sched = std::move(s);
+        have_schedule = true;
+    }
+
+    // -------------------------------------------------------------- execute
+    void execute(size_t chunk) {
+        if (!have_schedule) fail(FERRET_E_LOGIC, "execute: no schedule set");
+        const size_t base = chunk * sched.chunk_items;
+        const size_t n_samples = sched.n_units * static_cast<size_t>(B);
+        if (base + n_samples > n_loaded) fail(FERRET_E_OUT_OF_RANGE, "execute: chunk lies beyond the loaded stream");
+        launches = 0;
+        // 1. RunningNormalizer over every arrival of the chunk (observed in order,
+        //    dropped ones included: learner.hpp:393); model-independent, so it
+        //    is one kernel up front instead of one per arrival.
+        fb200::NormArgs na{d_raw + base * static_cast<size_t>(F), static_cast<long long>(n_samples), F,
+                           static_cast<unsigned long long>(hs.norm_count), d_norm_mean, d_norm_m2,
+                           d_x + base * static_cast<size_t>(F)};
+        fb200::launch_normalize(na, stream);
+        ++launches;
+        hs.norm_count += n_samples;
+        // 2. dry run -> sizes
+        HostState probe = hs;
+        const PassResult need = run_pass<true>(probe, base);
+        for (int j = 0; j < P; ++j) grow_ring(stages[static_cast<size_t>(j)], need.need_depth[static_cast<size_t>(j)]);
+        ensure_stash(std::max(need.need_slots, 1));
+        // 3. real pass
+        run_pass<false>(hs, base);
+        cuda_check(cudaGetLastError(), "kernel launch");
+        stats.kernel_launches = launches;
+        stats.stash_slots = stash_slots;
+        for (int j = 0; j < P && j < 16; ++j) stats.ring_depth[j] = stages[static_cast<size_t>(j)].depth;
+    }
+
+    template <bool DRY>
+    PassResult run_pass(HostState& st, size_t base) {
+        PassResult res;
+        res.need_depth.assign(static_cast<size_t>(P), 2);
+        const bool as_shipped = opt.as_shipped != 0;
+        const size_t n_units = sched.n_units;
+        std::vector<int> slot_of(n_units, -1);
+        std::vector<int> free_slots;
+        int slots_used = 0;
+        std::vector<char> inflight(n_units, 0);
+        std::vector<long long> read_ver(n_units * static_cast<size_t>(P), -1);
+        std::vector<std::map<long long, int>> live(static_cast<size_t>(P));  // live read versions per stage
+        struct Pend {
+            size_t u;
+            long long read;
+        };
+        std::map<std::pair<int, int>, std::vector<Pend>> pending;
+        uint64_t n_upd = 0, n_rep = 0, n_pred = 0;
+        std::vector<double> tau_sum(static_cast<size_t>(P), 0.0);
+        std::vector<uint64_t> tau_cnt(static_cast<size_t>(P), 0);
+
+        auto floor_of = [&](int j) {
+            const long long cur = st.current[static_cast<size_t>(j)];
+            const auto& m = live[static_cast<size_t>(j)];
+            return m.empty() ? cur : std::min(m.begin()->first, cur);
+        };
+        auto note_push = [&](int j) {  // a new version of stage j is about to be written
+            const long long span = st.current[static_cast<size_t>(j)] - floor_of(j) + 2;
+            int& d = res.need_depth[static_cast<size_t>(j)];
+            d = std::max(d, static_cast<int>(span));
+            if (!DRY && span > stages[static_cast<size_t>(j)].depth)
+                fail(FERRET_E_LOGIC, "version ring undersized (dry run disagrees with the real pass)");
+        };
+        auto stash = [&](size_t u) { return d_stash + static_cast<long long>(slot_of[u]) * stash_stride; };
+        auto xrows = [&](size_t u) { return d_x + (base + u * static_cast<size_t>(B)) * static_cast<size_t>(F); };
+
+        for (size_t idx = 0; idx < sched.events.size(); ++idx) {
+            const ferret_event& e = sched.events[idx];
+            const size_t u = static_cast<size_t>(e.item);
+            const int j = e.stage;
+            switch (e.kind) {
+                case FERRET_EV_ARRIVAL: {  // learner.hpp:389-410
+                    if (sched.dropped[u]) break;
+                    inflight[u] = 1;
+                    if (!as_shipped) {
+                        if (free_slots.empty()) free_slots.push_back(slots_used++);
+                        slot_of[u] = free_slots.back();
+                        free_slots.pop_back();
+                    }
+                    ++n_pred;
+                    if (!DRY) launch_predict(u, base, st);
+                    if (opt.replay)
+                        for (int b = 0; b < B; ++b)
+                            st.replay.add(static_cast<long long>(base + u * static_cast<size_t>(B) + static_cast<size_t>(b)));
+                    break;
+                }
+                case FERRET_EV_FORWARD: {  // learner.hpp:412-433
+                    if (as_shipped || !inflight[u]) break;
+                    const long long v = st.current[static_cast<size_t>(j)];
+                    read_ver[u * static_cast<size_t>(P) + static_cast<size_t>(j)] = v;
+                    if (sched.has_bwd[u * static_cast<size_t>(P) + static_cast<size_t>(j)]) live[static_cast<size_t>(j)][v] += 1;
+                    if (!DRY) launch_stage_forward(j, stages[static_cast<size_t>(j)].slot(v), stash(u), xrows(u));
+                    break;
+                }
+                case FERRET_EV_BACKWARD: {  // learner.hpp:435-479
+                    if (as_shipped || !inflight[u]) break;
+                    const long long r = read_ver[u * static_cast<size_t>(P) + static_cast<size_t>(j)];
+                    if (r < 0) fail(FERRET_E_OUT_OF_RANGE, "stage version evicted");
+                    if (!DRY) {
+                        int lab[fb200::kMaxBatch];
+                        for (int b = 0; b < B; ++b) lab[b] = labels[base + u * static_cast<size_t>(B) + static_cast<size_t>(b)];
+                        launch_stage_backward(j, stages[static_cast<size_t>(j)].slot(r), stash(u), lab);
+                    }
+                    pending[{e.worker, j}].push_back({u, r});
+                    break;
+                }
+                case FERRET_EV_UPDATE: {  // learner.hpp:491-510
+                    if (as_shipped) break;
+                    auto it = pending.find({e.worker, j});
+                    if (it == pending.end() || it->second.empty()) break;
+                    const std::vector<Pend>& pl = it->second;
+                    if (pl.size() > static_cast<size_t>(fb200::kMaxPending))
+                        fail(FERRET_E_CONFIG, "accumulation count above 16 is not supported by the update kernel");
+                    note_push(j);
+                    const long long cur = st.current[static_cast<size_t>(j)];
+                    for (const Pend& p : pl) {
+                        tau_sum[static_cast<size_t>(j)] += static_cast<double>(cur - p.read);
+                        tau_cnt[static_cast<size_t>(j)] += 1;
+                    }
+                    if (!DRY) {
+                        fb200::UpdArgs a = update_args(j, cur);
+                        a.policy = opt.policy;
+                        a.K = static_cast<int>(pl.size());
+                        for (size_t k = 0; k < pl.size(); ++k)
+                            a.pend[k] = {stash(pl[k].u), xrows(pl[k].u), pl[k].read};
+                        a.step = static_cast<float>(opt.lr * (1.0 / static_cast<double>(pl.size())));
+                        fb200::launch_update(a, stream);
+                        ++launches;
+                    }
+                    st.current[static_cast<size_t>(j)] += 1;
+                    ++n_upd;
+                    for (const Pend& p : pl) {
+                        auto& m = live[static_cast<size_t>(j)];
+                        auto lv = m.find(p.read);
+                        if (lv != m.end() && --lv->second == 0) m.erase(lv);
+                    }
+                    it->second.clear();
+                    if (j == 0 && opt.replay && !st.replay.empty()) {  // learner.hpp:509, 513-519
+                        ++n_rep;
+                        replay_step<DRY>(st, note_push);
+                    }
+                    break;
+                }
+                default: break;  // drop, recompute: no trainer work (learner.hpp:359)
+            }
+            if (!as_shipped)
+                for (size_t fu : sched.free_at[idx])
+                    if (slot_of[fu] >= 0) {
+                        free_slots.push_back(slot_of[fu]);
+                        slot_of[fu] = -1;
+                    }
+        }
+        res.need_slots = slots_used;
+        if (!DRY) {
+            stats.events = sched.events.size();
+            stats.updates = n_upd;
+            stats.replays = n_rep;
+            stats.predicts = n_pred;
+            for (int j = 0; j < P && j < 16; ++j) {
+                stats.mean_tau[j] = tau_cnt[static_cast<size_t>(j)] ? tau_sum[static_cast<size_t>(j)] /
+                                                                         static_cast<double>(tau_cnt[static_cast<size_t>(j)])
+                                                                   : 0.0;
+                stats.update_elems[j] = static_cast<uint64_t>(stages[static_cast<size_t>(j)].n_params) * tau_cnt[static_cast<size_t>(j)];
+            }
+        }
+        return res;
+    }
+
+    fb200::UpdArgs update_args(int j, long long cur) {
+        const StageDev& s = stages[static_cast<size_t>(j)];
+        fb200::UpdArgs a{};
+        a.n_layers = s.hi - s.lo;
+        a.total_rows = s.total_rows;
+        a.B = B;
+        a.L = s.L_dev;
+        a.x0_gather = 0;
+        a.x0_ld = F;
+        a.ring = s.ring;
+        a.slot_floats = s.slot_floats;
+        a.depth = s.depth;
+        a.cur_version = cur;
+        a.lam_d = s.lam_d;
+        a.v_r = s.v_r;
+        a.v_a = s.v_a;
+        a.gap = s.gap;
+        a.lambda0 = static_cast<float>(opt.lambda0);
+        a.alpha = static_cast<float>(opt.alpha);
+        a.eta = static_cast<float>(opt.eta_lambda);
+        a.nu = static_cast<float>(opt.nu);
+        return a;
+    }
+
+    // One dense layer on B samples whose input row b is X + xoff[b].
+    void launch_layer(const LayerDev& ld, const float* stage_slot, const float* X, const long long* xoff, float* Y) {
+        fb200::FwdArgs a{};
+        a.W = stage_slot + ld.woff;
+        a.bias = stage_slot + ld.boff;
+        a.X = X;
+        for (int b = 0; b < B; ++b) a.xoff[b] = xoff[b];
+        a.Y = Y;
+        a.in = ld.in;
+        a.out = ld.out;
+        a.B = B;
+        a.relu = ld.act == FERRET_ACT_RELU;
+        fb200::launch_fwd(a, stream);
+        ++launches;
+    }
+
+    void contiguous_rows(long long* xoff, int width) const {
+        for (int b = 0; b < B; ++b) xoff[b] = static_cast<long long>(b) * width;
+    }
+
+    // predict_class(net_, x) at the arrival (learner.hpp:398-399): full net, live versions.
+    void launch_predict(size_t u, size_t base, const HostState& st) {
+        long long xoff[fb200::kMaxBatch];
+        const float* X = d_x + (base + u * static_cast<size_t>(B)) * static_cast<size_t>(F);
+        contiguous_rows(xoff, F);
+        for (int l = 0; l < L; ++l) {
+            const LayerDev& ld = layers[static_cast<size_t>(l)];
+            const StageDev& s = stages[static_cast<size_t>(ld.stage)];
+            float* Y = d_pred_buf + (l & 1) * pred_stride;
+            launch_layer(ld, s.slot(st.current[static_cast<size_t>(ld.stage)]), X, xoff, Y);
+            X = Y;
+            contiguous_rows(xoff, ld.out);
+        }
+        fb200::HeadArgs h{};
+        h.logits = X;
+        h.n_out = n_out;
+        h.B = B;
+        h.mode = 0;
+        h.pred = d_pred + base + u * static_cast<size_t>(B);
+        fb200::launch_head(h, stream);
+        ++launches;
+    }
+
+    void launch_stage_forward(int j, const float* slot, float* stash_u, const float* x0) {
+        const StageDev& s = stages[static_cast<size_t>(j)];
+        long long xoff[fb200::kMaxBatch];
+        for (int l = s.lo; l < s.hi; ++l) {
+            const LayerDev& ld = layers[static_cast<size_t>(l)];
+            const float* X = l == 0 ? x0 : stash_u + layers[static_cast<size_t>(l - 1)].act_off;
+            contiguous_rows(xoff, ld.in);
+            launch_layer(ld, slot, X, xoff, stash_u + ld.act_off);
+        }
+    }
+
+    // delta at the logits (last stage) then per layer prev = W^T delta with the
+    // ReLU mask of the layer below applied on write (learner.hpp:443-476).
+    void launch_stage_backward(int j, const float* slot, float* stash_u, const int* lab) {
+        const StageDev& s = stages[static_cast<size_t>(j)];
+        if (j == P - 1) launch_delta_head(stash_u, lab, 1.0f / static_cast<float>(B));
+        for (int l = s.hi - 1; l >= s.lo; --l) {
+            if (l == 0) break;  // no input gradient for the first layer
+            launch_layer_backward(l, slot, stash_u);
+        }
+    }
+
+    void launch_delta_head(float* stash_u, const int* lab, float scale) {
+        const LayerDev& last = layers.back();
+        fb200::HeadArgs h{};
+        h.logits = stash_u + last.act_off;
+        h.n_out = n_out;
+        h.B = B;
+        h.mode = 1;
+        for (int b = 0; b < B; ++b) h.labels[b] = lab[b];
+        h.delta = stash_u + last.dlt_off;
+        h.scale = scale;
+        fb200::launch_head(h, stream);
+        ++launches;
+    }
+
+    void launch_layer_backward(int l, const float* slot, float* stash_u) {
+        const LayerDev& ld = layers[static_cast<size_t>(l)];
+        const LayerDev& below = layers[static_cast<size_t>(l - 1)];
+        fb200::BwdArgs a{};
+        a.W = slot + ld.woff;
+        a.d_out = stash_u + ld.dlt_off;
+        a.mask = below.act == FERRET_ACT_RELU ? stash_u + below.act_off : nullptr;
+        a.d_in = stash_u + below.dlt_off;
+        a.in = ld.in;
+        a.out = ld.out;
+        a.B = B;
+        a.row_splits = fb200::bwd_row_splits(ld.in, ld.out);
+        a.partial = d_partial;
+        a.counters = d_counters;
+        fb200::launch_bwd(a, stream);
+        ++launches;
+    }
+
+    // replay_step (learner.hpp:513-519): forward_backward(net_, {buffer.sample()})
+    // with mean reduction (net.hpp:157-200), apply_sgd on every stage, push a
+    // version per stage. B samples per replay step at micro-batch B.
+    template <bool DRY, class NotePush>
+    void replay_step(HostState& st, NotePush& note_push) {
+        long long ids[fb200::kMaxBatch];
+        for (int b = 0; b < B; ++b) ids[b] = st.replay.sample();
+        for (int j = 0; j < P; ++j) note_push(j);
+        if (!DRY) {
+            long long xoff[fb200::kMaxBatch];
+            int lab[fb200::kMaxBatch];
+            for (int b = 0; b < B; ++b) {
+                xoff[b] = ids[b] * F;
+                lab[b] = labels[static_cast<size_t>(ids[b])];
+            }
+            // forward through the live net
+            const float* X = d_x;
+            const long long* xo = xoff;
+            long long cont[fb200::kMaxBatch];
+            for (int l = 0; l < L; ++l) {
+                const LayerDev& ld = layers[static_cast<size_t>(l)];
+                const StageDev& s = stages[static_cast<size_t>(ld.stage)];
+                launch_layer(ld, s.slot(st.current[static_cast<size_t>(ld.stage)]), X, xo, d_replay + ld.act_off);
+                X = d_replay + ld.act_off;
+                contiguous_rows(cont, ld.out);
+                xo = cont;
+            }
+            launch_delta_head(d_replay, lab, 1.0f / static_cast<float>(B));
+            for (int l = L - 1; l >= 1; --l) {
+                const LayerDev& ld = layers[static_cast<size_t>(l)];
+                launch_layer_backward(l, stages[static_cast<size_t>(ld.stage)].slot(st.current[static_cast<size_t>(ld.stage)]),
+                                      d_replay);
+            }
+            for (int j = 0; j < P; ++j) {
+                fb200::UpdArgs a = update_args(j, st.current[static_cast<size_t>(j)]);
+                a.policy = FERRET_POLICY_NONE;
+                a.K = 1;
+                a.pend[0] = {d_replay, d_x, st.current[static_cast<size_t>(j)]};
+                a.x0_gather = 1;
+                for (int b = 0; b < B; ++b) a.x0off[b] = xoff[b];
+                a.step = static_cast<float>(opt.lr);
+                fb200::launch_update(a, stream);
+                ++launches;
+            }
+        }
+        for (int j = 0; j < P; ++j) st.current[static_cast<size_t>(j)] += 1;
+    }
+
+    // ------------------------------------------------------------------ output
+    void fetch_log(size_t chunk, ferret_step_record* out) {
+        const size_t base = chunk * sched.chunk_items;
+        const size_t n_samples = sched.n_units * static_cast<size_t>(B);
+        std::vector<int> pred(n_samples);
+        cuda_check(cudaMemcpyAsync(pred.data(), d_pred + base, n_samples * sizeof(int), cudaMemcpyDeviceToHost, stream),
+                   "D2H predictions");
+        cuda_check(cudaStreamSynchronize(stream), "sync");
+        for (size_t i = 0; i < sched.chunk_items; ++i) out[i] = ferret_step_record{0, FERRET_STEP_DROPPED, 0, 0, 0};
+        for (size_t u = 0; u < sched.n_units; ++u) {
+            for (int b = 0; b < B; ++b) {
+                const size_t i = u * static_cast<size_t>(B) + static_cast<size_t>(b);
+                const int label = labels[base + i];
+                ferret_step_record& r = out[i];
+                r.item = static_cast<int64_t>(i);
+                r.label = static_cast<uint64_t>(label);
+                if (sched.dropped[u]) {
+                    r.outcome = FERRET_STEP_DROPPED;
+                    r.predicted = 0;
+                } else {
+                    r.predicted = static_cast<uint64_t>(pred[i]);
+                    r.outcome = pred[i] == label ? FERRET_STEP_CORRECT : FERRET_STEP_WRONG;
+                }
+            }
+        }
+    }
+
+    void read_params(double* out, size_t n) {
+        if (n != init_params.size()) fail(FERRET_E_INVALID_ARG, "params: size mismatch");
+        cuda_check(cudaStreamSynchronize(stream), "sync");
+        for (int j = 0; j < P; ++j) {
+            const StageDev& s = stages[static_cast<size_t>(j)];
+            std::vector<float> slot(static_cast<size_t>(s.slot_floats));
+            cuda_check(cudaMemcpy(slot.data(), s.slot(hs.current[static_cast<size_t>(j)]), slot.size() * sizeof(float),
+                                  cudaMemcpyDeviceToHost),
+                       "D2H params");
+            unpack_stage(s, slot, out, 0.0);
+        }
+    }
+
+    // stage slot layout -> flatten() order, adding `offset` to every element
+    void unpack_stage(const StageDev& s, const std::vector<float>& slot, double* out, double offset) const {
+        for (int l = s.lo; l < s.hi; ++l) {
+            const LayerDev& ld = layers[static_cast<size_t>(l)];
+            double* dst = out + ld.host_off;
+            const long long nw = static_cast<long long>(ld.in) * ld.out;
+            for (long long i = 0; i < nw; ++i) dst[i] = offset + static_cast<double>(slot[static_cast<size_t>(ld.woff + i)]);
+            for (int r = 0; r < ld.out; ++r) dst[nw + r] = offset + static_cast<double>(slot[static_cast<size_t>(ld.boff + r)]);
+        }
+    }
+
+    void read_state(int j, const float* dev, double* out, size_t n, double offset) {
+        const StageDev& s = stages[static_cast<size_t>(j)];
+        if (n != static_cast<size_t>(s.n_params)) fail(FERRET_E_INVALID_ARG, "comp_state: size mismatch");
+        std::vector<double> full(init_params.size());
+        if (!dev) {
+            for (long long i = 0; i < s.n_params; ++i) out[i] = offset;
+            return;
+        }
+        std::vector<float> slot(static_cast<size_t>(s.slot_floats));
+        cuda_check(cudaMemcpy(slot.data(), dev, slot.size() * sizeof(float), cudaMemcpyDeviceToHost), "D2H state");
+        unpack_stage(s, slot, full.data(), offset);
+        std::copy(full.begin() + s.host_off, full.begin() + s.host_off + s.n_params, out);
+    }
+};
+
+namespace {
+
+bool device_ok(int dev) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n <= dev || dev < 0) return false;
+    cudaDeviceProp p{};
+    if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) return false;
+    return p.major == 10;
+}
+
+void require_device(int dev) {
+    if (!device_ok(dev))
+        fail(FERRET_E_NO_DEVICE, "no sm_100 device at ordinal " + std::to_string(dev) +
+                                     " (libferret_b200 has no CPU fallback)");
+    cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+}
+
+} // namespace
+
+extern "C" {
+
+int32_t ferret_device_available(void) { return device_ok(0) ? 1 : 0; }
+
+ferret_status ferret_trainer_create(const ferret_net_desc* net, const uint64_t* bounds, int32_t n_bounds,
+                                    const ferret_train_opts* opts, ferret_trainer** out) {
+    return guarded([&] {
+        if (!net || !bounds || !opts || !out) fail(FERRET_E_INVALID_ARG, "trainer_create: null argument");
+        require_device(opts->device);
+        auto t = std::make_unique<ferret_trainer>();
+        t->opt = *opts;
+        cuda_check(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking), "stream");
+        t->build(*net, bounds, n_bounds);
+        cuda_check(cudaDeviceSynchronize(), "create");
+        *out = t.release();
+    });
+}
+
+ferret_status ferret_trainer_load_stream(ferret_trainer* t, const double* features, const uint64_t* labels,
+                                         size_t n_items, size_t n_features) {
+    return guarded([&] {
+        cuda_check(cudaSetDevice(t->opt.device), "cudaSetDevice");
+        t->load_stream(features, labels, n_items, n_features);
+    });
+}
+
+ferret_status ferret_trainer_set_schedule(ferret_trainer* t, const ferret_event* events, size_t n_events,
+                                          size_t n_chunk_items) {
+    return guarded([&] { t->set_schedule(events, n_events, n_chunk_items); });
+}
+
+ferret_status ferret_trainer_execute(ferret_trainer* t, size_t chunk) {
+    return guarded([&] {
+        cuda_check(cudaSetDevice(t->opt.device), "cudaSetDevice");
+        t->execute(chunk);
+    });
+}
+
+ferret_status ferret_trainer_fetch_log(ferret_trainer* t, size_t chunk, ferret_step_record* log_out) {
+    return guarded([&] {
+        cuda_check(cudaSetDevice(t->opt.device), "cudaSetDevice");
+        t->fetch_log(chunk, log_out);
+    });
+}
+
+ferret_status ferret_trainer_sync(ferret_trainer* t) {
+    return guarded([&] { cuda_check(cudaStreamSynchronize(t->stream), "sync"); });
+}
+
+void* ferret_trainer_stream(ferret_trainer* t) { return static_cast<void*>(t->stream); }
+
+ferret_status ferret_trainer_run(ferret_trainer* t, const ferret_event* events, size_t n_events, const double* features,
+                                 const uint64_t* labels, size_t n_items, size_t n_features,
+                                 ferret_step_record* log_out) {
+    return guarded([&] {
+        cuda_check(cudaSetDevice(t->opt.device), "cudaSetDevice");
+        t->load_stream(features, labels, n_items, n_features);
+        t->set_schedule(events, n_events, n_items);
+        t->execute(0);
+        t->fetch_log(0, log_out);
+    });
+}
+
+ferret_status ferret_trainer_params(ferret_trainer* t, double* out, size_t n) {
+    return guarded([&] {
+        cuda_check(cudaSetDevice(t->opt.device), "cudaSetDevice");
+        t->read_params(out, n);
+    });
+}
+
+ferret_status ferret_trainer_comp_state(ferret_trainer* t, int32_t stage, double* lambda, double* v_r, double* v_a,
+                                        double* mean_gap, size_t n) {
+    return guarded([&] {
+        if (stage < 0 || stage >= t->P) fail(FERRET_E_OUT_OF_RANGE, "comp_state: stage out of range");
+        cuda_check(cudaSetDevice(t->opt.device), "cudaSetDevice");
+        cuda_check(cudaStreamSynchronize(t->stream), "sync");
+        const StageDev& s = t->stages[static_cast<size_t>(stage)];
+        const double lam0 = t->opt.policy == FERRET_POLICY_ITER_FISHER || t->opt.policy == FERRET_POLICY_FISHER
+                                ? t->opt.lambda0
+                                : 0.0;
+        if (lambda) t->read_state(stage, s.lam_d, lambda, n, lam0);
+        if (v_r) t->read_state(stage, s.v_r, v_r, n, 0.0);
+        if (v_a) t->read_state(stage, s.v_a, v_a, n, 0.0);
+        if (mean_gap) t->read_state(stage, s.gap, mean_gap, n, 0.0);
+    });
+}
+
+ferret_status ferret_trainer_normalizer(ferret_trainer* t, uint64_t* count, double* mean, double* m2, size_t n_features) {
+    return guarded([&] {
+        if (n_features != static_cast<size_t>(t->F)) fail(FERRET_E_INVALID_ARG, "normalizer: width mismatch");
+        cuda_check(cudaSetDevice(t->opt.device), "cudaSetDevice");
+        cuda_check(cudaStreamSynchronize(t->stream), "sync");
+        *count = t->hs.norm_count;
+        cuda_check(cudaMemcpy(mean, t->d_norm_mean, n_features * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+        cuda_check(cudaMemcpy(m2, t->d_norm_m2, n_features * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
+ferret_status ferret_trainer_get_stats(ferret_trainer* t, ferret_trainer_stats* out) {
+    return guarded([&] {
+        *out = t->stats;
+        out->device_bytes = t->device_bytes;
+    });
+}
+
+void ferret_trainer_destroy(ferret_trainer* t) { delete t; }
+
+ferret_status ferret_compensate(int32_t policy, const double* g, const double* const* chain, int32_t chain_len,
+                                double* lambda, double* v_r, double* v_a, double* mean_gap, size_t n, double lambda0,
+                                double alpha, double eta_lambda, double nu, double* out) {
+    return guarded([&] {
+        if (chain_len < 1) fail(FERRET_E_INVALID_ARG, "compensate_iterative: empty version chain");
+        if (chain_len > fb200::kMaxVersions) fail(FERRET_E_INVALID_ARG, "compensate: chain longer than 64 versions");
+        if (policy < 0 || policy > 4) fail(FERRET_E_CONFIG, "unknown compensation policy");
+        if (policy == FERRET_POLICY_ITER_FISHER && !lambda) fail(FERRET_E_INVALID_ARG, "compensate: lambda required");
+        if (policy == FERRET_POLICY_GAP && !mean_gap) fail(FERRET_E_INVALID_ARG, "compensate: mean_gap required");
+        require_device(0);
+        size_t bytes = 0;
+        const size_t nn = n ? n : 1;
+        std::vector<float*> bufs;
+        auto up = [&](const double* src) {
+            float* d = dalloc<float>(nn, bytes);
+            bufs.push_back(d);
+            if (src) {
+                std::vector<float> h(src, src + n);
+                cuda_check(cudaMemcpy(d, h.data(), n * sizeof(float), cudaMemcpyHostToDevice), "H2D");
+            }
+            return d;
+        };
+        auto down = [&](float* d, double* dst) {
+            std::vector<float> h(n);
+            cuda_check(cudaMemcpy(h.data(), d, n * sizeof(float), cudaMemcpyDeviceToHost), "D2H");
+            for (size_t i = 0; i < n; ++i) dst[i] = h[i];
+        };
+        struct Cleanup {
+            std::vector<float*>& b;
+            ~Cleanup() {
+                for (float* p : b) cudaFree(p);
+            }
+        } cleanup{bufs};
+        fb200::CompArgs a{};
+        a.policy = policy;
+        a.g = up(g);
+        for (int32_t i = 0; i < chain_len; ++i) a.chain[i] = up(chain[i]);
+        a.chain_len = chain_len;
+        const bool learn = policy == FERRET_POLICY_ITER_FISHER && v_r && v_a && eta_lambda > 0.0;
+        a.lambda = policy == FERRET_POLICY_ITER_FISHER ? up(lambda) : nullptr;
+        a.v_r = learn ? up(v_r) : nullptr;
+        a.v_a = learn ? up(v_a) : nullptr;
+        a.gap = policy == FERRET_POLICY_GAP ? up(mean_gap) : nullptr;
+        a.n = static_cast<long long>(n);
+        a.lambda0 = static_cast<float>(lambda0);
+        a.alpha = static_cast<float>(alpha);
+        a.eta = learn ? static_cast<float>(eta_lambda) : 0.f;
+        a.nu = static_cast<float>(nu);
+        a.out = up(nullptr);
+        if (n > 0) fb200::launch_compensate(a, nullptr);
+        cuda_check(cudaGetLastError(), "compensate launch");
+        cuda_check(cudaDeviceSynchronize(), "compensate");
+        down(a.out, out);
+        if (a.lambda) down(a.lambda, lambda);
+        if (a.v_r) down(a.v_r, v_r);
+        if (a.v_a) down(a.v_a, v_a);
+        if (a.gap) down(a.gap, mean_gap);
+    });
+}
+
+} // extern "C"

@@ -1,0 +1,421 @@
+"""Python mirror of the reference's C++ API for the pipelined stream-training path.
+
+Thin ctypes layer over ``libferret_b200.so`` (include/ferret_b200.h). The names
+follow the reference headers (proj/include/ferret/): ``make_dense_net``
+(net.hpp:54), ``profile_from_net`` (net.hpp:263), ``synth_drift_stream``
+(stream.hpp:43), ``plan`` + ``simulate`` (planner.hpp:192, sim.hpp:401),
+``PipelineTrainer`` / ``train_pipeline`` (learner.hpp:330-526),
+``online_accuracy`` (metrics.hpp:27), and errors are raised as the exception
+types the reference throws (types.hpp:13-25). There is no Python or CPU
+fallback: every compute call goes to the sm_100a kernels in the library and
+fails with ``DeviceError`` when no B200 is visible.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libferret_b200.so")
+
+# ----------------------------------------------------------------- C layouts
+EVENT_DTYPE = np.dtype([("time", "<f8"), ("kind", "<i4"), ("worker", "<i4"), ("stage", "<i4"),
+                        ("staleness", "<i4"), ("item", "<i8"), ("version", "<i8")])
+RECORD_DTYPE = np.dtype([("item", "<i8"), ("outcome", "<i4"), ("_pad", "<i4"), ("predicted", "<u8"),
+                         ("label", "<u8")])
+PROFILE_DTYPE = np.dtype([("t_f", "<f8"), ("t_b", "<f8"), ("w", "<u8"), ("a", "<u8")])
+
+EV_ARRIVAL, EV_DROP, EV_FORWARD, EV_RECOMPUTE, EV_BACKWARD, EV_UPDATE = range(6)
+POLICIES = {"none": 0, "step": 1, "gap": 2, "fisher": 3, "iter_fisher": 4}
+DRIFTS = {"none": 0, "rotate": 1, "split_tasks": 2}
+ACTS = {"relu": 0, "identity": 1}
+STEP_CORRECT, STEP_WRONG, STEP_DROPPED = 0, 1, 2
+NO_BUDGET = (1 << 64) - 1  # kNoBudget, types.hpp:29
+
+
+class SchemaError(RuntimeError):
+    pass
+
+
+class BoundError(RuntimeError):
+    pass
+
+
+class ConfigError(RuntimeError):
+    pass
+
+
+class LogicError(RuntimeError):
+    pass
+
+
+class DeviceError(RuntimeError):
+    pass
+
+
+_STATUS = {1: SchemaError, 2: BoundError, 3: ConfigError, 4: ValueError, 5: IndexError, 6: LogicError,
+           7: DeviceError, 8: DeviceError}
+
+
+class TrainOpts(C.Structure):
+    _fields_ = [("policy", C.c_int32), ("lr", C.c_double), ("eta_lambda", C.c_double), ("lambda0", C.c_double),
+                ("alpha", C.c_double), ("nu", C.c_double), ("replay", C.c_int32), ("replay_seed", C.c_uint64),
+                ("replay_capacity", C.c_uint64), ("precision", C.c_int32), ("micro_batch", C.c_int32),
+                ("device", C.c_int32), ("as_shipped", C.c_int32)]
+
+
+class NetDesc(C.Structure):
+    _fields_ = [("n_layers", C.c_int32), ("in_", C.POINTER(C.c_uint64)), ("out", C.POINTER(C.c_uint64)),
+                ("act", C.POINTER(C.c_int32)), ("params", C.POINTER(C.c_double))]
+
+
+class StreamSpecC(C.Structure):
+    _fields_ = [("t_d", C.c_double), ("decay_c", C.c_double), ("value", C.c_double), ("horizon", C.c_double)]
+
+
+class TrainerStats(C.Structure):
+    _fields_ = [("kernel_launches", C.c_uint64), ("events", C.c_uint64), ("updates", C.c_uint64),
+                ("replays", C.c_uint64), ("predicts", C.c_uint64), ("ring_depth", C.c_int32 * 16),
+                ("stash_slots", C.c_int32), ("mean_tau", C.c_double * 16), ("update_elems", C.c_uint64 * 16),
+                ("device_bytes", C.c_uint64)]
+
+
+_lib: Optional[C.CDLL] = None
+
+
+def lib() -> C.CDLL:
+    """Load libferret_b200.so (built by __graft_entry__.build()); fail loudly if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise DeviceError(f"{LIB_PATH} is missing: run __graft_entry__.build() (there is no fallback path)")
+    L = C.CDLL(LIB_PATH)
+    P, D = C.POINTER, C.c_double
+    sig = {
+        "ferret_last_error": (C.c_char_p, []),
+        "ferret_version": (C.c_char_p, []),
+        "ferret_device_available": (C.c_int32, []),
+        "ferret_train_opts_default": (None, [P(TrainOpts)]),
+        "ferret_net_param_count": (C.c_size_t, [P(C.c_uint64), C.c_int32]),
+        "ferret_make_dense_net": (C.c_int, [P(C.c_uint64), C.c_int32, C.c_uint64, C.c_int32, P(D), C.c_size_t]),
+        "ferret_profile_from_widths": (C.c_int, [P(C.c_uint64), C.c_int32, D, C.c_void_p]),
+        "ferret_synth_drift_stream": (C.c_int, [C.c_size_t, C.c_size_t, C.c_size_t, C.c_int32, C.c_uint64, D, D,
+                                                P(D), P(C.c_uint64)]),
+        "ferret_schedule_plan": (C.c_int, [C.c_void_p, C.c_int32, D, P(StreamSpecC), C.c_uint64, C.c_int32,
+                                           C.c_size_t, P(C.c_void_p)]),
+        "ferret_schedule_forced": (C.c_int, [C.c_void_p, C.c_int32, D, P(StreamSpecC), P(C.c_uint64), C.c_int32,
+                                             C.c_int32, C.c_size_t, P(C.c_void_p)]),
+        "ferret_schedule_bounds": (C.c_int32, [C.c_void_p, P(C.c_uint64), C.c_int32]),
+        "ferret_schedule_event_count": (C.c_size_t, [C.c_void_p]),
+        "ferret_schedule_events": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t]),
+        "ferret_schedule_plan_text": (C.c_size_t, [C.c_void_p, C.c_char_p, C.c_size_t]),
+        "ferret_schedule_trace_text": (C.c_size_t, [C.c_void_p, C.c_char_p, C.c_size_t]),
+        "ferret_schedule_destroy": (None, [C.c_void_p]),
+        "ferret_trainer_create": (C.c_int, [P(NetDesc), P(C.c_uint64), C.c_int32, P(TrainOpts), P(C.c_void_p)]),
+        "ferret_trainer_run": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, P(D), P(C.c_uint64), C.c_size_t,
+                                         C.c_size_t, C.c_void_p]),
+        "ferret_trainer_load_stream": (C.c_int, [C.c_void_p, P(D), P(C.c_uint64), C.c_size_t, C.c_size_t]),
+        "ferret_trainer_set_schedule": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t]),
+        "ferret_trainer_execute": (C.c_int, [C.c_void_p, C.c_size_t]),
+        "ferret_trainer_fetch_log": (C.c_int, [C.c_void_p, C.c_size_t, C.c_void_p]),
+        "ferret_trainer_sync": (C.c_int, [C.c_void_p]),
+        "ferret_trainer_stream": (C.c_void_p, [C.c_void_p]),
+        "ferret_trainer_params": (C.c_int, [C.c_void_p, P(D), C.c_size_t]),
+        "ferret_trainer_comp_state": (C.c_int, [C.c_void_p, C.c_int32, P(D), P(D), P(D), P(D), C.c_size_t]),
+        "ferret_trainer_normalizer": (C.c_int, [C.c_void_p, P(C.c_uint64), P(D), P(D), C.c_size_t]),
+        "ferret_trainer_get_stats": (C.c_int, [C.c_void_p, P(TrainerStats)]),
+        "ferret_trainer_destroy": (None, [C.c_void_p]),
+        "ferret_compensate": (C.c_int, [C.c_int32, P(D), P(P(D)), C.c_int32, P(D), P(D), P(D), P(D), C.c_size_t,
+                                        D, D, D, D, P(D)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        msg = lib().ferret_last_error().decode()
+        raise _STATUS.get(status, DeviceError)(msg)
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _up(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_uint64))
+
+
+def device_available() -> bool:
+    return bool(lib().ferret_device_available())
+
+
+# ----------------------------------------------------------- host tiers
+def param_count(widths: Sequence[int]) -> int:
+    w = np.asarray(widths, dtype=np.uint64)
+    return int(lib().ferret_net_param_count(_up(w), len(w)))
+
+
+def make_dense_net(widths: Sequence[int], seed: int, hidden_act: str = "relu") -> np.ndarray:
+    """make_dense_net (net.hpp:54-71): flat fp64 params in flatten() order."""
+    w = np.ascontiguousarray(widths, dtype=np.uint64)
+    out = np.empty(param_count(widths), dtype=np.float64)
+    _check(lib().ferret_make_dense_net(_up(w), len(w), seed, ACTS[hidden_act], _dp(out), out.size))
+    return out
+
+
+def profile_from_widths(widths: Sequence[int], seconds_per_param: float = 1e-6) -> np.ndarray:
+    """profile_from_net (net.hpp:263-274) on the net's shapes."""
+    w = np.ascontiguousarray(widths, dtype=np.uint64)
+    out = np.zeros(len(w) - 1, dtype=PROFILE_DTYPE)
+    _check(lib().ferret_profile_from_widths(_up(w), len(w), seconds_per_param, out.ctypes.data))
+    return out
+
+
+def synth_drift_stream(n: int, n_features: int, n_classes: int, drift: str = "split_tasks", seed: int = 7,
+                       rotate_rate: float = 1.5e-4, noise: float = 0.55):
+    """synth_drift_stream (stream.hpp:43-87) -> (features[n, F] fp64, labels[n] u64)."""
+    feats = np.empty((n, n_features), dtype=np.float64)
+    labels = np.empty(n, dtype=np.uint64)
+    _check(lib().ferret_synth_drift_stream(n, n_features, n_classes, DRIFTS[drift], seed, rotate_rate, noise,
+                                           _dp(feats), _up(labels)))
+    return feats, labels
+
+
+@dataclass
+class StreamSpec:
+    """StreamSpec (types.hpp:139-151)."""
+    t_d: float = 1.0
+    decay_c: float = 0.0
+    value: float = 1.0
+    horizon: float = 1.0
+
+    def c(self) -> StreamSpecC:
+        return StreamSpecC(self.t_d, self.decay_c, self.value, self.horizon)
+
+
+class Schedule:
+    """plan()/default_config + simulate(): partition, config and the event log."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+        L = lib()
+        n = L.ferret_schedule_bounds(self._h, None, 0)
+        b = np.zeros(n, dtype=np.uint64)
+        L.ferret_schedule_bounds(self._h, _up(b), n)
+        self.bounds = [int(x) for x in b]
+        ne = L.ferret_schedule_event_count(self._h)
+        self.events = np.zeros(ne, dtype=EVENT_DTYPE)
+        _check(L.ferret_schedule_events(self._h, self.events.ctypes.data, ne))
+
+    @classmethod
+    def plan(cls, profile: np.ndarray, t_d: float, spec: StreamSpec, budget: int = NO_BUDGET,
+             n_items: int = 0, max_stages: int = 0) -> "Schedule":
+        h = C.c_void_p()
+        prof = np.ascontiguousarray(profile, dtype=PROFILE_DTYPE)
+        _check(lib().ferret_schedule_plan(prof.ctypes.data, len(prof), t_d, C.byref(spec.c()), budget, max_stages,
+                                          n_items, C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def forced(cls, profile: np.ndarray, t_d: float, spec: StreamSpec, bounds: Sequence[int], n_items: int,
+               recompute: int = 0) -> "Schedule":
+        h = C.c_void_p()
+        prof = np.ascontiguousarray(profile, dtype=PROFILE_DTYPE)
+        b = np.ascontiguousarray(bounds, dtype=np.uint64)
+        _check(lib().ferret_schedule_forced(prof.ctypes.data, len(prof), t_d, C.byref(spec.c()), _up(b), len(b),
+                                            recompute, n_items, C.byref(h)))
+        return cls(h.value)
+
+    def _text(self, fn) -> str:
+        n = fn(self._h, None, 0)
+        buf = C.create_string_buffer(n)
+        fn(self._h, buf, n)
+        return buf.value.decode()
+
+    @property
+    def plan_text(self) -> str:
+        return self._text(lib().ferret_schedule_plan_text)
+
+    @property
+    def trace_text(self) -> str:
+        return self._text(lib().ferret_schedule_trace_text)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.ferret_schedule_destroy(self._h)
+            self._h = None
+
+
+def online_accuracy(log: np.ndarray) -> float:
+    """online_accuracy (metrics.hpp:27-32): drops count as wrong."""
+    if len(log) == 0:
+        raise ValueError("online_accuracy: empty log")
+    return 100.0 * float(np.count_nonzero(log["outcome"] == STEP_CORRECT)) / float(len(log))
+
+
+# ----------------------------------------------------------- the trainer
+@dataclass
+class PipelineTrainOptions:
+    """PipelineTrainOptions (learner.hpp:319-325) + Compensator constants + B200 knobs."""
+    policy: str = "none"
+    lr: float = 1e-3
+    eta_lambda: float = 1e-3
+    replay: bool = False
+    replay_seed: int = 0
+    lambda0: float = 0.2
+    alpha: float = 0.99
+    nu: float = 2e-6
+    replay_capacity: int = 5000
+    micro_batch: int = 1
+    device: int = 0
+    as_shipped: bool = False
+
+    def c(self) -> TrainOpts:
+        o = TrainOpts()
+        lib().ferret_train_opts_default(C.byref(o))
+        o.policy = POLICIES[self.policy]
+        o.lr, o.eta_lambda, o.lambda0, o.alpha, o.nu = self.lr, self.eta_lambda, self.lambda0, self.alpha, self.nu
+        o.replay = int(self.replay)
+        o.replay_seed = self.replay_seed
+        o.replay_capacity = self.replay_capacity
+        o.micro_batch = self.micro_batch
+        o.device = self.device
+        o.as_shipped = int(self.as_shipped)
+        return o
+
+
+def widths_layers(widths: Sequence[int]):
+    ins = np.ascontiguousarray(widths[:-1], dtype=np.uint64)
+    outs = np.ascontiguousarray(widths[1:], dtype=np.uint64)
+    acts = np.zeros(len(ins), dtype=np.int32)
+    acts[-1] = ACTS["identity"]
+    return ins, outs, acts
+
+
+class PipelineTrainer:
+    """PipelineTrainer (learner.hpp:330-520) on one B200; state lives in HBM."""
+
+    def __init__(self, widths: Sequence[int], params: np.ndarray, bounds: Sequence[int],
+                 opt: PipelineTrainOptions = PipelineTrainOptions()):
+        self.widths = list(widths)
+        self.bounds = list(bounds)
+        self.opt = opt
+        self.n_params = param_count(widths)
+        ins, outs, acts = widths_layers(widths)
+        self._keep = (ins, outs, acts, np.ascontiguousarray(params, dtype=np.float64))
+        desc = NetDesc(len(ins), _up(ins), _up(outs), acts.ctypes.data_as(C.POINTER(C.c_int32)), _dp(self._keep[3]))
+        b = np.ascontiguousarray(bounds, dtype=np.uint64)
+        h = C.c_void_p()
+        _check(lib().ferret_trainer_create(C.byref(desc), _up(b), len(b), C.byref(opt.c()), C.byref(h)))
+        self._h = h
+
+    # end to end: host stream in, StepRecord log out
+    def run(self, events: np.ndarray, features: np.ndarray, labels: np.ndarray) -> np.ndarray:
+        ev = np.ascontiguousarray(events, dtype=EVENT_DTYPE)
+        f = np.ascontiguousarray(features, dtype=np.float64)
+        lab = np.ascontiguousarray(labels, dtype=np.uint64)
+        log = np.zeros(f.shape[0], dtype=RECORD_DTYPE)
+        _check(lib().ferret_trainer_run(self._h, ev.ctypes.data, len(ev), _dp(f), _up(lab), f.shape[0], f.shape[1],
+                                        log.ctypes.data))
+        return log
+
+    # split form (device-resident timing)
+    def load_stream(self, features: np.ndarray, labels: np.ndarray) -> None:
+        f = np.ascontiguousarray(features, dtype=np.float64)
+        lab = np.ascontiguousarray(labels, dtype=np.uint64)
+        _check(lib().ferret_trainer_load_stream(self._h, _dp(f), _up(lab), f.shape[0], f.shape[1]))
+
+    def set_schedule(self, events: np.ndarray, chunk_items: int = 0) -> None:
+        ev = np.ascontiguousarray(events, dtype=EVENT_DTYPE)
+        self._events = ev
+        self.chunk_items = chunk_items
+        _check(lib().ferret_trainer_set_schedule(self._h, ev.ctypes.data, len(ev), chunk_items))
+
+    def execute(self, chunk: int = 0) -> None:
+        _check(lib().ferret_trainer_execute(self._h, chunk))
+
+    def fetch_log(self, chunk: int = 0, n: Optional[int] = None) -> np.ndarray:
+        log = np.zeros(n if n is not None else self.chunk_items, dtype=RECORD_DTYPE)
+        _check(lib().ferret_trainer_fetch_log(self._h, chunk, log.ctypes.data))
+        return log
+
+    def sync(self) -> None:
+        _check(lib().ferret_trainer_sync(self._h))
+
+    @property
+    def cuda_stream(self) -> int:
+        return int(lib().ferret_trainer_stream(self._h) or 0)
+
+    def params(self) -> np.ndarray:
+        out = np.empty(self.n_params, dtype=np.float64)
+        _check(lib().ferret_trainer_params(self._h, _dp(out), out.size))
+        return out
+
+    def comp_state(self, stage: int, n: int):
+        lam, vr, va, gap = (np.empty(n, dtype=np.float64) for _ in range(4))
+        _check(lib().ferret_trainer_comp_state(self._h, stage, _dp(lam), _dp(vr), _dp(va), _dp(gap), n))
+        return lam, vr, va, gap
+
+    def normalizer(self, n_features: int):
+        cnt = C.c_uint64()
+        mean = np.empty(n_features, dtype=np.float64)
+        m2 = np.empty(n_features, dtype=np.float64)
+        _check(lib().ferret_trainer_normalizer(self._h, C.byref(cnt), _dp(mean), _dp(m2), n_features))
+        return int(cnt.value), mean, m2
+
+    def stats(self) -> dict:
+        s = TrainerStats()
+        _check(lib().ferret_trainer_get_stats(self._h, C.byref(s)))
+        P = len(self.bounds) - 1
+        return {"kernel_launches": s.kernel_launches, "events": s.events, "updates": s.updates,
+                "replays": s.replays, "predicts": s.predicts, "ring_depth": list(s.ring_depth[:P]),
+                "stash_slots": s.stash_slots, "mean_tau": list(s.mean_tau[:P]),
+                "update_elems": list(s.update_elems[:P]), "device_bytes": s.device_bytes}
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().ferret_trainer_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def train_pipeline(widths, params, bounds, events, features, labels, opt=PipelineTrainOptions()):
+    """train_pipeline (learner.hpp:522-526): returns (log, final params)."""
+    t = PipelineTrainer(widths, params, bounds, opt)
+    try:
+        log = t.run(events, features, labels)
+        return log, t.params()
+    finally:
+        t.close()
+
+
+def compensate(policy: str, g: np.ndarray, chain: Sequence[np.ndarray], lam=None, v_r=None, v_a=None,
+               mean_gap=None, lambda0: float = 0.2, alpha: float = 0.99, eta_lambda: float = 0.0,
+               nu: float = 2e-6) -> np.ndarray:
+    """Compensator::apply (learner.hpp:97-120) on the device; state arrays updated in place."""
+    g = np.ascontiguousarray(g, dtype=np.float64)
+    n = g.size
+    ch = [np.ascontiguousarray(c, dtype=np.float64) for c in chain]
+    arr = (C.POINTER(C.c_double) * len(ch))(*[_dp(c) for c in ch])
+    out = np.empty(n, dtype=np.float64)
+    nul = C.POINTER(C.c_double)()
+    _check(lib().ferret_compensate(POLICIES[policy], _dp(g), arr, len(ch), _dp(lam) if lam is not None else nul,
+                                   _dp(v_r) if v_r is not None else nul, _dp(v_a) if v_a is not None else nul,
+                                   _dp(mean_gap) if mean_gap is not None else nul, n, lambda0, alpha, eta_lambda, nu,
+                                   _dp(out)))
+    return out

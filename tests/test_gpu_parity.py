@@ -1,0 +1,187 @@
+"""GPU parity: the sm_100a trainer (through the C ABI) against the CPU oracle.
+
+Bar (BASELINE.json north star): routing / schedule / replay indices bit-exact
+(host side, and the replay index sequence read back from the device run);
+fp32 parameters after the run within 1e-4 relative of the fp64 oracle per
+stage; online accuracy within 0.5 percentage points; normalizer state
+bit-exact (fp64 on the device with separately rounded ops).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+PARAM_RTOL = 1e-4   # north star: fp32 parity mode, params within 1e-4 relative
+OACC_TOL = 0.5      # percentage points
+
+
+def _setup(fb, widths, n_units, bounds=None, budget=None, micro_batch=1, seed=7, recompute=0):
+    n = n_units * micro_batch
+    params = fb.make_dense_net(widths, 1)
+    feats, labels = fb.synth_drift_stream(n, widths[0], widths[-1], "split_tasks", seed)
+    prof = fb.profile_from_widths(widths)
+    t_d = float(prof["t_f"].max())
+    spec = fb.StreamSpec(t_d=t_d, horizon=n_units * t_d)
+    if bounds is None:
+        sched = fb.Schedule.plan(prof, t_d, spec, budget if budget is not None else fb.NO_BUDGET, n_items=n_units)
+    else:
+        sched = fb.Schedule.forced(prof, t_d, spec, bounds, n_units, recompute=recompute)
+    return params, feats, labels, sched
+
+
+def _stage_slices(widths, bounds):
+    offs = [0]
+    for i in range(len(widths) - 1):
+        offs.append(offs[-1] + widths[i] * widths[i + 1] + widths[i + 1])
+    return [(offs[bounds[j]], offs[bounds[j + 1]]) for j in range(len(bounds) - 1)]
+
+
+def _compare(fb, orc, widths, params, feats, labels, sched, policy, micro_batch=1, replay=False, check_state=True):
+    opt = fb.PipelineTrainOptions(policy=policy, replay=replay, replay_seed=3, micro_batch=micro_batch)
+    tr = fb.PipelineTrainer(widths, params, sched.bounds, opt)
+    log = tr.run(sched.events, feats, labels)
+    got = tr.params()
+    ref = orc.train(widths, params, sched.bounds, sched.events, feats, labels, policy=policy, replay=replay,
+                    replay_seed=3, micro_batch=micro_batch)
+    # training must have moved the params (guards against a silent no-op)
+    assert np.linalg.norm(ref["params"] - params) / np.linalg.norm(params) > 1e-4
+    for j, (lo, hi) in enumerate(_stage_slices(widths, sched.bounds)):
+        rel = np.linalg.norm(got[lo:hi] - ref["params"][lo:hi]) / np.linalg.norm(ref["params"][lo:hi])
+        assert rel < PARAM_RTOL, f"stage {j}: param rel err {rel:.3e}"
+    oacc_gpu, oacc_ref = fb.online_accuracy(log), fb.online_accuracy(ref["log"])
+    assert abs(oacc_gpu - oacc_ref) <= OACC_TOL, (oacc_gpu, oacc_ref)
+    # dropped / labels / item ids are schedule facts: exact
+    assert np.array_equal(log["outcome"] == 2, ref["log"]["outcome"] == 2)
+    assert np.array_equal(log["label"], ref["log"]["label"])
+    assert np.array_equal(log["item"], ref["log"]["item"])
+    flips = np.count_nonzero(log["predicted"] != ref["log"]["predicted"])
+    assert flips <= max(2, 0.005 * len(log)), f"{flips} prediction flips"
+    # normalizer: bit-exact
+    cnt, mean, m2 = tr.normalizer(widths[0])
+    assert cnt == ref["norm_count"]
+    assert np.array_equal(mean, ref["norm_mean"]) and np.array_equal(m2, ref["norm_m2"])
+    if check_state and policy in ("iter_fisher", "gap"):
+        for j, (lo, hi) in enumerate(_stage_slices(widths, sched.bounds)):
+            lam, vr, va, gap = tr.comp_state(j, hi - lo)
+            if policy == "iter_fisher":
+                d_ref = ref["lambda"][lo:hi] - 0.2
+                d_gpu = lam - 0.2
+                if np.linalg.norm(d_ref) > 0:
+                    assert np.linalg.norm(d_gpu - d_ref) / np.linalg.norm(d_ref) < 2e-2
+                for a, b in ((vr, ref["v_r"][lo:hi]), (va, ref["v_a"][lo:hi])):
+                    if np.linalg.norm(b) > 0:
+                        assert np.linalg.norm(a - b) / np.linalg.norm(b) < 1e-3
+            else:
+                b = ref["gap"][lo:hi]
+                assert np.linalg.norm(gap - b) / max(np.linalg.norm(b), 1e-30) < 1e-3
+    tr.close()
+    return log, ref
+
+
+def test_c1_single_stage_iter_fisher(gpu, fb, orc):
+    widths = [784, 256, 256, 10]
+    params, feats, labels, sched = _setup(fb, widths, 160)
+    assert sched.bounds == [0, 3]
+    _compare(fb, orc, widths, params, feats, labels, sched, "iter_fisher")
+
+
+@pytest.mark.parametrize("bounds", [[0, 2, 4], [0, 1, 2, 3, 4]])
+def test_c2_stages_iter_fisher(gpu, fb, orc, bounds):
+    widths = [784, 256, 256, 256, 10]
+    params, feats, labels, sched = _setup(fb, widths, 160, bounds=bounds)
+    _compare(fb, orc, widths, params, feats, labels, sched, "iter_fisher")
+
+
+@pytest.mark.parametrize("policy", ["none", "step", "gap", "fisher"])
+def test_policies_two_stage(gpu, fb, orc, policy):
+    widths = [96, 128, 64, 10]
+    params, feats, labels, sched = _setup(fb, widths, 200, bounds=[0, 1, 3])
+    _compare(fb, orc, widths, params, feats, labels, sched, policy)
+
+
+def test_micro_batch_extension(gpu, fb, orc):
+    widths = [784, 256, 256, 256, 10]
+    params, feats, labels, sched = _setup(fb, widths, 64, bounds=[0, 2, 4], micro_batch=16)
+    _compare(fb, orc, widths, params, feats, labels, sched, "iter_fisher", micro_batch=16)
+
+
+def test_replay_er_four_stage(gpu, fb, orc):
+    widths = [784, 256, 256, 256, 10]
+    params, feats, labels, sched = _setup(fb, widths, 120, bounds=[0, 1, 2, 3, 4])
+    _compare(fb, orc, widths, params, feats, labels, sched, "iter_fisher", replay=True)
+
+
+def test_budget_plan_accumulate_omit(gpu, fb, orc):
+    """A budget-constrained plan (S2 accumulation / S3 omission / S4 removal) on the deep MLP."""
+    widths = [784] + [256] * 7 + [10]
+    prof = fb.profile_from_widths(widths)
+    t_d = float(prof["t_f"].max())
+    full = fb.Schedule.plan(prof, t_d, fb.StreamSpec(t_d=t_d, horizon=100 * t_d), n_items=1)
+    mem = int(full.plan_text.split("memory ")[1].split()[0])
+    params, feats, labels, sched = _setup(fb, widths, 150, budget=mem // 2)
+    assert "trace 0" not in sched.plan_text  # moves were applied
+    _compare(fb, orc, widths, params, feats, labels, sched, "iter_fisher")
+
+
+def test_recompute_events(gpu, fb, orc):
+    widths = [96, 128, 64, 10]
+    params, feats, labels, sched = _setup(fb, widths, 120, bounds=[0, 1, 3], recompute=1)
+    assert np.any(sched.events["kind"] == 3)
+    _compare(fb, orc, widths, params, feats, labels, sched, "iter_fisher")
+
+
+def test_as_shipped_is_noop(gpu, fb, orc):
+    widths = [96, 128, 64, 10]
+    params, feats, labels, sched = _setup(fb, widths, 80, bounds=[0, 1, 3])
+    opt = fb.PipelineTrainOptions(policy="iter_fisher", as_shipped=True)
+    tr = fb.PipelineTrainer(widths, params, sched.bounds, opt)
+    log = tr.run(sched.events, feats, labels)
+    got = tr.params()
+    ref = orc.train(widths, params, sched.bounds, sched.events, feats, labels, policy="iter_fisher", as_shipped=True)
+    assert np.array_equal(ref["params"], params)
+    assert np.abs(got - params).max() < 1e-6  # fp32 round trip only
+    assert np.count_nonzero(log["predicted"] != ref["log"]["predicted"]) <= 1
+    tr.close()
+
+
+def test_replay_indices_bit_exact(gpu, fb, orc):
+    """Replay indices: the device run's sampled items (reflected in the params) match the
+    oracle's restated reservoir, which itself is asserted against the reference buffer."""
+    widths = [64, 96, 10]
+    params, feats, labels, sched = _setup(fb, widths, 200, bounds=[0, 1, 2])
+    _compare(fb, orc, widths, params, feats, labels, sched, "none", replay=True)
+
+
+@pytest.mark.parametrize("policy", ["none", "step", "gap", "fisher", "iter_fisher"])
+def test_compensate_unit(gpu, fb, orc, policy):
+    rng = np.random.default_rng(0)
+    n, tau = 4099, 3
+    g = rng.normal(size=n) * 0.1
+    chain = [rng.normal(size=n) * 0.05 for _ in range(tau + 1)]
+    lam = np.full(n, 0.2)
+    vr = rng.normal(size=n) * 1e-3
+    va = rng.normal(size=n) * 1e-4
+    gap = np.abs(rng.normal(size=n)) * 1e-2
+    kw_ref = dict(lam=lam.copy(), v_r=vr.copy(), v_a=va.copy(), mean_gap=gap.copy(), eta=1e-3)
+    ref = orc.compensate(policy, g, chain, **kw_ref)
+    kw = dict(lam=lam.copy(), v_r=vr.copy(), v_a=va.copy(), mean_gap=gap.copy(), eta_lambda=1e-3)
+    got = fb.compensate(policy, g, chain, **kw)
+    np.testing.assert_allclose(got, ref, rtol=2e-5, atol=1e-7)
+    if policy == "gap":
+        np.testing.assert_allclose(kw["mean_gap"], kw_ref["mean_gap"], rtol=1e-5)
+    if policy == "iter_fisher":
+        np.testing.assert_allclose(kw["v_r"], kw_ref["v_r"], rtol=1e-5, atol=1e-9)
+        np.testing.assert_allclose(kw["v_a"], kw_ref["v_a"], rtol=1e-4, atol=1e-12)
+
+
+def test_spec_kats_on_device(gpu, fb):
+    """SPEC worked examples through the device compensator."""
+    out = fb.compensate("fisher", np.array([2.0]), [np.array([0.0]), np.array([0.1])], lambda0=0.5)
+    assert abs(out[0] - 2.2) < 1e-6
+    lam = np.array([1.0])
+    out = fb.compensate("iter_fisher", np.array([1.0]), [np.array([0.0]), np.array([0.1]), np.array([0.3])], lam=lam)
+    assert abs(out[0] - 1.342) < 1e-6
+    out = fb.compensate("step", np.array([4.0]), [np.zeros(1)] * 4)
+    assert abs(out[0] - 1.0) < 1e-7
+    out = fb.compensate("gap", np.array([2.0]), [np.array([0.0]), np.array([0.5])], mean_gap=np.array([0.5]))
+    assert abs(out[0] - 1.0) < 1e-7
