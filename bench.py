@@ -1,0 +1,303 @@
+"""Benchmark: stream samples/sec of Ferret's pipelined stream training on B200.
+
+Workload (BASELINE.json configs[1], the metric's config that fits one GPU):
+MLP 784-256-256-256-10 split into 4 pipeline stages (bounds 0,1,2,3,4,
+default_config workers), iter_fisher gradient compensation, micro-batch 16,
+synthetic class-incremental stream (synth_drift_stream, split_tasks, seed 7).
+A step = one replay of the simulator's event log over one chunk of the stream
+(UNITS pipeline units x 16 samples), continuing training from the previous
+chunk. All stages share one GPU at N=1.
+
+  value      samples/s with the stream already resident in HBM (device time,
+             CUDA events on the trainer's stream, L2 flushed between steps)
+  e2e        the same metric through the reference-facing call
+             (ferret_trainer_run == PipelineTrainer::run) from pinned host
+             buffers: H2D stream copy + replay + D2H StepRecord log per step
+  roofline   the fused compensation + SGD update kernel against the measured
+             HBM copy bandwidth (algorithmic bytes per launch / event time)
+  cpu_baseline  the reference CPU pipeline (oracle/_ref: reference headers +
+             item-keyed PipelineTrainer restatement) on a bounded sample, 1 core
+
+--impl reference times that CPU reference alone on the same config.
+Multi-GPU (--gpus N>1, torchrun): every rank runs an independent replica of the
+pipeline on its own stream shard ("replicas only" scaling); value
+= total samples / max-over-ranks time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WIDTHS = [784, 256, 256, 256, 10]
+BOUNDS = [0, 1, 2, 3, 4]
+MICRO_BATCH = 16
+UNITS = 256            # pipeline units per step (x16 samples)
+POLICY = "iter_fisher"
+CPU_UNITS = 24          # bounded CPU sample: 24 units x 16 samples
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        for k in ("hbm_gbs", "hbm_GBs", "hbm_gb_s"):
+            if k in d:
+                return float(d[k]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                if len(parts) == 6:
+                    self.rows.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def make_workload(fb, n_chunks, units):
+    prof = fb.profile_from_widths(WIDTHS)
+    t_d = float(prof["t_f"].max())
+    sched = fb.Schedule.forced(prof, t_d, fb.StreamSpec(t_d=t_d, horizon=units * t_d), BOUNDS, units)
+    chunk = units * MICRO_BATCH
+    feats, labels = fb.synth_drift_stream(n_chunks * chunk, WIDTHS[0], WIDTHS[-1], "split_tasks", 7)
+    return sched, feats, labels, chunk
+
+
+def cpu_reference(units: int, steps: int, warmup: int):
+    """The reference CPU pipeline on `units` pipeline units per step (1 core)."""
+    import paper_2503_12053_b200 as fb
+    from oracle import oracle as orc
+
+    sched, feats, labels, chunk = make_workload(fb, 1, units)
+    params = fb.make_dense_net(WIDTHS, 1)
+    times = []
+    for s in range(warmup + steps):
+        t0 = time.perf_counter()
+        orc.train(WIDTHS, params, BOUNDS, sched.events, feats, labels, policy=POLICY, micro_batch=MICRO_BATCH)
+        dt = time.perf_counter() - t0
+        if s >= warmup:
+            times.append(dt)
+    tot = sum(times)
+    return chunk * len(times) / tot, tot, chunk
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    units = max(4, CPU_UNITS // 2)
+    value, tot, chunk = cpu_reference(units, args.steps, args.warmup)
+    sample = f"{units} units x {MICRO_BATCH} samples = {chunk} samples per step, {args.steps} timed steps"
+    line = {"impl": "reference", "metric": "stream samples/sec", "value": value, "unit": "samples/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C2: MLP 784-256-256-256-10, 4 stages, iter_fisher, micro-batch 16",
+                       "global_batch": MICRO_BATCH, "stages": 4},
+            "cpu_baseline": {"value": value, "unit": "samples/s", "cores": 1, "kind": "reference",
+                             "sample": sample + "; reference headers + item-keyed PipelineTrainer restatement "
+                                                "(single-threaded by design)"},
+            "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--units", type=int, default=UNITS)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+
+    import paper_2503_12053_b200 as fb
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    units = args.units
+    n_chunks = args.warmup + args.steps
+    sched, feats, labels, chunk = make_workload(fb, n_chunks, units)
+    # each rank trains its own replica on its own shard of the stream
+    if world > 1:
+        feats2, labels2 = fb.synth_drift_stream(n_chunks * chunk, WIDTHS[0], WIDTHS[-1], "split_tasks", 7 + rank)
+        feats, labels = feats2, labels2
+    params = fb.make_dense_net(WIDTHS, 1)
+    opt = fb.PipelineTrainOptions(policy=POLICY, micro_batch=MICRO_BATCH, device=local)
+    tr = fb.PipelineTrainer(WIDTHS, params, BOUNDS, opt)
+    tr.load_stream(feats, labels)
+    tr.set_schedule(sched.events, chunk)
+    stream = torch.cuda.ExternalStream(tr.cuda_stream, device=torch.device("cuda", local))
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
+
+    for c in range(args.warmup):
+        tr.execute(c)
+    tr.sync()
+    launches_per_step = tr.stats()["kernel_launches"]
+
+    # ---- device-resident timed region
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for s in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+                starts[s].record(stream)
+            tr.execute(args.warmup + s)
+            with torch.cuda.stream(stream):
+                ends[s].record(stream)
+        tr.sync()
+        torch.cuda.synchronize()
+    dev_ms = sum(a.elapsed_time(b) for a, b in zip(starts, ends))
+    if dist:
+        t = torch.tensor([dev_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms = float(t.item())
+        dist.barrier()
+    total_samples = chunk * args.steps * world
+    value = total_samples / (dev_ms / 1e3)
+    log = tr.fetch_log(args.warmup + args.steps - 1)
+    oacc_last = fb.online_accuracy(log)
+
+    # ---- roofline of the update kernel (separate pass, events around each launch)
+    tr.set_timing(True)
+    tr.execute(0)  # replays chunk 0 again (continues training; not part of the timed region)
+    upd_ms, upd_n, upd_bytes = tr.update_timing()
+    tr.set_timing(False)
+    peak, peak_kind = _peaks()
+    achieved = (upd_bytes / upd_n) / (upd_ms / upd_n / 1e3) / 1e9 if upd_n else 0.0
+    stats = tr.stats()
+    tr.close()
+
+    # ---- e2e through the reference-facing call from pinned host buffers
+    tr2 = fb.PipelineTrainer(WIDTHS, params, BOUNDS, opt)
+    pin_f = torch.empty((chunk, WIDTHS[0]), dtype=torch.float64).pin_memory()
+    pin_l = torch.empty((chunk,), dtype=torch.int64).pin_memory()
+    e2e_times = []
+    h2d = chunk * WIDTHS[0] * 8 + chunk * 8
+    d2h = chunk * 4
+    for s in range(args.warmup + args.steps):
+        c = s % n_chunks
+        pin_f.numpy()[:] = feats[c * chunk:(c + 1) * chunk]
+        pin_l.numpy()[:] = labels[c * chunk:(c + 1) * chunk].astype(np.int64)
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        tr2.run(sched.events, pin_f.numpy(), pin_l.numpy().view(np.uint64))
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            e2e_times.append(dt)
+    e2e_s = sum(e2e_times)
+    if dist:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = total_samples / e2e_s
+    tr2.close()
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if not args.no_cpu and world == 1:
+        try:
+            v, tot, n = cpu_reference(CPU_UNITS, 1, 0)
+            cpu = {"value": v, "unit": "samples/s", "cores": 1, "kind": "reference",
+                   "sample": f"{CPU_UNITS} units x {MICRO_BATCH} samples ({n} samples, {tot:.1f} s) of the same "
+                             "workload; reference headers + item-keyed PipelineTrainer restatement, fp64, "
+                             f"single-threaded (host nproc={os.cpu_count()})"}
+        except Exception as e:  # the oracle .so is built where /root/reference exists
+            cpu = {"value": None, "unit": "samples/s", "cores": 1, "kind": "reference", "sample": f"unavailable: {e}"}
+    line = {
+        "metric": "stream samples/sec", "value": value, "unit": "samples/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (synth_drift_stream split_tasks seed 7; make_dense_net seed 1)",
+        "config": {"workload": "C2: MLP 784-256-256-256-10, 4 pipeline stages on one GPU, iter_fisher, micro-batch 16",
+                   "global_batch": MICRO_BATCH, "units_per_step": units, "samples_per_step": chunk,
+                   "stages": len(BOUNDS) - 1, "parallelism": f"replicas{world}" if world > 1 else "pipeline-on-1",
+                   "l2": "flushed between timed steps (256 MB write)"},
+        "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "call": "ferret_trainer_run (PipelineTrainer::run) from pinned host buffers"},
+        "roofline": {"bound": "hbm", "kernel": "update_kernel (fused compensation + SGD)", "achieved": achieved,
+                     "peak": peak, "unit": "GB/s", "frac": achieved / peak, "peak_kind": peak_kind,
+                     "traffic": None, "alg_bytes_per_launch": upd_bytes / max(upd_n, 1),
+                     "avg_launch_us": 1e3 * upd_ms / max(upd_n, 1)},
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+        "gpu_launches": int(launches_per_step * args.steps),
+        "online_accuracy_last_chunk": oacc_last,
+        "trainer": {"ring_depth": stats["ring_depth"], "stash_slots": stats["stash_slots"],
+                    "mean_tau": stats["mean_tau"], "device_bytes": stats["device_bytes"]},
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -225,6 +225,15 @@ typedef struct {
 FERRET_API ferret_status ferret_trainer_get_stats(ferret_trainer* t, ferret_trainer_stats* out);
 FERRET_API void ferret_trainer_destroy(ferret_trainer* t);
 
+/* Measurement hook (no reference counterpart): when enabled, every update
+ * launch (the fused compensation + SGD kernel, learner.hpp:491-504) is
+ * bracketed by CUDA events on the trainer's stream. update_timing() returns the
+ * summed kernel time, the number of timed launches and their algorithmic HBM
+ * bytes, then resets the counters. */
+FERRET_API ferret_status ferret_trainer_set_timing(ferret_trainer* t, int32_t enable);
+FERRET_API ferret_status ferret_trainer_update_timing(ferret_trainer* t, double* total_ms, uint64_t* launches,
+                                                      double* alg_bytes);
+
 /* ---------------- unit entry: the fused compensation kernel ---------------- */
 
 /* One Compensator::apply (learner.hpp:97-120) on the device, fp32:

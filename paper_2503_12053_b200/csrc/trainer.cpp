@@ -161,9 +161,62 @@ struct ferret_trainer {
     ferret_trainer_stats stats{};
     uint64_t launches = 0;
 
+    // optional per-launch timing of the update kernel (CUDA events on `stream`)
+    bool timing = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    double upd_alg_bytes = 0.0;   // algorithmic HBM bytes of the timed update launches
+    uint64_t upd_timed = 0;
+
+    void time_begin() {
+        if (!timing) return;
+        while (ev_pool.size() < ev_used + 2) {
+            cudaEvent_t e;
+            cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+            ev_pool.push_back(e);
+        }
+        cuda_check(cudaEventRecord(ev_pool[ev_used], stream), "cudaEventRecord");
+    }
+    void time_end(double alg_bytes) {
+        if (!timing) return;
+        cuda_check(cudaEventRecord(ev_pool[ev_used + 1], stream), "cudaEventRecord");
+        ev_used += 2;
+        upd_alg_bytes += alg_bytes;
+        upd_timed += 1;
+    }
+    // Algorithmic bytes of one update launch: every parameter element reads the
+    // versions it needs + its compensator state and writes the new version +
+    // state; plus the deltas and layer inputs of each pending gradient.
+    double update_bytes(int j, int policy, const std::vector<long long>& reads, long long cur) const {
+        const StageDev& s = stages[static_cast<size_t>(j)];
+        long long lo = cur;
+        for (long long r : reads) lo = std::min(lo, r);
+        double per = 0.0;
+        switch (policy) {
+            case FERRET_POLICY_ITER_FISHER:
+                per = 4.0 * static_cast<double>(cur - lo + 1) + 4.0 + 4.0 * (s.v_r ? 6.0 : 2.0);
+                break;
+            case FERRET_POLICY_GAP: per = 4.0 * static_cast<double>(std::min<long long>(cur - lo, 1) + 1) + 4.0 + 8.0; break;
+            case FERRET_POLICY_FISHER: {
+                std::vector<long long> d(reads.begin(), reads.end());
+                d.push_back(cur);
+                std::sort(d.begin(), d.end());
+                d.erase(std::unique(d.begin(), d.end()), d.end());
+                per = 4.0 * static_cast<double>(d.size()) + 4.0;
+                break;
+            }
+            default: per = 8.0;
+        }
+        double side = 0.0;
+        for (int l = s.lo; l < s.hi; ++l)
+            side += 4.0 * B * (layers[static_cast<size_t>(l)].in + layers[static_cast<size_t>(l)].out);
+        return per * static_cast<double>(s.n_params) + side * static_cast<double>(reads.size());
+    }
+
     ~ferret_trainer() {
         cudaSetDevice(opt.device);
         if (stream) cudaStreamSynchronize(stream);
+        for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
         for (StageDev& s : stages) {
             dfree(s.ring);
             dfree(s.lam_d);
@@ -541,7 +594,11 @@ struct ferret_trainer {
                         for (size_t k = 0; k < pl.size(); ++k)
                             a.pend[k] = {stash(pl[k].u), xrows(pl[k].u), pl[k].read};
                         a.step = static_cast<float>(opt.lr * (1.0 / static_cast<double>(pl.size())));
+                        std::vector<long long> reads;
+                        for (const Pend& p : pl) reads.push_back(p.read);
+                        time_begin();
                         fb200::launch_update(a, stream);
+                        time_end(update_bytes(j, opt.policy, reads, cur));
                         ++launches;
                     }
                     st.current[static_cast<size_t>(j)] += 1;
@@ -943,6 +1000,34 @@ ferret_status ferret_trainer_get_stats(ferret_trainer* t, ferret_trainer_stats* 
 }
 
 void ferret_trainer_destroy(ferret_trainer* t) { delete t; }
+
+ferret_status ferret_trainer_set_timing(ferret_trainer* t, int32_t enable) {
+    return guarded([&] {
+        cuda_check(cudaStreamSynchronize(t->stream), "sync");
+        t->timing = enable != 0;
+        t->ev_used = 0;
+        t->upd_alg_bytes = 0.0;
+        t->upd_timed = 0;
+    });
+}
+
+ferret_status ferret_trainer_update_timing(ferret_trainer* t, double* total_ms, uint64_t* launches, double* alg_bytes) {
+    return guarded([&] {
+        cuda_check(cudaStreamSynchronize(t->stream), "sync");
+        double ms = 0.0;
+        for (size_t i = 0; i + 1 < t->ev_used; i += 2) {
+            float part = 0.f;
+            cuda_check(cudaEventElapsedTime(&part, t->ev_pool[i], t->ev_pool[i + 1]), "cudaEventElapsedTime");
+            ms += part;
+        }
+        *total_ms = ms;
+        *launches = t->upd_timed;
+        *alg_bytes = t->upd_alg_bytes;
+        t->ev_used = 0;
+        t->upd_alg_bytes = 0.0;
+        t->upd_timed = 0;
+    });
+}
 
 ferret_status ferret_compensate(int32_t policy, const double* g, const double* const* chain, int32_t chain_len,
                                 double* lambda, double* v_r, double* v_a, double* mean_gap, size_t n, double lambda0,

