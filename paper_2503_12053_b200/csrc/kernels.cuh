@@ -1,13 +1,12 @@
-// Device kernels of the ferret-b200 trainer and their launch records.
+// Device kernels of the ferret-b200 trainer and their launch arguments.
 //
-// Each struct below is the full argument set of one kernel launch; the trainer
-// (trainer.cpp) compiles the event log into a vector of these records with
-// every device pointer resolved, then replays them on one CUDA stream (or as
-// one CUDA graph). Kernels are SIMT fp32: at micro-batch B <= 16 every
-// stage op is a skinny GEMM with arithmetic intensity ~B/4 flop/byte, far
-// below the tensor-core ridge (~200 flop/byte), so the roofline is HBM (or L2
-// for nets that fit in it) and the design goal is coalesced, vectorised
-// streaming of the weights and version slots.
+// The trainer (trainer.cpp) compiles the event log into kernel launches with
+// every device pointer resolved on the host. Kernels are SIMT fp32: at
+// micro-batch B <= 16 every stage op is a skinny GEMM (arithmetic intensity
+// ~B/4 flop/byte, far below the ~200 flop/byte tensor-core ridge), so the
+// bound is memory — HBM for large stages, L2 + latency for the small nets of
+// configs 1-4 — and the design goal is grid-wide parallelism with coalesced
+// float4 streaming of weights and version slots.
 #pragma once
 
 #include <cstddef>
@@ -17,12 +16,14 @@
 
 namespace fb200 {
 
-constexpr int kMaxBatch = 16;      // micro-batch ceiling (one register lane per sample)
+constexpr int kMaxBatch = 16;      // micro-batch ceiling (register accumulators per sample)
 constexpr int kMaxStageLayers = 16;
 constexpr int kMaxPending = 16;    // pending gradients folded by one update launch
+constexpr int kMaxChain = 48;      // parameter versions one update launch may read
 constexpr int kMaxVersions = 64;   // chain length of the unit compensation entry
 
 // z[b][r] = act(bias[r] + sum_c W[r][c] * x_b[c])    (reference net.hpp:99-113)
+// Split-K CTA tiles: each CTA owns a few output rows, its 8 warps split K.
 struct FwdArgs {
     const float* W;      // out x in, row-major
     const float* bias;   // out
@@ -46,50 +47,58 @@ struct HeadArgs {
 };
 
 // d_in[b][c] = mask_b[c] * sum_r W[r][c] * d_out[b][r]   (reference learner.hpp:468-474)
-// mask (nullable) = post-activation output of the layer below (relu: keep where > 0)
+// mask (nullable) = post-activation output of the layer below (ReLU: keep where > 0).
+// Column tiles x row splits; warps of a CTA split its rows and reduce in smem;
+// with row_splits > 1 the last CTA of a column tile sums the split partials.
 struct BwdArgs {
     const float* W;
     const float* d_out;  // B x out
     const float* mask;   // B x in or nullptr
     float* d_in;         // B x in
     int in, out, B;
-    int row_splits;      // grid.y; >1 uses `partial` + `counters` (last CTA reduces)
+    int row_splits;
     float* partial;      // row_splits x B x in
     unsigned* counters;  // one per column tile, self-resetting
 };
 
-struct UpdLayer {
+// A contiguous run of update work items inside one stage: the weight matrix
+// of a layer (items = out x in/V, V = 4 when rows are float4-aligned) or its
+// bias vector (items = out, V = 1).
+struct UpdSeg {
+    int layer;            // index into the stage's layers (0-based)
+    int bias;             // 1 = bias segment
+    int vec;              // elements per item (1 or 4)
+    int per_row;          // items per row (in / vec) for weight segments
+    long long item0;      // first item of this segment
+    long long elem0;      // float offset of element 0 inside a stage slot
     int in, out;
-    long long woff, boff;  // float offsets inside a stage slot
-    int row0;              // first flat row of this layer in the stage
-    long long xin_off;     // stash offset of this layer's input (activation of layer l-1); -1 = net input
-    long long dlt_off;     // stash offset of this layer's delta
+    long long xin_off;    // stash offset of the layer input (activation of layer l-1); -1 = net input
+    long long dlt_off;    // stash offset of the layer's delta
 };
 
 struct UpdPending {
-    const float* stash;    // the unit's stash slot (activations + deltas)
-    const float* x0;       // net-input rows of the unit (used when the stage holds layer 0)
-    long long read_version;
+    const float* stash;   // the unit's stash slot (activations + deltas)
+    const float* x0;      // net-input rows of the unit (when the stage holds layer 0)
+    int first;            // index of its read version in vers[]
 };
 
 // One stage update (reference learner.hpp:491-510 + compensate.hpp:42-130):
 // for every parameter, for each pending gradient k (in order):
 //   g_k = sum_b delta_k[b][r] * x_k[b][c]   (bias: sum_b delta_k[b][r])
-//   out_k = Compensator::apply(g_k, versions read_k .. cur)
-// then theta_new = theta_cur - step * sum_k out_k, written to version cur+1.
-// Version v of the stage lives in ring slot (v mod depth).
+//   out_k = Compensator::apply(g_k, vers[first_k .. nv-1])
+// then theta_new = theta_cur - step * sum_k out_k, written to `dst`.
 struct UpdArgs {
-    int n_layers, total_rows, B, K, policy;
-    const UpdLayer* L;       // device array, n_layers entries
+    int n_segs, B, K, policy;
+    long long n_items;
+    const UpdSeg* segs;      // device array
     UpdPending pend[kMaxPending];
-    int x0_gather;           // 1: net-input row b of pending 0 is x0 + x0off[b] (replay)
-    int x0_ld;               // else row b is x0 + b * x0_ld
+    int x0_gather;           // 1: net-input row b is x0 + x0off[b] (replay); else x0 + b * x0_ld
+    int x0_ld;
     long long x0off[kMaxBatch];
-    const float* ring;
-    long long slot_floats;
-    int depth;
-    long long cur_version;
-    float* lam_d;   // iter_fisher: lambda - lambda0 (fp32 offset keeps the 1e-10 drift exact)
+    const float* vers[kMaxChain]; // oldest needed version .. current (vers[nv-1])
+    int nv;
+    float* dst;              // new version slot
+    float* lam_d;   // iter_fisher: lambda - lambda0 (fp32 offset keeps the ~1e-10 drift)
     float* v_r;
     float* v_a;
     float* gap;     // gap policy running mean
@@ -114,7 +123,7 @@ void launch_head(const HeadArgs& a, cudaStream_t s);
 void launch_bwd(const BwdArgs& a, cudaStream_t s);
 void launch_update(const UpdArgs& a, cudaStream_t s);
 void launch_normalize(const NormArgs& a, cudaStream_t s);
-// column tiles / rows per split the bwd launcher uses (for scratch sizing)
+// grid geometry of the bwd launcher (for scratch sizing)
 int bwd_col_tiles(int in);
 int bwd_row_splits(int in, int out);
 

@@ -104,7 +104,9 @@ struct StageDev {
     float* v_r = nullptr;
     float* v_a = nullptr;
     float* gap = nullptr;
-    fb200::UpdLayer* L_dev = nullptr;
+    fb200::UpdSeg* segs_dev = nullptr;
+    int n_segs = 0;
+    long long n_items = 0;
     float* slot(long long v) const { return ring + (v % depth) * slot_floats; }
 };
 
@@ -133,6 +135,9 @@ struct ferret_trainer {
     std::vector<StageDev> stages;
     std::vector<double> init_params;
     cudaStream_t stream = nullptr;
+    cudaStream_t nstream = nullptr;          // side stream: the normalizer runs ahead of training
+    std::vector<cudaEvent_t> norm_events;    // one per group of kNormGroup units
+    static constexpr size_t kNormGroup = 16;
     size_t device_bytes = 0;
 
     // stream resident in HBM
@@ -216,14 +221,16 @@ struct ferret_trainer {
     ~ferret_trainer() {
         cudaSetDevice(opt.device);
         if (stream) cudaStreamSynchronize(stream);
+        if (nstream) cudaStreamSynchronize(nstream);
         for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
+        for (cudaEvent_t e : norm_events) cudaEventDestroy(e);
         for (StageDev& s : stages) {
             dfree(s.ring);
             dfree(s.lam_d);
             dfree(s.v_r);
             dfree(s.v_a);
             dfree(s.gap);
-            dfree(s.L_dev);
+            dfree(s.segs_dev);
         }
         dfree(d_raw);
         dfree(d_x);
@@ -236,6 +243,7 @@ struct ferret_trainer {
         dfree(d_partial);
         dfree(d_counters);
         if (stream) cudaStreamDestroy(stream);
+        if (nstream) cudaStreamDestroy(nstream);
     }
 
     // ------------------------------------------------------------------ setup
@@ -290,7 +298,7 @@ struct ferret_trainer {
             if (s.hi - s.lo > fb200::kMaxStageLayers) fail(FERRET_E_CONFIG, "at most 16 layers per stage");
             s.host_off = layers[static_cast<size_t>(s.lo)].host_off;
             long long c = 0;
-            std::vector<fb200::UpdLayer> tab;
+            std::vector<fb200::UpdSeg> tab;
             for (int l = s.lo; l < s.hi; ++l) {
                 LayerDev& ld = layers[static_cast<size_t>(l)];
                 ld.stage = j;
@@ -299,15 +307,30 @@ struct ferret_trainer {
                 ld.boff = align_up(c, 32);
                 c = ld.boff + ld.out;
                 s.n_params += static_cast<long long>(ld.in) * ld.out + ld.out;
-                fb200::UpdLayer ul{};
-                ul.in = ld.in;
-                ul.out = ld.out;
-                ul.woff = ld.woff;
-                ul.boff = ld.boff;
-                ul.row0 = s.total_rows;
-                ul.xin_off = l == 0 ? -1 : layers[static_cast<size_t>(l - 1)].act_off;
-                ul.dlt_off = ld.dlt_off;
-                tab.push_back(ul);
+                // float4 items need 16-byte aligned weight rows and input rows
+                // (stash rows are B x in, x rows are B x F with F == in at layer 0)
+                const int vec = (ld.in % 4 == 0) ? 4 : 1;
+                fb200::UpdSeg w{};
+                w.layer = l - s.lo;
+                w.bias = 0;
+                w.vec = vec;
+                w.per_row = ld.in / vec;
+                w.item0 = s.n_items;
+                w.elem0 = ld.woff;
+                w.in = ld.in;
+                w.out = ld.out;
+                w.xin_off = l == 0 ? -1 : layers[static_cast<size_t>(l - 1)].act_off;
+                w.dlt_off = ld.dlt_off;
+                tab.push_back(w);
+                s.n_items += static_cast<long long>(ld.out) * w.per_row;
+                fb200::UpdSeg bs = w;
+                bs.bias = 1;
+                bs.vec = 1;
+                bs.per_row = 1;
+                bs.item0 = s.n_items;
+                bs.elem0 = ld.boff;
+                tab.push_back(bs);
+                s.n_items += ld.out;
                 s.total_rows += ld.out;
                 if (l > 0) {
                     max_partial = std::max(max_partial, static_cast<size_t>(fb200::bwd_row_splits(ld.in, ld.out)) *
@@ -316,9 +339,10 @@ struct ferret_trainer {
                 }
             }
             s.slot_floats = align_up(c, 64);
-            s.L_dev = dalloc<fb200::UpdLayer>(tab.size(), device_bytes);
-            cuda_check(cudaMemcpy(s.L_dev, tab.data(), tab.size() * sizeof(fb200::UpdLayer), cudaMemcpyHostToDevice),
-                       "upload layer table");
+            s.n_segs = static_cast<int>(tab.size());
+            s.segs_dev = dalloc<fb200::UpdSeg>(tab.size(), device_bytes);
+            cuda_check(cudaMemcpy(s.segs_dev, tab.data(), tab.size() * sizeof(fb200::UpdSeg), cudaMemcpyHostToDevice),
+                       "upload segment table");
             const size_t n = static_cast<size_t>(s.slot_floats);
             if (opt.policy == FERRET_POLICY_ITER_FISHER) {
                 s.lam_d = dalloc<float>(n, device_bytes);
@@ -477,14 +501,34 @@ struct ferret_trainer {
         if (base + n_samples > n_loaded) fail(FERRET_E_OUT_OF_RANGE, "execute: chunk lies beyond the loaded stream");
         launches = 0;
         // 1. RunningNormalizer over every arrival of the chunk (observed in order,
-        //    dropped ones included: learner.hpp:393); model-independent, so it
-        //    is one kernel up front instead of one per arrival.
-        fb200::NormArgs na{d_raw + base * static_cast<size_t>(F), static_cast<long long>(n_samples), F,
-                           static_cast<unsigned long long>(hs.norm_count), d_norm_mean, d_norm_m2,
-                           d_x + base * static_cast<size_t>(F)};
-        fb200::launch_normalize(na, stream);
-        ++launches;
-        hs.norm_count += n_samples;
+        //    dropped ones included: learner.hpp:393). It is model-independent,
+        //    so it runs ahead on a side stream in groups of kNormGroup units;
+        //    the training stream waits on a group's event at the group's first
+        //    arrival. Sequential fp64 per feature (bit-exact), hidden behind the
+        //    training kernels except for the first group.
+        const size_t groups = (sched.n_units + kNormGroup - 1) / kNormGroup;
+        while (norm_events.size() < groups) {
+            cudaEvent_t e;
+            cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+            norm_events.push_back(e);
+        }
+        {
+            cudaEvent_t ready = norm_events[0];
+            cuda_check(cudaEventRecord(ready, stream), "cudaEventRecord");  // stream data (H2D) is in
+            cuda_check(cudaStreamWaitEvent(nstream, ready, 0), "cudaStreamWaitEvent");
+        }
+        for (size_t g = 0; g < groups; ++g) {
+            const size_t u0 = g * kNormGroup, u1 = std::min(sched.n_units, u0 + kNormGroup);
+            const size_t s0 = base + u0 * static_cast<size_t>(B);
+            const size_t ns = (u1 - u0) * static_cast<size_t>(B);
+            fb200::NormArgs na{d_raw + s0 * static_cast<size_t>(F), static_cast<long long>(ns), F,
+                               static_cast<unsigned long long>(hs.norm_count), d_norm_mean, d_norm_m2,
+                               d_x + s0 * static_cast<size_t>(F)};
+            fb200::launch_normalize(na, nstream);
+            cuda_check(cudaEventRecord(norm_events[g], nstream), "cudaEventRecord");
+            ++launches;
+            hs.norm_count += ns;
+        }
         // 2. dry run -> sizes
         HostState probe = hs;
         const PassResult need = run_pass<true>(probe, base);
@@ -540,6 +584,8 @@ struct ferret_trainer {
             const int j = e.stage;
             switch (e.kind) {
                 case FERRET_EV_ARRIVAL: {  // learner.hpp:389-410
+                    if (!DRY && u % kNormGroup == 0)
+                        cuda_check(cudaStreamWaitEvent(stream, norm_events[u / kNormGroup], 0), "cudaStreamWaitEvent");
                     if (sched.dropped[u]) break;
                     inflight[u] = 1;
                     if (!as_shipped) {
@@ -588,11 +634,13 @@ struct ferret_trainer {
                         tau_cnt[static_cast<size_t>(j)] += 1;
                     }
                     if (!DRY) {
-                        fb200::UpdArgs a = update_args(j, cur);
+                        long long oldest = cur;
+                        for (const Pend& p : pl) oldest = std::min(oldest, p.read);
+                        fb200::UpdArgs a = update_args(j, cur, oldest);
                         a.policy = opt.policy;
                         a.K = static_cast<int>(pl.size());
                         for (size_t k = 0; k < pl.size(); ++k)
-                            a.pend[k] = {stash(pl[k].u), xrows(pl[k].u), pl[k].read};
+                            a.pend[k] = {stash(pl[k].u), xrows(pl[k].u), static_cast<int>(pl[k].read - oldest)};
                         a.step = static_cast<float>(opt.lr * (1.0 / static_cast<double>(pl.size())));
                         std::vector<long long> reads;
                         for (const Pend& p : pl) reads.push_back(p.read);
@@ -640,19 +688,22 @@ struct ferret_trainer {
         return res;
     }
 
-    fb200::UpdArgs update_args(int j, long long cur) {
+    // Launch arguments of one update of stage j: the chain table holds the
+    // versions oldest_read .. cur (ring slots resolved here), dst = slot(cur+1).
+    fb200::UpdArgs update_args(int j, long long cur, long long oldest) {
         const StageDev& s = stages[static_cast<size_t>(j)];
         fb200::UpdArgs a{};
-        a.n_layers = s.hi - s.lo;
-        a.total_rows = s.total_rows;
+        a.n_segs = s.n_segs;
+        a.n_items = s.n_items;
         a.B = B;
-        a.L = s.L_dev;
+        a.segs = s.segs_dev;
         a.x0_gather = 0;
         a.x0_ld = F;
-        a.ring = s.ring;
-        a.slot_floats = s.slot_floats;
-        a.depth = s.depth;
-        a.cur_version = cur;
+        if (cur - oldest + 1 > fb200::kMaxChain)
+            fail(FERRET_E_CONFIG, "staleness chain longer than 48 versions is not supported by the update kernel");
+        a.nv = static_cast<int>(cur - oldest + 1);
+        for (long long v = oldest; v <= cur; ++v) a.vers[v - oldest] = s.slot(v);
+        a.dst = s.slot(cur + 1);
         a.lam_d = s.lam_d;
         a.v_r = s.v_r;
         a.v_a = s.v_a;
@@ -795,10 +846,11 @@ struct ferret_trainer {
                                       d_replay);
             }
             for (int j = 0; j < P; ++j) {
-                fb200::UpdArgs a = update_args(j, st.current[static_cast<size_t>(j)]);
+                const long long cur = st.current[static_cast<size_t>(j)];
+                fb200::UpdArgs a = update_args(j, cur, cur);
                 a.policy = FERRET_POLICY_NONE;
                 a.K = 1;
-                a.pend[0] = {d_replay, d_x, st.current[static_cast<size_t>(j)]};
+                a.pend[0] = {d_replay, d_x, 0};
                 a.x0_gather = 1;
                 for (int b = 0; b < B; ++b) a.x0off[b] = xoff[b];
                 a.step = static_cast<float>(opt.lr);
@@ -906,6 +958,7 @@ ferret_status ferret_trainer_create(const ferret_net_desc* net, const uint64_t* 
         auto t = std::make_unique<ferret_trainer>();
         t->opt = *opts;
         cuda_check(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking), "stream");
+        cuda_check(cudaStreamCreateWithFlags(&t->nstream, cudaStreamNonBlocking), "stream");
         t->build(*net, bounds, n_bounds);
         cuda_check(cudaDeviceSynchronize(), "create");
         *out = t.release();
