@@ -201,12 +201,15 @@ def main():
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
+    host_s = 0.0
     with ClockSampler(local) as clk:
         for s in range(args.steps):
             with torch.cuda.stream(stream):
                 flush.zero_()
                 starts[s].record(stream)
+            h0 = time.perf_counter()
             tr.execute(args.warmup + s)
+            host_s += time.perf_counter() - h0
             with torch.cuda.stream(stream):
                 ends[s].record(stream)
         tr.sync()
@@ -290,6 +293,7 @@ def main():
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
         "gpu_launches": int(launches_per_step * args.steps),
+        "host_issue_ms_per_step": 1e3 * host_s / args.steps,
         "online_accuracy_last_chunk": oacc_last,
         "trainer": {"ring_depth": stats["ring_depth"], "stash_slots": stats["stash_slots"],
                     "mean_tau": stats["mean_tau"], "device_bytes": stats["device_bytes"]},

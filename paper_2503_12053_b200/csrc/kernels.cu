@@ -440,7 +440,7 @@ __device__ __forceinline__ void update_item(const UpdArgs& a, const UpdSeg& sg, 
 }
 
 template <int POLICY>
-__global__ void __launch_bounds__(kThreads) update_kernel(const UpdArgs a) {
+__global__ void __launch_bounds__(kThreads, 3) update_kernel(const UpdArgs a) {
     const long long stride = (long long)gridDim.x * kThreads;
     for (long long q = (long long)blockIdx.x * kThreads + threadIdx.x; q < a.n_items; q += stride) {
         int s = 0;
