@@ -71,8 +71,8 @@ def test_oracle_pinned_to_golden(orc):
 def test_oracle_as_shipped_reproduces_reference_defect(fb, orc):
     """as shipped the reference trainer keys arrivals by worker -1 and never
     trains; the restated (item-keyed) trainer does."""
-    widths = [32, 48, 10]
-    n = 150
+    widths = [784, 64, 10]
+    n = 400
     params = fb.make_dense_net(widths, 1)
     feats, labels = fb.synth_drift_stream(n, widths[0], widths[-1], "split_tasks", 7)
     prof = fb.profile_from_widths(widths)
