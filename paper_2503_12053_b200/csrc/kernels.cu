@@ -70,6 +70,10 @@ __global__ void __launch_bounds__(kThreads) fwd_kernel(const FwdArgs a, int nwk)
     const int kc = (nk + nwk - 1) / nwk;
     const int k_lo = kw * kc, k_hi = min(nk, k_lo + kc);
     const int B = a.B;
+    const float* xr[BT];
+#pragma unroll
+    for (int b = 0; b < BT; ++b)
+        xr[b] = a.X + (size_t)(b < B ? (a.xidx ? __ldg(a.xidx + b) : b) : 0) * a.in;
     float acc[RW][BT];
 #pragma unroll
     for (int i = 0; i < RW; ++i)
@@ -81,7 +85,7 @@ __global__ void __launch_bounds__(kThreads) fwd_kernel(const FwdArgs a, int nwk)
                 float4 xv[BT];
 #pragma unroll
                 for (int b = 0; b < BT; ++b)
-                    xv[b] = b < B ? __ldg(reinterpret_cast<const float4*>(a.X + a.xoff[b]) + k)
+                    xv[b] = b < B ? __ldg(reinterpret_cast<const float4*>(xr[b]) + k)
                                   : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                 for (int i = 0; i < RW; ++i) {
@@ -98,7 +102,7 @@ __global__ void __launch_bounds__(kThreads) fwd_kernel(const FwdArgs a, int nwk)
             } else {
                 float xv[BT];
 #pragma unroll
-                for (int b = 0; b < BT; ++b) xv[b] = b < B ? __ldg(a.X + a.xoff[b] + k) : 0.f;
+                for (int b = 0; b < BT; ++b) xv[b] = b < B ? __ldg(xr[b] + k) : 0.f;
 #pragma unroll
                 for (int i = 0; i < RW; ++i) {
                     if (r0 + i >= a.out) break;
@@ -175,7 +179,7 @@ __global__ void __launch_bounds__(kThreads) head_kernel(const HeadArgs a) {
     float sum = 0.f;
     for (int k = lane; k < a.n_out; k += 32) sum += expf(z[k] - best);
     sum = warp_sum(sum);
-    const int label = a.labels[b];
+    const int label = a.labels[a.lidx ? a.lidx[b] : b];
     float* d = a.delta + (size_t)b * a.n_out;
     for (int k = lane; k < a.n_out; k += 32) {
         const float p = expf(z[k] - best) / sum;
@@ -393,7 +397,7 @@ __device__ __forceinline__ void update_item(const UpdArgs& a, const UpdSeg& sg, 
                 continue;
             }
             const float* xr = sg.xin_off >= 0 ? pk.stash + sg.xin_off + (size_t)b * sg.in
-                              : a.x0_gather   ? pk.x0 + a.x0off[b]
+                              : a.x0idx       ? pk.x0 + (size_t)__ldg(a.x0idx + b) * a.x0_ld
                                               : pk.x0 + (size_t)b * a.x0_ld;
             if (V == 4) {
                 const float4 x4 = __ldg(reinterpret_cast<const float4*>(xr + c));
@@ -486,7 +490,7 @@ __global__ void normalize_kernel(const NormArgs a) {
     const int f = blockIdx.x * blockDim.x + threadIdx.x;
     if (f >= a.F) return;
     double mu = a.mean[f], m2 = a.m2[f];
-    unsigned long long cnt = a.count0;
+    unsigned long long cnt = *a.count_base + a.count_off;
     for (long long i = 0; i < a.n; ++i) {
         const double x = a.raw[i * a.F + f];
         ++cnt;
@@ -501,11 +505,22 @@ __global__ void normalize_kernel(const NormArgs a) {
     a.m2[f] = m2;
 }
 
+// Replay-pool insertion: one CTA per sample of the unit.
+__global__ void pool_kernel(const PoolArgs a) {
+    const int b = blockIdx.x;
+    const int dst = a.dst[b];
+    if (dst < 0) return;
+    const float* src = a.x + (size_t)b * a.F;
+    float* out = a.pool_x + (size_t)dst * a.F;
+    for (int f = threadIdx.x; f < a.F; f += blockDim.x) out[f] = src[f];
+    if (threadIdx.x == 0) a.pool_labels[dst] = a.labels[b];
+}
+
 } // namespace
 
 void launch_fwd(const FwdArgs& a, cudaStream_t s) {
-    bool vec = (a.in & 3) == 0 && aligned16(a.W);
-    for (int b = 0; b < a.B && vec; ++b) vec = aligned16(a.X + a.xoff[b]);
+    // rows are b * in (or xidx[b] * in) floats from X: float4 needs in % 4 == 0 and aligned bases
+    const bool vec = (a.in & 3) == 0 && aligned16(a.W) && aligned16(a.X);
     if (a.B <= 1) fwd_dispatch<1, 4>(a, s, vec);
     else if (a.B <= 2) fwd_dispatch<2, 4>(a, s, vec);
     else if (a.B <= 4) fwd_dispatch<4, 4>(a, s, vec);
@@ -578,6 +593,10 @@ void launch_compensate(const CompArgs& a, cudaStream_t s) {
 
 void launch_normalize(const NormArgs& a, cudaStream_t s) {
     normalize_kernel<<<(a.F + 127) / 128, 128, 0, s>>>(a);
+}
+
+void launch_pool(const PoolArgs& a, cudaStream_t s) {
+    pool_kernel<<<a.B, 128, 0, s>>>(a);
 }
 
 } // namespace fb200

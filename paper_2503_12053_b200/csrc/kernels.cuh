@@ -28,7 +28,7 @@ struct FwdArgs {
     const float* W;      // out x in, row-major
     const float* bias;   // out
     const float* X;      // base of the input rows
-    long long xoff[kMaxBatch]; // row b of the input is X + xoff[b] (gather for replay)
+    const int* xidx;     // nullable: input row b is X + xidx[b] * in (replay gather), else X + b * in
     float* Y;            // B x out, row-major
     int in, out, B;
     int relu;
@@ -40,7 +40,8 @@ struct FwdArgs {
 struct HeadArgs {
     const float* logits; // B x n_out
     int n_out, B, mode;
-    int labels[kMaxBatch];
+    const int* labels;   // label of sample b: labels[lidx ? lidx[b] : b]
+    const int* lidx;     // nullable (replay: pool positions)
     int* pred;
     float* delta;        // B x n_out
     float scale;
@@ -92,9 +93,8 @@ struct UpdArgs {
     long long n_items;
     const UpdSeg* segs;      // device array
     UpdPending pend[kMaxPending];
-    int x0_gather;           // 1: net-input row b is x0 + x0off[b] (replay); else x0 + b * x0_ld
+    const int* x0idx;        // nullable: net-input row b is x0 + x0idx[b] * x0_ld (replay), else x0 + b * x0_ld
     int x0_ld;
-    long long x0off[kMaxBatch];
     const float* vers[kMaxChain]; // oldest needed version .. current (vers[nv-1])
     int nv;
     float* dst;              // new version slot
@@ -112,10 +112,22 @@ struct NormArgs {
     const double* raw;   // n x F
     long long n;
     int F;
-    unsigned long long count0;
+    const unsigned long long* count_base;  // device: observations before this chunk
+    unsigned long long count_off;          // observations of this chunk before this group
     double* mean;
     double* m2;
     float* out;          // n x F
+};
+
+// Replay-pool insertion at an arrival (ReplayBuffer::add, learner.hpp:61-69):
+// sample b of the unit goes to pool position dst[b] (>= 0) or is skipped.
+struct PoolArgs {
+    const float* x;      // B x F normalised rows of the unit
+    const int* labels;   // B labels of the unit
+    const int* dst;      // B pool positions (or -1), filled per chunk by the host reservoir
+    float* pool_x;       // capacity x F
+    int* pool_labels;    // capacity
+    int B, F;
 };
 
 void launch_fwd(const FwdArgs& a, cudaStream_t s);
@@ -123,6 +135,7 @@ void launch_head(const HeadArgs& a, cudaStream_t s);
 void launch_bwd(const BwdArgs& a, cudaStream_t s);
 void launch_update(const UpdArgs& a, cudaStream_t s);
 void launch_normalize(const NormArgs& a, cudaStream_t s);
+void launch_pool(const PoolArgs& a, cudaStream_t s);
 // grid geometry of the bwd launcher (for scratch sizing)
 int bwd_col_tiles(int in);
 int bwd_row_splits(int in, int out);

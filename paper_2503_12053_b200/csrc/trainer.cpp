@@ -1,23 +1,37 @@
 // ferret_trainer: PipelineTrainer (reference learner.hpp:330-526) on one B200.
 //
 // The reference interprets the simulator's event log one event at a time on
-// the host, copying whole nets per event. Here the log is compiled into a
-// sequence of sm_100a kernel launches whose device pointers are all resolved
-// on the host, in two passes over the log:
-//   1. a dry run on a copy of the host state sizes the HBM structures exactly:
-//      the per-stage version ring (depth = the longest live chain + 1, not the
-//      reference's leaky hold set, learner.hpp:419/507) and the stash slots
-//      (one per in-flight pipeline unit, freed at the unit's last use);
-//   2. the real pass launches the kernels on one CUDA stream in log order.
-// Everything the north star requires to be bit-exact (routing, schedule,
-// replay indices) is decided here on the host with the reference's own
-// arithmetic; the device only does fp32 math.
+// the host, copying whole nets per event. Here the log is compiled ONCE per
+// schedule into a CUDA graph of sm_100a kernels and replayed per stream chunk:
 //
-// HBM layout: per stage a ring of `depth` version slots
-// (fp32, per-layer W/b at 128-byte-aligned offsets), the compensator state
-// (lambda offset, v_r, v_a or mean_gap) of the same shape, the normalised
-// stream x[n][F], and the stash: per in-flight unit every layer's activation
-// and delta (B x width).
+//   set_schedule   analyse the log: drops, per-unit last use, which (unit,
+//                  stage) backwards exist, which updates fire.
+//   build_graph    (first execute) a dry pass sizes the HBM structures — the
+//                  per-stage version ring (depth = the longest live chain + 1;
+//                  the reference's hold set leaks, learner.hpp:419/507) and the
+//                  stash slots (one per in-flight unit, freed at its last use)
+//                  — then a second pass launches every kernel in log order
+//                  under stream capture. All launch parameters are chunk
+//                  invariant: chunk data sit in fixed staging buffers, version
+//                  slots are relative to the chunk start (the live version is
+//                  moved back to slot 0 at the end of the graph), and the
+//                  per-chunk replay decisions are read from device arrays.
+//   execute(c)     host: run the replay reservoir over chunk c (the only
+//                  stateful host arithmetic, identical RNG draws to
+//                  learner.hpp:56-80) and copy its decisions + the chunk's
+//                  stream data into the staging buffers; device: one
+//                  cudaGraphLaunch.
+//
+// Everything the north star requires to be bit-exact (routing, schedule,
+// replay indices) is decided on the host with the reference's own arithmetic;
+// the device does fp32 math plus the fp64 normalizer.
+//
+// HBM layout: per stage a ring of `depth` version slots (fp32,
+// per-layer W/b at 128-byte aligned offsets) and the compensator state of the
+// same shape (lambda offset, v_r, v_a or mean_gap); the resident stream
+// (fp64 raw, int32 labels, int32 predictions); per chunk the raw/normalised
+// staging rows; the stash (per in-flight unit: every layer's activation and
+// delta, B x width); the replay pool (capacity x F normalised rows + labels).
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -56,48 +70,43 @@ void dfree(void* p) {
     if (p) cudaFree(p);
 }
 
-// Reservoir over stream positions (reference ReplayBuffer, learner.hpp:56-80):
-// identical RNG draws; stores the sample's index instead of its features
-// because the normalised features of every sample stay resident in HBM.
-struct ReplayIndex {
+// Reservoir over pool positions (reference ReplayBuffer, learner.hpp:56-80):
+// the same RNG draws, tracking where each added sample lands instead of the
+// sample itself — the normalised rows live in the device pool.
+struct Reservoir {
     uint64_t cap = 0;
     ferret::Rng rng{0};
     uint64_t seen = 0;
-    std::vector<long long> items;
+    uint64_t size = 0;
 
-    ReplayIndex() = default;
-    ReplayIndex(uint64_t capacity, uint64_t seed) : cap(capacity), rng(seed ^ 0xbf58476d1ce4e5b9ULL) {}
+    Reservoir() = default;
+    Reservoir(uint64_t capacity, uint64_t seed) : cap(capacity), rng(seed ^ 0xbf58476d1ce4e5b9ULL) {}
 
-    void add(long long id) {
+    int add() {  // pool position the new sample is written to, or -1
         ++seen;
-        if (items.size() < cap) {
-            items.push_back(id);
-            return;
-        }
+        if (size < cap) return static_cast<int>(size++);
         const uint64_t at = rng.below(seen);
-        if (at < cap) items[static_cast<size_t>(at)] = id;
+        return at < cap ? static_cast<int>(at) : -1;
     }
-    bool empty() const { return items.empty(); }
-    long long sample() { return items[static_cast<size_t>(rng.below(items.size()))]; }
+    int sample() { return static_cast<int>(rng.below(size)); }
 };
 
 struct HostState {
-    std::vector<long long> current;  // per stage: version of the live parameters
-    ReplayIndex replay;
+    std::vector<long long> current;  // per stage: absolute version of the live parameters
+    Reservoir replay;
     uint64_t norm_count = 0;
 };
 
 struct LayerDev {
     int in = 0, out = 0, act = 0, stage = 0;
-    long long woff = 0, boff = 0;      // inside the stage slot
-    long long host_off = 0;            // in flatten() order of the whole net
-    long long act_off = 0, dlt_off = 0; // inside a stash slot
+    long long woff = 0, boff = 0;        // inside the stage slot
+    long long host_off = 0;              // in flatten() order of the whole net
+    long long act_off = 0, dlt_off = 0;  // inside a stash slot
 };
 
 struct StageDev {
     int lo = 0, hi = 0;
     long long n_params = 0, slot_floats = 0, host_off = 0;
-    int total_rows = 0;
     int depth = 0;
     float* ring = nullptr;
     float* lam_d = nullptr;
@@ -107,23 +116,34 @@ struct StageDev {
     fb200::UpdSeg* segs_dev = nullptr;
     int n_segs = 0;
     long long n_items = 0;
-    float* slot(long long v) const { return ring + (v % depth) * slot_floats; }
+    // slot of a version counted from the chunk start (the live version is in slot 0 between chunks)
+    float* slot(long long rel) const { return ring + (rel % depth) * slot_floats; }
 };
 
 // Schedule facts independent of the mutable state (computed once per log).
 struct Schedule {
     std::vector<ferret_event> events;
     size_t n_units = 0;
-    size_t chunk_items = 0;               // stream samples per execute()
-    std::vector<char> dropped;            // per unit
-    std::vector<char> has_bwd;            // per unit x stage
-    std::vector<long long> last_use;      // per unit: last event index touching its stash
-    std::vector<std::vector<size_t>> free_at; // per event index: units whose stash frees after it
+    size_t chunk_items = 0;                    // stream samples per execute()
+    std::vector<char> dropped;                 // per unit
+    std::vector<char> has_bwd;                 // per unit x stage
+    std::vector<char> update_fires;            // per event: an update with pending gradients
+    std::vector<std::vector<size_t>> free_at;  // per event index: units whose stash frees after it
+};
+
+// What the device graph needs from the host for one chunk.
+struct ChunkPlan {
+    std::vector<int> pool_dst;  // per chunk sample: replay-pool position or -1
+    std::vector<int> rep_ids;   // per replay step x B: pool positions sampled
+    size_t n_replays = 0;
 };
 
 struct PassResult {
     std::vector<int> need_depth;
+    std::vector<long long> pushes;
     int need_slots = 0;
+    size_t n_replays = 0;
+    size_t n_updates_timed = 0;
 };
 
 } // namespace
@@ -135,19 +155,37 @@ struct ferret_trainer {
     std::vector<StageDev> stages;
     std::vector<double> init_params;
     cudaStream_t stream = nullptr;
-    cudaStream_t nstream = nullptr;          // side stream: the normalizer runs ahead of training
-    std::vector<cudaEvent_t> norm_events;    // one per group of kNormGroup units
+    cudaStream_t nstream = nullptr;  // side stream: the normalizer runs ahead of training
     static constexpr size_t kNormGroup = 16;
+    std::vector<cudaEvent_t> norm_events;
+    cudaEvent_t fork_event = nullptr;
     size_t device_bytes = 0;
 
-    // stream resident in HBM
+    // resident stream
     double* d_raw = nullptr;
-    float* d_x = nullptr;
+    int* d_lab = nullptr;
     int* d_pred = nullptr;
     size_t n_loaded = 0;
     std::vector<int> labels;
     double* d_norm_mean = nullptr;
     double* d_norm_m2 = nullptr;
+
+    // per-chunk staging (fixed addresses baked into the graph)
+    size_t chunk_cap = 0;
+    double* d_rawc = nullptr;
+    float* d_xc = nullptr;
+    int* d_labc = nullptr;
+    int* d_predc = nullptr;
+    // control block: [count_base u64][pool_dst chunk_cap x i32][rep_ids max_rep x B x i32]
+    unsigned char* d_ctl = nullptr;
+    std::vector<unsigned char*> h_ctl;  // pinned, double-buffered
+    std::vector<cudaEvent_t> ctl_done;
+    size_t ctl_bytes = 0, max_rep = 0;
+    int ctl_flip = 0;
+
+    // replay pool
+    float* d_pool_x = nullptr;
+    int* d_pool_lab = nullptr;
 
     // scratch
     float* d_stash = nullptr;
@@ -163,23 +201,818 @@ struct ferret_trainer {
     Schedule sched;
     bool have_schedule = false;
 
+    // the compiled graph of the current schedule
+    cudaGraphExec_t graph_exec = nullptr;
+    bool graph_timing = false;
+    bool graph_seen_any = false;  // reservoir non-empty at chunk start when captured
+    PassResult graph_shape;
+
     ferret_trainer_stats stats{};
     uint64_t launches = 0;
 
-    // optional per-launch timing of the update kernel (CUDA events on `stream`)
+    // optional per-launch timing of the update kernel (event record nodes)
     bool timing = false;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
-    double upd_alg_bytes = 0.0;   // algorithmic HBM bytes of the timed update launches
+    double upd_alg_bytes = 0.0;
     uint64_t upd_timed = 0;
 
+    ~ferret_trainer() {
+        cudaSetDevice(opt.device);
+        if (stream) cudaStreamSynchronize(stream);
+        if (nstream) cudaStreamSynchronize(nstream);
+        if (graph_exec) cudaGraphExecDestroy(graph_exec);
+        for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
+        for (cudaEvent_t e : norm_events) cudaEventDestroy(e);
+        for (cudaEvent_t e : ctl_done) cudaEventDestroy(e);
+        if (fork_event) cudaEventDestroy(fork_event);
+        for (unsigned char* p : h_ctl) cudaFreeHost(p);
+        for (StageDev& s : stages) {
+            dfree(s.ring);
+            dfree(s.lam_d);
+            dfree(s.v_r);
+            dfree(s.v_a);
+            dfree(s.gap);
+            dfree(s.segs_dev);
+        }
+        for (void* p : {static_cast<void*>(d_raw), static_cast<void*>(d_lab), static_cast<void*>(d_pred),
+                        static_cast<void*>(d_norm_mean), static_cast<void*>(d_norm_m2), static_cast<void*>(d_rawc),
+                        static_cast<void*>(d_xc), static_cast<void*>(d_labc), static_cast<void*>(d_predc),
+                        static_cast<void*>(d_ctl), static_cast<void*>(d_pool_x), static_cast<void*>(d_pool_lab),
+                        static_cast<void*>(d_stash), static_cast<void*>(d_pred_buf), static_cast<void*>(d_replay),
+                        static_cast<void*>(d_partial), static_cast<void*>(d_counters)})
+            dfree(p);
+        if (stream) cudaStreamDestroy(stream);
+        if (nstream) cudaStreamDestroy(nstream);
+    }
+
+    void invalidate_graph() {
+        if (graph_exec) {
+            cudaStreamSynchronize(stream);
+            cudaGraphExecDestroy(graph_exec);
+            graph_exec = nullptr;
+        }
+    }
+
+    // ------------------------------------------------------------------ setup
+    void build(const ferret_net_desc& net, const uint64_t* bounds, int32_t n_bounds) {
+        L = net.n_layers;
+        if (L <= 0) fail(FERRET_E_CONFIG, "net needs at least one layer");
+        if (n_bounds < 2 || bounds[0] != 0 || bounds[n_bounds - 1] != static_cast<uint64_t>(L))
+            fail(FERRET_E_CONFIG, "partition bounds must run from 0 to the layer count");
+        for (int32_t i = 1; i < n_bounds; ++i)
+            if (bounds[i] <= bounds[i - 1]) fail(FERRET_E_CONFIG, "partition bounds must be strictly increasing");
+        P = n_bounds - 1;
+        if (P > 16) fail(FERRET_E_CONFIG, "at most 16 stages per trainer");
+        B = opt.micro_batch;
+        if (B < 1 || B > fb200::kMaxBatch) fail(FERRET_E_CONFIG, "micro_batch must lie in [1, 16]");
+        if (opt.policy < 0 || opt.policy > 4) fail(FERRET_E_CONFIG, "unknown compensation policy");
+        if (opt.precision != FERRET_PREC_FP32) fail(FERRET_E_CONFIG, "only the fp32 parity precision is built");
+        if (opt.replay && (opt.replay_capacity == 0 || opt.replay_capacity > (1ull << 30)))
+            fail(FERRET_E_CONFIG, "replay capacity must lie in [1, 2^30]");
+        layers.resize(static_cast<size_t>(L));
+        long long host_off = 0;
+        for (int l = 0; l < L; ++l) {
+            LayerDev& ld = layers[static_cast<size_t>(l)];
+            ld.in = static_cast<int>(net.in[l]);
+            ld.out = static_cast<int>(net.out[l]);
+            ld.act = net.act[l];
+            if (l > 0 && net.in[l] != net.out[l - 1])
+                fail(FERRET_E_CONFIG, "layer " + std::to_string(l) + ": input width mismatch");
+            ld.host_off = host_off;
+            host_off += static_cast<long long>(ld.in) * ld.out + ld.out;
+        }
+        F = layers.front().in;
+        n_out = layers.back().out;
+        init_params.assign(net.params, net.params + host_off);
+        long long cursor = 0;
+        int max_width = F;
+        for (LayerDev& ld : layers) {
+            ld.act_off = align_up(cursor, 32);
+            cursor = ld.act_off + static_cast<long long>(B) * ld.out;
+            ld.dlt_off = align_up(cursor, 32);
+            cursor = ld.dlt_off + static_cast<long long>(B) * ld.out;
+            max_width = std::max(max_width, ld.out);
+        }
+        stash_stride = align_up(cursor, 64);
+        pred_stride = align_up(static_cast<long long>(B) * max_width, 64);
+        stages.resize(static_cast<size_t>(P));
+        hs.current.assign(static_cast<size_t>(P), 0);
+        size_t max_partial = 1, max_tiles = 1;
+        for (int j = 0; j < P; ++j) {
+            StageDev& s = stages[static_cast<size_t>(j)];
+            s.lo = static_cast<int>(bounds[j]);
+            s.hi = static_cast<int>(bounds[j + 1]);
+            if (s.hi - s.lo > fb200::kMaxStageLayers) fail(FERRET_E_CONFIG, "at most 16 layers per stage");
+            s.host_off = layers[static_cast<size_t>(s.lo)].host_off;
+            long long c = 0;
+            std::vector<fb200::UpdSeg> tab;
+            for (int l = s.lo; l < s.hi; ++l) {
+                LayerDev& ld = layers[static_cast<size_t>(l)];
+                ld.stage = j;
+                ld.woff = align_up(c, 32);
+                c = ld.woff + static_cast<long long>(ld.in) * ld.out;
+                ld.boff = align_up(c, 32);
+                c = ld.boff + ld.out;
+                s.n_params += static_cast<long long>(ld.in) * ld.out + ld.out;
+                // float4 items need 16-byte aligned weight rows and input rows
+                // (stash rows are B x in; x rows are F wide with F == in at layer 0)
+                const int vec = (ld.in % 4 == 0) ? 4 : 1;
+                fb200::UpdSeg w{};
+                w.layer = l - s.lo;
+                w.bias = 0;
+                w.vec = vec;
+                w.per_row = ld.in / vec;
+                w.item0 = s.n_items;
+                w.elem0 = ld.woff;
+                w.in = ld.in;
+                w.out = ld.out;
+                w.xin_off = l == 0 ? -1 : layers[static_cast<size_t>(l - 1)].act_off;
+                w.dlt_off = ld.dlt_off;
+                tab.push_back(w);
+                s.n_items += static_cast<long long>(ld.out) * w.per_row;
+                fb200::UpdSeg bs = w;
+                bs.bias = 1;
+                bs.vec = 1;
+                bs.per_row = 1;
+                bs.item0 = s.n_items;
+                bs.elem0 = ld.boff;
+                tab.push_back(bs);
+                s.n_items += ld.out;
+                if (l > 0) {
+                    max_partial = std::max(max_partial, static_cast<size_t>(fb200::bwd_row_splits(ld.in, ld.out)) *
+                                                            static_cast<size_t>(B) * static_cast<size_t>(ld.in));
+                    max_tiles = std::max(max_tiles, static_cast<size_t>(fb200::bwd_col_tiles(ld.in)));
+                }
+            }
+            s.slot_floats = align_up(c, 64);
+            s.n_segs = static_cast<int>(tab.size());
+            s.segs_dev = dalloc<fb200::UpdSeg>(tab.size(), device_bytes);
+            cuda_check(cudaMemcpy(s.segs_dev, tab.data(), tab.size() * sizeof(fb200::UpdSeg), cudaMemcpyHostToDevice),
+                       "upload segment table");
+            const size_t n = static_cast<size_t>(s.slot_floats);
+            if (opt.policy == FERRET_POLICY_ITER_FISHER) {
+                s.lam_d = dalloc<float>(n, device_bytes);
+                cuda_check(cudaMemset(s.lam_d, 0, n * sizeof(float)), "memset");
+                if (opt.eta_lambda > 0.0) {
+                    s.v_r = dalloc<float>(n, device_bytes);
+                    s.v_a = dalloc<float>(n, device_bytes);
+                    cuda_check(cudaMemset(s.v_r, 0, n * sizeof(float)), "memset");
+                    cuda_check(cudaMemset(s.v_a, 0, n * sizeof(float)), "memset");
+                }
+            } else if (opt.policy == FERRET_POLICY_GAP) {
+                s.gap = dalloc<float>(n, device_bytes);
+                cuda_check(cudaMemset(s.gap, 0, n * sizeof(float)), "memset");
+            }
+            grow_ring(s, 2);
+        }
+        upload_initial_params();
+        d_pred_buf = dalloc<float>(static_cast<size_t>(2 * pred_stride), device_bytes);
+        d_replay = dalloc<float>(static_cast<size_t>(stash_stride), device_bytes);
+        d_partial = dalloc<float>(max_partial, device_bytes);
+        d_counters = dalloc<unsigned>(max_tiles, device_bytes);
+        cuda_check(cudaMemset(d_counters, 0, max_tiles * sizeof(unsigned)), "memset");
+        d_norm_mean = dalloc<double>(static_cast<size_t>(F), device_bytes);
+        d_norm_m2 = dalloc<double>(static_cast<size_t>(F), device_bytes);
+        cuda_check(cudaMemset(d_norm_mean, 0, static_cast<size_t>(F) * sizeof(double)), "memset");
+        cuda_check(cudaMemset(d_norm_m2, 0, static_cast<size_t>(F) * sizeof(double)), "memset");
+        if (opt.replay) {
+            d_pool_x = dalloc<float>(static_cast<size_t>(opt.replay_capacity) * static_cast<size_t>(F), device_bytes);
+            d_pool_lab = dalloc<int>(static_cast<size_t>(opt.replay_capacity), device_bytes);
+        }
+        hs.replay = Reservoir(opt.replay_capacity, opt.replay_seed);
+        cuda_check(cudaEventCreateWithFlags(&fork_event, cudaEventDisableTiming), "cudaEventCreate");
+    }
+
+    void upload_initial_params() {
+        for (StageDev& s : stages) {
+            std::vector<float> slot(static_cast<size_t>(s.slot_floats), 0.f);
+            for (int l = s.lo; l < s.hi; ++l) {
+                const LayerDev& ld = layers[static_cast<size_t>(l)];
+                const double* src = init_params.data() + ld.host_off;
+                const long long nw = static_cast<long long>(ld.in) * ld.out;
+                for (long long i = 0; i < nw; ++i) slot[static_cast<size_t>(ld.woff + i)] = static_cast<float>(src[i]);
+                for (int r = 0; r < ld.out; ++r)
+                    slot[static_cast<size_t>(ld.boff + r)] = static_cast<float>(src[nw + r]);
+            }
+            cuda_check(cudaMemcpy(s.slot(0), slot.data(), slot.size() * sizeof(float), cudaMemcpyHostToDevice),
+                       "upload params");
+        }
+    }
+
+    // Grow a stage ring to `depth` slots; the live version is in slot 0 between chunks.
+    void grow_ring(StageDev& s, int depth) {
+        if (depth <= s.depth) return;
+        float* fresh = dalloc<float>(static_cast<size_t>(depth) * static_cast<size_t>(s.slot_floats), device_bytes);
+        if (s.ring) {
+            cuda_check(cudaStreamSynchronize(stream), "sync");
+            cuda_check(cudaMemcpy(fresh, s.ring, static_cast<size_t>(s.slot_floats) * sizeof(float),
+                                  cudaMemcpyDeviceToDevice),
+                       "ring copy");
+            cudaFree(s.ring);
+            device_bytes -= static_cast<size_t>(s.depth) * static_cast<size_t>(s.slot_floats) * sizeof(float);
+        }
+        s.ring = fresh;
+        s.depth = depth;
+    }
+
+    void ensure_stash(int slots) {
+        if (slots <= stash_slots) return;
+        cuda_check(cudaStreamSynchronize(stream), "sync");
+        if (d_stash) {
+            cudaFree(d_stash);
+            device_bytes -= static_cast<size_t>(stash_slots) * static_cast<size_t>(stash_stride) * sizeof(float);
+        }
+        d_stash = dalloc<float>(static_cast<size_t>(slots) * static_cast<size_t>(stash_stride), device_bytes);
+        stash_slots = slots;
+    }
+
+    // ---------------------------------------------------------------- stream
+    void load_stream(const double* features, const uint64_t* lab, size_t n, size_t f) {
+        if (static_cast<int>(f) != F) fail(FERRET_E_INVALID_ARG, "stream feature width does not match the net input");
+        std::vector<int> l32(n);
+        for (size_t i = 0; i < n; ++i) {
+            if (lab[i] >= static_cast<uint64_t>(n_out)) fail(FERRET_E_INVALID_ARG, "forward_backward: label out of range");
+            l32[i] = static_cast<int>(lab[i]);
+        }
+        cuda_check(cudaStreamSynchronize(stream), "sync");
+        if (n > n_loaded || !d_raw) {
+            dfree(d_raw);
+            dfree(d_lab);
+            dfree(d_pred);
+            d_raw = dalloc<double>(n * f, device_bytes);
+            d_lab = dalloc<int>(n, device_bytes);
+            d_pred = dalloc<int>(n, device_bytes);
+        }
+        n_loaded = n;
+        labels = std::move(l32);
+        cuda_check(cudaMemcpyAsync(d_raw, features, n * f * sizeof(double), cudaMemcpyHostToDevice, stream), "H2D stream");
+        cuda_check(cudaMemcpyAsync(d_lab, labels.data(), n * sizeof(int), cudaMemcpyHostToDevice, stream), "H2D labels");
+        cuda_check(cudaStreamSynchronize(stream), "sync");  // `labels` may be reassigned by the next load
+    }
+
+    void set_schedule(const ferret_event* ev, size_t n_ev, size_t chunk_items) {
+        // same log and chunking: keep the compiled graph
+        if (have_schedule && sched.events.size() == n_ev && (chunk_items ? chunk_items : sched.chunk_items) == sched.chunk_items &&
+            (n_ev == 0 || std::memcmp(sched.events.data(), ev, n_ev * sizeof(ferret_event)) == 0))
+            return;
+        Schedule s;
+        s.events.assign(ev, ev + n_ev);
+        long long expect = 0;
+        for (const ferret_event& e : s.events) {
+            if (e.kind == FERRET_EV_ARRIVAL) {
+                if (e.item != expect) fail(FERRET_E_INVALID_ARG, "event log: arrivals must cover items 0..n-1 in order");
+                ++expect;
+            }
+        }
+        s.n_units = static_cast<size_t>(expect);
+        s.chunk_items = chunk_items ? chunk_items : s.n_units * static_cast<size_t>(B);
+        if (s.n_units * static_cast<size_t>(B) > s.chunk_items)
+            fail(FERRET_E_INVALID_ARG, "event log covers more samples than one chunk");
+        s.dropped.assign(s.n_units, 0);
+        s.has_bwd.assign(s.n_units * static_cast<size_t>(P), 0);
+        s.update_fires.assign(s.events.size(), 0);
+        std::vector<long long> last_use(s.n_units, -1);
+        std::map<std::pair<int, int>, std::vector<long long>> open;  // (worker, stage) -> units awaiting update
+        for (size_t i = 0; i < s.events.size(); ++i) {
+            const ferret_event& e = s.events[i];
+            const bool staged = e.kind == FERRET_EV_FORWARD || e.kind == FERRET_EV_BACKWARD || e.kind == FERRET_EV_UPDATE;
+            if (e.kind < FERRET_EV_ARRIVAL || e.kind > FERRET_EV_UPDATE) fail(FERRET_E_INVALID_ARG, "event log: unknown event kind");
+            if (staged && (e.stage < 0 || e.stage >= P))
+                fail(FERRET_E_INVALID_ARG, "event log: stage out of range for this partition");
+            if (e.kind != FERRET_EV_UPDATE && (e.item < 0 || static_cast<size_t>(e.item) >= s.n_units))
+                fail(FERRET_E_INVALID_ARG, "event log: item out of range");
+            const size_t u = static_cast<size_t>(e.item);
+            switch (e.kind) {
+                case FERRET_EV_DROP: s.dropped[u] = 1; break;
+                case FERRET_EV_ARRIVAL:
+                case FERRET_EV_FORWARD: last_use[u] = static_cast<long long>(i); break;
+                case FERRET_EV_BACKWARD:
+                    last_use[u] = static_cast<long long>(i);
+                    s.has_bwd[u * static_cast<size_t>(P) + static_cast<size_t>(e.stage)] = 1;
+                    open[{e.worker, e.stage}].push_back(static_cast<long long>(u));
+                    break;
+                case FERRET_EV_UPDATE: {
+                    auto it = open.find({e.worker, e.stage});
+                    if (it == open.end() || it->second.empty()) break;
+                    s.update_fires[i] = 1;
+                    for (long long uu : it->second) last_use[static_cast<size_t>(uu)] = static_cast<long long>(i);
+                    it->second.clear();
+                    break;
+                }
+                default: break;
+            }
+        }
+        s.free_at.assign(s.events.size(), {});
+        for (size_t u = 0; u < s.n_units; ++u)
+            if (!s.dropped[u] && last_use[u] >= 0) s.free_at[static_cast<size_t>(last_use[u])].push_back(u);
+        sched = std::move(s);
+        have_schedule = true;
+        invalidate_graph();
+        alloc_chunk_buffers();
+    }
+
+    void alloc_chunk_buffers() {
+        const size_t cap = sched.chunk_items;
+        // replay steps per chunk <= stage-0 updates that fire
+        size_t upd0 = 0;
+        for (size_t i = 0; i < sched.events.size(); ++i)
+            if (sched.update_fires[i] && sched.events[i].stage == 0) ++upd0;
+        const size_t need_rep = opt.replay ? upd0 : 0;
+        const size_t need_ctl = 8 + cap * sizeof(int) + std::max<size_t>(need_rep, 1) * static_cast<size_t>(B) * sizeof(int);
+        if (cap > chunk_cap) {
+            cuda_check(cudaStreamSynchronize(stream), "sync");
+            for (void* p : {static_cast<void*>(d_rawc), static_cast<void*>(d_xc), static_cast<void*>(d_labc),
+                            static_cast<void*>(d_predc)})
+                dfree(p);
+            d_rawc = dalloc<double>(cap * static_cast<size_t>(F), device_bytes);
+            d_xc = dalloc<float>(cap * static_cast<size_t>(F), device_bytes);
+            d_labc = dalloc<int>(cap, device_bytes);
+            d_predc = dalloc<int>(cap, device_bytes);
+            chunk_cap = cap;
+        }
+        if (need_ctl > ctl_bytes) {
+            cuda_check(cudaStreamSynchronize(stream), "sync");
+            dfree(d_ctl);
+            for (unsigned char* p : h_ctl) cudaFreeHost(p);
+            h_ctl.clear();
+            d_ctl = dalloc<unsigned char>(need_ctl, device_bytes);
+            for (int k = 0; k < 2; ++k) {
+                void* p = nullptr;
+                cuda_check(cudaMallocHost(&p, need_ctl), "cudaMallocHost");
+                h_ctl.push_back(static_cast<unsigned char*>(p));
+                if (ctl_done.size() < 2) {
+                    cudaEvent_t e;
+                    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+                    ctl_done.push_back(e);
+                    cuda_check(cudaEventRecord(e, stream), "cudaEventRecord");
+                }
+            }
+            ctl_bytes = need_ctl;
+        }
+        max_rep = std::max<size_t>(need_rep, 1);
+    }
+
+    unsigned long long* ctl_count() const { return reinterpret_cast<unsigned long long*>(d_ctl); }
+    int* ctl_pool_dst() const { return reinterpret_cast<int*>(d_ctl + 8); }
+    int* ctl_rep_ids() const { return reinterpret_cast<int*>(d_ctl + 8 + chunk_cap * sizeof(int)); }
+
+    // -------------------------------------------------- host reservoir per chunk
+    // Walks the log exactly like the reference trainer's buffer_ calls
+    // (learner.hpp:409 add at every non-dropped arrival, :509/:514 sample at
+    // every firing stage-0 update while non-empty).
+    ChunkPlan plan_chunk(Reservoir& res) const {
+        ChunkPlan cp;
+        cp.pool_dst.assign(sched.chunk_items, -1);
+        if (!opt.replay || opt.as_shipped) return cp;
+        for (size_t i = 0; i < sched.events.size(); ++i) {
+            const ferret_event& e = sched.events[i];
+            if (e.kind == FERRET_EV_ARRIVAL && !sched.dropped[static_cast<size_t>(e.item)]) {
+                for (int b = 0; b < B; ++b)
+                    cp.pool_dst[static_cast<size_t>(e.item) * static_cast<size_t>(B) + static_cast<size_t>(b)] = res.add();
+            } else if (e.kind == FERRET_EV_UPDATE && e.stage == 0 && sched.update_fires[i] && res.size > 0) {
+                for (int b = 0; b < B; ++b) cp.rep_ids.push_back(res.sample());
+                ++cp.n_replays;
+            }
+        }
+        return cp;
+    }
+
+    // -------------------------------------------------------------- execute
+    void execute(size_t chunk) {
+        if (!have_schedule) fail(FERRET_E_LOGIC, "execute: no schedule set");
+        const size_t base = chunk * sched.chunk_items;
+        const size_t n_samples = sched.n_units * static_cast<size_t>(B);
+        if (base + n_samples > n_loaded) fail(FERRET_E_OUT_OF_RANGE, "execute: chunk lies beyond the loaded stream");
+        const bool seen_any = hs.replay.seen > 0;
+        if (graph_exec && (graph_timing != timing || graph_seen_any != seen_any)) invalidate_graph();
+        if (!graph_exec) build_graph(seen_any);
+        // host decisions for this chunk
+        const ChunkPlan cp = plan_chunk(hs.replay);
+        if (cp.n_replays != graph_shape.n_replays)
+            fail(FERRET_E_LOGIC, "replay pattern of this chunk differs from the compiled graph");
+        // control block -> device (double-buffered pinned staging)
+        unsigned char* h = h_ctl[static_cast<size_t>(ctl_flip)];
+        cuda_check(cudaEventSynchronize(ctl_done[static_cast<size_t>(ctl_flip)]), "cudaEventSynchronize");
+        const unsigned long long count = hs.norm_count;
+        std::memcpy(h, &count, 8);
+        std::memcpy(h + 8, cp.pool_dst.data(), cp.pool_dst.size() * sizeof(int));
+        if (!cp.rep_ids.empty())
+            std::memcpy(h + 8 + chunk_cap * sizeof(int), cp.rep_ids.data(), cp.rep_ids.size() * sizeof(int));
+        const size_t used = 8 + chunk_cap * sizeof(int) + cp.rep_ids.size() * sizeof(int);
+        cuda_check(cudaMemcpyAsync(d_ctl, h, used, cudaMemcpyHostToDevice, stream), "H2D control");
+        cuda_check(cudaEventRecord(ctl_done[static_cast<size_t>(ctl_flip)], stream), "cudaEventRecord");
+        ctl_flip ^= 1;
+        // chunk data -> staging
+        cuda_check(cudaMemcpyAsync(d_rawc, d_raw + base * static_cast<size_t>(F), n_samples * static_cast<size_t>(F) * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, stream),
+                   "D2D chunk");
+        cuda_check(cudaMemcpyAsync(d_labc, d_lab + base, n_samples * sizeof(int), cudaMemcpyDeviceToDevice, stream),
+                   "D2D labels");
+        cuda_check(cudaGraphLaunch(graph_exec, stream), "cudaGraphLaunch");
+        cuda_check(cudaMemcpyAsync(d_pred + base, d_predc, n_samples * sizeof(int), cudaMemcpyDeviceToDevice, stream),
+                   "D2D predictions");
+        hs.norm_count += n_samples;
+        for (int j = 0; j < P; ++j) hs.current[static_cast<size_t>(j)] += graph_shape.pushes[static_cast<size_t>(j)];
+        stats.kernel_launches = launches;
+        stats.stash_slots = stash_slots;
+        for (int j = 0; j < P && j < 16; ++j) stats.ring_depth[j] = stages[static_cast<size_t>(j)].depth;
+    }
+
+    void build_graph(bool seen_any) {
+        HostState probe = hs;
+        const PassResult need = run_pass<true>(probe, seen_any);
+        for (int j = 0; j < P; ++j) grow_ring(stages[static_cast<size_t>(j)], need.need_depth[static_cast<size_t>(j)]);
+        ensure_stash(std::max(need.need_slots, 1));
+        const size_t groups = (sched.n_units + kNormGroup - 1) / kNormGroup;
+        while (norm_events.size() < std::max<size_t>(groups, 1)) {
+            cudaEvent_t e;
+            cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+            norm_events.push_back(e);
+        }
+        if (timing)
+            while (ev_pool.size() < 2 * need.n_updates_timed) {
+                cudaEvent_t e;
+                cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+                ev_pool.push_back(e);
+            }
+        cuda_check(cudaStreamSynchronize(stream), "sync");
+        cudaGraph_t graph = nullptr;
+        cuda_check(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+        PassResult got;
+        try {
+            HostState cap = hs;
+            got = run_pass<false>(cap, seen_any);
+        } catch (...) {
+            cudaStreamEndCapture(stream, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            throw;
+        }
+        cuda_check(cudaStreamEndCapture(stream, &graph), "cudaStreamEndCapture");
+        const cudaError_t inst = cudaGraphInstantiate(&graph_exec, graph, 0);
+        cudaGraphDestroy(graph);
+        cuda_check(inst, "cudaGraphInstantiate");
+        graph_shape = got;
+        graph_timing = timing;
+        graph_seen_any = seen_any;
+    }
+
+    // One pass over the log. DRY only sizes; otherwise every kernel is
+    // launched on `stream`/`nstream` (under capture). `seen_any`: the replay
+    // buffer already holds samples at the chunk start.
+    template <bool DRY>
+    PassResult run_pass(HostState& st, bool seen_any) {
+        PassResult res;
+        res.need_depth.assign(static_cast<size_t>(P), 2);
+        res.pushes.assign(static_cast<size_t>(P), 0);
+        const bool as_shipped = opt.as_shipped != 0;
+        const size_t n_units = sched.n_units;
+        std::vector<long long> rel(static_cast<size_t>(P), 0);  // versions pushed since the chunk start
+        std::vector<int> slot_of(n_units, -1);
+        std::vector<int> free_slots;
+        int slots_used = 0;
+        std::vector<char> inflight(n_units, 0);
+        std::vector<long long> read_ver(n_units * static_cast<size_t>(P), -1);
+        std::vector<std::map<long long, int>> live(static_cast<size_t>(P));  // live read versions per stage
+        struct Pend {
+            size_t u;
+            long long read;
+        };
+        std::map<std::pair<int, int>, std::vector<Pend>> pending;
+        bool buffer_nonempty = seen_any;
+        uint64_t n_upd = 0, n_pred = 0;
+        std::vector<double> tau_sum(static_cast<size_t>(P), 0.0);
+        std::vector<uint64_t> tau_cnt(static_cast<size_t>(P), 0);
+        if (!DRY) {
+            launches = 0;
+            ev_used = 0;
+            upd_alg_bytes = 0.0;
+            upd_timed = 0;
+        }
+
+        auto floor_of = [&](int j) {
+            const long long cur = rel[static_cast<size_t>(j)];
+            const auto& m = live[static_cast<size_t>(j)];
+            return m.empty() ? cur : std::min(m.begin()->first, cur);
+        };
+        auto note_push = [&](int j) {  // a new version of stage j is about to be written
+            const long long span = rel[static_cast<size_t>(j)] - floor_of(j) + 2;
+            int& d = res.need_depth[static_cast<size_t>(j)];
+            d = std::max(d, static_cast<int>(span));
+            if (!DRY && span > stages[static_cast<size_t>(j)].depth)
+                fail(FERRET_E_LOGIC, "version ring undersized (dry run disagrees with the real pass)");
+        };
+        auto stash = [&](size_t u) { return d_stash + static_cast<long long>(slot_of[u]) * stash_stride; };
+        auto xrows = [&](size_t u) { return d_xc + u * static_cast<size_t>(B) * static_cast<size_t>(F); };
+
+        if (!DRY) {
+            // normalizer groups on the side stream (fork from the main stream)
+            cuda_check(cudaEventRecord(fork_event, stream), "cudaEventRecord");
+            cuda_check(cudaStreamWaitEvent(nstream, fork_event, 0), "cudaStreamWaitEvent");
+            const size_t groups = (n_units + kNormGroup - 1) / kNormGroup;
+            for (size_t g = 0; g < groups; ++g) {
+                const size_t u0 = g * kNormGroup, u1 = std::min(n_units, u0 + kNormGroup);
+                const size_t s0 = u0 * static_cast<size_t>(B);
+                const size_t ns = (u1 - u0) * static_cast<size_t>(B);
+                fb200::NormArgs na{d_rawc + s0 * static_cast<size_t>(F), static_cast<long long>(ns), F, ctl_count(),
+                                   static_cast<unsigned long long>(s0), d_norm_mean, d_norm_m2,
+                                   d_xc + s0 * static_cast<size_t>(F)};
+                fb200::launch_normalize(na, nstream);
+                cuda_check(cudaEventRecord(norm_events[g], nstream), "cudaEventRecord");
+                ++launches;
+            }
+            if (groups == 0) {  // join the fork even without arrivals
+                cuda_check(cudaEventRecord(norm_events[0], nstream), "cudaEventRecord");
+                cuda_check(cudaStreamWaitEvent(stream, norm_events[0], 0), "cudaStreamWaitEvent");
+            }
+        }
+
+        for (size_t idx = 0; idx < sched.events.size(); ++idx) {
+            const ferret_event& e = sched.events[idx];
+            const size_t u = static_cast<size_t>(e.item);
+            const int j = e.stage;
+            switch (e.kind) {
+                case FERRET_EV_ARRIVAL: {  // learner.hpp:389-410
+                    if (!DRY && u % kNormGroup == 0)
+                        cuda_check(cudaStreamWaitEvent(stream, norm_events[u / kNormGroup], 0), "cudaStreamWaitEvent");
+                    if (sched.dropped[u]) break;
+                    inflight[u] = 1;
+                    if (!as_shipped) {
+                        if (free_slots.empty()) free_slots.push_back(slots_used++);
+                        slot_of[u] = free_slots.back();
+                        free_slots.pop_back();
+                    }
+                    ++n_pred;
+                    if (!DRY) launch_predict(u, rel);
+                    if (opt.replay && !as_shipped) {
+                        buffer_nonempty = true;
+                        if (!DRY) {
+                            fb200::PoolArgs pa{xrows(u), d_labc + u * static_cast<size_t>(B),
+                                               ctl_pool_dst() + u * static_cast<size_t>(B), d_pool_x, d_pool_lab, B, F};
+                            fb200::launch_pool(pa, stream);
+                            ++launches;
+                        }
+                    }
+                    break;
+                }
+                case FERRET_EV_FORWARD: {  // learner.hpp:412-433
+                    if (as_shipped || !inflight[u]) break;
+                    const long long v = rel[static_cast<size_t>(j)];
+                    read_ver[u * static_cast<size_t>(P) + static_cast<size_t>(j)] = v;
+                    if (sched.has_bwd[u * static_cast<size_t>(P) + static_cast<size_t>(j)]) live[static_cast<size_t>(j)][v] += 1;
+                    if (!DRY) launch_stage_forward(j, stages[static_cast<size_t>(j)].slot(v), stash(u), xrows(u));
+                    break;
+                }
+                case FERRET_EV_BACKWARD: {  // learner.hpp:435-479
+                    if (as_shipped || !inflight[u]) break;
+                    const long long r = read_ver[u * static_cast<size_t>(P) + static_cast<size_t>(j)];
+                    if (r < 0) fail(FERRET_E_OUT_OF_RANGE, "stage version evicted");
+                    if (!DRY)
+                        launch_stage_backward(j, stages[static_cast<size_t>(j)].slot(r), stash(u),
+                                              d_labc + u * static_cast<size_t>(B));
+                    pending[{e.worker, j}].push_back({u, r});
+                    break;
+                }
+                case FERRET_EV_UPDATE: {  // learner.hpp:491-510
+                    if (as_shipped) break;
+                    auto it = pending.find({e.worker, j});
+                    if (it == pending.end() || it->second.empty()) break;
+                    const std::vector<Pend>& pl = it->second;
+                    if (pl.size() > static_cast<size_t>(fb200::kMaxPending))
+                        fail(FERRET_E_CONFIG, "accumulation count above 16 is not supported by the update kernel");
+                    note_push(j);
+                    const long long cur = rel[static_cast<size_t>(j)];
+                    long long oldest = cur;
+                    for (const Pend& p : pl) {
+                        tau_sum[static_cast<size_t>(j)] += static_cast<double>(cur - p.read);
+                        tau_cnt[static_cast<size_t>(j)] += 1;
+                        oldest = std::min(oldest, p.read);
+                    }
+                    ++n_upd;
+                    if (timing) ++res.n_updates_timed;
+                    if (!DRY) {
+                        fb200::UpdArgs a = update_args(j, cur, oldest);
+                        a.policy = opt.policy;
+                        a.K = static_cast<int>(pl.size());
+                        std::vector<long long> reads;
+                        for (size_t k = 0; k < pl.size(); ++k) {
+                            a.pend[k] = {stash(pl[k].u), xrows(pl[k].u), static_cast<int>(pl[k].read - oldest)};
+                            reads.push_back(pl[k].read);
+                        }
+                        a.step = static_cast<float>(opt.lr * (1.0 / static_cast<double>(pl.size())));
+                        time_begin();
+                        fb200::launch_update(a, stream);
+                        time_end(update_bytes(j, opt.policy, reads, cur));
+                        ++launches;
+                    }
+                    rel[static_cast<size_t>(j)] += 1;
+                    res.pushes[static_cast<size_t>(j)] += 1;
+                    for (const Pend& p : pl) {
+                        auto& m = live[static_cast<size_t>(j)];
+                        auto lv = m.find(p.read);
+                        if (lv != m.end() && --lv->second == 0) m.erase(lv);
+                    }
+                    it->second.clear();
+                    if (j == 0 && opt.replay && buffer_nonempty) {  // learner.hpp:509, 513-519
+                        replay_step<DRY>(res.n_replays, rel, note_push);
+                        for (int s = 0; s < P; ++s) res.pushes[static_cast<size_t>(s)] += 1;
+                        ++res.n_replays;
+                    }
+                    break;
+                }
+                default: break;  // drop, recompute: no trainer work (learner.hpp:359)
+            }
+            if (!as_shipped)
+                for (size_t fu : sched.free_at[idx])
+                    if (slot_of[fu] >= 0) {
+                        free_slots.push_back(slot_of[fu]);
+                        slot_of[fu] = -1;
+                    }
+        }
+        if (!DRY) {
+            // leave every stage's live version in slot 0 for the next chunk
+            for (int j = 0; j < P; ++j) {
+                const StageDev& s = stages[static_cast<size_t>(j)];
+                const long long fin = rel[static_cast<size_t>(j)] % s.depth;
+                if (fin != 0)
+                    cuda_check(cudaMemcpyAsync(s.ring, s.slot(fin), static_cast<size_t>(s.slot_floats) * sizeof(float),
+                                               cudaMemcpyDeviceToDevice, stream),
+                               "ring rebase");
+            }
+            stats.events = sched.events.size();
+            stats.updates = n_upd;
+            stats.replays = res.n_replays;
+            stats.predicts = n_pred;
+            for (int j = 0; j < P && j < 16; ++j) {
+                const double cnt = static_cast<double>(tau_cnt[static_cast<size_t>(j)]);
+                stats.mean_tau[j] = cnt > 0 ? tau_sum[static_cast<size_t>(j)] / cnt : 0.0;
+                stats.update_elems[j] = static_cast<uint64_t>(stages[static_cast<size_t>(j)].n_params) *
+                                        tau_cnt[static_cast<size_t>(j)];
+            }
+        }
+        res.need_slots = slots_used;
+        (void)st;
+        return res;
+    }
+
+    // Launch arguments of one update of stage j: the chain table holds the
+    // versions oldest_read .. cur (ring slots resolved here), dst = slot(cur+1).
+    fb200::UpdArgs update_args(int j, long long cur, long long oldest) {
+        const StageDev& s = stages[static_cast<size_t>(j)];
+        fb200::UpdArgs a{};
+        a.n_segs = s.n_segs;
+        a.n_items = s.n_items;
+        a.B = B;
+        a.segs = s.segs_dev;
+        a.x0idx = nullptr;
+        a.x0_ld = F;
+        if (cur - oldest + 1 > fb200::kMaxChain)
+            fail(FERRET_E_CONFIG, "staleness chain longer than 48 versions is not supported by the update kernel");
+        a.nv = static_cast<int>(cur - oldest + 1);
+        for (long long v = oldest; v <= cur; ++v) a.vers[v - oldest] = s.slot(v);
+        a.dst = s.slot(cur + 1);
+        a.lam_d = s.lam_d;
+        a.v_r = s.v_r;
+        a.v_a = s.v_a;
+        a.gap = s.gap;
+        a.lambda0 = static_cast<float>(opt.lambda0);
+        a.alpha = static_cast<float>(opt.alpha);
+        a.eta = static_cast<float>(opt.eta_lambda);
+        a.nu = static_cast<float>(opt.nu);
+        return a;
+    }
+
+    // ----------------------------------------------------- launch helpers
+    void launch_layer(const LayerDev& ld, const float* stage_slot, const float* X, const int* xidx, float* Y) {
+        fb200::FwdArgs a{};
+        a.W = stage_slot + ld.woff;
+        a.bias = stage_slot + ld.boff;
+        a.X = X;
+        a.xidx = xidx;
+        a.Y = Y;
+        a.in = ld.in;
+        a.out = ld.out;
+        a.B = B;
+        a.relu = ld.act == FERRET_ACT_RELU;
+        fb200::launch_fwd(a, stream);
+        ++launches;
+    }
+
+    // predict_class(net_, x) at the arrival (learner.hpp:398-399): full net, live versions.
+    void launch_predict(size_t u, const std::vector<long long>& rel) {
+        const float* X = d_xc + u * static_cast<size_t>(B) * static_cast<size_t>(F);
+        for (int l = 0; l < L; ++l) {
+            const LayerDev& ld = layers[static_cast<size_t>(l)];
+            const StageDev& s = stages[static_cast<size_t>(ld.stage)];
+            float* Y = d_pred_buf + (l & 1) * pred_stride;
+            launch_layer(ld, s.slot(rel[static_cast<size_t>(ld.stage)]), X, nullptr, Y);
+            X = Y;
+        }
+        fb200::HeadArgs h{};
+        h.logits = X;
+        h.n_out = n_out;
+        h.B = B;
+        h.mode = 0;
+        h.pred = d_predc + u * static_cast<size_t>(B);
+        fb200::launch_head(h, stream);
+        ++launches;
+    }
+
+    void launch_stage_forward(int j, const float* slot, float* stash_u, const float* x0) {
+        const StageDev& s = stages[static_cast<size_t>(j)];
+        for (int l = s.lo; l < s.hi; ++l) {
+            const LayerDev& ld = layers[static_cast<size_t>(l)];
+            const float* X = l == 0 ? x0 : stash_u + layers[static_cast<size_t>(l - 1)].act_off;
+            launch_layer(ld, slot, X, nullptr, stash_u + ld.act_off);
+        }
+    }
+
+    // delta at the logits (last stage) then per layer prev = W^T delta with the
+    // ReLU mask of the layer below applied on write (learner.hpp:443-476).
+    void launch_stage_backward(int j, const float* slot, float* stash_u, const int* lab) {
+        const StageDev& s = stages[static_cast<size_t>(j)];
+        if (j == P - 1) launch_delta_head(stash_u, lab, nullptr, 1.0f / static_cast<float>(B));
+        for (int l = s.hi - 1; l >= s.lo; --l) {
+            if (l == 0) break;  // no input gradient for the first layer
+            launch_layer_backward(l, slot, stash_u);
+        }
+    }
+
+    void launch_delta_head(float* stash_u, const int* lab, const int* lidx, float scale) {
+        const LayerDev& last = layers.back();
+        fb200::HeadArgs h{};
+        h.logits = stash_u + last.act_off;
+        h.n_out = n_out;
+        h.B = B;
+        h.mode = 1;
+        h.labels = lab;
+        h.lidx = lidx;
+        h.delta = stash_u + last.dlt_off;
+        h.scale = scale;
+        fb200::launch_head(h, stream);
+        ++launches;
+    }
+
+    void launch_layer_backward(int l, const float* slot, float* stash_u) {
+        const LayerDev& ld = layers[static_cast<size_t>(l)];
+        const LayerDev& below = layers[static_cast<size_t>(l - 1)];
+        fb200::BwdArgs a{};
+        a.W = slot + ld.woff;
+        a.d_out = stash_u + ld.dlt_off;
+        a.mask = below.act == FERRET_ACT_RELU ? stash_u + below.act_off : nullptr;
+        a.d_in = stash_u + below.dlt_off;
+        a.in = ld.in;
+        a.out = ld.out;
+        a.B = B;
+        a.row_splits = fb200::bwd_row_splits(ld.in, ld.out);
+        a.partial = d_partial;
+        a.counters = d_counters;
+        fb200::launch_bwd(a, stream);
+        ++launches;
+    }
+
+    // replay_step (learner.hpp:513-519): forward_backward(net_, {buffer.sample()})
+    // with mean reduction (net.hpp:157-200), apply_sgd on every stage, push a
+    // version per stage. B pool samples per replay step at micro-batch B; the
+    // pool positions come from the control block (row r of rep_ids).
+    template <bool DRY, class NotePush>
+    void replay_step(size_t r, std::vector<long long>& rel, NotePush& note_push) {
+        for (int j = 0; j < P; ++j) note_push(j);
+        if (!DRY) {
+            const int* ids = ctl_rep_ids() + r * static_cast<size_t>(B);
+            const float* X = d_pool_x;
+            const int* xidx = ids;
+            for (int l = 0; l < L; ++l) {
+                const LayerDev& ld = layers[static_cast<size_t>(l)];
+                const StageDev& s = stages[static_cast<size_t>(ld.stage)];
+                launch_layer(ld, s.slot(rel[static_cast<size_t>(ld.stage)]), X, xidx, d_replay + ld.act_off);
+                X = d_replay + ld.act_off;
+                xidx = nullptr;
+            }
+            launch_delta_head(d_replay, d_pool_lab, ids, 1.0f / static_cast<float>(B));
+            for (int l = L - 1; l >= 1; --l) {
+                const LayerDev& ld = layers[static_cast<size_t>(l)];
+                launch_layer_backward(l, stages[static_cast<size_t>(ld.stage)].slot(rel[static_cast<size_t>(ld.stage)]),
+                                      d_replay);
+            }
+            for (int j = 0; j < P; ++j) {
+                const long long cur = rel[static_cast<size_t>(j)];
+                fb200::UpdArgs a = update_args(j, cur, cur);
+                a.policy = FERRET_POLICY_NONE;
+                a.K = 1;
+                a.pend[0] = {d_replay, d_pool_x, 0};
+                a.x0idx = ids;
+                a.step = static_cast<float>(opt.lr);
+                fb200::launch_update(a, stream);
+                ++launches;
+            }
+        }
+        for (int j = 0; j < P; ++j) rel[static_cast<size_t>(j)] += 1;
+    }
+
+    // --------------------------------------------------------------- timing
     void time_begin() {
         if (!timing) return;
-        while (ev_pool.size() < ev_used + 2) {
-            cudaEvent_t e;
-            cuda_check(cudaEventCreate(&e), "cudaEventCreate");
-            ev_pool.push_back(e);
-        }
         cuda_check(cudaEventRecord(ev_pool[ev_used], stream), "cudaEventRecord");
     }
     void time_end(double alg_bytes) {
@@ -218,653 +1051,12 @@ struct ferret_trainer {
         return per * static_cast<double>(s.n_params) + side * static_cast<double>(reads.size());
     }
 
-    ~ferret_trainer() {
-        cudaSetDevice(opt.device);
-        if (stream) cudaStreamSynchronize(stream);
-        if (nstream) cudaStreamSynchronize(nstream);
-        for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
-        for (cudaEvent_t e : norm_events) cudaEventDestroy(e);
-        for (StageDev& s : stages) {
-            dfree(s.ring);
-            dfree(s.lam_d);
-            dfree(s.v_r);
-            dfree(s.v_a);
-            dfree(s.gap);
-            dfree(s.segs_dev);
-        }
-        dfree(d_raw);
-        dfree(d_x);
-        dfree(d_pred);
-        dfree(d_norm_mean);
-        dfree(d_norm_m2);
-        dfree(d_stash);
-        dfree(d_pred_buf);
-        dfree(d_replay);
-        dfree(d_partial);
-        dfree(d_counters);
-        if (stream) cudaStreamDestroy(stream);
-        if (nstream) cudaStreamDestroy(nstream);
-    }
-
-    // ------------------------------------------------------------------ setup
-    void build(const ferret_net_desc& net, const uint64_t* bounds, int32_t n_bounds) {
-        L = net.n_layers;
-        if (L <= 0) fail(FERRET_E_CONFIG, "net needs at least one layer");
-        if (n_bounds < 2 || bounds[0] != 0 || bounds[n_bounds - 1] != static_cast<uint64_t>(L))
-            fail(FERRET_E_CONFIG, "partition bounds must run from 0 to the layer count");
-        for (int32_t i = 1; i < n_bounds; ++i)
-            if (bounds[i] <= bounds[i - 1]) fail(FERRET_E_CONFIG, "partition bounds must be strictly increasing");
-        P = n_bounds - 1;
-        if (P > 16) fail(FERRET_E_CONFIG, "at most 16 stages per trainer");
-        B = opt.micro_batch;
-        if (B < 1 || B > fb200::kMaxBatch) fail(FERRET_E_CONFIG, "micro_batch must lie in [1, 16]");
-        if (opt.policy < 0 || opt.policy > 4) fail(FERRET_E_CONFIG, "unknown compensation policy");
-        if (opt.precision != FERRET_PREC_FP32) fail(FERRET_E_CONFIG, "only the fp32 parity precision is built");
-        layers.resize(static_cast<size_t>(L));
-        long long host_off = 0;
-        for (int l = 0; l < L; ++l) {
-            LayerDev& ld = layers[static_cast<size_t>(l)];
-            ld.in = static_cast<int>(net.in[l]);
-            ld.out = static_cast<int>(net.out[l]);
-            ld.act = net.act[l];
-            if (l > 0 && net.in[l] != net.out[l - 1])
-                fail(FERRET_E_CONFIG, "layer " + std::to_string(l) + ": input width mismatch");
-            ld.host_off = host_off;
-            host_off += static_cast<long long>(ld.in) * ld.out + ld.out;
-        }
-        F = layers.front().in;
-        n_out = layers.back().out;
-        init_params.assign(net.params, net.params + host_off);
-        // stash layout (per unit): activation + delta of every layer, B x out each
-        long long cursor = 0;
-        int max_width = F;
-        for (LayerDev& ld : layers) {
-            ld.act_off = align_up(cursor, 32);
-            cursor = ld.act_off + static_cast<long long>(B) * ld.out;
-            ld.dlt_off = align_up(cursor, 32);
-            cursor = ld.dlt_off + static_cast<long long>(B) * ld.out;
-            max_width = std::max(max_width, ld.out);
-        }
-        stash_stride = align_up(cursor, 64);
-        pred_stride = align_up(static_cast<long long>(B) * max_width, 64);
-        // stages
-        stages.resize(static_cast<size_t>(P));
-        hs.current.assign(static_cast<size_t>(P), 0);
-        size_t max_partial = 1, max_tiles = 1;
-        for (int j = 0; j < P; ++j) {
-            StageDev& s = stages[static_cast<size_t>(j)];
-            s.lo = static_cast<int>(bounds[j]);
-            s.hi = static_cast<int>(bounds[j + 1]);
-            if (s.hi - s.lo > fb200::kMaxStageLayers) fail(FERRET_E_CONFIG, "at most 16 layers per stage");
-            s.host_off = layers[static_cast<size_t>(s.lo)].host_off;
-            long long c = 0;
-            std::vector<fb200::UpdSeg> tab;
-            for (int l = s.lo; l < s.hi; ++l) {
-                LayerDev& ld = layers[static_cast<size_t>(l)];
-                ld.stage = j;
-                ld.woff = align_up(c, 32);
-                c = ld.woff + static_cast<long long>(ld.in) * ld.out;
-                ld.boff = align_up(c, 32);
-                c = ld.boff + ld.out;
-                s.n_params += static_cast<long long>(ld.in) * ld.out + ld.out;
-                // float4 items need 16-byte aligned weight rows and input rows
-                // (stash rows are B x in, x rows are B x F with F == in at layer 0)
-                const int vec = (ld.in % 4 == 0) ? 4 : 1;
-                fb200::UpdSeg w{};
-                w.layer = l - s.lo;
-                w.bias = 0;
-                w.vec = vec;
-                w.per_row = ld.in / vec;
-                w.item0 = s.n_items;
-                w.elem0 = ld.woff;
-                w.in = ld.in;
-                w.out = ld.out;
-                w.xin_off = l == 0 ? -1 : layers[static_cast<size_t>(l - 1)].act_off;
-                w.dlt_off = ld.dlt_off;
-                tab.push_back(w);
-                s.n_items += static_cast<long long>(ld.out) * w.per_row;
-                fb200::UpdSeg bs = w;
-                bs.bias = 1;
-                bs.vec = 1;
-                bs.per_row = 1;
-                bs.item0 = s.n_items;
-                bs.elem0 = ld.boff;
-                tab.push_back(bs);
-                s.n_items += ld.out;
-                s.total_rows += ld.out;
-                if (l > 0) {
-                    max_partial = std::max(max_partial, static_cast<size_t>(fb200::bwd_row_splits(ld.in, ld.out)) *
-                                                            static_cast<size_t>(B) * static_cast<size_t>(ld.in));
-                    max_tiles = std::max(max_tiles, static_cast<size_t>(fb200::bwd_col_tiles(ld.in)));
-                }
-            }
-            s.slot_floats = align_up(c, 64);
-            s.n_segs = static_cast<int>(tab.size());
-            s.segs_dev = dalloc<fb200::UpdSeg>(tab.size(), device_bytes);
-            cuda_check(cudaMemcpy(s.segs_dev, tab.data(), tab.size() * sizeof(fb200::UpdSeg), cudaMemcpyHostToDevice),
-                       "upload segment table");
-            const size_t n = static_cast<size_t>(s.slot_floats);
-            if (opt.policy == FERRET_POLICY_ITER_FISHER) {
-                s.lam_d = dalloc<float>(n, device_bytes);
-                cuda_check(cudaMemset(s.lam_d, 0, n * sizeof(float)), "memset");
-                if (opt.eta_lambda > 0.0) {
-                    s.v_r = dalloc<float>(n, device_bytes);
-                    s.v_a = dalloc<float>(n, device_bytes);
-                    cuda_check(cudaMemset(s.v_r, 0, n * sizeof(float)), "memset");
-                    cuda_check(cudaMemset(s.v_a, 0, n * sizeof(float)), "memset");
-                }
-            } else if (opt.policy == FERRET_POLICY_GAP) {
-                s.gap = dalloc<float>(n, device_bytes);
-                cuda_check(cudaMemset(s.gap, 0, n * sizeof(float)), "memset");
-            }
-            grow_ring(s, 2);
-        }
-        upload_initial_params();
-        d_pred_buf = dalloc<float>(static_cast<size_t>(2 * pred_stride), device_bytes);
-        d_replay = dalloc<float>(static_cast<size_t>(stash_stride), device_bytes);
-        d_partial = dalloc<float>(max_partial, device_bytes);
-        d_counters = dalloc<unsigned>(max_tiles, device_bytes);
-        cuda_check(cudaMemset(d_counters, 0, max_tiles * sizeof(unsigned)), "memset");
-        d_norm_mean = dalloc<double>(static_cast<size_t>(F), device_bytes);
-        d_norm_m2 = dalloc<double>(static_cast<size_t>(F), device_bytes);
-        cuda_check(cudaMemset(d_norm_mean, 0, static_cast<size_t>(F) * sizeof(double)), "memset");
-        cuda_check(cudaMemset(d_norm_m2, 0, static_cast<size_t>(F) * sizeof(double)), "memset");
-        hs.replay = ReplayIndex(opt.replay_capacity, opt.replay_seed);
-    }
-
-    void upload_initial_params() {
-        for (StageDev& s : stages) {
-            std::vector<float> slot(static_cast<size_t>(s.slot_floats), 0.f);
-            for (int l = s.lo; l < s.hi; ++l) {
-                const LayerDev& ld = layers[static_cast<size_t>(l)];
-                const double* src = init_params.data() + ld.host_off;
-                const long long nw = static_cast<long long>(ld.in) * ld.out;
-                for (long long i = 0; i < nw; ++i) slot[static_cast<size_t>(ld.woff + i)] = static_cast<float>(src[i]);
-                for (int r = 0; r < ld.out; ++r)
-                    slot[static_cast<size_t>(ld.boff + r)] = static_cast<float>(src[nw + r]);
-            }
-            cuda_check(cudaMemcpy(s.slot(0), slot.data(), slot.size() * sizeof(float), cudaMemcpyHostToDevice),
-                       "upload params");
-        }
-    }
-
-    // Grow a stage ring to `depth` slots, keeping the live version.
-    void grow_ring(StageDev& s, int depth) {
-        if (depth <= s.depth) return;
-        float* fresh = dalloc<float>(static_cast<size_t>(depth) * static_cast<size_t>(s.slot_floats), device_bytes);
-        if (s.ring) {
-            const long long v = hs.current[static_cast<size_t>(&s - stages.data())];
-            cuda_check(cudaStreamSynchronize(stream), "sync");
-            cuda_check(cudaMemcpy(fresh + (v % depth) * s.slot_floats, s.slot(v),
-                                  static_cast<size_t>(s.slot_floats) * sizeof(float), cudaMemcpyDeviceToDevice),
-                       "ring copy");
-            cudaFree(s.ring);
-            device_bytes -= static_cast<size_t>(s.depth) * static_cast<size_t>(s.slot_floats) * sizeof(float);
-        }
-        s.ring = fresh;
-        s.depth = depth;
-    }
-
-    void ensure_stash(int slots) {
-        if (slots <= stash_slots) return;
-        cuda_check(cudaStreamSynchronize(stream), "sync");
-        if (d_stash) {
-            cudaFree(d_stash);
-            device_bytes -= static_cast<size_t>(stash_slots) * static_cast<size_t>(stash_stride) * sizeof(float);
-        }
-        d_stash = dalloc<float>(static_cast<size_t>(slots) * static_cast<size_t>(stash_stride), device_bytes);
-        stash_slots = slots;
-    }
-
-    // ---------------------------------------------------------------- stream
-    void load_stream(const double* features, const uint64_t* lab, size_t n, size_t f) {
-        if (static_cast<int>(f) != F) fail(FERRET_E_INVALID_ARG, "stream feature width does not match the net input");
-        cuda_check(cudaStreamSynchronize(stream), "sync");
-        if (n > n_loaded) {
-            dfree(d_raw);
-            dfree(d_x);
-            dfree(d_pred);
-            d_raw = dalloc<double>(n * f, device_bytes);
-            d_x = dalloc<float>(n * f, device_bytes);
-            d_pred = dalloc<int>(n, device_bytes);
-        }
-        n_loaded = n;
-        labels.resize(n);
-        for (size_t i = 0; i < n; ++i) {
-            if (lab[i] >= static_cast<uint64_t>(n_out)) fail(FERRET_E_INVALID_ARG, "forward_backward: label out of range");
-            labels[i] = static_cast<int>(lab[i]);
-        }
-        cuda_check(cudaMemcpyAsync(d_raw, features, n * f * sizeof(double), cudaMemcpyHostToDevice, stream), "H2D stream");
-    }
-
-    void set_schedule(const ferret_event* ev, size_t n_ev, size_t chunk_items) {
-        Schedule s;
-        s.events.assign(ev, ev + n_ev);
-        // arrivals: units 0..n-1 in order (sim.hpp:171-173 pushes them by time)
-        long long expect = 0;
-        for (const ferret_event& e : s.events) {
-            if (e.kind == FERRET_EV_ARRIVAL) {
-                if (e.item != expect) fail(FERRET_E_INVALID_ARG, "event log: arrivals must cover items 0..n-1 in order");
-                ++expect;
-            }
-        }
-        s.n_units = static_cast<size_t>(expect);
-        s.chunk_items = chunk_items ? chunk_items : s.n_units * static_cast<size_t>(B);
-        if (s.n_units * static_cast<size_t>(B) > s.chunk_items)
-            fail(FERRET_E_INVALID_ARG, "event log covers more samples than one chunk");
-        s.dropped.assign(s.n_units, 0);
-        s.has_bwd.assign(s.n_units * static_cast<size_t>(P), 0);
-        s.last_use.assign(s.n_units, -1);
-        std::map<std::pair<int, int>, std::vector<long long>> open;  // (worker, stage) -> units awaiting update
-        for (size_t i = 0; i < s.events.size(); ++i) {
-            const ferret_event& e = s.events[i];
-            const bool staged = e.kind == FERRET_EV_FORWARD || e.kind == FERRET_EV_BACKWARD || e.kind == FERRET_EV_UPDATE;
-            if (staged && (e.stage < 0 || e.stage >= P))
-                fail(FERRET_E_INVALID_ARG, "event log: stage out of range for this partition");
-            if (e.kind != FERRET_EV_UPDATE && e.kind != FERRET_EV_ARRIVAL && e.kind != FERRET_EV_DROP &&
-                e.kind != FERRET_EV_FORWARD && e.kind != FERRET_EV_BACKWARD && e.kind != FERRET_EV_RECOMPUTE)
-                fail(FERRET_E_INVALID_ARG, "event log: unknown event kind");
-            if (e.kind != FERRET_EV_UPDATE && (e.item < 0 || static_cast<size_t>(e.item) >= s.n_units))
-                fail(FERRET_E_INVALID_ARG, "event log: item out of range");
-            const size_t u = static_cast<size_t>(e.item);
-            switch (e.kind) {
-                case FERRET_EV_DROP: s.dropped[u] = 1; break;
-                case FERRET_EV_ARRIVAL:
-                case FERRET_EV_FORWARD: s.last_use[u] = static_cast<long long>(i); break;
-                case FERRET_EV_BACKWARD:
-                    s.last_use[u] = static_cast<long long>(i);
-                    s.has_bwd[u * static_cast<size_t>(P) + static_cast<size_t>(e.stage)] = 1;
-                    open[{e.worker, e.stage}].push_back(static_cast<long long>(u));
-                    break;
-                case FERRET_EV_UPDATE: {
-                    auto it = open.find({e.worker, e.stage});
-                    if (it == open.end()) break;
-                    for (long long uu : it->second) s.last_use[static_cast<size_t>(uu)] = static_cast<long long>(i);
-                    it->second.clear();
-                    break;
-                }
-                default: break;
-            }
-        }
-        s.free_at.assign(s.events.size(), {});
-        for (size_t u = 0; u < s.n_units; ++u)
-            if (!s.dropped[u] && s.last_use[u] >= 0) s.free_at[static_cast<size_t>(s.last_use[u])].push_back(u);
-        sched = std::move(s);
-        have_schedule = true;
-    }
-
-    // -------------------------------------------------------------- execute
-    void execute(size_t chunk) {
-        if (!have_schedule) fail(FERRET_E_LOGIC, "execute: no schedule set");
-        const size_t base = chunk * sched.chunk_items;
-        const size_t n_samples = sched.n_units * static_cast<size_t>(B);
-        if (base + n_samples > n_loaded) fail(FERRET_E_OUT_OF_RANGE, "execute: chunk lies beyond the loaded stream");
-        launches = 0;
-        // 1. RunningNormalizer over every arrival of the chunk (observed in order,
-        //    dropped ones included: learner.hpp:393). It is model-independent,
-        //    so it runs ahead on a side stream in groups of kNormGroup units;
-        //    the training stream waits on a group's event at the group's first
-        //    arrival. Sequential fp64 per feature (bit-exact), hidden behind the
-        //    training kernels except for the first group.
-        const size_t groups = (sched.n_units + kNormGroup - 1) / kNormGroup;
-        while (norm_events.size() < groups) {
-            cudaEvent_t e;
-            cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
-            norm_events.push_back(e);
-        }
-        {
-            cudaEvent_t ready = norm_events[0];
-            cuda_check(cudaEventRecord(ready, stream), "cudaEventRecord");  // stream data (H2D) is in
-            cuda_check(cudaStreamWaitEvent(nstream, ready, 0), "cudaStreamWaitEvent");
-        }
-        for (size_t g = 0; g < groups; ++g) {
-            const size_t u0 = g * kNormGroup, u1 = std::min(sched.n_units, u0 + kNormGroup);
-            const size_t s0 = base + u0 * static_cast<size_t>(B);
-            const size_t ns = (u1 - u0) * static_cast<size_t>(B);
-            fb200::NormArgs na{d_raw + s0 * static_cast<size_t>(F), static_cast<long long>(ns), F,
-                               static_cast<unsigned long long>(hs.norm_count), d_norm_mean, d_norm_m2,
-                               d_x + s0 * static_cast<size_t>(F)};
-            fb200::launch_normalize(na, nstream);
-            cuda_check(cudaEventRecord(norm_events[g], nstream), "cudaEventRecord");
-            ++launches;
-            hs.norm_count += ns;
-        }
-        // 2. dry run -> sizes
-        HostState probe = hs;
-        const PassResult need = run_pass<true>(probe, base);
-        for (int j = 0; j < P; ++j) grow_ring(stages[static_cast<size_t>(j)], need.need_depth[static_cast<size_t>(j)]);
-        ensure_stash(std::max(need.need_slots, 1));
-        // 3. real pass
-        run_pass<false>(hs, base);
-        cuda_check(cudaGetLastError(), "kernel launch");
-        stats.kernel_launches = launches;
-        stats.stash_slots = stash_slots;
-        for (int j = 0; j < P && j < 16; ++j) stats.ring_depth[j] = stages[static_cast<size_t>(j)].depth;
-    }
-
-    template <bool DRY>
-    PassResult run_pass(HostState& st, size_t base) {
-        PassResult res;
-        res.need_depth.assign(static_cast<size_t>(P), 2);
-        const bool as_shipped = opt.as_shipped != 0;
-        const size_t n_units = sched.n_units;
-        std::vector<int> slot_of(n_units, -1);
-        std::vector<int> free_slots;
-        int slots_used = 0;
-        std::vector<char> inflight(n_units, 0);
-        std::vector<long long> read_ver(n_units * static_cast<size_t>(P), -1);
-        std::vector<std::map<long long, int>> live(static_cast<size_t>(P));  // live read versions per stage
-        struct Pend {
-            size_t u;
-            long long read;
-        };
-        std::map<std::pair<int, int>, std::vector<Pend>> pending;
-        uint64_t n_upd = 0, n_rep = 0, n_pred = 0;
-        std::vector<double> tau_sum(static_cast<size_t>(P), 0.0);
-        std::vector<uint64_t> tau_cnt(static_cast<size_t>(P), 0);
-
-        auto floor_of = [&](int j) {
-            const long long cur = st.current[static_cast<size_t>(j)];
-            const auto& m = live[static_cast<size_t>(j)];
-            return m.empty() ? cur : std::min(m.begin()->first, cur);
-        };
-        auto note_push = [&](int j) {  // a new version of stage j is about to be written
-            const long long span = st.current[static_cast<size_t>(j)] - floor_of(j) + 2;
-            int& d = res.need_depth[static_cast<size_t>(j)];
-            d = std::max(d, static_cast<int>(span));
-            if (!DRY && span > stages[static_cast<size_t>(j)].depth)
-                fail(FERRET_E_LOGIC, "version ring undersized (dry run disagrees with the real pass)");
-        };
-        auto stash = [&](size_t u) { return d_stash + static_cast<long long>(slot_of[u]) * stash_stride; };
-        auto xrows = [&](size_t u) { return d_x + (base + u * static_cast<size_t>(B)) * static_cast<size_t>(F); };
-
-        for (size_t idx = 0; idx < sched.events.size(); ++idx) {
-            const ferret_event& e = sched.events[idx];
-            const size_t u = static_cast<size_t>(e.item);
-            const int j = e.stage;
-            switch (e.kind) {
-                case FERRET_EV_ARRIVAL: {  // learner.hpp:389-410
-                    if (!DRY && u % kNormGroup == 0)
-                        cuda_check(cudaStreamWaitEvent(stream, norm_events[u / kNormGroup], 0), "cudaStreamWaitEvent");
-                    if (sched.dropped[u]) break;
-                    inflight[u] = 1;
-                    if (!as_shipped) {
-                        if (free_slots.empty()) free_slots.push_back(slots_used++);
-                        slot_of[u] = free_slots.back();
-                        free_slots.pop_back();
-                    }
-                    ++n_pred;
-                    if (!DRY) launch_predict(u, base, st);
-                    if (opt.replay)
-                        for (int b = 0; b < B; ++b)
-                            st.replay.add(static_cast<long long>(base + u * static_cast<size_t>(B) + static_cast<size_t>(b)));
-                    break;
-                }
-                case FERRET_EV_FORWARD: {  // learner.hpp:412-433
-                    if (as_shipped || !inflight[u]) break;
-                    const long long v = st.current[static_cast<size_t>(j)];
-                    read_ver[u * static_cast<size_t>(P) + static_cast<size_t>(j)] = v;
-                    if (sched.has_bwd[u * static_cast<size_t>(P) + static_cast<size_t>(j)]) live[static_cast<size_t>(j)][v] += 1;
-                    if (!DRY) launch_stage_forward(j, stages[static_cast<size_t>(j)].slot(v), stash(u), xrows(u));
-                    break;
-                }
-                case FERRET_EV_BACKWARD: {  // learner.hpp:435-479
-                    if (as_shipped || !inflight[u]) break;
-                    const long long r = read_ver[u * static_cast<size_t>(P) + static_cast<size_t>(j)];
-                    if (r < 0) fail(FERRET_E_OUT_OF_RANGE, "stage version evicted");
-                    if (!DRY) {
-                        int lab[fb200::kMaxBatch];
-                        for (int b = 0; b < B; ++b) lab[b] = labels[base + u * static_cast<size_t>(B) + static_cast<size_t>(b)];
-                        launch_stage_backward(j, stages[static_cast<size_t>(j)].slot(r), stash(u), lab);
-                    }
-                    pending[{e.worker, j}].push_back({u, r});
-                    break;
-                }
-                case FERRET_EV_UPDATE: {  // learner.hpp:491-510
-                    if (as_shipped) break;
-                    auto it = pending.find({e.worker, j});
-                    if (it == pending.end() || it->second.empty()) break;
-                    const std::vector<Pend>& pl = it->second;
-                    if (pl.size() > static_cast<size_t>(fb200::kMaxPending))
-                        fail(FERRET_E_CONFIG, "accumulation count above 16 is not supported by the update kernel");
-                    note_push(j);
-                    const long long cur = st.current[static_cast<size_t>(j)];
-                    for (const Pend& p : pl) {
-                        tau_sum[static_cast<size_t>(j)] += static_cast<double>(cur - p.read);
-                        tau_cnt[static_cast<size_t>(j)] += 1;
-                    }
-                    if (!DRY) {
-                        long long oldest = cur;
-                        for (const Pend& p : pl) oldest = std::min(oldest, p.read);
-                        fb200::UpdArgs a = update_args(j, cur, oldest);
-                        a.policy = opt.policy;
-                        a.K = static_cast<int>(pl.size());
-                        for (size_t k = 0; k < pl.size(); ++k)
-                            a.pend[k] = {stash(pl[k].u), xrows(pl[k].u), static_cast<int>(pl[k].read - oldest)};
-                        a.step = static_cast<float>(opt.lr * (1.0 / static_cast<double>(pl.size())));
-                        std::vector<long long> reads;
-                        for (const Pend& p : pl) reads.push_back(p.read);
-                        time_begin();
-                        fb200::launch_update(a, stream);
-                        time_end(update_bytes(j, opt.policy, reads, cur));
-                        ++launches;
-                    }
-                    st.current[static_cast<size_t>(j)] += 1;
-                    ++n_upd;
-                    for (const Pend& p : pl) {
-                        auto& m = live[static_cast<size_t>(j)];
-                        auto lv = m.find(p.read);
-                        if (lv != m.end() && --lv->second == 0) m.erase(lv);
-                    }
-                    it->second.clear();
-                    if (j == 0 && opt.replay && !st.replay.empty()) {  // learner.hpp:509, 513-519
-                        ++n_rep;
-                        replay_step<DRY>(st, note_push);
-                    }
-                    break;
-                }
-                default: break;  // drop, recompute: no trainer work (learner.hpp:359)
-            }
-            if (!as_shipped)
-                for (size_t fu : sched.free_at[idx])
-                    if (slot_of[fu] >= 0) {
-                        free_slots.push_back(slot_of[fu]);
-                        slot_of[fu] = -1;
-                    }
-        }
-        res.need_slots = slots_used;
-        if (!DRY) {
-            stats.events = sched.events.size();
-            stats.updates = n_upd;
-            stats.replays = n_rep;
-            stats.predicts = n_pred;
-            for (int j = 0; j < P && j < 16; ++j) {
-                stats.mean_tau[j] = tau_cnt[static_cast<size_t>(j)] ? tau_sum[static_cast<size_t>(j)] /
-                                                                         static_cast<double>(tau_cnt[static_cast<size_t>(j)])
-                                                                   : 0.0;
-                stats.update_elems[j] = static_cast<uint64_t>(stages[static_cast<size_t>(j)].n_params) * tau_cnt[static_cast<size_t>(j)];
-            }
-        }
-        return res;
-    }
-
-    // Launch arguments of one update of stage j: the chain table holds the
-    // versions oldest_read .. cur (ring slots resolved here), dst = slot(cur+1).
-    fb200::UpdArgs update_args(int j, long long cur, long long oldest) {
-        const StageDev& s = stages[static_cast<size_t>(j)];
-        fb200::UpdArgs a{};
-        a.n_segs = s.n_segs;
-        a.n_items = s.n_items;
-        a.B = B;
-        a.segs = s.segs_dev;
-        a.x0_gather = 0;
-        a.x0_ld = F;
-        if (cur - oldest + 1 > fb200::kMaxChain)
-            fail(FERRET_E_CONFIG, "staleness chain longer than 48 versions is not supported by the update kernel");
-        a.nv = static_cast<int>(cur - oldest + 1);
-        for (long long v = oldest; v <= cur; ++v) a.vers[v - oldest] = s.slot(v);
-        a.dst = s.slot(cur + 1);
-        a.lam_d = s.lam_d;
-        a.v_r = s.v_r;
-        a.v_a = s.v_a;
-        a.gap = s.gap;
-        a.lambda0 = static_cast<float>(opt.lambda0);
-        a.alpha = static_cast<float>(opt.alpha);
-        a.eta = static_cast<float>(opt.eta_lambda);
-        a.nu = static_cast<float>(opt.nu);
-        return a;
-    }
-
-    // One dense layer on B samples whose input row b is X + xoff[b].
-    void launch_layer(const LayerDev& ld, const float* stage_slot, const float* X, const long long* xoff, float* Y) {
-        fb200::FwdArgs a{};
-        a.W = stage_slot + ld.woff;
-        a.bias = stage_slot + ld.boff;
-        a.X = X;
-        for (int b = 0; b < B; ++b) a.xoff[b] = xoff[b];
-        a.Y = Y;
-        a.in = ld.in;
-        a.out = ld.out;
-        a.B = B;
-        a.relu = ld.act == FERRET_ACT_RELU;
-        fb200::launch_fwd(a, stream);
-        ++launches;
-    }
-
-    void contiguous_rows(long long* xoff, int width) const {
-        for (int b = 0; b < B; ++b) xoff[b] = static_cast<long long>(b) * width;
-    }
-
-    // predict_class(net_, x) at the arrival (learner.hpp:398-399): full net, live versions.
-    void launch_predict(size_t u, size_t base, const HostState& st) {
-        long long xoff[fb200::kMaxBatch];
-        const float* X = d_x + (base + u * static_cast<size_t>(B)) * static_cast<size_t>(F);
-        contiguous_rows(xoff, F);
-        for (int l = 0; l < L; ++l) {
-            const LayerDev& ld = layers[static_cast<size_t>(l)];
-            const StageDev& s = stages[static_cast<size_t>(ld.stage)];
-            float* Y = d_pred_buf + (l & 1) * pred_stride;
-            launch_layer(ld, s.slot(st.current[static_cast<size_t>(ld.stage)]), X, xoff, Y);
-            X = Y;
-            contiguous_rows(xoff, ld.out);
-        }
-        fb200::HeadArgs h{};
-        h.logits = X;
-        h.n_out = n_out;
-        h.B = B;
-        h.mode = 0;
-        h.pred = d_pred + base + u * static_cast<size_t>(B);
-        fb200::launch_head(h, stream);
-        ++launches;
-    }
-
-    void launch_stage_forward(int j, const float* slot, float* stash_u, const float* x0) {
-        const StageDev& s = stages[static_cast<size_t>(j)];
-        long long xoff[fb200::kMaxBatch];
-        for (int l = s.lo; l < s.hi; ++l) {
-            const LayerDev& ld = layers[static_cast<size_t>(l)];
-            const float* X = l == 0 ? x0 : stash_u + layers[static_cast<size_t>(l - 1)].act_off;
-            contiguous_rows(xoff, ld.in);
-            launch_layer(ld, slot, X, xoff, stash_u + ld.act_off);
-        }
-    }
-
-    // delta at the logits (last stage) then per layer prev = W^T delta with the
-    // ReLU mask of the layer below applied on write (learner.hpp:443-476).
-    void launch_stage_backward(int j, const float* slot, float* stash_u, const int* lab) {
-        const StageDev& s = stages[static_cast<size_t>(j)];
-        if (j == P - 1) launch_delta_head(stash_u, lab, 1.0f / static_cast<float>(B));
-        for (int l = s.hi - 1; l >= s.lo; --l) {
-            if (l == 0) break;  // no input gradient for the first layer
-            launch_layer_backward(l, slot, stash_u);
-        }
-    }
-
-    void launch_delta_head(float* stash_u, const int* lab, float scale) {
-        const LayerDev& last = layers.back();
-        fb200::HeadArgs h{};
-        h.logits = stash_u + last.act_off;
-        h.n_out = n_out;
-        h.B = B;
-        h.mode = 1;
-        for (int b = 0; b < B; ++b) h.labels[b] = lab[b];
-        h.delta = stash_u + last.dlt_off;
-        h.scale = scale;
-        fb200::launch_head(h, stream);
-        ++launches;
-    }
-
-    void launch_layer_backward(int l, const float* slot, float* stash_u) {
-        const LayerDev& ld = layers[static_cast<size_t>(l)];
-        const LayerDev& below = layers[static_cast<size_t>(l - 1)];
-        fb200::BwdArgs a{};
-        a.W = slot + ld.woff;
-        a.d_out = stash_u + ld.dlt_off;
-        a.mask = below.act == FERRET_ACT_RELU ? stash_u + below.act_off : nullptr;
-        a.d_in = stash_u + below.dlt_off;
-        a.in = ld.in;
-        a.out = ld.out;
-        a.B = B;
-        a.row_splits = fb200::bwd_row_splits(ld.in, ld.out);
-        a.partial = d_partial;
-        a.counters = d_counters;
-        fb200::launch_bwd(a, stream);
-        ++launches;
-    }
-
-    // replay_step (learner.hpp:513-519): forward_backward(net_, {buffer.sample()})
-    // with mean reduction (net.hpp:157-200), apply_sgd on every stage, push a
-    // version per stage. B samples per replay step at micro-batch B.
-    template <bool DRY, class NotePush>
-    void replay_step(HostState& st, NotePush& note_push) {
-        long long ids[fb200::kMaxBatch];
-        for (int b = 0; b < B; ++b) ids[b] = st.replay.sample();
-        for (int j = 0; j < P; ++j) note_push(j);
-        if (!DRY) {
-            long long xoff[fb200::kMaxBatch];
-            int lab[fb200::kMaxBatch];
-            for (int b = 0; b < B; ++b) {
-                xoff[b] = ids[b] * F;
-                lab[b] = labels[static_cast<size_t>(ids[b])];
-            }
-            // forward through the live net
-            const float* X = d_x;
-            const long long* xo = xoff;
-            long long cont[fb200::kMaxBatch];
-            for (int l = 0; l < L; ++l) {
-                const LayerDev& ld = layers[static_cast<size_t>(l)];
-                const StageDev& s = stages[static_cast<size_t>(ld.stage)];
-                launch_layer(ld, s.slot(st.current[static_cast<size_t>(ld.stage)]), X, xo, d_replay + ld.act_off);
-                X = d_replay + ld.act_off;
-                contiguous_rows(cont, ld.out);
-                xo = cont;
-            }
-            launch_delta_head(d_replay, lab, 1.0f / static_cast<float>(B));
-            for (int l = L - 1; l >= 1; --l) {
-                const LayerDev& ld = layers[static_cast<size_t>(l)];
-                launch_layer_backward(l, stages[static_cast<size_t>(ld.stage)].slot(st.current[static_cast<size_t>(ld.stage)]),
-                                      d_replay);
-            }
-            for (int j = 0; j < P; ++j) {
-                const long long cur = st.current[static_cast<size_t>(j)];
-                fb200::UpdArgs a = update_args(j, cur, cur);
-                a.policy = FERRET_POLICY_NONE;
-                a.K = 1;
-                a.pend[0] = {d_replay, d_x, 0};
-                a.x0_gather = 1;
-                for (int b = 0; b < B; ++b) a.x0off[b] = xoff[b];
-                a.step = static_cast<float>(opt.lr);
-                fb200::launch_update(a, stream);
-                ++launches;
-            }
-        }
-        for (int j = 0; j < P; ++j) st.current[static_cast<size_t>(j)] += 1;
-    }
-
     // ------------------------------------------------------------------ output
     void fetch_log(size_t chunk, ferret_step_record* out) {
+        if (!have_schedule) fail(FERRET_E_LOGIC, "fetch_log: no schedule set");
         const size_t base = chunk * sched.chunk_items;
         const size_t n_samples = sched.n_units * static_cast<size_t>(B);
+        if (base + n_samples > n_loaded) fail(FERRET_E_OUT_OF_RANGE, "fetch_log: chunk lies beyond the loaded stream");
         std::vector<int> pred(n_samples);
         cuda_check(cudaMemcpyAsync(pred.data(), d_pred + base, n_samples * sizeof(int), cudaMemcpyDeviceToHost, stream),
                    "D2H predictions");
@@ -894,8 +1086,7 @@ struct ferret_trainer {
         for (int j = 0; j < P; ++j) {
             const StageDev& s = stages[static_cast<size_t>(j)];
             std::vector<float> slot(static_cast<size_t>(s.slot_floats));
-            cuda_check(cudaMemcpy(slot.data(), s.slot(hs.current[static_cast<size_t>(j)]), slot.size() * sizeof(float),
-                                  cudaMemcpyDeviceToHost),
+            cuda_check(cudaMemcpy(slot.data(), s.slot(0), slot.size() * sizeof(float), cudaMemcpyDeviceToHost),
                        "D2H params");
             unpack_stage(s, slot, out, 0.0);
         }
@@ -915,11 +1106,11 @@ struct ferret_trainer {
     void read_state(int j, const float* dev, double* out, size_t n, double offset) {
         const StageDev& s = stages[static_cast<size_t>(j)];
         if (n != static_cast<size_t>(s.n_params)) fail(FERRET_E_INVALID_ARG, "comp_state: size mismatch");
-        std::vector<double> full(init_params.size());
         if (!dev) {
             for (long long i = 0; i < s.n_params; ++i) out[i] = offset;
             return;
         }
+        std::vector<double> full(init_params.size());
         std::vector<float> slot(static_cast<size_t>(s.slot_floats));
         cuda_check(cudaMemcpy(slot.data(), dev, slot.size() * sizeof(float), cudaMemcpyDeviceToHost), "D2H state");
         unpack_stage(s, slot, full.data(), offset);
@@ -975,7 +1166,10 @@ ferret_status ferret_trainer_load_stream(ferret_trainer* t, const double* featur
 
 ferret_status ferret_trainer_set_schedule(ferret_trainer* t, const ferret_event* events, size_t n_events,
                                           size_t n_chunk_items) {
-    return guarded([&] { t->set_schedule(events, n_events, n_chunk_items); });
+    return guarded([&] {
+        cuda_check(cudaSetDevice(t->opt.device), "cudaSetDevice");
+        t->set_schedule(events, n_events, n_chunk_items);
+    });
 }
 
 ferret_status ferret_trainer_execute(ferret_trainer* t, size_t chunk) {
@@ -1058,9 +1252,6 @@ ferret_status ferret_trainer_set_timing(ferret_trainer* t, int32_t enable) {
     return guarded([&] {
         cuda_check(cudaStreamSynchronize(t->stream), "sync");
         t->timing = enable != 0;
-        t->ev_used = 0;
-        t->upd_alg_bytes = 0.0;
-        t->upd_timed = 0;
     });
 }
 
@@ -1068,17 +1259,15 @@ ferret_status ferret_trainer_update_timing(ferret_trainer* t, double* total_ms, 
     return guarded([&] {
         cuda_check(cudaStreamSynchronize(t->stream), "sync");
         double ms = 0.0;
-        for (size_t i = 0; i + 1 < t->ev_used; i += 2) {
-            float part = 0.f;
-            cuda_check(cudaEventElapsedTime(&part, t->ev_pool[i], t->ev_pool[i + 1]), "cudaEventElapsedTime");
-            ms += part;
-        }
+        if (t->graph_timing)
+            for (size_t i = 0; i + 1 < t->ev_used; i += 2) {
+                float part = 0.f;
+                cuda_check(cudaEventElapsedTime(&part, t->ev_pool[i], t->ev_pool[i + 1]), "cudaEventElapsedTime");
+                ms += part;
+            }
         *total_ms = ms;
-        *launches = t->upd_timed;
-        *alg_bytes = t->upd_alg_bytes;
-        t->ev_used = 0;
-        t->upd_alg_bytes = 0.0;
-        t->upd_timed = 0;
+        *launches = t->graph_timing ? t->upd_timed : 0;
+        *alg_bytes = t->graph_timing ? t->upd_alg_bytes : 0.0;
     });
 }
 
@@ -1095,6 +1284,12 @@ ferret_status ferret_compensate(int32_t policy, const double* g, const double* c
         size_t bytes = 0;
         const size_t nn = n ? n : 1;
         std::vector<float*> bufs;
+        struct Cleanup {
+            std::vector<float*>& b;
+            ~Cleanup() {
+                for (float* p : b) cudaFree(p);
+            }
+        } cleanup{bufs};
         auto up = [&](const double* src) {
             float* d = dalloc<float>(nn, bytes);
             bufs.push_back(d);
@@ -1109,12 +1304,6 @@ ferret_status ferret_compensate(int32_t policy, const double* g, const double* c
             cuda_check(cudaMemcpy(h.data(), d, n * sizeof(float), cudaMemcpyDeviceToHost), "D2H");
             for (size_t i = 0; i < n; ++i) dst[i] = h[i];
         };
-        struct Cleanup {
-            std::vector<float*>& b;
-            ~Cleanup() {
-                for (float* p : b) cudaFree(p);
-            }
-        } cleanup{bufs};
         fb200::CompArgs a{};
         a.policy = policy;
         a.g = up(g);
