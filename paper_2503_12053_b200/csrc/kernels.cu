@@ -218,11 +218,36 @@ __global__ void __launch_bounds__(kThreads) bwd_kernel(const BwdArgs a) {
 #pragma unroll
         for (int v = 0; v < V; ++v) acc[b][v] = 0.f;
     if (c0 < a.in) {
-        for (int r = rs + warp; r < re; r += kWarps) {
+        // RU rows per trip with independent loads in flight (the rows are
+        // L2/HBM latency-bound, not bandwidth-bound, at these sizes)
+        constexpr int RU = 4;
+        int r = rs + warp;
+        for (; r + (RU - 1) * kWarps < re; r += RU * kWarps) {
+            float w[RU][V];
+#pragma unroll
+            for (int q = 0; q < RU; ++q) {
+                const float* wp = a.W + (size_t)(r + q * kWarps) * a.in + c0;
+                if (V == 4) {
+                    const float4 w4 = __ldg(reinterpret_cast<const float4*>(wp));
+                    w[q][0] = w4.x; w[q][1 % V] = w4.y; w[q][2 % V] = w4.z; w[q][3 % V] = w4.w;
+                } else {
+                    w[q][0] = __ldg(wp);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < RU; ++q)
+#pragma unroll
+                for (int b = 0; b < BT; ++b) {
+                    const float d = sd[b][r + q * kWarps - rs];
+#pragma unroll
+                    for (int v = 0; v < V; ++v) acc[b][v] = fmaf(w[q][v], d, acc[b][v]);
+                }
+        }
+        for (; r < re; r += kWarps) {
             float w[V];
             if (V == 4) {
                 const float4 w4 = __ldg(reinterpret_cast<const float4*>(a.W + (size_t)r * a.in + c0));
-                w[0] = w4.x; w[1] = w4.y; w[2 % V] = w4.z; w[3 % V] = w4.w;
+                w[0] = w4.x; w[1 % V] = w4.y; w[2 % V] = w4.z; w[3 % V] = w4.w;
             } else {
                 w[0] = __ldg(a.W + (size_t)r * a.in + c0);
             }
@@ -344,7 +369,46 @@ __device__ __forceinline__ float compensate_elem(float g, const float* const* ve
 // fused update: one thread per work item (V consecutive parameters of one
 // weight row, or one bias), grid-stride over the stage's segments.
 // ---------------------------------------------------------------------------
-template <int POLICY, int V>
+constexpr int kRegChain = 12;  // chain versions the iter_fisher fold keeps in registers
+
+// iter_fisher (compensate.hpp:82-104) for one element with the chain values
+// already in registers: cv[i] = version i (i < last), th = version `last`.
+// Loops are fully unrolled and predicated so every cv[] index is static.
+template <int V>
+__device__ __forceinline__ float fold_iter_cached(float g, const float (&cv)[kRegChain + 1][V], int v, int first,
+                                                  int last, float th, ElemState& st, float lam_base, float alpha,
+                                                  float eta, float nu, bool learn) {
+    float lam = lam_base + st.ld;
+    if (learn && last - first >= 1) {
+        float v0 = 0.f, v1 = 0.f;
+#pragma unroll
+        for (int i = 0; i < kRegChain; ++i)
+            if (i == first) {
+                v0 = cv[i][v];
+                v1 = (i + 1 < last) ? cv[i + 1][v] : th;
+            }
+        const float one_m_a = 1.f - alpha;
+        const float dv = one_m_a * (g - st.vr);
+        const float resid = dv - lam * st.va;
+        const float grad_l = -2.f * resid * st.va + 2.f * nu * lam;
+        st.ld -= eta * grad_l;
+        lam = lam_base + st.ld;
+        st.vr = alpha * st.vr + one_m_a * g;
+        st.va = alpha * st.va + one_m_a * g * g * (v1 - v0);
+    }
+    float o = g;
+#pragma unroll
+    for (int i = 0; i < kRegChain; ++i)
+        if (i >= first && i < last) {
+            const float nxt = (i + 1 < last) ? cv[i + 1][v] : th;
+            o += lam * o * o * (nxt - cv[i][v]);
+        }
+    return o;
+}
+
+// One work item: V consecutive parameters of a weight row (or one bias) of a
+// stage, all K pending gradients folded in order (BT >= B, loads unrolled).
+template <int POLICY, int V, int BT>
 __device__ __forceinline__ void update_item(const UpdArgs& a, const UpdSeg& sg, long long q) {
     const int K = a.K, B = a.B;
     const bool learn = a.eta > 0.f && a.v_r != nullptr;
@@ -381,6 +445,27 @@ __device__ __forceinline__ void update_item(const UpdArgs& a, const UpdSeg& sg, 
     if (POLICY == 2)
 #pragma unroll
         for (int v = 0; v < V; ++v) gp[v] = a.gap[e0 + v];
+    // iter_fisher: every older chain version this element needs, loaded at once
+    const bool cached = POLICY == 4 && last <= kRegChain;
+    float cv[kRegChain + 1][V];
+    if (POLICY == 4 && cached) {
+#pragma unroll
+        for (int i = 0; i < kRegChain; ++i) {
+            if (i < last) {
+                if (V == 4) {
+                    const float4 c4 = __ldg(reinterpret_cast<const float4*>(a.vers[i] + e0));
+                    cv[i][0] = c4.x; cv[i][1 % V] = c4.y; cv[i][2 % V] = c4.z; cv[i][3 % V] = c4.w;
+                } else {
+                    cv[i][0] = __ldg(a.vers[i] + e0);
+                }
+            } else {
+#pragma unroll
+                for (int v = 0; v < V; ++v) cv[i][v] = 0.f;
+            }
+        }
+#pragma unroll
+        for (int v = 0; v < V; ++v) cv[kRegChain][v] = 0.f;
+    }
     float mean[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) mean[v] = 0.f;
@@ -390,7 +475,9 @@ __device__ __forceinline__ void update_item(const UpdArgs& a, const UpdSeg& sg, 
         float g[V];
 #pragma unroll
         for (int v = 0; v < V; ++v) g[v] = 0.f;
-        for (int b = 0; b < B; ++b) {
+#pragma unroll
+        for (int b = 0; b < BT; ++b) {
+            if (b >= B) break;
             const float d = __ldg(dl + (size_t)b * sg.out);
             if (sg.bias) {
                 g[0] += d;
@@ -412,8 +499,12 @@ __device__ __forceinline__ void update_item(const UpdArgs& a, const UpdSeg& sg, 
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             ElemState st{ld[v], vr[v], va[v], gp[v]};
-            mean[v] += compensate_elem<POLICY>(g[v], a.vers, pk.first, last, e0 + v, th[v], st, a.lambda0, a.alpha,
-                                               a.eta, a.nu, learn);
+            if (POLICY == 4 && cached)
+                mean[v] += fold_iter_cached<V>(g[v], cv, v, pk.first, last, th[v], st, a.lambda0, a.alpha, a.eta,
+                                               a.nu, learn);
+            else
+                mean[v] += compensate_elem<POLICY>(g[v], a.vers, pk.first, last, e0 + v, th[v], st, a.lambda0,
+                                                   a.alpha, a.eta, a.nu, learn);
             ld[v] = st.ld;
             vr[v] = st.vr;
             va[v] = st.va;
@@ -443,16 +534,25 @@ __device__ __forceinline__ void update_item(const UpdArgs& a, const UpdSeg& sg, 
         for (int v = 0; v < V; ++v) a.gap[e0 + v] = gp[v];
 }
 
-template <int POLICY>
-__global__ void __launch_bounds__(kThreads, 3) update_kernel(const UpdArgs a) {
+template <int POLICY, int BT>
+__global__ void __launch_bounds__(kThreads, 2) update_kernel(const UpdArgs a) {
     const long long stride = (long long)gridDim.x * kThreads;
     for (long long q = (long long)blockIdx.x * kThreads + threadIdx.x; q < a.n_items; q += stride) {
         int s = 0;
         while (s + 1 < a.n_segs && q >= a.segs[s + 1].item0) ++s;
         const UpdSeg sg = a.segs[s];
-        if (sg.vec == 4) update_item<POLICY, 4>(a, sg, q - sg.item0);
-        else update_item<POLICY, 1>(a, sg, q - sg.item0);
+        if (sg.vec == 4) update_item<POLICY, 4, BT>(a, sg, q - sg.item0);
+        else update_item<POLICY, 1, BT>(a, sg, q - sg.item0);
     }
+}
+
+template <int POLICY>
+void update_dispatch(const UpdArgs& a, int grid, cudaStream_t s) {
+    if (a.B <= 1) update_kernel<POLICY, 1><<<grid, kThreads, 0, s>>>(a);
+    else if (a.B <= 2) update_kernel<POLICY, 2><<<grid, kThreads, 0, s>>>(a);
+    else if (a.B <= 4) update_kernel<POLICY, 4><<<grid, kThreads, 0, s>>>(a);
+    else if (a.B <= 8) update_kernel<POLICY, 8><<<grid, kThreads, 0, s>>>(a);
+    else update_kernel<POLICY, 16><<<grid, kThreads, 0, s>>>(a);
 }
 
 // ---------------------------------------------------------------------------
@@ -542,7 +642,7 @@ int bwd_col_tiles(int in) {
 int bwd_row_splits(int in, int out) {
     const int tiles = bwd_col_tiles(in);
     int splits = (2 * 148 + tiles - 1) / tiles;
-    const int max_by_rows = (out + 63) / 64;  // >= 8 rows per warp
+    const int max_by_rows = (out + 31) / 32;  // >= 4 rows per warp (one unrolled trip)
     if (splits > max_by_rows) splits = max_by_rows;
     const int min_for_smem = (out + kBwdMaxRows - 1) / kBwdMaxRows;
     if (splits < min_for_smem) splits = min_for_smem;
@@ -570,11 +670,11 @@ void launch_update(const UpdArgs& a, cudaStream_t s) {
     if (blocks < 1) blocks = 1;
     const int grid = (int)blocks;
     switch (a.policy) {
-        case 0: update_kernel<0><<<grid, kThreads, 0, s>>>(a); break;
-        case 1: update_kernel<1><<<grid, kThreads, 0, s>>>(a); break;
-        case 2: update_kernel<2><<<grid, kThreads, 0, s>>>(a); break;
-        case 3: update_kernel<3><<<grid, kThreads, 0, s>>>(a); break;
-        default: update_kernel<4><<<grid, kThreads, 0, s>>>(a); break;
+        case 0: update_dispatch<0>(a, grid, s); break;
+        case 1: update_dispatch<1>(a, grid, s); break;
+        case 2: update_dispatch<2>(a, grid, s); break;
+        case 3: update_dispatch<3>(a, grid, s); break;
+        default: update_dispatch<4>(a, grid, s); break;
     }
 }
 

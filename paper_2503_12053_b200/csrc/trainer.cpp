@@ -1013,11 +1013,13 @@ struct ferret_trainer {
     // --------------------------------------------------------------- timing
     void time_begin() {
         if (!timing) return;
-        cuda_check(cudaEventRecord(ev_pool[ev_used], stream), "cudaEventRecord");
+        // External: an event record node that fires when the graph runs (a plain
+        // record under capture is only a dependency marker)
+        cuda_check(cudaEventRecordWithFlags(ev_pool[ev_used], stream, cudaEventRecordExternal), "cudaEventRecord");
     }
     void time_end(double alg_bytes) {
         if (!timing) return;
-        cuda_check(cudaEventRecord(ev_pool[ev_used + 1], stream), "cudaEventRecord");
+        cuda_check(cudaEventRecordWithFlags(ev_pool[ev_used + 1], stream, cudaEventRecordExternal), "cudaEventRecord");
         ev_used += 2;
         upd_alg_bytes += alg_bytes;
         upd_timed += 1;
