@@ -12,6 +12,7 @@
 
 #include <cfloat>
 #include <cstdio>
+#include <cstring>
 
 namespace fb200 {
 
@@ -134,15 +135,29 @@ __global__ void __launch_bounds__(kThreads) fwd_kernel(const FwdArgs a, int nwk)
     }
 }
 
+template <class Args>
+void fill(KernelSpec& k, const void* func, dim3 grid, dim3 block, const Args& a) {
+    static_assert(sizeof(Args) <= sizeof(k.arg0), "kernel argument too large");
+    k.func = func;
+    k.grid = grid;
+    k.block = block;
+    k.smem = 0;
+    std::memcpy(k.arg0, &a, sizeof(Args));
+    k.nargs = 1;
+}
+
 template <int BT, int RW>
-void fwd_dispatch(const FwdArgs& a, cudaStream_t s, bool vec) {
+void fwd_spec(const FwdArgs& a, bool vec, KernelSpec& k) {
     const int nk = vec ? (a.in >> 2) : a.in;
     int nwk = (nk + 63) / 64;  // >= 2 K-units per lane per warp
     nwk = nwk >= 8 ? 8 : nwk >= 4 ? 4 : nwk >= 2 ? 2 : 1;
     const int rows_per_cta = (kWarps / nwk) * RW;
     const int grid = (a.out + rows_per_cta - 1) / rows_per_cta;
-    if (vec) fwd_kernel<BT, RW, true><<<grid, kThreads, 0, s>>>(a, nwk);
-    else fwd_kernel<BT, RW, false><<<grid, kThreads, 0, s>>>(a, nwk);
+    const void* f = vec ? reinterpret_cast<const void*>(&fwd_kernel<BT, RW, true>)
+                        : reinterpret_cast<const void*>(&fwd_kernel<BT, RW, false>);
+    fill(k, f, dim3(grid), dim3(kThreads), a);
+    k.arg1 = nwk;
+    k.nargs = 2;
 }
 
 // ---------------------------------------------------------------------------
@@ -547,12 +562,12 @@ __global__ void __launch_bounds__(kThreads, 2) update_kernel(const UpdArgs a) {
 }
 
 template <int POLICY>
-void update_dispatch(const UpdArgs& a, int grid, cudaStream_t s) {
-    if (a.B <= 1) update_kernel<POLICY, 1><<<grid, kThreads, 0, s>>>(a);
-    else if (a.B <= 2) update_kernel<POLICY, 2><<<grid, kThreads, 0, s>>>(a);
-    else if (a.B <= 4) update_kernel<POLICY, 4><<<grid, kThreads, 0, s>>>(a);
-    else if (a.B <= 8) update_kernel<POLICY, 8><<<grid, kThreads, 0, s>>>(a);
-    else update_kernel<POLICY, 16><<<grid, kThreads, 0, s>>>(a);
+const void* update_func(int B) {
+    if (B <= 1) return reinterpret_cast<const void*>(&update_kernel<POLICY, 1>);
+    if (B <= 2) return reinterpret_cast<const void*>(&update_kernel<POLICY, 2>);
+    if (B <= 4) return reinterpret_cast<const void*>(&update_kernel<POLICY, 4>);
+    if (B <= 8) return reinterpret_cast<const void*>(&update_kernel<POLICY, 8>);
+    return reinterpret_cast<const void*>(&update_kernel<POLICY, 16>);
 }
 
 // ---------------------------------------------------------------------------
@@ -618,18 +633,18 @@ __global__ void pool_kernel(const PoolArgs a) {
 
 } // namespace
 
-void launch_fwd(const FwdArgs& a, cudaStream_t s) {
+void spec_fwd(const FwdArgs& a, KernelSpec& k) {
     // rows are b * in (or xidx[b] * in) floats from X: float4 needs in % 4 == 0 and aligned bases
     const bool vec = (a.in & 3) == 0 && aligned16(a.W) && aligned16(a.X);
-    if (a.B <= 1) fwd_dispatch<1, 4>(a, s, vec);
-    else if (a.B <= 2) fwd_dispatch<2, 4>(a, s, vec);
-    else if (a.B <= 4) fwd_dispatch<4, 4>(a, s, vec);
-    else if (a.B <= 8) fwd_dispatch<8, 4>(a, s, vec);
-    else fwd_dispatch<16, 2>(a, s, vec);
+    if (a.B <= 1) fwd_spec<1, 4>(a, vec, k);
+    else if (a.B <= 2) fwd_spec<2, 4>(a, vec, k);
+    else if (a.B <= 4) fwd_spec<4, 4>(a, vec, k);
+    else if (a.B <= 8) fwd_spec<8, 4>(a, vec, k);
+    else fwd_spec<16, 2>(a, vec, k);
 }
 
-void launch_head(const HeadArgs& a, cudaStream_t s) {
-    head_kernel<<<(a.B + kWarps - 1) / kWarps, kThreads, 0, s>>>(a);
+void spec_head(const HeadArgs& a, KernelSpec& k) {
+    fill(k, reinterpret_cast<const void*>(&head_kernel), dim3((a.B + kWarps - 1) / kWarps), dim3(kThreads), a);
 }
 
 static int bwd_vec(int in) { return (in & 3) == 0 ? 4 : 1; }
@@ -650,32 +665,37 @@ int bwd_row_splits(int in, int out) {
 }
 
 template <int BT>
-static void bwd_dispatch(const BwdArgs& a, cudaStream_t s) {
-    dim3 grid(bwd_col_tiles(a.in), a.row_splits);
-    if (bwd_vec(a.in) == 4 && aligned16(a.W)) bwd_kernel<BT, 4><<<grid, kThreads, 0, s>>>(a);
-    else bwd_kernel<BT, 1><<<grid, kThreads, 0, s>>>(a);
+static const void* bwd_func(bool vec) {
+    return vec ? reinterpret_cast<const void*>(&bwd_kernel<BT, 4>) : reinterpret_cast<const void*>(&bwd_kernel<BT, 1>);
 }
 
-void launch_bwd(const BwdArgs& a, cudaStream_t s) {
-    if (a.B <= 1) bwd_dispatch<1>(a, s);
-    else if (a.B <= 2) bwd_dispatch<2>(a, s);
-    else if (a.B <= 4) bwd_dispatch<4>(a, s);
-    else if (a.B <= 8) bwd_dispatch<8>(a, s);
-    else bwd_dispatch<16>(a, s);
+void spec_bwd(const BwdArgs& a, KernelSpec& k) {
+    const dim3 grid(bwd_col_tiles(a.in), a.row_splits);
+    const bool vec = bwd_vec(a.in) == 4 && aligned16(a.W);
+    const void* f = a.B <= 1 ? bwd_func<1>(vec) : a.B <= 2 ? bwd_func<2>(vec) : a.B <= 4 ? bwd_func<4>(vec)
+                  : a.B <= 8 ? bwd_func<8>(vec) : bwd_func<16>(vec);
+    fill(k, f, grid, dim3(kThreads), a);
 }
 
-void launch_update(const UpdArgs& a, cudaStream_t s) {
+void spec_update(const UpdArgs& a, KernelSpec& k) {
     long long blocks = (a.n_items + kThreads - 1) / kThreads;
     if (blocks > 148 * 16) blocks = 148 * 16;
     if (blocks < 1) blocks = 1;
-    const int grid = (int)blocks;
-    switch (a.policy) {
-        case 0: update_dispatch<0>(a, grid, s); break;
-        case 1: update_dispatch<1>(a, grid, s); break;
-        case 2: update_dispatch<2>(a, grid, s); break;
-        case 3: update_dispatch<3>(a, grid, s); break;
-        default: update_dispatch<4>(a, grid, s); break;
-    }
+    const void* f = a.policy == 0 ? update_func<0>(a.B) : a.policy == 1 ? update_func<1>(a.B)
+                  : a.policy == 2 ? update_func<2>(a.B) : a.policy == 3 ? update_func<3>(a.B) : update_func<4>(a.B);
+    fill(k, f, dim3((unsigned)blocks), dim3(kThreads), a);
+}
+
+void spec_normalize(const NormArgs& a, KernelSpec& k) {
+    fill(k, reinterpret_cast<const void*>(&normalize_kernel), dim3((a.F + 127) / 128), dim3(128), a);
+}
+
+void spec_pool(const PoolArgs& a, KernelSpec& k) {
+    fill(k, reinterpret_cast<const void*>(&pool_kernel), dim3(a.B), dim3(128), a);
+}
+
+cudaError_t launch_spec(KernelSpec& k, cudaStream_t s) {
+    return cudaLaunchKernel(k.func, k.grid, k.block, k.kernel_params(), k.smem, s);
 }
 
 void launch_compensate(const CompArgs& a, cudaStream_t s) {
@@ -689,14 +709,6 @@ void launch_compensate(const CompArgs& a, cudaStream_t s) {
         case 3: compensate_kernel<3><<<(int)blocks, kThreads, 0, s>>>(a); break;
         default: compensate_kernel<4><<<(int)blocks, kThreads, 0, s>>>(a); break;
     }
-}
-
-void launch_normalize(const NormArgs& a, cudaStream_t s) {
-    normalize_kernel<<<(a.F + 127) / 128, 128, 0, s>>>(a);
-}
-
-void launch_pool(const PoolArgs& a, cudaStream_t s) {
-    pool_kernel<<<a.B, 128, 0, s>>>(a);
 }
 
 } // namespace fb200

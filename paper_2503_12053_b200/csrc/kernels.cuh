@@ -130,12 +130,33 @@ struct PoolArgs {
     int B, F;
 };
 
-void launch_fwd(const FwdArgs& a, cudaStream_t s);
-void launch_head(const HeadArgs& a, cudaStream_t s);
-void launch_bwd(const BwdArgs& a, cudaStream_t s);
-void launch_update(const UpdArgs& a, cudaStream_t s);
-void launch_normalize(const NormArgs& a, cudaStream_t s);
-void launch_pool(const PoolArgs& a, cudaStream_t s);
+// A fully resolved kernel launch: the trainer either launches it on a stream
+// or adds it to its CUDA graph as a node with explicit dependencies.
+struct KernelSpec {
+    const void* func = nullptr;
+    dim3 grid, block;
+    size_t smem = 0;
+    alignas(16) unsigned char arg0[2048];  // the kernel's struct argument
+    int arg1 = 0;                         // optional trailing int argument
+    int nargs = 1;
+    void* params[2];
+    KernelSpec() = default;
+    KernelSpec(const KernelSpec&) = delete;
+    KernelSpec& operator=(const KernelSpec&) = delete;
+    void** kernel_params() {
+        params[0] = arg0;
+        params[1] = &arg1;
+        return params;
+    }
+};
+
+void spec_fwd(const FwdArgs& a, KernelSpec& k);
+void spec_head(const HeadArgs& a, KernelSpec& k);
+void spec_bwd(const BwdArgs& a, KernelSpec& k);
+void spec_update(const UpdArgs& a, KernelSpec& k);
+void spec_normalize(const NormArgs& a, KernelSpec& k);
+void spec_pool(const PoolArgs& a, KernelSpec& k);
+cudaError_t launch_spec(KernelSpec& k, cudaStream_t s);
 // grid geometry of the bwd launcher (for scratch sizing)
 int bwd_col_tiles(int in);
 int bwd_row_splits(int in, int out);

@@ -138,6 +138,96 @@ struct ChunkPlan {
     size_t n_replays = 0;
 };
 
+// Builds the chunk graph as a DAG. Every node declares the HBM resources it
+// reads and writes; it depends on the last writer of each (RAW/WAW) and, for
+// writes, on the readers since that writer (WAR). Events that touch disjoint
+// resources — different stages, different in-flight units — therefore run
+// concurrently, which is the pipeline parallelism of the 1F1B schedule
+// realised on one GPU. `serial` chains every node instead (timing mode).
+struct GraphBuilder {
+    enum : uint64_t { kVSlot = 1, kState, kStash, kPred, kNorm, kNormState, kPool, kReplay };
+    static uint64_t key(uint64_t kind, uint64_t a, uint64_t b = 0) { return (kind << 56) | (a << 32) | b; }
+
+    cudaGraph_t g = nullptr;
+    bool serial = false;
+    cudaGraphNode_t last = nullptr;
+    uint64_t kernels = 0;
+    struct Res {
+        cudaGraphNode_t writer = nullptr;
+        std::vector<cudaGraphNode_t> readers;
+    };
+    std::map<uint64_t, Res> res;
+
+    explicit GraphBuilder(bool serial_) : serial(serial_) { cuda_check(cudaGraphCreate(&g, 0), "cudaGraphCreate"); }
+    ~GraphBuilder() {
+        if (g) cudaGraphDestroy(g);
+    }
+
+    std::vector<cudaGraphNode_t> deps(const std::vector<uint64_t>& reads, const std::vector<uint64_t>& writes) {
+        std::vector<cudaGraphNode_t> d;
+        if (serial) {
+            if (last) d.push_back(last);
+            return d;
+        }
+        for (uint64_t r : reads) {
+            auto it = res.find(r);
+            if (it != res.end() && it->second.writer) d.push_back(it->second.writer);
+        }
+        for (uint64_t w : writes) {
+            auto it = res.find(w);
+            if (it == res.end()) continue;
+            if (it->second.writer) d.push_back(it->second.writer);
+            d.insert(d.end(), it->second.readers.begin(), it->second.readers.end());
+        }
+        std::sort(d.begin(), d.end());
+        d.erase(std::unique(d.begin(), d.end()), d.end());
+        return d;
+    }
+
+    void commit(cudaGraphNode_t n, const std::vector<uint64_t>& reads, const std::vector<uint64_t>& writes) {
+        last = n;
+        if (serial) return;
+        for (uint64_t r : reads) res[r].readers.push_back(n);
+        for (uint64_t w : writes) {
+            Res& x = res[w];
+            x.writer = n;
+            x.readers.clear();
+        }
+    }
+
+    cudaGraphNode_t kernel(fb200::KernelSpec& k, const std::vector<uint64_t>& reads, const std::vector<uint64_t>& writes) {
+        const std::vector<cudaGraphNode_t> d = deps(reads, writes);
+        cudaKernelNodeParams p{};
+        p.func = const_cast<void*>(k.func);
+        p.gridDim = k.grid;
+        p.blockDim = k.block;
+        p.sharedMemBytes = static_cast<unsigned>(k.smem);
+        p.kernelParams = k.kernel_params();
+        cudaGraphNode_t n;
+        cuda_check(cudaGraphAddKernelNode(&n, g, d.data(), d.size(), &p), "cudaGraphAddKernelNode");
+        commit(n, reads, writes);
+        ++kernels;
+        return n;
+    }
+
+    cudaGraphNode_t copy(void* dst, const void* src, size_t bytes, const std::vector<uint64_t>& reads,
+                         const std::vector<uint64_t>& writes) {
+        const std::vector<cudaGraphNode_t> d = deps(reads, writes);
+        cudaGraphNode_t n;
+        cuda_check(cudaGraphAddMemcpyNode1D(&n, g, d.data(), d.size(), dst, src, bytes, cudaMemcpyDeviceToDevice),
+                   "cudaGraphAddMemcpyNode1D");
+        commit(n, reads, writes);
+        return n;
+    }
+
+    // event record node after `last` (serial mode only: brackets a kernel)
+    void event(cudaEvent_t e) {
+        cudaGraphNode_t n;
+        cuda_check(cudaGraphAddEventRecordNode(&n, g, last ? &last : nullptr, last ? 1 : 0, e), "cudaGraphAddEventRecordNode");
+        last = n;
+    }
+};
+
 struct PassResult {
     std::vector<int> need_depth;
     std::vector<long long> pushes;
@@ -191,11 +281,16 @@ struct ferret_trainer {
     float* d_stash = nullptr;
     long long stash_stride = 0;
     int stash_slots = 0;
-    float* d_pred_buf = nullptr;  // 2 x B x max_width
+    long long pred_off = 0;       // predict ping-pong scratch (2 x B x max_width) inside a stash slot
     long long pred_stride = 0;
     float* d_replay = nullptr;    // one stash-shaped slot
+    // bwd split-reduction scratch, one region per stash slot (+1 for replay) so
+    // that concurrent backwards of different units never share it
     float* d_partial = nullptr;
     unsigned* d_counters = nullptr;
+    size_t max_partial = 1, max_tiles = 1;
+    int scratch_slots = 0;
+    GraphBuilder* gb = nullptr;   // set while the graph is being built
 
     HostState hs;
     Schedule sched;
@@ -239,7 +334,7 @@ struct ferret_trainer {
                         static_cast<void*>(d_norm_mean), static_cast<void*>(d_norm_m2), static_cast<void*>(d_rawc),
                         static_cast<void*>(d_xc), static_cast<void*>(d_labc), static_cast<void*>(d_predc),
                         static_cast<void*>(d_ctl), static_cast<void*>(d_pool_x), static_cast<void*>(d_pool_lab),
-                        static_cast<void*>(d_stash), static_cast<void*>(d_pred_buf), static_cast<void*>(d_replay),
+                        static_cast<void*>(d_stash), static_cast<void*>(d_replay),
                         static_cast<void*>(d_partial), static_cast<void*>(d_counters)})
             dfree(p);
         if (stream) cudaStreamDestroy(stream);
@@ -294,11 +389,11 @@ struct ferret_trainer {
             cursor = ld.dlt_off + static_cast<long long>(B) * ld.out;
             max_width = std::max(max_width, ld.out);
         }
-        stash_stride = align_up(cursor, 64);
         pred_stride = align_up(static_cast<long long>(B) * max_width, 64);
+        pred_off = align_up(cursor, 64);
+        stash_stride = align_up(pred_off + 2 * pred_stride, 64);
         stages.resize(static_cast<size_t>(P));
         hs.current.assign(static_cast<size_t>(P), 0);
-        size_t max_partial = 1, max_tiles = 1;
         for (int j = 0; j < P; ++j) {
             StageDev& s = stages[static_cast<size_t>(j)];
             s.lo = static_cast<int>(bounds[j]);
@@ -367,11 +462,7 @@ struct ferret_trainer {
             grow_ring(s, 2);
         }
         upload_initial_params();
-        d_pred_buf = dalloc<float>(static_cast<size_t>(2 * pred_stride), device_bytes);
         d_replay = dalloc<float>(static_cast<size_t>(stash_stride), device_bytes);
-        d_partial = dalloc<float>(max_partial, device_bytes);
-        d_counters = dalloc<unsigned>(max_tiles, device_bytes);
-        cuda_check(cudaMemset(d_counters, 0, max_tiles * sizeof(unsigned)), "memset");
         d_norm_mean = dalloc<double>(static_cast<size_t>(F), device_bytes);
         d_norm_m2 = dalloc<double>(static_cast<size_t>(F), device_bytes);
         cuda_check(cudaMemset(d_norm_mean, 0, static_cast<size_t>(F) * sizeof(double)), "memset");
@@ -414,6 +505,18 @@ struct ferret_trainer {
         }
         s.ring = fresh;
         s.depth = depth;
+    }
+
+    // per-slot bwd reduction scratch: slots 0..stash_slots-1 for units, the last for replay
+    void ensure_scratch(int slots) {
+        if (slots <= scratch_slots) return;
+        cuda_check(cudaStreamSynchronize(stream), "sync");
+        dfree(d_partial);
+        dfree(d_counters);
+        d_partial = dalloc<float>(static_cast<size_t>(slots) * max_partial, device_bytes);
+        d_counters = dalloc<unsigned>(static_cast<size_t>(slots) * max_tiles, device_bytes);
+        cuda_check(cudaMemset(d_counters, 0, static_cast<size_t>(slots) * max_tiles * sizeof(unsigned)), "memset");
+        scratch_slots = slots;
     }
 
     void ensure_stash(int slots) {
@@ -624,12 +727,7 @@ struct ferret_trainer {
         const PassResult need = run_pass<true>(probe, seen_any);
         for (int j = 0; j < P; ++j) grow_ring(stages[static_cast<size_t>(j)], need.need_depth[static_cast<size_t>(j)]);
         ensure_stash(std::max(need.need_slots, 1));
-        const size_t groups = (sched.n_units + kNormGroup - 1) / kNormGroup;
-        while (norm_events.size() < std::max<size_t>(groups, 1)) {
-            cudaEvent_t e;
-            cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
-            norm_events.push_back(e);
-        }
+        ensure_scratch(stash_slots + 1);
         if (timing)
             while (ev_pool.size() < 2 * need.n_updates_timed) {
                 cudaEvent_t e;
@@ -637,21 +735,20 @@ struct ferret_trainer {
                 ev_pool.push_back(e);
             }
         cuda_check(cudaStreamSynchronize(stream), "sync");
-        cudaGraph_t graph = nullptr;
-        cuda_check(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+        // timing mode serialises the graph so each update's events bracket it alone
+        GraphBuilder builder(timing);
+        gb = &builder;
         PassResult got;
         try {
             HostState cap = hs;
             got = run_pass<false>(cap, seen_any);
         } catch (...) {
-            cudaStreamEndCapture(stream, &graph);
-            if (graph) cudaGraphDestroy(graph);
+            gb = nullptr;
             throw;
         }
-        cuda_check(cudaStreamEndCapture(stream, &graph), "cudaStreamEndCapture");
-        const cudaError_t inst = cudaGraphInstantiate(&graph_exec, graph, 0);
-        cudaGraphDestroy(graph);
-        cuda_check(inst, "cudaGraphInstantiate");
+        gb = nullptr;
+        cuda_check(cudaGraphInstantiate(&graph_exec, builder.g, 0), "cudaGraphInstantiate");
+        launches = builder.kernels;
         graph_shape = got;
         graph_timing = timing;
         graph_seen_any = seen_any;
@@ -705,10 +802,16 @@ struct ferret_trainer {
         auto stash = [&](size_t u) { return d_stash + static_cast<long long>(slot_of[u]) * stash_stride; };
         auto xrows = [&](size_t u) { return d_xc + u * static_cast<size_t>(B) * static_cast<size_t>(F); };
 
+        using GB = GraphBuilder;
+        auto vslot = [&](int j, long long v) {  // resource key of the ring slot holding version v of stage j
+            return GB::key(GB::kVSlot, static_cast<uint64_t>(j), static_cast<uint64_t>(v % stages[static_cast<size_t>(j)].depth));
+        };
+        auto ustash = [&](size_t u) { return GB::key(GB::kStash, static_cast<uint64_t>(slot_of[u])); };
+        auto ngroup = [&](size_t u) { return GB::key(GB::kNorm, u / kNormGroup); };
+
         if (!DRY) {
-            // normalizer groups on the side stream (fork from the main stream)
-            cuda_check(cudaEventRecord(fork_event, stream), "cudaEventRecord");
-            cuda_check(cudaStreamWaitEvent(nstream, fork_event, 0), "cudaStreamWaitEvent");
+            // normalizer groups: a chain of their own (mean/m2 state), each unit's
+            // ops wait only for the group holding its rows
             const size_t groups = (n_units + kNormGroup - 1) / kNormGroup;
             for (size_t g = 0; g < groups; ++g) {
                 const size_t u0 = g * kNormGroup, u1 = std::min(n_units, u0 + kNormGroup);
@@ -717,13 +820,9 @@ struct ferret_trainer {
                 fb200::NormArgs na{d_rawc + s0 * static_cast<size_t>(F), static_cast<long long>(ns), F, ctl_count(),
                                    static_cast<unsigned long long>(s0), d_norm_mean, d_norm_m2,
                                    d_xc + s0 * static_cast<size_t>(F)};
-                fb200::launch_normalize(na, nstream);
-                cuda_check(cudaEventRecord(norm_events[g], nstream), "cudaEventRecord");
-                ++launches;
-            }
-            if (groups == 0) {  // join the fork even without arrivals
-                cuda_check(cudaEventRecord(norm_events[0], nstream), "cudaEventRecord");
-                cuda_check(cudaStreamWaitEvent(stream, norm_events[0], 0), "cudaStreamWaitEvent");
+                fb200::KernelSpec k;
+                fb200::spec_normalize(na, k);
+                gb->kernel(k, {}, {GB::key(GB::kNorm, g), GB::key(GB::kNormState, 0)});
             }
         }
 
@@ -733,8 +832,6 @@ struct ferret_trainer {
             const int j = e.stage;
             switch (e.kind) {
                 case FERRET_EV_ARRIVAL: {  // learner.hpp:389-410
-                    if (!DRY && u % kNormGroup == 0)
-                        cuda_check(cudaStreamWaitEvent(stream, norm_events[u / kNormGroup], 0), "cudaStreamWaitEvent");
                     if (sched.dropped[u]) break;
                     inflight[u] = 1;
                     if (!as_shipped) {
@@ -743,14 +840,19 @@ struct ferret_trainer {
                         free_slots.pop_back();
                     }
                     ++n_pred;
-                    if (!DRY) launch_predict(u, rel);
+                    if (!DRY) {
+                        std::vector<uint64_t> reads{ngroup(u)};
+                        for (int s = 0; s < P; ++s) reads.push_back(vslot(s, rel[static_cast<size_t>(s)]));
+                        launch_predict(u, rel, as_shipped ? -1 : slot_of[u], reads);
+                    }
                     if (opt.replay && !as_shipped) {
                         buffer_nonempty = true;
                         if (!DRY) {
                             fb200::PoolArgs pa{xrows(u), d_labc + u * static_cast<size_t>(B),
                                                ctl_pool_dst() + u * static_cast<size_t>(B), d_pool_x, d_pool_lab, B, F};
-                            fb200::launch_pool(pa, stream);
-                            ++launches;
+                            fb200::KernelSpec k;
+                            fb200::spec_pool(pa, k);
+                            gb->kernel(k, {ngroup(u)}, {GB::key(GB::kPool, 0)});
                         }
                     }
                     break;
@@ -760,7 +862,9 @@ struct ferret_trainer {
                     const long long v = rel[static_cast<size_t>(j)];
                     read_ver[u * static_cast<size_t>(P) + static_cast<size_t>(j)] = v;
                     if (sched.has_bwd[u * static_cast<size_t>(P) + static_cast<size_t>(j)]) live[static_cast<size_t>(j)][v] += 1;
-                    if (!DRY) launch_stage_forward(j, stages[static_cast<size_t>(j)].slot(v), stash(u), xrows(u));
+                    if (!DRY)
+                        launch_stage_forward(j, stages[static_cast<size_t>(j)].slot(v), stash(u), xrows(u),
+                                             {vslot(j, v), ngroup(u)}, ustash(u));
                     break;
                 }
                 case FERRET_EV_BACKWARD: {  // learner.hpp:435-479
@@ -769,7 +873,7 @@ struct ferret_trainer {
                     if (r < 0) fail(FERRET_E_OUT_OF_RANGE, "stage version evicted");
                     if (!DRY)
                         launch_stage_backward(j, stages[static_cast<size_t>(j)].slot(r), stash(u),
-                                              d_labc + u * static_cast<size_t>(B));
+                                              d_labc + u * static_cast<size_t>(B), slot_of[u], {vslot(j, r)}, ustash(u));
                     pending[{e.worker, j}].push_back({u, r});
                     break;
                 }
@@ -795,15 +899,20 @@ struct ferret_trainer {
                         a.policy = opt.policy;
                         a.K = static_cast<int>(pl.size());
                         std::vector<long long> reads;
+                        std::vector<uint64_t> rk;
                         for (size_t k = 0; k < pl.size(); ++k) {
                             a.pend[k] = {stash(pl[k].u), xrows(pl[k].u), static_cast<int>(pl[k].read - oldest)};
                             reads.push_back(pl[k].read);
+                            rk.push_back(ustash(pl[k].u));
+                            rk.push_back(ngroup(pl[k].u));
                         }
+                        for (long long v = oldest; v <= cur; ++v) rk.push_back(vslot(j, v));
                         a.step = static_cast<float>(opt.lr * (1.0 / static_cast<double>(pl.size())));
+                        fb200::KernelSpec k;
+                        fb200::spec_update(a, k);
                         time_begin();
-                        fb200::launch_update(a, stream);
+                        gb->kernel(k, rk, {vslot(j, cur + 1), GB::key(GB::kState, static_cast<uint64_t>(j))});
                         time_end(update_bytes(j, opt.policy, reads, cur));
-                        ++launches;
                     }
                     rel[static_cast<size_t>(j)] += 1;
                     res.pushes[static_cast<size_t>(j)] += 1;
@@ -814,7 +923,7 @@ struct ferret_trainer {
                     }
                     it->second.clear();
                     if (j == 0 && opt.replay && buffer_nonempty) {  // learner.hpp:509, 513-519
-                        replay_step<DRY>(res.n_replays, rel, note_push);
+                        replay_step<DRY>(res.n_replays, rel, note_push, vslot);
                         for (int s = 0; s < P; ++s) res.pushes[static_cast<size_t>(s)] += 1;
                         ++res.n_replays;
                     }
@@ -835,9 +944,8 @@ struct ferret_trainer {
                 const StageDev& s = stages[static_cast<size_t>(j)];
                 const long long fin = rel[static_cast<size_t>(j)] % s.depth;
                 if (fin != 0)
-                    cuda_check(cudaMemcpyAsync(s.ring, s.slot(fin), static_cast<size_t>(s.slot_floats) * sizeof(float),
-                                               cudaMemcpyDeviceToDevice, stream),
-                               "ring rebase");
+                    gb->copy(s.ring, s.slot(fin), static_cast<size_t>(s.slot_floats) * sizeof(float), {vslot(j, fin)},
+                             {vslot(j, 0)});
             }
             stats.events = sched.events.size();
             stats.updates = n_upd;
@@ -882,8 +990,10 @@ struct ferret_trainer {
         return a;
     }
 
-    // ----------------------------------------------------- launch helpers
-    void launch_layer(const LayerDev& ld, const float* stage_slot, const float* X, const int* xidx, float* Y) {
+    // ----------------------------------------------------- node helpers
+    // One dense layer on B samples (input row b = X + (xidx ? xidx[b] : b) * in).
+    void emit_layer(const LayerDev& ld, const float* stage_slot, const float* X, const int* xidx, float* Y,
+                    const std::vector<uint64_t>& reads, const std::vector<uint64_t>& writes) {
         fb200::FwdArgs a{};
         a.W = stage_slot + ld.woff;
         a.bias = stage_slot + ld.boff;
@@ -894,18 +1004,24 @@ struct ferret_trainer {
         a.out = ld.out;
         a.B = B;
         a.relu = ld.act == FERRET_ACT_RELU;
-        fb200::launch_fwd(a, stream);
-        ++launches;
+        fb200::KernelSpec k;
+        fb200::spec_fwd(a, k);
+        gb->kernel(k, reads, writes);
     }
 
-    // predict_class(net_, x) at the arrival (learner.hpp:398-399): full net, live versions.
-    void launch_predict(size_t u, const std::vector<long long>& rel) {
+    // predict_class(net_, x) at the arrival (learner.hpp:398-399): full net at
+    // the live versions, ping-pong scratch inside the unit's stash slot (as
+    // shipped there is no slot: the replay stash's scratch is used, serialised).
+    void launch_predict(size_t u, const std::vector<long long>& rel, int slot, const std::vector<uint64_t>& reads) {
+        using GB = GraphBuilder;
+        float* scratch = (slot >= 0 ? d_stash + static_cast<long long>(slot) * stash_stride : d_replay) + pred_off;
+        const uint64_t sk = slot >= 0 ? GB::key(GB::kPred, static_cast<uint64_t>(slot)) : GB::key(GB::kReplay, 0);
         const float* X = d_xc + u * static_cast<size_t>(B) * static_cast<size_t>(F);
         for (int l = 0; l < L; ++l) {
             const LayerDev& ld = layers[static_cast<size_t>(l)];
             const StageDev& s = stages[static_cast<size_t>(ld.stage)];
-            float* Y = d_pred_buf + (l & 1) * pred_stride;
-            launch_layer(ld, s.slot(rel[static_cast<size_t>(ld.stage)]), X, nullptr, Y);
+            float* Y = scratch + (l & 1) * pred_stride;
+            emit_layer(ld, s.slot(rel[static_cast<size_t>(ld.stage)]), X, nullptr, Y, reads, {sk});
             X = Y;
         }
         fb200::HeadArgs h{};
@@ -914,31 +1030,35 @@ struct ferret_trainer {
         h.B = B;
         h.mode = 0;
         h.pred = d_predc + u * static_cast<size_t>(B);
-        fb200::launch_head(h, stream);
-        ++launches;
+        fb200::KernelSpec k;
+        fb200::spec_head(h, k);
+        gb->kernel(k, {}, {sk});
     }
 
-    void launch_stage_forward(int j, const float* slot, float* stash_u, const float* x0) {
+    void launch_stage_forward(int j, const float* slot, float* stash_u, const float* x0, const std::vector<uint64_t>& reads,
+                              uint64_t stash_key) {
         const StageDev& s = stages[static_cast<size_t>(j)];
         for (int l = s.lo; l < s.hi; ++l) {
             const LayerDev& ld = layers[static_cast<size_t>(l)];
             const float* X = l == 0 ? x0 : stash_u + layers[static_cast<size_t>(l - 1)].act_off;
-            launch_layer(ld, slot, X, nullptr, stash_u + ld.act_off);
+            emit_layer(ld, slot, X, nullptr, stash_u + ld.act_off, reads, {stash_key});
         }
     }
 
     // delta at the logits (last stage) then per layer prev = W^T delta with the
     // ReLU mask of the layer below applied on write (learner.hpp:443-476).
-    void launch_stage_backward(int j, const float* slot, float* stash_u, const int* lab) {
+    void launch_stage_backward(int j, const float* slot, float* stash_u, const int* lab, int scratch,
+                               const std::vector<uint64_t>& reads, uint64_t stash_key) {
         const StageDev& s = stages[static_cast<size_t>(j)];
-        if (j == P - 1) launch_delta_head(stash_u, lab, nullptr, 1.0f / static_cast<float>(B));
+        if (j == P - 1) emit_delta_head(stash_u, lab, nullptr, 1.0f / static_cast<float>(B), {}, stash_key);
         for (int l = s.hi - 1; l >= s.lo; --l) {
             if (l == 0) break;  // no input gradient for the first layer
-            launch_layer_backward(l, slot, stash_u);
+            emit_layer_backward(l, slot, stash_u, scratch, reads, stash_key);
         }
     }
 
-    void launch_delta_head(float* stash_u, const int* lab, const int* lidx, float scale) {
+    void emit_delta_head(float* stash_u, const int* lab, const int* lidx, float scale, const std::vector<uint64_t>& reads,
+                         uint64_t stash_key) {
         const LayerDev& last = layers.back();
         fb200::HeadArgs h{};
         h.logits = stash_u + last.act_off;
@@ -949,11 +1069,13 @@ struct ferret_trainer {
         h.lidx = lidx;
         h.delta = stash_u + last.dlt_off;
         h.scale = scale;
-        fb200::launch_head(h, stream);
-        ++launches;
+        fb200::KernelSpec k;
+        fb200::spec_head(h, k);
+        gb->kernel(k, reads, {stash_key});
     }
 
-    void launch_layer_backward(int l, const float* slot, float* stash_u) {
+    void emit_layer_backward(int l, const float* slot, float* stash_u, int scratch, const std::vector<uint64_t>& reads,
+                             uint64_t stash_key) {
         const LayerDev& ld = layers[static_cast<size_t>(l)];
         const LayerDev& below = layers[static_cast<size_t>(l - 1)];
         fb200::BwdArgs a{};
@@ -965,35 +1087,42 @@ struct ferret_trainer {
         a.out = ld.out;
         a.B = B;
         a.row_splits = fb200::bwd_row_splits(ld.in, ld.out);
-        a.partial = d_partial;
-        a.counters = d_counters;
-        fb200::launch_bwd(a, stream);
-        ++launches;
+        a.partial = d_partial + static_cast<size_t>(scratch) * max_partial;
+        a.counters = d_counters + static_cast<size_t>(scratch) * max_tiles;
+        fb200::KernelSpec k;
+        fb200::spec_bwd(a, k);
+        gb->kernel(k, reads, {stash_key});
     }
 
     // replay_step (learner.hpp:513-519): forward_backward(net_, {buffer.sample()})
     // with mean reduction (net.hpp:157-200), apply_sgd on every stage, push a
     // version per stage. B pool samples per replay step at micro-batch B; the
     // pool positions come from the control block (row r of rep_ids).
-    template <bool DRY, class NotePush>
-    void replay_step(size_t r, std::vector<long long>& rel, NotePush& note_push) {
+    template <bool DRY, class NotePush, class VSlot>
+    void replay_step(size_t r, std::vector<long long>& rel, NotePush& note_push, VSlot& vslot) {
+        using GB = GraphBuilder;
         for (int j = 0; j < P; ++j) note_push(j);
         if (!DRY) {
+            const uint64_t rk = GB::key(GB::kReplay, 0), pk = GB::key(GB::kPool, 0);
+            std::vector<uint64_t> live_slots;
+            for (int j = 0; j < P; ++j) live_slots.push_back(vslot(j, rel[static_cast<size_t>(j)]));
             const int* ids = ctl_rep_ids() + r * static_cast<size_t>(B);
             const float* X = d_pool_x;
             const int* xidx = ids;
+            std::vector<uint64_t> reads = live_slots;
+            reads.push_back(pk);
             for (int l = 0; l < L; ++l) {
                 const LayerDev& ld = layers[static_cast<size_t>(l)];
                 const StageDev& s = stages[static_cast<size_t>(ld.stage)];
-                launch_layer(ld, s.slot(rel[static_cast<size_t>(ld.stage)]), X, xidx, d_replay + ld.act_off);
+                emit_layer(ld, s.slot(rel[static_cast<size_t>(ld.stage)]), X, xidx, d_replay + ld.act_off, reads, {rk});
                 X = d_replay + ld.act_off;
                 xidx = nullptr;
             }
-            launch_delta_head(d_replay, d_pool_lab, ids, 1.0f / static_cast<float>(B));
+            emit_delta_head(d_replay, d_pool_lab, ids, 1.0f / static_cast<float>(B), {pk}, rk);
             for (int l = L - 1; l >= 1; --l) {
                 const LayerDev& ld = layers[static_cast<size_t>(l)];
-                launch_layer_backward(l, stages[static_cast<size_t>(ld.stage)].slot(rel[static_cast<size_t>(ld.stage)]),
-                                      d_replay);
+                emit_layer_backward(l, stages[static_cast<size_t>(ld.stage)].slot(rel[static_cast<size_t>(ld.stage)]),
+                                    d_replay, stash_slots, live_slots, rk);
             }
             for (int j = 0; j < P; ++j) {
                 const long long cur = rel[static_cast<size_t>(j)];
@@ -1003,23 +1132,24 @@ struct ferret_trainer {
                 a.pend[0] = {d_replay, d_pool_x, 0};
                 a.x0idx = ids;
                 a.step = static_cast<float>(opt.lr);
-                fb200::launch_update(a, stream);
-                ++launches;
+                fb200::KernelSpec k;
+                fb200::spec_update(a, k);
+                gb->kernel(k, {rk, pk, vslot(j, cur)}, {vslot(j, cur + 1)});
             }
         }
         for (int j = 0; j < P; ++j) rel[static_cast<size_t>(j)] += 1;
     }
 
     // --------------------------------------------------------------- timing
+    // timing mode builds a serial graph, so an event node before and after an
+    // update node brackets that kernel alone
     void time_begin() {
         if (!timing) return;
-        // External: an event record node that fires when the graph runs (a plain
-        // record under capture is only a dependency marker)
-        cuda_check(cudaEventRecordWithFlags(ev_pool[ev_used], stream, cudaEventRecordExternal), "cudaEventRecord");
+        gb->event(ev_pool[ev_used]);
     }
     void time_end(double alg_bytes) {
         if (!timing) return;
-        cuda_check(cudaEventRecordWithFlags(ev_pool[ev_used + 1], stream, cudaEventRecordExternal), "cudaEventRecord");
+        gb->event(ev_pool[ev_used + 1]);
         ev_used += 2;
         upd_alg_bytes += alg_bytes;
         upd_timed += 1;
