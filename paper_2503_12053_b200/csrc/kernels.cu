@@ -421,153 +421,101 @@ __device__ __forceinline__ float fold_iter_cached(float g, const float (&cv)[kRe
     return o;
 }
 
-// One work item: V consecutive parameters of a weight row (or one bias) of a
-// stage, all K pending gradients folded in order (BT >= B, loads unrolled).
-template <int POLICY, int V, int BT>
-__device__ __forceinline__ void update_item(const UpdArgs& a, const UpdSeg& sg, long long q) {
-    const int K = a.K, B = a.B;
-    const bool learn = a.eta > 0.f && a.v_r != nullptr;
-    int r, c;
-    if (sg.bias) {
-        r = (int)q;
-        c = 0;
-    } else {
-        r = (int)(q / sg.per_row);
-        c = (int)(q - (long long)r * sg.per_row) * V;
-    }
-    const size_t e0 = (size_t)sg.elem0 + (sg.bias ? (size_t)r : (size_t)r * sg.in + c);
-    const int last = a.nv - 1;
-    const float* cur = a.vers[last];
-    float th[V], ld[V], vr[V], va[V], gp[V];
-    if (V == 4) {
-        const float4 t4 = __ldg(reinterpret_cast<const float4*>(cur + e0));
-        th[0] = t4.x; th[1 % V] = t4.y; th[2 % V] = t4.z; th[3 % V] = t4.w;
-    } else {
-        th[0] = __ldg(cur + e0);
-    }
-#pragma unroll
-    for (int v = 0; v < V; ++v) ld[v] = vr[v] = va[v] = gp[v] = 0.f;
-    if (POLICY == 4) {
-#pragma unroll
-        for (int v = 0; v < V; ++v) ld[v] = a.lam_d[e0 + v];
-        if (learn)
-#pragma unroll
-            for (int v = 0; v < V; ++v) {
-                vr[v] = a.v_r[e0 + v];
-                va[v] = a.v_a[e0 + v];
-            }
-    }
-    if (POLICY == 2)
-#pragma unroll
-        for (int v = 0; v < V; ++v) gp[v] = a.gap[e0 + v];
-    // iter_fisher: every older chain version this element needs, loaded at once
-    const bool cached = POLICY == 4 && last <= kRegChain;
-    float cv[kRegChain + 1][V];
-    if (POLICY == 4 && cached) {
-#pragma unroll
-        for (int i = 0; i < kRegChain; ++i) {
-            if (i < last) {
-                if (V == 4) {
-                    const float4 c4 = __ldg(reinterpret_cast<const float4*>(a.vers[i] + e0));
-                    cv[i][0] = c4.x; cv[i][1 % V] = c4.y; cv[i][2 % V] = c4.z; cv[i][3 % V] = c4.w;
-                } else {
-                    cv[i][0] = __ldg(a.vers[i] + e0);
-                }
-            } else {
-#pragma unroll
-                for (int v = 0; v < V; ++v) cv[i][v] = 0.f;
-            }
-        }
-#pragma unroll
-        for (int v = 0; v < V; ++v) cv[kRegChain][v] = 0.f;
-    }
-    float mean[V];
-#pragma unroll
-    for (int v = 0; v < V; ++v) mean[v] = 0.f;
-    for (int k = 0; k < K; ++k) {
-        const UpdPending& pk = a.pend[k];
-        const float* dl = pk.stash + sg.dlt_off + r;
-        float g[V];
-#pragma unroll
-        for (int v = 0; v < V; ++v) g[v] = 0.f;
-#pragma unroll
-        for (int b = 0; b < BT; ++b) {
-            if (b >= B) break;
-            const float d = __ldg(dl + (size_t)b * sg.out);
-            if (sg.bias) {
-                g[0] += d;
-                continue;
-            }
-            const float* xr = sg.xin_off >= 0 ? pk.stash + sg.xin_off + (size_t)b * sg.in
-                              : a.x0idx       ? pk.x0 + (size_t)__ldg(a.x0idx + b) * a.x0_ld
-                                              : pk.x0 + (size_t)b * a.x0_ld;
-            if (V == 4) {
-                const float4 x4 = __ldg(reinterpret_cast<const float4*>(xr + c));
-                g[0] = fmaf(d, x4.x, g[0]);
-                g[1 % V] = fmaf(d, x4.y, g[1 % V]);
-                g[2 % V] = fmaf(d, x4.z, g[2 % V]);
-                g[3 % V] = fmaf(d, x4.w, g[3 % V]);
-            } else {
-                g[0] = fmaf(d, __ldg(xr + c), g[0]);
-            }
-        }
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-            ElemState st{ld[v], vr[v], va[v], gp[v]};
-            if (POLICY == 4 && cached)
-                mean[v] += fold_iter_cached<V>(g[v], cv, v, pk.first, last, th[v], st, a.lambda0, a.alpha, a.eta,
-                                               a.nu, learn);
-            else
-                mean[v] += compensate_elem<POLICY>(g[v], a.vers, pk.first, last, e0 + v, th[v], st, a.lambda0,
-                                                   a.alpha, a.eta, a.nu, learn);
-            ld[v] = st.ld;
-            vr[v] = st.vr;
-            va[v] = st.va;
-            gp[v] = st.gp;
-        }
-    }
-    float nt[V];
-#pragma unroll
-    for (int v = 0; v < V; ++v) nt[v] = th[v] - a.step * mean[v];
-    if (V == 4) {
-        *reinterpret_cast<float4*>(a.dst + e0) = make_float4(nt[0], nt[1 % V], nt[2 % V], nt[3 % V]);
-    } else {
-        a.dst[e0] = nt[0];
-    }
-    if (POLICY == 4) {
-#pragma unroll
-        for (int v = 0; v < V; ++v) a.lam_d[e0 + v] = ld[v];
-        if (learn)
-#pragma unroll
-            for (int v = 0; v < V; ++v) {
-                a.v_r[e0 + v] = vr[v];
-                a.v_a[e0 + v] = va[v];
-            }
-    }
-    if (POLICY == 2)
-#pragma unroll
-        for (int v = 0; v < V; ++v) a.gap[e0 + v] = gp[v];
-}
-
+// ---------------------------------------------------------------------------
+// tiled update: one parameter per thread. A CTA covers up to 8 rows x 256
+// columns of one layer; the deltas of those rows (K pending x B samples) are
+// staged in smem and broadcast, and with one pending gradient the unit's B
+// input values of the thread's column stay in registers across the rows.
+// Chain versions are read coalesced across the CTA (consecutive columns).
+// ---------------------------------------------------------------------------
 template <int POLICY, int BT>
-__global__ void __launch_bounds__(kThreads, 2) update_kernel(const UpdArgs a) {
-    const long long stride = (long long)gridDim.x * kThreads;
-    for (long long q = (long long)blockIdx.x * kThreads + threadIdx.x; q < a.n_items; q += stride) {
-        int s = 0;
-        while (s + 1 < a.n_segs && q >= a.segs[s + 1].item0) ++s;
-        const UpdSeg sg = a.segs[s];
-        if (sg.vec == 4) update_item<POLICY, 4, BT>(a, sg, q - sg.item0);
-        else update_item<POLICY, 1, BT>(a, sg, q - sg.item0);
+__global__ void __launch_bounds__(kThreads) update_tile_kernel(const UpdArgs a) {
+    __shared__ float sdel[kMaxPending * kMaxBatch * kUpdMaxTileRows];
+    const UpdTile t = a.tiles[blockIdx.x];
+    const UpdSeg sg = a.segs[t.seg];
+    const int K = a.K, B = a.B, R = t.nrows;
+    const int tid = threadIdx.x;
+    const int last = a.nv - 1;
+    const bool learn = a.eta > 0.f && a.v_r != nullptr;
+    const bool cached = POLICY == 4 && last <= kRegChain;
+    if (!sg.bias) {
+        for (int i = tid; i < K * B * R; i += kThreads) {
+            const int k = i / (B * R), rem = i - k * B * R, b = rem / R, rr = rem - b * R;
+            sdel[i] = __ldg(a.pend[k].stash + sg.dlt_off + (size_t)b * sg.out + t.r0 + rr);
+        }
+        __syncthreads();
     }
+    // the element's new value, compensator state and write-back
+    auto apply = [&](size_t e, int row_in_tile, int c) {
+        const float th = __ldg(a.vers[last] + e);
+        ElemState st{0.f, 0.f, 0.f, 0.f};
+        if (POLICY == 4) {
+            st.ld = a.lam_d[e];
+            if (learn) {
+                st.vr = a.v_r[e];
+                st.va = a.v_a[e];
+            }
+        }
+        if (POLICY == 2) st.gp = a.gap[e];
+        float cv[kRegChain + 1][1];
+        if (cached) {
+#pragma unroll
+            for (int i = 0; i < kRegChain; ++i) cv[i][0] = i < last ? __ldg(a.vers[i] + e) : 0.f;
+            cv[kRegChain][0] = 0.f;
+        }
+        float mean = 0.f;
+        for (int k = 0; k < K; ++k) {
+            float g = 0.f;
+            if (sg.bias) {
+                const float* dl = a.pend[k].stash + sg.dlt_off + row_in_tile;  // row_in_tile = absolute row here
+#pragma unroll
+                for (int b = 0; b < BT; ++b)
+                    if (b < B) g += __ldg(dl + (size_t)b * sg.out);
+            } else {
+                const float* sd = sdel + (size_t)k * B * R + row_in_tile;
+                const UpdPending& pk = a.pend[k];
+#pragma unroll
+                for (int b = 0; b < BT; ++b) {
+                    if (b >= B) break;
+                    const float* xr = sg.xin_off >= 0 ? pk.stash + sg.xin_off + (size_t)b * sg.in
+                                      : a.x0idx       ? pk.x0 + (size_t)__ldg(a.x0idx + b) * a.x0_ld
+                                                      : pk.x0 + (size_t)b * a.x0_ld;
+                    g = fmaf(sd[b * R], __ldg(xr + c), g);
+                }
+            }
+            if (cached)
+                mean += fold_iter_cached<1>(g, cv, 0, a.pend[k].first, last, th, st, a.lambda0, a.alpha, a.eta, a.nu,
+                                            learn);
+            else
+                mean += compensate_elem<POLICY>(g, a.vers, a.pend[k].first, last, e, th, st, a.lambda0, a.alpha, a.eta,
+                                                a.nu, learn);
+        }
+        a.dst[e] = th - a.step * mean;
+        if (POLICY == 4) {
+            a.lam_d[e] = st.ld;
+            if (learn) {
+                a.v_r[e] = st.vr;
+                a.v_a[e] = st.va;
+            }
+        }
+        if (POLICY == 2) a.gap[e] = st.gp;
+    };
+    if (sg.bias) {
+        if (tid < R) apply((size_t)sg.elem0 + t.r0 + tid, t.r0 + tid, 0);
+        return;
+    }
+    const int c = t.c0 + tid;
+    if (c >= sg.in) return;
+    for (int i = 0; i < R; ++i) apply((size_t)sg.elem0 + (size_t)(t.r0 + i) * sg.in + c, i, c);
 }
 
 template <int POLICY>
 const void* update_func(int B) {
-    if (B <= 1) return reinterpret_cast<const void*>(&update_kernel<POLICY, 1>);
-    if (B <= 2) return reinterpret_cast<const void*>(&update_kernel<POLICY, 2>);
-    if (B <= 4) return reinterpret_cast<const void*>(&update_kernel<POLICY, 4>);
-    if (B <= 8) return reinterpret_cast<const void*>(&update_kernel<POLICY, 8>);
-    return reinterpret_cast<const void*>(&update_kernel<POLICY, 16>);
+    if (B <= 1) return reinterpret_cast<const void*>(&update_tile_kernel<POLICY, 1>);
+    if (B <= 2) return reinterpret_cast<const void*>(&update_tile_kernel<POLICY, 2>);
+    if (B <= 4) return reinterpret_cast<const void*>(&update_tile_kernel<POLICY, 4>);
+    if (B <= 8) return reinterpret_cast<const void*>(&update_tile_kernel<POLICY, 8>);
+    return reinterpret_cast<const void*>(&update_tile_kernel<POLICY, 16>);
 }
 
 // ---------------------------------------------------------------------------
@@ -678,9 +626,7 @@ void spec_bwd(const BwdArgs& a, KernelSpec& k) {
 }
 
 void spec_update(const UpdArgs& a, KernelSpec& k) {
-    long long blocks = (a.n_items + kThreads - 1) / kThreads;
-    if (blocks > 148 * 16) blocks = 148 * 16;
-    if (blocks < 1) blocks = 1;
+    const long long blocks = a.n_tiles;
     const void* f = a.policy == 0 ? update_func<0>(a.B) : a.policy == 1 ? update_func<1>(a.B)
                   : a.policy == 2 ? update_func<2>(a.B) : a.policy == 3 ? update_func<3>(a.B) : update_func<4>(a.B);
     fill(k, f, dim3((unsigned)blocks), dim3(kThreads), a);

@@ -77,6 +77,17 @@ struct UpdSeg {
     long long dlt_off;    // stash offset of the layer's delta
 };
 
+// One CTA of the update kernel: `nrows` rows x 256 columns of a layer's
+// weights starting at (r0, c0), or 256 consecutive bias elements from r0.
+constexpr int kUpdTileCols = 256;
+constexpr int kUpdMaxTileRows = 8;
+struct UpdTile {
+    int seg;    // index into the stage's segment table
+    int r0;     // first row (weights) or first bias element
+    int nrows;  // rows in this tile (weights) / elements (bias)
+    int c0;     // first column (weights)
+};
+
 struct UpdPending {
     const float* stash;   // the unit's stash slot (activations + deltas)
     const float* x0;      // net-input rows of the unit (when the stage holds layer 0)
@@ -92,6 +103,8 @@ struct UpdArgs {
     int n_segs, B, K, policy;
     long long n_items;
     const UpdSeg* segs;      // device array
+    const UpdTile* tiles;    // device array, one per CTA
+    int n_tiles;
     UpdPending pend[kMaxPending];
     const int* x0idx;        // nullable: net-input row b is x0 + x0idx[b] * x0_ld (replay), else x0 + b * x0_ld
     int x0_ld;

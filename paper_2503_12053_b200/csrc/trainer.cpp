@@ -115,6 +115,8 @@ struct StageDev {
     float* gap = nullptr;
     fb200::UpdSeg* segs_dev = nullptr;
     int n_segs = 0;
+    fb200::UpdTile* tiles_dev = nullptr;
+    int n_tiles = 0;
     long long n_items = 0;
     // slot of a version counted from the chunk start (the live version is in slot 0 between chunks)
     float* slot(long long rel) const { return ring + (rel % depth) * slot_floats; }
@@ -329,6 +331,7 @@ struct ferret_trainer {
             dfree(s.v_a);
             dfree(s.gap);
             dfree(s.segs_dev);
+            dfree(s.tiles_dev);
         }
         for (void* p : {static_cast<void*>(d_raw), static_cast<void*>(d_lab), static_cast<void*>(d_pred),
                         static_cast<void*>(d_norm_mean), static_cast<void*>(d_norm_m2), static_cast<void*>(d_rawc),
@@ -445,6 +448,28 @@ struct ferret_trainer {
             s.segs_dev = dalloc<fb200::UpdSeg>(tab.size(), device_bytes);
             cuda_check(cudaMemcpy(s.segs_dev, tab.data(), tab.size() * sizeof(fb200::UpdSeg), cudaMemcpyHostToDevice),
                        "upload segment table");
+            // update tiles: rows x 256 columns per CTA, the row count chosen so a
+            // stage update spans a few hundred CTAs (>= 2 per SM)
+            long long row_tiles = 0;
+            for (const fb200::UpdSeg& sg : tab)
+                if (!sg.bias) row_tiles += static_cast<long long>(sg.out) * ((sg.in + fb200::kUpdTileCols - 1) / fb200::kUpdTileCols);
+            const int R = static_cast<int>(std::min<long long>(fb200::kUpdMaxTileRows, std::max<long long>(1, (row_tiles + 399) / 400)));
+            std::vector<fb200::UpdTile> tiles;
+            for (size_t q = 0; q < tab.size(); ++q) {
+                const fb200::UpdSeg& sg = tab[q];
+                if (sg.bias) {
+                    for (int r0 = 0; r0 < sg.out; r0 += fb200::kUpdTileCols)
+                        tiles.push_back({static_cast<int>(q), r0, std::min(fb200::kUpdTileCols, sg.out - r0), 0});
+                } else {
+                    for (int r0 = 0; r0 < sg.out; r0 += R)
+                        for (int c0 = 0; c0 < sg.in; c0 += fb200::kUpdTileCols)
+                            tiles.push_back({static_cast<int>(q), r0, std::min(R, sg.out - r0), c0});
+                }
+            }
+            s.n_tiles = static_cast<int>(tiles.size());
+            s.tiles_dev = dalloc<fb200::UpdTile>(tiles.size(), device_bytes);
+            cuda_check(cudaMemcpy(s.tiles_dev, tiles.data(), tiles.size() * sizeof(fb200::UpdTile), cudaMemcpyHostToDevice),
+                       "upload tile table");
             const size_t n = static_cast<size_t>(s.slot_floats);
             if (opt.policy == FERRET_POLICY_ITER_FISHER) {
                 s.lam_d = dalloc<float>(n, device_bytes);
@@ -972,6 +997,8 @@ struct ferret_trainer {
         a.n_items = s.n_items;
         a.B = B;
         a.segs = s.segs_dev;
+        a.tiles = s.tiles_dev;
+        a.n_tiles = s.n_tiles;
         a.x0idx = nullptr;
         a.x0_ld = F;
         if (cur - oldest + 1 > fb200::kMaxChain)
