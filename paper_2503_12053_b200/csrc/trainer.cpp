@@ -154,31 +154,36 @@ struct GraphBuilder {
     bool serial = false;
     cudaGraphNode_t last = nullptr;
     uint64_t kernels = 0;
+    // Logical DAG (node index = creation order), kept in both modes: the
+    // profile mode (serial graph, events around every node) uses it to
+    // compute the critical path the concurrent graph is bound by.
+    std::vector<std::vector<int>> ldeps;
+    std::vector<int> category;
+    int cur_category = 0;
     struct Res {
-        cudaGraphNode_t writer = nullptr;
-        std::vector<cudaGraphNode_t> readers;
+        int writer = -1;
+        std::vector<int> readers;
     };
     std::map<uint64_t, Res> res;
+    std::vector<cudaGraphNode_t> nodes;
+    // profiling: an event before and after every node
+    std::vector<cudaEvent_t>* prof_events = nullptr;
 
     explicit GraphBuilder(bool serial_) : serial(serial_) { cuda_check(cudaGraphCreate(&g, 0), "cudaGraphCreate"); }
     ~GraphBuilder() {
         if (g) cudaGraphDestroy(g);
     }
 
-    std::vector<cudaGraphNode_t> deps(const std::vector<uint64_t>& reads, const std::vector<uint64_t>& writes) {
-        std::vector<cudaGraphNode_t> d;
-        if (serial) {
-            if (last) d.push_back(last);
-            return d;
-        }
+    std::vector<int> logical(const std::vector<uint64_t>& reads, const std::vector<uint64_t>& writes) {
+        std::vector<int> d;
         for (uint64_t r : reads) {
             auto it = res.find(r);
-            if (it != res.end() && it->second.writer) d.push_back(it->second.writer);
+            if (it != res.end() && it->second.writer >= 0) d.push_back(it->second.writer);
         }
         for (uint64_t w : writes) {
             auto it = res.find(w);
             if (it == res.end()) continue;
-            if (it->second.writer) d.push_back(it->second.writer);
+            if (it->second.writer >= 0) d.push_back(it->second.writer);
             d.insert(d.end(), it->second.readers.begin(), it->second.readers.end());
         }
         std::sort(d.begin(), d.end());
@@ -186,19 +191,52 @@ struct GraphBuilder {
         return d;
     }
 
-    void commit(cudaGraphNode_t n, const std::vector<uint64_t>& reads, const std::vector<uint64_t>& writes) {
+    std::vector<cudaGraphNode_t> deps(const std::vector<int>& ld) {
+        std::vector<cudaGraphNode_t> d;
+        if (serial) {
+            if (last) d.push_back(last);
+            if (prof_events) {  // event before the node
+                const size_t i = nodes.size();
+                while (prof_events->size() < 2 * i + 2) {
+                    cudaEvent_t e;
+                    cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+                    prof_events->push_back(e);
+                }
+                cudaGraphNode_t n;
+                cuda_check(cudaGraphAddEventRecordNode(&n, g, d.data(), d.size(), (*prof_events)[2 * i]),
+                           "cudaGraphAddEventRecordNode");
+                d.assign(1, n);
+            }
+            return d;
+        }
+        for (int x : ld) d.push_back(nodes[static_cast<size_t>(x)]);
+        return d;
+    }
+
+    void commit(cudaGraphNode_t n, const std::vector<int>& ld, const std::vector<uint64_t>& reads,
+                const std::vector<uint64_t>& writes) {
+        const int idx = static_cast<int>(nodes.size());
+        nodes.push_back(n);
+        ldeps.push_back(ld);
+        category.push_back(cur_category);
         last = n;
-        if (serial) return;
-        for (uint64_t r : reads) res[r].readers.push_back(n);
+        if (serial && prof_events) {  // event after the node
+            cudaGraphNode_t e;
+            cuda_check(cudaGraphAddEventRecordNode(&e, g, &n, 1, (*prof_events)[2 * static_cast<size_t>(idx) + 1]),
+                       "cudaGraphAddEventRecordNode");
+            last = e;
+        }
+        for (uint64_t r : reads) res[r].readers.push_back(idx);
         for (uint64_t w : writes) {
             Res& x = res[w];
-            x.writer = n;
+            x.writer = idx;
             x.readers.clear();
         }
     }
 
     cudaGraphNode_t kernel(fb200::KernelSpec& k, const std::vector<uint64_t>& reads, const std::vector<uint64_t>& writes) {
-        const std::vector<cudaGraphNode_t> d = deps(reads, writes);
+        const std::vector<int> ld = logical(reads, writes);
+        const std::vector<cudaGraphNode_t> d = deps(ld);
         cudaKernelNodeParams p{};
         p.func = const_cast<void*>(k.func);
         p.gridDim = k.grid;
@@ -207,18 +245,19 @@ struct GraphBuilder {
         p.kernelParams = k.kernel_params();
         cudaGraphNode_t n;
         cuda_check(cudaGraphAddKernelNode(&n, g, d.data(), d.size(), &p), "cudaGraphAddKernelNode");
-        commit(n, reads, writes);
+        commit(n, ld, reads, writes);
         ++kernels;
         return n;
     }
 
     cudaGraphNode_t copy(void* dst, const void* src, size_t bytes, const std::vector<uint64_t>& reads,
                          const std::vector<uint64_t>& writes) {
-        const std::vector<cudaGraphNode_t> d = deps(reads, writes);
+        const std::vector<int> ld = logical(reads, writes);
+        const std::vector<cudaGraphNode_t> d = deps(ld);
         cudaGraphNode_t n;
         cuda_check(cudaGraphAddMemcpyNode1D(&n, g, d.data(), d.size(), dst, src, bytes, cudaMemcpyDeviceToDevice),
                    "cudaGraphAddMemcpyNode1D");
-        commit(n, reads, writes);
+        commit(n, ld, reads, writes);
         return n;
     }
 
@@ -229,6 +268,9 @@ struct GraphBuilder {
         last = n;
     }
 };
+
+// node classes reported by the profile mode
+enum { kCatNorm = 0, kCatPredict, kCatForward, kCatBackward, kCatUpdate, kCatReplay, kCatOther, kNumCat };
 
 struct PassResult {
     std::vector<int> need_depth;
@@ -307,6 +349,12 @@ struct ferret_trainer {
     ferret_trainer_stats stats{};
     uint64_t launches = 0;
 
+    // profile mode: serial graph with events around every node + the logical DAG
+    bool profiling = false, graph_profiling = false;
+    std::vector<cudaEvent_t> prof_events;
+    std::vector<std::vector<int>> prof_ldeps;
+    std::vector<int> prof_cat;
+
     // optional per-launch timing of the update kernel (event record nodes)
     bool timing = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -320,6 +368,7 @@ struct ferret_trainer {
         if (nstream) cudaStreamSynchronize(nstream);
         if (graph_exec) cudaGraphExecDestroy(graph_exec);
         for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
+        for (cudaEvent_t e : prof_events) cudaEventDestroy(e);
         for (cudaEvent_t e : norm_events) cudaEventDestroy(e);
         for (cudaEvent_t e : ctl_done) cudaEventDestroy(e);
         if (fork_event) cudaEventDestroy(fork_event);
@@ -713,7 +762,8 @@ struct ferret_trainer {
         const size_t n_samples = sched.n_units * static_cast<size_t>(B);
         if (base + n_samples > n_loaded) fail(FERRET_E_OUT_OF_RANGE, "execute: chunk lies beyond the loaded stream");
         const bool seen_any = hs.replay.seen > 0;
-        if (graph_exec && (graph_timing != timing || graph_seen_any != seen_any)) invalidate_graph();
+        if (graph_exec && (graph_timing != timing || graph_profiling != profiling || graph_seen_any != seen_any))
+            invalidate_graph();
         if (!graph_exec) build_graph(seen_any);
         // host decisions for this chunk
         const ChunkPlan cp = plan_chunk(hs.replay);
@@ -760,8 +810,9 @@ struct ferret_trainer {
                 ev_pool.push_back(e);
             }
         cuda_check(cudaStreamSynchronize(stream), "sync");
-        // timing mode serialises the graph so each update's events bracket it alone
-        GraphBuilder builder(timing);
+        // timing / profile modes serialise the graph so events bracket one node each
+        GraphBuilder builder(timing || profiling);
+        if (profiling) builder.prof_events = &prof_events;
         gb = &builder;
         PassResult got;
         try {
@@ -774,6 +825,9 @@ struct ferret_trainer {
         gb = nullptr;
         cuda_check(cudaGraphInstantiate(&graph_exec, builder.g, 0), "cudaGraphInstantiate");
         launches = builder.kernels;
+        prof_ldeps = std::move(builder.ldeps);
+        prof_cat = std::move(builder.category);
+        graph_profiling = profiling;
         graph_shape = got;
         graph_timing = timing;
         graph_seen_any = seen_any;
@@ -847,6 +901,7 @@ struct ferret_trainer {
                                    d_xc + s0 * static_cast<size_t>(F)};
                 fb200::KernelSpec k;
                 fb200::spec_normalize(na, k);
+                gb->cur_category = kCatNorm;
                 gb->kernel(k, {}, {GB::key(GB::kNorm, g), GB::key(GB::kNormState, 0)});
             }
         }
@@ -877,6 +932,7 @@ struct ferret_trainer {
                                                ctl_pool_dst() + u * static_cast<size_t>(B), d_pool_x, d_pool_lab, B, F};
                             fb200::KernelSpec k;
                             fb200::spec_pool(pa, k);
+                            gb->cur_category = kCatOther;
                             gb->kernel(k, {ngroup(u)}, {GB::key(GB::kPool, 0)});
                         }
                     }
@@ -936,6 +992,7 @@ struct ferret_trainer {
                         fb200::KernelSpec k;
                         fb200::spec_update(a, k);
                         time_begin();
+                        gb->cur_category = kCatUpdate;
                         gb->kernel(k, rk, {vslot(j, cur + 1), GB::key(GB::kState, static_cast<uint64_t>(j))});
                         time_end(update_bytes(j, opt.policy, reads, cur));
                     }
@@ -969,6 +1026,7 @@ struct ferret_trainer {
                 const StageDev& s = stages[static_cast<size_t>(j)];
                 const long long fin = rel[static_cast<size_t>(j)] % s.depth;
                 if (fin != 0)
+                    gb->cur_category = kCatOther;
                     gb->copy(s.ring, s.slot(fin), static_cast<size_t>(s.slot_floats) * sizeof(float), {vslot(j, fin)},
                              {vslot(j, 0)});
             }
@@ -1041,6 +1099,7 @@ struct ferret_trainer {
     // shipped there is no slot: the replay stash's scratch is used, serialised).
     void launch_predict(size_t u, const std::vector<long long>& rel, int slot, const std::vector<uint64_t>& reads) {
         using GB = GraphBuilder;
+        gb->cur_category = kCatPredict;
         float* scratch = (slot >= 0 ? d_stash + static_cast<long long>(slot) * stash_stride : d_replay) + pred_off;
         const uint64_t sk = slot >= 0 ? GB::key(GB::kPred, static_cast<uint64_t>(slot)) : GB::key(GB::kReplay, 0);
         const float* X = d_xc + u * static_cast<size_t>(B) * static_cast<size_t>(F);
@@ -1064,6 +1123,7 @@ struct ferret_trainer {
 
     void launch_stage_forward(int j, const float* slot, float* stash_u, const float* x0, const std::vector<uint64_t>& reads,
                               uint64_t stash_key) {
+        gb->cur_category = kCatForward;
         const StageDev& s = stages[static_cast<size_t>(j)];
         for (int l = s.lo; l < s.hi; ++l) {
             const LayerDev& ld = layers[static_cast<size_t>(l)];
@@ -1076,6 +1136,7 @@ struct ferret_trainer {
     // ReLU mask of the layer below applied on write (learner.hpp:443-476).
     void launch_stage_backward(int j, const float* slot, float* stash_u, const int* lab, int scratch,
                                const std::vector<uint64_t>& reads, uint64_t stash_key) {
+        gb->cur_category = kCatBackward;
         const StageDev& s = stages[static_cast<size_t>(j)];
         if (j == P - 1) emit_delta_head(stash_u, lab, nullptr, 1.0f / static_cast<float>(B), {}, stash_key);
         for (int l = s.hi - 1; l >= s.lo; --l) {
@@ -1130,6 +1191,7 @@ struct ferret_trainer {
         using GB = GraphBuilder;
         for (int j = 0; j < P; ++j) note_push(j);
         if (!DRY) {
+            gb->cur_category = kCatReplay;
             const uint64_t rk = GB::key(GB::kReplay, 0), pk = GB::key(GB::kPool, 0);
             std::vector<uint64_t> live_slots;
             for (int j = 0; j < P; ++j) live_slots.push_back(vslot(j, rel[static_cast<size_t>(j)]));
@@ -1411,6 +1473,46 @@ ferret_status ferret_trainer_set_timing(ferret_trainer* t, int32_t enable) {
     return guarded([&] {
         cuda_check(cudaStreamSynchronize(t->stream), "sync");
         t->timing = enable != 0;
+    });
+}
+
+ferret_status ferret_trainer_set_profiling(ferret_trainer* t, int32_t enable) {
+    return guarded([&] {
+        cuda_check(cudaStreamSynchronize(t->stream), "sync");
+        t->profiling = enable != 0;
+        if (t->profiling) t->timing = false;
+    });
+}
+
+ferret_status ferret_trainer_profile(ferret_trainer* t, double* class_ms, uint64_t* class_nodes, int32_t n_classes,
+                                     double* critical_ms, double* serial_ms) {
+    return guarded([&] {
+        if (!t->graph_profiling) fail(FERRET_E_LOGIC, "profile: the last execute() did not run a profiling graph");
+        cuda_check(cudaStreamSynchronize(t->stream), "sync");
+        const size_t n = t->prof_cat.size();
+        std::vector<double> dur(n, 0.0), finish(n, 0.0);
+        for (int c = 0; c < n_classes; ++c) {
+            class_ms[c] = 0.0;
+            class_nodes[c] = 0;
+        }
+        double total = 0.0, crit = 0.0;
+        for (size_t i = 0; i < n; ++i) {
+            float ms = 0.f;
+            cuda_check(cudaEventElapsedTime(&ms, t->prof_events[2 * i], t->prof_events[2 * i + 1]), "cudaEventElapsedTime");
+            dur[i] = ms;
+            total += ms;
+            const int c = t->prof_cat[i];
+            if (c < n_classes) {
+                class_ms[c] += ms;
+                class_nodes[c] += 1;
+            }
+            double start = 0.0;
+            for (int d : t->prof_ldeps[i]) start = std::max(start, finish[static_cast<size_t>(d)]);
+            finish[i] = start + ms;
+            crit = std::max(crit, finish[i]);
+        }
+        *critical_ms = crit;
+        *serial_ms = total;
     });
 }
 

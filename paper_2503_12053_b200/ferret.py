@@ -132,6 +132,8 @@ def lib() -> C.CDLL:
         "ferret_trainer_destroy": (None, [C.c_void_p]),
         "ferret_trainer_set_timing": (C.c_int, [C.c_void_p, C.c_int32]),
         "ferret_trainer_update_timing": (C.c_int, [C.c_void_p, P(D), P(C.c_uint64), P(D)]),
+        "ferret_trainer_set_profiling": (C.c_int, [C.c_void_p, C.c_int32]),
+        "ferret_trainer_profile": (C.c_int, [C.c_void_p, P(D), P(C.c_uint64), C.c_int32, P(D), P(D)]),
         "ferret_compensate": (C.c_int, [C.c_int32, P(D), P(P(D)), C.c_int32, P(D), P(D), P(D), P(D), C.c_size_t,
                                         D, D, D, D, P(D)]),
     }
@@ -392,6 +394,22 @@ class PipelineTrainer:
         ms, n, b = C.c_double(), C.c_uint64(), C.c_double()
         _check(lib().ferret_trainer_update_timing(self._h, C.byref(ms), C.byref(n), C.byref(b)))
         return ms.value, int(n.value), b.value
+
+    PROFILE_CLASSES = ("normalize", "predict", "forward", "backward", "update", "replay", "other")
+
+    def set_profiling(self, enable: bool) -> None:
+        _check(lib().ferret_trainer_set_profiling(self._h, int(enable)))
+
+    def profile(self) -> dict:
+        """Per node class device ms / node count, serial total and DAG critical path of the
+        last execute() (which must have run with set_profiling(True))."""
+        n = len(self.PROFILE_CLASSES)
+        ms = (C.c_double * n)()
+        cnt = (C.c_uint64 * n)()
+        crit, tot = C.c_double(), C.c_double()
+        _check(lib().ferret_trainer_profile(self._h, ms, cnt, n, C.byref(crit), C.byref(tot)))
+        return {"classes": {k: {"ms": ms[i], "nodes": int(cnt[i])} for i, k in enumerate(self.PROFILE_CLASSES)},
+                "critical_path_ms": crit.value, "serial_ms": tot.value}
 
     def close(self) -> None:
         if getattr(self, "_h", None):
