@@ -213,7 +213,7 @@ constexpr int kBwdMaxRows = 512;   // rows per split (delta staging in smem)
 template <int BT, int V>
 __global__ void __launch_bounds__(kThreads) bwd_kernel(const BwdArgs a) {
     __shared__ float sd[BT][kBwdMaxRows];
-    __shared__ float sacc[BT][32 * V];
+    extern __shared__ float wpart[];  // [kWarps][BT][32 * V] per-warp partials (dynamic)
     __shared__ bool last_cta;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int splits = gridDim.y;
@@ -225,7 +225,6 @@ __global__ void __launch_bounds__(kThreads) bwd_kernel(const BwdArgs a) {
         const int b = i / rows_per, rr = i % rows_per;
         sd[b][rr] = (b < B && rs + rr < re) ? a.d_out[(size_t)b * a.out + rs + rr] : 0.f;
     }
-    for (int i = threadIdx.x; i < BT * 32 * V; i += kThreads) sacc[i / (32 * V)][i % (32 * V)] = 0.f;
     __syncthreads();
     float acc[BT][V];
 #pragma unroll
@@ -274,22 +273,26 @@ __global__ void __launch_bounds__(kThreads) bwd_kernel(const BwdArgs a) {
             }
         }
     }
-    // fixed-order cross-warp sum
-    for (int q = 0; q < kWarps; ++q) {
-        if (warp == q) {
+    // cross-warp sum: every warp parks its partials, one barrier, then each
+    // thread sums its (sample, column) pairs over the warps in warp order
+    constexpr int TC = 32 * V;
 #pragma unroll
-            for (int b = 0; b < BT; ++b)
+    for (int b = 0; b < BT; ++b)
 #pragma unroll
-                for (int v = 0; v < V; ++v) sacc[b][lane * V + v] += acc[b][v];
-        }
-        __syncthreads();
-    }
+        for (int v = 0; v < V; ++v) wpart[(warp * BT + b) * TC + lane * V + v] = acc[b][v];
+    __syncthreads();
+    auto sacc_at = [&](int b, int cc) {
+        float s = 0.f;
+#pragma unroll
+        for (int q = 0; q < kWarps; ++q) s += wpart[(q * BT + b) * TC + cc];
+        return s;
+    };
     const int tile0 = blockIdx.x * 32 * V;
     if (splits == 1) {
         for (int i = threadIdx.x; i < B * 32 * V; i += kThreads) {
             const int b = i / (32 * V), cc = i % (32 * V), c = tile0 + cc;
             if (c >= a.in) continue;
-            float val = sacc[b][cc];
+            float val = sacc_at(b, cc);
             if (a.mask && !(a.mask[(size_t)b * a.in + c] > 0.f)) val = 0.f;
             a.d_in[(size_t)b * a.in + c] = val;
         }
@@ -297,7 +300,7 @@ __global__ void __launch_bounds__(kThreads) bwd_kernel(const BwdArgs a) {
     }
     for (int i = threadIdx.x; i < B * 32 * V; i += kThreads) {
         const int b = i / (32 * V), cc = i % (32 * V), c = tile0 + cc;
-        if (c < a.in) a.partial[((size_t)blockIdx.y * B + b) * a.in + c] = sacc[b][cc];
+        if (c < a.in) a.partial[((size_t)blockIdx.y * B + b) * a.in + c] = sacc_at(b, cc);
     }
     __threadfence();
     __syncthreads();
@@ -509,6 +512,91 @@ __global__ void __launch_bounds__(kThreads) update_tile_kernel(const UpdArgs a) 
     for (int i = 0; i < R; ++i) apply((size_t)sg.elem0 + (size_t)(t.r0 + i) * sg.in + c, i, c);
 }
 
+// ---------------------------------------------------------------------------
+// iter_fisher with one pending gradient (accumulation count 1, the default
+// config): the chain is versions 0..NV-1 of the launch's table, so the fold
+// length is a compile-time constant and every loop is straight-line code.
+// One parameter per thread; the unit's B input values of the thread's column
+// stay in registers across the tile's rows; deltas are broadcast from smem.
+// ---------------------------------------------------------------------------
+template <int BT, int NV>
+__global__ void __launch_bounds__(kThreads) update_iter1_kernel(const UpdArgs a) {
+    __shared__ float sdel[kMaxBatch * kUpdMaxTileRows];
+    const UpdTile t = a.tiles[blockIdx.x];
+    const UpdSeg sg = a.segs[t.seg];
+    const int B = a.B, R = t.nrows, tid = threadIdx.x;
+    const bool learn = a.eta > 0.f && a.v_r != nullptr;
+    const UpdPending& pk = a.pend[0];
+    const float one_m_a = 1.f - a.alpha;
+    auto fold = [&](size_t e, float g) {
+        float cv[NV];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) cv[i] = __ldg(a.vers[i] + e);
+        float ld = a.lam_d[e];
+        float lam = a.lambda0 + ld;
+        if (NV >= 2 && learn) {  // compensate.hpp:87-98
+            float vr = a.v_r[e], va = a.v_a[e];
+            const float dv = one_m_a * (g - vr);
+            const float resid = dv - lam * va;
+            const float grad_l = -2.f * resid * va + 2.f * a.nu * lam;
+            ld -= a.eta * grad_l;
+            lam = a.lambda0 + ld;
+            vr = a.alpha * vr + one_m_a * g;
+            va = a.alpha * va + one_m_a * g * g * (cv[NV >= 2 ? 1 : 0] - cv[0]);
+            a.v_r[e] = vr;
+            a.v_a[e] = va;
+            a.lam_d[e] = ld;
+        }
+        float o = g;  // compensate.hpp:99-102
+#pragma unroll
+        for (int s = 0; s + 1 < NV; ++s) o += lam * o * o * (cv[s + 1] - cv[s]);
+        a.dst[e] = cv[NV - 1] - a.step * o;
+    };
+    if (sg.bias) {
+        if (tid >= R) return;
+        const int r = t.r0 + tid;
+        const float* dl = pk.stash + sg.dlt_off + r;
+        float g = 0.f;
+#pragma unroll
+        for (int b = 0; b < BT; ++b)
+            if (b < B) g += __ldg(dl + (size_t)b * sg.out);
+        fold((size_t)sg.elem0 + r, g);
+        return;
+    }
+    for (int i = tid; i < B * R; i += kThreads) {
+        const int b = i / R, rr = i - b * R;
+        sdel[i] = __ldg(pk.stash + sg.dlt_off + (size_t)b * sg.out + t.r0 + rr);
+    }
+    __syncthreads();
+    const int c = t.c0 + tid;
+    if (c >= sg.in) return;
+    float xv[BT];
+#pragma unroll
+    for (int b = 0; b < BT; ++b) {
+        const float* xr = sg.xin_off >= 0 ? pk.stash + sg.xin_off + (size_t)b * sg.in
+                          : a.x0idx       ? pk.x0 + (size_t)__ldg(a.x0idx + b) * a.x0_ld
+                                          : pk.x0 + (size_t)b * a.x0_ld;
+        xv[b] = b < B ? __ldg(xr + c) : 0.f;
+    }
+    for (int i = 0; i < R; ++i) {
+        float g = 0.f;
+#pragma unroll
+        for (int b = 0; b < BT; ++b) g = fmaf(sdel[b * R + i], xv[b], g);
+        fold((size_t)sg.elem0 + (size_t)(t.r0 + i) * sg.in + c, g);
+    }
+}
+
+template <int BT>
+const void* iter1_func(int nv) {
+    switch (nv) {
+#define FB_NV(n) case n: return reinterpret_cast<const void*>(&update_iter1_kernel<BT, n>);
+        FB_NV(1) FB_NV(2) FB_NV(3) FB_NV(4) FB_NV(5) FB_NV(6) FB_NV(7) FB_NV(8)
+        FB_NV(9) FB_NV(10) FB_NV(11) FB_NV(12) FB_NV(13) FB_NV(14) FB_NV(15) FB_NV(16)
+#undef FB_NV
+        default: return nullptr;
+    }
+}
+
 template <int POLICY>
 const void* update_func(int B) {
     if (B <= 1) return reinterpret_cast<const void*>(&update_tile_kernel<POLICY, 1>);
@@ -612,21 +700,41 @@ int bwd_row_splits(int in, int out) {
     return splits < 1 ? 1 : splits;
 }
 
+template <int BT, int V>
+static const void* bwd_func_v(size_t& smem) {
+    smem = sizeof(float) * kWarps * BT * 32 * V;
+    static bool configured = false;  // > 48 KB dynamic smem needs an opt-in per function
+    if (!configured) {
+        cudaFuncSetAttribute(reinterpret_cast<const void*>(&bwd_kernel<BT, V>), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        configured = true;
+    }
+    return reinterpret_cast<const void*>(&bwd_kernel<BT, V>);
+}
+
 template <int BT>
-static const void* bwd_func(bool vec) {
-    return vec ? reinterpret_cast<const void*>(&bwd_kernel<BT, 4>) : reinterpret_cast<const void*>(&bwd_kernel<BT, 1>);
+static const void* bwd_func(bool vec, size_t& smem) {
+    return vec ? bwd_func_v<BT, 4>(smem) : bwd_func_v<BT, 1>(smem);
 }
 
 void spec_bwd(const BwdArgs& a, KernelSpec& k) {
     const dim3 grid(bwd_col_tiles(a.in), a.row_splits);
     const bool vec = bwd_vec(a.in) == 4 && aligned16(a.W);
-    const void* f = a.B <= 1 ? bwd_func<1>(vec) : a.B <= 2 ? bwd_func<2>(vec) : a.B <= 4 ? bwd_func<4>(vec)
-                  : a.B <= 8 ? bwd_func<8>(vec) : bwd_func<16>(vec);
+    size_t smem = 0;
+    const void* f = a.B <= 1 ? bwd_func<1>(vec, smem) : a.B <= 2 ? bwd_func<2>(vec, smem) : a.B <= 4 ? bwd_func<4>(vec, smem)
+                  : a.B <= 8 ? bwd_func<8>(vec, smem) : bwd_func<16>(vec, smem);
     fill(k, f, grid, dim3(kThreads), a);
+    k.smem = smem;
 }
 
 void spec_update(const UpdArgs& a, KernelSpec& k) {
     const long long blocks = a.n_tiles;
+    if (a.policy == 4 && a.K == 1 && a.nv <= 16 && a.lam_d != nullptr) {
+        const void* f = a.B <= 1 ? iter1_func<1>(a.nv) : a.B <= 2 ? iter1_func<2>(a.nv) : a.B <= 4 ? iter1_func<4>(a.nv)
+                      : a.B <= 8 ? iter1_func<8>(a.nv) : iter1_func<16>(a.nv);
+        fill(k, f, dim3((unsigned)blocks), dim3(kThreads), a);
+        return;
+    }
     const void* f = a.policy == 0 ? update_func<0>(a.B) : a.policy == 1 ? update_func<1>(a.B)
                   : a.policy == 2 ? update_func<2>(a.B) : a.policy == 3 ? update_func<3>(a.B) : update_func<4>(a.B);
     fill(k, f, dim3((unsigned)blocks), dim3(kThreads), a);
