@@ -44,7 +44,7 @@ BOUNDS = [0, 1, 2, 3, 4]
 MICRO_BATCH = 16
 UNITS = 256            # pipeline units per step (x16 samples)
 POLICY = "iter_fisher"
-CPU_UNITS = 24          # bounded CPU sample: 24 units x 16 samples
+CPU_UNITS = 512         # bounded CPU sample (~10 s of reference work): 512 units x 16 samples
 
 
 def _peaks():
@@ -134,7 +134,7 @@ def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    units = max(4, CPU_UNITS // 2)
+    units = 64  # per step: 64 units x 16 samples (~1 s of reference work)
     value, tot, chunk = cpu_reference(units, args.steps, args.warmup)
     sample = f"{units} units x {MICRO_BATCH} samples = {chunk} samples per step, {args.steps} timed steps"
     line = {"impl": "reference", "metric": "stream samples/sec", "value": value, "unit": "samples/s",
