@@ -234,11 +234,13 @@ FERRET_API ferret_status ferret_trainer_set_timing(ferret_trainer* t, int32_t en
 /* Profile mode (no reference counterpart): the next execute() runs the chunk
  * graph serialised with an event pair around every node. profile() returns per
  * node class {normalize, predict, forward, backward, update, replay, other}
- * the summed device time and node count, the serial total, and the critical
+ * the summed device time, node count and algorithmic HBM bytes,
+ * the serial total, and the critical
  * path of the concurrent DAG computed from the measured node times. */
 FERRET_API ferret_status ferret_trainer_set_profiling(ferret_trainer* t, int32_t enable);
 FERRET_API ferret_status ferret_trainer_profile(ferret_trainer* t, double* class_ms, uint64_t* class_nodes,
-                                                int32_t n_classes, double* critical_ms, double* serial_ms);
+                                                double* class_bytes, int32_t n_classes, double* critical_ms,
+                                                double* serial_ms);
 FERRET_API ferret_status ferret_trainer_update_timing(ferret_trainer* t, double* total_ms, uint64_t* launches,
                                                       double* alg_bytes);
 

@@ -160,6 +160,8 @@ struct GraphBuilder {
     std::vector<std::vector<int>> ldeps;
     std::vector<int> category;
     int cur_category = 0;
+    double cur_bytes = 0.0;       // algorithmic HBM bytes of the next node (set by the emitter)
+    std::vector<double> bytes;
     struct Res {
         int writer = -1;
         std::vector<int> readers;
@@ -219,6 +221,8 @@ struct GraphBuilder {
         nodes.push_back(n);
         ldeps.push_back(ld);
         category.push_back(cur_category);
+        bytes.push_back(cur_bytes);
+        cur_bytes = 0.0;
         last = n;
         if (serial && prof_events) {  // event after the node
             cudaGraphNode_t e;
@@ -354,6 +358,7 @@ struct ferret_trainer {
     std::vector<cudaEvent_t> prof_events;
     std::vector<std::vector<int>> prof_ldeps;
     std::vector<int> prof_cat;
+    std::vector<double> prof_bytes;
 
     // optional per-launch timing of the update kernel (event record nodes)
     bool timing = false;
@@ -827,6 +832,7 @@ struct ferret_trainer {
         launches = builder.kernels;
         prof_ldeps = std::move(builder.ldeps);
         prof_cat = std::move(builder.category);
+        prof_bytes = std::move(builder.bytes);
         graph_profiling = profiling;
         graph_shape = got;
         graph_timing = timing;
@@ -901,6 +907,7 @@ struct ferret_trainer {
                                    d_xc + s0 * static_cast<size_t>(F)};
                 fb200::KernelSpec k;
                 fb200::spec_normalize(na, k);
+                gb->cur_bytes = 20.0 * static_cast<double>(ns) * F;  // raw fp64 in, fp32 out, + state
                 gb->cur_category = kCatNorm;
                 gb->kernel(k, {}, {GB::key(GB::kNorm, g), GB::key(GB::kNormState, 0)});
             }
@@ -932,6 +939,7 @@ struct ferret_trainer {
                                                ctl_pool_dst() + u * static_cast<size_t>(B), d_pool_x, d_pool_lab, B, F};
                             fb200::KernelSpec k;
                             fb200::spec_pool(pa, k);
+                            gb->cur_bytes = 8.0 * B * F;
                             gb->cur_category = kCatOther;
                             gb->kernel(k, {ngroup(u)}, {GB::key(GB::kPool, 0)});
                         }
@@ -991,6 +999,7 @@ struct ferret_trainer {
                         a.step = static_cast<float>(opt.lr * (1.0 / static_cast<double>(pl.size())));
                         fb200::KernelSpec k;
                         fb200::spec_update(a, k);
+                        gb->cur_bytes = update_bytes(j, opt.policy, reads, cur);
                         time_begin();
                         gb->cur_category = kCatUpdate;
                         gb->kernel(k, rk, {vslot(j, cur + 1), GB::key(GB::kState, static_cast<uint64_t>(j))});
@@ -1027,6 +1036,7 @@ struct ferret_trainer {
                 const long long fin = rel[static_cast<size_t>(j)] % s.depth;
                 if (fin != 0)
                     gb->cur_category = kCatOther;
+                    gb->cur_bytes = 8.0 * static_cast<double>(s.slot_floats);
                     gb->copy(s.ring, s.slot(fin), static_cast<size_t>(s.slot_floats) * sizeof(float), {vslot(j, fin)},
                              {vslot(j, 0)});
             }
@@ -1091,6 +1101,7 @@ struct ferret_trainer {
         a.relu = ld.act == FERRET_ACT_RELU;
         fb200::KernelSpec k;
         fb200::spec_fwd(a, k);
+        gb->cur_bytes = 4.0 * ld.in * ld.out + 4.0 * ld.out + 4.0 * B * (ld.in + ld.out);  // W, b, X, Y
         gb->kernel(k, reads, writes);
     }
 
@@ -1118,6 +1129,7 @@ struct ferret_trainer {
         h.pred = d_predc + u * static_cast<size_t>(B);
         fb200::KernelSpec k;
         fb200::spec_head(h, k);
+        gb->cur_bytes = 4.0 * B * n_out + 4.0 * B;
         gb->kernel(k, {}, {sk});
     }
 
@@ -1159,6 +1171,7 @@ struct ferret_trainer {
         h.scale = scale;
         fb200::KernelSpec k;
         fb200::spec_head(h, k);
+        gb->cur_bytes = 8.0 * B * n_out;
         gb->kernel(k, reads, {stash_key});
     }
 
@@ -1179,6 +1192,7 @@ struct ferret_trainer {
         a.counters = d_counters + static_cast<size_t>(scratch) * max_tiles;
         fb200::KernelSpec k;
         fb200::spec_bwd(a, k);
+        gb->cur_bytes = 4.0 * ld.in * ld.out + 4.0 * B * (ld.out + 2.0 * ld.in);  // W, delta_out, mask, delta_in
         gb->kernel(k, reads, {stash_key});
     }
 
@@ -1223,6 +1237,7 @@ struct ferret_trainer {
                 a.step = static_cast<float>(opt.lr);
                 fb200::KernelSpec k;
                 fb200::spec_update(a, k);
+                gb->cur_bytes = update_bytes(j, FERRET_POLICY_NONE, {cur}, cur);
                 gb->kernel(k, {rk, pk, vslot(j, cur)}, {vslot(j, cur + 1)});
             }
         }
@@ -1484,8 +1499,8 @@ ferret_status ferret_trainer_set_profiling(ferret_trainer* t, int32_t enable) {
     });
 }
 
-ferret_status ferret_trainer_profile(ferret_trainer* t, double* class_ms, uint64_t* class_nodes, int32_t n_classes,
-                                     double* critical_ms, double* serial_ms) {
+ferret_status ferret_trainer_profile(ferret_trainer* t, double* class_ms, uint64_t* class_nodes, double* class_bytes,
+                                     int32_t n_classes, double* critical_ms, double* serial_ms) {
     return guarded([&] {
         if (!t->graph_profiling) fail(FERRET_E_LOGIC, "profile: the last execute() did not run a profiling graph");
         cuda_check(cudaStreamSynchronize(t->stream), "sync");
@@ -1494,6 +1509,7 @@ ferret_status ferret_trainer_profile(ferret_trainer* t, double* class_ms, uint64
         for (int c = 0; c < n_classes; ++c) {
             class_ms[c] = 0.0;
             class_nodes[c] = 0;
+            class_bytes[c] = 0.0;
         }
         double total = 0.0, crit = 0.0;
         for (size_t i = 0; i < n; ++i) {
@@ -1505,6 +1521,7 @@ ferret_status ferret_trainer_profile(ferret_trainer* t, double* class_ms, uint64
             if (c < n_classes) {
                 class_ms[c] += ms;
                 class_nodes[c] += 1;
+                class_bytes[c] += t->prof_bytes[i];
             }
             double start = 0.0;
             for (int d : t->prof_ldeps[i]) start = std::max(start, finish[static_cast<size_t>(d)]);

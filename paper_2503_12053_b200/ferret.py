@@ -133,7 +133,7 @@ def lib() -> C.CDLL:
         "ferret_trainer_set_timing": (C.c_int, [C.c_void_p, C.c_int32]),
         "ferret_trainer_update_timing": (C.c_int, [C.c_void_p, P(D), P(C.c_uint64), P(D)]),
         "ferret_trainer_set_profiling": (C.c_int, [C.c_void_p, C.c_int32]),
-        "ferret_trainer_profile": (C.c_int, [C.c_void_p, P(D), P(C.c_uint64), C.c_int32, P(D), P(D)]),
+        "ferret_trainer_profile": (C.c_int, [C.c_void_p, P(D), P(C.c_uint64), P(D), C.c_int32, P(D), P(D)]),
         "ferret_compensate": (C.c_int, [C.c_int32, P(D), P(P(D)), C.c_int32, P(D), P(D), P(D), P(D), C.c_size_t,
                                         D, D, D, D, P(D)]),
     }
@@ -406,9 +406,12 @@ class PipelineTrainer:
         n = len(self.PROFILE_CLASSES)
         ms = (C.c_double * n)()
         cnt = (C.c_uint64 * n)()
+        byt = (C.c_double * n)()
         crit, tot = C.c_double(), C.c_double()
-        _check(lib().ferret_trainer_profile(self._h, ms, cnt, n, C.byref(crit), C.byref(tot)))
-        return {"classes": {k: {"ms": ms[i], "nodes": int(cnt[i])} for i, k in enumerate(self.PROFILE_CLASSES)},
+        _check(lib().ferret_trainer_profile(self._h, ms, cnt, byt, n, C.byref(crit), C.byref(tot)))
+        return {"classes": {k: {"ms": ms[i], "nodes": int(cnt[i]), "alg_bytes": byt[i],
+                                "gbs": (byt[i] / (ms[i] * 1e-3) / 1e9) if ms[i] > 0 else 0.0}
+                            for i, k in enumerate(self.PROFILE_CLASSES)},
                 "critical_path_ms": crit.value, "serial_ms": tot.value}
 
     def close(self) -> None:
