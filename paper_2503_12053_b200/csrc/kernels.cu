@@ -71,56 +71,63 @@ __global__ void __launch_bounds__(kThreads) fwd_kernel(const FwdArgs a, int nwk)
     const int kc = (nk + nwk - 1) / nwk;
     const int k_lo = kw * kc, k_hi = min(nk, k_lo + kc);
     const int B = a.B;
-    const float* xr[BT];
-#pragma unroll
-    for (int b = 0; b < BT; ++b)
-        xr[b] = a.X + (size_t)(b < B ? (a.xidx ? __ldg(a.xidx + b) : b) : 0) * a.in;
+    // input row b starts at X + xrow(b) * in (replay gathers rows from the pool)
+    auto xrow = [&](int b) -> size_t { return (size_t)(a.xidx ? __ldg(a.xidx + b) : b) * a.in; };
     float acc[RW][BT];
 #pragma unroll
     for (int i = 0; i < RW; ++i)
 #pragma unroll
         for (int b = 0; b < BT; ++b) acc[i][b] = 0.f;
     if (r0 < a.out) {
+        // RW weight rows stay in registers while the B input rows stream past:
+        // each input load is reused RW times, each weight load B times
         for (int k = k_lo + lane; k < k_hi; k += 32) {
             if (VEC) {
-                float4 xv[BT];
+                float4 w[RW];
 #pragma unroll
-                for (int b = 0; b < BT; ++b)
-                    xv[b] = b < B ? __ldg(reinterpret_cast<const float4*>(xr[b]) + k)
-                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int i = 0; i < RW; ++i)
+                    w[i] = r0 + i < a.out ? __ldg(reinterpret_cast<const float4*>(a.W + (size_t)(r0 + i) * a.in) + k)
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-                for (int i = 0; i < RW; ++i) {
-                    if (r0 + i >= a.out) break;
-                    const float4 w = __ldg(reinterpret_cast<const float4*>(a.W + (size_t)(r0 + i) * a.in) + k);
+                for (int b = 0; b < BT; ++b) {
+                    if (b >= B) break;
+                    const float4 x = __ldg(reinterpret_cast<const float4*>(a.X + xrow(b)) + k);
 #pragma unroll
-                    for (int b = 0; b < BT; ++b) {
-                        acc[i][b] = fmaf(w.x, xv[b].x, acc[i][b]);
-                        acc[i][b] = fmaf(w.y, xv[b].y, acc[i][b]);
-                        acc[i][b] = fmaf(w.z, xv[b].z, acc[i][b]);
-                        acc[i][b] = fmaf(w.w, xv[b].w, acc[i][b]);
+                    for (int i = 0; i < RW; ++i) {
+                        acc[i][b] = fmaf(w[i].x, x.x, acc[i][b]);
+                        acc[i][b] = fmaf(w[i].y, x.y, acc[i][b]);
+                        acc[i][b] = fmaf(w[i].z, x.z, acc[i][b]);
+                        acc[i][b] = fmaf(w[i].w, x.w, acc[i][b]);
                     }
                 }
             } else {
-                float xv[BT];
+                float w[RW];
 #pragma unroll
-                for (int b = 0; b < BT; ++b) xv[b] = b < B ? __ldg(xr[b] + k) : 0.f;
+                for (int i = 0; i < RW; ++i) w[i] = r0 + i < a.out ? __ldg(a.W + (size_t)(r0 + i) * a.in + k) : 0.f;
 #pragma unroll
-                for (int i = 0; i < RW; ++i) {
-                    if (r0 + i >= a.out) break;
-                    const float w = __ldg(a.W + (size_t)(r0 + i) * a.in + k);
+                for (int b = 0; b < BT; ++b) {
+                    if (b >= B) break;
+                    const float x = __ldg(a.X + xrow(b) + k);
 #pragma unroll
-                    for (int b = 0; b < BT; ++b) acc[i][b] = fmaf(w, xv[b], acc[i][b]);
+                    for (int i = 0; i < RW; ++i) acc[i][b] = fmaf(w[i], x, acc[i][b]);
                 }
             }
         }
     }
-    float flat[NV];
+    // transpose-reduce in chunks of 32 values: lane L ends with value c*32 + L
+    constexpr int NC = NV > 32 ? NV / 32 : 1;
+    constexpr int NW = NV > 32 ? 32 : NV;
 #pragma unroll
-    for (int i = 0; i < RW; ++i)
+    for (int c = 0; c < NC; ++c) {
+        float flat[NW];
 #pragma unroll
-        for (int b = 0; b < BT; ++b) flat[i * BT + b] = acc[i][b];
-    const float s = warp_transpose_sum<NV>(flat, lane);
-    if (lane < NV) part[warp][lane] = s;
+        for (int q = 0; q < NW; ++q) {
+            const int idx = c * NW + q;
+            flat[q] = acc[idx / BT][idx % BT];
+        }
+        const float s = warp_transpose_sum<NW>(flat, lane);
+        if (lane < NW) part[warp][c * NW + lane] = s;
+    }
     __syncthreads();
     for (int t = threadIdx.x; t < groups * NV; t += kThreads) {
         const int gg = t / NV, idx = t % NV;
@@ -212,7 +219,8 @@ constexpr int kBwdMaxRows = 512;   // rows per split (delta staging in smem)
 
 template <int BT, int V>
 __global__ void __launch_bounds__(kThreads) bwd_kernel(const BwdArgs a) {
-    __shared__ float sd[BT][kBwdMaxRows];
+    // deltas as [row][sample]: one row's B values are read as float4s
+    __shared__ __align__(16) float sd[kBwdMaxRows][BT];
     extern __shared__ float wpart[];  // [kWarps][BT][32 * V] per-warp partials (dynamic)
     __shared__ bool last_cta;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -223,9 +231,32 @@ __global__ void __launch_bounds__(kThreads) bwd_kernel(const BwdArgs a) {
     const int c0 = blockIdx.x * 32 * V + lane * V;
     for (int i = threadIdx.x; i < BT * rows_per; i += kThreads) {
         const int b = i / rows_per, rr = i % rows_per;
-        sd[b][rr] = (b < B && rs + rr < re) ? a.d_out[(size_t)b * a.out + rs + rr] : 0.f;
+        sd[rr][b] = (b < B && rs + rr < re) ? a.d_out[(size_t)b * a.out + rs + rr] : 0.f;
     }
     __syncthreads();
+    // acc[b][v] += w[v] * delta(row, b), delta read 4 samples at a time
+    auto row_fma = [&](const float (&w)[V], int rr, float (&acc)[BT][V]) {
+        if (BT % 4 == 0) {
+#pragma unroll
+            for (int b = 0; b < BT; b += 4) {
+                const float4 d = *reinterpret_cast<const float4*>(&sd[rr][b]);
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    acc[b][v] = fmaf(w[v], d.x, acc[b][v]);
+                    acc[(b + 1) % BT][v] = fmaf(w[v], d.y, acc[(b + 1) % BT][v]);
+                    acc[(b + 2) % BT][v] = fmaf(w[v], d.z, acc[(b + 2) % BT][v]);
+                    acc[(b + 3) % BT][v] = fmaf(w[v], d.w, acc[(b + 3) % BT][v]);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int b = 0; b < BT; ++b) {
+                const float d = sd[rr][b];
+#pragma unroll
+                for (int v = 0; v < V; ++v) acc[b][v] = fmaf(w[v], d, acc[b][v]);
+            }
+        }
+    };
     float acc[BT][V];
 #pragma unroll
     for (int b = 0; b < BT; ++b)
@@ -249,13 +280,7 @@ __global__ void __launch_bounds__(kThreads) bwd_kernel(const BwdArgs a) {
                 }
             }
 #pragma unroll
-            for (int q = 0; q < RU; ++q)
-#pragma unroll
-                for (int b = 0; b < BT; ++b) {
-                    const float d = sd[b][r + q * kWarps - rs];
-#pragma unroll
-                    for (int v = 0; v < V; ++v) acc[b][v] = fmaf(w[q][v], d, acc[b][v]);
-                }
+            for (int q = 0; q < RU; ++q) row_fma(w[q], r + q * kWarps - rs, acc);
         }
         for (; r < re; r += kWarps) {
             float w[V];
@@ -265,12 +290,7 @@ __global__ void __launch_bounds__(kThreads) bwd_kernel(const BwdArgs a) {
             } else {
                 w[0] = __ldg(a.W + (size_t)r * a.in + c0);
             }
-#pragma unroll
-            for (int b = 0; b < BT; ++b) {
-                const float d = sd[b][r - rs];
-#pragma unroll
-                for (int v = 0; v < V; ++v) acc[b][v] = fmaf(w[v], d, acc[b][v]);
-            }
+            row_fma(w, r - rs, acc);
         }
     }
     // cross-warp sum: every warp parks its partials, one barrier, then each
@@ -676,7 +696,7 @@ void spec_fwd(const FwdArgs& a, KernelSpec& k) {
     else if (a.B <= 2) fwd_spec<2, 4>(a, vec, k);
     else if (a.B <= 4) fwd_spec<4, 4>(a, vec, k);
     else if (a.B <= 8) fwd_spec<8, 4>(a, vec, k);
-    else fwd_spec<16, 2>(a, vec, k);
+    else fwd_spec<16, 4>(a, vec, k);
 }
 
 void spec_head(const HeadArgs& a, KernelSpec& k) {
