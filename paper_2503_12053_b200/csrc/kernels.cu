@@ -696,6 +696,9 @@ void spec_fwd(const FwdArgs& a, KernelSpec& k) {
     else if (a.B <= 2) fwd_spec<2, 4>(a, vec, k);
     else if (a.B <= 4) fwd_spec<4, 4>(a, vec, k);
     else if (a.B <= 8) fwd_spec<8, 4>(a, vec, k);
+    // small layers are latency-bound: 2 rows per warp doubles the CTA count;
+    // wide layers reuse each input load across 4 weight rows
+    else if ((long long)a.out * a.in < (1 << 20)) fwd_spec<16, 2>(a, vec, k);
     else fwd_spec<16, 4>(a, vec, k);
 }
 
