@@ -71,8 +71,12 @@ __global__ void __launch_bounds__(kThreads) fwd_kernel(const FwdArgs a, int nwk)
     const int kc = (nk + nwk - 1) / nwk;
     const int k_lo = kw * kc, k_hi = min(nk, k_lo + kc);
     const int B = a.B;
-    // input row b starts at X + xrow(b) * in (replay gathers rows from the pool)
-    auto xrow = [&](int b) -> size_t { return (size_t)(a.xidx ? __ldg(a.xidx + b) : b) * a.in; };
+    // input row b starts at X + xrow(b) (replay gathers rows from the pool);
+    // offsets resolved once, before the K loop
+    size_t xo[BT];
+#pragma unroll
+    for (int b = 0; b < BT; ++b) xo[b] = (size_t)(b < B ? (a.xidx ? __ldg(a.xidx + b) : b) : 0) * a.in;
+    auto xrow = [&](int b) -> size_t { return xo[b]; };
     float acc[RW][BT];
 #pragma unroll
     for (int i = 0; i < RW; ++i)
