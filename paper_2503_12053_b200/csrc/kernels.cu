@@ -83,37 +83,37 @@ __global__ void __launch_bounds__(kThreads) fwd_kernel(const FwdArgs a, int nwk)
 #pragma unroll
         for (int b = 0; b < BT; ++b) acc[i][b] = 0.f;
     if (r0 < a.out) {
-        // RW weight rows stay in registers while the B input rows stream past:
-        // each input load is reused RW times, each weight load B times
+        // the B input values of this K position are loaded once and reused by
+        // the RW weight rows; each weight load is reused by the B samples
         for (int k = k_lo + lane; k < k_hi; k += 32) {
             if (VEC) {
-                float4 w[RW];
+                float4 xv[BT];
 #pragma unroll
-                for (int i = 0; i < RW; ++i)
-                    w[i] = r0 + i < a.out ? __ldg(reinterpret_cast<const float4*>(a.W + (size_t)(r0 + i) * a.in) + k)
-                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int b = 0; b < BT; ++b)
+                    xv[b] = b < B ? __ldg(reinterpret_cast<const float4*>(a.X + xrow(b)) + k)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-                for (int b = 0; b < BT; ++b) {
-                    if (b >= B) break;
-                    const float4 x = __ldg(reinterpret_cast<const float4*>(a.X + xrow(b)) + k);
+                for (int i = 0; i < RW; ++i) {
+                    if (r0 + i >= a.out) break;
+                    const float4 w = __ldg(reinterpret_cast<const float4*>(a.W + (size_t)(r0 + i) * a.in) + k);
 #pragma unroll
-                    for (int i = 0; i < RW; ++i) {
-                        acc[i][b] = fmaf(w[i].x, x.x, acc[i][b]);
-                        acc[i][b] = fmaf(w[i].y, x.y, acc[i][b]);
-                        acc[i][b] = fmaf(w[i].z, x.z, acc[i][b]);
-                        acc[i][b] = fmaf(w[i].w, x.w, acc[i][b]);
+                    for (int b = 0; b < BT; ++b) {
+                        acc[i][b] = fmaf(w.x, xv[b].x, acc[i][b]);
+                        acc[i][b] = fmaf(w.y, xv[b].y, acc[i][b]);
+                        acc[i][b] = fmaf(w.z, xv[b].z, acc[i][b]);
+                        acc[i][b] = fmaf(w.w, xv[b].w, acc[i][b]);
                     }
                 }
             } else {
-                float w[RW];
+                float xv[BT];
 #pragma unroll
-                for (int i = 0; i < RW; ++i) w[i] = r0 + i < a.out ? __ldg(a.W + (size_t)(r0 + i) * a.in + k) : 0.f;
+                for (int b = 0; b < BT; ++b) xv[b] = b < B ? __ldg(a.X + xrow(b) + k) : 0.f;
 #pragma unroll
-                for (int b = 0; b < BT; ++b) {
-                    if (b >= B) break;
-                    const float x = __ldg(a.X + xrow(b) + k);
+                for (int i = 0; i < RW; ++i) {
+                    if (r0 + i >= a.out) break;
+                    const float w = __ldg(a.W + (size_t)(r0 + i) * a.in + k);
 #pragma unroll
-                    for (int i = 0; i < RW; ++i) acc[i][b] = fmaf(w[i], x, acc[i][b]);
+                    for (int b = 0; b < BT; ++b) acc[i][b] = fmaf(w, xv[b], acc[i][b]);
                 }
             }
         }
@@ -700,10 +700,7 @@ void spec_fwd(const FwdArgs& a, KernelSpec& k) {
     else if (a.B <= 2) fwd_spec<2, 4>(a, vec, k);
     else if (a.B <= 4) fwd_spec<4, 4>(a, vec, k);
     else if (a.B <= 8) fwd_spec<8, 4>(a, vec, k);
-    // small layers are latency-bound: 2 rows per warp doubles the CTA count;
-    // wide layers reuse each input load across 4 weight rows
-    else if ((long long)a.out * a.in < (1 << 20)) fwd_spec<16, 2>(a, vec, k);
-    else fwd_spec<16, 4>(a, vec, k);
+    else fwd_spec<16, 2>(a, vec, k);
 }
 
 void spec_head(const HeadArgs& a, KernelSpec& k) {
