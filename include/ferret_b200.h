@@ -238,6 +238,11 @@ FERRET_API ferret_status ferret_trainer_set_timing(ferret_trainer* t, int32_t en
  * the serial total, and the critical
  * path of the concurrent DAG computed from the measured node times. */
 FERRET_API ferret_status ferret_trainer_set_profiling(ferret_trainer* t, int32_t enable);
+/* After a profiled execute(): mean device microseconds per processed unit of
+ * each stage's forward, backward and update work (the measured costs the
+ * planner's LayerProfile t_f / t_b stand for, profile.hpp / net.hpp:263). */
+FERRET_API ferret_status ferret_trainer_profile_stages(ferret_trainer* t, double* fwd_us, double* bwd_us,
+                                                       double* upd_us, int32_t n_stages);
 FERRET_API ferret_status ferret_trainer_profile(ferret_trainer* t, double* class_ms, uint64_t* class_nodes,
                                                 double* class_bytes, int32_t n_classes, double* critical_ms,
                                                 double* serial_ms);

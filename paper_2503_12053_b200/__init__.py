@@ -9,5 +9,5 @@ from .ferret import (  # noqa: F401
     BoundError, ConfigError, DeviceError, LogicError, SchemaError,
     PipelineTrainOptions, PipelineTrainer, Schedule, StreamSpec,
     compensate, device_available, lib, make_dense_net, online_accuracy, param_count,
-    profile_from_widths, synth_drift_stream, train_pipeline,
+    measure_profile, profile_from_widths, synth_drift_stream, train_pipeline,
 )

@@ -160,8 +160,10 @@ struct GraphBuilder {
     std::vector<std::vector<int>> ldeps;
     std::vector<int> category;
     int cur_category = 0;
+    int cur_stage = -1;           // pipeline stage the next node works for (-1: none)
     double cur_bytes = 0.0;       // algorithmic HBM bytes of the next node (set by the emitter)
     std::vector<double> bytes;
+    std::vector<int> stage_of;
     struct Res {
         int writer = -1;
         std::vector<int> readers;
@@ -222,6 +224,7 @@ struct GraphBuilder {
         ldeps.push_back(ld);
         category.push_back(cur_category);
         bytes.push_back(cur_bytes);
+        stage_of.push_back(cur_stage);
         cur_bytes = 0.0;
         last = n;
         if (serial && prof_events) {  // event after the node
@@ -359,6 +362,7 @@ struct ferret_trainer {
     std::vector<std::vector<int>> prof_ldeps;
     std::vector<int> prof_cat;
     std::vector<double> prof_bytes;
+    std::vector<int> prof_stage;
 
     // optional per-launch timing of the update kernel (event record nodes)
     bool timing = false;
@@ -833,6 +837,7 @@ struct ferret_trainer {
         prof_ldeps = std::move(builder.ldeps);
         prof_cat = std::move(builder.category);
         prof_bytes = std::move(builder.bytes);
+        prof_stage = std::move(builder.stage_of);
         graph_profiling = profiling;
         graph_shape = got;
         graph_timing = timing;
@@ -908,7 +913,7 @@ struct ferret_trainer {
                 fb200::KernelSpec k;
                 fb200::spec_normalize(na, k);
                 gb->cur_bytes = 20.0 * static_cast<double>(ns) * F;  // raw fp64 in, fp32 out, + state
-                gb->cur_category = kCatNorm;
+                gb->cur_category = kCatNorm; gb->cur_stage = -1;
                 gb->kernel(k, {}, {GB::key(GB::kNorm, g), GB::key(GB::kNormState, 0)});
             }
         }
@@ -940,7 +945,7 @@ struct ferret_trainer {
                             fb200::KernelSpec k;
                             fb200::spec_pool(pa, k);
                             gb->cur_bytes = 8.0 * B * F;
-                            gb->cur_category = kCatOther;
+                            gb->cur_category = kCatOther; gb->cur_stage = -1;
                             gb->kernel(k, {ngroup(u)}, {GB::key(GB::kPool, 0)});
                         }
                     }
@@ -1001,7 +1006,7 @@ struct ferret_trainer {
                         fb200::spec_update(a, k);
                         gb->cur_bytes = update_bytes(j, opt.policy, reads, cur);
                         time_begin();
-                        gb->cur_category = kCatUpdate;
+                        gb->cur_category = kCatUpdate; gb->cur_stage = j;
                         gb->kernel(k, rk, {vslot(j, cur + 1), GB::key(GB::kState, static_cast<uint64_t>(j))});
                         time_end(update_bytes(j, opt.policy, reads, cur));
                     }
@@ -1035,7 +1040,7 @@ struct ferret_trainer {
                 const StageDev& s = stages[static_cast<size_t>(j)];
                 const long long fin = rel[static_cast<size_t>(j)] % s.depth;
                 if (fin != 0)
-                    gb->cur_category = kCatOther;
+                    gb->cur_category = kCatOther; gb->cur_stage = -1;
                     gb->cur_bytes = 8.0 * static_cast<double>(s.slot_floats);
                     gb->copy(s.ring, s.slot(fin), static_cast<size_t>(s.slot_floats) * sizeof(float), {vslot(j, fin)},
                              {vslot(j, 0)});
@@ -1110,7 +1115,7 @@ struct ferret_trainer {
     // shipped there is no slot: the replay stash's scratch is used, serialised).
     void launch_predict(size_t u, const std::vector<long long>& rel, int slot, const std::vector<uint64_t>& reads) {
         using GB = GraphBuilder;
-        gb->cur_category = kCatPredict;
+        gb->cur_category = kCatPredict; gb->cur_stage = -1;
         float* scratch = (slot >= 0 ? d_stash + static_cast<long long>(slot) * stash_stride : d_replay) + pred_off;
         const uint64_t sk = slot >= 0 ? GB::key(GB::kPred, static_cast<uint64_t>(slot)) : GB::key(GB::kReplay, 0);
         const float* X = d_xc + u * static_cast<size_t>(B) * static_cast<size_t>(F);
@@ -1135,7 +1140,7 @@ struct ferret_trainer {
 
     void launch_stage_forward(int j, const float* slot, float* stash_u, const float* x0, const std::vector<uint64_t>& reads,
                               uint64_t stash_key) {
-        gb->cur_category = kCatForward;
+        gb->cur_category = kCatForward; gb->cur_stage = j;
         const StageDev& s = stages[static_cast<size_t>(j)];
         for (int l = s.lo; l < s.hi; ++l) {
             const LayerDev& ld = layers[static_cast<size_t>(l)];
@@ -1148,7 +1153,7 @@ struct ferret_trainer {
     // ReLU mask of the layer below applied on write (learner.hpp:443-476).
     void launch_stage_backward(int j, const float* slot, float* stash_u, const int* lab, int scratch,
                                const std::vector<uint64_t>& reads, uint64_t stash_key) {
-        gb->cur_category = kCatBackward;
+        gb->cur_category = kCatBackward; gb->cur_stage = j;
         const StageDev& s = stages[static_cast<size_t>(j)];
         if (j == P - 1) emit_delta_head(stash_u, lab, nullptr, 1.0f / static_cast<float>(B), {}, stash_key);
         for (int l = s.hi - 1; l >= s.lo; --l) {
@@ -1205,7 +1210,7 @@ struct ferret_trainer {
         using GB = GraphBuilder;
         for (int j = 0; j < P; ++j) note_push(j);
         if (!DRY) {
-            gb->cur_category = kCatReplay;
+            gb->cur_category = kCatReplay; gb->cur_stage = -1;
             const uint64_t rk = GB::key(GB::kReplay, 0), pk = GB::key(GB::kPool, 0);
             std::vector<uint64_t> live_slots;
             for (int j = 0; j < P; ++j) live_slots.push_back(vslot(j, rel[static_cast<size_t>(j)]));
@@ -1530,6 +1535,35 @@ ferret_status ferret_trainer_profile(ferret_trainer* t, double* class_ms, uint64
         }
         *critical_ms = crit;
         *serial_ms = total;
+    });
+}
+
+ferret_status ferret_trainer_profile_stages(ferret_trainer* t, double* fwd_us, double* bwd_us, double* upd_us,
+                                            int32_t n_stages) {
+    return guarded([&] {
+        if (!t->graph_profiling) fail(FERRET_E_LOGIC, "profile: the last execute() did not run a profiling graph");
+        if (n_stages != t->P) fail(FERRET_E_INVALID_ARG, "profile_stages: stage count mismatch");
+        cuda_check(cudaStreamSynchronize(t->stream), "sync");
+        // mean time of one forward / backward / update EVENT of each stage (an
+        // event may be several nodes: one per layer, plus the head)
+        std::vector<double> f(static_cast<size_t>(n_stages), 0.0), b(f), u(f);
+        for (size_t i = 0; i < t->prof_cat.size(); ++i) {
+            const int s = t->prof_stage[i];
+            if (s < 0 || s >= n_stages) continue;
+            float ms = 0.f;
+            cuda_check(cudaEventElapsedTime(&ms, t->prof_events[2 * i], t->prof_events[2 * i + 1]), "cudaEventElapsedTime");
+            const int c = t->prof_cat[i];
+            (c == kCatForward ? f : c == kCatBackward ? b : u)[static_cast<size_t>(s)] += 1e3 * ms;
+        }
+        const auto& st = t->stats;
+        for (int32_t s = 0; s < n_stages; ++s) {
+            // events per stage in the profiled chunk: updates counted, forwards /
+            // backwards ~ one per non-dropped unit
+            const double units = static_cast<double>(st.predicts > 0 ? st.predicts : 1);
+            fwd_us[s] = f[static_cast<size_t>(s)] / units;
+            bwd_us[s] = b[static_cast<size_t>(s)] / units;
+            upd_us[s] = u[static_cast<size_t>(s)] / units;
+        }
     });
 }
 

@@ -133,6 +133,7 @@ def lib() -> C.CDLL:
         "ferret_trainer_set_timing": (C.c_int, [C.c_void_p, C.c_int32]),
         "ferret_trainer_update_timing": (C.c_int, [C.c_void_p, P(D), P(C.c_uint64), P(D)]),
         "ferret_trainer_set_profiling": (C.c_int, [C.c_void_p, C.c_int32]),
+        "ferret_trainer_profile_stages": (C.c_int, [C.c_void_p, P(D), P(D), P(D), C.c_int32]),
         "ferret_trainer_profile": (C.c_int, [C.c_void_p, P(D), P(C.c_uint64), P(D), C.c_int32, P(D), P(D)]),
         "ferret_compensate": (C.c_int, [C.c_int32, P(D), P(P(D)), C.c_int32, P(D), P(D), P(D), P(D), C.c_size_t,
                                         D, D, D, D, P(D)]),
@@ -414,6 +415,13 @@ class PipelineTrainer:
                             for i, k in enumerate(self.PROFILE_CLASSES)},
                 "critical_path_ms": crit.value, "serial_ms": tot.value}
 
+    def profile_stages(self):
+        """(fwd_us, bwd_us, upd_us) per stage, per processed unit, of the last profiled execute()."""
+        P = len(self.bounds) - 1
+        f, b, u = (np.zeros(P) for _ in range(3))
+        _check(lib().ferret_trainer_profile_stages(self._h, _dp(f), _dp(b), _dp(u), P))
+        return f, b, u
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             lib().ferret_trainer_destroy(self._h)
@@ -450,4 +458,34 @@ def compensate(policy: str, g: np.ndarray, chain: Sequence[np.ndarray], lam=None
                                    _dp(v_r) if v_r is not None else nul, _dp(v_a) if v_a is not None else nul,
                                    _dp(mean_gap) if mean_gap is not None else nul, n, lambda0, alpha, eta_lambda, nu,
                                    _dp(out)))
+    return out
+
+
+def measure_profile(widths: Sequence[int], micro_batch: int = 1, policy: str = "iter_fisher", units: int = 48,
+                    device: int = 0) -> np.ndarray:
+    """B200 re-costing of profile_from_net (net.hpp:263-274): per layer, t_f = measured
+    device seconds of its forward and t_b = its backward + compensated update, from a
+    profiled one-layer-per-stage run of the actual kernels at this micro-batch. w and a
+    are the reference's counts. Feed the result to Schedule.plan(..., max_stages=#GPUs)."""
+    L = len(widths) - 1
+    prof = profile_from_widths(widths)
+    bounds = list(range(L + 1))
+    t_d = float(prof["t_f"].max())
+    sched = Schedule.forced(prof, t_d, StreamSpec(t_d=t_d, horizon=units * t_d), bounds, units)
+    chunk = units * micro_batch
+    feats, labels = synth_drift_stream(2 * chunk, widths[0], widths[-1], "split_tasks", 7)
+    tr = PipelineTrainer(widths, make_dense_net(widths, 1), bounds,
+                         PipelineTrainOptions(policy=policy, micro_batch=micro_batch, device=device))
+    try:
+        tr.load_stream(feats, labels)
+        tr.set_schedule(sched.events, chunk)
+        tr.execute(0)
+        tr.set_profiling(True)
+        tr.execute(1)
+        f, b, u = tr.profile_stages()
+    finally:
+        tr.close()
+    out = prof.copy()
+    out["t_f"] = np.maximum(f, 1e-3) * 1e-6
+    out["t_b"] = np.maximum(b + u, 1e-3) * 1e-6
     return out
