@@ -200,6 +200,24 @@ FERRET_API ferret_status ferret_trainer_sync(ferret_trainer* t);
 /* cudaStream_t the trainer launches on, as an opaque pointer (for CUDA-event timing) */
 FERRET_API void* ferret_trainer_stream(ferret_trainer* t);
 
+/* Stage sharding, one process per GPU (no reference counterpart: the reference
+ * is single-process, learner.hpp:384-385 keeps every stage in one object).
+ * Call set_shard before set_schedule on every rank with the same stage->rank
+ * map (non-decreasing, stage 0 on rank 0). set_schedule then sizes this rank's
+ * inbox from the log's hand-off plan; exchange inbox_handle() (a 64-byte CUDA
+ * IPC handle) between ranks and open_peer() every rank this one sends to.
+ * Each rank replays the whole log but launches only its stages' kernels; stage
+ * outputs, input gradients (sent unmasked, masked by the receiver) and the
+ * predict / replay sweeps cross ranks as direct stores into the peer's inbox
+ * followed by a release flag (NVLink P2P on an 8xB200 box). Ranks must finish
+ * chunk c before any rank starts chunk c+1 (the caller's barrier). Only the
+ * rank owning the last stage produces predictions (fetch_log); only rank 0
+ * holds the normalizer; params/comp_state are valid for the stages a rank owns. */
+FERRET_API ferret_status ferret_trainer_set_shard(ferret_trainer* t, int32_t rank, int32_t world,
+                                                  const int32_t* stage_owner);
+FERRET_API ferret_status ferret_trainer_inbox_handle(ferret_trainer* t, void* out, size_t cap);
+FERRET_API ferret_status ferret_trainer_open_peer(ferret_trainer* t, int32_t peer, const void* handle);
+
 /* TrainOutcome::net (learner.hpp:177-181): current params, fp64, flatten() order */
 FERRET_API ferret_status ferret_trainer_params(ferret_trainer* t, double* out, size_t n);
 /* per-stage compensator state (compensate.hpp:55-58); any pointer may be NULL.

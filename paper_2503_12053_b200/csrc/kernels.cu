@@ -691,7 +691,54 @@ __global__ void pool_kernel(const PoolArgs a) {
     if (threadIdx.x == 0) a.pool_labels[dst] = a.labels[b];
 }
 
+// Hand-off between ranks. One CTA each: messages are B x width floats (<= 256 KB).
+__global__ void __launch_bounds__(512) send_kernel(const SendArgs a) {
+    const bool vec = ((reinterpret_cast<uintptr_t>(a.src) | reinterpret_cast<uintptr_t>(a.dst)) & 15u) == 0 && (a.n & 3) == 0;
+    if (vec) {
+        const float4* s = reinterpret_cast<const float4*>(a.src);
+        float4* d = reinterpret_cast<float4*>(a.dst);
+        for (int i = threadIdx.x; i < a.n / 4; i += blockDim.x) d[i] = s[i];
+    } else {
+        for (int i = threadIdx.x; i < a.n; i += blockDim.x) a.dst[i] = a.src[i];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned e = *a.epoch;
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.flag), "r"(e) : "memory");
+    }
+}
+
+__global__ void __launch_bounds__(512) recv_kernel(const RecvArgs a) {
+    __shared__ unsigned ready;
+    if (threadIdx.x == 0) {
+        const unsigned e = *a.epoch;
+        unsigned v;
+        for (;;) {
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a.flag) : "memory");
+            if (v == e) break;
+            __nanosleep(64);
+        }
+        ready = 1;
+    }
+    __syncthreads();
+    (void)ready;
+    for (int i = threadIdx.x; i < a.n; i += blockDim.x) {
+        float v = __ldcv(a.src + i);  // bypass L1: the peer wrote it
+        if (a.mask && !(a.mask[i] > 0.f)) v = 0.f;
+        a.dst[i] = v;
+    }
+}
+
 } // namespace
+
+void spec_send(const SendArgs& a, KernelSpec& k) {
+    fill(k, reinterpret_cast<const void*>(&send_kernel), dim3(1), dim3(512), a);
+}
+
+void spec_recv(const RecvArgs& a, KernelSpec& k) {
+    fill(k, reinterpret_cast<const void*>(&recv_kernel), dim3(1), dim3(512), a);
+}
 
 void spec_fwd(const FwdArgs& a, KernelSpec& k) {
     // rows are b * in (or xidx[b] * in) floats from X: float4 needs in % 4 == 0 and aligned bases

@@ -143,6 +143,28 @@ struct PoolArgs {
     int B, F;
 };
 
+// Stage-to-stage hand-off between ranks (one process per GPU): the sender
+// stores the message straight into the receiver's inbox (CUDA-IPC mapped peer
+// memory, NVLink on a multi-GPU box) and then publishes flag = epoch with a
+// system-scope release; the receiver spins on its flag with acquire loads and
+// copies the message into its stash (applying the ReLU mask of its own layer,
+// which the sender does not hold).
+struct SendArgs {
+    const float* src;
+    float* dst;                // peer inbox
+    unsigned* flag;            // peer flag
+    const unsigned* epoch;     // control block (this chunk's epoch)
+    int n;
+};
+struct RecvArgs {
+    const float* src;          // own inbox
+    float* dst;
+    const float* mask;         // nullable
+    unsigned* flag;            // own flag
+    const unsigned* epoch;
+    int n;
+};
+
 // A fully resolved kernel launch: the trainer either launches it on a stream
 // or adds it to its CUDA graph as a node with explicit dependencies.
 struct KernelSpec {
@@ -169,6 +191,8 @@ void spec_bwd(const BwdArgs& a, KernelSpec& k);
 void spec_update(const UpdArgs& a, KernelSpec& k);
 void spec_normalize(const NormArgs& a, KernelSpec& k);
 void spec_pool(const PoolArgs& a, KernelSpec& k);
+void spec_send(const SendArgs& a, KernelSpec& k);
+void spec_recv(const RecvArgs& a, KernelSpec& k);
 cudaError_t launch_spec(KernelSpec& k, cudaStream_t s);
 // grid geometry of the bwd launcher (for scratch sizing)
 int bwd_col_tiles(int in);

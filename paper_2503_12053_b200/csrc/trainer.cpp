@@ -82,11 +82,22 @@ struct Reservoir {
     Reservoir() = default;
     Reservoir(uint64_t capacity, uint64_t seed) : cap(capacity), rng(seed ^ 0xbf58476d1ce4e5b9ULL) {}
 
-    int add() {  // pool position the new sample is written to, or -1
+    std::vector<int> label_at;  // label of the sample held at each pool position
+
+    int add(int label) {  // pool position the new sample is written to, or -1
         ++seen;
-        if (size < cap) return static_cast<int>(size++);
-        const uint64_t at = rng.below(seen);
-        return at < cap ? static_cast<int>(at) : -1;
+        int pos = -1;
+        if (size < cap) {
+            pos = static_cast<int>(size++);
+        } else {
+            const uint64_t at = rng.below(seen);
+            if (at < cap) pos = static_cast<int>(at);
+        }
+        if (pos >= 0) {
+            if (label_at.size() <= static_cast<size_t>(pos)) label_at.resize(static_cast<size_t>(pos) + 1);
+            label_at[static_cast<size_t>(pos)] = label;
+        }
+        return pos;
     }
     int sample() { return static_cast<int>(rng.below(size)); }
 };
@@ -137,6 +148,7 @@ struct Schedule {
 struct ChunkPlan {
     std::vector<int> pool_dst;  // per chunk sample: replay-pool position or -1
     std::vector<int> rep_ids;   // per replay step x B: pool positions sampled
+    std::vector<int> rep_labels;  // their labels
     size_t n_replays = 0;
 };
 
@@ -280,6 +292,7 @@ struct GraphBuilder {
 enum { kCatNorm = 0, kCatPredict, kCatForward, kCatBackward, kCatUpdate, kCatReplay, kCatOther, kNumCat };
 
 struct PassResult {
+    std::vector<size_t> inbox_bytes, inbox_flags;  // per rank: incoming message bytes / flags per chunk
     std::vector<int> need_depth;
     std::vector<long long> pushes;
     int need_slots = 0;
@@ -343,6 +356,74 @@ struct ferret_trainer {
     int scratch_slots = 0;
     GraphBuilder* gb = nullptr;   // set while the graph is being built
 
+    // stage sharding across ranks (one process per GPU); world 1 = everything local
+    int rank = 0, world = 1;
+    std::vector<int> owner;                 // per stage: owning rank
+    bool mine(int j) const { return owner[static_cast<size_t>(j)] == rank; }
+    unsigned char* d_inbox = nullptr;       // this rank's incoming hand-offs: data, then flags
+    size_t inbox_alloc = 0;
+    std::vector<size_t> inbox_data_bytes;   // per rank: data bytes (flags follow, 256-aligned)
+    std::vector<float*> peer_data;          // per rank: inbox data base (own included)
+    std::vector<unsigned*> peer_flags;
+    std::vector<void*> peer_opened;         // IPC mappings to close
+    unsigned epoch_counter = 0;
+
+    void set_shard(int r, int w, const int32_t* own) {
+        if (w < 1 || r < 0 || r >= w) fail(FERRET_E_CONFIG, "shard: rank must lie in [0, world)");
+        for (int j = 0; j < P; ++j)
+            if (own[j] < 0 || own[j] >= w) fail(FERRET_E_CONFIG, "shard: stage owner out of range");
+        for (int j = 1; j < P; ++j)
+            if (own[j] < own[j - 1]) fail(FERRET_E_CONFIG, "shard: stages must be assigned to ranks in order");
+        if (own[0] != 0) fail(FERRET_E_CONFIG, "shard: stage 0 (the stream input) must live on rank 0");
+        rank = r;
+        world = w;
+        owner.assign(own, own + P);
+        peer_data.assign(static_cast<size_t>(w), nullptr);
+        peer_flags.assign(static_cast<size_t>(w), nullptr);
+        have_schedule = false;
+        invalidate_graph();
+    }
+
+    // Size and allocate this rank's inbox from the message plan of the log.
+    void setup_inbox() {
+        if (world == 1) return;
+        HostState probe = hs;
+        const PassResult plan = run_pass<true>(probe, false);
+        inbox_data_bytes = plan.inbox_bytes;
+        const size_t data = (inbox_data_bytes[static_cast<size_t>(rank)] + 255) / 256 * 256;
+        const size_t need = data + plan.inbox_flags[static_cast<size_t>(rank)] * sizeof(unsigned) + 256;
+        if (need > inbox_alloc) {
+            cuda_check(cudaStreamSynchronize(stream), "sync");
+            dfree(d_inbox);
+            d_inbox = dalloc<unsigned char>(need, device_bytes);
+            inbox_alloc = need;
+            for (size_t p = 0; p < peer_opened.size(); ++p)
+                if (peer_opened[p]) cudaIpcCloseMemHandle(peer_opened[p]);
+            peer_opened.assign(static_cast<size_t>(world), nullptr);
+            std::fill(peer_data.begin(), peer_data.end(), nullptr);
+            std::fill(peer_flags.begin(), peer_flags.end(), nullptr);
+        }
+        cuda_check(cudaMemset(d_inbox, 0, inbox_alloc), "memset inbox");  // flags start below every epoch
+        peer_data[static_cast<size_t>(rank)] = reinterpret_cast<float*>(d_inbox);
+        peer_flags[static_cast<size_t>(rank)] = reinterpret_cast<unsigned*>(d_inbox + data);
+    }
+
+    void open_peer(int p, const void* handle) {
+        if (p < 0 || p >= world || p == rank) fail(FERRET_E_INVALID_ARG, "open_peer: bad peer rank");
+        if (inbox_data_bytes.empty()) fail(FERRET_E_LOGIC, "open_peer: set_schedule first");
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof h);
+        void* ptr = nullptr;
+        cuda_check(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+        if (peer_opened.size() < static_cast<size_t>(world)) peer_opened.resize(static_cast<size_t>(world), nullptr);
+        if (peer_opened[static_cast<size_t>(p)]) cudaIpcCloseMemHandle(peer_opened[static_cast<size_t>(p)]);
+        peer_opened[static_cast<size_t>(p)] = ptr;
+        const size_t data = (inbox_data_bytes[static_cast<size_t>(p)] + 255) / 256 * 256;
+        peer_data[static_cast<size_t>(p)] = static_cast<float*>(ptr);
+        peer_flags[static_cast<size_t>(p)] = reinterpret_cast<unsigned*>(static_cast<unsigned char*>(ptr) + data);
+        invalidate_graph();
+    }
+
     HostState hs;
     Schedule sched;
     bool have_schedule = false;
@@ -378,6 +459,9 @@ struct ferret_trainer {
         if (graph_exec) cudaGraphExecDestroy(graph_exec);
         for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
         for (cudaEvent_t e : prof_events) cudaEventDestroy(e);
+        for (void* p : peer_opened)
+            if (p) cudaIpcCloseMemHandle(p);
+        dfree(d_inbox);
         for (cudaEvent_t e : norm_events) cudaEventDestroy(e);
         for (cudaEvent_t e : ctl_done) cudaEventDestroy(e);
         if (fork_event) cudaEventDestroy(fork_event);
@@ -455,6 +539,9 @@ struct ferret_trainer {
         stash_stride = align_up(pred_off + 2 * pred_stride, 64);
         stages.resize(static_cast<size_t>(P));
         hs.current.assign(static_cast<size_t>(P), 0);
+        owner.assign(static_cast<size_t>(P), 0);
+        peer_data.assign(1, nullptr);
+        peer_flags.assign(1, nullptr);
         for (int j = 0; j < P; ++j) {
             StageDev& s = stages[static_cast<size_t>(j)];
             s.lo = static_cast<int>(bounds[j]);
@@ -696,6 +783,7 @@ struct ferret_trainer {
         have_schedule = true;
         invalidate_graph();
         alloc_chunk_buffers();
+        setup_inbox();
     }
 
     void alloc_chunk_buffers() {
@@ -705,7 +793,8 @@ struct ferret_trainer {
         for (size_t i = 0; i < sched.events.size(); ++i)
             if (sched.update_fires[i] && sched.events[i].stage == 0) ++upd0;
         const size_t need_rep = opt.replay ? upd0 : 0;
-        const size_t need_ctl = 8 + cap * sizeof(int) + std::max<size_t>(need_rep, 1) * static_cast<size_t>(B) * sizeof(int);
+        const size_t need_ctl =
+            kCtlHeader + (cap + 2 * std::max<size_t>(need_rep, 1) * static_cast<size_t>(B)) * sizeof(int);
         if (cap > chunk_cap) {
             cuda_check(cudaStreamSynchronize(stream), "sync");
             for (void* p : {static_cast<void*>(d_rawc), static_cast<void*>(d_xc), static_cast<void*>(d_labc),
@@ -739,25 +828,37 @@ struct ferret_trainer {
         max_rep = std::max<size_t>(need_rep, 1);
     }
 
+    // control block: [count u64][epoch u32][pad u32][pool_dst x chunk_cap][rep_ids x max_rep*B][rep_labels x max_rep*B]
+    static constexpr size_t kCtlHeader = 16;
     unsigned long long* ctl_count() const { return reinterpret_cast<unsigned long long*>(d_ctl); }
-    int* ctl_pool_dst() const { return reinterpret_cast<int*>(d_ctl + 8); }
-    int* ctl_rep_ids() const { return reinterpret_cast<int*>(d_ctl + 8 + chunk_cap * sizeof(int)); }
+    const unsigned* ctl_epoch() const { return reinterpret_cast<const unsigned*>(d_ctl + 8); }
+    int* ctl_pool_dst() const { return reinterpret_cast<int*>(d_ctl + kCtlHeader); }
+    int* ctl_rep_ids() const { return reinterpret_cast<int*>(d_ctl + kCtlHeader + chunk_cap * sizeof(int)); }
+    int* ctl_rep_labels() const {
+        return reinterpret_cast<int*>(d_ctl + kCtlHeader + (chunk_cap + max_rep * static_cast<size_t>(B)) * sizeof(int));
+    }
 
     // -------------------------------------------------- host reservoir per chunk
     // Walks the log exactly like the reference trainer's buffer_ calls
     // (learner.hpp:409 add at every non-dropped arrival, :509/:514 sample at
     // every firing stage-0 update while non-empty).
-    ChunkPlan plan_chunk(Reservoir& res) const {
+    ChunkPlan plan_chunk(Reservoir& res, size_t base) const {
         ChunkPlan cp;
         cp.pool_dst.assign(sched.chunk_items, -1);
         if (!opt.replay || opt.as_shipped) return cp;
         for (size_t i = 0; i < sched.events.size(); ++i) {
             const ferret_event& e = sched.events[i];
             if (e.kind == FERRET_EV_ARRIVAL && !sched.dropped[static_cast<size_t>(e.item)]) {
-                for (int b = 0; b < B; ++b)
-                    cp.pool_dst[static_cast<size_t>(e.item) * static_cast<size_t>(B) + static_cast<size_t>(b)] = res.add();
+                for (int b = 0; b < B; ++b) {
+                    const size_t s = static_cast<size_t>(e.item) * static_cast<size_t>(B) + static_cast<size_t>(b);
+                    cp.pool_dst[s] = res.add(labels[base + s]);
+                }
             } else if (e.kind == FERRET_EV_UPDATE && e.stage == 0 && sched.update_fires[i] && res.size > 0) {
-                for (int b = 0; b < B; ++b) cp.rep_ids.push_back(res.sample());
+                for (int b = 0; b < B; ++b) {
+                    const int pos = res.sample();
+                    cp.rep_ids.push_back(pos);
+                    cp.rep_labels.push_back(res.label_at[static_cast<size_t>(pos)]);
+                }
                 ++cp.n_replays;
             }
         }
@@ -775,18 +876,24 @@ struct ferret_trainer {
             invalidate_graph();
         if (!graph_exec) build_graph(seen_any);
         // host decisions for this chunk
-        const ChunkPlan cp = plan_chunk(hs.replay);
+        const ChunkPlan cp = plan_chunk(hs.replay, base);
         if (cp.n_replays != graph_shape.n_replays)
             fail(FERRET_E_LOGIC, "replay pattern of this chunk differs from the compiled graph");
         // control block -> device (double-buffered pinned staging)
         unsigned char* h = h_ctl[static_cast<size_t>(ctl_flip)];
         cuda_check(cudaEventSynchronize(ctl_done[static_cast<size_t>(ctl_flip)]), "cudaEventSynchronize");
         const unsigned long long count = hs.norm_count;
+        const unsigned epoch = ++epoch_counter;  // hand-off flags of this chunk (identical on every rank)
         std::memcpy(h, &count, 8);
-        std::memcpy(h + 8, cp.pool_dst.data(), cp.pool_dst.size() * sizeof(int));
-        if (!cp.rep_ids.empty())
-            std::memcpy(h + 8 + chunk_cap * sizeof(int), cp.rep_ids.data(), cp.rep_ids.size() * sizeof(int));
-        const size_t used = 8 + chunk_cap * sizeof(int) + cp.rep_ids.size() * sizeof(int);
+        std::memcpy(h + 8, &epoch, 4);
+        std::memcpy(h + kCtlHeader, cp.pool_dst.data(), cp.pool_dst.size() * sizeof(int));
+        const size_t rep_off = kCtlHeader + chunk_cap * sizeof(int);
+        const size_t lab_off = rep_off + max_rep * static_cast<size_t>(B) * sizeof(int);
+        if (!cp.rep_ids.empty()) {
+            std::memcpy(h + rep_off, cp.rep_ids.data(), cp.rep_ids.size() * sizeof(int));
+            std::memcpy(h + lab_off, cp.rep_labels.data(), cp.rep_labels.size() * sizeof(int));
+        }
+        const size_t used = cp.rep_ids.empty() ? rep_off : lab_off + cp.rep_labels.size() * sizeof(int);
         cuda_check(cudaMemcpyAsync(d_ctl, h, used, cudaMemcpyHostToDevice, stream), "H2D control");
         cuda_check(cudaEventRecord(ctl_done[static_cast<size_t>(ctl_flip)], stream), "cudaEventRecord");
         ctl_flip ^= 1;
@@ -899,7 +1006,40 @@ struct ferret_trainer {
         auto ustash = [&](size_t u) { return GB::key(GB::kStash, static_cast<uint64_t>(slot_of[u])); };
         auto ngroup = [&](size_t u) { return GB::key(GB::kNorm, u / kNormGroup); };
 
-        if (!DRY) {
+        // Cross-rank hand-off: every rank numbers every message identically (same
+        // log, same pass), so the sender knows where the receiver's inbox slot and
+        // flag are. Only the sender emits the send node and only the receiver the
+        // recv node; message bytes land in `dst_key` on the receiver.
+        std::vector<size_t> in_off(static_cast<size_t>(world), 0), in_flags(static_cast<size_t>(world), 0);
+        auto xfer = [&](int src, int dst, auto src_ptr, auto dst_ptr, size_t n, const float* mask, uint64_t key) {
+            if (src == dst) return;
+            const size_t off = in_off[static_cast<size_t>(dst)], fl = in_flags[static_cast<size_t>(dst)];
+            in_off[static_cast<size_t>(dst)] += (n * sizeof(float) + 255) / 256 * 256;
+            in_flags[static_cast<size_t>(dst)] += 1;
+            if (DRY) return;
+            if (rank == src && !peer_data[static_cast<size_t>(dst)])
+                fail(FERRET_E_LOGIC, "hand-off to rank " + std::to_string(dst) + ": peer inbox not opened");
+            if (rank == src) {
+                fb200::SendArgs a{src_ptr(), peer_data[static_cast<size_t>(dst)] + off / sizeof(float),
+                                  peer_flags[static_cast<size_t>(dst)] + fl, ctl_epoch(), static_cast<int>(n)};
+                fb200::KernelSpec k;
+                fb200::spec_send(a, k);
+                gb->cur_category = kCatOther;
+                gb->cur_bytes = 4.0 * static_cast<double>(n);
+                gb->kernel(k, {key}, {});
+            }
+            if (rank == dst) {
+                fb200::RecvArgs a{peer_data[static_cast<size_t>(rank)] + off / sizeof(float), dst_ptr(), mask,
+                                  peer_flags[static_cast<size_t>(rank)] + fl, ctl_epoch(), static_cast<int>(n)};
+                fb200::KernelSpec k;
+                fb200::spec_recv(a, k);
+                gb->cur_category = kCatOther;
+                gb->cur_bytes = 4.0 * static_cast<double>(n);
+                gb->kernel(k, {}, {key});
+            }
+        };
+
+        if (!DRY && mine(0)) {
             // normalizer groups: a chain of their own (mean/m2 state), each unit's
             // ops wait only for the group holding its rows
             const size_t groups = (n_units + kNormGroup - 1) / kNormGroup;
@@ -932,14 +1072,10 @@ struct ferret_trainer {
                         free_slots.pop_back();
                     }
                     ++n_pred;
-                    if (!DRY) {
-                        std::vector<uint64_t> reads{ngroup(u)};
-                        for (int s = 0; s < P; ++s) reads.push_back(vslot(s, rel[static_cast<size_t>(s)]));
-                        launch_predict(u, rel, as_shipped ? -1 : slot_of[u], reads);
-                    }
+                    emit_predict<DRY>(u, rel, as_shipped ? -1 : slot_of[u], xfer, vslot, ngroup);
                     if (opt.replay && !as_shipped) {
                         buffer_nonempty = true;
-                        if (!DRY) {
+                        if (!DRY && mine(0)) {
                             fb200::PoolArgs pa{xrows(u), d_labc + u * static_cast<size_t>(B),
                                                ctl_pool_dst() + u * static_cast<size_t>(B), d_pool_x, d_pool_lab, B, F};
                             fb200::KernelSpec k;
@@ -956,18 +1092,36 @@ struct ferret_trainer {
                     const long long v = rel[static_cast<size_t>(j)];
                     read_ver[u * static_cast<size_t>(P) + static_cast<size_t>(j)] = v;
                     if (sched.has_bwd[u * static_cast<size_t>(P) + static_cast<size_t>(j)]) live[static_cast<size_t>(j)][v] += 1;
-                    if (!DRY)
+                    if (!DRY && mine(j))
                         launch_stage_forward(j, stages[static_cast<size_t>(j)].slot(v), stash(u), xrows(u),
                                              {vslot(j, v), ngroup(u)}, ustash(u));
+                    if (j + 1 < P) {  // hand the stage output to the next stage's rank
+                        const LayerDev& top = layers[static_cast<size_t>(stages[static_cast<size_t>(j)].hi - 1)];
+                        const long long off = top.act_off;
+                        xfer(owner[static_cast<size_t>(j)], owner[static_cast<size_t>(j + 1)], [&] { return stash(u) + off; },
+                             [&] { return stash(u) + off; }, static_cast<size_t>(B) * top.out, nullptr, ustash(u));
+                    }
                     break;
                 }
                 case FERRET_EV_BACKWARD: {  // learner.hpp:435-479
                     if (as_shipped || !inflight[u]) break;
                     const long long r = read_ver[u * static_cast<size_t>(P) + static_cast<size_t>(j)];
                     if (r < 0) fail(FERRET_E_OUT_OF_RANGE, "stage version evicted");
-                    if (!DRY)
+                    // the input gradient of the stage's first layer goes to stage j-1;
+                    // across ranks it is sent unmasked (the ReLU mask lives there)
+                    const bool cross = j > 0 && owner[static_cast<size_t>(j - 1)] != owner[static_cast<size_t>(j)];
+                    if (!DRY && mine(j))
                         launch_stage_backward(j, stages[static_cast<size_t>(j)].slot(r), stash(u),
-                                              d_labc + u * static_cast<size_t>(B), slot_of[u], {vslot(j, r)}, ustash(u));
+                                              d_labc + u * static_cast<size_t>(B), slot_of[u], {vslot(j, r)}, ustash(u),
+                                              cross);
+                    if (cross && sched.has_bwd[u * static_cast<size_t>(P) + static_cast<size_t>(j - 1)]) {
+                        const LayerDev& below = layers[static_cast<size_t>(stages[static_cast<size_t>(j)].lo - 1)];
+                        const long long doff = below.dlt_off, aoff = below.act_off;
+                        const bool relu = below.act == FERRET_ACT_RELU;
+                        xfer(owner[static_cast<size_t>(j)], owner[static_cast<size_t>(j - 1)], [&] { return stash(u) + doff; },
+                             [&] { return stash(u) + doff; }, static_cast<size_t>(B) * below.out,
+                             relu ? stash(u) + aoff : nullptr, ustash(u));
+                    }
                     pending[{e.worker, j}].push_back({u, r});
                     break;
                 }
@@ -987,8 +1141,8 @@ struct ferret_trainer {
                         oldest = std::min(oldest, p.read);
                     }
                     ++n_upd;
-                    if (timing) ++res.n_updates_timed;
-                    if (!DRY) {
+                    if (timing && mine(j)) ++res.n_updates_timed;
+                    if (!DRY && mine(j)) {
                         fb200::UpdArgs a = update_args(j, cur, oldest);
                         a.policy = opt.policy;
                         a.K = static_cast<int>(pl.size());
@@ -1019,7 +1173,7 @@ struct ferret_trainer {
                     }
                     it->second.clear();
                     if (j == 0 && opt.replay && buffer_nonempty) {  // learner.hpp:509, 513-519
-                        replay_step<DRY>(res.n_replays, rel, note_push, vslot);
+                        replay_step<DRY>(res.n_replays, rel, note_push, vslot, xfer);
                         for (int s = 0; s < P; ++s) res.pushes[static_cast<size_t>(s)] += 1;
                         ++res.n_replays;
                     }
@@ -1039,11 +1193,13 @@ struct ferret_trainer {
             for (int j = 0; j < P; ++j) {
                 const StageDev& s = stages[static_cast<size_t>(j)];
                 const long long fin = rel[static_cast<size_t>(j)] % s.depth;
-                if (fin != 0)
-                    gb->cur_category = kCatOther; gb->cur_stage = -1;
+                if (fin != 0 && mine(j)) {
+                    gb->cur_category = kCatOther;
+                    gb->cur_stage = -1;
                     gb->cur_bytes = 8.0 * static_cast<double>(s.slot_floats);
                     gb->copy(s.ring, s.slot(fin), static_cast<size_t>(s.slot_floats) * sizeof(float), {vslot(j, fin)},
                              {vslot(j, 0)});
+                }
             }
             stats.events = sched.events.size();
             stats.updates = n_upd;
@@ -1057,6 +1213,8 @@ struct ferret_trainer {
             }
         }
         res.need_slots = slots_used;
+        res.inbox_bytes = in_off;
+        res.inbox_flags = in_flags;
         (void)st;
         return res;
     }
@@ -1113,21 +1271,35 @@ struct ferret_trainer {
     // predict_class(net_, x) at the arrival (learner.hpp:398-399): full net at
     // the live versions, ping-pong scratch inside the unit's stash slot (as
     // shipped there is no slot: the replay stash's scratch is used, serialised).
-    void launch_predict(size_t u, const std::vector<long long>& rel, int slot, const std::vector<uint64_t>& reads) {
+    // Where the next stage lives on another rank the running activation is
+    // handed over.
+    template <bool DRY, class Xfer, class VSlot, class NGroup>
+    void emit_predict(size_t u, const std::vector<long long>& rel, int slot, Xfer& xfer, VSlot& vslot, NGroup& ngroup) {
         using GB = GraphBuilder;
-        gb->cur_category = kCatPredict; gb->cur_stage = -1;
         float* scratch = (slot >= 0 ? d_stash + static_cast<long long>(slot) * stash_stride : d_replay) + pred_off;
         const uint64_t sk = slot >= 0 ? GB::key(GB::kPred, static_cast<uint64_t>(slot)) : GB::key(GB::kReplay, 0);
-        const float* X = d_xc + u * static_cast<size_t>(B) * static_cast<size_t>(F);
-        for (int l = 0; l < L; ++l) {
-            const LayerDev& ld = layers[static_cast<size_t>(l)];
-            const StageDev& s = stages[static_cast<size_t>(ld.stage)];
-            float* Y = scratch + (l & 1) * pred_stride;
-            emit_layer(ld, s.slot(rel[static_cast<size_t>(ld.stage)]), X, nullptr, Y, reads, {sk});
-            X = Y;
+        const float* x0 = d_xc + u * static_cast<size_t>(B) * static_cast<size_t>(F);
+        for (int j = 0; j < P; ++j) {
+            const StageDev& s = stages[static_cast<size_t>(j)];
+            if (j > 0) {
+                const int l = s.lo - 1;
+                float* buf = scratch + (l & 1) * pred_stride;
+                xfer(owner[static_cast<size_t>(j - 1)], owner[static_cast<size_t>(j)], [&] { return buf; },
+                     [&] { return buf; }, static_cast<size_t>(B) * layers[static_cast<size_t>(l)].out, nullptr, sk);
+            }
+            if (DRY || !mine(j)) continue;
+            gb->cur_category = kCatPredict;
+            gb->cur_stage = -1;
+            const std::vector<uint64_t> reads{vslot(j, rel[static_cast<size_t>(j)]), ngroup(u)};
+            for (int l = s.lo; l < s.hi; ++l) {
+                const float* X = l == 0 ? x0 : scratch + ((l - 1) & 1) * pred_stride;
+                emit_layer(layers[static_cast<size_t>(l)], s.slot(rel[static_cast<size_t>(j)]), X, nullptr,
+                           scratch + (l & 1) * pred_stride, reads, {sk});
+            }
         }
+        if (DRY || !mine(P - 1)) return;
         fb200::HeadArgs h{};
-        h.logits = X;
+        h.logits = scratch + ((L - 1) & 1) * pred_stride;
         h.n_out = n_out;
         h.B = B;
         h.mode = 0;
@@ -1140,7 +1312,8 @@ struct ferret_trainer {
 
     void launch_stage_forward(int j, const float* slot, float* stash_u, const float* x0, const std::vector<uint64_t>& reads,
                               uint64_t stash_key) {
-        gb->cur_category = kCatForward; gb->cur_stage = j;
+        gb->cur_category = kCatForward;
+        gb->cur_stage = j;
         const StageDev& s = stages[static_cast<size_t>(j)];
         for (int l = s.lo; l < s.hi; ++l) {
             const LayerDev& ld = layers[static_cast<size_t>(l)];
@@ -1150,15 +1323,17 @@ struct ferret_trainer {
     }
 
     // delta at the logits (last stage) then per layer prev = W^T delta with the
-    // ReLU mask of the layer below applied on write (learner.hpp:443-476).
+    // ReLU mask of the layer below applied on write (learner.hpp:443-476);
+    // `cross`: the stage below is on another rank, which applies the mask.
     void launch_stage_backward(int j, const float* slot, float* stash_u, const int* lab, int scratch,
-                               const std::vector<uint64_t>& reads, uint64_t stash_key) {
-        gb->cur_category = kCatBackward; gb->cur_stage = j;
+                               const std::vector<uint64_t>& reads, uint64_t stash_key, bool cross) {
+        gb->cur_category = kCatBackward;
+        gb->cur_stage = j;
         const StageDev& s = stages[static_cast<size_t>(j)];
         if (j == P - 1) emit_delta_head(stash_u, lab, nullptr, 1.0f / static_cast<float>(B), {}, stash_key);
         for (int l = s.hi - 1; l >= s.lo; --l) {
             if (l == 0) break;  // no input gradient for the first layer
-            emit_layer_backward(l, slot, stash_u, scratch, reads, stash_key);
+            emit_layer_backward(l, slot, stash_u, scratch, reads, stash_key, !(cross && l == s.lo));
         }
     }
 
@@ -1181,13 +1356,13 @@ struct ferret_trainer {
     }
 
     void emit_layer_backward(int l, const float* slot, float* stash_u, int scratch, const std::vector<uint64_t>& reads,
-                             uint64_t stash_key) {
+                             uint64_t stash_key, bool mask_on_write = true) {
         const LayerDev& ld = layers[static_cast<size_t>(l)];
         const LayerDev& below = layers[static_cast<size_t>(l - 1)];
         fb200::BwdArgs a{};
         a.W = slot + ld.woff;
         a.d_out = stash_u + ld.dlt_off;
-        a.mask = below.act == FERRET_ACT_RELU ? stash_u + below.act_off : nullptr;
+        a.mask = mask_on_write && below.act == FERRET_ACT_RELU ? stash_u + below.act_off : nullptr;
         a.d_in = stash_u + below.dlt_off;
         a.in = ld.in;
         a.out = ld.out;
@@ -1204,35 +1379,59 @@ struct ferret_trainer {
     // replay_step (learner.hpp:513-519): forward_backward(net_, {buffer.sample()})
     // with mean reduction (net.hpp:157-200), apply_sgd on every stage, push a
     // version per stage. B pool samples per replay step at micro-batch B; the
-    // pool positions come from the control block (row r of rep_ids).
-    template <bool DRY, class NotePush, class VSlot>
-    void replay_step(size_t r, std::vector<long long>& rel, NotePush& note_push, VSlot& vslot) {
+    // pool positions and their labels come from the control block (row r).
+    // Across ranks: activations hand forward, deltas (unmasked) hand back.
+    template <bool DRY, class NotePush, class VSlot, class Xfer>
+    void replay_step(size_t r, std::vector<long long>& rel, NotePush& note_push, VSlot& vslot, Xfer& xfer) {
         using GB = GraphBuilder;
         for (int j = 0; j < P; ++j) note_push(j);
+        const uint64_t rk = GB::key(GB::kReplay, 0), pk = GB::key(GB::kPool, 0);
+        const int* ids = ctl_rep_ids() + r * static_cast<size_t>(B);
+        auto owner_of = [&](int j) { return owner[static_cast<size_t>(j)]; };
+        for (int j = 0; j < P; ++j) {  // forward sweep
+            const StageDev& s = stages[static_cast<size_t>(j)];
+            if (j > 0) {
+                const LayerDev& in_l = layers[static_cast<size_t>(s.lo - 1)];
+                float* buf = d_replay + in_l.act_off;
+                xfer(owner_of(j - 1), owner_of(j), [&] { return buf; }, [&] { return buf; },
+                     static_cast<size_t>(B) * in_l.out, nullptr, rk);
+            }
+            if (DRY || !mine(j)) continue;
+            gb->cur_category = kCatReplay;
+            gb->cur_stage = -1;
+            for (int l = s.lo; l < s.hi; ++l) {
+                const LayerDev& ld = layers[static_cast<size_t>(l)];
+                const float* X = l == 0 ? d_pool_x : d_replay + layers[static_cast<size_t>(l - 1)].act_off;
+                emit_layer(ld, s.slot(rel[static_cast<size_t>(j)]), X, l == 0 ? ids : nullptr, d_replay + ld.act_off,
+                           {vslot(j, rel[static_cast<size_t>(j)]), pk}, {rk});
+            }
+        }
+        if (!DRY && mine(P - 1)) {
+            gb->cur_category = kCatReplay;
+            emit_delta_head(d_replay, ctl_rep_labels() + r * static_cast<size_t>(B), nullptr,
+                            1.0f / static_cast<float>(B), {}, rk);
+        }
+        for (int j = P - 1; j >= 0; --j) {  // backward sweep
+            const StageDev& s = stages[static_cast<size_t>(j)];
+            const bool cross = j > 0 && owner_of(j - 1) != owner_of(j);
+            if (!DRY && mine(j)) {
+                gb->cur_category = kCatReplay;
+                for (int l = s.hi - 1; l >= std::max(s.lo, 1); --l)
+                    emit_layer_backward(l, s.slot(rel[static_cast<size_t>(j)]), d_replay, stash_slots,
+                                        {vslot(j, rel[static_cast<size_t>(j)])}, rk, !(cross && l == s.lo));
+            }
+            if (cross) {
+                const LayerDev& below = layers[static_cast<size_t>(s.lo - 1)];
+                float* buf = d_replay + below.dlt_off;
+                xfer(owner_of(j), owner_of(j - 1), [&] { return buf; }, [&] { return buf; },
+                     static_cast<size_t>(B) * below.out, below.act == FERRET_ACT_RELU ? d_replay + below.act_off : nullptr,
+                     rk);
+            }
+        }
         if (!DRY) {
-            gb->cur_category = kCatReplay; gb->cur_stage = -1;
-            const uint64_t rk = GB::key(GB::kReplay, 0), pk = GB::key(GB::kPool, 0);
-            std::vector<uint64_t> live_slots;
-            for (int j = 0; j < P; ++j) live_slots.push_back(vslot(j, rel[static_cast<size_t>(j)]));
-            const int* ids = ctl_rep_ids() + r * static_cast<size_t>(B);
-            const float* X = d_pool_x;
-            const int* xidx = ids;
-            std::vector<uint64_t> reads = live_slots;
-            reads.push_back(pk);
-            for (int l = 0; l < L; ++l) {
-                const LayerDev& ld = layers[static_cast<size_t>(l)];
-                const StageDev& s = stages[static_cast<size_t>(ld.stage)];
-                emit_layer(ld, s.slot(rel[static_cast<size_t>(ld.stage)]), X, xidx, d_replay + ld.act_off, reads, {rk});
-                X = d_replay + ld.act_off;
-                xidx = nullptr;
-            }
-            emit_delta_head(d_replay, d_pool_lab, ids, 1.0f / static_cast<float>(B), {pk}, rk);
-            for (int l = L - 1; l >= 1; --l) {
-                const LayerDev& ld = layers[static_cast<size_t>(l)];
-                emit_layer_backward(l, stages[static_cast<size_t>(ld.stage)].slot(rel[static_cast<size_t>(ld.stage)]),
-                                    d_replay, stash_slots, live_slots, rk);
-            }
             for (int j = 0; j < P; ++j) {
+                if (!mine(j)) continue;
+                gb->cur_category = kCatReplay;
                 const long long cur = rel[static_cast<size_t>(j)];
                 fb200::UpdArgs a = update_args(j, cur, cur);
                 a.policy = FERRET_POLICY_NONE;
@@ -1493,6 +1692,31 @@ ferret_status ferret_trainer_set_timing(ferret_trainer* t, int32_t enable) {
     return guarded([&] {
         cuda_check(cudaStreamSynchronize(t->stream), "sync");
         t->timing = enable != 0;
+    });
+}
+
+ferret_status ferret_trainer_set_shard(ferret_trainer* t, int32_t rank, int32_t world, const int32_t* stage_owner) {
+    return guarded([&] {
+        cuda_check(cudaSetDevice(t->opt.device), "cudaSetDevice");
+        t->set_shard(rank, world, stage_owner);
+    });
+}
+
+ferret_status ferret_trainer_inbox_handle(ferret_trainer* t, void* out, size_t cap) {
+    return guarded([&] {
+        if (cap < sizeof(cudaIpcMemHandle_t)) fail(FERRET_E_INVALID_ARG, "inbox_handle: buffer smaller than 64 bytes");
+        if (!t->d_inbox) fail(FERRET_E_LOGIC, "inbox_handle: no inbox (world 1, or set_schedule not called)");
+        cuda_check(cudaSetDevice(t->opt.device), "cudaSetDevice");
+        cudaIpcMemHandle_t h;
+        cuda_check(cudaIpcGetMemHandle(&h, t->d_inbox), "cudaIpcGetMemHandle");
+        std::memcpy(out, &h, sizeof h);
+    });
+}
+
+ferret_status ferret_trainer_open_peer(ferret_trainer* t, int32_t peer, const void* handle) {
+    return guarded([&] {
+        cuda_check(cudaSetDevice(t->opt.device), "cudaSetDevice");
+        t->open_peer(peer, handle);
     });
 }
 

@@ -134,6 +134,9 @@ def lib() -> C.CDLL:
         "ferret_trainer_update_timing": (C.c_int, [C.c_void_p, P(D), P(C.c_uint64), P(D)]),
         "ferret_trainer_set_profiling": (C.c_int, [C.c_void_p, C.c_int32]),
         "ferret_trainer_profile_stages": (C.c_int, [C.c_void_p, P(D), P(D), P(D), C.c_int32]),
+        "ferret_trainer_set_shard": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, P(C.c_int32)]),
+        "ferret_trainer_inbox_handle": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t]),
+        "ferret_trainer_open_peer": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
         "ferret_trainer_profile": (C.c_int, [C.c_void_p, P(D), P(C.c_uint64), P(D), C.c_int32, P(D), P(D)]),
         "ferret_compensate": (C.c_int, [C.c_int32, P(D), P(P(D)), C.c_int32, P(D), P(D), P(D), P(D), C.c_size_t,
                                         D, D, D, D, P(D)]),
@@ -415,6 +418,28 @@ class PipelineTrainer:
                             for i, k in enumerate(self.PROFILE_CLASSES)},
                 "critical_path_ms": crit.value, "serial_ms": tot.value}
 
+    # ---- stage sharding (one process per GPU; ferret_b200.h: ferret_trainer_set_shard)
+    def set_shard(self, rank: int, world: int, stage_owner: Sequence[int]) -> None:
+        own = np.ascontiguousarray(stage_owner, dtype=np.int32)
+        _check(lib().ferret_trainer_set_shard(self._h, rank, world, own.ctypes.data_as(C.POINTER(C.c_int32))))
+        self.rank, self.world, self.stage_owner = rank, world, list(stage_owner)
+
+    def inbox_handle(self) -> bytes:
+        buf = C.create_string_buffer(64)
+        _check(lib().ferret_trainer_inbox_handle(self._h, buf, 64))
+        return buf.raw
+
+    def open_peer(self, peer: int, handle: bytes) -> None:
+        _check(lib().ferret_trainer_open_peer(self._h, peer, C.c_char_p(handle)))
+
+    def connect(self, all_gather) -> None:
+        """Exchange inbox handles (`all_gather(bytes) -> list[bytes]`, e.g. over
+        torch.distributed) and map every peer's inbox."""
+        handles = all_gather(self.inbox_handle())
+        for p, h in enumerate(handles):
+            if p != self.rank:
+                self.open_peer(p, h)
+
     def profile_stages(self):
         """(fwd_us, bwd_us, upd_us) per stage, per processed unit, of the last profiled execute()."""
         P = len(self.bounds) - 1
@@ -459,6 +484,11 @@ def compensate(policy: str, g: np.ndarray, chain: Sequence[np.ndarray], lam=None
                                    _dp(mean_gap) if mean_gap is not None else nul, n, lambda0, alpha, eta_lambda, nu,
                                    _dp(out)))
     return out
+
+
+def stage_owners(n_stages: int, world: int) -> list:
+    """Contiguous stage -> rank map: stage j on rank floor(j * world / P) (one stage per GPU when P == world)."""
+    return [min(world - 1, (j * world) // n_stages) for j in range(n_stages)]
 
 
 def measure_profile(widths: Sequence[int], micro_batch: int = 1, policy: str = "iter_fisher", units: int = 48,

@@ -1,0 +1,79 @@
+"""One rank of a stage-sharded pipelined run (launched by tests/test_gpu_shard.py
+with torch.distributed.run). Every rank replays the same log; rank r launches
+only the kernels of its stages and hands activations / deltas to its
+neighbours through CUDA-IPC mapped inboxes. Results go to <out>/rank<r>.npz."""
+import argparse
+import os
+import pickle
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", required=True)
+    ap.add_argument("--widths", default="96,128,64,48,10")
+    ap.add_argument("--bounds", default="0,1,2,3,4")
+    ap.add_argument("--units", type=int, default=48)
+    ap.add_argument("--chunks", type=int, default=2)
+    ap.add_argument("--micro-batch", type=int, default=4)
+    ap.add_argument("--policy", default="iter_fisher")
+    ap.add_argument("--replay", type=int, default=1)
+    ap.add_argument("--device", type=int, default=-1, help="-1: LOCAL_RANK")
+    args = ap.parse_args()
+    import torch
+    import torch.distributed as dist
+
+    import paper_2503_12053_b200 as fb
+
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    dev = int(os.environ.get("LOCAL_RANK", "0")) if args.device < 0 else args.device
+    dist.init_process_group("gloo")
+    widths = [int(x) for x in args.widths.split(",")]
+    bounds = [int(x) for x in args.bounds.split(",")]
+    P = len(bounds) - 1
+    B = args.micro_batch
+    prof = fb.profile_from_widths(widths)
+    t_d = float(prof["t_f"].max())
+    sched = fb.Schedule.forced(prof, t_d, fb.StreamSpec(t_d=t_d, horizon=args.units * t_d), bounds, args.units)
+    chunk = args.units * B
+    feats, labels = fb.synth_drift_stream(args.chunks * chunk, widths[0], widths[-1], "split_tasks", 7)
+    params = fb.make_dense_net(widths, 1)
+    tr = fb.PipelineTrainer(widths, params, bounds,
+                            fb.PipelineTrainOptions(policy=args.policy, micro_batch=B, replay=bool(args.replay),
+                                                    replay_seed=3, device=dev))
+    owners = fb.ferret.stage_owners(P, world)
+    tr.set_shard(rank, world, owners)
+    tr.load_stream(feats, labels)
+    tr.set_schedule(sched.events, chunk)
+
+    def gather(b):
+        out = [None] * world
+        dist.all_gather_object(out, b)
+        return out
+
+    tr.connect(gather)
+    logs = []
+    for c in range(args.chunks):
+        tr.execute(c)
+        tr.sync()
+        dist.barrier()  # no rank starts chunk c+1 before every rank finished chunk c
+        if owners[-1] == rank:
+            logs.append(tr.fetch_log(c))
+    res = {"params": tr.params(), "owners": owners, "stats": tr.stats()}
+    if owners[-1] == rank:
+        res["log"] = np.concatenate(logs)
+    if rank == 0:
+        res["normalizer"] = tr.normalizer(widths[0])
+    with open(os.path.join(args.out, f"rank{rank}.pkl"), "wb") as f:
+        pickle.dump(res, f)
+    tr.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
