@@ -217,6 +217,12 @@ FERRET_API ferret_status ferret_trainer_set_shard(ferret_trainer* t, int32_t ran
                                                   const int32_t* stage_owner);
 FERRET_API ferret_status ferret_trainer_inbox_handle(ferret_trainer* t, void* out, size_t cap);
 FERRET_API ferret_status ferret_trainer_open_peer(ferret_trainer* t, int32_t peer, const void* handle);
+/* The hand-off plan of the current schedule: per destination rank, incoming
+ * message bytes and message count per chunk. Works on plan-only trainers
+ * (created with opts.device = -1: host passes only, no device touched), so the
+ * multi-rank logic can be checked without a GPU. */
+FERRET_API ferret_status ferret_trainer_handoff_plan(ferret_trainer* t, uint64_t* bytes_to_rank, uint64_t* msgs_to_rank,
+                                                     int32_t world);
 
 /* TrainOutcome::net (learner.hpp:177-181): current params, fp64, flatten() order */
 FERRET_API ferret_status ferret_trainer_params(ferret_trainer* t, double* out, size_t n);

@@ -51,7 +51,19 @@ using fb200::guarded;
 
 namespace {
 
+// Plan-only trainers (device -1) run the host passes without any device: every
+// allocation is null and CUDA calls are skipped. Used to check the multi-rank
+// hand-off plan on machines without a GPU (tests/test_shard_plan.py).
+thread_local bool t_plan_only = false;
+
+struct PlanOnlyScope {
+    bool prev;
+    explicit PlanOnlyScope(bool on) : prev(t_plan_only) { t_plan_only = on; }
+    ~PlanOnlyScope() { t_plan_only = prev; }
+};
+
 void cuda_check(cudaError_t e, const char* what) {
+    if (t_plan_only) return;
     if (e != cudaSuccess) fail(FERRET_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
@@ -60,6 +72,7 @@ long long align_up(long long v, long long a) { return (v + a - 1) / a * a; }
 template <class T>
 T* dalloc(size_t n, size_t& counter) {
     void* p = nullptr;
+    if (t_plan_only) return nullptr;
     if (n == 0) n = 1;
     cuda_check(cudaMalloc(&p, n * sizeof(T)), "cudaMalloc");
     counter += n * sizeof(T);
@@ -355,6 +368,10 @@ struct ferret_trainer {
     size_t max_partial = 1, max_tiles = 1;
     int scratch_slots = 0;
     GraphBuilder* gb = nullptr;   // set while the graph is being built
+    bool plan_only = false;       // created with device -1: host passes only
+    void require_device_mode() const {
+        if (plan_only) fail(FERRET_E_NO_DEVICE, "plan-only trainer (device -1) cannot run device work");
+    }
 
     // stage sharding across ranks (one process per GPU); world 1 = everything local
     int rank = 0, world = 1;
@@ -1585,9 +1602,12 @@ ferret_status ferret_trainer_create(const ferret_net_desc* net, const uint64_t* 
                                     const ferret_train_opts* opts, ferret_trainer** out) {
     return guarded([&] {
         if (!net || !bounds || !opts || !out) fail(FERRET_E_INVALID_ARG, "trainer_create: null argument");
-        require_device(opts->device);
+        const bool plan_only = opts->device < 0;
+        if (!plan_only) require_device(opts->device);
+        PlanOnlyScope scope(plan_only);
         auto t = std::make_unique<ferret_trainer>();
         t->opt = *opts;
+        t->plan_only = plan_only;
         cuda_check(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking), "stream");
         cuda_check(cudaStreamCreateWithFlags(&t->nstream, cudaStreamNonBlocking), "stream");
         t->build(*net, bounds, n_bounds);
@@ -1599,6 +1619,7 @@ ferret_status ferret_trainer_create(const ferret_net_desc* net, const uint64_t* 
 ferret_status ferret_trainer_load_stream(ferret_trainer* t, const double* features, const uint64_t* labels,
                                          size_t n_items, size_t n_features) {
     return guarded([&] {
+        t->require_device_mode();
         cuda_check(cudaSetDevice(t->opt.device), "cudaSetDevice");
         t->load_stream(features, labels, n_items, n_features);
     });
@@ -1607,13 +1628,30 @@ ferret_status ferret_trainer_load_stream(ferret_trainer* t, const double* featur
 ferret_status ferret_trainer_set_schedule(ferret_trainer* t, const ferret_event* events, size_t n_events,
                                           size_t n_chunk_items) {
     return guarded([&] {
+        PlanOnlyScope scope(t->plan_only);
         cuda_check(cudaSetDevice(t->opt.device), "cudaSetDevice");
         t->set_schedule(events, n_events, n_chunk_items);
     });
 }
 
+ferret_status ferret_trainer_handoff_plan(ferret_trainer* t, uint64_t* bytes_to_rank, uint64_t* msgs_to_rank,
+                                          int32_t world) {
+    return guarded([&] {
+        if (world != t->world) fail(FERRET_E_INVALID_ARG, "handoff_plan: world mismatch");
+        if (!t->have_schedule) fail(FERRET_E_LOGIC, "handoff_plan: set_schedule first");
+        PlanOnlyScope scope(true);  // sizing pass only: no device work
+        HostState probe = t->hs;
+        const PassResult plan = t->run_pass<true>(probe, false);
+        for (int32_t r = 0; r < world; ++r) {
+            bytes_to_rank[r] = plan.inbox_bytes[static_cast<size_t>(r)];
+            msgs_to_rank[r] = plan.inbox_flags[static_cast<size_t>(r)];
+        }
+    });
+}
+
 ferret_status ferret_trainer_execute(ferret_trainer* t, size_t chunk) {
     return guarded([&] {
+        t->require_device_mode();
         cuda_check(cudaSetDevice(t->opt.device), "cudaSetDevice");
         t->execute(chunk);
     });
@@ -1697,6 +1735,7 @@ ferret_status ferret_trainer_set_timing(ferret_trainer* t, int32_t enable) {
 
 ferret_status ferret_trainer_set_shard(ferret_trainer* t, int32_t rank, int32_t world, const int32_t* stage_owner) {
     return guarded([&] {
+        PlanOnlyScope scope(t->plan_only);
         cuda_check(cudaSetDevice(t->opt.device), "cudaSetDevice");
         t->set_shard(rank, world, stage_owner);
     });

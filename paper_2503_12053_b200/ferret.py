@@ -137,6 +137,7 @@ def lib() -> C.CDLL:
         "ferret_trainer_set_shard": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, P(C.c_int32)]),
         "ferret_trainer_inbox_handle": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t]),
         "ferret_trainer_open_peer": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
+        "ferret_trainer_handoff_plan": (C.c_int, [C.c_void_p, P(C.c_uint64), P(C.c_uint64), C.c_int32]),
         "ferret_trainer_profile": (C.c_int, [C.c_void_p, P(D), P(C.c_uint64), P(D), C.c_int32, P(D), P(D)]),
         "ferret_compensate": (C.c_int, [C.c_int32, P(D), P(P(D)), C.c_int32, P(D), P(D), P(D), P(D), C.c_size_t,
                                         D, D, D, D, P(D)]),
@@ -431,6 +432,13 @@ class PipelineTrainer:
 
     def open_peer(self, peer: int, handle: bytes) -> None:
         _check(lib().ferret_trainer_open_peer(self._h, peer, C.c_char_p(handle)))
+
+    def handoff_plan(self):
+        """(bytes, messages) per destination rank per chunk for the current schedule."""
+        b = np.zeros(self.world, dtype=np.uint64)
+        m = np.zeros(self.world, dtype=np.uint64)
+        _check(lib().ferret_trainer_handoff_plan(self._h, _up(b), _up(m), self.world))
+        return b, m
 
     def connect(self, all_gather) -> None:
         """Exchange inbox handles (`all_gather(bytes) -> list[bytes]`, e.g. over
