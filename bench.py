@@ -146,6 +146,52 @@ def large_stage_roofline(fb, device):
             "mean_tau": st["mean_tau"], "ring_depth": st["ring_depth"]}
 
 
+def stage_shard_measure(fb, torch, dist, rank, world, local, args, units):
+    """The same C2 stream pipelined with its stages sharded over min(N, 4) GPUs (one
+    stage group per rank, NVLink hand-offs via CUDA-IPC inboxes; ranks beyond the
+    stage count idle). Device time per chunk, max over ranks."""
+    P = len(BOUNDS) - 1
+    used = min(world, P)
+    owners = fb.ferret.stage_owners(P, used)
+    sched, feats, labels, chunk = make_workload(fb, args.warmup + args.steps, units)
+    tr = fb.PipelineTrainer(WIDTHS, fb.make_dense_net(WIDTHS, 1), BOUNDS,
+                            fb.PipelineTrainOptions(policy=POLICY, micro_batch=MICRO_BATCH, device=local))
+    tr.set_shard(rank, world, owners)
+    tr.load_stream(feats, labels)
+    tr.set_schedule(sched.events, chunk)
+
+    def gather(b):
+        out = [None] * world
+        dist.all_gather_object(out, b)
+        return out
+
+    tr.connect(gather)
+    stream = torch.cuda.ExternalStream(tr.cuda_stream, device=torch.device("cuda", local))
+    for c in range(args.warmup):
+        tr.execute(c)
+        tr.sync()
+        dist.barrier()
+    ms = 0.0
+    for s in range(args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dist.barrier()
+        with torch.cuda.stream(stream):
+            a.record(stream)
+        tr.execute(args.warmup + s)
+        with torch.cuda.stream(stream):
+            b.record(stream)
+        tr.sync()
+        ms += a.elapsed_time(b)
+    t = torch.tensor([ms], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    tr.close()
+    return {"value": chunk * args.steps / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms / args.steps,
+            "ranks_with_stages": used, "stage_owner": owners,
+            "note": "one stream, stages sharded across GPUs (strong scaling); hand-offs are peer stores "
+                    "into CUDA-IPC inboxes + release flags; ranks synchronise per chunk"}
+
+
 def make_workload(fb, n_chunks, units):
     prof = fb.profile_from_widths(WIDTHS)
     t_d = float(prof["t_f"].max())
@@ -285,6 +331,7 @@ def main():
     dc = classes[dom]
     achieved = dc["gbs"]
     large = large_stage_roofline(fb, local) if not args.no_large else None
+    shard = stage_shard_measure(fb, torch, dist, rank, world, local, args, units) if world > 1 else None
 
     # ---- e2e through the reference-facing call from pinned host buffers
     tr2 = fb.PipelineTrainer(WIDTHS, params, BOUNDS, opt)
@@ -346,6 +393,7 @@ def main():
                      "note": "C2 weights (1.3 MB) live in L2: the small-net path is latency-bound; "
                              "see large_stage for the same kernels on a config-5 stage"},
         "large_stage": large,
+        "stage_shard": shard,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
         "gpu_launches": int(launches_per_step * args.steps),
