@@ -44,6 +44,7 @@ BOUNDS = [0, 1, 2, 3, 4]
 MICRO_BATCH = 16
 UNITS = 256            # pipeline units per step (x16 samples)
 POLICY = "iter_fisher"
+REDUCE_DEV = "cuda"     # device of the tensors max-reduced over ranks
 CPU_UNITS = 512         # bounded CPU sample (~10 s of reference work): 512 units x 16 samples
 
 
@@ -182,7 +183,7 @@ def stage_shard_measure(fb, torch, dist, rank, world, local, args, units):
             b.record(stream)
         tr.sync()
         ms += a.elapsed_time(b)
-    t = torch.tensor([ms], device="cuda")
+    t = torch.tensor([ms], device=REDUCE_DEV)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     tr.close()
@@ -258,12 +259,20 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    share = os.environ.get("FERRET_BENCH_SHARE_DEVICE") == "1"  # test mode: every rank on cuda:0, gloo
+    if share:
+        local = 0
+    global REDUCE_DEV
+    REDUCE_DEV = "cpu" if share else "cuda"
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     units = args.units
     n_chunks = args.warmup + args.steps
@@ -306,7 +315,7 @@ def main():
         torch.cuda.synchronize()
     dev_ms = sum(a.elapsed_time(b) for a, b in zip(starts, ends))
     if dist:
-        t = torch.tensor([dev_ms], device="cuda")
+        t = torch.tensor([dev_ms], device=REDUCE_DEV)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dev_ms = float(t.item())
         dist.barrier()
@@ -353,7 +362,7 @@ def main():
             e2e_times.append(dt)
     e2e_s = sum(e2e_times)
     if dist:
-        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        t = torch.tensor([e2e_s], device=REDUCE_DEV, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e_value = total_samples / e2e_s
