@@ -262,6 +262,9 @@ FERRET_API ferret_status ferret_trainer_set_timing(ferret_trainer* t, int32_t en
  * the serial total, and the critical
  * path of the concurrent DAG computed from the measured node times. */
 FERRET_API ferret_status ferret_trainer_set_profiling(ferret_trainer* t, int32_t enable);
+/* After ferret_trainer_profile: per node class, device ms and node count along the critical path. */
+FERRET_API ferret_status ferret_trainer_profile_critical(ferret_trainer* t, double* class_ms, uint64_t* class_nodes,
+                                                         int32_t n_classes);
 /* After a profiled execute(): mean device microseconds per processed unit of
  * each stage's forward, backward and update work (the measured costs the
  * planner's LayerProfile t_f / t_b stand for, profile.hpp / net.hpp:263). */

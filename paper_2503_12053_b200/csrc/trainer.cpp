@@ -460,6 +460,8 @@ struct ferret_trainer {
     std::vector<std::vector<int>> prof_ldeps;
     std::vector<int> prof_cat;
     std::vector<double> prof_bytes;
+    std::vector<double> crit_class_ms;     // critical path composition of the last profile()
+    std::vector<uint64_t> crit_class_nodes;
     std::vector<int> prof_stage;
 
     // optional per-launch timing of the update kernel (event record nodes)
@@ -1780,6 +1782,8 @@ ferret_status ferret_trainer_profile(ferret_trainer* t, double* class_ms, uint64
             class_bytes[c] = 0.0;
         }
         double total = 0.0, crit = 0.0;
+        std::vector<int> pred_node(n, -1);
+        size_t last = 0;
         for (size_t i = 0; i < n; ++i) {
             float ms = 0.f;
             cuda_check(cudaEventElapsedTime(&ms, t->prof_events[2 * i], t->prof_events[2 * i + 1]), "cudaEventElapsedTime");
@@ -1792,12 +1796,27 @@ ferret_status ferret_trainer_profile(ferret_trainer* t, double* class_ms, uint64
                 class_bytes[c] += t->prof_bytes[i];
             }
             double start = 0.0;
-            for (int d : t->prof_ldeps[i]) start = std::max(start, finish[static_cast<size_t>(d)]);
+            for (int d : t->prof_ldeps[i])
+                if (finish[static_cast<size_t>(d)] > start) {
+                    start = finish[static_cast<size_t>(d)];
+                    pred_node[i] = d;
+                }
             finish[i] = start + ms;
-            crit = std::max(crit, finish[i]);
+            if (finish[i] > crit) {
+                crit = finish[i];
+                last = i;
+            }
         }
         *critical_ms = crit;
         *serial_ms = total;
+        // critical path composition (per class), reported after the n_classes slots
+        t->crit_class_ms.assign(static_cast<size_t>(kNumCat), 0.0);
+        t->crit_class_nodes.assign(static_cast<size_t>(kNumCat), 0);
+        for (long long i = n ? static_cast<long long>(last) : -1; i >= 0; i = pred_node[static_cast<size_t>(i)]) {
+            const int c = t->prof_cat[static_cast<size_t>(i)];
+            t->crit_class_ms[static_cast<size_t>(c)] += dur[static_cast<size_t>(i)];
+            t->crit_class_nodes[static_cast<size_t>(c)] += 1;
+        }
     });
 }
 
@@ -1826,6 +1845,17 @@ ferret_status ferret_trainer_profile_stages(ferret_trainer* t, double* fwd_us, d
             fwd_us[s] = f[static_cast<size_t>(s)] / units;
             bwd_us[s] = b[static_cast<size_t>(s)] / units;
             upd_us[s] = u[static_cast<size_t>(s)] / units;
+        }
+    });
+}
+
+ferret_status ferret_trainer_profile_critical(ferret_trainer* t, double* class_ms, uint64_t* class_nodes,
+                                              int32_t n_classes) {
+    return guarded([&] {
+        if (t->crit_class_ms.empty()) fail(FERRET_E_LOGIC, "profile_critical: call ferret_trainer_profile first");
+        for (int32_t c = 0; c < n_classes && c < kNumCat; ++c) {
+            class_ms[c] = t->crit_class_ms[static_cast<size_t>(c)];
+            class_nodes[c] = t->crit_class_nodes[static_cast<size_t>(c)];
         }
     });
 }

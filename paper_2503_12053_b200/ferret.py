@@ -138,6 +138,7 @@ def lib() -> C.CDLL:
         "ferret_trainer_inbox_handle": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t]),
         "ferret_trainer_open_peer": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
         "ferret_trainer_handoff_plan": (C.c_int, [C.c_void_p, P(C.c_uint64), P(C.c_uint64), C.c_int32]),
+        "ferret_trainer_profile_critical": (C.c_int, [C.c_void_p, P(D), P(C.c_uint64), C.c_int32]),
         "ferret_trainer_profile": (C.c_int, [C.c_void_p, P(D), P(C.c_uint64), P(D), C.c_int32, P(D), P(D)]),
         "ferret_compensate": (C.c_int, [C.c_int32, P(D), P(P(D)), C.c_int32, P(D), P(D), P(D), P(D), C.c_size_t,
                                         D, D, D, D, P(D)]),
@@ -414,9 +415,14 @@ class PipelineTrainer:
         byt = (C.c_double * n)()
         crit, tot = C.c_double(), C.c_double()
         _check(lib().ferret_trainer_profile(self._h, ms, cnt, byt, n, C.byref(crit), C.byref(tot)))
+        cms = (C.c_double * n)()
+        cnn = (C.c_uint64 * n)()
+        _check(lib().ferret_trainer_profile_critical(self._h, cms, cnn, n))
         return {"classes": {k: {"ms": ms[i], "nodes": int(cnt[i]), "alg_bytes": byt[i],
                                 "gbs": (byt[i] / (ms[i] * 1e-3) / 1e9) if ms[i] > 0 else 0.0}
                             for i, k in enumerate(self.PROFILE_CLASSES)},
+                "critical_path": {k: {"ms": cms[i], "nodes": int(cnn[i])} for i, k in enumerate(self.PROFILE_CLASSES)
+                                  if cnn[i]},
                 "critical_path_ms": crit.value, "serial_ms": tot.value}
 
     # ---- stage sharding (one process per GPU; ferret_b200.h: ferret_trainer_set_shard)
