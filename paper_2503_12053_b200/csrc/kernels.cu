@@ -221,6 +221,66 @@ __global__ void __launch_bounds__(kThreads) head_kernel(const HeadArgs a) {
 // ---------------------------------------------------------------------------
 constexpr int kBwdMaxRows = 512;   // rows per split (delta staging in smem)
 
+// Small layers (out <= 256): latency, not bandwidth, bounds the node. One CTA
+// per 32 columns, every row of the layer: each warp loads its 32 rows of the
+// column strip in one trip (32 independent loads in flight per lane), the 8
+// warps reduce once through smem and the CTA writes d_in directly — no split
+// partials, no second global round trip.
+constexpr int kBwdSmallRows = 256;
+
+template <int BT>
+__global__ void __launch_bounds__(kThreads) bwd_small_kernel(const BwdArgs a) {
+    __shared__ __align__(16) float sd[kBwdSmallRows][BT];
+    __shared__ float part[kWarps][BT][33];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = blockIdx.x * 32 + lane;
+    const int B = a.B, out = a.out;
+    for (int i = threadIdx.x; i < BT * out; i += kThreads) {
+        const int b = i / out, r = i - b * out;
+        sd[r][b] = b < B ? a.d_out[(size_t)b * out + r] : 0.f;
+    }
+    float w[kBwdSmallRows / kWarps];
+    constexpr int RPW = kBwdSmallRows / kWarps;  // rows per warp
+#pragma unroll
+    for (int q = 0; q < RPW; ++q) {
+        const int r = warp + q * kWarps;
+        w[q] = (r < out && c < a.in) ? __ldg(a.W + (size_t)r * a.in + c) : 0.f;
+    }
+    __syncthreads();
+    float acc[BT];
+#pragma unroll
+    for (int b = 0; b < BT; ++b) acc[b] = 0.f;
+#pragma unroll
+    for (int q = 0; q < RPW; ++q) {
+        const int r = warp + q * kWarps;
+        if (r >= out) break;
+#pragma unroll
+        for (int b = 0; b < BT; b += (BT % 4 == 0 ? 4 : 1)) {
+            if (BT % 4 == 0) {
+                const float4 d = *reinterpret_cast<const float4*>(&sd[r][b]);
+                acc[b] = fmaf(w[q], d.x, acc[b]);
+                acc[(b + 1) % BT] = fmaf(w[q], d.y, acc[(b + 1) % BT]);
+                acc[(b + 2) % BT] = fmaf(w[q], d.z, acc[(b + 2) % BT]);
+                acc[(b + 3) % BT] = fmaf(w[q], d.w, acc[(b + 3) % BT]);
+            } else {
+                acc[b] = fmaf(w[q], sd[r][b], acc[b]);
+            }
+        }
+    }
+#pragma unroll
+    for (int b = 0; b < BT; ++b) part[warp][b][lane] = acc[b];
+    __syncthreads();
+    for (int i = threadIdx.x; i < B * 32; i += kThreads) {
+        const int b = i >> 5, cc = i & 31, col = blockIdx.x * 32 + cc;
+        if (col >= a.in) continue;
+        float v = 0.f;
+#pragma unroll
+        for (int q = 0; q < kWarps; ++q) v += part[q][b][cc];
+        if (a.mask && !(a.mask[(size_t)b * a.in + col] > 0.f)) v = 0.f;
+        a.d_in[(size_t)b * a.in + col] = v;
+    }
+}
+
 template <int BT, int V>
 __global__ void __launch_bounds__(kThreads) bwd_kernel(const BwdArgs a) {
     // deltas as [row][sample]: one row's B values are read as float4s
@@ -789,6 +849,15 @@ static const void* bwd_func(bool vec, size_t& smem) {
 }
 
 void spec_bwd(const BwdArgs& a, KernelSpec& k) {
+    if (a.out <= kBwdSmallRows) {
+        const void* f = a.B <= 1 ? reinterpret_cast<const void*>(&bwd_small_kernel<1>)
+                      : a.B <= 2 ? reinterpret_cast<const void*>(&bwd_small_kernel<2>)
+                      : a.B <= 4 ? reinterpret_cast<const void*>(&bwd_small_kernel<4>)
+                      : a.B <= 8 ? reinterpret_cast<const void*>(&bwd_small_kernel<8>)
+                                 : reinterpret_cast<const void*>(&bwd_small_kernel<16>);
+        fill(k, f, dim3((a.in + 31) / 32), dim3(kThreads), a);
+        return;
+    }
     const dim3 grid(bwd_col_tiles(a.in), a.row_splits);
     const bool vec = bwd_vec(a.in) == 4 && aligned16(a.W);
     size_t smem = 0;
