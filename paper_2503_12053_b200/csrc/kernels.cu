@@ -12,6 +12,7 @@
 
 #include <cfloat>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 namespace fb200 {
@@ -953,7 +954,11 @@ void spec_bwd(const BwdArgs& a, KernelSpec& k) {
 
 void spec_update(const UpdArgs& a, KernelSpec& k) {
     const long long blocks = a.n_tiles;
-    if (a.policy == 4 && a.K == 1 && a.nv <= 16 && a.lam_d != nullptr && a.row_blocks > 0) {
+    static const bool tiled_only = [] {  // FERRET_UPDATE_KERNEL=tile: experiment switch
+        const char* v = std::getenv("FERRET_UPDATE_KERNEL");
+        return v && std::strcmp(v, "tile") == 0;
+    }();
+    if (!tiled_only && a.policy == 4 && a.K == 1 && a.nv <= 16 && a.lam_d != nullptr && a.row_blocks > 0) {
         const void* f = a.B <= 1 ? row_func<1>(a.nv) : a.B <= 2 ? row_func<2>(a.nv) : a.B <= 4 ? row_func<4>(a.nv)
                       : a.B <= 8 ? row_func<8>(a.nv) : row_func<16>(a.nv);
         fill(k, f, dim3((unsigned)a.row_blocks), dim3(kThreads), a);
