@@ -671,90 +671,6 @@ __global__ void __launch_bounds__(kThreads) update_iter1_kernel(const UpdArgs a)
     }
 }
 
-// Row update (iter_fisher, one pending gradient, chain length NV): CTA = 256
-// consecutive parameters of one weight row (or of a bias vector). Segment
-// geometry comes from the kernel parameters; the row's B deltas are
-// warp-broadcast loads; every load of the element (NV chain versions, lambda,
-// v_r, v_a, B inputs, B deltas) is issued before any use — one memory round
-// trip per CTA, no barrier. This is the latency-bound small-stage path.
-template <int BT, int NV>
-__global__ void __launch_bounds__(kThreads) update_row_kernel(const UpdArgs a) {
-    const int blk = blockIdx.x;
-    int s = 0;
-    while (s + 1 < a.n_psegs && blk >= a.psegs[s + 1].block0) ++s;
-    const UpdSegP& sg = a.psegs[s];
-    const int t = blk - sg.block0;
-    int r, c;
-    if (sg.bias) {
-        r = t * kUpdTileCols + threadIdx.x;
-        c = 0;
-        if (r >= sg.out) return;
-    } else {
-        r = t / sg.col_tiles;
-        c = (t - r * sg.col_tiles) * kUpdTileCols + threadIdx.x;
-        if (c >= sg.in) return;
-    }
-    const size_t e = (size_t)sg.elem0 + (sg.bias ? (size_t)r : (size_t)r * sg.in + c);
-    const UpdPending& pk = a.pend[0];
-    const int B = a.B;
-    const bool learn = a.eta > 0.f && a.v_r != nullptr;
-    // ---- issue every load
-    float cv[NV];
-#pragma unroll
-    for (int i = 0; i < NV; ++i) cv[i] = __ldg(a.vers[i] + e);
-    float ld = a.lam_d[e];
-    float vr = 0.f, va = 0.f;
-    if (NV >= 2 && learn) {
-        vr = a.v_r[e];
-        va = a.v_a[e];
-    }
-    const float* dl = pk.stash + sg.dlt_off + r;
-    float d[BT], x[BT];
-#pragma unroll
-    for (int b = 0; b < BT; ++b) {
-        d[b] = b < B ? __ldg(dl + (size_t)b * sg.out) : 0.f;
-        if (sg.bias) {
-            x[b] = 1.f;
-        } else {
-            const float* xr = sg.xin_off >= 0 ? pk.stash + sg.xin_off + (size_t)b * sg.in
-                              : a.x0idx       ? pk.x0 + (size_t)__ldg(a.x0idx + b) * a.x0_ld
-                                              : pk.x0 + (size_t)b * a.x0_ld;
-            x[b] = b < B ? __ldg(xr + c) : 0.f;
-        }
-    }
-    // ---- gW element, compensation (compensate.hpp:87-102), SGD step
-    float g = 0.f;
-#pragma unroll
-    for (int b = 0; b < BT; ++b) g = fmaf(d[b], x[b], g);
-    float lam = a.lambda0 + ld;
-    if (NV >= 2 && learn) {
-        const float one_m_a = 1.f - a.alpha;
-        const float dv = one_m_a * (g - vr);
-        const float resid = dv - lam * va;
-        const float grad_l = -2.f * resid * va + 2.f * a.nu * lam;
-        ld -= a.eta * grad_l;
-        lam = a.lambda0 + ld;
-        a.v_r[e] = a.alpha * vr + one_m_a * g;
-        a.v_a[e] = a.alpha * va + one_m_a * g * g * (cv[NV >= 2 ? 1 : 0] - cv[0]);
-        a.lam_d[e] = ld;
-    }
-    float o = g;
-#pragma unroll
-    for (int i = 0; i + 1 < NV; ++i) o += lam * o * o * (cv[i + 1] - cv[i]);
-    a.dst[e] = cv[NV - 1] - a.step * o;
-}
-
-template <int BT>
-const void* row_func(int nv) {
-    switch (nv) {
-#define FB_NV(n) case n: return reinterpret_cast<const void*>(&update_row_kernel<BT, n>);
-        FB_NV(1) FB_NV(2) FB_NV(3) FB_NV(4) FB_NV(5) FB_NV(6) FB_NV(7) FB_NV(8)
-        FB_NV(9) FB_NV(10) FB_NV(11) FB_NV(12) FB_NV(13) FB_NV(14) FB_NV(15) FB_NV(16)
-#undef FB_NV
-        default: return nullptr;
-    }
-}
-
 template <int BT>
 const void* iter1_func(int nv) {
     switch (nv) {
@@ -954,16 +870,6 @@ void spec_bwd(const BwdArgs& a, KernelSpec& k) {
 
 void spec_update(const UpdArgs& a, KernelSpec& k) {
     const long long blocks = a.n_tiles;
-    static const bool tiled_only = [] {  // FERRET_UPDATE_KERNEL=tile: experiment switch
-        const char* v = std::getenv("FERRET_UPDATE_KERNEL");
-        return v && std::strcmp(v, "tile") == 0;
-    }();
-    if (!tiled_only && a.policy == 4 && a.K == 1 && a.nv <= 16 && a.lam_d != nullptr && a.row_blocks > 0) {
-        const void* f = a.B <= 1 ? row_func<1>(a.nv) : a.B <= 2 ? row_func<2>(a.nv) : a.B <= 4 ? row_func<4>(a.nv)
-                      : a.B <= 8 ? row_func<8>(a.nv) : row_func<16>(a.nv);
-        fill(k, f, dim3((unsigned)a.row_blocks), dim3(kThreads), a);
-        return;
-    }
     if (a.policy == 4 && a.K == 1 && a.nv <= 16 && a.lam_d != nullptr) {
         const void* f = a.B <= 1 ? iter1_func<1>(a.nv) : a.B <= 2 ? iter1_func<2>(a.nv) : a.B <= 4 ? iter1_func<4>(a.nv)
                       : a.B <= 8 ? iter1_func<8>(a.nv) : iter1_func<16>(a.nv);

@@ -88,15 +88,6 @@ struct UpdTile {
     int c0;     // first column (weights)
 };
 
-// Segment geometry carried in the kernel parameters by the row-update kernel:
-// CTA b of the launch works on segment s with block0[s] <= b < block0[s+1].
-struct UpdSegP {
-    int bias, in, out, col_tiles;  // col_tiles = ceil(in / 256) for weights
-    int block0;                    // first CTA of this segment
-    int pad;
-    long long elem0, xin_off, dlt_off;
-};
-
 struct UpdPending {
     const float* stash;   // the unit's stash slot (activations + deltas)
     const float* x0;      // net-input rows of the unit (when the stage holds layer 0)
@@ -114,9 +105,6 @@ struct UpdArgs {
     const UpdSeg* segs;      // device array
     const UpdTile* tiles;    // device array, one per CTA
     int n_tiles;
-    UpdSegP psegs[2 * kMaxStageLayers];  // row-update kernel: segment geometry by CTA range
-    int n_psegs;
-    int row_blocks;                      // CTAs of the row-update kernel
     UpdPending pend[kMaxPending];
     const int* x0idx;        // nullable: net-input row b is x0 + x0idx[b] * x0_ld (replay), else x0 + b * x0_ld
     int x0_ld;
@@ -183,7 +171,7 @@ struct KernelSpec {
     const void* func = nullptr;
     dim3 grid, block;
     size_t smem = 0;
-    alignas(16) unsigned char arg0[4096];  // the kernel's struct argument
+    alignas(16) unsigned char arg0[2048];  // the kernel's struct argument
     int arg1 = 0;                         // optional trailing int argument
     int nargs = 1;
     void* params[2];

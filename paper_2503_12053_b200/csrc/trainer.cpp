@@ -140,8 +140,6 @@ struct StageDev {
     fb200::UpdSeg* segs_dev = nullptr;
     int n_segs = 0;
     fb200::UpdTile* tiles_dev = nullptr;
-    std::vector<fb200::UpdSegP> psegs;  // row-update kernel geometry
-    int row_blocks = 0;
     int n_tiles = 0;
     long long n_items = 0;
     // slot of a version counted from the chunk start (the live version is in slot 0 between chunks)
@@ -615,11 +613,11 @@ struct ferret_trainer {
             cuda_check(cudaMemcpy(s.segs_dev, tab.data(), tab.size() * sizeof(fb200::UpdSeg), cudaMemcpyHostToDevice),
                        "upload segment table");
             // update tiles: rows x 256 columns per CTA, the row count chosen so a
-            // stage update spans a few hundred CTAs (>= 2 per SM)
+            // stage update spans ~8 CTAs per SM (one row per tile for small stages: latency-bound)
             long long row_tiles = 0;
             for (const fb200::UpdSeg& sg : tab)
                 if (!sg.bias) row_tiles += static_cast<long long>(sg.out) * ((sg.in + fb200::kUpdTileCols - 1) / fb200::kUpdTileCols);
-            const int R = static_cast<int>(std::min<long long>(fb200::kUpdMaxTileRows, std::max<long long>(1, (row_tiles + 399) / 400)));
+            const int R = static_cast<int>(std::min<long long>(fb200::kUpdMaxTileRows, std::max<long long>(1, (row_tiles + 1183) / 1184)));
             std::vector<fb200::UpdTile> tiles;
             for (size_t q = 0; q < tab.size(); ++q) {
                 const fb200::UpdSeg& sg = tab[q];
@@ -633,19 +631,6 @@ struct ferret_trainer {
                 }
             }
             s.n_tiles = static_cast<int>(tiles.size());
-            for (const fb200::UpdSeg& sg : tab) {
-                fb200::UpdSegP p{};
-                p.bias = sg.bias;
-                p.in = sg.in;
-                p.out = sg.out;
-                p.col_tiles = (sg.in + fb200::kUpdTileCols - 1) / fb200::kUpdTileCols;
-                p.block0 = s.row_blocks;
-                p.elem0 = sg.elem0;
-                p.xin_off = sg.xin_off;
-                p.dlt_off = sg.dlt_off;
-                s.psegs.push_back(p);
-                s.row_blocks += sg.bias ? (sg.out + fb200::kUpdTileCols - 1) / fb200::kUpdTileCols : sg.out * p.col_tiles;
-            }
             s.tiles_dev = dalloc<fb200::UpdTile>(tiles.size(), device_bytes);
             cuda_check(cudaMemcpy(s.tiles_dev, tiles.data(), tiles.size() * sizeof(fb200::UpdTile), cudaMemcpyHostToDevice),
                        "upload tile table");
@@ -1264,10 +1249,6 @@ struct ferret_trainer {
         a.segs = s.segs_dev;
         a.tiles = s.tiles_dev;
         a.n_tiles = s.n_tiles;
-        // small stages (latency-bound): the row-update kernel with the geometry in parameters
-        a.n_psegs = static_cast<int>(s.psegs.size());
-        for (size_t q = 0; q < s.psegs.size(); ++q) a.psegs[q] = s.psegs[q];
-        a.row_blocks = s.n_params <= (8ll << 20) ? s.row_blocks : 0;
         a.x0idx = nullptr;
         a.x0_ld = F;
         if (cur - oldest + 1 > fb200::kMaxChain)
