@@ -613,11 +613,12 @@ struct ferret_trainer {
             cuda_check(cudaMemcpy(s.segs_dev, tab.data(), tab.size() * sizeof(fb200::UpdSeg), cudaMemcpyHostToDevice),
                        "upload segment table");
             // update tiles: rows x 256 columns per CTA, the row count chosen so a
-            // stage update spans ~8 CTAs per SM (one row per tile for small stages: latency-bound)
+            // stage update spans ~400 CTAs (measured: faster than one-row tiles,
+            // whose per-CTA setup then dominates; profiles/README.md)
             long long row_tiles = 0;
             for (const fb200::UpdSeg& sg : tab)
                 if (!sg.bias) row_tiles += static_cast<long long>(sg.out) * ((sg.in + fb200::kUpdTileCols - 1) / fb200::kUpdTileCols);
-            const int R = static_cast<int>(std::min<long long>(fb200::kUpdMaxTileRows, std::max<long long>(1, (row_tiles + 1183) / 1184)));
+            const int R = static_cast<int>(std::min<long long>(fb200::kUpdMaxTileRows, std::max<long long>(1, (row_tiles + 399) / 400)));
             std::vector<fb200::UpdTile> tiles;
             for (size_t q = 0; q < tab.size(); ++q) {
                 const fb200::UpdSeg& sg = tab[q];
