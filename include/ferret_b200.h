@@ -57,7 +57,12 @@ enum { FERRET_ACT_RELU = 0, FERRET_ACT_IDENTITY = 1 };
 /* StepOutcome, metrics.hpp:15 */
 enum { FERRET_STEP_CORRECT = 0, FERRET_STEP_WRONG = 1, FERRET_STEP_DROPPED = 2 };
 /* arithmetic of the device path (no reference counterpart: the reference is fp64) */
-enum { FERRET_PREC_FP32 = 0, FERRET_PREC_BF16 = 1 };
+/* FP32: parity mode (SIMT fp32, 1e-4 parameter parity with the fp64 oracle).
+ * BF16 / TF32: fast modes — dense-layer forward and input-gradient on the
+ * tcgen05 tensor cores (bf16 copies of the weight versions, or tf32 reads of
+ * the fp32 versions), fp32 accumulation; the compensation + SGD update stays
+ * fp32 on the fp32 master versions. Parity bar: online accuracy within 0.5 pp. */
+enum { FERRET_PREC_FP32 = 0, FERRET_PREC_BF16 = 1, FERRET_PREC_TF32 = 2 };
 
 /* DenseNet, net.hpp:20-51. params in flatten() order (learner.hpp:26-34):
  * per layer W (row-major out x in) then b. */
@@ -286,6 +291,20 @@ FERRET_API ferret_status ferret_compensate(int32_t policy, const double* g, cons
                                 int32_t chain_len, double* lambda, double* v_r, double* v_a,
                                 double* mean_gap, size_t n, double lambda0, double alpha,
                                 double eta_lambda, double nu, double* out);
+
+/* ---------------- unit entry: one dense layer on the tensor cores ---------------- */
+
+/* One dense layer of the fast modes (tcgen05.mma, TMA-fed, TMEM accumulator),
+ * host fp32 buffers in and out; precision FERRET_PREC_TF32 or FERRET_PREC_BF16
+ * (W and X rounded to bf16 on the device path, fp32 accumulation).
+ *   direction 0 — affine_forward + apply_activation (net.hpp:99-113):
+ *       Y[b][r] = act(sum_c W[r][c] X[b][c] + bias[r]); X: B x in, Y: B x out; act = ReLU if relu
+ *   direction 1 — the input gradient of learner.hpp:468-474:
+ *       Y[b][c] = [mask[b][c] > 0] * sum_r W[r][c] X[b][r]; X: B x out, Y (and mask, nullable): B x in
+ * W is out x in row-major; 1 <= B <= 16. */
+FERRET_API ferret_status ferret_dense_layer(int32_t precision, int32_t direction, const float* W, const float* bias,
+                                            const float* X, const float* mask, int32_t B, int32_t in, int32_t out,
+                                            int32_t relu, float* Y);
 
 #ifdef __cplusplus
 }

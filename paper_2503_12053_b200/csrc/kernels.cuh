@@ -12,6 +12,7 @@
 #include <cstddef>
 #include <cstdint>
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace fb200 {
@@ -171,7 +172,7 @@ struct KernelSpec {
     const void* func = nullptr;
     dim3 grid, block;
     size_t smem = 0;
-    alignas(16) unsigned char arg0[2048];  // the kernel's struct argument
+    alignas(64) unsigned char arg0[2048];  // the kernel's struct argument
     int arg1 = 0;                         // optional trailing int argument
     int nargs = 1;
     void* params[2];
@@ -184,6 +185,39 @@ struct KernelSpec {
         return params;
     }
 };
+
+// Fast precision modes: one dense layer (forward or input-gradient) on the
+// tensor cores, tcgen05.mma kind::tf32 on the fp32 weights or kind::f16 on a
+// bf16 copy, A streamed by TMA, fp32 accumulator in TMEM (mma.cu).
+struct MmaArgs {
+    CUtensorMap tmap;      // W (out x in, row-major) as a TMA tensor
+    const float* bias;     // forward
+    const float* X;        // B operand rows (K-major): row n at X + (xidx ? xidx[n] : n) * ldx
+    const int* xidx;
+    const float* mask;     // backward: ReLU mask of the layer below (nullable)
+    float* Y;              // output: element (m, n) at Y[n * ldy + m]
+    int M, K, N, ldx, ldy;
+    int katoms, atoms_per_cta, stages;
+    int relu, vec;
+};
+struct MmaLayer {
+    const void* W;         // fp32 (tf32 mode) or bf16 weights, out x in row-major
+    bool bwd = false;      // false: Y = act(W X + b); true: Y = mask * (W^T X)
+    bool bf16 = false;
+    const float* bias = nullptr;
+    const float* X = nullptr;
+    const int* xidx = nullptr;
+    const float* mask = nullptr;
+    float* Y = nullptr;
+    int in = 0, out = 0, B = 0, relu = 0;
+};
+struct MmaGeom {
+    int mtiles, katoms, S, apc, stages;
+    size_t smem;
+};
+bool mma_supported(bool bf16, int in, int out);
+MmaGeom mma_geom(bool bf16, bool bwd, int in, int out);
+void spec_mma(const MmaLayer& L, KernelSpec& k);
 
 void spec_fwd(const FwdArgs& a, KernelSpec& k);
 void spec_head(const HeadArgs& a, KernelSpec& k);

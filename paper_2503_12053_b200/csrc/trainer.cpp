@@ -69,6 +69,15 @@ void cuda_check(cudaError_t e, const char* what) {
 
 long long align_up(long long v, long long a) { return (v + a - 1) / a * a; }
 
+// fp32 -> bf16 bits, round to nearest even (the device's __float2bfloat16_rn)
+uint16_t bf16_bits(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7FFFFFFFu) > 0x7F800000u) return static_cast<uint16_t>((u >> 16) | 0x40u);  // NaN stays NaN
+    u += 0x7FFFu + ((u >> 16) & 1u);
+    return static_cast<uint16_t>(u >> 16);
+}
+
 template <class T>
 T* dalloc(size_t n, size_t& counter) {
     void* p = nullptr;
@@ -1874,6 +1883,65 @@ ferret_status ferret_trainer_update_timing(ferret_trainer* t, double* total_ms, 
         *total_ms = ms;
         *launches = t->graph_timing ? t->upd_timed : 0;
         *alg_bytes = t->graph_timing ? t->upd_alg_bytes : 0.0;
+    });
+}
+
+ferret_status ferret_dense_layer(int32_t precision, int32_t direction, const float* W, const float* bias,
+                                 const float* X, const float* mask, int32_t B, int32_t in, int32_t out, int32_t relu,
+                                 float* Y) {
+    return guarded([&] {
+        if (precision != FERRET_PREC_TF32 && precision != FERRET_PREC_BF16)
+            fail(FERRET_E_CONFIG, "dense_layer: precision must be FERRET_PREC_TF32 or FERRET_PREC_BF16");
+        if (direction != 0 && direction != 1) fail(FERRET_E_INVALID_ARG, "dense_layer: direction must be 0 or 1");
+        if (B < 1 || B > fb200::kMaxBatch) fail(FERRET_E_INVALID_ARG, "dense_layer: batch must lie in [1, 16]");
+        if (in < 1 || out < 1) fail(FERRET_E_INVALID_ARG, "dense_layer: empty layer");
+        if (!W || !X || !Y || (direction == 0 && !bias)) fail(FERRET_E_INVALID_ARG, "dense_layer: null buffer");
+        const bool bf16 = precision == FERRET_PREC_BF16;
+        if (!fb200::mma_supported(bf16, in, out))
+            fail(FERRET_E_CONFIG, "dense_layer: row stride of W must be a multiple of 16 bytes");
+        require_device(0);
+        const size_t nw = static_cast<size_t>(in) * out;
+        const size_t nx = static_cast<size_t>(B) * (direction == 0 ? in : out);
+        const size_t ny = static_cast<size_t>(B) * (direction == 0 ? out : in);
+        size_t bytes = 0;
+        std::vector<void*> bufs;
+        struct Cleanup {
+            std::vector<void*>& b;
+            ~Cleanup() {
+                for (void* p : b) cudaFree(p);
+            }
+        } cleanup{bufs};
+        auto up = [&](const void* src, size_t nbytes) {
+            unsigned char* d = dalloc<unsigned char>(nbytes, bytes);
+            bufs.push_back(d);
+            if (src) cuda_check(cudaMemcpy(d, src, nbytes, cudaMemcpyHostToDevice), "H2D");
+            return d;
+        };
+        void* dW;
+        if (bf16) {
+            std::vector<uint16_t> h(nw);
+            for (size_t i = 0; i < nw; ++i) h[i] = bf16_bits(W[i]);
+            dW = up(h.data(), nw * 2);
+        } else {
+            dW = up(W, nw * 4);
+        }
+        fb200::MmaLayer L;
+        L.W = dW;
+        L.bwd = direction == 1;
+        L.bf16 = bf16;
+        L.bias = direction == 0 ? reinterpret_cast<const float*>(up(bias, static_cast<size_t>(out) * 4)) : nullptr;
+        L.X = reinterpret_cast<const float*>(up(X, nx * 4));
+        L.mask = direction == 1 && mask ? reinterpret_cast<const float*>(up(mask, ny * 4)) : nullptr;
+        L.Y = reinterpret_cast<float*>(up(nullptr, ny * 4));
+        L.in = in;
+        L.out = out;
+        L.B = B;
+        L.relu = relu;
+        fb200::KernelSpec k;
+        fb200::spec_mma(L, k);
+        cuda_check(fb200::launch_spec(k, nullptr), "dense_layer launch");
+        cuda_check(cudaDeviceSynchronize(), "dense_layer");
+        cuda_check(cudaMemcpy(Y, L.Y, ny * 4, cudaMemcpyDeviceToHost), "D2H");
     });
 }
 

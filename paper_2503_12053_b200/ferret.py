@@ -32,6 +32,7 @@ PROFILE_DTYPE = np.dtype([("t_f", "<f8"), ("t_b", "<f8"), ("w", "<u8"), ("a", "<
 EV_ARRIVAL, EV_DROP, EV_FORWARD, EV_RECOMPUTE, EV_BACKWARD, EV_UPDATE = range(6)
 POLICIES = {"none": 0, "step": 1, "gap": 2, "fisher": 3, "iter_fisher": 4}
 DRIFTS = {"none": 0, "rotate": 1, "split_tasks": 2}
+PRECISIONS = {"fp32": 0, "bf16": 1, "tf32": 2}
 ACTS = {"relu": 0, "identity": 1}
 STEP_CORRECT, STEP_WRONG, STEP_DROPPED = 0, 1, 2
 NO_BUDGET = (1 << 64) - 1  # kNoBudget, types.hpp:29
@@ -140,6 +141,8 @@ def lib() -> C.CDLL:
         "ferret_trainer_handoff_plan": (C.c_int, [C.c_void_p, P(C.c_uint64), P(C.c_uint64), C.c_int32]),
         "ferret_trainer_profile_critical": (C.c_int, [C.c_void_p, P(D), P(C.c_uint64), C.c_int32]),
         "ferret_trainer_profile": (C.c_int, [C.c_void_p, P(D), P(C.c_uint64), P(D), C.c_int32, P(D), P(D)]),
+        "ferret_dense_layer": (C.c_int, [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                         C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]),
         "ferret_compensate": (C.c_int, [C.c_int32, P(D), P(P(D)), C.c_int32, P(D), P(D), P(D), P(D), C.c_size_t,
                                         D, D, D, D, P(D)]),
     }
@@ -289,6 +292,7 @@ class PipelineTrainOptions:
     micro_batch: int = 1
     device: int = 0
     as_shipped: bool = False
+    precision: str = "fp32"  # fp32 parity mode, or the tensor-core fast modes bf16 / tf32
 
     def c(self) -> TrainOpts:
         o = TrainOpts()
@@ -301,6 +305,7 @@ class PipelineTrainOptions:
         o.micro_batch = self.micro_batch
         o.device = self.device
         o.as_shipped = int(self.as_shipped)
+        o.precision = PRECISIONS[self.precision]
         return o
 
 
@@ -481,6 +486,25 @@ def train_pipeline(widths, params, bounds, events, features, labels, opt=Pipelin
         return log, t.params()
     finally:
         t.close()
+
+
+def dense_layer(precision: str, direction: int, W: np.ndarray, X: np.ndarray, bias=None, mask=None,
+                relu: bool = False) -> np.ndarray:
+    """One dense layer on the tensor cores (tcgen05, fast modes): direction 0 is
+    affine_forward + activation (net.hpp:99-113), Y = act(X W^T + b) with X: B x in;
+    direction 1 is the input gradient (learner.hpp:468-474), Y = [mask > 0] * (X W)
+    with X: B x out."""
+    W = np.ascontiguousarray(W, dtype=np.float32)
+    X = np.ascontiguousarray(X, dtype=np.float32)
+    out_f, in_f = W.shape
+    B = X.shape[0]
+    Y = np.empty((B, out_f if direction == 0 else in_f), dtype=np.float32)
+    b = np.ascontiguousarray(bias, dtype=np.float32) if bias is not None else None
+    m = np.ascontiguousarray(mask, dtype=np.float32) if mask is not None else None
+    _check(lib().ferret_dense_layer(PRECISIONS[precision], direction, W.ctypes.data, b.ctypes.data if b is not None else None,
+                                    X.ctypes.data, m.ctypes.data if m is not None else None, B, in_f, out_f, int(relu),
+                                    Y.ctypes.data))
+    return Y
 
 
 def compensate(policy: str, g: np.ndarray, chain: Sequence[np.ndarray], lam=None, v_r=None, v_a=None,
