@@ -10,6 +10,8 @@
 // All fp32 except the normalizer (fp64, bit-exact with the host).
 #include "kernels.cuh"
 
+#include <cuda_bf16.h>
+
 #include <cfloat>
 #include <cstdio>
 #include <cstdlib>
@@ -578,7 +580,9 @@ __global__ void __launch_bounds__(kThreads) update_tile_kernel(const UpdArgs a) 
                 mean += compensate_elem<POLICY>(g, a.vers, a.pend[k].first, last, e, th, st, a.lambda0, a.alpha, a.eta,
                                                 a.nu, learn);
         }
-        a.dst[e] = th - a.step * mean;
+        const float nv = th - a.step * mean;
+        a.dst[e] = nv;
+        if (a.dst16) reinterpret_cast<__nv_bfloat16*>(a.dst16)[e] = __float2bfloat16_rn(nv);
         if (POLICY == 4) {
             a.lam_d[e] = st.ld;
             if (learn) {
@@ -635,7 +639,9 @@ __global__ void __launch_bounds__(kThreads) update_iter1_kernel(const UpdArgs a)
         float o = g;  // compensate.hpp:99-102
 #pragma unroll
         for (int s = 0; s + 1 < NV; ++s) o += lam * o * o * (cv[s + 1] - cv[s]);
-        a.dst[e] = cv[NV - 1] - a.step * o;
+        const float nv = cv[NV - 1] - a.step * o;
+        a.dst[e] = nv;
+        if (a.dst16) reinterpret_cast<__nv_bfloat16*>(a.dst16)[e] = __float2bfloat16_rn(nv);
     };
     if (sg.bias) {
         if (tid >= R) return;

@@ -112,6 +112,7 @@ struct UpdArgs {
     const float* vers[kMaxChain]; // oldest needed version .. current (vers[nv-1])
     int nv;
     float* dst;              // new version slot
+    unsigned short* dst16;   // bf16 fast mode: the slot's bf16 copy read by the tensor-core layers (nullable)
     float* lam_d;   // iter_fisher: lambda - lambda0 (fp32 offset keeps the ~1e-10 drift)
     float* v_r;
     float* v_a;

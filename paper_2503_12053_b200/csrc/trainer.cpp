@@ -142,6 +142,7 @@ struct StageDev {
     long long n_params = 0, slot_floats = 0, host_off = 0;
     int depth = 0;
     float* ring = nullptr;
+    uint16_t* ring16 = nullptr;  // bf16 fast mode: bf16 copy of every ring slot (tensor-core operand)
     float* lam_d = nullptr;
     float* v_r = nullptr;
     float* v_a = nullptr;
@@ -153,6 +154,8 @@ struct StageDev {
     long long n_items = 0;
     // slot of a version counted from the chunk start (the live version is in slot 0 between chunks)
     float* slot(long long rel) const { return ring + (rel % depth) * slot_floats; }
+    // the bf16 copy of the slot a float pointer into the ring lies in
+    const uint16_t* shadow(const float* p) const { return ring16 + (p - ring); }
 };
 
 // Schedule facts independent of the mutable state (computed once per log).
@@ -535,7 +538,8 @@ struct ferret_trainer {
         B = opt.micro_batch;
         if (B < 1 || B > fb200::kMaxBatch) fail(FERRET_E_CONFIG, "micro_batch must lie in [1, 16]");
         if (opt.policy < 0 || opt.policy > 4) fail(FERRET_E_CONFIG, "unknown compensation policy");
-        if (opt.precision != FERRET_PREC_FP32) fail(FERRET_E_CONFIG, "only the fp32 parity precision is built");
+        if (opt.precision != FERRET_PREC_FP32 && opt.precision != FERRET_PREC_BF16 && opt.precision != FERRET_PREC_TF32)
+            fail(FERRET_E_CONFIG, "precision must be FERRET_PREC_FP32, FERRET_PREC_BF16 or FERRET_PREC_TF32");
         if (opt.replay && (opt.replay_capacity == 0 || opt.replay_capacity > (1ull << 30)))
             fail(FERRET_E_CONFIG, "replay capacity must lie in [1, 2^30]");
         layers.resize(static_cast<size_t>(L));
@@ -687,6 +691,12 @@ struct ferret_trainer {
             }
             cuda_check(cudaMemcpy(s.slot(0), slot.data(), slot.size() * sizeof(float), cudaMemcpyHostToDevice),
                        "upload params");
+            if (s.ring16) {
+                std::vector<uint16_t> h(slot.size());
+                for (size_t i = 0; i < slot.size(); ++i) h[i] = bf16_bits(slot[i]);
+                cuda_check(cudaMemcpy(s.ring16, h.data(), h.size() * sizeof(uint16_t), cudaMemcpyHostToDevice),
+                           "upload bf16 params");
+            }
         }
     }
 
@@ -703,6 +713,18 @@ struct ferret_trainer {
             device_bytes -= static_cast<size_t>(s.depth) * static_cast<size_t>(s.slot_floats) * sizeof(float);
         }
         s.ring = fresh;
+        if (opt.precision == FERRET_PREC_BF16) {
+            uint16_t* fresh16 =
+                dalloc<uint16_t>(static_cast<size_t>(depth) * static_cast<size_t>(s.slot_floats), device_bytes);
+            if (s.ring16) {
+                cuda_check(cudaMemcpy(fresh16, s.ring16, static_cast<size_t>(s.slot_floats) * sizeof(uint16_t),
+                                      cudaMemcpyDeviceToDevice),
+                           "ring copy");
+                cudaFree(s.ring16);
+                device_bytes -= static_cast<size_t>(s.depth) * static_cast<size_t>(s.slot_floats) * sizeof(uint16_t);
+            }
+            s.ring16 = fresh16;
+        }
         s.depth = depth;
     }
 
@@ -1228,6 +1250,9 @@ struct ferret_trainer {
                     gb->cur_bytes = 8.0 * static_cast<double>(s.slot_floats);
                     gb->copy(s.ring, s.slot(fin), static_cast<size_t>(s.slot_floats) * sizeof(float), {vslot(j, fin)},
                              {vslot(j, 0)});
+                    if (s.ring16)
+                        gb->copy(s.ring16, s.shadow(s.slot(fin)), static_cast<size_t>(s.slot_floats) * sizeof(uint16_t),
+                                 {vslot(j, fin)}, {vslot(j, 0)});
                 }
             }
             stats.events = sched.events.size();
@@ -1266,6 +1291,7 @@ struct ferret_trainer {
         a.nv = static_cast<int>(cur - oldest + 1);
         for (long long v = oldest; v <= cur; ++v) a.vers[v - oldest] = s.slot(v);
         a.dst = s.slot(cur + 1);
+        a.dst16 = s.ring16 ? const_cast<uint16_t*>(s.shadow(a.dst)) : nullptr;
         a.lam_d = s.lam_d;
         a.v_r = s.v_r;
         a.v_a = s.v_a;
@@ -1279,8 +1305,38 @@ struct ferret_trainer {
 
     // ----------------------------------------------------- node helpers
     // One dense layer on B samples (input row b = X + (xidx ? xidx[b] : b) * in).
+    // fast modes: this layer's forward / input gradient runs on the tensor cores
+    bool use_mma(const LayerDev& ld) const {
+        return opt.precision != FERRET_PREC_FP32 && fb200::mma_supported(opt.precision == FERRET_PREC_BF16, ld.in, ld.out);
+    }
+    void emit_mma(const LayerDev& ld, const float* stage_slot, bool bwd, const float* X, const int* xidx,
+                  const float* mask, float* Y, const std::vector<uint64_t>& reads, const std::vector<uint64_t>& writes) {
+        const bool bf16 = opt.precision == FERRET_PREC_BF16;
+        const StageDev& s = stages[static_cast<size_t>(ld.stage)];
+        fb200::MmaLayer m;
+        m.W = bf16 ? static_cast<const void*>(s.shadow(stage_slot + ld.woff)) : static_cast<const void*>(stage_slot + ld.woff);
+        m.bwd = bwd;
+        m.bf16 = bf16;
+        m.bias = bwd ? nullptr : stage_slot + ld.boff;
+        m.X = X;
+        m.xidx = xidx;
+        m.mask = mask;
+        m.Y = Y;
+        m.in = ld.in;
+        m.out = ld.out;
+        m.B = B;
+        m.relu = !bwd && ld.act == FERRET_ACT_RELU;
+        fb200::KernelSpec k;
+        if (!plan_only) fb200::spec_mma(m, k);
+        const double wbytes = (bf16 ? 2.0 : 4.0) * ld.in * ld.out;
+        gb->cur_bytes = bwd ? wbytes + 4.0 * B * (ld.out + 2.0 * ld.in)
+                            : wbytes + 4.0 * ld.out + 4.0 * B * (ld.in + ld.out);
+        gb->kernel(k, reads, writes);
+    }
+
     void emit_layer(const LayerDev& ld, const float* stage_slot, const float* X, const int* xidx, float* Y,
                     const std::vector<uint64_t>& reads, const std::vector<uint64_t>& writes) {
+        if (use_mma(ld)) return emit_mma(ld, stage_slot, false, X, xidx, nullptr, Y, reads, writes);
         fb200::FwdArgs a{};
         a.W = stage_slot + ld.woff;
         a.bias = stage_slot + ld.boff;
@@ -1388,6 +1444,10 @@ struct ferret_trainer {
                              uint64_t stash_key, bool mask_on_write = true) {
         const LayerDev& ld = layers[static_cast<size_t>(l)];
         const LayerDev& below = layers[static_cast<size_t>(l - 1)];
+        if (use_mma(ld))
+            return emit_mma(ld, slot, true, stash_u + ld.dlt_off,  nullptr,
+                            mask_on_write && below.act == FERRET_ACT_RELU ? stash_u + below.act_off : nullptr,
+                            stash_u + below.dlt_off, reads, {stash_key});
         fb200::BwdArgs a{};
         a.W = slot + ld.woff;
         a.d_out = stash_u + ld.dlt_off;
