@@ -475,6 +475,8 @@ __device__ __forceinline__ float compensate_elem(float g, const float* const* ve
 // weight row, or one bias), grid-stride over the stage's segments.
 // ---------------------------------------------------------------------------
 constexpr int kRegChain = 12;  // chain versions the iter_fisher fold keeps in registers
+// iter_fisher K = 1 chains longer than this take the smem-staged update_stream_kernel
+constexpr int kStreamMinChain = 16;
 
 // iter_fisher (compensate.hpp:82-104) for one element with the chain values
 // already in registers: cv[i] = version i (i < last), th = version `last`.
@@ -677,6 +679,172 @@ __global__ void __launch_bounds__(kThreads) update_iter1_kernel(const UpdArgs a)
     }
 }
 
+// ---------------------------------------------------------------------------
+// iter_fisher with one pending gradient and a chain of any length (<= 48
+// versions: the deep pipelines of config 5 reach tau ~ 16-32). The version
+// chain, not the arithmetic, is the cost: (nv + 3) x 4 bytes read and 16
+// written per parameter. Each weight row of the tile is staged in smem with
+// cp.async.bulk (one 1 KB bulk copy per version and state array, completing
+// on an mbarrier), double-buffered so the copies of row i+1 are in flight
+// while row i folds; the fold reads the chain from smem (consecutive threads,
+// consecutive words). Bias tiles and rows that are not 16-byte aligned take
+// direct loads. Arithmetic order is exactly update_iter1_kernel's.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+template <int BT>
+__global__ void __launch_bounds__(kThreads) update_stream_kernel(const UpdArgs a) {
+    extern __shared__ __align__(128) float sbuf[];  // 2 buffers x (nv + 3) x 256 floats
+    __shared__ float sdel[kMaxBatch * kUpdMaxTileRows];
+    __shared__ __align__(8) uint64_t full[2];
+    const UpdTile t = a.tiles[blockIdx.x];
+    const UpdSeg sg = a.segs[t.seg];
+    const int B = a.B, R = t.nrows, tid = threadIdx.x, nv = a.nv;
+    const bool learn = a.eta > 0.f && a.v_r != nullptr;
+    const UpdPending& pk = a.pend[0];
+    const float one_m_a = 1.f - a.alpha;
+    // fold of one element given accessors for chain version i and the state
+    auto fold = [&](size_t e, float g, auto ver, float ld, float vr, float va) {
+        float lam = a.lambda0 + ld;
+        if (nv >= 2 && learn) {  // compensate.hpp:87-98
+            const float dv = one_m_a * (g - vr);
+            const float resid = dv - lam * va;
+            const float grad_l = -2.f * resid * va + 2.f * a.nu * lam;
+            ld -= a.eta * grad_l;
+            lam = a.lambda0 + ld;
+            vr = a.alpha * vr + one_m_a * g;
+            va = a.alpha * va + one_m_a * g * g * (ver(1) - ver(0));
+            a.v_r[e] = vr;
+            a.v_a[e] = va;
+            a.lam_d[e] = ld;
+        }
+        float o = g;  // compensate.hpp:99-102
+        float prev = ver(0);
+        for (int s = 1; s < nv; ++s) {
+            const float nxt = ver(s);
+            o += lam * o * o * (nxt - prev);
+            prev = nxt;
+        }
+        const float nvv = prev - a.step * o;
+        a.dst[e] = nvv;
+        if (a.dst16) reinterpret_cast<__nv_bfloat16*>(a.dst16)[e] = __float2bfloat16_rn(nvv);
+    };
+    auto fold_global = [&](size_t e, float g) {
+        fold(e, g, [&](int i) { return __ldg(a.vers[i] + e); }, a.lam_d[e], learn ? a.v_r[e] : 0.f,
+             learn ? a.v_a[e] : 0.f);
+    };
+    if (sg.bias) {
+        if (tid >= R) return;
+        const int r = t.r0 + tid;
+        const float* dl = pk.stash + sg.dlt_off + r;
+        float g = 0.f;
+#pragma unroll
+        for (int b = 0; b < BT; ++b)
+            if (b < B) g += __ldg(dl + (size_t)b * sg.out);
+        fold_global((size_t)sg.elem0 + r, g);
+        return;
+    }
+    for (int i = tid; i < B * R; i += kThreads) {
+        const int b = i / R, rr = i - b * R;
+        sdel[i] = __ldg(pk.stash + sg.dlt_off + (size_t)b * sg.out + t.r0 + rr);
+    }
+    const int c = t.c0 + tid;
+    const int ncols = min(kUpdTileCols, sg.in - t.c0);
+    float xv[BT];
+#pragma unroll
+    for (int b = 0; b < BT; ++b) {
+        const float* xr = sg.xin_off >= 0 ? pk.stash + sg.xin_off + (size_t)b * sg.in
+                          : a.x0idx       ? pk.x0 + (size_t)__ldg(a.x0idx + b) * a.x0_ld
+                                          : pk.x0 + (size_t)b * a.x0_ld;
+        xv[b] = (b < B && c < sg.in) ? __ldg(xr + c) : 0.f;
+    }
+    const bool staged = (sg.in & 3) == 0;  // 16-byte aligned rows (every version slot is 128-byte aligned)
+    if (!staged) {
+        __syncthreads();
+        if (c >= sg.in) return;
+        for (int i = 0; i < R; ++i) {
+            float g = 0.f;
+#pragma unroll
+            for (int b = 0; b < BT; ++b) g = fmaf(sdel[b * R + i], xv[b], g);
+            fold_global((size_t)sg.elem0 + (size_t)(t.r0 + i) * sg.in + c, g);
+        }
+        return;
+    }
+    const int nbuf = nv + 3;  // versions, lambda offset, v_r, v_a
+    const uint32_t row_bytes = static_cast<uint32_t>(ncols) * 4u;
+    auto buf = [&](int bsel, int k) { return sbuf + ((size_t)bsel * nbuf + k) * kUpdTileCols; };
+    auto issue = [&](int i) {  // warp 0: bulk copies of row i into buffer i & 1
+        const int bs = i & 1;
+        const size_t e0 = (size_t)sg.elem0 + (size_t)(t.r0 + i) * sg.in + t.c0;
+        const int ncopy = nv + (learn ? 3 : 1);
+        if (tid == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&full[bs])),
+                         "r"(row_bytes * ncopy)
+                         : "memory");
+        }
+        __syncwarp();
+        for (int k = tid; k < ncopy; k += 32) {
+            const float* src = k < nv ? a.vers[k] + e0 : k == nv ? a.lam_d + e0 : k == nv + 1 ? a.v_r + e0 : a.v_a + e0;
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_addr(buf(bs, k))),
+                "l"(src), "r"(row_bytes), "r"(smem_addr(&full[bs]))
+                : "memory");
+        }
+    };
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&full[0])) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&full[1])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid < 32) {
+        issue(0);
+        if (R > 1) issue(1);
+    }
+    for (int i = 0; i < R; ++i) {
+        const int bs = i & 1;
+        {
+            const uint32_t addr = smem_addr(&full[bs]), parity = (i >> 1) & 1;
+            uint32_t done = 0;
+            while (!done)
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                    "selp.u32 %0, 1, 0, p;\n\t}"
+                    : "=r"(done)
+                    : "r"(addr), "r"(parity)
+                    : "memory");
+        }
+        if (tid < ncols) {
+            float g = 0.f;
+#pragma unroll
+            for (int b = 0; b < BT; ++b) g = fmaf(sdel[b * R + i], xv[b], g);
+            const float* base = buf(bs, 0) + tid;
+            fold((size_t)sg.elem0 + (size_t)(t.r0 + i) * sg.in + c, g,
+                 [&](int k) { return base[(size_t)k * kUpdTileCols]; }, base[(size_t)nv * kUpdTileCols],
+                 learn ? base[(size_t)(nv + 1) * kUpdTileCols] : 0.f, learn ? base[(size_t)(nv + 2) * kUpdTileCols] : 0.f);
+        }
+        if (i + 2 < R) {
+            __syncthreads();  // every thread is done with buffer bs
+            if (tid < 32) issue(i + 2);
+        }
+    }
+}
+
+template <int BT>
+const void* stream_func(size_t smem) {
+    static size_t configured = 0;  // (static smem counts against the 48 KB default too)
+    const void* f = reinterpret_cast<const void*>(&update_stream_kernel<BT>);
+    if (smem > configured) {
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = smem;
+    }
+    return f;
+}
+
 template <int BT>
 const void* iter1_func(int nv) {
     switch (nv) {
@@ -876,6 +1044,18 @@ void spec_bwd(const BwdArgs& a, KernelSpec& k) {
 
 void spec_update(const UpdArgs& a, KernelSpec& k) {
     const long long blocks = a.n_tiles;
+    // FERRET_STREAM_MIN_CHAIN (test / experiment knob): chain length above which
+    // the smem-staged kernel takes over from the register-resident one
+    const char* env = std::getenv("FERRET_STREAM_MIN_CHAIN");
+    const int min_chain = env ? std::atoi(env) : kStreamMinChain;
+    if (a.policy == 4 && a.K == 1 && a.nv > min_chain && a.lam_d != nullptr) {
+        const size_t smem = sizeof(float) * 2 * (size_t)(a.nv + 3) * kUpdTileCols;
+        const void* f = a.B <= 1 ? stream_func<1>(smem) : a.B <= 2 ? stream_func<2>(smem) : a.B <= 4 ? stream_func<4>(smem)
+                      : a.B <= 8 ? stream_func<8>(smem) : stream_func<16>(smem);
+        fill(k, f, dim3((unsigned)blocks), dim3(kThreads), a);
+        k.smem = smem;
+        return;
+    }
     if (a.policy == 4 && a.K == 1 && a.nv <= 16 && a.lam_d != nullptr) {
         const void* f = a.B <= 1 ? iter1_func<1>(a.nv) : a.B <= 2 ? iter1_func<2>(a.nv) : a.B <= 4 ? iter1_func<4>(a.nv)
                       : a.B <= 8 ? iter1_func<8>(a.nv) : iter1_func<16>(a.nv);

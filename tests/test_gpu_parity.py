@@ -198,3 +198,22 @@ def test_spec_kats_on_device(gpu, fb):
     assert abs(out[0] - 1.0) < 1e-7
     out = fb.compensate("gap", np.array([2.0]), [np.array([0.0]), np.array([0.5])], mean_gap=np.array([0.5]))
     assert abs(out[0] - 1.0) < 1e-7
+
+
+def test_deep_pipeline_long_chains(gpu, fb, orc):
+    """Eight stages of a narrow deep MLP: trainer staleness reaches ~16 versions, so the
+    iter_fisher updates of the early stages fold chains longer than 16 (the smem-staged
+    update_stream_kernel); fp32 parity with the oracle as for every other config."""
+    widths = [64] * 9 + [10]
+    params, feats, labels, sched = _setup(fb, widths, 160, bounds=[0, 1, 2, 3, 4, 5, 6, 7, 9])
+    _compare(fb, orc, widths, params, feats, labels, sched, "iter_fisher")
+
+
+@pytest.mark.parametrize("replay", [False, True])
+def test_stream_update_kernel_everywhere(gpu, fb, orc, monkeypatch, replay):
+    """Force every K = 1 iter_fisher update through update_stream_kernel (chain threshold 0)
+    and check the same oracle bar as the register-resident kernel."""
+    monkeypatch.setenv("FERRET_STREAM_MIN_CHAIN", "0")
+    widths = [784, 256, 256, 256, 10]
+    params, feats, labels, sched = _setup(fb, widths, 120, bounds=[0, 1, 2, 3, 4])
+    _compare(fb, orc, widths, params, feats, labels, sched, "iter_fisher", replay=replay)
