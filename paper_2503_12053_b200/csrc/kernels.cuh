@@ -200,6 +200,10 @@ struct MmaArgs {
     int M, K, N, ldx, ldy;
     int katoms, atoms_per_cta, stages;
     int relu, vec;
+    int splits;            // CTAs splitting K per M tile
+    float* partial;        // split-K scratch: mtiles x splits x 16 x 128 floats
+    unsigned* counters;    // one per M tile, zero between launches (self-resetting)
+    unsigned long long* stamps;  // nullable: 8 phase timestamps per CTA (measurement)
 };
 struct MmaLayer {
     const void* W;         // fp32 (tf32 mode) or bf16 weights, out x in row-major
@@ -211,10 +215,14 @@ struct MmaLayer {
     const float* mask = nullptr;
     float* Y = nullptr;
     int in = 0, out = 0, B = 0, relu = 0;
+    float* partial = nullptr;     // split-K scratch (MmaGeom::partial_floats), nullable when S == 1
+    unsigned* counters = nullptr; // MmaGeom::mtiles zeroed counters
+    unsigned long long* stamps = nullptr;
 };
 struct MmaGeom {
     int mtiles, katoms, S, apc, stages;
     size_t smem;
+    size_t partial_floats;
 };
 bool mma_supported(bool bf16, int in, int out);
 MmaGeom mma_geom(bool bf16, bool bwd, int in, int out);

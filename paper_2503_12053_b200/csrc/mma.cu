@@ -14,8 +14,7 @@
 // so the weight matrix is streamed from HBM exactly once per launch, by TMA,
 // in its stored row-major layout, with no transposed copy.
 //
-// CTA = 4 warps. The grid is (S, ceil(M/128)) with S CTAs per cluster
-// splitting K. Per CTA:
+// CTA = 4 warps. The grid is (S, ceil(M/128)), S CTAs splitting K. Per CTA:
 //   * all 128 threads stage the B operand of the CTA's K range (16 x K_cta,
 //     converted to the MMA type, 128-byte swizzled K-major) in smem once;
 //   * warp 0 / lane 0 streams 16 KB A tiles (128 x 128 bytes) through an
@@ -23,9 +22,14 @@
 //   * warp 1 / lane 0 issues tcgen05.mma (M = 128, N = 16, fp32 accumulator in
 //     32 TMEM columns) — 4 MMAs per 16 KB tile — and tcgen05.commit frees the slot;
 //   * all 4 warps read the 128 x 16 accumulator back with tcgen05.ld (warp w
-//     owns TMEM lanes 32w..32w+31 = rows m0+32w..), the S partials of a cluster
-//     are summed in rank order through distributed shared memory (deterministic),
-//     and the epilogue applies bias + ReLU (forward) or the ReLU mask (backward).
+//     owns TMEM lanes 32w..32w+31 = rows m0+32w..); with S > 1 the partial tile
+//     goes to L2 scratch and the last CTA of the M tile sums the S partials in
+//     split order (deterministic), then applies bias + ReLU (forward) or the
+//     ReLU mask (backward).
+// The grid is sized to one wave of one CTA per SM with the deepest A ring the
+// shared memory holds (the first version used 8-CTA clusters and a DSMEM
+// reduction: cluster residency capped it at 120 co-resident CTAs, two waves,
+// 21 % of HBM bandwidth — profiles/README.md).
 //
 // At micro-batch 16 a weight feeds 16 MACs: ~8 flop per 4-byte (tf32) or 16
 // flop per 2-byte (bf16) element — far under the tensor ridge, so the kernel is
@@ -33,25 +37,24 @@
 // SIMT issue bound.
 #include "kernels.cuh"
 
-#include <cooperative_groups.h>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
-
-namespace cg = cooperative_groups;
 
 namespace fb200 {
 
 namespace {
 
-constexpr int kMmaThreads = 128;
+constexpr int kMmaThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 stage B; warps 2-5 run the epilogue
+constexpr int kStagers = 256;
 constexpr int kTileBytes = 16384;      // A tile per pipeline stage: 128 rows x 128 bytes
 constexpr int kBAtomBytes = 16 * 128;  // B operand per 128-byte K atom: 16 rows x 128 bytes
-constexpr int kRedStride = 17;         // padded row of the split-K partial tile
+constexpr size_t kMaxSmem = 225 * 1024;  // opt-in dynamic shared memory per CTA (227 KB less static)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -127,8 +130,8 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 }
 
 // ES = operand bytes (4: tf32 from fp32, 2: bf16); BWD = A is MN-major (W^T).
-template <int ES, bool BWD, int S>
-__global__ void __cluster_dims__(S, 1, 1) __launch_bounds__(kMmaThreads, 1) mma_layer_kernel(const __grid_constant__ MmaArgs a) {
+template <int ES, bool BWD>
+__global__ void __launch_bounds__(kMmaThreads, 1) mma_layer_kernel(const __grid_constant__ MmaArgs a) {
     constexpr int KA = 128 / ES;       // K elements per 128-byte atom
     constexpr int UK = 32 / ES;        // K per tcgen05.mma (32 bytes of operand)
     constexpr bool TF32 = ES == 4;
@@ -137,14 +140,25 @@ __global__ void __cluster_dims__(S, 1, 1) __launch_bounds__(kMmaThreads, 1) mma_
     const int nst = a.stages;
     unsigned char* sA = base;
     unsigned char* sB = sA + nst * kTileBytes;
-    float* red = reinterpret_cast<float*>(sB + a.atoms_per_cta * kBAtomBytes);
-    uint64_t* full = reinterpret_cast<uint64_t*>(red + 128 * kRedStride);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + a.atoms_per_cta * kBAtomBytes);
     uint64_t* empty = full + nst;
     uint64_t* done = empty + nst;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+    uint64_t* bready = done + 1;  // per B atom: staged by the 64 threads of warps 2-3
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bready + a.atoms_per_cta);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int q = S > 1 ? static_cast<int>(cg::this_cluster().block_rank()) : 0;
+    const int S = a.splits, q = blockIdx.x;
+    // optional phase timestamps (globaltimer ns) per CTA: start, setup done,
+    // B staged, first A tile landed, accumulator done, exit
+    unsigned long long* stamp = a.stamps ? a.stamps + (static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * 8 : nullptr;
+    auto tick = [&](int k) {
+        if (stamp) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            stamp[k] = t;
+        }
+    };
+    if (threadIdx.x == 0) tick(0);
     const int m0 = blockIdx.y * 128;
     const int a_lo = q * a.atoms_per_cta;
     const int a_hi = min(a.katoms, a_lo + a.atoms_per_cta);
@@ -157,65 +171,21 @@ __global__ void __cluster_dims__(S, 1, 1) __launch_bounds__(kMmaThreads, 1) mma_
             mbar_init(empty + s, 1);
         }
         mbar_init(done, 1);
+        for (int i = 0; i < na; ++i) mbar_init(bready + i, kStagers);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(smem_u32(tmem_slot)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-
-    // ---- B operand: rows n < B of the CTA's K range, 16-byte chunks, swizzled
-    // chunk j of row n lands at (n/8)*1024 + (n%8)*128 + ((j ^ n%8) * 16)
-    {
-        const int chunks = na * 16 * 8;  // atoms x rows x 16-byte chunks
-        for (int e = threadIdx.x; e < chunks; e += kMmaThreads) {
-            const int j = e & 7, n = (e >> 3) & 15, at = e >> 7;
-            const int k0 = (a_lo + at) * KA + j * (16 / ES);
-            float v[16 / ES];
-#pragma unroll
-            for (int i = 0; i < 16 / ES; ++i) v[i] = 0.f;
-            if (n < a.N) {
-                const float* row = a.X + static_cast<size_t>(a.xidx ? __ldg(a.xidx + n) : n) * a.ldx;
-                if (k0 + 16 / ES <= a.K && a.vec) {
-                    if constexpr (ES == 4) {
-                        const float4 t = __ldg(reinterpret_cast<const float4*>(row + k0));
-                        v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
-                    } else {
-                        const float4 t0 = __ldg(reinterpret_cast<const float4*>(row + k0));
-                        const float4 t1 = __ldg(reinterpret_cast<const float4*>(row + k0 + 4));
-                        v[0] = t0.x; v[1] = t0.y; v[2] = t0.z; v[3] = t0.w;
-                        v[4] = t1.x; v[5] = t1.y; v[6] = t1.z; v[7] = t1.w;
-                    }
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 16 / ES; ++i)
-                        if (k0 + i < a.K) v[i] = __ldg(row + k0 + i);
-                }
-            }
-            unsigned char* dst = sB + at * kBAtomBytes + (n >> 3) * 1024 + (n & 7) * 128 + ((j ^ (n & 7)) << 4);
-            if constexpr (ES == 4) {
-                *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
-            } else {
-                uint4 p;
-                __nv_bfloat162 h0 = __floats2bfloat162_rn(v[0], v[1]), h1 = __floats2bfloat162_rn(v[2], v[3]);
-                __nv_bfloat162 h2 = __floats2bfloat162_rn(v[4], v[5]), h3 = __floats2bfloat162_rn(v[6], v[7]);
-                p.x = *reinterpret_cast<uint32_t*>(&h0);
-                p.y = *reinterpret_cast<uint32_t*>(&h1);
-                p.z = *reinterpret_cast<uint32_t*>(&h2);
-                p.w = *reinterpret_cast<uint32_t*>(&h3);
-                *reinterpret_cast<uint4*>(dst) = p;
-            }
-        }
-    }
-    // generic-proxy smem writes -> visible to the tensor core (async proxy)
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) tick(1);
 
     if (warp == 0 && lane == 0 && na > 0) {
-        // ---- TMA producer
+        // ---- TMA producer: one 16 KB A tile per ring stage
         for (int i = 0; i < na; ++i) {
             const int s = i % nst;
             if (i >= nst) mbar_wait(empty + s, ((i / nst) - 1) & 1);
@@ -238,7 +208,9 @@ __global__ void __cluster_dims__(S, 1, 1) __launch_bounds__(kMmaThreads, 1) mma_
                                ((128u >> 4) << 24);
         for (int i = 0; i < na; ++i) {
             const int s = i % nst;
+            mbar_wait(bready + i, 0);
             mbar_wait(full + s, (i / nst) & 1);
+            if (i == 0) tick(3);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t abase = smem_u32(sA + s * kTileBytes);
             const uint32_t bbase = smem_u32(sB + i * kBAtomBytes);
@@ -257,54 +229,134 @@ __global__ void __cluster_dims__(S, 1, 1) __launch_bounds__(kMmaThreads, 1) mma_
             umma_commit(empty + s);
         }
         umma_commit(done);
+    } else if (warp >= 2) {
+        // ---- B operand, staged by warps 2-9 while A streams: rows n < N of the
+        // CTA's K range as 16-byte chunks, swizzled: chunk j of row n lands at
+        // (n/8)*1024 + (n%8)*128 + ((j ^ n%8) * 16). Rows n >= N stay unwritten
+        // (D column n depends on B row n only; those columns are never stored).
+        // Thread t owns chunk column j = t % 8 of row n = (t / 8) % 16 in atoms
+        // t / 128, t / 128 + 2, ... of each round of G atoms, so its row pointer
+        // is resolved once and a round's U loads have no dependence on each
+        // other; each staged atom is published on its mbarrier after a proxy fence.
+        constexpr int CE = 16 / ES, G = 16, U = G * 128 / kStagers;  // elements/chunk, atoms/round, chunks/thread
+        const int t = threadIdx.x - 64, j = t & 7, n = (t >> 3) & 15, ao = t >> 7;
+        const bool rowv = n < a.N;
+        const float* rowp = rowv ? a.X + static_cast<size_t>(a.xidx ? __ldg(a.xidx + n) : n) * a.ldx : a.X;
+        for (int g0 = 0; g0 < na; g0 += G) {
+            float v[U][CE];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int at = g0 + ao + 2 * u;
+                const int k0 = (a_lo + at) * KA + j * CE;
+                const float* src = rowp + k0;
+                if (at < na && rowv && a.vec && k0 + CE <= a.K) {
+#pragma unroll
+                    for (int c = 0; c < CE / 4; ++c) {
+                        const float4 x4 = __ldg(reinterpret_cast<const float4*>(src) + c);
+                        v[u][4 * c] = x4.x; v[u][4 * c + 1] = x4.y; v[u][4 * c + 2] = x4.z; v[u][4 * c + 3] = x4.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < CE; ++i) v[u][i] = (at < na && rowv && k0 + i < a.K) ? __ldg(src + i) : 0.f;
+                }
+            }
+            if (rowv) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int at = g0 + ao + 2 * u;
+                    if (at >= na) continue;
+                    unsigned char* dst = sB + at * kBAtomBytes + (n >> 3) * 1024 + (n & 7) * 128 + ((j ^ (n & 7)) << 4);
+                    if constexpr (ES == 4) {
+                        *reinterpret_cast<float4*>(dst) = make_float4(v[u][0], v[u][1], v[u][2], v[u][3]);
+                    } else {
+                        uint4 p;
+                        __nv_bfloat162 h0 = __floats2bfloat162_rn(v[u][0], v[u][1]), h1 = __floats2bfloat162_rn(v[u][2], v[u][3]);
+                        __nv_bfloat162 h2 = __floats2bfloat162_rn(v[u][4], v[u][5]), h3 = __floats2bfloat162_rn(v[u][6], v[u][7]);
+                        p.x = *reinterpret_cast<uint32_t*>(&h0);
+                        p.y = *reinterpret_cast<uint32_t*>(&h1);
+                        p.z = *reinterpret_cast<uint32_t*>(&h2);
+                        p.w = *reinterpret_cast<uint32_t*>(&h3);
+                        *reinterpret_cast<uint4*>(dst) = p;
+                    }
+                }
+            }
+            // generic-proxy smem writes -> visible to the tensor core (async proxy)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            for (int at = g0; at < min(na, g0 + G); ++at)
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bready + at)) : "memory");
+        }
+        if (threadIdx.x == 64) tick(2);
     }
     __syncwarp();
 
-    // ---- epilogue: TMEM -> registers (thread = row m, 16 columns n)
-    float acc[16];
-    if (na > 0) {
-        mbar_wait(done, 0);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16), acc);
-    } else {
+    // ---- epilogue, warps 2-5: TMEM -> registers (warp w reads TMEM lanes of
+    // quadrant w % 4: thread = accumulator row m0 + row, 16 columns n)
+    if (warp >= 2 && warp < 6) {
+        const int row = (warp & 3) * 32 + lane;
+        float acc[16];
+        if (na > 0) {
+            mbar_wait(done, 0);
+            if (warp == 2 && lane == 0) tick(4);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            tmem_ld16(tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16), acc);
+        } else {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) acc[i] = 0.f;
-    }
-    const int row = threadIdx.x;  // accumulator row m0 + row
-
-    auto finish = [&](int m, int n, float v) {
-        if (m >= a.M || n >= a.N) return;
-        const size_t o = static_cast<size_t>(n) * a.ldy + m;
-        if (!BWD) {
-            v += __ldg(a.bias + m);
-            if (a.relu) v = v > 0.f ? v : 0.f;
-        } else if (a.mask) {
-            v = __ldg(a.mask + o) > 0.f ? v : 0.f;
+            for (int i = 0; i < 16; ++i) acc[i] = 0.f;
         }
-        a.Y[o] = v;
-    };
-
-    if (S == 1) {
+        auto finish = [&](int m, int nn, float v) {
+            if (m >= a.M || nn >= a.N) return;
+            const size_t o = static_cast<size_t>(nn) * a.ldy + m;
+            if (!BWD) {
+                v += __ldg(a.bias + m);
+                if (a.relu) v = v > 0.f ? v : 0.f;
+            } else if (a.mask) {
+                v = __ldg(a.mask + o) > 0.f ? v : 0.f;
+            }
+            a.Y[o] = v;
+        };
+        if (S == 1) {
 #pragma unroll
-        for (int n = 0; n < 16; ++n) finish(m0 + row, n, acc[n]);
-    } else {
+            for (int nn = 0; nn < 16; ++nn) finish(m0 + row, nn, acc[nn]);
+        } else {
+            // split-K: partial tile to global scratch ([n][128], coalesced); the last
+            // CTA of the M tile to arrive sums the S partials in split order
+            // (deterministic) and runs the epilogue
+            float* part = a.partial + (static_cast<size_t>(blockIdx.y) * S + q) * 128 * 16;
 #pragma unroll
-        for (int n = 0; n < 16; ++n) red[row * kRedStride + n] = acc[n];
-        cg::cluster_group cl = cg::this_cluster();
-        cl.sync();
-        // CTA q of the cluster finishes rows [q*R, (q+1)*R), summing the S
-        // partials in rank order
-        constexpr int R = 128 / S;
-        for (int e = threadIdx.x; e < R * 16; e += kMmaThreads) {
-            const int r = q * R + (e % R), n = e / R;
-            float v = 0.f;
+            for (int nn = 0; nn < 16; ++nn) part[nn * 128 + row] = acc[nn];
+            __threadfence();
+            asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps
+            __shared__ unsigned last;
+            if (warp == 2 && lane == 0) last = atomicAdd(a.counters + blockIdx.y, 1u) == static_cast<unsigned>(S - 1);
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (last) {
+                __threadfence();
+                // sum in split order; this CTA's own partial is still in registers,
+                // the others' 16 values per split are loaded together
+                const float* base = a.partial + static_cast<size_t>(blockIdx.y) * S * 128 * 16 + row;
+                float v[16];
 #pragma unroll
-            for (int p = 0; p < S; ++p) v += cl.map_shared_rank(red, p)[r * kRedStride + n];
-            finish(m0 + r, n, v);
+                for (int nn = 0; nn < 16; ++nn) v[nn] = 0.f;
+                for (int p = 0; p < S; ++p) {
+                    float tv[16];
+                    if (p == q) {
+#pragma unroll
+                        for (int nn = 0; nn < 16; ++nn) tv[nn] = acc[nn];
+                    } else {
+#pragma unroll
+                        for (int nn = 0; nn < 16; ++nn) tv[nn] = __ldcg(base + (static_cast<size_t>(p) * 16 + nn) * 128);
+                    }
+#pragma unroll
+                    for (int nn = 0; nn < 16; ++nn) v[nn] += tv[nn];
+                }
+#pragma unroll
+                for (int nn = 0; nn < 16; ++nn) finish(m0 + row, nn, v[nn]);
+                if (warp == 2 && lane == 0) a.counters[blockIdx.y] = 0u;  // self-resetting (graph replays)
+            }
         }
-        cl.sync();  // peers keep their smem until every partial is read
     }
 
+    if (warp == 2 && lane == 0) tick(5);
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 1) {
@@ -326,25 +378,15 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-template <int ES, bool BWD, int S>
+template <int ES, bool BWD>
 const void* mma_func(size_t smem) {
     static size_t configured = 0;  // > 48 KB dynamic smem needs an opt-in per function
-    const void* f = reinterpret_cast<const void*>(&mma_layer_kernel<ES, BWD, S>);
+    const void* f = reinterpret_cast<const void*>(&mma_layer_kernel<ES, BWD>);
     if (smem > configured) {
         cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         configured = smem;
     }
     return f;
-}
-
-template <int ES, bool BWD>
-const void* mma_func_s(int S, size_t smem) {
-    switch (S) {
-        case 1: return mma_func<ES, BWD, 1>(smem);
-        case 2: return mma_func<ES, BWD, 2>(smem);
-        case 4: return mma_func<ES, BWD, 4>(smem);
-        default: return mma_func<ES, BWD, 8>(smem);
-    }
 }
 
 }  // namespace
@@ -361,15 +403,22 @@ MmaGeom mma_geom(bool bf16, bool bwd, int in, int out) {
     const int M = bwd ? in : out, K = bwd ? out : in;
     g.mtiles = (M + 127) / 128;
     g.katoms = static_cast<int>((static_cast<long long>(K) * es + 127) / 128);
-    // ~256 CTAs (<= 2 per SM, all resident) so the weight stream has enough
-    // bytes in flight; the cluster splits K and reduces through DSMEM
-    int S = 1;
-    while (S < 8 && g.mtiles * S * 2 <= 256 && S * 2 <= g.katoms) S *= 2;
-    g.S = S;
+    // one wave of one CTA per SM: the K splits of an M tile are separate CTAs
+    // (partials reduced through L2 by the last one), every CTA streams its A
+    // slice through the deepest TMA ring its shared memory holds
+    int S = 148 / g.mtiles;
+    if (S > 16) S = 16;
+    if (S > g.katoms) S = g.katoms;
+    if (S < 1) S = 1;
+    if (const char* env = std::getenv("FERRET_MMA_SPLIT")) S = std::atoi(env);  // experiment knob
     g.apc = (g.katoms + S - 1) / S;
-    g.stages = g.apc < 4 ? g.apc : 4;
-    g.smem = 1024 + static_cast<size_t>(g.stages) * kTileBytes + static_cast<size_t>(g.apc) * kBAtomBytes +
-             128 * kRedStride * sizeof(float) + (2 * g.stages + 1) * 8 + 16;
+    g.S = (g.katoms + g.apc - 1) / g.apc;  // every split owns >= 1 atom
+    const size_t fixed = 1024 + static_cast<size_t>(g.apc) * (kBAtomBytes + 8) + 256;
+    g.stages = static_cast<int>((kMaxSmem - fixed) / kTileBytes);
+    if (g.stages > g.apc) g.stages = g.apc;
+    if (g.stages > 16) g.stages = 16;
+    g.smem = fixed + static_cast<size_t>(g.stages) * kTileBytes;
+    g.partial_floats = g.S > 1 ? static_cast<size_t>(g.mtiles) * g.S * 128 * 16 : 0;
     return g;
 }
 
@@ -406,9 +455,17 @@ void spec_mma(const MmaLayer& L, KernelSpec& k) {
     a.atoms_per_cta = g.apc;
     a.stages = g.stages;
     a.relu = L.relu;
+    a.splits = g.S;
+    a.partial = L.partial;
+    a.counters = L.counters;
+    a.stamps = L.stamps;
+    if (g.S > 1 && (!L.partial || !L.counters)) {
+        std::fprintf(stderr, "ferret-b200: split-K dense layer without scratch\n");
+        std::abort();
+    }
     a.vec = (a.ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(L.X) & 15u) == 0);
-    const void* f = es == 2 ? (L.bwd ? mma_func_s<2, true>(g.S, g.smem) : mma_func_s<2, false>(g.S, g.smem))
-                            : (L.bwd ? mma_func_s<4, true>(g.S, g.smem) : mma_func_s<4, false>(g.S, g.smem));
+    const void* f = es == 2 ? (L.bwd ? mma_func<2, true>(g.smem) : mma_func<2, false>(g.smem))
+                            : (L.bwd ? mma_func<4, true>(g.smem) : mma_func<4, false>(g.smem));
     static_assert(sizeof(MmaArgs) <= sizeof(k.arg0), "kernel argument too large");
     k.func = f;
     k.grid = dim3(g.S, g.mtiles);

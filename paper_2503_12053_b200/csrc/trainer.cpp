@@ -34,8 +34,11 @@
 // delta, B x width); the replay pool (capacity x F normalised rows + labels).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <memory>
 #include <string>
 #include <vector>
@@ -505,6 +508,11 @@ struct ferret_trainer {
             dfree(s.gap);
             dfree(s.segs_dev);
             dfree(s.tiles_dev);
+            dfree(s.ring16);
+        }
+        for (auto& kv : mma_scratch) {
+            dfree(kv.second.first);
+            dfree(kv.second.second);
         }
         for (void* p : {static_cast<void*>(d_raw), static_cast<void*>(d_lab), static_cast<void*>(d_pred),
                         static_cast<void*>(d_norm_mean), static_cast<void*>(d_norm_m2), static_cast<void*>(d_rawc),
@@ -1305,6 +1313,29 @@ struct ferret_trainer {
 
     // ----------------------------------------------------- node helpers
     // One dense layer on B samples (input row b = X + (xidx ? xidx[b] : b) * in).
+    // split-K scratch of the tensor-core layers, one region per written resource
+    // (nodes writing the same resource are serialised by the DAG, so they can
+    // share it); allocated while the graph is built, counters zeroed
+    std::map<uint64_t, std::pair<float*, unsigned*>> mma_scratch;
+    size_t mma_partial_floats = 0, mma_counter_n = 0;
+    std::pair<float*, unsigned*> mma_scratch_for(uint64_t key) {
+        auto it = mma_scratch.find(key);
+        if (it != mma_scratch.end()) return it->second;
+        if (!mma_partial_floats) {
+            const bool bf16 = opt.precision == FERRET_PREC_BF16;
+            for (const LayerDev& ld : layers)
+                for (bool bwd : {false, true}) {
+                    const fb200::MmaGeom g = fb200::mma_geom(bf16, bwd, ld.in, ld.out);
+                    mma_partial_floats = std::max(mma_partial_floats, g.partial_floats);
+                    mma_counter_n = std::max(mma_counter_n, static_cast<size_t>(g.mtiles));
+                }
+        }
+        float* p = dalloc<float>(std::max<size_t>(mma_partial_floats, 1), device_bytes);
+        unsigned* c = dalloc<unsigned>(mma_counter_n, device_bytes);
+        if (c) cuda_check(cudaMemset(c, 0, mma_counter_n * sizeof(unsigned)), "memset");
+        return mma_scratch[key] = {p, c};
+    }
+
     // fast modes: this layer's forward / input gradient runs on the tensor cores
     bool use_mma(const LayerDev& ld) const {
         return opt.precision != FERRET_PREC_FP32 && fb200::mma_supported(opt.precision == FERRET_PREC_BF16, ld.in, ld.out);
@@ -1326,6 +1357,7 @@ struct ferret_trainer {
         m.out = ld.out;
         m.B = B;
         m.relu = !bwd && ld.act == FERRET_ACT_RELU;
+        if (!plan_only) std::tie(m.partial, m.counters) = mma_scratch_for(writes.at(0));
         fb200::KernelSpec k;
         if (!plan_only) fb200::spec_mma(m, k);
         const double wbytes = (bf16 ? 2.0 : 4.0) * ld.in * ld.out;
@@ -1997,10 +2029,34 @@ ferret_status ferret_dense_layer(int32_t precision, int32_t direction, const flo
         L.out = out;
         L.B = B;
         L.relu = relu;
+        const fb200::MmaGeom g = fb200::mma_geom(bf16, L.bwd, in, out);
+        if (g.partial_floats) {
+            L.partial = reinterpret_cast<float*>(up(nullptr, g.partial_floats * 4));
+            L.counters = reinterpret_cast<unsigned*>(up(nullptr, static_cast<size_t>(g.mtiles) * 4));
+            cuda_check(cudaMemset(L.counters, 0, static_cast<size_t>(g.mtiles) * 4), "memset");
+        }
+        // FERRET_MMA_STAMPS=<file>: append the per-CTA phase timestamps (measurement)
+        const char* stamp_file = std::getenv("FERRET_MMA_STAMPS");
+        const size_t n_stamps = static_cast<size_t>(g.S) * g.mtiles * 8;
+        if (stamp_file) {
+            L.stamps = reinterpret_cast<unsigned long long*>(up(nullptr, n_stamps * 8));
+            cuda_check(cudaMemset(L.stamps, 0, n_stamps * 8), "memset");
+        }
         fb200::KernelSpec k;
         fb200::spec_mma(L, k);
         cuda_check(fb200::launch_spec(k, nullptr), "dense_layer launch");
         cuda_check(cudaDeviceSynchronize(), "dense_layer");
+        if (stamp_file) {
+            std::vector<unsigned long long> h(n_stamps);
+            cuda_check(cudaMemcpy(h.data(), L.stamps, n_stamps * 8, cudaMemcpyDeviceToHost), "D2H");
+            if (FILE* f = std::fopen(stamp_file, "a")) {
+                std::fprintf(f, "layer %d %d %d %d %d\n", precision, direction, in, out, g.S * g.mtiles);
+                for (size_t i = 0; i < n_stamps; i += 8)
+                    std::fprintf(f, "%llu %llu %llu %llu %llu %llu\n", h[i], h[i + 1], h[i + 2], h[i + 3], h[i + 4],
+                                 h[i + 5]);
+                std::fclose(f);
+            }
+        }
         cuda_check(cudaMemcpy(Y, L.Y, ny * 4, cudaMemcpyDeviceToHost), "D2H");
     });
 }
