@@ -119,32 +119,42 @@ def _traffic(cls):
         return json.load(f).get(cls)
 
 
-def large_stage_roofline(fb, device):
-    """The same kernels on a config-5-shaped stage: MLP 4096-4096-4096-10 split [0,2,3] (stage 0 =
-    two 4096x4096 layers, 33.6 M params), iter_fisher, micro-batch 16, a short forced schedule,
-    run in profile mode; reports per-class achieved GB/s (HBM-bound at this size)."""
-    widths, bounds, units = [4096, 4096, 4096, 10], [0, 2, 3], 24
-    prof = fb.profile_from_widths(widths)
-    t_d = float(prof["t_f"].max())
-    sched = fb.Schedule.forced(prof, t_d, fb.StreamSpec(t_d=t_d, horizon=units * t_d), bounds, units)
-    chunk = units * MICRO_BATCH
-    feats, labels = fb.synth_drift_stream(3 * chunk, widths[0], widths[-1], "split_tasks", 7)
-    tr = fb.PipelineTrainer(widths, fb.make_dense_net(widths, 1), bounds,
-                            fb.PipelineTrainOptions(policy=POLICY, micro_batch=MICRO_BATCH, device=device))
-    tr.load_stream(feats, labels)
-    tr.set_schedule(sched.events, chunk)
-    tr.execute(0)
-    tr.set_profiling(True)
-    tr.execute(1)
-    p = tr.profile()
-    st = tr.stats()
-    tr.close()
-    classes = {k: v for k, v in p["classes"].items() if v["nodes"] > 0}
+def config5_roofline(fb, torch, device):
+    """BASELINE config 5 on one GPU: MLP 16x4096+10, 8 stages [0,2,...,16], iter_fisher,
+    micro-batch 16, bf16 fast mode (tcgen05 layers + fp32 compensation/SGD over HBM version
+    rings), 32 units per chunk (steady-state staleness). samples/s from CUDA events on the
+    trainer's stream (L2 flushed between chunks), per-class rooflines from one profiled chunk
+    (profiles/c5_fast.py)."""
+    from profiles.c5_fast import measure
+
+    r = measure(fb, torch, "bf16", units=32, steps=2, device=device)
     peak, kind = _peaks()
-    return {"workload": "stage 0 of MLP 4096-4096-4096-10, bounds [0,2,3], iter_fisher, micro-batch 16, "
-                        f"{units} units", "classes": classes,
-            "update_frac_of_hbm_peak": classes["update"]["gbs"] / peak, "peak": peak, "peak_kind": kind,
-            "mean_tau": st["mean_tau"], "ring_depth": st["ring_depth"]}
+    tflops = None
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            tflops = json.load(f).get("bf16_tflops")
+    tot = sum(v["alg_bytes"] for v in r["classes"].values())
+    out = {"workload": "C5: MLP 16x4096+10, 8 stages [0,2,...,16] on one GPU, iter_fisher, micro-batch 16, bf16 fast mode",
+           "value": r["samples_per_s"], "unit": "samples/s", "ms_per_chunk": r["ms_per_chunk"],
+           "samples_per_chunk": r["samples_per_chunk"], "dtype": "bf16 layers, f32 update",
+           "step_achieved_gbs": tot / (r["ms_per_chunk"] * 1e-3) / 1e9, "peak": peak, "peak_kind": kind,
+           "classes": r["classes"], "critical_ms": r["critical_ms"], "serial_ms": r["serial_ms"],
+           "ring_depth": r["ring_depth"], "mean_tau": r["mean_tau"], "device_gb": r["device_gb"]}
+    out["step_frac"] = out["step_achieved_gbs"] / peak
+    # the tensor-core layer kernels: weight-stream bandwidth and tensor-pipe share
+    # (2 * 16 * in * out flops per layer node; bound by HBM at micro-batch 16)
+    for k in ("predict", "forward", "backward"):
+        c = r["classes"].get(k)
+        if c and c["nodes"]:
+            c["frac_of_hbm_peak"] = c["gbs"] / peak
+    fwd = r["classes"].get("forward")
+    if fwd and tflops:
+        # 4096x4096 layers dominate: 2*16*4096*4096 flops per node
+        fl = 2.0 * 16 * 4096 * 4096 / (fwd["us_per_node"] * 1e-6) / 1e12
+        out["tensor"] = {"achieved_tflops": fl, "peak_tflops": tflops, "frac": fl / tflops,
+                         "note": "micro-batch 16: 16 MACs per 2-byte weight, HBM-bound by construction"}
+    return out
 
 
 def stage_shard_measure(fb, torch, dist, rank, world, local, args, units):
@@ -247,7 +257,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--units", type=int, default=UNITS)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-large", action="store_true", help="skip the config-5 stage roofline measurement")
+    ap.add_argument("--no-large", action="store_true", help="skip the config-5 (16x4096, bf16) measurement")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
@@ -339,7 +349,7 @@ def main():
     dom = max(classes, key=lambda k: classes[k]["ms"])
     dc = classes[dom]
     achieved = dc["gbs"]
-    large = large_stage_roofline(fb, local) if not args.no_large else None
+    large = config5_roofline(fb, torch, local) if not args.no_large else None
     shard = stage_shard_measure(fb, torch, dist, rank, world, local, args, units) if world > 1 else None
 
     # ---- e2e through the reference-facing call from pinned host buffers
@@ -400,8 +410,8 @@ def main():
                      "share_of_serial_device_time": dc["ms"] / prof["serial_ms"],
                      "dag_critical_path_ms": prof["critical_path_ms"], "classes": classes,
                      "note": "C2 weights (1.3 MB) live in L2: the small-net path is latency-bound; "
-                             "see large_stage for the same kernels on a config-5 stage"},
-        "large_stage": large,
+                             "config5_bf16 has the HBM-bound wide net"},
+        "config5_bf16": large,
         "stage_shard": shard,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
