@@ -281,6 +281,49 @@ FERRET_API ferret_status ferret_trainer_profile(ferret_trainer* t, double* class
 FERRET_API ferret_status ferret_trainer_update_timing(ferret_trainer* t, double* total_ms, uint64_t* launches,
                                                       double* alg_bytes);
 
+/* ---------------- sequential learners on the device ---------------- */
+
+/* Options of a sequential learner: StaleHarness(net, policy, ring_depth, lr,
+ * eta_lambda) (learner.hpp:134-143) and train_sequential's lr / replay /
+ * replay_seed (learner.hpp:197-199). Compensator constants as in
+ * ferret_train_opts_default (lambda0 0.2, alpha 0.99, nu 2e-6). */
+typedef struct {
+    int32_t policy;            /* FERRET_POLICY_*: the harness's compensation (train_sequential: none) */
+    uint64_t ring_depth;       /* VersionRing capacity (harness); 1 for train_sequential */
+    double lr;                 /* 1e-3 */
+    double eta_lambda;         /* 1e-3 */
+    int32_t replay;            /* train_sequential: one ER sample per step */
+    uint64_t replay_seed;
+    uint64_t replay_capacity;  /* 5000 (kReplayBuffer) */
+    int32_t precision;         /* FERRET_PREC_* */
+    int32_t device;
+} ferret_seq_opts;
+
+/* A sequential learner: a trainer holding every layer in one stage, whose items
+ * run in order (each item's kernels captured into one CUDA graph per call).
+ * ferret_trainer_params / _normalizer / _comp_state / _destroy apply to it. */
+FERRET_API ferret_status ferret_seq_create(const ferret_net_desc* net, const ferret_seq_opts* opts,
+                                           ferret_trainer** out);
+/* StaleHarness::ocl_step (learner.hpp:145-163) for n_items items in order:
+ * observe + standardise, predict with the live net (preds_out[i]), gradient at
+ * the version taus[i] steps behind (clamped to the ring), Compensator::apply
+ * over the chain, SGD, push. One call with n items == n ocl_step calls. */
+FERRET_API ferret_status ferret_seq_ocl_steps(ferret_trainer* t, const double* features, const uint64_t* labels,
+                                              const int32_t* taus, size_t n_items, size_t n_features,
+                                              uint64_t* preds_out);
+/* train_sequential (learner.hpp:197-225) over the kept items of the stream
+ * (indices from ferret_apply_skip_policy, ascending): log_out gets n_items
+ * StepRecords, skipped items logged as dropped. */
+FERRET_API ferret_status ferret_seq_train(ferret_trainer* t, const double* features, const uint64_t* labels,
+                                          size_t n_items, size_t n_features, const int64_t* kept, size_t n_kept,
+                                          ferret_step_record* log_out);
+/* apply_skip_policy (stream.hpp:225-304) on the host: kind 0 oracle, 1 one_skip,
+ * 2 random_n, 3 last_n (SkipPolicy{kind, window, keep, seed}); kept_out and
+ * start_out (nullable) hold up to n_items entries, *n_kept is set. */
+FERRET_API ferret_status ferret_apply_skip_policy(size_t n_items, double t_d, int32_t kind, uint64_t window,
+                                                  uint64_t keep, uint64_t seed, double processing_time,
+                                                  int64_t* kept_out, double* start_out, size_t* n_kept);
+
 /* ---------------- unit entry: the fused compensation kernel ---------------- */
 
 /* One Compensator::apply (learner.hpp:97-120) on the device, fp32:

@@ -667,3 +667,42 @@ ORACLE_API int ferret_oracle_normalize(const double* features, size_t n, size_t 
         }
     });
 }
+
+// ---------------------------------------------------------------------------
+// Sequential learners, the reference's own code unchanged (learner.hpp:132-225):
+// StaleHarness::ocl_step per item, and train_sequential with apply_skip_policy.
+// ---------------------------------------------------------------------------
+ORACLE_API int ferret_oracle_harness(const ONet* net, int32_t policy, uint64_t ring_depth, double lr, double eta_lambda,
+                                     const double* features, const uint64_t* labels, const int32_t* taus, size_t n,
+                                     size_t f, uint64_t* preds, double* params_out) {
+    return guard([&] {
+        ferret::StaleHarness h(to_net(*net), static_cast<ferret::CompensationPolicy>(policy), ring_depth, lr, eta_lambda);
+        const ferret::DataStream ds = to_stream(features, labels, n, f);
+        for (size_t i = 0; i < n; ++i) preds[i] = h.ocl_step(ds.items[i], taus[i]);
+        const ferret::ParamVec p = ferret::flatten(h.net());
+        std::copy(p.begin(), p.end(), params_out);
+    });
+}
+
+ORACLE_API int ferret_oracle_train_sequential(const ONet* net, const double* features, const uint64_t* labels, size_t n,
+                                              size_t f, double t_d, int32_t skip_kind, uint64_t window, uint64_t keep,
+                                              uint64_t skip_seed, double processing_time, double lr, int32_t replay,
+                                              uint64_t replay_seed, ORecord* log_out, double* params_out,
+                                              int64_t* kept_out, size_t* n_kept) {
+    return guard([&] {
+        ferret::SkipPolicy sp;
+        sp.kind = static_cast<ferret::SkipKind>(skip_kind);
+        sp.window = window;
+        sp.keep = keep;
+        sp.seed = skip_seed;
+        const ferret::DataStream ds = to_stream(features, labels, n, f);
+        const ferret::TrainOutcome out =
+            ferret::train_sequential(to_net(*net), ds, t_d, sp, processing_time, lr, replay != 0, replay_seed);
+        copy_records(out.log, log_out);
+        const ferret::ParamVec p = ferret::flatten(out.net);
+        std::copy(p.begin(), p.end(), params_out);
+        const ferret::FilteredStream fs = ferret::apply_skip_policy(n, t_d, sp, processing_time);
+        for (size_t i = 0; i < fs.kept.size(); ++i) kept_out[i] = fs.kept[i].index;
+        *n_kept = fs.kept.size();
+    });
+}

@@ -197,3 +197,52 @@ def normalize(features: np.ndarray) -> np.ndarray:
     out = np.empty_like(f)
     _ck(lib().ferret_oracle_normalize(_dp(f), C.c_size_t(f.shape[0]), C.c_size_t(f.shape[1]), _dp(out)))
     return out
+
+
+def _net(widths, params):
+    ins = np.ascontiguousarray(widths[:-1], dtype=np.uint64)
+    outs = np.ascontiguousarray(widths[1:], dtype=np.uint64)
+    acts = np.zeros(len(ins), dtype=np.int32)
+    acts[-1] = 1
+    p = np.ascontiguousarray(params, dtype=np.float64)
+    keep = (ins, outs, acts, p)
+    return ONet(len(ins), _up(ins), _up(outs), acts.ctypes.data_as(C.POINTER(C.c_int32)), _dp(p)), keep
+
+
+def harness(widths, params, features, labels, taus, policy="none", ring_depth=8, lr=1e-3, eta_lambda=1e-3) -> dict:
+    """The reference's StaleHarness (learner.hpp:132-170): ocl_step(item_i, taus[i]) for every item."""
+    net, keep = _net(widths, params)
+    f = np.ascontiguousarray(features, dtype=np.float64)
+    lab = np.ascontiguousarray(labels, dtype=np.uint64)
+    t = np.ascontiguousarray(taus, dtype=np.int32)
+    n, F = f.shape
+    preds = np.zeros(n, dtype=np.uint64)
+    out = np.zeros(keep[3].size, dtype=np.float64)
+    lib().ferret_oracle_harness.restype = C.c_int
+    _ck(lib().ferret_oracle_harness(C.byref(net), C.c_int32(POLICIES[policy]), C.c_uint64(ring_depth), C.c_double(lr),
+                                    C.c_double(eta_lambda), _dp(f), _up(lab), t.ctypes.data_as(C.POINTER(C.c_int32)),
+                                    C.c_size_t(n), C.c_size_t(F), _up(preds), _dp(out)))
+    return {"preds": preds, "params": out}
+
+
+SKIPS = {"oracle": 0, "one_skip": 1, "random_n": 2, "last_n": 3}
+
+
+def train_sequential(widths, params, features, labels, t_d=1.0, skip="oracle", window=1, keep=1, skip_seed=0,
+                     processing_time=1.0, lr=1e-3, replay=False, replay_seed=0) -> dict:
+    """The reference's train_sequential (learner.hpp:197-225) with apply_skip_policy (stream.hpp:225-304)."""
+    net, k = _net(widths, params)
+    f = np.ascontiguousarray(features, dtype=np.float64)
+    lab = np.ascontiguousarray(labels, dtype=np.uint64)
+    n, F = f.shape
+    log = np.zeros(n, dtype=RECORD_DTYPE)
+    out = np.zeros(k[3].size, dtype=np.float64)
+    kept = np.zeros(max(n, 1), dtype=np.int64)
+    nk = C.c_size_t()
+    lib().ferret_oracle_train_sequential.restype = C.c_int
+    _ck(lib().ferret_oracle_train_sequential(
+        C.byref(net), _dp(f), _up(lab), C.c_size_t(n), C.c_size_t(F), C.c_double(t_d), C.c_int32(SKIPS[skip]),
+        C.c_uint64(window), C.c_uint64(keep), C.c_uint64(skip_seed), C.c_double(processing_time), C.c_double(lr),
+        C.c_int32(int(replay)), C.c_uint64(replay_seed), C.c_void_p(log.ctypes.data), _dp(out),
+        C.c_void_p(kept.ctypes.data), C.byref(nk)))
+    return {"log": log, "params": out, "kept": kept[: nk.value].copy()}

@@ -191,6 +191,26 @@ size_t ferret_schedule_trace_text(const ferret_schedule* s, char* buf, size_t ca
 
 void ferret_schedule_destroy(ferret_schedule* s) { delete s; }
 
+ferret_status ferret_apply_skip_policy(size_t n_items, double t_d, int32_t kind, uint64_t window, uint64_t keep,
+                                      uint64_t seed, double processing_time, int64_t* kept_out, double* start_out,
+                                      size_t* n_kept) {
+    return guarded([&] {
+        if (!n_kept || (n_items && !kept_out)) fail(FERRET_E_INVALID_ARG, "apply_skip_policy: null buffer");
+        if (kind < 0 || kind > 3) fail(FERRET_E_CONFIG, "unknown skip policy");
+        ferret::SkipPolicy p;
+        p.kind = static_cast<ferret::SkipKind>(kind);
+        p.window = static_cast<std::size_t>(window);
+        p.keep = static_cast<std::size_t>(keep);
+        p.seed = seed;
+        const ferret::FilteredStream fs = ferret::apply_skip_policy(n_items, t_d, p, processing_time);
+        for (size_t i = 0; i < fs.kept.size(); ++i) {
+            kept_out[i] = fs.kept[i].index;
+            if (start_out) start_out[i] = fs.kept[i].start;
+        }
+        *n_kept = fs.kept.size();
+    });
+}
+
 void ferret_train_opts_default(ferret_train_opts* o) {
     o->policy = FERRET_POLICY_NONE;
     o->lr = 1e-3;

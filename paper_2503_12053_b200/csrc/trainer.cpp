@@ -214,6 +214,7 @@ struct GraphBuilder {
     std::vector<cudaEvent_t>* prof_events = nullptr;
 
     explicit GraphBuilder(bool serial_) : serial(serial_) { cuda_check(cudaGraphCreate(&g, 0), "cudaGraphCreate"); }
+    explicit GraphBuilder(cudaStream_t s) : eager(s) {}
     ~GraphBuilder() {
         if (g) cudaGraphDestroy(g);
     }
@@ -281,7 +282,17 @@ struct GraphBuilder {
         }
     }
 
+    // eager mode (sequential learners): launch on this stream instead of adding
+    // graph nodes (the caller may be capturing the stream into a graph)
+    cudaStream_t eager = nullptr;
+
     cudaGraphNode_t kernel(fb200::KernelSpec& k, const std::vector<uint64_t>& reads, const std::vector<uint64_t>& writes) {
+        if (eager) {
+            cuda_check(fb200::launch_spec(k, eager), "kernel launch");
+            ++kernels;
+            cur_bytes = 0.0;
+            return nullptr;
+        }
         const std::vector<int> ld = logical(reads, writes);
         const std::vector<cudaGraphNode_t> d = deps(ld);
         cudaKernelNodeParams p{};
@@ -299,6 +310,10 @@ struct GraphBuilder {
 
     cudaGraphNode_t copy(void* dst, const void* src, size_t bytes, const std::vector<uint64_t>& reads,
                          const std::vector<uint64_t>& writes) {
+        if (eager) {
+            cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, eager), "cudaMemcpyAsync");
+            return nullptr;
+        }
         const std::vector<int> ld = logical(reads, writes);
         const std::vector<cudaGraphNode_t> d = deps(ld);
         cudaGraphNode_t n;
@@ -1497,6 +1512,212 @@ struct ferret_trainer {
         gb->kernel(k, reads, {stash_key});
     }
 
+    // ------------------------------------------------ sequential learners
+    // StaleHarness (learner.hpp:132-170) and train_sequential (learner.hpp:197-225)
+    // on the device. The trainer holds every layer in one stage; each item's
+    // kernels are issued in item order on the trainer's stream through the
+    // graph builder's eager mode, and one call's items are captured into a
+    // single CUDA graph (every item depends on the previous update).
+    struct Seq {
+        bool on = false;
+        long long version = 0;     // absolute version of the live parameters (ring slot version % depth)
+        long long ring_size = 1;   // versions the reference's VersionRing holds (compensate.hpp:140-170)
+        long long ring_cap = 1;
+        uint64_t norm_count = 0;
+        unsigned long long* d_zero = nullptr;
+        float* d_ux = nullptr;     // the unit's input rows: the item (row 0), the replay sample (row 1)
+        double* d_raw = nullptr;   // raw features of the call
+        int* d_lab = nullptr;      // per item: label, replay-sample label
+        int* d_pred = nullptr;
+        size_t cap = 0;
+        std::unique_ptr<GraphBuilder> gb;  // eager builder on the trainer's stream
+    } sq;
+
+    void seq_init(long long ring_depth) {
+        if (ring_depth + 1 > fb200::kMaxChain)
+            fail(FERRET_E_CONFIG, "ring depth above 47 versions is not supported by the update kernel");
+        sq.on = true;
+        sq.ring_cap = std::max<long long>(ring_depth, 1);
+        grow_ring(stages[0], static_cast<int>(sq.ring_cap + 1));  // + the slot written while the chain is read
+        ensure_stash(1);
+        ensure_scratch(2);
+        sq.d_zero = dalloc<unsigned long long>(1, device_bytes);
+        cuda_check(cudaMemset(sq.d_zero, 0, sizeof(unsigned long long)), "memset");
+        sq.d_ux = dalloc<float>(2 * static_cast<size_t>(F), device_bytes);
+        cuda_check(cudaMemset(sq.d_ux, 0, 2 * static_cast<size_t>(F) * sizeof(float)), "memset");
+        sq.gb = std::make_unique<GraphBuilder>(stream);
+        if (opt.precision != FERRET_PREC_FP32)  // split-K scratch exists before any capture
+            for (uint64_t k : {GraphBuilder::key(GraphBuilder::kPred, 0), GraphBuilder::key(GraphBuilder::kStash, 0)})
+                mma_scratch_for(k);
+    }
+
+    void seq_upload(const double* features, const uint64_t* labels, size_t n) {
+        if (n > sq.cap) {
+            cuda_check(cudaStreamSynchronize(stream), "sync");
+            dfree(sq.d_raw);
+            dfree(sq.d_lab);
+            dfree(sq.d_pred);
+            sq.cap = std::max(n, 2 * sq.cap);
+            sq.d_raw = dalloc<double>(sq.cap * static_cast<size_t>(F), device_bytes);
+            sq.d_lab = dalloc<int>(2 * sq.cap, device_bytes);
+            sq.d_pred = dalloc<int>(sq.cap, device_bytes);
+        }
+        cuda_check(cudaMemcpyAsync(sq.d_raw, features, n * static_cast<size_t>(F) * sizeof(double),
+                                   cudaMemcpyHostToDevice, stream),
+                   "H2D features");
+        std::vector<int> lab(2 * n, 0);
+        for (size_t i = 0; i < n; ++i) {
+            if (labels[i] >= static_cast<uint64_t>(n_out)) fail(FERRET_E_INVALID_ARG, "label out of range");
+            lab[2 * i] = static_cast<int>(labels[i]);
+        }
+        seq_labels = std::move(lab);
+    }
+    std::vector<int> seq_labels;  // host copy, replay labels filled in while the items are emitted
+
+    // One item: RunningNormalizer observe + apply, predict_class at the live
+    // version, forward_backward of the `rows`-row batch at version `read`, then
+    // Compensator::apply over the chain [read .. live] and the SGD step into a
+    // new version (learner.hpp:145-160; with policy none and read = live this is
+    // forward_backward + apply_sgd of train_sequential, learner.hpp:207-220).
+    void seq_item(size_t i, long long read, int rows, int policy) {
+        using GB = GraphBuilder;
+        fb200::NormArgs na{sq.d_raw + i * static_cast<size_t>(F), 1, F, sq.d_zero,
+                           static_cast<unsigned long long>(sq.norm_count), d_norm_mean, d_norm_m2, sq.d_ux};
+        fb200::KernelSpec kn;
+        fb200::spec_normalize(na, kn);
+        gb->kernel(kn, {}, {});
+        ++sq.norm_count;
+        const StageDev& s = stages[0];
+        float* su = d_stash;
+        const int keep_b = B;
+        B = 1;
+        for (int l = 0; l < L; ++l) {  // predict_class (net.hpp:150-154)
+            const float* X = l == 0 ? sq.d_ux : su + pred_off + ((l - 1) & 1) * pred_stride;
+            emit_layer(layers[static_cast<size_t>(l)], s.slot(sq.version), X, nullptr, su + pred_off + (l & 1) * pred_stride,
+                       {}, {GB::key(GB::kPred, 0)});
+        }
+        fb200::HeadArgs h{};
+        h.logits = su + pred_off + ((L - 1) & 1) * pred_stride;
+        h.n_out = n_out;
+        h.B = 1;
+        h.mode = 0;
+        h.pred = sq.d_pred + i;
+        fb200::KernelSpec kh;
+        fb200::spec_head(h, kh);
+        gb->kernel(kh, {}, {});
+        B = rows;
+        for (int l = 0; l < L; ++l) {  // forward_backward (net.hpp:157-200) at the read version
+            const LayerDev& ld = layers[static_cast<size_t>(l)];
+            const float* X = l == 0 ? sq.d_ux : su + layers[static_cast<size_t>(l - 1)].act_off;
+            emit_layer(ld, s.slot(read), X, nullptr, su + ld.act_off, {}, {GB::key(GB::kStash, 0)});
+        }
+        emit_delta_head(su, sq.d_lab + 2 * i, nullptr, 1.0f / static_cast<float>(rows), {}, GB::key(GB::kStash, 0));
+        for (int l = L - 1; l >= 1; --l) emit_layer_backward(l, s.slot(read), su, 0, {}, GB::key(GB::kStash, 0), true);
+        fb200::UpdArgs a = update_args(0, sq.version, read);
+        a.policy = policy;
+        a.K = 1;
+        a.pend[0] = {su, sq.d_ux, 0};
+        a.step = static_cast<float>(opt.lr);
+        fb200::KernelSpec ku;
+        fb200::spec_update(a, ku);
+        gb->kernel(ku, {}, {});
+        B = keep_b;
+        ++sq.version;
+        sq.ring_size = std::min(sq.ring_size + 1, sq.ring_cap);
+    }
+
+    // Runs `emit(i)` for every item inside one captured graph on the trainer's stream.
+    template <class Emit>
+    void seq_run(size_t n, Emit&& emit) {
+        gb = sq.gb.get();
+        cudaGraph_t g = nullptr;
+        cuda_check(cudaStreamBeginCapture(stream, cudaStreamCaptureModeRelaxed), "cudaStreamBeginCapture");
+        try {
+            for (size_t i = 0; i < n; ++i) emit(i);
+        } catch (...) {
+            cudaStreamEndCapture(stream, &g);
+            if (g) cudaGraphDestroy(g);
+            gb = nullptr;
+            throw;
+        }
+        cuda_check(cudaStreamEndCapture(stream, &g), "cudaStreamEndCapture");
+        gb = nullptr;
+        cudaGraphExec_t ge = nullptr;
+        const cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
+        cudaGraphDestroy(g);
+        cuda_check(e, "cudaGraphInstantiate");
+        const cudaError_t l = cudaGraphLaunch(ge, stream);
+        const cudaError_t y = cudaStreamSynchronize(stream);
+        cudaGraphExecDestroy(ge);
+        cuda_check(l, "cudaGraphLaunch");
+        cuda_check(y, "sequential run");
+    }
+
+    // StaleHarness::ocl_step over n items (learner.hpp:145-163)
+    void harness_steps(const double* features, const uint64_t* labels, const int32_t* taus, size_t n,
+                       uint64_t* preds) {
+        if (n == 0) return;
+        seq_upload(features, labels, n);
+        cuda_check(cudaMemcpyAsync(sq.d_lab, seq_labels.data(), 2 * n * sizeof(int), cudaMemcpyHostToDevice, stream),
+                   "H2D labels");
+        seq_run(n, [&](size_t i) {
+            const long long eff = std::min<long long>(std::max(taus[i], 0), sq.ring_size - 1);
+            seq_item(i, sq.version - eff, 1, opt.policy);
+        });
+        std::vector<int> p(n);
+        cuda_check(cudaMemcpy(p.data(), sq.d_pred, n * sizeof(int), cudaMemcpyDeviceToHost), "D2H predictions");
+        for (size_t i = 0; i < n; ++i) preds[i] = static_cast<uint64_t>(p[i]);
+    }
+
+    // train_sequential over the kept items (learner.hpp:207-222): predict,
+    // forward_backward on {item} (+ one replay sample drawn before the item is
+    // added, mean over the batch), apply_sgd, then ReplayBuffer::add.
+    void sequential_train(const double* features, const uint64_t* labels, size_t n, const int64_t* kept,
+                          size_t n_kept, ferret_step_record* log) {
+        for (size_t i = 0; i < n; ++i) log[i] = {static_cast<int64_t>(i), FERRET_STEP_DROPPED, 0, 0, labels[i]};
+        if (n_kept == 0) return;
+        std::vector<double> kf(n_kept * static_cast<size_t>(F));
+        std::vector<uint64_t> kl(n_kept);
+        for (size_t k = 0; k < n_kept; ++k) {
+            if (kept[k] < 0 || static_cast<size_t>(kept[k]) >= n) fail(FERRET_E_INVALID_ARG, "kept index out of range");
+            std::memcpy(kf.data() + k * static_cast<size_t>(F), features + static_cast<size_t>(kept[k]) * static_cast<size_t>(F),
+                        static_cast<size_t>(F) * sizeof(double));
+            kl[k] = labels[kept[k]];
+        }
+        seq_upload(kf.data(), kl.data(), n_kept);
+        std::vector<int> rows(n_kept, 1);
+        std::vector<int> src(n_kept, -1), dst(n_kept, -1);  // replay sample drawn / pool position written
+        for (size_t k = 0; k < n_kept; ++k) {  // the reservoir's host arithmetic, in item order
+            if (opt.replay && hs.replay.size > 0) {
+                src[k] = hs.replay.sample();
+                seq_labels[2 * k + 1] = hs.replay.label_at[static_cast<size_t>(src[k])];
+                rows[k] = 2;
+            }
+            if (opt.replay) dst[k] = hs.replay.add(seq_labels[2 * k]);
+        }
+        cuda_check(cudaMemcpyAsync(sq.d_lab, seq_labels.data(), 2 * n_kept * sizeof(int), cudaMemcpyHostToDevice, stream),
+                   "H2D labels");
+        const size_t row_bytes = static_cast<size_t>(F) * sizeof(float);
+        seq_run(n_kept, [&](size_t k) {
+            if (src[k] >= 0)
+                cuda_check(cudaMemcpyAsync(sq.d_ux + F, d_pool_x + static_cast<size_t>(src[k]) * static_cast<size_t>(F),
+                                           row_bytes, cudaMemcpyDeviceToDevice, stream),
+                           "replay row");
+            seq_item(k, sq.version, rows[k], FERRET_POLICY_NONE);
+            if (dst[k] >= 0)
+                cuda_check(cudaMemcpyAsync(d_pool_x + static_cast<size_t>(dst[k]) * static_cast<size_t>(F), sq.d_ux,
+                                           row_bytes, cudaMemcpyDeviceToDevice, stream),
+                           "replay add");
+        });
+        std::vector<int> p(n_kept);
+        cuda_check(cudaMemcpy(p.data(), sq.d_pred, n_kept * sizeof(int), cudaMemcpyDeviceToHost), "D2H predictions");
+        for (size_t k = 0; k < n_kept; ++k) {
+            ferret_step_record& r = log[kept[k]];
+            r.predicted = static_cast<uint64_t>(p[k]);
+            r.outcome = r.predicted == r.label ? FERRET_STEP_CORRECT : FERRET_STEP_WRONG;
+        }
+    }
+
     // replay_step (learner.hpp:513-519): forward_backward(net_, {buffer.sample()})
     // with mean reduction (net.hpp:157-200), apply_sgd on every stage, push a
     // version per stage. B pool samples per replay step at micro-batch B; the
@@ -1647,7 +1868,8 @@ struct ferret_trainer {
         for (int j = 0; j < P; ++j) {
             const StageDev& s = stages[static_cast<size_t>(j)];
             std::vector<float> slot(static_cast<size_t>(s.slot_floats));
-            cuda_check(cudaMemcpy(slot.data(), s.slot(0), slot.size() * sizeof(float), cudaMemcpyDeviceToHost),
+            cuda_check(cudaMemcpy(slot.data(), s.slot(sq.on ? sq.version : 0), slot.size() * sizeof(float),
+                                  cudaMemcpyDeviceToHost),
                        "D2H params");
             unpack_stage(s, slot, out, 0.0);
         }
@@ -1717,6 +1939,58 @@ ferret_status ferret_trainer_create(const ferret_net_desc* net, const uint64_t* 
         t->build(*net, bounds, n_bounds);
         cuda_check(cudaDeviceSynchronize(), "create");
         *out = t.release();
+    });
+}
+
+ferret_status ferret_seq_create(const ferret_net_desc* net, const ferret_seq_opts* o, ferret_trainer** out) {
+    return guarded([&] {
+        if (!net || !o || !out) fail(FERRET_E_INVALID_ARG, "seq_create: null argument");
+        if (net->n_layers <= 0) fail(FERRET_E_CONFIG, "net needs at least one layer");
+        if (net->n_layers > fb200::kMaxStageLayers) fail(FERRET_E_CONFIG, "at most 16 layers per sequential learner");
+        require_device(o->device);
+        ferret_train_opts t_o{};
+        ferret_train_opts_default(&t_o);
+        t_o.policy = o->policy;
+        t_o.lr = o->lr;
+        t_o.eta_lambda = o->eta_lambda;
+        t_o.replay = o->replay;
+        t_o.replay_seed = o->replay_seed;
+        t_o.replay_capacity = o->replay_capacity;
+        t_o.precision = o->precision;
+        t_o.micro_batch = o->replay ? 2 : 1;  // train_sequential's batch: the item + one replay sample
+        t_o.device = o->device;
+        auto t = std::make_unique<ferret_trainer>();
+        t->opt = t_o;
+        cuda_check(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking), "stream");
+        cuda_check(cudaStreamCreateWithFlags(&t->nstream, cudaStreamNonBlocking), "stream");
+        const uint64_t bounds[2] = {0, static_cast<uint64_t>(net->n_layers)};
+        t->build(*net, bounds, 2);
+        t->seq_init(static_cast<long long>(std::max<uint64_t>(o->ring_depth, 1)));
+        cuda_check(cudaDeviceSynchronize(), "create");
+        *out = t.release();
+    });
+}
+
+ferret_status ferret_seq_ocl_steps(ferret_trainer* t, const double* features, const uint64_t* labels,
+                                   const int32_t* taus, size_t n_items, size_t n_features, uint64_t* preds_out) {
+    return guarded([&] {
+        if (!t->sq.on) fail(FERRET_E_CONFIG, "seq_ocl_steps: not a sequential learner (ferret_seq_create)");
+        if (n_features != static_cast<size_t>(t->F)) fail(FERRET_E_INVALID_ARG, "feature width mismatch");
+        if (n_items && (!features || !labels || !taus || !preds_out)) fail(FERRET_E_INVALID_ARG, "null buffer");
+        cuda_check(cudaSetDevice(t->opt.device), "cudaSetDevice");
+        t->harness_steps(features, labels, taus, n_items, preds_out);
+    });
+}
+
+ferret_status ferret_seq_train(ferret_trainer* t, const double* features, const uint64_t* labels, size_t n_items,
+                               size_t n_features, const int64_t* kept, size_t n_kept, ferret_step_record* log_out) {
+    return guarded([&] {
+        if (!t->sq.on) fail(FERRET_E_CONFIG, "seq_train: not a sequential learner (ferret_seq_create)");
+        if (n_features != static_cast<size_t>(t->F)) fail(FERRET_E_INVALID_ARG, "feature width mismatch");
+        if (n_items && (!features || !labels || !log_out)) fail(FERRET_E_INVALID_ARG, "null buffer");
+        if (n_kept && !kept) fail(FERRET_E_INVALID_ARG, "null kept index list");
+        cuda_check(cudaSetDevice(t->opt.device), "cudaSetDevice");
+        t->sequential_train(features, labels, n_items, kept, n_kept, log_out);
     });
 }
 
@@ -1815,7 +2089,7 @@ ferret_status ferret_trainer_normalizer(ferret_trainer* t, uint64_t* count, doub
         if (n_features != static_cast<size_t>(t->F)) fail(FERRET_E_INVALID_ARG, "normalizer: width mismatch");
         cuda_check(cudaSetDevice(t->opt.device), "cudaSetDevice");
         cuda_check(cudaStreamSynchronize(t->stream), "sync");
-        *count = t->hs.norm_count;
+        *count = t->sq.on ? t->sq.norm_count : t->hs.norm_count;
         cuda_check(cudaMemcpy(mean, t->d_norm_mean, n_features * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
         cuda_check(cudaMemcpy(m2, t->d_norm_m2, n_features * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
     });

@@ -74,6 +74,12 @@ class NetDesc(C.Structure):
                 ("act", C.POINTER(C.c_int32)), ("params", C.POINTER(C.c_double))]
 
 
+class SeqOpts(C.Structure):
+    _fields_ = [("policy", C.c_int32), ("ring_depth", C.c_uint64), ("lr", C.c_double), ("eta_lambda", C.c_double),
+                ("replay", C.c_int32), ("replay_seed", C.c_uint64), ("replay_capacity", C.c_uint64),
+                ("precision", C.c_int32), ("device", C.c_int32)]
+
+
 class StreamSpecC(C.Structure):
     _fields_ = [("t_d", C.c_double), ("decay_c", C.c_double), ("value", C.c_double), ("horizon", C.c_double)]
 
@@ -141,6 +147,13 @@ def lib() -> C.CDLL:
         "ferret_trainer_handoff_plan": (C.c_int, [C.c_void_p, P(C.c_uint64), P(C.c_uint64), C.c_int32]),
         "ferret_trainer_profile_critical": (C.c_int, [C.c_void_p, P(D), P(C.c_uint64), C.c_int32]),
         "ferret_trainer_profile": (C.c_int, [C.c_void_p, P(D), P(C.c_uint64), P(D), C.c_int32, P(D), P(D)]),
+        "ferret_seq_create": (C.c_int, [P(NetDesc), P(SeqOpts), P(C.c_void_p)]),
+        "ferret_seq_ocl_steps": (C.c_int, [C.c_void_p, P(D), P(C.c_uint64), P(C.c_int32), C.c_size_t, C.c_size_t,
+                                           P(C.c_uint64)]),
+        "ferret_seq_train": (C.c_int, [C.c_void_p, P(D), P(C.c_uint64), C.c_size_t, C.c_size_t, P(C.c_int64),
+                                       C.c_size_t, C.c_void_p]),
+        "ferret_apply_skip_policy": (C.c_int, [C.c_size_t, D, C.c_int32, C.c_uint64, C.c_uint64, C.c_uint64, D,
+                                               P(C.c_int64), P(D), P(C.c_size_t)]),
         "ferret_dense_layer": (C.c_int, [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                          C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]),
         "ferret_compensate": (C.c_int, [C.c_int32, P(D), P(P(D)), C.c_int32, P(D), P(D), P(D), P(D), C.c_size_t,
@@ -486,6 +499,97 @@ def train_pipeline(widths, params, bounds, events, features, labels, opt=Pipelin
         return log, t.params()
     finally:
         t.close()
+
+
+SKIPS = {"oracle": 0, "one_skip": 1, "random_n": 2, "last_n": 3}
+
+
+def apply_skip_policy(n_items: int, t_d: float, kind: str = "oracle", window: int = 1, keep: int = 1, seed: int = 0,
+                      processing_time: float = 1.0):
+    """apply_skip_policy (stream.hpp:225-304) -> (kept indices, start times)."""
+    kept = np.zeros(max(n_items, 1), dtype=np.int64)
+    start = np.zeros(max(n_items, 1), dtype=np.float64)
+    nk = C.c_size_t()
+    _check(lib().ferret_apply_skip_policy(n_items, t_d, SKIPS[kind], window, keep, seed, processing_time,
+                                          kept.ctypes.data_as(C.POINTER(C.c_int64)), _dp(start), C.byref(nk)))
+    return kept[: nk.value].copy(), start[: nk.value].copy()
+
+
+class _SeqLearner:
+    """A sequential learner on the device (ferret_seq_create): every layer in one stage,
+    items in order, one captured CUDA graph per call."""
+
+    def __init__(self, widths, params, policy="none", ring_depth=1, lr=1e-3, eta_lambda=1e-3, replay=False,
+                 replay_seed=0, replay_capacity=5000, precision="fp32", device=0):
+        self.widths = list(widths)
+        self.n_params = param_count(widths)
+        ins, outs, acts = widths_layers(widths)
+        self._keep = (ins, outs, acts, np.ascontiguousarray(params, dtype=np.float64))
+        desc = NetDesc(len(ins), _up(ins), _up(outs), acts.ctypes.data_as(C.POINTER(C.c_int32)), _dp(self._keep[3]))
+        o = SeqOpts(POLICIES[policy], ring_depth, lr, eta_lambda, int(replay), replay_seed, replay_capacity,
+                    PRECISIONS[precision], device)
+        h = C.c_void_p()
+        _check(lib().ferret_seq_create(C.byref(desc), C.byref(o), C.byref(h)))
+        self._h = h
+
+    def params(self) -> np.ndarray:
+        out = np.empty(self.n_params, dtype=np.float64)
+        _check(lib().ferret_trainer_params(self._h, _dp(out), out.size))
+        return out
+
+    def normalizer(self, n_features: int):
+        cnt = C.c_uint64()
+        mean = np.empty(n_features)
+        m2 = np.empty(n_features)
+        _check(lib().ferret_trainer_normalizer(self._h, C.byref(cnt), _dp(mean), _dp(m2), n_features))
+        return int(cnt.value), mean, m2
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().ferret_trainer_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class StaleHarness(_SeqLearner):
+    """StaleHarness (learner.hpp:132-170) on the device: ocl_step predicts then trains with an
+    injected staleness tau (gradient at the version tau steps behind, compensated by `policy`)."""
+
+    def __init__(self, widths, params, policy="none", ring_depth=1, lr=1e-3, eta_lambda=1e-3, precision="fp32",
+                 device=0):
+        super().__init__(widths, params, policy=policy, ring_depth=ring_depth, lr=lr, eta_lambda=eta_lambda,
+                         precision=precision, device=device)
+
+    def ocl_steps(self, features: np.ndarray, labels: np.ndarray, taus) -> np.ndarray:
+        f = np.ascontiguousarray(features, dtype=np.float64)
+        lab = np.ascontiguousarray(labels, dtype=np.uint64)
+        t = np.ascontiguousarray(np.broadcast_to(np.asarray(taus, dtype=np.int32), (len(f),)))
+        preds = np.empty(len(f), dtype=np.uint64)
+        _check(lib().ferret_seq_ocl_steps(self._h, _dp(f), _up(lab), t.ctypes.data_as(C.POINTER(C.c_int32)), len(f),
+                                          f.shape[1], _up(preds)))
+        return preds
+
+    def ocl_step(self, features: np.ndarray, label: int, tau: int) -> int:
+        return int(self.ocl_steps(np.asarray(features, dtype=np.float64)[None, :], np.array([label]), [tau])[0])
+
+
+def train_sequential(widths, params, features, labels, t_d=1.0, skip="oracle", window=1, keep=1, skip_seed=0,
+                     processing_time=1.0, lr=1e-3, replay=False, replay_seed=0, precision="fp32", device=0):
+    """train_sequential (learner.hpp:197-225) on the device -> (StepRecord log, params, learner)."""
+    f = np.ascontiguousarray(features, dtype=np.float64)
+    lab = np.ascontiguousarray(labels, dtype=np.uint64)
+    kept, _ = apply_skip_policy(len(f), t_d, skip, window, keep, skip_seed, processing_time)
+    learner = _SeqLearner(widths, params, lr=lr, replay=replay, replay_seed=replay_seed, precision=precision,
+                          device=device)
+    log = np.zeros(len(f), dtype=RECORD_DTYPE)
+    _check(lib().ferret_seq_train(learner._h, _dp(f), _up(lab), len(f), f.shape[1],
+                                  kept.ctypes.data_as(C.POINTER(C.c_int64)), len(kept), log.ctypes.data))
+    return log, learner.params(), learner
 
 
 def dense_layer(precision: str, direction: int, W: np.ndarray, X: np.ndarray, bias=None, mask=None,
