@@ -225,6 +225,149 @@ class PipelineTrainer {
     std::unique_ptr<ferret_trainer, Release> handle_;
 };
 
+namespace detail {
+struct SeqRelease {
+    void operator()(ferret_trainer* t) const { ferret_trainer_destroy(t); }
+};
+using SeqHandle = std::unique_ptr<ferret_trainer, SeqRelease>;
+
+inline SeqHandle make_seq(const DenseNet& net, const ferret_seq_opts& o) {
+    std::vector<uint64_t> in, out;
+    std::vector<int32_t> act;
+    for (const DenseLayer& l : net.layers) {
+        in.push_back(l.in);
+        out.push_back(l.out);
+        act.push_back(static_cast<int32_t>(l.act));
+    }
+    const ParamVec params = flatten(net);
+    const ferret_net_desc desc{static_cast<int32_t>(net.layers.size()), in.data(), out.data(), act.data(),
+                               params.data()};
+    ferret_trainer* raw = nullptr;
+    b200_check(ferret_seq_create(&desc, &o, &raw));
+    return SeqHandle(raw);
+}
+
+inline void read_back(ferret_trainer* t, DenseNet& net, RunningNormalizer& norm, std::size_t f) {
+    ParamVec params(net.n_params());
+    b200_check(ferret_trainer_params(t, params.data(), params.size()));
+    unflatten_into(net, params);
+    uint64_t count = 0;
+    std::vector<double> mean(f), m2(f);
+    b200_check(ferret_trainer_normalizer(t, &count, mean.data(), m2.data(), f));
+    norm.restore(static_cast<std::size_t>(count), std::move(mean), std::move(m2));
+}
+} // namespace detail
+
+/// StaleHarness (reference learner.hpp:132-170) on the device: predict-then-train
+/// with an injected staleness tau, compensated by `policy` over the version chain.
+class StaleHarness {
+  public:
+    StaleHarness(DenseNet net, CompensationPolicy policy, std::size_t ring_depth, double lr = kLearningRate,
+                 double eta_lambda = 1e-3, const B200Options& b200 = B200Options{})
+        : net_(std::move(net)), norm_(net_.n_inputs()) {
+        net_.validate();
+        ferret_seq_opts o{};
+        o.policy = static_cast<int32_t>(policy);
+        o.ring_depth = std::max<std::size_t>(ring_depth, 1);
+        o.lr = lr;
+        o.eta_lambda = eta_lambda;
+        o.replay_capacity = kReplayBuffer;
+        o.precision = b200.precision;
+        o.device = b200.device;
+        handle_ = detail::make_seq(net_, o);
+    }
+
+    /// Predict-then-train on one item; returns the prediction (learner.hpp:145-163).
+    std::size_t ocl_step(const StreamItem& item, int tau) {
+        const uint64_t label = item.label;
+        uint64_t pred = 0;
+        const int32_t t = tau;
+        b200_check(ferret_seq_ocl_steps(handle_.get(), item.features.data(), &label, &t, 1, item.features.size(), &pred));
+        stale_ = true;
+        return static_cast<std::size_t>(pred);
+    }
+
+    const DenseNet& net() const {
+        refresh();
+        return net_;
+    }
+    const RunningNormalizer& normalizer() const {
+        refresh();
+        return norm_;
+    }
+
+  private:
+    void refresh() const {
+        if (!stale_) return;
+        detail::read_back(handle_.get(), net_, norm_, net_.n_inputs());
+        stale_ = false;
+    }
+    mutable DenseNet net_;
+    mutable RunningNormalizer norm_;
+    mutable bool stale_ = false;
+    detail::SeqHandle handle_;
+};
+
+/// Held-out accuracy in percentage points (learner.hpp:185-192): standardise with
+/// `norm`, predict_class on the device.
+inline double test_accuracy(const DenseNet& net, const RunningNormalizer& norm, const std::vector<Sample>& held_out,
+                            const B200Options& b200 = B200Options{}) {
+    if (held_out.empty()) return 0.0;
+    ferret_seq_opts o{};
+    o.ring_depth = 1;
+    o.lr = kLearningRate;
+    o.replay_capacity = kReplayBuffer;
+    o.precision = b200.precision;
+    o.device = b200.device;
+    detail::SeqHandle h = detail::make_seq(net, o);
+    const std::size_t f = net.n_inputs(), n = held_out.size();
+    b200_check(ferret_seq_set_normalizer(h.get(), norm.count(), norm.mean().data(), norm.m2().data(), f));
+    std::vector<double> x(n * f);
+    for (std::size_t i = 0; i < n; ++i) std::copy(held_out[i].x.begin(), held_out[i].x.end(), x.begin() + i * f);
+    std::vector<uint64_t> pred(n);
+    b200_check(ferret_seq_predict(h.get(), x.data(), n, f, pred.data()));
+    std::size_t correct = 0;
+    for (std::size_t i = 0; i < n; ++i) correct += pred[i] == held_out[i].label ? 1 : 0;
+    return 100.0 * static_cast<double>(correct) / static_cast<double>(n);
+}
+
+/// Sequential baseline trainer (learner.hpp:197-225) on the device: the skip policy
+/// decides which items train; skipped items log as dropped.
+inline TrainOutcome train_sequential(DenseNet net, const DataStream& stream, double t_d, const SkipPolicy& policy,
+                                     double processing_time, double lr = kLearningRate, bool replay = false,
+                                     std::uint64_t replay_seed = 0, const B200Options& b200 = B200Options{}) {
+    net.validate();
+    const FilteredStream filtered = apply_skip_policy(stream.items.size(), t_d, policy, processing_time);
+    const std::size_t n = stream.items.size(), f = stream.n_features;
+    std::vector<double> features(n * f);
+    std::vector<uint64_t> labels(n);
+    for (std::size_t i = 0; i < n; ++i) {
+        std::copy(stream.items[i].features.begin(), stream.items[i].features.end(), features.begin() + i * f);
+        labels[i] = stream.items[i].label;
+    }
+    std::vector<int64_t> kept;
+    for (const KeptItem& k : filtered.kept) kept.push_back(k.index);
+    ferret_seq_opts o{};
+    o.policy = FERRET_POLICY_NONE;
+    o.ring_depth = 1;
+    o.lr = lr;
+    o.eta_lambda = 0.0;
+    o.replay = replay ? 1 : 0;
+    o.replay_seed = replay_seed;
+    o.replay_capacity = kReplayBuffer;
+    o.precision = b200.precision;
+    o.device = b200.device;
+    detail::SeqHandle h = detail::make_seq(net, o);
+    std::vector<ferret_step_record> raw(n);
+    b200_check(ferret_seq_train(h.get(), features.data(), labels.data(), n, f, kept.data(), kept.size(), raw.data()));
+    TrainOutcome res{std::vector<StepRecord>(n), std::move(net), RunningNormalizer(f)};
+    for (std::size_t i = 0; i < n; ++i)
+        res.log[i] = StepRecord{raw[i].item, static_cast<StepOutcome>(raw[i].outcome),
+                                static_cast<std::size_t>(raw[i].predicted), static_cast<std::size_t>(raw[i].label)};
+    detail::read_back(h.get(), res.net, res.normalizer, f);
+    return res;
+}
+
 inline TrainOutcome train_pipeline(DenseNet net, const PartitionScheme& scheme, const SimTrace& trace,
                                    const DataStream& stream, const PipelineTrainOptions& opt) {
     return PipelineTrainer(std::move(net), scheme, opt).run(trace, stream);

@@ -317,6 +317,14 @@ FERRET_API ferret_status ferret_seq_ocl_steps(ferret_trainer* t, const double* f
 FERRET_API ferret_status ferret_seq_train(ferret_trainer* t, const double* features, const uint64_t* labels,
                                           size_t n_items, size_t n_features, const int64_t* kept, size_t n_kept,
                                           ferret_step_record* log_out);
+/* predict_class (net.hpp:150-154) at the live version for n_items held-out rows,
+ * standardised with the learner's normalizer state, observing nothing
+ * (test_accuracy, learner.hpp:185-192). */
+FERRET_API ferret_status ferret_seq_predict(ferret_trainer* t, const double* features, size_t n_items,
+                                            size_t n_features, uint64_t* preds_out);
+/* Restore a RunningNormalizer state (count, mean[f], m2[f]) into the learner. */
+FERRET_API ferret_status ferret_seq_set_normalizer(ferret_trainer* t, uint64_t count, const double* mean,
+                                                   const double* m2, size_t n_features);
 /* apply_skip_policy (stream.hpp:225-304) on the host: kind 0 oracle, 1 one_skip,
  * 2 random_n, 3 last_n (SkipPolicy{kind, window, keep, seed}); kept_out and
  * start_out (nullable) hold up to n_items entries, *n_kept is set. */

@@ -903,16 +903,20 @@ __global__ void normalize_kernel(const NormArgs a) {
     unsigned long long cnt = *a.count_base + a.count_off;
     for (long long i = 0; i < a.n; ++i) {
         const double x = a.raw[i * a.F + f];
-        ++cnt;
-        const double d = __dsub_rn(x, mu);
-        mu = __dadd_rn(mu, __ddiv_rn(d, (double)cnt));
-        m2 = __dadd_rn(m2, __dmul_rn(d, __dsub_rn(x, mu)));
+        if (!a.apply_only) {
+            ++cnt;
+            const double d = __dsub_rn(x, mu);
+            mu = __dadd_rn(mu, __ddiv_rn(d, (double)cnt));
+            m2 = __dadd_rn(m2, __dmul_rn(d, __dsub_rn(x, mu)));
+        }
         const double var = cnt > 1 ? __ddiv_rn(m2, (double)(cnt - 1)) : 1.0;
         const double sd = __dsqrt_rn(var < 1e-8 ? 1e-8 : var);
         a.out[i * a.F + f] = (float)__ddiv_rn(__dsub_rn(x, mu), sd);
     }
-    a.mean[f] = mu;
-    a.m2[f] = m2;
+    if (!a.apply_only) {
+        a.mean[f] = mu;
+        a.m2[f] = m2;
+    }
 }
 
 // Replay-pool insertion: one CTA per sample of the unit.

@@ -132,6 +132,7 @@ struct NormArgs {
     double* mean;
     double* m2;
     float* out;          // n x F
+    int apply_only;      // 1: standardise with the current state, observe nothing (held-out evaluation)
 };
 
 // Replay-pool insertion at an arrival (ReplayBuffer::add, learner.hpp:61-69):

@@ -1123,7 +1123,7 @@ struct ferret_trainer {
                 const size_t ns = (u1 - u0) * static_cast<size_t>(B);
                 fb200::NormArgs na{d_rawc + s0 * static_cast<size_t>(F), static_cast<long long>(ns), F, ctl_count(),
                                    static_cast<unsigned long long>(s0), d_norm_mean, d_norm_m2,
-                                   d_xc + s0 * static_cast<size_t>(F)};
+                                   d_xc + s0 * static_cast<size_t>(F), 0};
                 fb200::KernelSpec k;
                 fb200::spec_normalize(na, k);
                 gb->cur_bytes = 20.0 * static_cast<double>(ns) * F;  // raw fp64 in, fp32 out, + state
@@ -1529,6 +1529,8 @@ struct ferret_trainer {
         double* d_raw = nullptr;   // raw features of the call
         int* d_lab = nullptr;      // per item: label, replay-sample label
         int* d_pred = nullptr;
+        float* d_px = nullptr;     // held-out rows (16 x F), standardised
+        float* d_pp = nullptr;     // their layer ping-pong (2 x 16 x max width)
         size_t cap = 0;
         std::unique_ptr<GraphBuilder> gb;  // eager builder on the trainer's stream
     } sq;
@@ -1582,7 +1584,7 @@ struct ferret_trainer {
     void seq_item(size_t i, long long read, int rows, int policy) {
         using GB = GraphBuilder;
         fb200::NormArgs na{sq.d_raw + i * static_cast<size_t>(F), 1, F, sq.d_zero,
-                           static_cast<unsigned long long>(sq.norm_count), d_norm_mean, d_norm_m2, sq.d_ux};
+                           static_cast<unsigned long long>(sq.norm_count), d_norm_mean, d_norm_m2, sq.d_ux, 0};
         fb200::KernelSpec kn;
         fb200::spec_normalize(na, kn);
         gb->kernel(kn, {}, {});
@@ -1651,6 +1653,62 @@ struct ferret_trainer {
         cudaGraphExecDestroy(ge);
         cuda_check(l, "cudaGraphLaunch");
         cuda_check(y, "sequential run");
+    }
+
+    // predict_class at the live version for held-out items, standardised with the
+    // current normalizer state and observing nothing (test_accuracy, learner.hpp:185-192):
+    // groups of up to 16 rows through the layer kernels.
+    void seq_predict(const double* features, size_t n, uint64_t* preds) {
+        if (n == 0) return;
+        using GB = GraphBuilder;
+        constexpr int G = fb200::kMaxBatch;
+        int max_width = F;
+        for (const LayerDev& ld : layers) max_width = std::max(max_width, ld.out);
+        if (!sq.d_px) {
+            sq.d_px = dalloc<float>(static_cast<size_t>(G) * static_cast<size_t>(F), device_bytes);
+            sq.d_pp = dalloc<float>(2 * static_cast<size_t>(G) * static_cast<size_t>(max_width), device_bytes);
+            if (opt.precision != FERRET_PREC_FP32) mma_scratch_for(GB::key(GB::kReplay, 1));
+        }
+        std::vector<uint64_t> none(n, 0);
+        seq_upload(features, none.data(), n);
+        const size_t pstride = static_cast<size_t>(G) * static_cast<size_t>(max_width);
+        const StageDev& s = stages[0];
+        const int keep_b = B;
+        seq_run((n + G - 1) / G, [&](size_t g) {
+            const size_t i0 = g * G;
+            const int rows = static_cast<int>(std::min<size_t>(G, n - i0));
+            fb200::NormArgs na{sq.d_raw + i0 * static_cast<size_t>(F), rows, F, sq.d_zero,
+                               static_cast<unsigned long long>(sq.norm_count), d_norm_mean, d_norm_m2, sq.d_px, 1};
+            fb200::KernelSpec kn;
+            fb200::spec_normalize(na, kn);
+            gb->kernel(kn, {}, {});
+            B = rows;
+            for (int l = 0; l < L; ++l) {
+                const float* X = l == 0 ? sq.d_px : sq.d_pp + static_cast<size_t>((l - 1) & 1) * pstride;
+                emit_layer(layers[static_cast<size_t>(l)], s.slot(sq.version), X, nullptr,
+                           sq.d_pp + static_cast<size_t>(l & 1) * pstride, {}, {GB::key(GB::kReplay, 1)});
+            }
+            fb200::HeadArgs h{};
+            h.logits = sq.d_pp + static_cast<size_t>((L - 1) & 1) * pstride;
+            h.n_out = n_out;
+            h.B = rows;
+            h.mode = 0;
+            h.pred = sq.d_pred + i0;
+            fb200::KernelSpec kh;
+            fb200::spec_head(h, kh);
+            gb->kernel(kh, {}, {});
+            B = keep_b;
+        });
+        std::vector<int> p(n);
+        cuda_check(cudaMemcpy(p.data(), sq.d_pred, n * sizeof(int), cudaMemcpyDeviceToHost), "D2H predictions");
+        for (size_t i = 0; i < n; ++i) preds[i] = static_cast<uint64_t>(p[i]);
+    }
+
+    void set_normalizer(uint64_t count, const double* mean, const double* m2) {
+        cuda_check(cudaStreamSynchronize(stream), "sync");
+        cuda_check(cudaMemcpy(d_norm_mean, mean, static_cast<size_t>(F) * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+        cuda_check(cudaMemcpy(d_norm_m2, m2, static_cast<size_t>(F) * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+        sq.norm_count = count;
     }
 
     // StaleHarness::ocl_step over n items (learner.hpp:145-163)
@@ -1979,6 +2037,27 @@ ferret_status ferret_seq_ocl_steps(ferret_trainer* t, const double* features, co
         if (n_items && (!features || !labels || !taus || !preds_out)) fail(FERRET_E_INVALID_ARG, "null buffer");
         cuda_check(cudaSetDevice(t->opt.device), "cudaSetDevice");
         t->harness_steps(features, labels, taus, n_items, preds_out);
+    });
+}
+
+ferret_status ferret_seq_predict(ferret_trainer* t, const double* features, size_t n_items, size_t n_features,
+                                 uint64_t* preds_out) {
+    return guarded([&] {
+        if (!t->sq.on) fail(FERRET_E_CONFIG, "seq_predict: not a sequential learner (ferret_seq_create)");
+        if (n_features != static_cast<size_t>(t->F)) fail(FERRET_E_INVALID_ARG, "feature width mismatch");
+        if (n_items && (!features || !preds_out)) fail(FERRET_E_INVALID_ARG, "null buffer");
+        cuda_check(cudaSetDevice(t->opt.device), "cudaSetDevice");
+        t->seq_predict(features, n_items, preds_out);
+    });
+}
+
+ferret_status ferret_seq_set_normalizer(ferret_trainer* t, uint64_t count, const double* mean, const double* m2,
+                                        size_t n_features) {
+    return guarded([&] {
+        if (!t->sq.on) fail(FERRET_E_CONFIG, "seq_set_normalizer: not a sequential learner (ferret_seq_create)");
+        if (n_features != static_cast<size_t>(t->F)) fail(FERRET_E_INVALID_ARG, "normalizer: width mismatch");
+        cuda_check(cudaSetDevice(t->opt.device), "cudaSetDevice");
+        t->set_normalizer(count, mean, m2);
     });
 }
 

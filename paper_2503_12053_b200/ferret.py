@@ -152,6 +152,8 @@ def lib() -> C.CDLL:
                                            P(C.c_uint64)]),
         "ferret_seq_train": (C.c_int, [C.c_void_p, P(D), P(C.c_uint64), C.c_size_t, C.c_size_t, P(C.c_int64),
                                        C.c_size_t, C.c_void_p]),
+        "ferret_seq_predict": (C.c_int, [C.c_void_p, P(D), C.c_size_t, C.c_size_t, P(C.c_uint64)]),
+        "ferret_seq_set_normalizer": (C.c_int, [C.c_void_p, C.c_uint64, P(D), P(D), C.c_size_t]),
         "ferret_apply_skip_policy": (C.c_int, [C.c_size_t, D, C.c_int32, C.c_uint64, C.c_uint64, C.c_uint64, D,
                                                P(C.c_int64), P(D), P(C.c_size_t)]),
         "ferret_dense_layer": (C.c_int, [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -543,6 +545,24 @@ class _SeqLearner:
         m2 = np.empty(n_features)
         _check(lib().ferret_trainer_normalizer(self._h, C.byref(cnt), _dp(mean), _dp(m2), n_features))
         return int(cnt.value), mean, m2
+
+    def set_normalizer(self, count: int, mean: np.ndarray, m2: np.ndarray) -> None:
+        mean = np.ascontiguousarray(mean, dtype=np.float64)
+        m2 = np.ascontiguousarray(m2, dtype=np.float64)
+        _check(lib().ferret_seq_set_normalizer(self._h, count, _dp(mean), _dp(m2), mean.size))
+
+    def predict(self, features: np.ndarray) -> np.ndarray:
+        """predict_class at the live version for held-out rows (standardised, nothing observed)."""
+        f = np.ascontiguousarray(features, dtype=np.float64)
+        out = np.empty(len(f), dtype=np.uint64)
+        _check(lib().ferret_seq_predict(self._h, _dp(f), len(f), f.shape[1], _up(out)))
+        return out
+
+    def test_accuracy(self, features: np.ndarray, labels: np.ndarray) -> float:
+        """test_accuracy (learner.hpp:185-192) on the device, in percentage points."""
+        if len(features) == 0:
+            return 0.0
+        return 100.0 * float(np.mean(self.predict(features) == np.asarray(labels, dtype=np.uint64)))
 
     def close(self) -> None:
         if getattr(self, "_h", None):

@@ -87,3 +87,37 @@ def test_train_sequential_fast(gpu, fb, orc, prec):
     ref = orc.train_sequential(widths, params, feats, labels, **kw)
     assert abs(fb.online_accuracy(log) - fb.online_accuracy(ref["log"])) <= OACC_TOL
     assert _rel(got, ref["params"], params) < 2e-2
+
+
+def _np_predict(widths, params, x):
+    """fp64 numpy predict_class (net.hpp:130-154): ReLU hidden layers, first-index argmax."""
+    off = 0
+    h = x
+    for i in range(len(widths) - 1):
+        n_in, n_out = widths[i], widths[i + 1]
+        W = params[off:off + n_in * n_out].reshape(n_out, n_in)
+        b = params[off + n_in * n_out:off + n_in * n_out + n_out]
+        off += n_in * n_out + n_out
+        h = h @ W.T + b
+        if i < len(widths) - 2:
+            h = np.maximum(h, 0.0)
+    return np.argmax(h, axis=1)
+
+
+@pytest.mark.gpu
+def test_held_out_accuracy(gpu, fb, orc):
+    """test_accuracy: standardise with the learner's normalizer (nothing observed), predict on the device."""
+    widths = [96, 128, 64, 10]
+    params = fb.make_dense_net(widths, 1)
+    feats, labels = fb.synth_drift_stream(300, widths[0], widths[-1], "split_tasks", 7)
+    log, got, learner = fb.train_sequential(widths, params, feats[:200], labels[:200])
+    cnt, mean, m2 = learner.normalizer(widths[0])
+    assert cnt == 200
+    var = np.where(cnt > 1, m2 / (cnt - 1), 1.0)
+    x = (feats[200:] - mean) / np.sqrt(np.maximum(var, 1e-8))
+    ref = _np_predict(widths, got, x)
+    pred = learner.predict(feats[200:])
+    assert np.count_nonzero(pred != ref) <= 1
+    assert abs(learner.test_accuracy(feats[200:], labels[200:]) - 100.0 * np.mean(ref == labels[200:])) <= 1.0
+    assert learner.normalizer(widths[0])[0] == 200  # nothing observed
+    learner.close()
