@@ -165,6 +165,12 @@ FERRET_API ferret_status ferret_schedule_forced(const ferret_layer_profile* laye
                                      int32_t n_bounds, int32_t recompute, size_t n_items,
                                      ferret_schedule** out);
 /* number of bounds; copies min(n, cap) into out */
+/* A schedule from persisted text (no reference counterpart: the reference
+ * writes plans and traces, planner.hpp:217-246, sim.hpp:406-436, and reads
+ * only plans, planner.hpp:248-309): ferret-plan v1 gives the partition, the
+ * ferret-trace v1 event log the replay. Malformed text -> FERRET_E_SCHEMA. */
+FERRET_API ferret_status ferret_schedule_load(const char* plan_text, size_t plan_len, const char* trace_text,
+                                              size_t trace_len, ferret_schedule** out);
 FERRET_API int32_t ferret_schedule_bounds(const ferret_schedule* s, uint64_t* out, int32_t cap);
 FERRET_API size_t ferret_schedule_event_count(const ferret_schedule* s);
 FERRET_API ferret_status ferret_schedule_events(const ferret_schedule* s, ferret_event* out, size_t cap);

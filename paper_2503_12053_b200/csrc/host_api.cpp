@@ -159,6 +159,25 @@ ferret_status ferret_schedule_forced(const ferret_layer_profile* layers, int32_t
     });
 }
 
+ferret_status ferret_schedule_load(const char* plan_text, size_t plan_len, const char* trace_text, size_t trace_len,
+                                   ferret_schedule** out) {
+    return guarded([&] {
+        if (!plan_text || !trace_text || !out) fail(FERRET_E_INVALID_ARG, "schedule_load: null argument");
+        auto s = std::make_unique<ferret_schedule>();
+        std::istringstream pin(std::string(plan_text, plan_len));
+        s->plan = ferret::parse_plan(pin, "plan");
+        std::istringstream tin(std::string(trace_text, trace_len));
+        ferret::LoadedTrace lt = ferret::parse_trace(tin, "trace");
+        s->trace = std::move(lt.trace);
+        s->spec.t_d = s->trace.t_d;
+        s->spec.horizon = static_cast<double>(s->trace.n_items) * s->trace.t_d;
+        const std::size_t P = s->plan.partition.stages();
+        for (const ferret::SimEvent& e : s->trace.events)
+            if (e.stage >= static_cast<int>(P)) fail(FERRET_E_SCHEMA, "trace: event stage beyond the plan's partition");
+        *out = s.release();
+    });
+}
+
 int32_t ferret_schedule_bounds(const ferret_schedule* s, uint64_t* out, int32_t cap) {
     const auto& b = s->plan.partition.bounds;
     for (int32_t i = 0; i < cap && i < static_cast<int32_t>(b.size()); ++i) out[i] = b[static_cast<size_t>(i)];

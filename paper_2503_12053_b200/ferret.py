@@ -117,6 +117,7 @@ def lib() -> C.CDLL:
                                            C.c_size_t, P(C.c_void_p)]),
         "ferret_schedule_forced": (C.c_int, [C.c_void_p, C.c_int32, D, P(StreamSpecC), P(C.c_uint64), C.c_int32,
                                              C.c_int32, C.c_size_t, P(C.c_void_p)]),
+        "ferret_schedule_load": (C.c_int, [C.c_char_p, C.c_size_t, C.c_char_p, C.c_size_t, P(C.c_void_p)]),
         "ferret_schedule_bounds": (C.c_int32, [C.c_void_p, P(C.c_uint64), C.c_int32]),
         "ferret_schedule_event_count": (C.c_size_t, [C.c_void_p]),
         "ferret_schedule_events": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t]),
@@ -263,6 +264,22 @@ class Schedule:
         _check(lib().ferret_schedule_forced(prof.ctypes.data, len(prof), t_d, C.byref(spec.c()), _up(b), len(b),
                                             recompute, n_items, C.byref(h)))
         return cls(h.value)
+
+    @classmethod
+    def from_text(cls, plan_text: str, trace_text: str) -> "Schedule":
+        """A schedule from persisted ferret-plan v1 + ferret-trace v1 text (SchemaError if malformed)."""
+        h = C.c_void_p()
+        p, t = plan_text.encode(), trace_text.encode()
+        _check(lib().ferret_schedule_load(p, len(p), t, len(t), C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def load(cls, plan_path: str, trace_path: str) -> "Schedule":
+        with open(plan_path) as f:
+            plan_text = f.read()
+        with open(trace_path) as f:
+            trace_text = f.read()
+        return cls.from_text(plan_text, trace_text)
 
     def _text(self, fn) -> str:
         n = fn(self._h, None, 0)
