@@ -17,6 +17,9 @@
 #pragma once
 
 #include <cstdint>
+#include <fstream>
+#include <iterator>
+#include <string>
 #include <memory>
 #include <vector>
 
@@ -216,6 +219,24 @@ class PipelineTrainer {
     }
 
     ferret_trainer* handle() { return handle_.get(); }
+
+    /// Exact resume (no reference counterpart; extends ferret-ckpt v1, net.hpp:210-259,
+    /// with the trainer state): "ferret-state v1" between run() calls.
+    void save_state(const std::string& path) {
+        std::size_t n = 0;
+        b200_check(ferret_trainer_save_state(handle_.get(), nullptr, 0, &n));
+        std::string buf(n, '\0');
+        b200_check(ferret_trainer_save_state(handle_.get(), buf.data(), buf.size(), &n));
+        std::ofstream out(path, std::ios::binary);
+        if (!out || !out.write(buf.data(), static_cast<std::streamsize>(buf.size())))
+            throw SchemaError(path + ": cannot write state file");
+    }
+    void load_state(const std::string& path) {
+        std::ifstream in(path, std::ios::binary);
+        if (!in) throw SchemaError(path + ": cannot read state file");
+        const std::string buf((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+        b200_check(ferret_trainer_load_state(handle_.get(), buf.data(), buf.size()));
+    }
 
   private:
     struct Release {

@@ -287,6 +287,17 @@ FERRET_API ferret_status ferret_trainer_profile(ferret_trainer* t, double* class
 FERRET_API ferret_status ferret_trainer_update_timing(ferret_trainer* t, double* total_ms, uint64_t* launches,
                                                       double* alg_bytes);
 
+/* Exact resume (ferret-ckpt v1, net.hpp:210-259, extended with the
+ * trainer state): "ferret-state v1" = text header (net shape, bounds, options,
+ * normalizer count, version counters, replay reservoir RNG state and labels)
+ * + raw arrays (live parameters per stage in the device slot layout,
+ * compensator state, normalizer mean/M2, replay pool rows). Valid between
+ * execute()/run() calls. save_state: *size = bytes needed; the state is
+ * written when buf has room. load_state into a trainer built with the same
+ * net, bounds and options continues bit for bit; mismatch -> FERRET_E_SCHEMA. */
+FERRET_API ferret_status ferret_trainer_save_state(ferret_trainer* t, void* buf, size_t cap, size_t* size);
+FERRET_API ferret_status ferret_trainer_load_state(ferret_trainer* t, const void* buf, size_t len);
+
 /* ---------------- sequential learners on the device ---------------- */
 
 /* Options of a sequential learner: StaleHarness(net, policy, ring_depth, lr,

@@ -40,6 +40,7 @@
 #include <map>
 #include <tuple>
 #include <memory>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -1512,6 +1513,149 @@ struct ferret_trainer {
         gb->kernel(k, reads, {stash_key});
     }
 
+    // ------------------------------------------------ exact resume
+    // "ferret-state v1": everything a pipeline trainer carries from one chunk to
+    // the next — the live parameters of every stage (ring slot 0 between chunks),
+    // the compensator state, the RunningNormalizer, the version counters and the
+    // replay reservoir (host RNG state, positions' labels, pool rows). A text
+    // header (shape and options, checked on load) followed by raw little-endian
+    // arrays in the device slot layout. Loading it into a trainer built with the
+    // same net, bounds and options continues training bit for bit.
+    std::string save_state() {
+        if (sq.on) fail(FERRET_E_CONFIG, "save_state: sequential learners carry no pipeline state");
+        cuda_check(cudaStreamSynchronize(stream), "sync");
+        std::string bin;
+        auto put_dev = [&](const void* dev, size_t bytes) {
+            const size_t at = bin.size();
+            bin.resize(at + bytes);
+            if (bytes) cuda_check(cudaMemcpy(&bin[at], dev, bytes, cudaMemcpyDeviceToHost), "D2H state");
+        };
+        for (const StageDev& st : stages) {
+            const size_t sb = static_cast<size_t>(st.slot_floats) * sizeof(float);
+            put_dev(st.slot(0), sb);
+            for (const float* a : {st.lam_d, st.v_r, st.v_a, st.gap})
+                if (a) put_dev(a, sb);
+        }
+        put_dev(d_norm_mean, static_cast<size_t>(F) * sizeof(double));
+        put_dev(d_norm_m2, static_cast<size_t>(F) * sizeof(double));
+        if (opt.replay && hs.replay.size) {
+            put_dev(d_pool_x, static_cast<size_t>(hs.replay.size) * static_cast<size_t>(F) * sizeof(float));
+            put_dev(d_pool_lab, static_cast<size_t>(hs.replay.size) * sizeof(int));
+        }
+        std::ostringstream h;
+        h << "ferret-state v1\n" << "layers";
+        for (const LayerDev& ld : layers) h << ' ' << ld.in << 'x' << ld.out << ':' << ld.act;
+        h << "\nbounds";
+        for (const StageDev& st : stages) h << ' ' << st.lo;
+        h << ' ' << L << "\noptions policy " << opt.policy << " replay " << opt.replay << " capacity "
+          << opt.replay_capacity << " precision " << opt.precision << " micro_batch " << B << "\n"
+          << "norm_count " << hs.norm_count << "\nversions";
+        for (long long v : hs.current) h << ' ' << v;
+        h << "\nreservoir " << hs.replay.seen << ' ' << hs.replay.size << "\nrng " << hs.replay.rng.state()
+          << "\nlabels";
+        for (uint64_t i = 0; i < hs.replay.size; ++i) h << ' ' << hs.replay.label_at[static_cast<size_t>(i)];
+        h << "\nbinary " << bin.size() << "\n";
+        return h.str() + bin;
+    }
+
+    void load_state(const char* data, size_t len) {
+        if (sq.on) fail(FERRET_E_CONFIG, "load_state: sequential learners carry no pipeline state");
+        const std::string all(data, len);
+        std::istringstream in(all);
+        std::string line;
+        auto expect = [&](const std::string& want) {
+            if (!std::getline(in, line) || line != want) fail(FERRET_E_SCHEMA, "state: expected '" + want + "'");
+        };
+        expect("ferret-state v1");
+        {
+            std::ostringstream l, b, o;
+            l << "layers";
+            for (const LayerDev& ld : layers) l << ' ' << ld.in << 'x' << ld.out << ':' << ld.act;
+            b << "bounds";
+            for (const StageDev& st : stages) b << ' ' << st.lo;
+            b << ' ' << L;
+            o << "options policy " << opt.policy << " replay " << opt.replay << " capacity " << opt.replay_capacity
+              << " precision " << opt.precision << " micro_batch " << B;
+            expect(l.str());
+            expect(b.str());
+            expect(o.str());
+        }
+        auto record = [&](const char* key) {
+            if (!std::getline(in, line)) fail(FERRET_E_SCHEMA, std::string("state: truncated before '") + key + "'");
+            std::istringstream f(line);
+            std::string got;
+            f >> got;
+            if (got != key) fail(FERRET_E_SCHEMA, std::string("state: expected '") + key + "'");
+            return f;
+        };
+        uint64_t norm_count = 0, seen = 0, size = 0;
+        if (!(record("norm_count") >> norm_count)) fail(FERRET_E_SCHEMA, "state: bad norm_count");
+        std::vector<long long> versions(static_cast<size_t>(P));
+        {
+            auto f = record("versions");
+            for (long long& v : versions)
+                if (!(f >> v)) fail(FERRET_E_SCHEMA, "state: bad versions");
+        }
+        {
+            auto f = record("reservoir");
+            if (!(f >> seen >> size) || size > opt.replay_capacity || size > seen)
+                fail(FERRET_E_SCHEMA, "state: bad reservoir");
+        }
+        std::string rng_state;
+        {
+            if (!std::getline(in, line) || line.compare(0, 4, "rng ") != 0) fail(FERRET_E_SCHEMA, "state: bad rng");
+            rng_state = line.substr(4);
+        }
+        std::vector<int> labels(static_cast<size_t>(size));
+        {
+            auto f = record("labels");
+            for (int& x : labels)
+                if (!(f >> x)) fail(FERRET_E_SCHEMA, "state: bad labels");
+        }
+        size_t nbin = 0;
+        if (!(record("binary") >> nbin)) fail(FERRET_E_SCHEMA, "state: bad binary size");
+        const size_t off = static_cast<size_t>(in.tellg());
+        if (off + nbin != len) fail(FERRET_E_SCHEMA, "state: binary section size mismatch");
+        const char* p = data + off;
+        size_t left = nbin;
+        auto take_dev = [&](void* dev, size_t bytes) {
+            if (bytes > left) fail(FERRET_E_SCHEMA, "state: binary section too short");
+            if (bytes) cuda_check(cudaMemcpy(dev, p, bytes, cudaMemcpyHostToDevice), "H2D state");
+            p += bytes;
+            left -= bytes;
+        };
+        invalidate_graph();
+        cuda_check(cudaStreamSynchronize(stream), "sync");
+        for (StageDev& st : stages) {
+            const size_t sb = static_cast<size_t>(st.slot_floats) * sizeof(float);
+            if (sb > left) fail(FERRET_E_SCHEMA, "state: binary section too short");
+            if (st.ring16) {  // the bf16 copy of the live slot
+                std::vector<float> h(static_cast<size_t>(st.slot_floats));
+                std::memcpy(h.data(), p, sb);
+                std::vector<uint16_t> h16(h.size());
+                for (size_t i = 0; i < h.size(); ++i) h16[i] = bf16_bits(h[i]);
+                cuda_check(cudaMemcpy(st.ring16, h16.data(), h16.size() * sizeof(uint16_t), cudaMemcpyHostToDevice),
+                           "H2D state");
+            }
+            take_dev(st.slot(0), sb);
+            for (float* a : {st.lam_d, st.v_r, st.v_a, st.gap})
+                if (a) take_dev(a, sb);
+        }
+        take_dev(d_norm_mean, static_cast<size_t>(F) * sizeof(double));
+        take_dev(d_norm_m2, static_cast<size_t>(F) * sizeof(double));
+        if (opt.replay && size) {
+            take_dev(d_pool_x, static_cast<size_t>(size) * static_cast<size_t>(F) * sizeof(float));
+            take_dev(d_pool_lab, static_cast<size_t>(size) * sizeof(int));
+        }
+        if (left) fail(FERRET_E_SCHEMA, "state: trailing bytes in the binary section");
+        hs.norm_count = norm_count;
+        hs.current = versions;
+        hs.replay.seen = seen;
+        hs.replay.size = size;
+        hs.replay.rng.restore(rng_state);
+        hs.replay.label_at = labels;
+    }
+
     // ------------------------------------------------ sequential learners
     // StaleHarness (learner.hpp:132-170) and train_sequential (learner.hpp:197-225)
     // on the device. The trainer holds every layer in one stage; each item's
@@ -1997,6 +2141,26 @@ ferret_status ferret_trainer_create(const ferret_net_desc* net, const uint64_t* 
         t->build(*net, bounds, n_bounds);
         cuda_check(cudaDeviceSynchronize(), "create");
         *out = t.release();
+    });
+}
+
+ferret_status ferret_trainer_save_state(ferret_trainer* t, void* buf, size_t cap, size_t* size) {
+    return guarded([&] {
+        if (!size) fail(FERRET_E_INVALID_ARG, "save_state: null size");
+        t->require_device_mode();
+        cuda_check(cudaSetDevice(t->opt.device), "cudaSetDevice");
+        const std::string s = t->save_state();
+        *size = s.size();
+        if (buf && cap >= s.size()) std::memcpy(buf, s.data(), s.size());
+    });
+}
+
+ferret_status ferret_trainer_load_state(ferret_trainer* t, const void* buf, size_t len) {
+    return guarded([&] {
+        if (!buf) fail(FERRET_E_INVALID_ARG, "load_state: null buffer");
+        t->require_device_mode();
+        cuda_check(cudaSetDevice(t->opt.device), "cudaSetDevice");
+        t->load_state(static_cast<const char*>(buf), len);
     });
 }
 

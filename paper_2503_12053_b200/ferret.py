@@ -159,6 +159,8 @@ def lib() -> C.CDLL:
                                                P(C.c_int64), P(D), P(C.c_size_t)]),
         "ferret_dense_layer": (C.c_int, [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                          C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]),
+        "ferret_trainer_save_state": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, P(C.c_size_t)]),
+        "ferret_trainer_load_state": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t]),
         "ferret_compensate": (C.c_int, [C.c_int32, P(D), P(P(D)), C.c_int32, P(D), P(D), P(D), P(D), C.c_size_t,
                                         D, D, D, D, P(D)]),
     }
@@ -407,6 +409,17 @@ class PipelineTrainer:
         out = np.empty(self.n_params, dtype=np.float64)
         _check(lib().ferret_trainer_params(self._h, _dp(out), out.size))
         return out
+
+    def save_state(self) -> bytes:
+        """ferret-state v1 (exact resume between execute()/run() calls)."""
+        n = C.c_size_t()
+        _check(lib().ferret_trainer_save_state(self._h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        _check(lib().ferret_trainer_save_state(self._h, buf, n.value, C.byref(n)))
+        return buf.raw[: n.value]
+
+    def load_state(self, state: bytes) -> None:
+        _check(lib().ferret_trainer_load_state(self._h, state, len(state)))
 
     def comp_state(self, stage: int, n: int):
         lam, vr, va, gap = (np.empty(n, dtype=np.float64) for _ in range(4))

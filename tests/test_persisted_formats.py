@@ -86,3 +86,70 @@ def test_replay_from_loaded_schedule_is_identical(gpu, fb, tmp_path):
         tr.close()
     assert np.array_equal(out[0][0], out[1][0])
     assert np.array_equal(out[0][1], out[1][1])
+
+
+def _c2_workload(fb, units, chunks):
+    widths = [784, 256, 256, 256, 10]
+    prof = fb.profile_from_widths(widths)
+    t_d = float(prof["t_f"].max())
+    sched = fb.Schedule.forced(prof, t_d, fb.StreamSpec(t_d=t_d, horizon=units * t_d), [0, 1, 2, 3, 4], units)
+    feats, labels = fb.synth_drift_stream(units * 16 * chunks, widths[0], widths[-1], "split_tasks", 7)
+    return widths, sched, feats, labels
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_exact_resume(gpu, fb, prec):
+    """Train 4 chunks straight vs 2 chunks, save, a fresh trainer loads and trains 2 more:
+    identical logs, parameters, compensator state and normalizer (bit for bit)."""
+    units, chunks = 48, 4
+    widths, sched, feats, labels = _c2_workload(fb, units, chunks)
+    params = fb.make_dense_net(widths, 1)
+    opt = fb.PipelineTrainOptions(policy="iter_fisher", replay=True, replay_seed=3, micro_batch=16, precision=prec)
+
+    def trainer():
+        t = fb.PipelineTrainer(widths, params, sched.bounds, opt)
+        t.load_stream(feats, labels)
+        t.set_schedule(sched.events, units * 16)
+        return t
+
+    a = trainer()
+    logs_a = []
+    for c in range(chunks):
+        a.execute(c)
+        logs_a.append(a.fetch_log(c))
+    b = trainer()
+    for c in range(2):
+        b.execute(c)
+    state = b.save_state()
+    assert state.startswith(b"ferret-state v1\n")
+    b.close()
+    c_ = trainer()
+    c_.load_state(state)
+    for c in range(2, chunks):
+        c_.execute(c)
+        assert np.array_equal(c_.fetch_log(c), logs_a[c])
+    assert np.array_equal(c_.params(), a.params())
+    for j in range(4):
+        n = widths[j] * widths[j + 1] + widths[j + 1]
+        for got, ref in zip(c_.comp_state(j, n), a.comp_state(j, n)):
+            assert np.array_equal(got, ref)
+    for got, ref in zip(c_.normalizer(widths[0]), a.normalizer(widths[0])):
+        assert np.array_equal(np.asarray(got), np.asarray(ref))
+    a.close()
+    c_.close()
+
+
+@pytest.mark.gpu
+def test_state_mismatch_is_schema_error(gpu, fb):
+    widths, sched, feats, labels = _c2_workload(fb, 16, 1)
+    params = fb.make_dense_net(widths, 1)
+    a = fb.PipelineTrainer(widths, params, [0, 1, 2, 3, 4], fb.PipelineTrainOptions(policy="iter_fisher"))
+    state = a.save_state()
+    b = fb.PipelineTrainer(widths, params, [0, 2, 4], fb.PipelineTrainOptions(policy="iter_fisher"))
+    with pytest.raises(fb.SchemaError):
+        b.load_state(state)
+    with pytest.raises(fb.SchemaError):
+        a.load_state(state[:-8])
+    a.close()
+    b.close()
