@@ -352,25 +352,23 @@ def main():
     large = config5_roofline(fb, torch, local) if not args.no_large else None
     shard = stage_shard_measure(fb, torch, dist, rank, world, local, args, units) if world > 1 else None
 
-    # ---- e2e through the reference-facing call from pinned host buffers
+    # ---- e2e through the public API with host buffers: PipelineTrainer ingest
+    # (ferret_trainer_ingest) of the step's samples from pinned host memory, each
+    # step's H2D copy and D2H StepRecord read inside the timed region (copies of
+    # step s+1 overlap the compute of step s through two staging slots)
     tr2 = fb.PipelineTrainer(WIDTHS, params, BOUNDS, opt)
-    pin_f = torch.empty((chunk, WIDTHS[0]), dtype=torch.float64).pin_memory()
-    pin_l = torch.empty((chunk,), dtype=torch.int64).pin_memory()
-    e2e_times = []
-    h2d = chunk * WIDTHS[0] * 8 + chunk * 8
+    tr2.set_schedule(sched.events, chunk)
+    pin_f = torch.from_numpy(np.ascontiguousarray(feats[: n_chunks * chunk])).pin_memory()
+    pin_l = torch.from_numpy(labels[: n_chunks * chunk].astype(np.int64)).pin_memory()
+    h2d = chunk * WIDTHS[0] * 8 + chunk * 4
     d2h = chunk * 4
-    for s in range(args.warmup + args.steps):
-        c = s % n_chunks
-        pin_f.numpy()[:] = feats[c * chunk:(c + 1) * chunk]
-        pin_l.numpy()[:] = labels[c * chunk:(c + 1) * chunk].astype(np.int64)
-        if dist:
-            dist.barrier()
-        t0 = time.perf_counter()
-        tr2.run(sched.events, pin_f.numpy(), pin_l.numpy().view(np.uint64))
-        dt = time.perf_counter() - t0
-        if s >= args.warmup:
-            e2e_times.append(dt)
-    e2e_s = sum(e2e_times)
+    w = args.warmup * chunk
+    tr2.ingest(pin_f.numpy()[:w], pin_l.numpy()[:w].view(np.uint64))
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    tr2.ingest(pin_f.numpy()[w:], pin_l.numpy()[w:].view(np.uint64))
+    e2e_s = time.perf_counter() - t0
     if dist:
         t = torch.tensor([e2e_s], device=REDUCE_DEV, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -402,7 +400,8 @@ def main():
                    "stages": len(BOUNDS) - 1, "parallelism": f"replicas{world}" if world > 1 else "pipeline-on-1",
                    "l2": "flushed between timed steps (256 MB write)"},
         "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "call": "ferret_trainer_run (PipelineTrainer::run) from pinned host buffers"},
+                "call": "ferret_trainer_ingest (PipelineTrainer::run chunk after chunk) from pinned host buffers, "
+                        "host wall clock around the call"},
         "roofline": {"bound": "hbm", "kernel": f"{dom} class ({KERNEL_OF[dom]})", "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak, "peak_kind": peak_kind,
                      "traffic": _traffic(dom), "alg_bytes_per_launch": dc["alg_bytes"] / dc["nodes"],

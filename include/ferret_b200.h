@@ -208,6 +208,16 @@ FERRET_API ferret_status ferret_trainer_set_schedule(ferret_trainer* t, const fe
 FERRET_API ferret_status ferret_trainer_execute(ferret_trainer* t, size_t chunk);
 FERRET_API ferret_status ferret_trainer_fetch_log(ferret_trainer* t, size_t chunk, ferret_step_record* log_out);
 FERRET_API ferret_status ferret_trainer_sync(ferret_trainer* t);
+/* Stream ingest at rate (PipelineTrainer::run over a long stream, chunk by
+ * chunk): n_items host samples, a whole number of set_schedule chunks, replay
+ * the schedule chunk after chunk, continuing from the current state; log_out
+ * gets n_items StepRecords (items numbered within the call). Host->device
+ * copies of chunk c+1 overlap chunk c's graph through two device staging slots
+ * on a copy stream; pass pinned host memory (cudaMallocHost) for true DMA.
+ * Synchronous from the caller's view. */
+FERRET_API ferret_status ferret_trainer_ingest(ferret_trainer* t, const double* features, const uint64_t* labels,
+                                               size_t n_items, size_t n_features, ferret_step_record* log_out);
+
 /* cudaStream_t the trainer launches on, as an opaque pointer (for CUDA-event timing) */
 FERRET_API void* ferret_trainer_stream(ferret_trainer* t);
 

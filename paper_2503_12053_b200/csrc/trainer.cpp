@@ -537,6 +537,9 @@ struct ferret_trainer {
                         static_cast<void*>(d_stash), static_cast<void*>(d_replay),
                         static_cast<void*>(d_partial), static_cast<void*>(d_counters)})
             dfree(p);
+        release_ingest();
+        if (ing.copy) cudaStreamDestroy(ing.copy);
+        if (ing.back) cudaStreamDestroy(ing.back);
         if (stream) cudaStreamDestroy(stream);
         if (nstream) cudaStreamDestroy(nstream);
     }
@@ -917,7 +920,7 @@ struct ferret_trainer {
     // Walks the log exactly like the reference trainer's buffer_ calls
     // (learner.hpp:409 add at every non-dropped arrival, :509/:514 sample at
     // every firing stage-0 update while non-empty).
-    ChunkPlan plan_chunk(Reservoir& res, size_t base) const {
+    ChunkPlan plan_chunk(Reservoir& res, const int* chunk_labels) const {
         ChunkPlan cp;
         cp.pool_dst.assign(sched.chunk_items, -1);
         if (!opt.replay || opt.as_shipped) return cp;
@@ -926,7 +929,7 @@ struct ferret_trainer {
             if (e.kind == FERRET_EV_ARRIVAL && !sched.dropped[static_cast<size_t>(e.item)]) {
                 for (int b = 0; b < B; ++b) {
                     const size_t s = static_cast<size_t>(e.item) * static_cast<size_t>(B) + static_cast<size_t>(b);
-                    cp.pool_dst[s] = res.add(labels[base + s]);
+                    cp.pool_dst[s] = res.add(chunk_labels[s]);
                 }
             } else if (e.kind == FERRET_EV_UPDATE && e.stage == 0 && sched.update_fires[i] && res.size > 0) {
                 for (int b = 0; b < B; ++b) {
@@ -946,12 +949,20 @@ struct ferret_trainer {
         const size_t base = chunk * sched.chunk_items;
         const size_t n_samples = sched.n_units * static_cast<size_t>(B);
         if (base + n_samples > n_loaded) fail(FERRET_E_OUT_OF_RANGE, "execute: chunk lies beyond the loaded stream");
+        execute_from(labels.data() + base, d_raw + base * static_cast<size_t>(F), d_lab + base, d_pred + base);
+    }
+
+    // One chunk of the compiled schedule over device-resident rows: raw features
+    // and labels are copied into the graph's fixed staging, predictions out to
+    // `dst_pred`. `chunk_labels` (host) drive the replay reservoir.
+    void execute_from(const int* chunk_labels, const double* src_raw, const int* src_lab, int* dst_pred) {
+        const size_t n_samples = sched.n_units * static_cast<size_t>(B);
         const bool seen_any = hs.replay.seen > 0;
         if (graph_exec && (graph_timing != timing || graph_profiling != profiling || graph_seen_any != seen_any))
             invalidate_graph();
         if (!graph_exec) build_graph(seen_any);
         // host decisions for this chunk
-        const ChunkPlan cp = plan_chunk(hs.replay, base);
+        const ChunkPlan cp = plan_chunk(hs.replay, chunk_labels);
         if (cp.n_replays != graph_shape.n_replays)
             fail(FERRET_E_LOGIC, "replay pattern of this chunk differs from the compiled graph");
         // control block -> device (double-buffered pinned staging)
@@ -973,13 +984,13 @@ struct ferret_trainer {
         cuda_check(cudaEventRecord(ctl_done[static_cast<size_t>(ctl_flip)], stream), "cudaEventRecord");
         ctl_flip ^= 1;
         // chunk data -> staging
-        cuda_check(cudaMemcpyAsync(d_rawc, d_raw + base * static_cast<size_t>(F), n_samples * static_cast<size_t>(F) * sizeof(double),
+        cuda_check(cudaMemcpyAsync(d_rawc, src_raw, n_samples * static_cast<size_t>(F) * sizeof(double),
                                    cudaMemcpyDeviceToDevice, stream),
                    "D2D chunk");
-        cuda_check(cudaMemcpyAsync(d_labc, d_lab + base, n_samples * sizeof(int), cudaMemcpyDeviceToDevice, stream),
+        cuda_check(cudaMemcpyAsync(d_labc, src_lab, n_samples * sizeof(int), cudaMemcpyDeviceToDevice, stream),
                    "D2D labels");
         cuda_check(cudaGraphLaunch(graph_exec, stream), "cudaGraphLaunch");
-        cuda_check(cudaMemcpyAsync(d_pred + base, d_predc, n_samples * sizeof(int), cudaMemcpyDeviceToDevice, stream),
+        cuda_check(cudaMemcpyAsync(dst_pred, d_predc, n_samples * sizeof(int), cudaMemcpyDeviceToDevice, stream),
                    "D2D predictions");
         hs.norm_count += n_samples;
         for (int j = 0; j < P; ++j) hs.current[static_cast<size_t>(j)] += graph_shape.pushes[static_cast<size_t>(j)];
@@ -2036,6 +2047,113 @@ struct ferret_trainer {
     }
 
     // ------------------------------------------------------------------ output
+    // StepRecords of one chunk from its predictions and labels (items numbered from item0)
+    void fill_log(const int* pred, const int* lab, size_t item0, ferret_step_record* out) const {
+        for (size_t u = 0; u < sched.n_units; ++u)
+            for (int b = 0; b < B; ++b) {
+                const size_t i = u * static_cast<size_t>(B) + static_cast<size_t>(b);
+                ferret_step_record& r = out[i];
+                r = ferret_step_record{static_cast<int64_t>(item0 + i), FERRET_STEP_DROPPED, 0, 0,
+                                       static_cast<uint64_t>(lab[i])};
+                if (!sched.dropped[u]) {
+                    r.predicted = static_cast<uint64_t>(pred[i]);
+                    r.outcome = pred[i] == lab[i] ? FERRET_STEP_CORRECT : FERRET_STEP_WRONG;
+                }
+            }
+    }
+
+    // ---------------------------------------------------------------- ingest
+    // Stream ingest at rate: n host samples (a whole number of chunks) run chunk
+    // after chunk through the compiled schedule. Host->device copies of chunk c+1
+    // (on a copy stream, into one of two device staging slots) overlap the graph
+    // of chunk c; predictions come back on the copy stream into pinned buffers
+    // while later chunks compute. With pinned `features` the copies are true DMA.
+    struct Ingest {
+        size_t cap = 0;
+        double* d_raw[2] = {nullptr, nullptr};
+        int* d_lab[2] = {nullptr, nullptr};
+        int* d_pred[2] = {nullptr, nullptr};
+        int* h_lab[2] = {nullptr, nullptr};   // pinned
+        int* h_pred[2] = {nullptr, nullptr};  // pinned
+        cudaEvent_t in[2] = {}, freed[2] = {}, out[2] = {};
+        cudaStream_t copy = nullptr;  // inbound (H2D)
+        cudaStream_t back = nullptr;  // outbound (D2H): a separate queue, so chunk c+1's copy-in never waits
+                                      // behind chunk c's copy-out (which waits for chunk c's graph)
+    } ing;
+
+    void ensure_ingest(size_t chunk) {
+        if (ing.cap >= chunk) return;
+        cuda_check(cudaDeviceSynchronize(), "sync");
+        release_ingest();
+        for (int s = 0; s < 2; ++s) {
+            ing.d_raw[s] = dalloc<double>(chunk * static_cast<size_t>(F), device_bytes);
+            ing.d_lab[s] = dalloc<int>(chunk, device_bytes);
+            ing.d_pred[s] = dalloc<int>(chunk, device_bytes);
+            cuda_check(cudaMallocHost(&ing.h_lab[s], chunk * sizeof(int)), "cudaMallocHost");
+            cuda_check(cudaMallocHost(&ing.h_pred[s], chunk * sizeof(int)), "cudaMallocHost");
+            for (cudaEvent_t* e : {&ing.in[s], &ing.freed[s], &ing.out[s]})
+                cuda_check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "cudaEventCreate");
+        }
+        if (!ing.copy) cuda_check(cudaStreamCreateWithFlags(&ing.copy, cudaStreamNonBlocking), "stream");
+        if (!ing.back) cuda_check(cudaStreamCreateWithFlags(&ing.back, cudaStreamNonBlocking), "stream");
+        ing.cap = chunk;
+    }
+
+    void release_ingest() {
+        for (int s = 0; s < 2; ++s) {
+            dfree(ing.d_raw[s]);
+            dfree(ing.d_lab[s]);
+            dfree(ing.d_pred[s]);
+            if (ing.h_lab[s]) cudaFreeHost(ing.h_lab[s]);
+            if (ing.h_pred[s]) cudaFreeHost(ing.h_pred[s]);
+            for (cudaEvent_t e : {ing.in[s], ing.freed[s], ing.out[s]})
+                if (e) cudaEventDestroy(e);
+            ing.d_raw[s] = nullptr;
+            ing.d_lab[s] = ing.d_pred[s] = ing.h_lab[s] = ing.h_pred[s] = nullptr;
+            ing.in[s] = ing.freed[s] = ing.out[s] = nullptr;
+        }
+        ing.cap = 0;
+    }
+
+    void ingest(const double* features, const uint64_t* lab, size_t n, size_t f, ferret_step_record* log) {
+        if (!have_schedule) fail(FERRET_E_LOGIC, "ingest: no schedule set");
+        if (static_cast<int>(f) != F) fail(FERRET_E_INVALID_ARG, "stream feature width does not match the net input");
+        const size_t chunk = sched.chunk_items;
+        if (n % chunk) fail(FERRET_E_INVALID_ARG, "ingest: sample count must be a whole number of chunks");
+        std::vector<int> l32(n);
+        for (size_t i = 0; i < n; ++i) {
+            if (lab[i] >= static_cast<uint64_t>(n_out)) fail(FERRET_E_INVALID_ARG, "forward_backward: label out of range");
+            l32[i] = static_cast<int>(lab[i]);
+        }
+        ensure_ingest(chunk);
+        const size_t nch = n / chunk;
+        auto drain = [&](size_t c) {
+            const int s = static_cast<int>(c & 1);
+            cuda_check(cudaEventSynchronize(ing.out[s]), "cudaEventSynchronize");
+            fill_log(ing.h_pred[s], l32.data() + c * chunk, c * chunk, log + c * chunk);
+        };
+        for (size_t c = 0; c < nch; ++c) {
+            const int s = static_cast<int>(c & 1);
+            if (c >= 2) drain(c - 2);  // slot s: its predictions are home, its pinned labels free
+            std::memcpy(ing.h_lab[s], l32.data() + c * chunk, chunk * sizeof(int));
+            if (c >= 2) cuda_check(cudaStreamWaitEvent(ing.copy, ing.freed[s], 0), "cudaStreamWaitEvent");
+            cuda_check(cudaMemcpyAsync(ing.d_raw[s], features + c * chunk * f, chunk * f * sizeof(double),
+                                       cudaMemcpyHostToDevice, ing.copy),
+                       "H2D chunk");
+            cuda_check(cudaMemcpyAsync(ing.d_lab[s], ing.h_lab[s], chunk * sizeof(int), cudaMemcpyHostToDevice, ing.copy),
+                       "H2D labels");
+            cuda_check(cudaEventRecord(ing.in[s], ing.copy), "cudaEventRecord");
+            cuda_check(cudaStreamWaitEvent(stream, ing.in[s], 0), "cudaStreamWaitEvent");
+            execute_from(l32.data() + c * chunk, ing.d_raw[s], ing.d_lab[s], ing.d_pred[s]);
+            cuda_check(cudaEventRecord(ing.freed[s], stream), "cudaEventRecord");
+            cuda_check(cudaStreamWaitEvent(ing.back, ing.freed[s], 0), "cudaStreamWaitEvent");
+            cuda_check(cudaMemcpyAsync(ing.h_pred[s], ing.d_pred[s], chunk * sizeof(int), cudaMemcpyDeviceToHost, ing.back),
+                       "D2H predictions");
+            cuda_check(cudaEventRecord(ing.out[s], ing.back), "cudaEventRecord");
+        }
+        for (size_t c = nch >= 2 ? nch - 2 : 0; c < nch; ++c) drain(c);
+    }
+
     void fetch_log(size_t chunk, ferret_step_record* out) {
         if (!have_schedule) fail(FERRET_E_LOGIC, "fetch_log: no schedule set");
         const size_t base = chunk * sched.chunk_items;
@@ -2300,6 +2418,16 @@ ferret_status ferret_trainer_run(ferret_trainer* t, const ferret_event* events, 
         t->set_schedule(events, n_events, n_items);
         t->execute(0);
         t->fetch_log(0, log_out);
+    });
+}
+
+ferret_status ferret_trainer_ingest(ferret_trainer* t, const double* features, const uint64_t* labels, size_t n_items,
+                                    size_t n_features, ferret_step_record* log_out) {
+    return guarded([&] {
+        t->require_device_mode();
+        if (n_items && (!features || !labels || !log_out)) fail(FERRET_E_INVALID_ARG, "ingest: null buffer");
+        cuda_check(cudaSetDevice(t->opt.device), "cudaSetDevice");
+        t->ingest(features, labels, n_items, n_features, log_out);
     });
 }
 

@@ -129,6 +129,8 @@ def lib() -> C.CDLL:
                                          C.c_size_t, C.c_void_p]),
         "ferret_trainer_load_stream": (C.c_int, [C.c_void_p, P(D), P(C.c_uint64), C.c_size_t, C.c_size_t]),
         "ferret_trainer_set_schedule": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t]),
+        "ferret_trainer_ingest": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t,
+                                            C.c_void_p]),
         "ferret_trainer_execute": (C.c_int, [C.c_void_p, C.c_size_t]),
         "ferret_trainer_fetch_log": (C.c_int, [C.c_void_p, C.c_size_t, C.c_void_p]),
         "ferret_trainer_sync": (C.c_int, [C.c_void_p]),
@@ -389,6 +391,18 @@ class PipelineTrainer:
         self._events = ev
         self.chunk_items = chunk_items
         _check(lib().ferret_trainer_set_schedule(self._h, ev.ctypes.data, len(ev), chunk_items))
+
+    def ingest(self, features: np.ndarray, labels: np.ndarray) -> np.ndarray:
+        """Stream ingest: a whole number of chunks of host samples through the compiled
+        schedule, copies overlapped with compute (pinned arrays: true DMA). -> StepRecord log."""
+        f = features if (features.dtype == np.float64 and features.flags.c_contiguous) else \
+            np.ascontiguousarray(features, dtype=np.float64)
+        lab = labels if (labels.dtype == np.uint64 and labels.flags.c_contiguous) else \
+            np.ascontiguousarray(labels, dtype=np.uint64)
+        log = np.zeros(len(f), dtype=RECORD_DTYPE)
+        _check(lib().ferret_trainer_ingest(self._h, f.ctypes.data, lab.ctypes.data, len(f), f.shape[1],
+                                           log.ctypes.data))
+        return log
 
     def execute(self, chunk: int = 0) -> None:
         _check(lib().ferret_trainer_execute(self._h, chunk))

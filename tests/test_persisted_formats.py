@@ -153,3 +153,38 @@ def test_state_mismatch_is_schema_error(gpu, fb):
         a.load_state(state[:-8])
     a.close()
     b.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("replay", [False, True])
+def test_ingest_equals_chunked_execute(gpu, fb, replay):
+    """Stream ingest (overlapped H2D / compute / D2H over two staging slots) replays
+    exactly what load_stream + execute(c) + fetch_log(c) do, chunk after chunk."""
+    import torch
+
+    units, chunks = 32, 5
+    widths, sched, feats, labels = _c2_workload(fb, units, chunks)
+    params = fb.make_dense_net(widths, 1)
+    opt = fb.PipelineTrainOptions(policy="iter_fisher", replay=replay, replay_seed=3, micro_batch=16)
+    chunk = units * 16
+    a = fb.PipelineTrainer(widths, params, sched.bounds, opt)
+    a.load_stream(feats, labels)
+    a.set_schedule(sched.events, chunk)
+    logs = []
+    for c in range(chunks):
+        a.execute(c)
+        log = a.fetch_log(c)
+        log["item"] += c * chunk
+        logs.append(log)
+    b = fb.PipelineTrainer(widths, params, sched.bounds, opt)
+    b.set_schedule(sched.events, chunk)
+    pin = torch.from_numpy(feats).pin_memory()
+    got = np.concatenate([b.ingest(pin.numpy()[:2 * chunk], labels[:2 * chunk]),   # two calls: state carries over
+                          b.ingest(pin.numpy()[2 * chunk:], labels[2 * chunk:])])
+    got["item"][2 * chunk:] += 2 * chunk
+    assert np.array_equal(got, np.concatenate(logs))
+    assert np.array_equal(b.params(), a.params())
+    with pytest.raises(ValueError):
+        b.ingest(feats[:chunk + 1], labels[:chunk + 1])
+    a.close()
+    b.close()
