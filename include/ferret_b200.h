@@ -352,6 +352,15 @@ FERRET_API ferret_status ferret_seq_predict(ferret_trainer* t, const double* fea
 /* Restore a RunningNormalizer state (count, mean[f], m2[f]) into the learner. */
 FERRET_API ferret_status ferret_seq_set_normalizer(ferret_trainer* t, uint64_t count, const double* mean,
                                                    const double* m2, size_t n_features);
+/* load_csv_stream (stream.hpp:144-186): header row, numeric cells, one label
+ * column, optional gzip (.gz, zlib), host-side like the reference; errors as
+ * SchemaError. Read the rows with ferret_csv_read into n_items x n_features
+ * features (row-major) and n_items labels. */
+typedef struct ferret_csv ferret_csv;
+FERRET_API ferret_status ferret_csv_load(const char* path, const char* label_column, ferret_csv** out);
+FERRET_API ferret_status ferret_csv_shape(const ferret_csv* c, size_t* n_items, size_t* n_features, size_t* n_classes);
+FERRET_API ferret_status ferret_csv_read(const ferret_csv* c, double* features, uint64_t* labels);
+FERRET_API void ferret_csv_destroy(ferret_csv* c);
 /* apply_skip_policy (stream.hpp:225-304) on the host: kind 0 oracle, 1 one_skip,
  * 2 random_n, 3 last_n (SkipPolicy{kind, window, keep, seed}); kept_out and
  * start_out (nullable) hold up to n_items entries, *n_kept is set. */

@@ -706,3 +706,19 @@ ORACLE_API int ferret_oracle_train_sequential(const ONet* net, const double* fea
         *n_kept = fs.kept.size();
     });
 }
+
+// load_csv_stream of the reference (stream.hpp:144-186), gzip included.
+ORACLE_API int ferret_oracle_csv(const char* path, const char* label_column, double* features, uint64_t* labels,
+                                 size_t cap_rows, size_t* n, size_t* f, size_t* n_classes) {
+    return guard([&] {
+        const ferret::DataStream ds = ferret::load_csv_stream(path, label_column);
+        *n = ds.items.size();
+        *f = ds.n_features;
+        *n_classes = ds.n_classes;
+        if (cap_rows < ds.items.size()) return;
+        for (size_t i = 0; i < ds.items.size(); ++i) {
+            std::memcpy(features + i * ds.n_features, ds.items[i].features.data(), ds.n_features * sizeof(double));
+            labels[i] = ds.items[i].label;
+        }
+    });
+}

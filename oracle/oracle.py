@@ -246,3 +246,17 @@ def train_sequential(widths, params, features, labels, t_d=1.0, skip="oracle", w
         C.c_int32(int(replay)), C.c_uint64(replay_seed), C.c_void_p(log.ctypes.data), _dp(out),
         C.c_void_p(kept.ctypes.data), C.byref(nk)))
     return {"log": log, "params": out, "kept": kept[: nk.value].copy()}
+
+
+def load_csv_stream(path: str, label_column: str):
+    """The reference's load_csv_stream (stream.hpp:144-186)."""
+    n, f, k = C.c_size_t(), C.c_size_t(), C.c_size_t()
+    L = lib()
+    L.ferret_oracle_csv.restype = C.c_int
+    _ck(L.ferret_oracle_csv(path.encode(), label_column.encode(), None, None, C.c_size_t(0), C.byref(n), C.byref(f),
+                            C.byref(k)))
+    feats = np.empty((n.value, f.value), dtype=np.float64)
+    labels = np.empty(n.value, dtype=np.uint64)
+    _ck(L.ferret_oracle_csv(path.encode(), label_column.encode(), _dp(feats), _up(labels), C.c_size_t(n.value),
+                            C.byref(n), C.byref(f), C.byref(k)))
+    return feats, labels, int(k.value)

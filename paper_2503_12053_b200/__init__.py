@@ -8,7 +8,7 @@ from .ferret import (  # noqa: F401
     EVENT_DTYPE, RECORD_DTYPE, PROFILE_DTYPE, NO_BUDGET, POLICIES,
     BoundError, ConfigError, DeviceError, LogicError, SchemaError,
     PipelineTrainOptions, PipelineTrainer, Schedule, StreamSpec,
-    PRECISIONS, StaleHarness, apply_skip_policy, train_sequential,
+    PRECISIONS, StaleHarness, apply_skip_policy, load_csv_stream, train_sequential,
     compensate, dense_layer, device_available, lib, make_dense_net, online_accuracy, param_count,
     measure_profile, profile_from_widths, synth_drift_stream, train_pipeline,
 )

@@ -210,6 +210,41 @@ size_t ferret_schedule_trace_text(const ferret_schedule* s, char* buf, size_t ca
 
 void ferret_schedule_destroy(ferret_schedule* s) { delete s; }
 
+struct ferret_csv {
+    ferret::DataStream ds;
+};
+
+ferret_status ferret_csv_load(const char* path, const char* label_column, ferret_csv** out) {
+    return guarded([&] {
+        if (!path || !label_column || !out) fail(FERRET_E_INVALID_ARG, "csv_load: null argument");
+        auto c = std::make_unique<ferret_csv>();
+        c->ds = ferret::load_csv_stream(path, label_column);
+        *out = c.release();
+    });
+}
+
+ferret_status ferret_csv_shape(const ferret_csv* c, size_t* n_items, size_t* n_features, size_t* n_classes) {
+    return guarded([&] {
+        if (!c || !n_items || !n_features || !n_classes) fail(FERRET_E_INVALID_ARG, "csv_shape: null argument");
+        *n_items = c->ds.items.size();
+        *n_features = c->ds.n_features;
+        *n_classes = c->ds.n_classes;
+    });
+}
+
+ferret_status ferret_csv_read(const ferret_csv* c, double* features, uint64_t* labels) {
+    return guarded([&] {
+        if (!c || !features || !labels) fail(FERRET_E_INVALID_ARG, "csv_read: null argument");
+        const size_t f = c->ds.n_features;
+        for (size_t i = 0; i < c->ds.items.size(); ++i) {
+            std::memcpy(features + i * f, c->ds.items[i].features.data(), f * sizeof(double));
+            labels[i] = c->ds.items[i].label;
+        }
+    });
+}
+
+void ferret_csv_destroy(ferret_csv* c) { delete c; }
+
 ferret_status ferret_apply_skip_policy(size_t n_items, double t_d, int32_t kind, uint64_t window, uint64_t keep,
                                       uint64_t seed, double processing_time, int64_t* kept_out, double* start_out,
                                       size_t* n_kept) {

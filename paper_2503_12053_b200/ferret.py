@@ -157,6 +157,10 @@ def lib() -> C.CDLL:
                                        C.c_size_t, C.c_void_p]),
         "ferret_seq_predict": (C.c_int, [C.c_void_p, P(D), C.c_size_t, C.c_size_t, P(C.c_uint64)]),
         "ferret_seq_set_normalizer": (C.c_int, [C.c_void_p, C.c_uint64, P(D), P(D), C.c_size_t]),
+        "ferret_csv_load": (C.c_int, [C.c_char_p, C.c_char_p, P(C.c_void_p)]),
+        "ferret_csv_shape": (C.c_int, [C.c_void_p, P(C.c_size_t), P(C.c_size_t), P(C.c_size_t)]),
+        "ferret_csv_read": (C.c_int, [C.c_void_p, P(D), P(C.c_uint64)]),
+        "ferret_csv_destroy": (None, [C.c_void_p]),
         "ferret_apply_skip_policy": (C.c_int, [C.c_size_t, D, C.c_int32, C.c_uint64, C.c_uint64, C.c_uint64, D,
                                                P(C.c_int64), P(D), P(C.c_size_t)]),
         "ferret_dense_layer": (C.c_int, [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -545,6 +549,22 @@ def train_pipeline(widths, params, bounds, events, features, labels, opt=Pipelin
         return log, t.params()
     finally:
         t.close()
+
+
+def load_csv_stream(path: str, label_column: str):
+    """load_csv_stream (stream.hpp:144-186), gzip when the path ends in .gz
+    -> (features[n, F] fp64, labels[n] u64, n_classes)."""
+    h = C.c_void_p()
+    _check(lib().ferret_csv_load(path.encode(), label_column.encode(), C.byref(h)))
+    try:
+        n, f, k = C.c_size_t(), C.c_size_t(), C.c_size_t()
+        _check(lib().ferret_csv_shape(h, C.byref(n), C.byref(f), C.byref(k)))
+        feats = np.empty((n.value, f.value), dtype=np.float64)
+        labels = np.empty(n.value, dtype=np.uint64)
+        _check(lib().ferret_csv_read(h, _dp(feats), _up(labels)))
+        return feats, labels, int(k.value)
+    finally:
+        lib().ferret_csv_destroy(h)
 
 
 SKIPS = {"oracle": 0, "one_skip": 1, "random_n": 2, "last_n": 3}
