@@ -612,21 +612,22 @@ __global__ void __launch_bounds__(kThreads) update_tile_kernel(const UpdArgs a) 
 // ---------------------------------------------------------------------------
 template <int BT, int NV>
 __global__ void __launch_bounds__(kThreads) update_iter1_kernel(const UpdArgs a) {
+    // Latency-shaped: after the one dependent load of the CTA's work record,
+    // every load of the launch — the unit's deltas (to smem), its input values
+    // of the thread's column, and the version chain + compensator state of the
+    // first RB rows — is issued before any arithmetic, so the kernel costs ~two
+    // L2 round trips rather than one per row and stage of the address chain.
+    constexpr int RB = NV <= 8 ? 4 : 2;  // rows whose chains are held in registers at once
     __shared__ float sdel[kMaxBatch * kUpdMaxTileRows];
-    const UpdTile t = a.tiles[blockIdx.x];
-    const UpdSeg sg = a.segs[t.seg];
-    const int B = a.B, R = t.nrows, tid = threadIdx.x;
+    const UpdWork w = a.works[blockIdx.x];
+    const int B = a.B, R = w.nrows, tid = threadIdx.x;
     const bool learn = a.eta > 0.f && a.v_r != nullptr;
     const UpdPending& pk = a.pend[0];
     const float one_m_a = 1.f - a.alpha;
-    auto fold = [&](size_t e, float g) {
-        float cv[NV];
-#pragma unroll
-        for (int i = 0; i < NV; ++i) cv[i] = __ldg(a.vers[i] + e);
-        float ld = a.lam_d[e];
+    // the fold of one element (compensate.hpp:87-102) from values in registers
+    auto fold = [&](size_t e, float g, const float (&cv)[NV], float ld, float vr, float va) {
         float lam = a.lambda0 + ld;
-        if (NV >= 2 && learn) {  // compensate.hpp:87-98
-            float vr = a.v_r[e], va = a.v_a[e];
+        if (NV >= 2 && learn) {
             const float dv = one_m_a * (g - vr);
             const float resid = dv - lam * va;
             const float grad_l = -2.f * resid * va + 2.f * a.nu * lam;
@@ -638,44 +639,208 @@ __global__ void __launch_bounds__(kThreads) update_iter1_kernel(const UpdArgs a)
             a.v_a[e] = va;
             a.lam_d[e] = ld;
         }
-        float o = g;  // compensate.hpp:99-102
+        float o = g;
 #pragma unroll
         for (int s = 0; s + 1 < NV; ++s) o += lam * o * o * (cv[s + 1] - cv[s]);
         const float nv = cv[NV - 1] - a.step * o;
         a.dst[e] = nv;
         if (a.dst16) reinterpret_cast<__nv_bfloat16*>(a.dst16)[e] = __float2bfloat16_rn(nv);
     };
-    if (sg.bias) {
+    auto load = [&](size_t e, float (&cv)[NV], float& ld, float& vr, float& va) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) cv[i] = __ldg(a.vers[i] + e);
+        ld = a.lam_d[e];
+        vr = learn ? a.v_r[e] : 0.f;
+        va = learn ? a.v_a[e] : 0.f;
+    };
+    if (w.bias) {
         if (tid >= R) return;
-        const int r = t.r0 + tid;
-        const float* dl = pk.stash + sg.dlt_off + r;
+        const int r = w.r0 + tid;
+        const size_t e = (size_t)w.elem0 + r;
+        float cv[NV], ld, vr, va;
+        load(e, cv, ld, vr, va);
+        const float* dl = pk.stash + w.dlt_off + r;
         float g = 0.f;
 #pragma unroll
         for (int b = 0; b < BT; ++b)
-            if (b < B) g += __ldg(dl + (size_t)b * sg.out);
-        fold((size_t)sg.elem0 + r, g);
+            if (b < B) g += __ldg(dl + (size_t)b * w.out);
+        fold(e, g, cv, ld, vr, va);
         return;
     }
+    const int c = w.c0 + tid;
+    const bool live = c < w.in;
+    float cv[RB][NV], ld[RB], vr[RB], va[RB];
+#pragma unroll
+    for (int i = 0; i < RB; ++i)
+        if (live && i < R) load((size_t)w.elem0 + (size_t)(w.r0 + i) * w.in + c, cv[i], ld[i], vr[i], va[i]);
     for (int i = tid; i < B * R; i += kThreads) {
         const int b = i / R, rr = i - b * R;
-        sdel[i] = __ldg(pk.stash + sg.dlt_off + (size_t)b * sg.out + t.r0 + rr);
+        sdel[i] = __ldg(pk.stash + w.dlt_off + (size_t)b * w.out + w.r0 + rr);
     }
-    __syncthreads();
-    const int c = t.c0 + tid;
-    if (c >= sg.in) return;
     float xv[BT];
 #pragma unroll
     for (int b = 0; b < BT; ++b) {
-        const float* xr = sg.xin_off >= 0 ? pk.stash + sg.xin_off + (size_t)b * sg.in
-                          : a.x0idx       ? pk.x0 + (size_t)__ldg(a.x0idx + b) * a.x0_ld
-                                          : pk.x0 + (size_t)b * a.x0_ld;
-        xv[b] = b < B ? __ldg(xr + c) : 0.f;
+        const float* xr = w.xin_off >= 0 ? pk.stash + w.xin_off + (size_t)b * w.in
+                          : a.x0idx      ? pk.x0 + (size_t)__ldg(a.x0idx + b) * a.x0_ld
+                                         : pk.x0 + (size_t)b * a.x0_ld;
+        xv[b] = (b < B && live) ? __ldg(xr + c) : 0.f;
     }
-    for (int i = 0; i < R; ++i) {
+    __syncthreads();
+    if (!live) return;
+    auto grad = [&](int i) {
         float g = 0.f;
 #pragma unroll
         for (int b = 0; b < BT; ++b) g = fmaf(sdel[b * R + i], xv[b], g);
-        fold((size_t)sg.elem0 + (size_t)(t.r0 + i) * sg.in + c, g);
+        return g;
+    };
+#pragma unroll
+    for (int i = 0; i < RB; ++i)
+        if (i < R) fold((size_t)w.elem0 + (size_t)(w.r0 + i) * w.in + c, grad(i), cv[i], ld[i], vr[i], va[i]);
+    for (int i = RB; i < R; ++i) {  // rows beyond the register batch
+        const size_t e = (size_t)w.elem0 + (size_t)(w.r0 + i) * w.in + c;
+        float cr[NV], l0, r0, a0;
+        load(e, cr, l0, r0, a0);
+        fold(e, grad(i), cr, l0, r0, a0);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// iter_fisher with one pending gradient, float4 flavour: a thread owns four
+// consecutive columns of the tile's rows, so every chain version, state array
+// and new-slot store moves 16 bytes per instruction (a quarter of the memory
+// instructions of the scalar kernel, the same bytes); the unit's four input
+// values per sample sit in registers and the row deltas are broadcast from smem.
+// Same arithmetic order per element as update_iter1_kernel.
+// ---------------------------------------------------------------------------
+template <int BT, int NV>
+__global__ void __launch_bounds__(kThreads) update_iter1v4_kernel(const UpdArgs a) {
+    constexpr int RB = NV <= 6 ? 2 : 1;  // rows whose chains are loaded before any arithmetic
+    __shared__ float sdel[kMaxBatch * kUpdMaxTileRows];
+    const UpdWork w = a.works4[blockIdx.x];
+    const int B = a.B, R = w.nrows, tid = threadIdx.x;
+    const bool learn = a.eta > 0.f && a.v_r != nullptr;
+    const UpdPending& pk = a.pend[0];
+    const float one_m_a = 1.f - a.alpha;
+    auto fold1 = [&](float g, const float* cv, float& ld, float& vr, float& va) {  // one element
+        float lam = a.lambda0 + ld;
+        if (NV >= 2 && learn) {
+            const float dv = one_m_a * (g - vr);
+            const float resid = dv - lam * va;
+            const float grad_l = -2.f * resid * va + 2.f * a.nu * lam;
+            ld -= a.eta * grad_l;
+            lam = a.lambda0 + ld;
+            vr = a.alpha * vr + one_m_a * g;
+            va = a.alpha * va + one_m_a * g * g * (cv[NV >= 2 ? 1 : 0] - cv[0]);
+        }
+        float o = g;
+#pragma unroll
+        for (int s = 0; s + 1 < NV; ++s) o += lam * o * o * (cv[s + 1] - cv[s]);
+        return cv[NV - 1] - a.step * o;
+    };
+    if (w.bias) {  // one element per thread
+        if (tid >= R) return;
+        const int r = w.r0 + tid;
+        const size_t e = (size_t)w.elem0 + r;
+        float cv[NV];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) cv[i] = __ldg(a.vers[i] + e);
+        float ld = a.lam_d[e], vr = learn ? a.v_r[e] : 0.f, va = learn ? a.v_a[e] : 0.f;
+        const float* dl = pk.stash + w.dlt_off + r;
+        float g = 0.f;
+#pragma unroll
+        for (int b = 0; b < BT; ++b)
+            if (b < B) g += __ldg(dl + (size_t)b * w.out);
+        const float nv = fold1(g, cv, ld, vr, va);
+        a.dst[e] = nv;
+        if (a.dst16) reinterpret_cast<__nv_bfloat16*>(a.dst16)[e] = __float2bfloat16_rn(nv);
+        if (NV >= 2 && learn) {
+            a.v_r[e] = vr;
+            a.v_a[e] = va;
+            a.lam_d[e] = ld;
+        }
+        return;
+    }
+    const int c = w.c0 + 4 * tid;
+    const bool live = c < w.in;
+    float4 cv[RB][NV], st[RB][3];
+    auto eoff = [&](int i) { return (size_t)w.elem0 + (size_t)(w.r0 + i) * w.in + c; };
+    auto load = [&](size_t e, float4 (&v)[NV], float4 (&s3)[3]) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) v[k] = __ldg(reinterpret_cast<const float4*>(a.vers[k] + e));
+        s3[0] = *reinterpret_cast<const float4*>(a.lam_d + e);
+        s3[1] = learn ? *reinterpret_cast<const float4*>(a.v_r + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+        s3[2] = learn ? *reinterpret_cast<const float4*>(a.v_a + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+    };
+#pragma unroll
+    for (int i = 0; i < RB; ++i)
+        if (live && i < R) load(eoff(i), cv[i], st[i]);
+    for (int i = tid; i < B * R; i += blockDim.x) {
+        const int b = i / R, rr = i - b * R;
+        sdel[i] = __ldg(pk.stash + w.dlt_off + (size_t)b * w.out + w.r0 + rr);
+    }
+    float4 xv[BT];
+#pragma unroll
+    for (int b = 0; b < BT; ++b) {
+        const float* xr = w.xin_off >= 0 ? pk.stash + w.xin_off + (size_t)b * w.in
+                          : a.x0idx      ? pk.x0 + (size_t)__ldg(a.x0idx + b) * a.x0_ld
+                                         : pk.x0 + (size_t)b * a.x0_ld;
+        xv[b] = (b < B && live) ? __ldg(reinterpret_cast<const float4*>(xr + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncthreads();
+    if (!live) return;
+    auto row = [&](int i, const float4 (&v)[NV], const float4 (&s3)[3]) {
+        float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int b = 0; b < BT; ++b) {
+            const float d = sdel[b * R + i];
+            g.x = fmaf(d, xv[b].x, g.x);
+            g.y = fmaf(d, xv[b].y, g.y);
+            g.z = fmaf(d, xv[b].z, g.z);
+            g.w = fmaf(d, xv[b].w, g.w);
+        }
+        float lds[4] = {s3[0].x, s3[0].y, s3[0].z, s3[0].w};
+        float vrs[4] = {s3[1].x, s3[1].y, s3[1].z, s3[1].w};
+        float vas[4] = {s3[2].x, s3[2].y, s3[2].z, s3[2].w};
+        const float gs[4] = {g.x, g.y, g.z, g.w};
+        float out[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            float cj[NV];
+#pragma unroll
+            for (int k = 0; k < NV; ++k) cj[k] = j == 0 ? v[k].x : j == 1 ? v[k].y : j == 2 ? v[k].z : v[k].w;
+            out[j] = fold1(gs[j], cj, lds[j], vrs[j], vas[j]);
+        }
+        const size_t e = eoff(i);
+        *reinterpret_cast<float4*>(a.dst + e) = make_float4(out[0], out[1], out[2], out[3]);
+        if (a.dst16) {
+            __nv_bfloat162* d16 = reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<__nv_bfloat16*>(a.dst16) + e);
+            d16[0] = __floats2bfloat162_rn(out[0], out[1]);
+            d16[1] = __floats2bfloat162_rn(out[2], out[3]);
+        }
+        if (NV >= 2 && learn) {
+            *reinterpret_cast<float4*>(a.lam_d + e) = make_float4(lds[0], lds[1], lds[2], lds[3]);
+            *reinterpret_cast<float4*>(a.v_r + e) = make_float4(vrs[0], vrs[1], vrs[2], vrs[3]);
+            *reinterpret_cast<float4*>(a.v_a + e) = make_float4(vas[0], vas[1], vas[2], vas[3]);
+        }
+    };
+#pragma unroll
+    for (int i = 0; i < RB; ++i)
+        if (i < R) row(i, cv[i], st[i]);
+    for (int i = RB; i < R; ++i) {
+        float4 v[NV], s3[3];
+        load(eoff(i), v, s3);
+        row(i, v, s3);
+    }
+}
+
+template <int BT>
+const void* iter1v4_func(int nv) {
+    switch (nv) {
+#define FB_NV(n) case n: return reinterpret_cast<const void*>(&update_iter1v4_kernel<BT, n>);
+        FB_NV(1) FB_NV(2) FB_NV(3) FB_NV(4) FB_NV(5) FB_NV(6) FB_NV(7) FB_NV(8)
+        FB_NV(9) FB_NV(10) FB_NV(11) FB_NV(12) FB_NV(13) FB_NV(14) FB_NV(15) FB_NV(16)
+#undef FB_NV
+        default: return nullptr;
     }
 }
 
@@ -1058,6 +1223,14 @@ void spec_update(const UpdArgs& a, KernelSpec& k) {
                       : a.B <= 8 ? stream_func<8>(smem) : stream_func<16>(smem);
         fill(k, f, dim3((unsigned)blocks), dim3(kThreads), a);
         k.smem = smem;
+        return;
+    }
+    // FERRET_UPDATE_V4=0 (experiment knob) keeps the scalar kernel
+    static const bool v4_on = !std::getenv("FERRET_UPDATE_V4") || std::atoi(std::getenv("FERRET_UPDATE_V4")) != 0;
+    if (v4_on && a.policy == 4 && a.K == 1 && a.nv <= 16 && a.lam_d != nullptr && a.works4 != nullptr) {
+        const void* f = a.B <= 1 ? iter1v4_func<1>(a.nv) : a.B <= 2 ? iter1v4_func<2>(a.nv) : a.B <= 4 ? iter1v4_func<4>(a.nv)
+                      : a.B <= 8 ? iter1v4_func<8>(a.nv) : iter1v4_func<16>(a.nv);
+        fill(k, f, dim3((unsigned)a.n_tiles4), dim3(a.threads4), a);
         return;
     }
     if (a.policy == 4 && a.K == 1 && a.nv <= 16 && a.lam_d != nullptr) {

@@ -89,6 +89,16 @@ struct UpdTile {
     int c0;     // first column (weights)
 };
 
+// The tile and its segment's fields in one record: the update kernels need one
+// dependent load (not two) before every other address is known.
+struct UpdWork {
+    long long elem0;      // float offset of the segment's element 0 inside a stage slot
+    long long xin_off;    // stash offset of the layer input; -1 = net input
+    long long dlt_off;    // stash offset of the layer's delta
+    int in, out, bias;
+    int r0, nrows, c0;
+};
+
 struct UpdPending {
     const float* stash;   // the unit's stash slot (activations + deltas)
     const float* x0;      // net-input rows of the unit (when the stage holds layer 0)
@@ -105,7 +115,10 @@ struct UpdArgs {
     long long n_items;
     const UpdSeg* segs;      // device array
     const UpdTile* tiles;    // device array, one per CTA
+    const UpdWork* works;    // the same tiles with their segment fields (one per CTA)
     int n_tiles;
+    const UpdWork* works4;   // float4 tiles (4 columns per thread) when every weight row is 16-byte aligned
+    int n_tiles4, threads4;  // their CTA count and CTA size
     UpdPending pend[kMaxPending];
     const int* x0idx;        // nullable: net-input row b is x0 + x0idx[b] * x0_ld (replay), else x0 + b * x0_ld
     int x0_ld;
