@@ -695,7 +695,8 @@ struct ferret_trainer {
             // measured: ~2.5 % faster than the scalar kernel on HBM-bound 33 M-param
             // stages (config 5), ~10 % slower on L2-resident small stages (config 2,
             // lower occupancy) -> only for large stages
-            if (aligned && s.n_params >= (1LL << 22)) {
+            const char* v4min = std::getenv("FERRET_UPDATE_V4_MIN_PARAMS");  // test / experiment knob
+            if (aligned && s.n_params >= (v4min ? std::atoll(v4min) : (1LL << 22))) {
                 s.threads4 = std::min(256, std::max(32, ((widest / 4 + 31) / 32) * 32));
                 const int cols4 = 4 * s.threads4;
                 long long rt4 = 0;

@@ -217,3 +217,13 @@ def test_stream_update_kernel_everywhere(gpu, fb, orc, monkeypatch, replay):
     widths = [784, 256, 256, 256, 10]
     params, feats, labels, sched = _setup(fb, widths, 120, bounds=[0, 1, 2, 3, 4])
     _compare(fb, orc, widths, params, feats, labels, sched, "iter_fisher", replay=replay)
+
+
+@pytest.mark.parametrize("replay", [False, True])
+def test_float4_update_kernel(gpu, fb, orc, monkeypatch, replay):
+    """The float4 iter_fisher kernel (large stages by default) forced onto every stage:
+    same oracle bar as the scalar kernel."""
+    monkeypatch.setenv("FERRET_UPDATE_V4_MIN_PARAMS", "0")
+    widths = [784, 256, 256, 256, 10]
+    params, feats, labels, sched = _setup(fb, widths, 120, bounds=[0, 1, 2, 3, 4], micro_batch=16)
+    _compare(fb, orc, widths, params, feats, labels, sched, "iter_fisher", micro_batch=16, replay=replay)
