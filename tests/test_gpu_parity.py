@@ -68,9 +68,12 @@ def _compare(fb, orc, widths, params, feats, labels, sched, policy, micro_batch=
                 d_gpu = lam - 0.2
                 if np.linalg.norm(d_ref) > 0:
                     assert np.linalg.norm(d_gpu - d_ref) / np.linalg.norm(d_ref) < 2e-2
-                for a, b in ((vr, ref["v_r"][lo:hi]), (va, ref["v_a"][lo:hi])):
+                # v_a accumulates g^2 (theta_1 - theta_0): a difference of two nearly
+                # equal fp32 parameters (~1e-9 apart), so its fp32 error is ~1e-3 of
+                # its norm by construction; v_r is a plain EMA of g (tighter)
+                for a, b, tol in ((vr, ref["v_r"][lo:hi], 1e-3), (va, ref["v_a"][lo:hi], 3e-3)):
                     if np.linalg.norm(b) > 0:
-                        assert np.linalg.norm(a - b) / np.linalg.norm(b) < 1e-3
+                        assert np.linalg.norm(a - b) / np.linalg.norm(b) < tol
             else:
                 # mean_gap is an EMA of |theta_now - theta_read|: a difference of two
                 # nearly equal fp32 parameters (~1e-5 apart at ~5e-2), so its fp32
