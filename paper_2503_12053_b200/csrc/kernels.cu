@@ -1084,6 +1084,41 @@ __global__ void normalize_kernel(const NormArgs a) {
     }
 }
 
+// Two-phase RunningNormalizer (same arithmetic, same bits as normalize_kernel).
+// Only mean and M2 form a recurrence over the samples; the standardisation of
+// sample i (variance, sqrt, divide: most of the fp64 latency) depends on
+// (mean_i, M2_i) alone. Phase 1 walks the recurrence per feature and records
+// (mean_i, M2_i); phase 2 standardises every (sample, feature) in parallel.
+__global__ void welford_kernel(const NormArgs a) {
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= a.F) return;
+    double mu = a.mean[f], m2 = a.m2[f];
+    unsigned long long cnt = *a.count_base + a.count_off;
+#pragma unroll 4
+    for (long long i = 0; i < a.n; ++i) {
+        const double x = a.raw[i * a.F + f];
+        ++cnt;
+        const double d = __dsub_rn(x, mu);
+        mu = __dadd_rn(mu, __ddiv_rn(d, (double)cnt));
+        m2 = __dadd_rn(m2, __dmul_rn(d, __dsub_rn(x, mu)));
+        a.mu_i[i * a.F + f] = mu;
+        a.m2_i[i * a.F + f] = m2;
+    }
+    a.mean[f] = mu;
+    a.m2[f] = m2;
+}
+
+__global__ void standardize_kernel(const NormArgs a) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= a.n * a.F) return;
+    const long long i = t / a.F;
+    const unsigned long long cnt = *a.count_base + a.count_off + (unsigned long long)i + 1;
+    const double x = a.raw[t], mu = a.mu_i[t], m2 = a.m2_i[t];
+    const double var = cnt > 1 ? __ddiv_rn(m2, (double)(cnt - 1)) : 1.0;
+    const double sd = __dsqrt_rn(var < 1e-8 ? 1e-8 : var);
+    a.out[t] = (float)__ddiv_rn(__dsub_rn(x, mu), sd);
+}
+
 // Replay-pool insertion: one CTA per sample of the unit.
 __global__ void pool_kernel(const PoolArgs a) {
     const int b = blockIdx.x;
@@ -1246,6 +1281,15 @@ void spec_update(const UpdArgs& a, KernelSpec& k) {
 
 void spec_normalize(const NormArgs& a, KernelSpec& k) {
     fill(k, reinterpret_cast<const void*>(&normalize_kernel), dim3((a.F + 127) / 128), dim3(128), a);
+}
+
+void spec_welford(const NormArgs& a, KernelSpec& k) {
+    fill(k, reinterpret_cast<const void*>(&welford_kernel), dim3((a.F + 63) / 64), dim3(64), a);
+}
+
+void spec_standardize(const NormArgs& a, KernelSpec& k) {
+    const long long n = a.n * a.F;
+    fill(k, reinterpret_cast<const void*>(&standardize_kernel), dim3((unsigned)((n + 255) / 256)), dim3(256), a);
 }
 
 void spec_pool(const PoolArgs& a, KernelSpec& k) {

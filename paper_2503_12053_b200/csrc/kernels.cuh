@@ -146,6 +146,11 @@ struct NormArgs {
     double* m2;
     float* out;          // n x F
     int apply_only;      // 1: standardise with the current state, observe nothing (held-out evaluation)
+    // two-phase form (spec_welford + spec_standardize): the Welford chain writes
+    // the post-observation mean / M2 of every (sample, feature) here, and the
+    // standardisation of all samples then runs in parallel
+    double* mu_i;        // n x F (nullable: single-kernel form)
+    double* m2_i;        // n x F
 };
 
 // Replay-pool insertion at an arrival (ReplayBuffer::add, learner.hpp:61-69):
@@ -247,6 +252,8 @@ void spec_head(const HeadArgs& a, KernelSpec& k);
 void spec_bwd(const BwdArgs& a, KernelSpec& k);
 void spec_update(const UpdArgs& a, KernelSpec& k);
 void spec_normalize(const NormArgs& a, KernelSpec& k);
+void spec_welford(const NormArgs& a, KernelSpec& k);
+void spec_standardize(const NormArgs& a, KernelSpec& k);
 void spec_pool(const PoolArgs& a, KernelSpec& k);
 void spec_send(const SendArgs& a, KernelSpec& k);
 void spec_recv(const RecvArgs& a, KernelSpec& k);

@@ -191,7 +191,7 @@ struct ChunkPlan {
 // concurrently, which is the pipeline parallelism of the 1F1B schedule
 // realised on one GPU. `serial` chains every node instead (timing mode).
 struct GraphBuilder {
-    enum : uint64_t { kVSlot = 1, kState, kStash, kPred, kNorm, kNormState, kPool, kReplay };
+    enum : uint64_t { kVSlot = 1, kState, kStash, kPred, kNorm, kNormState, kPool, kReplay, kNormScratch };
     static uint64_t key(uint64_t kind, uint64_t a, uint64_t b = 0) { return (kind << 56) | (a << 32) | b; }
 
     cudaGraph_t g = nullptr;
@@ -297,6 +297,13 @@ struct GraphBuilder {
             cur_bytes = 0.0;
             return nullptr;
         }
+        // FERRET_EXPERIMENT_SKIP_CLASS=<class digits> (timing ablation only, results invalid):
+        // node classes 1 predict, 2 forward, 3 backward, 4 update are left out of the graph
+        static const char* skip = std::getenv("FERRET_EXPERIMENT_SKIP_CLASS");
+        if (skip && std::strchr(skip, '0' + cur_category)) {
+            cur_bytes = 0.0;
+            return nullptr;
+        }
         const std::vector<int> ld = logical(reads, writes);
         const std::vector<cudaGraphNode_t> d = deps(ld);
         cudaKernelNodeParams p{};
@@ -374,6 +381,8 @@ struct ferret_trainer {
     // per-chunk staging (fixed addresses baked into the graph)
     size_t chunk_cap = 0;
     double* d_rawc = nullptr;
+    double* d_norm_mu = nullptr;   // per chunk sample x feature: mean / M2 after observing it (two-phase normalizer)
+    double* d_norm_m2i = nullptr;
     float* d_xc = nullptr;
     int* d_labc = nullptr;
     int* d_predc = nullptr;
@@ -537,6 +546,7 @@ struct ferret_trainer {
         }
         for (void* p : {static_cast<void*>(d_raw), static_cast<void*>(d_lab), static_cast<void*>(d_pred),
                         static_cast<void*>(d_norm_mean), static_cast<void*>(d_norm_m2), static_cast<void*>(d_rawc),
+                        static_cast<void*>(d_norm_mu), static_cast<void*>(d_norm_m2i),
                         static_cast<void*>(d_xc), static_cast<void*>(d_labc), static_cast<void*>(d_predc),
                         static_cast<void*>(d_ctl), static_cast<void*>(d_pool_x), static_cast<void*>(d_pool_lab),
                         static_cast<void*>(d_stash), static_cast<void*>(d_replay),
@@ -926,9 +936,11 @@ struct ferret_trainer {
         if (cap > chunk_cap) {
             cuda_check(cudaStreamSynchronize(stream), "sync");
             for (void* p : {static_cast<void*>(d_rawc), static_cast<void*>(d_xc), static_cast<void*>(d_labc),
-                            static_cast<void*>(d_predc)})
+                            static_cast<void*>(d_predc), static_cast<void*>(d_norm_mu), static_cast<void*>(d_norm_m2i)})
                 dfree(p);
             d_rawc = dalloc<double>(cap * static_cast<size_t>(F), device_bytes);
+            d_norm_mu = dalloc<double>(cap * static_cast<size_t>(F), device_bytes);
+            d_norm_m2i = dalloc<double>(cap * static_cast<size_t>(F), device_bytes);
             d_xc = dalloc<float>(cap * static_cast<size_t>(F), device_bytes);
             d_labc = dalloc<int>(cap, device_bytes);
             d_predc = dalloc<int>(cap, device_bytes);
@@ -1183,14 +1195,20 @@ struct ferret_trainer {
                 const size_t u0 = g * kNormGroup, u1 = std::min(n_units, u0 + kNormGroup);
                 const size_t s0 = u0 * static_cast<size_t>(B);
                 const size_t ns = (u1 - u0) * static_cast<size_t>(B);
-                fb200::NormArgs na{d_rawc + s0 * static_cast<size_t>(F), static_cast<long long>(ns), F, ctl_count(),
-                                   static_cast<unsigned long long>(s0), d_norm_mean, d_norm_m2,
-                                   d_xc + s0 * static_cast<size_t>(F), 0};
-                fb200::KernelSpec k;
-                fb200::spec_normalize(na, k);
-                gb->cur_bytes = 20.0 * static_cast<double>(ns) * F;  // raw fp64 in, fp32 out, + state
+                const size_t o = s0 * static_cast<size_t>(F);
+                fb200::NormArgs na{d_rawc + o, static_cast<long long>(ns), F, ctl_count(),
+                                   static_cast<unsigned long long>(s0), d_norm_mean, d_norm_m2, d_xc + o, 0,
+                                   d_norm_mu + o, d_norm_m2i + o};
                 gb->cur_category = kCatNorm; gb->cur_stage = -1;
-                gb->kernel(k, {}, {GB::key(GB::kNorm, g), GB::key(GB::kNormState, 0)});
+                // the recurrence (a chain across groups), then the group's rows in parallel
+                fb200::KernelSpec kw;
+                fb200::spec_welford(na, kw);
+                gb->cur_bytes = 24.0 * static_cast<double>(ns) * F;  // raw fp64 in, mean_i / M2_i out
+                gb->kernel(kw, {}, {GB::key(GB::kNormScratch, g), GB::key(GB::kNormState, 0)});
+                fb200::KernelSpec ks;
+                fb200::spec_standardize(na, ks);
+                gb->cur_bytes = 28.0 * static_cast<double>(ns) * F;  // raw, mean_i, M2_i in, fp32 out
+                gb->kernel(ks, {GB::key(GB::kNormScratch, g)}, {GB::key(GB::kNorm, g)});
             }
         }
 
@@ -1795,7 +1813,8 @@ struct ferret_trainer {
     void seq_item(size_t i, long long read, int rows, int policy) {
         using GB = GraphBuilder;
         fb200::NormArgs na{sq.d_raw + i * static_cast<size_t>(F), 1, F, sq.d_zero,
-                           static_cast<unsigned long long>(sq.norm_count), d_norm_mean, d_norm_m2, sq.d_ux, 0};
+                           static_cast<unsigned long long>(sq.norm_count), d_norm_mean, d_norm_m2, sq.d_ux, 0,
+                           nullptr, nullptr};
         fb200::KernelSpec kn;
         fb200::spec_normalize(na, kn);
         gb->kernel(kn, {}, {});
@@ -1889,7 +1908,8 @@ struct ferret_trainer {
             const size_t i0 = g * G;
             const int rows = static_cast<int>(std::min<size_t>(G, n - i0));
             fb200::NormArgs na{sq.d_raw + i0 * static_cast<size_t>(F), rows, F, sq.d_zero,
-                               static_cast<unsigned long long>(sq.norm_count), d_norm_mean, d_norm_m2, sq.d_px, 1};
+                               static_cast<unsigned long long>(sq.norm_count), d_norm_mean, d_norm_m2, sq.d_px, 1,
+                               nullptr, nullptr};
             fb200::KernelSpec kn;
             fb200::spec_normalize(na, kn);
             gb->kernel(kn, {}, {});
