@@ -667,13 +667,18 @@ struct ferret_trainer {
             s.segs_dev = dalloc<fb200::UpdSeg>(tab.size(), device_bytes);
             cuda_check(cudaMemcpy(s.segs_dev, tab.data(), tab.size() * sizeof(fb200::UpdSeg), cudaMemcpyHostToDevice),
                        "upload segment table");
-            // update tiles: rows x 256 columns per CTA, the row count chosen so a
-            // stage update spans ~400 CTAs (measured: faster than one-row tiles,
-            // whose per-CTA setup then dominates; profiles/README.md)
+            // update tiles: R rows x 256 columns per CTA. In the concurrent chunk graph
+            // fewer, fuller CTAs per kernel leave the SMs to the other nodes
             long long row_tiles = 0;
             for (const fb200::UpdSeg& sg : tab)
                 if (!sg.bias) row_tiles += static_cast<long long>(sg.out) * ((sg.in + fb200::kUpdTileCols - 1) / fb200::kUpdTileCols);
-            const int R = static_cast<int>(std::min<long long>(fb200::kUpdMaxTileRows, std::max<long long>(1, (row_tiles + 399) / 400)));
+            const int r400 = static_cast<int>(std::min<long long>(fb200::kUpdMaxTileRows, std::max<long long>(1, (row_tiles + 399) / 400)));
+            // measured per update kernel (profiles/README.md): the iter_fisher kernel with
+            // 8-row tiles at micro-batch >= 8 (3.25 vs 3.8 ms per config-2 chunk), 2-row
+            // tiles at micro-batch 1; the generic kernel with ~400 CTAs per update
+            int R = opt.policy == FERRET_POLICY_ITER_FISHER ? (B >= 8 ? fb200::kUpdMaxTileRows : 2) : r400;
+            if (const char* rows = std::getenv("FERRET_UPD_ROWS"))  // tile-shape experiment knob (0: ~400 CTAs)
+                R = std::atoi(rows) <= 0 ? r400 : std::max(1, std::min(fb200::kUpdMaxTileRows, std::atoi(rows)));
             std::vector<fb200::UpdTile> tiles;
             for (size_t q = 0; q < tab.size(); ++q) {
                 const fb200::UpdSeg& sg = tab[q];
