@@ -1441,8 +1441,15 @@ struct ferret_trainer {
     }
 
     // fast modes: this layer's forward / input gradient runs on the tensor cores
+    // Layers under 256K weights stay on the SIMT kernels in the fast modes too: on
+    // config 2 (layers of 200K and 65K weights, many kernels in flight) the tensor-core
+    // path is neutral at 200K and slower at 65K (profiles/README.md).
+    // FERRET_MMA_MIN_PARAMS overrides the threshold (tests force 0).
+    long long mma_min_params =
+        std::getenv("FERRET_MMA_MIN_PARAMS") ? std::atoll(std::getenv("FERRET_MMA_MIN_PARAMS")) : (1LL << 18);
     bool use_mma(const LayerDev& ld) const {
-        return opt.precision != FERRET_PREC_FP32 && fb200::mma_supported(opt.precision == FERRET_PREC_BF16, ld.in, ld.out);
+        return opt.precision != FERRET_PREC_FP32 && static_cast<long long>(ld.in) * ld.out >= mma_min_params &&
+               fb200::mma_supported(opt.precision == FERRET_PREC_BF16, ld.in, ld.out);
     }
     void emit_mma(const LayerDev& ld, const float* stage_slot, bool bwd, const float* X, const int* xidx,
                   const float* mask, float* Y, const std::vector<uint64_t>& reads, const std::vector<uint64_t>& writes) {

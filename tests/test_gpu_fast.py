@@ -45,6 +45,12 @@ def _run(fb, orc, widths, bounds, n_units, prec, micro_batch=16, replay=False, p
     return fb.online_accuracy(log), fb.online_accuracy(ref["log"]), rels, params, got, ref
 
 
+@pytest.fixture(autouse=True)
+def _every_layer_on_tensor_cores(monkeypatch):
+    """Small layers stay on SIMT by default; these tests put every layer on tcgen05."""
+    monkeypatch.setenv("FERRET_MMA_MIN_PARAMS", "0")
+
+
 @pytest.mark.parametrize("prec", ["bf16", "tf32"])
 def test_c2_four_stage_fast(gpu, fb, orc, prec):
     widths = [784, 256, 256, 256, 10]

@@ -76,7 +76,8 @@ def test_train_sequential_parity(gpu, fb, orc, skip, replay):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("prec", ["bf16", "tf32"])
-def test_train_sequential_fast(gpu, fb, orc, prec):
+def test_train_sequential_fast(gpu, fb, orc, prec, monkeypatch):
+    monkeypatch.setenv("FERRET_MMA_MIN_PARAMS", "0")
     widths = [784, 256, 256, 10]
     n = 400
     params = fb.make_dense_net(widths, 1)
