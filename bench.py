@@ -157,16 +157,28 @@ def config5_roofline(fb, torch, device):
     return out
 
 
-def stage_shard_measure(fb, torch, dist, rank, world, local, args, units):
-    """The same C2 stream pipelined with its stages sharded over min(N, 4) GPUs (one
-    stage group per rank, NVLink hand-offs via CUDA-IPC inboxes; ranks beyond the
-    stage count idle). Device time per chunk, max over ranks."""
-    P = len(BOUNDS) - 1
+def stage_shard_measure(fb, torch, dist, rank, world, local, args, units, widths=None, bounds=None,
+                        precision="fp32", steps=None, warmup=None):
+    """One stream pipelined with its stages sharded over min(N, P) GPUs (one stage group
+    per rank, NVLink hand-offs: peer stores into CUDA-IPC inboxes + release flags; ranks
+    beyond the stage count idle). Default: the C2 stream; config 5 passes its widths and
+    bounds (8 stages -> one stage per GPU on an 8xB200 box). Device time per chunk, max
+    over ranks."""
+    widths = widths or WIDTHS
+    bounds = bounds or BOUNDS
+    steps = steps or args.steps
+    warmup = warmup if warmup is not None else args.warmup
+    P = len(bounds) - 1
     used = min(world, P)
     owners = fb.ferret.stage_owners(P, used)
-    sched, feats, labels, chunk = make_workload(fb, args.warmup + args.steps, units)
-    tr = fb.PipelineTrainer(WIDTHS, fb.make_dense_net(WIDTHS, 1), BOUNDS,
-                            fb.PipelineTrainOptions(policy=POLICY, micro_batch=MICRO_BATCH, device=local))
+    prof = fb.profile_from_widths(widths)
+    t_d = float(prof["t_f"].max())
+    sched = fb.Schedule.forced(prof, t_d, fb.StreamSpec(t_d=t_d, horizon=units * t_d), bounds, units)
+    chunk = units * MICRO_BATCH
+    feats, labels = fb.synth_drift_stream((warmup + steps) * chunk, widths[0], widths[-1], "split_tasks", 7)
+    tr = fb.PipelineTrainer(widths, fb.make_dense_net(widths, 1), bounds,
+                            fb.PipelineTrainOptions(policy=POLICY, micro_batch=MICRO_BATCH, device=local,
+                                                    precision=precision))
     tr.set_shard(rank, world, owners)
     tr.load_stream(feats, labels)
     tr.set_schedule(sched.events, chunk)
@@ -178,17 +190,17 @@ def stage_shard_measure(fb, torch, dist, rank, world, local, args, units):
 
     tr.connect(gather)
     stream = torch.cuda.ExternalStream(tr.cuda_stream, device=torch.device("cuda", local))
-    for c in range(args.warmup):
+    for c in range(warmup):
         tr.execute(c)
         tr.sync()
         dist.barrier()
     ms = 0.0
-    for s in range(args.steps):
+    for s in range(steps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         dist.barrier()
         with torch.cuda.stream(stream):
             a.record(stream)
-        tr.execute(args.warmup + s)
+        tr.execute(warmup + s)
         with torch.cuda.stream(stream):
             b.record(stream)
         tr.sync()
@@ -197,8 +209,10 @@ def stage_shard_measure(fb, torch, dist, rank, world, local, args, units):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     tr.close()
-    return {"value": chunk * args.steps / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms / args.steps,
-            "ranks_with_stages": used, "stage_owner": owners,
+    return {"value": chunk * steps / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms / steps,
+            "ranks_with_stages": used, "stage_owner": owners, "precision": precision,
+            "workload": f"MLP {widths[0]}-...-{widths[-1]} ({len(widths) - 1} layers), bounds {bounds}, "
+                        f"{units} units x {MICRO_BATCH} samples per chunk",
             "note": "one stream, stages sharded across GPUs (strong scaling); hand-offs are peer stores "
                     "into CUDA-IPC inboxes + release flags; ranks synchronise per chunk"}
 
@@ -351,6 +365,10 @@ def main():
     achieved = dc["gbs"]
     large = config5_roofline(fb, torch, local) if not args.no_large else None
     shard = stage_shard_measure(fb, torch, dist, rank, world, local, args, units) if world > 1 else None
+    shard5 = None
+    if world > 1 and not args.no_large:  # config 5, bf16: 8 stages over the N GPUs
+        shard5 = stage_shard_measure(fb, torch, dist, rank, world, local, args, 32, widths=[4096] * 16 + [10],
+                                     bounds=[0, 2, 4, 6, 8, 10, 12, 14, 16], precision="bf16", steps=2, warmup=2)
 
     # ---- e2e through the public API with host buffers: PipelineTrainer ingest
     # (ferret_trainer_ingest) of the step's samples from pinned host memory, each
@@ -412,6 +430,7 @@ def main():
                              "config5_bf16 has the HBM-bound wide net"},
         "config5_bf16": large,
         "stage_shard": shard,
+        "stage_shard_config5": shard5,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
         "gpu_launches": int(launches_per_step * args.steps),
