@@ -1153,10 +1153,17 @@ __global__ void __launch_bounds__(512) recv_kernel(const RecvArgs a) {
     if (threadIdx.x == 0) {
         const unsigned e = *a.epoch;
         unsigned v;
+        unsigned long long t0, t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
         for (;;) {
             asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a.flag) : "memory");
             if (v == e) break;
             __nanosleep(64);
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > 10000000000ull) {  // a peer rank is not progressing: fail the chunk, never hang
+                if (a.error) atomicExch(a.error, 1u);
+                break;
+            }
         }
         ready = 1;
     }

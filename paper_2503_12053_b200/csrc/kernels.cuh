@@ -184,6 +184,7 @@ struct RecvArgs {
     unsigned* flag;            // own flag
     const unsigned* epoch;
     int n;
+    unsigned* error;           // set to 1 when the flag did not arrive within 10 s (the chunk's results are invalid)
 };
 
 // A fully resolved kernel launch: the trainer either launches it on a stream

@@ -445,6 +445,17 @@ struct ferret_trainer {
     }
 
     // Size and allocate this rank's inbox from the message plan of the log.
+    // last word of the inbox allocation: a receive that timed out sets it
+    unsigned* handoff_error() const {
+        return d_inbox ? reinterpret_cast<unsigned*>(d_inbox + inbox_alloc - sizeof(unsigned)) : nullptr;
+    }
+    void check_handoffs() {
+        if (world == 1 || !d_inbox || plan_only) return;
+        unsigned e = 0;
+        cuda_check(cudaMemcpy(&e, handoff_error(), sizeof(e), cudaMemcpyDeviceToHost), "D2H hand-off status");
+        if (e) fail(FERRET_E_CUDA, "stage hand-off timed out: a peer rank did not deliver within 10 s");
+    }
+
     void setup_inbox() {
         if (world == 1) return;
         HostState probe = hs;
@@ -1183,7 +1194,8 @@ struct ferret_trainer {
             }
             if (rank == dst) {
                 fb200::RecvArgs a{peer_data[static_cast<size_t>(rank)] + off / sizeof(float), dst_ptr(), mask,
-                                  peer_flags[static_cast<size_t>(rank)] + fl, ctl_epoch(), static_cast<int>(n)};
+                                  peer_flags[static_cast<size_t>(rank)] + fl, ctl_epoch(), static_cast<int>(n),
+                                  handoff_error()};
                 fb200::KernelSpec k;
                 fb200::spec_recv(a, k);
                 gb->cur_category = kCatOther;
@@ -2492,7 +2504,10 @@ ferret_status ferret_trainer_fetch_log(ferret_trainer* t, size_t chunk, ferret_s
 }
 
 ferret_status ferret_trainer_sync(ferret_trainer* t) {
-    return guarded([&] { cuda_check(cudaStreamSynchronize(t->stream), "sync"); });
+    return guarded([&] {
+        cuda_check(cudaStreamSynchronize(t->stream), "sync");
+        t->check_handoffs();
+    });
 }
 
 void* ferret_trainer_stream(ferret_trainer* t) { return static_cast<void*>(t->stream); }
