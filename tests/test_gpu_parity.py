@@ -230,3 +230,63 @@ def test_float4_update_kernel(gpu, fb, orc, monkeypatch, replay):
     widths = [784, 256, 256, 256, 10]
     params, feats, labels, sched = _setup(fb, widths, 120, bounds=[0, 1, 2, 3, 4], micro_batch=16)
     _compare(fb, orc, widths, params, feats, labels, sched, "iter_fisher", micro_batch=16, replay=replay)
+
+
+def test_c3_cifar_shaped_four_stage_replay(gpu, fb, orc):
+    """BASELINE config 3's oracle-backed substitute: MLP 3072-1024-512-256-10
+    (3.8 M params), 4 stages, ER replay, micro-batch 16."""
+    widths = [3072, 1024, 512, 256, 10]
+    params, feats, labels, sched = _setup(fb, widths, 24, bounds=[0, 1, 2, 3, 4], micro_batch=16)
+    _compare(fb, orc, widths, params, feats, labels, sched, "iter_fisher", micro_batch=16, replay=True)
+
+
+def _np_welford(raw):
+    """RunningNormalizer (stream.hpp:307-334) in numpy fp64, same operation order
+    (separately rounded ops, no FMA): the final count / mean / M2."""
+    mean = np.zeros(raw.shape[1])
+    m2 = np.zeros(raw.shape[1])
+    for i, x in enumerate(raw, start=1):
+        d = x - mean
+        mean = mean + d / float(i)
+        m2 = m2 + d * (x - mean)
+    return len(raw), mean, m2
+
+
+def test_c5_full_size_properties(gpu, fb):
+    """Config 5 at full size (16 x 4096, 8 stages, bf16, micro-batch 16), where the fp64
+    oracle is too slow (0.018 items/s): size-independent properties — the replay is
+    deterministic (two trainers, identical logs and parameters), the normalizer state is
+    bit-exact with an fp64 Welford pass over the same rows, schedule facts are exact and
+    training moved the parameters."""
+    widths = [4096] * 16 + [10]
+    bounds = [0, 2, 4, 6, 8, 10, 12, 14, 16]
+    units = 24
+    prof = fb.profile_from_widths(widths)
+    t_d = float(prof["t_f"].max())
+    sched = fb.Schedule.forced(prof, t_d, fb.StreamSpec(t_d=t_d, horizon=units * t_d), bounds, units)
+    feats, labels = fb.synth_drift_stream(units * 16, widths[0], widths[-1], "split_tasks", 7)
+    params = fb.make_dense_net(widths, 1)
+    runs = []
+    for _ in range(2):
+        tr = fb.PipelineTrainer(widths, params, bounds,
+                                fb.PipelineTrainOptions(policy="iter_fisher", micro_batch=16, precision="bf16"))
+        log = tr.run(sched.events, feats, labels)
+        runs.append((log, tr.params(), tr.normalizer(widths[0])))
+        tr.close()
+    (log0, p0, n0), (log1, p1, n1) = runs
+    assert np.array_equal(log0, log1) and np.array_equal(p0, p1)
+    cnt, mean, m2 = _np_welford(feats)
+    assert n0[0] == cnt and np.array_equal(n0[1], mean) and np.array_equal(n0[2], m2)
+    assert np.all(np.isfinite(p0))
+    assert np.linalg.norm(p0 - params) / np.linalg.norm(params) > 1e-6
+    dropped = np.repeat([bool(x) for x in _dropped_units(sched, units)], 16)
+    assert np.array_equal(log0["outcome"] == 2, dropped)
+    assert np.array_equal(log0["label"], labels)
+
+
+def _dropped_units(sched, units):
+    out = [False] * units
+    for e in sched.events:
+        if e["kind"] == 1:  # drop
+            out[int(e["item"])] = True
+    return out
