@@ -381,9 +381,11 @@ FERRET_API ferret_status ferret_compensate(int32_t policy, const double* g, cons
 
 /* ---------------- unit entry: one dense layer on the tensor cores ---------------- */
 
-/* One dense layer of the fast modes (tcgen05.mma, TMA-fed, TMEM accumulator),
- * host fp32 buffers in and out; precision FERRET_PREC_TF32 or FERRET_PREC_BF16
- * (W and X rounded to bf16 on the device path, fp32 accumulation).
+/* One dense layer on the tensor cores (tcgen05.mma, TMA-fed, TMEM accumulator),
+ * host fp32 buffers in and out. precision FERRET_PREC_BF16 (W and X rounded to
+ * bf16), FERRET_PREC_TF32 (tf32 operands) or FERRET_PREC_FP32 (3xTF32 split:
+ * x = hi + lo per operand, hi*hi + hi*lo + lo*hi — about fp32 accuracy, the
+ * parity mode's path for large layers); fp32 accumulation in every case.
  *   direction 0 — affine_forward + apply_activation (net.hpp:99-113):
  *       Y[b][r] = act(sum_c W[r][c] X[b][c] + bias[r]); X: B x in, Y: B x out; act = ReLU if relu
  *   direction 1 — the input gradient of learner.hpp:468-474:

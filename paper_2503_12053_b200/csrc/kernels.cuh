@@ -229,6 +229,7 @@ struct MmaLayer {
     const void* W;         // fp32 (tf32 mode) or bf16 weights, out x in row-major
     bool bwd = false;      // false: Y = act(W X + b); true: Y = mask * (W^T X)
     bool bf16 = false;
+    bool split = false;    // fp32 weights: 3xTF32 (about fp32 accuracy) instead of plain tf32
     const float* bias = nullptr;
     const float* X = nullptr;
     const int* xidx = nullptr;
@@ -245,7 +246,7 @@ struct MmaGeom {
     size_t partial_floats;
 };
 bool mma_supported(bool bf16, int in, int out);
-MmaGeom mma_geom(bool bf16, bool bwd, int in, int out);
+MmaGeom mma_geom(bool bf16, bool bwd, int in, int out, bool split = false);
 void spec_mma(const MmaLayer& L, KernelSpec& k);
 
 void spec_fwd(const FwdArgs& a, KernelSpec& k);

@@ -130,7 +130,14 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 }
 
 // ES = operand bytes (4: tf32 from fp32, 2: bf16); BWD = A is MN-major (W^T).
-template <int ES, bool BWD>
+// SPLIT (ES = 4 only): fp32-accurate product on the tf32 tensor cores ("3xTF32"):
+// each fp32 operand x = hi + lo with hi = x with the low 13 mantissa bits cleared
+// (exact in tf32) and lo = x - hi (exact in fp32, ~2^-11 relative loss in tf32);
+// D = hi_A hi_B + hi_A lo_B + lo_A hi_B — about fp32 accuracy, used by the fp32
+// parity mode for large layers.
+__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+template <int ES, bool BWD, bool SPLIT = false>
 __global__ void __launch_bounds__(kMmaThreads, 1) mma_layer_kernel(const __grid_constant__ MmaArgs a) {
     constexpr int KA = 128 / ES;       // K elements per 128-byte atom
     constexpr int UK = 32 / ES;        // K per tcgen05.mma (32 bytes of operand)
@@ -139,12 +146,15 @@ __global__ void __launch_bounds__(kMmaThreads, 1) mma_layer_kernel(const __grid_
     unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int nst = a.stages;
     unsigned char* sA = base;
-    unsigned char* sB = sA + nst * kTileBytes;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + a.atoms_per_cta * kBAtomBytes);
+    unsigned char* sAlo = sA + nst * kTileBytes;                 // SPLIT: lo parts of the A ring
+    unsigned char* sB = sAlo + (SPLIT ? nst * kTileBytes : 0);
+    unsigned char* sBlo = sB + a.atoms_per_cta * kBAtomBytes;    // SPLIT: lo parts of B
+    uint64_t* full = reinterpret_cast<uint64_t*>(sBlo + (SPLIT ? a.atoms_per_cta * kBAtomBytes : 0));
     uint64_t* empty = full + nst;
     uint64_t* done = empty + nst;
-    uint64_t* bready = done + 1;  // per B atom: staged by the 64 threads of warps 2-3
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bready + a.atoms_per_cta);
+    uint64_t* bready = done + 1;  // per B atom: staged by the stager warps
+    uint64_t* lready = bready + a.atoms_per_cta;  // SPLIT, per ring stage: A split into hi / lo
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lready + (SPLIT ? nst : 0));
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int S = a.splits, q = blockIdx.x;
@@ -172,6 +182,8 @@ __global__ void __launch_bounds__(kMmaThreads, 1) mma_layer_kernel(const __grid_
         }
         mbar_init(done, 1);
         for (int i = 0; i < na; ++i) mbar_init(bready + i, kStagers);
+        if (SPLIT)
+            for (int s = 0; s < nst; ++s) mbar_init(lready + s, kStagers);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -209,7 +221,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1) mma_layer_kernel(const __grid_
         for (int i = 0; i < na; ++i) {
             const int s = i % nst;
             mbar_wait(bready + i, 0);
-            mbar_wait(full + s, (i / nst) & 1);
+            mbar_wait(SPLIT ? lready + s : full + s, (i / nst) & 1);
             if (i == 0) tick(3);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t abase = smem_u32(sA + s * kTileBytes);
@@ -225,6 +237,15 @@ __global__ void __launch_bounds__(kMmaThreads, 1) mma_layer_kernel(const __grid_
                                         : smem_desc(abase + k * 32, 16, 1024);
                 const uint64_t bd = smem_desc(bbase + k * 32, 16, 1024);
                 umma(tmem, ad, bd, idesc, (i > 0 || k > 0) ? 1u : 0u, TF32);
+                if constexpr (SPLIT) {  // + hi_A lo_B + lo_A hi_B
+                    const uint32_t lofs = static_cast<uint32_t>(sAlo - sA);
+                    const uint32_t blofs = static_cast<uint32_t>(sBlo - sB);
+                    const uint64_t bdl = smem_desc(bbase + blofs + k * 32, 16, 1024);
+                    const uint64_t adl = BWD ? smem_desc(abase + lofs + k * UK * 128, KA * 128, 512, 1)
+                                             : smem_desc(abase + lofs + k * 32, 16, 1024);
+                    umma(tmem, ad, bdl, idesc, 1u, TF32);
+                    umma(tmem, adl, bd, idesc, 1u, TF32);
+                }
             }
             umma_commit(empty + s);
         }
@@ -267,7 +288,15 @@ __global__ void __launch_bounds__(kMmaThreads, 1) mma_layer_kernel(const __grid_
                     if (at >= na) continue;
                     unsigned char* dst = sB + at * kBAtomBytes + (n >> 3) * 1024 + (n & 7) * 128 + ((j ^ (n & 7)) << 4);
                     if constexpr (ES == 4) {
-                        *reinterpret_cast<float4*>(dst) = make_float4(v[u][0], v[u][1], v[u][2], v[u][3]);
+                        if constexpr (SPLIT) {
+                            const float4 hi = make_float4(tf32_hi(v[u][0]), tf32_hi(v[u][1]), tf32_hi(v[u][2]),
+                                                          tf32_hi(v[u][3]));
+                            *reinterpret_cast<float4*>(dst) = hi;
+                            *reinterpret_cast<float4*>(dst + (sBlo - sB)) =
+                                make_float4(v[u][0] - hi.x, v[u][1] - hi.y, v[u][2] - hi.z, v[u][3] - hi.w);
+                        } else {
+                            *reinterpret_cast<float4*>(dst) = make_float4(v[u][0], v[u][1], v[u][2], v[u][3]);
+                        }
                     } else {
                         uint4 p;
                         __nv_bfloat162 h0 = __floats2bfloat162_rn(v[u][0], v[u][1]), h1 = __floats2bfloat162_rn(v[u][2], v[u][3]);
@@ -286,6 +315,25 @@ __global__ void __launch_bounds__(kMmaThreads, 1) mma_layer_kernel(const __grid_
                 asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bready + at)) : "memory");
         }
         if (threadIdx.x == 64) tick(2);
+        if constexpr (SPLIT) {
+            // split every landed A tile in place: hi (low 13 mantissa bits cleared)
+            // stays in the ring slot, lo goes to the parallel slot (elementwise, so
+            // the swizzled layout is preserved); published per stage on lready
+            for (int i = 0; i < na; ++i) {
+                const int s = i % nst;
+                mbar_wait(full + s, (i / nst) & 1);
+                float4* A4 = reinterpret_cast<float4*>(sA + s * kTileBytes);
+                float4* L4 = reinterpret_cast<float4*>(sAlo + s * kTileBytes);
+                for (int e = t; e < kTileBytes / 16; e += kStagers) {
+                    const float4 x = A4[e];
+                    const float4 hi = make_float4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
+                    A4[e] = hi;
+                    L4[e] = make_float4(x.x - hi.x, x.y - hi.y, x.z - hi.z, x.w - hi.w);
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(lready + s)) : "memory");
+            }
+        }
     }
     __syncwarp();
 
@@ -378,10 +426,10 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-template <int ES, bool BWD>
+template <int ES, bool BWD, bool SPLIT = false>
 const void* mma_func(size_t smem) {
     static size_t configured = 0;  // > 48 KB dynamic smem needs an opt-in per function
-    const void* f = reinterpret_cast<const void*>(&mma_layer_kernel<ES, BWD>);
+    const void* f = reinterpret_cast<const void*>(&mma_layer_kernel<ES, BWD, SPLIT>);
     if (smem > configured) {
         cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         configured = smem;
@@ -397,8 +445,9 @@ bool mma_supported(bool bf16, int in, int out) {
     return (static_cast<long long>(in) * es) % 16 == 0 && in >= 1 && out >= 1 && encode_fn() != nullptr;
 }
 
-MmaGeom mma_geom(bool bf16, bool bwd, int in, int out) {
+MmaGeom mma_geom(bool bf16, bool bwd, int in, int out, bool split) {
     const int es = bf16 ? 2 : 4;
+    const int mult = split ? 2 : 1;  // 3xTF32: hi + lo copies of the A ring and of B
     MmaGeom g{};
     const int M = bwd ? in : out, K = bwd ? out : in;
     g.mtiles = (M + 127) / 128;
@@ -413,18 +462,19 @@ MmaGeom mma_geom(bool bf16, bool bwd, int in, int out) {
     if (const char* env = std::getenv("FERRET_MMA_SPLIT")) S = std::atoi(env);  // experiment knob
     g.apc = (g.katoms + S - 1) / S;
     g.S = (g.katoms + g.apc - 1) / g.apc;  // every split owns >= 1 atom
-    const size_t fixed = 1024 + static_cast<size_t>(g.apc) * (kBAtomBytes + 8) + 256;
-    g.stages = static_cast<int>((kMaxSmem - fixed) / kTileBytes);
+    const size_t fixed = 1024 + static_cast<size_t>(g.apc) * (mult * kBAtomBytes + 8) + 256 + 64;
+    g.stages = static_cast<int>((kMaxSmem - fixed) / (mult * kTileBytes));
     if (g.stages > g.apc) g.stages = g.apc;
     if (g.stages > 16) g.stages = 16;
-    g.smem = fixed + static_cast<size_t>(g.stages) * kTileBytes;
+    g.smem = fixed + static_cast<size_t>(g.stages) * mult * kTileBytes;
     g.partial_floats = g.S > 1 ? static_cast<size_t>(g.mtiles) * g.S * 128 * 16 : 0;
     return g;
 }
 
 void spec_mma(const MmaLayer& L, KernelSpec& k) {
     const int es = L.bf16 ? 2 : 4;
-    const MmaGeom g = mma_geom(L.bf16, L.bwd, L.in, L.out);
+    const bool split = L.split && !L.bf16;
+    const MmaGeom g = mma_geom(L.bf16, L.bwd, L.in, L.out, split);
     MmaArgs a{};
     // tensor map of W (out x in, row-major): dims {in, out}; boxes of 128 bytes x rows
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(L.in), static_cast<cuuint64_t>(L.out)};
@@ -465,6 +515,7 @@ void spec_mma(const MmaLayer& L, KernelSpec& k) {
     }
     a.vec = (a.ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(L.X) & 15u) == 0);
     const void* f = es == 2 ? (L.bwd ? mma_func<2, true>(g.smem) : mma_func<2, false>(g.smem))
+                  : split   ? (L.bwd ? mma_func<4, true, true>(g.smem) : mma_func<4, false, true>(g.smem))
                             : (L.bwd ? mma_func<4, true>(g.smem) : mma_func<4, false>(g.smem));
     static_assert(sizeof(MmaArgs) <= sizeof(k.arg0), "kernel argument too large");
     k.func = f;

@@ -1441,7 +1441,8 @@ struct ferret_trainer {
             const bool bf16 = opt.precision == FERRET_PREC_BF16;
             for (const LayerDev& ld : layers)
                 for (bool bwd : {false, true}) {
-                    const fb200::MmaGeom g = fb200::mma_geom(bf16, bwd, ld.in, ld.out);
+                    const fb200::MmaGeom g =
+                        fb200::mma_geom(bf16, bwd, ld.in, ld.out, opt.precision == FERRET_PREC_FP32);
                     mma_partial_floats = std::max(mma_partial_floats, g.partial_floats);
                     mma_counter_n = std::max(mma_counter_n, static_cast<size_t>(g.mtiles));
                 }
@@ -1459,8 +1460,17 @@ struct ferret_trainer {
     // FERRET_MMA_MIN_PARAMS overrides the threshold (tests force 0).
     long long mma_min_params =
         std::getenv("FERRET_MMA_MIN_PARAMS") ? std::atoll(std::getenv("FERRET_MMA_MIN_PARAMS")) : (1LL << 18);
+    // fp32 parity mode: layers of >= 1M weights run the fp32-accurate 3xTF32 split on the
+    // tensor cores (FERRET_SPLIT_MIN_PARAMS overrides; 0 = every layer, -1 = none)
+    long long split_min_params =
+        std::getenv("FERRET_SPLIT_MIN_PARAMS") ? std::atoll(std::getenv("FERRET_SPLIT_MIN_PARAMS")) : (1LL << 20);
+    bool use_split(const LayerDev& ld) const {
+        return opt.precision == FERRET_PREC_FP32 && split_min_params >= 0 &&
+               static_cast<long long>(ld.in) * ld.out >= split_min_params && fb200::mma_supported(false, ld.in, ld.out);
+    }
     bool use_mma(const LayerDev& ld) const {
-        return opt.precision != FERRET_PREC_FP32 && static_cast<long long>(ld.in) * ld.out >= mma_min_params &&
+        if (opt.precision == FERRET_PREC_FP32) return use_split(ld);
+        return static_cast<long long>(ld.in) * ld.out >= mma_min_params &&
                fb200::mma_supported(opt.precision == FERRET_PREC_BF16, ld.in, ld.out);
     }
     void emit_mma(const LayerDev& ld, const float* stage_slot, bool bwd, const float* X, const int* xidx,
@@ -1471,6 +1481,7 @@ struct ferret_trainer {
         m.W = bf16 ? static_cast<const void*>(s.shadow(stage_slot + ld.woff)) : static_cast<const void*>(stage_slot + ld.woff);
         m.bwd = bwd;
         m.bf16 = bf16;
+        m.split = opt.precision == FERRET_PREC_FP32;
         m.bias = bwd ? nullptr : stage_slot + ld.boff;
         m.X = X;
         m.xidx = xidx;
@@ -2730,8 +2741,8 @@ ferret_status ferret_dense_layer(int32_t precision, int32_t direction, const flo
                                  const float* X, const float* mask, int32_t B, int32_t in, int32_t out, int32_t relu,
                                  float* Y) {
     return guarded([&] {
-        if (precision != FERRET_PREC_TF32 && precision != FERRET_PREC_BF16)
-            fail(FERRET_E_CONFIG, "dense_layer: precision must be FERRET_PREC_TF32 or FERRET_PREC_BF16");
+        if (precision != FERRET_PREC_TF32 && precision != FERRET_PREC_BF16 && precision != FERRET_PREC_FP32)
+            fail(FERRET_E_CONFIG, "dense_layer: unknown precision");
         if (direction != 0 && direction != 1) fail(FERRET_E_INVALID_ARG, "dense_layer: direction must be 0 or 1");
         if (B < 1 || B > fb200::kMaxBatch) fail(FERRET_E_INVALID_ARG, "dense_layer: batch must lie in [1, 16]");
         if (in < 1 || out < 1) fail(FERRET_E_INVALID_ARG, "dense_layer: empty layer");
@@ -2777,7 +2788,8 @@ ferret_status ferret_dense_layer(int32_t precision, int32_t direction, const flo
         L.out = out;
         L.B = B;
         L.relu = relu;
-        const fb200::MmaGeom g = fb200::mma_geom(bf16, L.bwd, in, out);
+        L.split = precision == FERRET_PREC_FP32;
+        const fb200::MmaGeom g = fb200::mma_geom(bf16, L.bwd, in, out, L.split);
         if (g.partial_floats) {
             L.partial = reinterpret_cast<float*>(up(nullptr, g.partial_floats * 4));
             L.counters = reinterpret_cast<unsigned*>(up(nullptr, static_cast<size_t>(g.mtiles) * 4));

@@ -36,7 +36,8 @@ def _stage_slices(widths, bounds):
     return [(offs[bounds[j]], offs[bounds[j + 1]]) for j in range(len(bounds) - 1)]
 
 
-def _compare(fb, orc, widths, params, feats, labels, sched, policy, micro_batch=1, replay=False, check_state=True):
+def _compare(fb, orc, widths, params, feats, labels, sched, policy, micro_batch=1, replay=False, check_state=True,
+             state_tol=1.0):
     opt = fb.PipelineTrainOptions(policy=policy, replay=replay, replay_seed=3, micro_batch=micro_batch)
     tr = fb.PipelineTrainer(widths, params, sched.bounds, opt)
     log = tr.run(sched.events, feats, labels)
@@ -73,7 +74,7 @@ def _compare(fb, orc, widths, params, feats, labels, sched, policy, micro_batch=
                 # its norm by construction; v_r is a plain EMA of g (tighter)
                 for a, b, tol in ((vr, ref["v_r"][lo:hi], 1e-3), (va, ref["v_a"][lo:hi], 3e-3)):
                     if np.linalg.norm(b) > 0:
-                        assert np.linalg.norm(a - b) / np.linalg.norm(b) < tol
+                        assert np.linalg.norm(a - b) / np.linalg.norm(b) < tol * state_tol
             else:
                 # mean_gap is an EMA of |theta_now - theta_read|: a difference of two
                 # nearly equal fp32 parameters (~1e-5 apart at ~5e-2), so its fp32
@@ -290,3 +291,16 @@ def _dropped_units(sched, units):
         if e["kind"] == 1:  # drop
             out[int(e["item"])] = True
     return out
+
+
+@pytest.mark.parametrize("replay", [False, True])
+def test_fp32_split_tensor_core_layers(gpu, fb, orc, monkeypatch, replay):
+    """fp32 parity mode with every layer on the tensor cores (3xTF32 split, on by default
+    for layers >= 1M weights): the same 1e-4 parameter bar against the fp64 oracle."""
+    monkeypatch.setenv("FERRET_SPLIT_MIN_PARAMS", "0")
+    widths = [784, 256, 256, 256, 10]
+    params, feats, labels, sched = _setup(fb, widths, 120, bounds=[0, 1, 2, 3, 4], micro_batch=16)
+    # the layer products carry ~2x the error of the SIMT fp32 path (tests/test_gpu_mma.py):
+    # parameters keep the 1e-4 bar; the gradient EMAs get twice the SIMT tolerance
+    _compare(fb, orc, widths, params, feats, labels, sched, "iter_fisher", micro_batch=16, replay=replay,
+             state_tol=2.0)
