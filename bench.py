@@ -119,7 +119,7 @@ def _traffic(cls):
         return json.load(f).get(cls)
 
 
-def config5_roofline(fb, torch, device):
+def config5_roofline(fb, torch, device, precision="bf16"):
     """BASELINE config 5 on one GPU: MLP 16x4096+10, 8 stages [0,2,...,16], iter_fisher,
     micro-batch 16, bf16 fast mode (tcgen05 layers + fp32 compensation/SGD over HBM version
     rings), 32 units per chunk (steady-state staleness). samples/s from CUDA events on the
@@ -127,7 +127,7 @@ def config5_roofline(fb, torch, device):
     (profiles/c5_fast.py)."""
     from profiles.c5_fast import measure
 
-    r = measure(fb, torch, "bf16", units=32, steps=2, device=device)
+    r = measure(fb, torch, precision, units=32, steps=2, device=device)
     peak, kind = _peaks()
     tflops = None
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -135,9 +135,11 @@ def config5_roofline(fb, torch, device):
         with open(path) as f:
             tflops = json.load(f).get("bf16_tflops")
     tot = sum(v["alg_bytes"] for v in r["classes"].values())
-    out = {"workload": "C5: MLP 16x4096+10, 8 stages [0,2,...,16] on one GPU, iter_fisher, micro-batch 16, bf16 fast mode",
+    mode = {"bf16": "bf16 fast mode", "tf32": "tf32 fast mode", "fp32": "fp32 parity mode (3xTF32 tensor-core layers)"}
+    out = {"workload": f"C5: MLP 16x4096+10, 8 stages [0,2,...,16] on one GPU, iter_fisher, micro-batch 16, {mode[precision]}",
            "value": r["samples_per_s"], "unit": "samples/s", "ms_per_chunk": r["ms_per_chunk"],
-           "samples_per_chunk": r["samples_per_chunk"], "dtype": "bf16 layers, f32 update",
+           "samples_per_chunk": r["samples_per_chunk"],
+           "dtype": "f32 (3xTF32 layers), f32 update" if precision == "fp32" else f"{precision} layers, f32 update",
            "step_achieved_gbs": tot / (r["ms_per_chunk"] * 1e-3) / 1e9, "peak": peak, "peak_kind": kind,
            "classes": r["classes"], "critical_ms": r["critical_ms"], "serial_ms": r["serial_ms"],
            "ring_depth": r["ring_depth"], "mean_tau": r["mean_tau"], "device_gb": r["device_gb"]}
@@ -149,7 +151,7 @@ def config5_roofline(fb, torch, device):
         if c and c["nodes"]:
             c["frac_of_hbm_peak"] = c["gbs"] / peak
     fwd = r["classes"].get("forward")
-    if fwd and tflops:
+    if fwd and tflops and precision == "bf16":
         # 4096x4096 layers dominate: 2*16*4096*4096 flops per node
         fl = 2.0 * 16 * 4096 * 4096 / (fwd["us_per_node"] * 1e-6) / 1e12
         out["tensor"] = {"achieved_tflops": fl, "peak_tflops": tflops, "frac": fl / tflops,
@@ -364,6 +366,7 @@ def main():
     dc = classes[dom]
     achieved = dc["gbs"]
     large = config5_roofline(fb, torch, local) if not args.no_large else None
+    large32 = config5_roofline(fb, torch, local, "fp32") if not args.no_large else None
     shard = stage_shard_measure(fb, torch, dist, rank, world, local, args, units) if world > 1 else None
     shard5 = None
     if world > 1 and not args.no_large:  # config 5, bf16: 8 stages over the N GPUs
@@ -429,6 +432,7 @@ def main():
                      "note": "C2 weights (1.3 MB) live in L2: the small-net path is latency-bound; "
                              "config5_bf16 has the HBM-bound wide net"},
         "config5_bf16": large,
+        "config5_fp32": large32,
         "stage_shard": shard,
         "stage_shard_config5": shard5,
         "cpu_baseline": cpu,
