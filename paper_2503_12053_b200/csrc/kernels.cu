@@ -56,6 +56,42 @@ __device__ __forceinline__ float warp_transpose_sum(float (&v)[NV], int lane) {
     return v[0];
 }
 
+// softmax head of sample b over logits z (net.hpp:115-125,150-154, learner.hpp:443-447),
+// one warp: first-index argmax (mode 0) or scale * (softmax - onehot) (mode 1)
+__device__ __forceinline__ void head_sample(const float* z, int n_out, int mode, int label, int* pred_b, float* d,
+                                            float scale, int lane) {
+    // max with first-index tie break
+    float best = -FLT_MAX;
+    int best_k = 0x7fffffff;
+    for (int k = lane; k < n_out; k += 32) {
+        const float v = z[k];
+        if (v > best || (v == best && k < best_k)) {
+            best = v;
+            best_k = k;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int ok = __shfl_xor_sync(0xffffffffu, best_k, o);
+        if (ov > best || (ov == best && ok < best_k)) {
+            best = ov;
+            best_k = ok;
+        }
+    }
+    if (mode == 0) {
+        if (lane == 0) *pred_b = best_k;
+        return;
+    }
+    float sum = 0.f;
+    for (int k = lane; k < n_out; k += 32) sum += expf(z[k] - best);
+    sum = warp_sum(sum);
+    for (int k = lane; k < n_out; k += 32) {
+        const float p = expf(z[k] - best) / sum;
+        d[k] = scale * (k == label ? p - 1.f : p);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // forward: CTA = `groups` row groups x `nwk` K-slices (groups * nwk = 8 warps).
 // A warp accumulates RW rows x B samples over its K slice (float4 when the
@@ -147,6 +183,12 @@ __global__ void __launch_bounds__(kThreads) fwd_kernel(const FwdArgs a, int nwk)
         if (a.relu) z = z > 0.f ? z : 0.f;
         a.Y[(size_t)b * a.out + r] = z;
     }
+    if (a.head_mode >= 0) {  // one CTA wrote every logit: the head in the same launch
+        __syncthreads();
+        for (int b = warp; b < B; b += kWarps)
+            head_sample(a.Y + (size_t)b * a.out, a.out, a.head_mode, a.head_mode == 0 ? 0 : a.labels[b],
+                        a.pred ? a.pred + b : nullptr, a.delta ? a.delta + (size_t)b * a.out : nullptr, a.scale, lane);
+    }
 }
 
 template <class Args>
@@ -158,6 +200,13 @@ void fill(KernelSpec& k, const void* func, dim3 grid, dim3 block, const Args& a)
     k.smem = 0;
     std::memcpy(k.arg0, &a, sizeof(Args));
     k.nargs = 1;
+}
+
+int fwd_rows_per_cta(int in, bool vec, int RW) {
+    const int nk = vec ? (in >> 2) : in;
+    int nwk = (nk + 63) / 64;
+    nwk = nwk >= 8 ? 8 : nwk >= 4 ? 4 : nwk >= 2 ? 2 : 1;
+    return (kWarps / nwk) * RW;
 }
 
 template <int BT, int RW>
@@ -181,39 +230,9 @@ __global__ void __launch_bounds__(kThreads) head_kernel(const HeadArgs a) {
     const int lane = threadIdx.x & 31;
     const int b = blockIdx.x * kWarps + (threadIdx.x >> 5);
     if (b >= a.B) return;
-    const float* z = a.logits + (size_t)b * a.n_out;
-    // max with first-index tie break
-    float best = -FLT_MAX;
-    int best_k = 0x7fffffff;
-    for (int k = lane; k < a.n_out; k += 32) {
-        const float v = z[k];
-        if (v > best || (v == best && k < best_k)) {
-            best = v;
-            best_k = k;
-        }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const float ov = __shfl_xor_sync(0xffffffffu, best, o);
-        const int ok = __shfl_xor_sync(0xffffffffu, best_k, o);
-        if (ov > best || (ov == best && ok < best_k)) {
-            best = ov;
-            best_k = ok;
-        }
-    }
-    if (a.mode == 0) {
-        if (lane == 0) a.pred[b] = best_k;
-        return;
-    }
-    float sum = 0.f;
-    for (int k = lane; k < a.n_out; k += 32) sum += expf(z[k] - best);
-    sum = warp_sum(sum);
-    const int label = a.labels[a.lidx ? a.lidx[b] : b];
-    float* d = a.delta + (size_t)b * a.n_out;
-    for (int k = lane; k < a.n_out; k += 32) {
-        const float p = expf(z[k] - best) / sum;
-        d[k] = a.scale * (k == label ? p - 1.f : p);
-    }
+    const int label = a.mode == 0 ? 0 : a.labels[a.lidx ? a.lidx[b] : b];
+    head_sample(a.logits + (size_t)b * a.n_out, a.n_out, a.mode, label, a.pred ? a.pred + b : nullptr,
+                a.delta ? a.delta + (size_t)b * a.n_out : nullptr, a.scale, lane);
 }
 
 // ---------------------------------------------------------------------------
@@ -1194,6 +1213,11 @@ void spec_fwd(const FwdArgs& a, KernelSpec& k) {
     else if (a.B <= 4) fwd_spec<4, 4>(a, vec, k);
     else if (a.B <= 8) fwd_spec<8, 4>(a, vec, k);
     else fwd_spec<16, 2>(a, vec, k);
+}
+
+bool fwd_single_cta(int in, int out, int B, bool vec) {
+    const int RW = B <= 8 ? 4 : 2;  // spec_fwd's choice
+    return out <= fwd_rows_per_cta(in, vec, RW);
 }
 
 void spec_head(const HeadArgs& a, KernelSpec& k) {

@@ -25,6 +25,7 @@ constexpr int kMaxVersions = 64;   // chain length of the unit compensation entr
 
 // z[b][r] = act(bias[r] + sum_c W[r][c] * x_b[c])    (reference net.hpp:99-113)
 // Split-K CTA tiles: each CTA owns a few output rows, its 8 warps split K.
+struct HeadArgs;
 struct FwdArgs {
     const float* W;      // out x in, row-major
     const float* bias;   // out
@@ -33,6 +34,13 @@ struct FwdArgs {
     float* Y;            // B x out, row-major
     int in, out, B;
     int relu;
+    // fused softmax head on the logits this launch produced (last layer, when one CTA
+    // computes every output row — fwd_single_cta): -1 none, else HeadArgs::mode
+    int head_mode;
+    const int* labels;   // head: label of sample b = labels[b]
+    int* pred;           // head mode 0
+    float* delta;        // head mode 1 (B x out)
+    float scale;         // head mode 1
 };
 
 // Softmax head over the last layer (reference net.hpp:115-125, learner.hpp:443-447):
@@ -250,6 +258,8 @@ MmaGeom mma_geom(bool bf16, bool bwd, int in, int out, bool split = false);
 void spec_mma(const MmaLayer& L, KernelSpec& k);
 
 void spec_fwd(const FwdArgs& a, KernelSpec& k);
+// true when spec_fwd computes every output row in one CTA (the head can be fused)
+bool fwd_single_cta(int in, int out, int B, bool vec);
 void spec_head(const HeadArgs& a, KernelSpec& k);
 void spec_bwd(const BwdArgs& a, KernelSpec& k);
 void spec_update(const UpdArgs& a, KernelSpec& k);

@@ -134,6 +134,15 @@ struct HostState {
     uint64_t norm_count = 0;
 };
 
+// softmax head fused into the last layer's forward (one CTA computes every logit)
+struct Head {
+    int mode = -1;  // -1 none, 0 argmax -> pred, 1 scale * (softmax - onehot) -> delta
+    const int* labels = nullptr;
+    int* pred = nullptr;
+    float* delta = nullptr;
+    float scale = 1.f;
+};
+
 struct LayerDev {
     int in = 0, out = 0, act = 0, stage = 0;
     long long woff = 0, boff = 0;        // inside the stage slot
@@ -1265,7 +1274,7 @@ struct ferret_trainer {
                     if (sched.has_bwd[u * static_cast<size_t>(P) + static_cast<size_t>(j)]) live[static_cast<size_t>(j)][v] += 1;
                     if (!DRY && mine(j))
                         launch_stage_forward(j, stages[static_cast<size_t>(j)].slot(v), stash(u), xrows(u),
-                                             {vslot(j, v), ngroup(u)}, ustash(u));
+                                             {vslot(j, v), ngroup(u)}, ustash(u), d_labc + u * static_cast<size_t>(B));
                     if (j + 1 < P) {  // hand the stage output to the next stage's rank
                         const LayerDev& top = layers[static_cast<size_t>(stages[static_cast<size_t>(j)].hi - 1)];
                         const long long off = top.act_off;
@@ -1500,10 +1509,21 @@ struct ferret_trainer {
         gb->kernel(k, reads, writes);
     }
 
+    bool can_fuse_head() const {
+        const LayerDev& last = layers.back();
+        return !use_mma(last) && fb200::fwd_single_cta(last.in, last.out, B, last.in % 4 == 0);
+    }
+
     void emit_layer(const LayerDev& ld, const float* stage_slot, const float* X, const int* xidx, float* Y,
-                    const std::vector<uint64_t>& reads, const std::vector<uint64_t>& writes) {
+                    const std::vector<uint64_t>& reads, const std::vector<uint64_t>& writes,
+                    const Head& head = Head{}) {
         if (use_mma(ld)) return emit_mma(ld, stage_slot, false, X, xidx, nullptr, Y, reads, writes);
         fb200::FwdArgs a{};
+        a.head_mode = head.mode;
+        a.labels = head.labels;
+        a.pred = head.pred;
+        a.delta = head.delta;
+        a.scale = head.scale;
         a.W = stage_slot + ld.woff;
         a.bias = stage_slot + ld.boff;
         a.X = X;
@@ -1546,11 +1566,16 @@ struct ferret_trainer {
             const std::vector<uint64_t> reads{vslot(j, rel[static_cast<size_t>(j)]), ngroup(u)};
             for (int l = s.lo; l < s.hi; ++l) {
                 const float* X = l == 0 ? x0 : scratch + ((l - 1) & 1) * pred_stride;
+                Head h;
+                if (l == L - 1 && can_fuse_head()) {
+                    h.mode = 0;
+                    h.pred = d_predc + u * static_cast<size_t>(B);
+                }
                 emit_layer(layers[static_cast<size_t>(l)], s.slot(rel[static_cast<size_t>(j)]), X, nullptr,
-                           scratch + (l & 1) * pred_stride, reads, {sk});
+                           scratch + (l & 1) * pred_stride, reads, {sk}, h);
             }
         }
-        if (DRY || !mine(P - 1)) return;
+        if (DRY || !mine(P - 1) || can_fuse_head()) return;
         fb200::HeadArgs h{};
         h.logits = scratch + ((L - 1) & 1) * pred_stride;
         h.n_out = n_out;
@@ -1564,14 +1589,23 @@ struct ferret_trainer {
     }
 
     void launch_stage_forward(int j, const float* slot, float* stash_u, const float* x0, const std::vector<uint64_t>& reads,
-                              uint64_t stash_key) {
+                              uint64_t stash_key, const int* lab) {
         gb->cur_category = kCatForward;
         gb->cur_stage = j;
         const StageDev& s = stages[static_cast<size_t>(j)];
         for (int l = s.lo; l < s.hi; ++l) {
             const LayerDev& ld = layers[static_cast<size_t>(l)];
             const float* X = l == 0 ? x0 : stash_u + layers[static_cast<size_t>(l - 1)].act_off;
-            emit_layer(ld, slot, X, nullptr, stash_u + ld.act_off, reads, {stash_key});
+            // the logits' delta (learner.hpp:443-447) is a function of the stashed logits and
+            // the labels alone: computed here, consumed by the stage's backward
+            Head h;
+            if (l == L - 1 && can_fuse_head()) {
+                h.mode = 1;
+                h.labels = lab;
+                h.delta = stash_u + ld.dlt_off;
+                h.scale = 1.0f / static_cast<float>(B);
+            }
+            emit_layer(ld, slot, X, nullptr, stash_u + ld.act_off, reads, {stash_key}, h);
         }
     }
 
@@ -1583,7 +1617,7 @@ struct ferret_trainer {
         gb->cur_category = kCatBackward;
         gb->cur_stage = j;
         const StageDev& s = stages[static_cast<size_t>(j)];
-        if (j == P - 1) emit_delta_head(stash_u, lab, nullptr, 1.0f / static_cast<float>(B), {}, stash_key);
+        if (j == P - 1 && !can_fuse_head()) emit_delta_head(stash_u, lab, nullptr, 1.0f / static_cast<float>(B), {}, stash_key);
         for (int l = s.hi - 1; l >= s.lo; --l) {
             if (l == 0) break;  // no input gradient for the first layer
             emit_layer_backward(l, slot, stash_u, scratch, reads, stash_key, !(cross && l == s.lo));
