@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--policy", default="iter_fisher")
     ap.add_argument("--replay", type=int, default=1)
     ap.add_argument("--device", type=int, default=-1, help="-1: LOCAL_RANK")
+    ap.add_argument("--precision", default="fp32")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -45,7 +46,7 @@ def main():
     params = fb.make_dense_net(widths, 1)
     tr = fb.PipelineTrainer(widths, params, bounds,
                             fb.PipelineTrainOptions(policy=args.policy, micro_batch=B, replay=bool(args.replay),
-                                                    replay_seed=3, device=dev))
+                                                    replay_seed=3, device=dev, precision=args.precision))
     owners = fb.ferret.stage_owners(P, world)
     tr.set_shard(rank, world, owners)
     tr.load_stream(feats, labels)

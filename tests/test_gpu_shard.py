@@ -18,14 +18,15 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _single(fb, widths, bounds, units, chunks, B, policy, replay):
+def _single(fb, widths, bounds, units, chunks, B, policy, replay, precision="fp32"):
     prof = fb.profile_from_widths(widths)
     t_d = float(prof["t_f"].max())
     sched = fb.Schedule.forced(prof, t_d, fb.StreamSpec(t_d=t_d, horizon=units * t_d), bounds, units)
     chunk = units * B
     feats, labels = fb.synth_drift_stream(chunks * chunk, widths[0], widths[-1], "split_tasks", 7)
     tr = fb.PipelineTrainer(widths, fb.make_dense_net(widths, 1), bounds,
-                            fb.PipelineTrainOptions(policy=policy, micro_batch=B, replay=replay, replay_seed=3))
+                            fb.PipelineTrainOptions(policy=policy, micro_batch=B, replay=replay, replay_seed=3,
+                                                    precision=precision))
     tr.load_stream(feats, labels)
     tr.set_schedule(sched.events, chunk)
     logs = []
@@ -44,18 +45,22 @@ def _offsets(widths):
     return o
 
 
-@pytest.mark.parametrize("bounds,replay", [("0,1,2,3,4", 1), ("0,2,4", 0)])
-def test_two_rank_stage_shard_matches_single_process(gpu, fb, tmp_path, bounds, replay):
+@pytest.mark.parametrize("bounds,replay,precision", [("0,1,2,3,4", 1, "fp32"), ("0,2,4", 0, "fp32"),
+                                                     ("0,1,2,3,4", 1, "bf16")])
+def test_two_rank_stage_shard_matches_single_process(gpu, fb, tmp_path, monkeypatch, bounds, replay, precision):
     import torch
 
+    monkeypatch.setenv("FERRET_MMA_MIN_PARAMS", "0")  # bf16: every layer on the tensor cores
     widths, units, chunks, B, policy = [96, 128, 64, 48, 10], 40, 2, 4, "iter_fisher"
+    if precision == "bf16":
+        widths = [512, 256, 256, 128, 16]  # 16-byte rows in bf16 for every layer
     b = [int(x) for x in bounds.split(",")]
-    ref = _single(fb, widths, b, units, chunks, B, policy, bool(replay))
+    ref = _single(fb, widths, b, units, chunks, B, policy, bool(replay), precision)
     dev = [] if torch.cuda.device_count() >= 2 else ["--device", "0"]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr=127.0.0.1",
            "--master-port=29533", os.path.join(ROOT, "tests", "shard_worker.py"), "--out", str(tmp_path),
            "--widths", ",".join(map(str, widths)), "--bounds", bounds, "--units", str(units), "--chunks", str(chunks),
-           "--micro-batch", str(B), "--policy", policy, "--replay", str(replay)] + dev
+           "--micro-batch", str(B), "--policy", policy, "--replay", str(replay), "--precision", precision] + dev
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env={**os.environ, "PYTHONPATH": ROOT})
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     ranks = [pickle.load(open(tmp_path / f"rank{k}.pkl", "rb")) for k in range(2)]
