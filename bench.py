@@ -236,14 +236,38 @@ def cpu_reference(units: int, steps: int, warmup: int):
     sched, feats, labels, chunk = make_workload(fb, 1, units)
     params = fb.make_dense_net(WIDTHS, 1)
     times = []
+    ref = None
     for s in range(warmup + steps):
         t0 = time.perf_counter()
-        orc.train(WIDTHS, params, BOUNDS, sched.events, feats, labels, policy=POLICY, micro_batch=MICRO_BATCH)
+        ref = orc.train(WIDTHS, params, BOUNDS, sched.events, feats, labels, policy=POLICY, micro_batch=MICRO_BATCH)
         dt = time.perf_counter() - t0
         if s >= warmup:
             times.append(dt)
     tot = sum(times)
+    cpu_run.update(ref=ref, sched=sched, feats=feats, labels=labels, params=params)
     return chunk * len(times) / tot, tot, chunk
+
+
+cpu_run = {}  # the last CPU reference run (its inputs and outputs), for the accuracy comparison
+
+
+def accuracy_vs_cpu(fb, device):
+    """Online accuracy of the B200 trainer vs the CPU reference on the identical bounded
+    sample (same schedule, same stream, same initial net): the '+ online accuracy vs CPU'
+    half of the metric, with the parameter agreement beside it."""
+    if not cpu_run:
+        return None
+    tr = fb.PipelineTrainer(WIDTHS, cpu_run["params"], BOUNDS,
+                            fb.PipelineTrainOptions(policy=POLICY, micro_batch=MICRO_BATCH, device=device))
+    log = tr.run(cpu_run["sched"].events, cpu_run["feats"], cpu_run["labels"])
+    got = tr.params()
+    tr.close()
+    ref = cpu_run["ref"]
+    g, c = fb.online_accuracy(log), fb.online_accuracy(ref["log"])
+    return {"b200": g, "cpu_reference": c, "diff_pp": g - c,
+            "param_rel_err": float(np.linalg.norm(got - ref["params"]) / np.linalg.norm(ref["params"])),
+            "prediction_flips": int(np.count_nonzero(log["predicted"] != ref["log"]["predicted"])),
+            "sample": f"{len(log)} samples of the bench stream ({CPU_UNITS} units x {MICRO_BATCH}), fp32 parity mode"}
 
 
 def run_reference_arm(args):
@@ -411,6 +435,7 @@ def main():
                              f"single-threaded (host nproc={os.cpu_count()})"}
         except Exception as e:  # the oracle .so is built where /root/reference exists
             cpu = {"value": None, "unit": "samples/s", "cores": 1, "kind": "reference", "sample": f"unavailable: {e}"}
+    acc = accuracy_vs_cpu(fb, local) if cpu and cpu.get("value") else None
     line = {
         "metric": "stream samples/sec", "value": value, "unit": "samples/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
@@ -440,6 +465,7 @@ def main():
         "gpu_launches": int(launches_per_step * args.steps),
         "host_issue_ms_per_step": 1e3 * host_s / args.steps,
         "online_accuracy_last_chunk": oacc_last,
+        "online_accuracy_vs_cpu": acc,
         "trainer": {"ring_depth": stats["ring_depth"], "stash_slots": stats["stash_slots"],
                     "mean_tau": stats["mean_tau"], "device_bytes": stats["device_bytes"]},
     }
