@@ -1927,14 +1927,21 @@ struct ferret_trainer {
         sq.ring_size = std::min(sq.ring_size + 1, sq.ring_cap);
     }
 
-    // Runs `emit(i)` for every item inside one captured graph on the trainer's stream.
+    // Runs `emit(i)` for every item in captured graphs on the trainer's stream, at most
+    // kSeqBlock items per graph (each item is ~8-12 nodes; long streams stay bounded).
+    static constexpr size_t kSeqBlock = 1024;
     template <class Emit>
     void seq_run(size_t n, Emit&& emit) {
+        for (size_t i0 = 0; i0 < n; i0 += kSeqBlock)
+            seq_run_block(i0, std::min(n, i0 + kSeqBlock), emit);
+    }
+    template <class Emit>
+    void seq_run_block(size_t i0, size_t i1, Emit& emit) {
         gb = sq.gb.get();
         cudaGraph_t g = nullptr;
         cuda_check(cudaStreamBeginCapture(stream, cudaStreamCaptureModeRelaxed), "cudaStreamBeginCapture");
         try {
-            for (size_t i = 0; i < n; ++i) emit(i);
+            for (size_t i = i0; i < i1; ++i) emit(i);
         } catch (...) {
             cudaStreamEndCapture(stream, &g);
             if (g) cudaGraphDestroy(g);
