@@ -227,9 +227,23 @@ struct GraphBuilder {
     std::vector<cudaEvent_t>* prof_events = nullptr;
 
     explicit GraphBuilder(bool serial_) : serial(serial_) { cuda_check(cudaGraphCreate(&g, 0), "cudaGraphCreate"); }
+    // Long logs: the graph is cut into segments launched in stream order, so every
+    // dependency across a cut is honoured by the stream; only the concurrency across
+    // the cut is lost. done_segments holds the finished graphs, g the open one.
+    std::vector<cudaGraph_t> done_segments;
+    size_t seg_first_node = 0;
+    size_t nodes_in_segment() const { return nodes.size() - seg_first_node; }
+    void new_segment() {
+        done_segments.push_back(g);
+        cuda_check(cudaGraphCreate(&g, 0), "cudaGraphCreate");
+        res.clear();
+        last = nullptr;
+        seg_first_node = nodes.size();
+    }
     explicit GraphBuilder(cudaStream_t s) : eager(s) {}
     ~GraphBuilder() {
         if (g) cudaGraphDestroy(g);
+        for (cudaGraph_t x : done_segments) cudaGraphDestroy(x);
     }
 
     std::vector<int> logical(const std::vector<uint64_t>& reads, const std::vector<uint64_t>& writes) {
@@ -510,6 +524,11 @@ struct ferret_trainer {
 
     // the compiled graph of the current schedule
     cudaGraphExec_t graph_exec = nullptr;
+    std::vector<cudaGraphExec_t> more_execs;  // further segments of a long log, launched after graph_exec
+    // nodes per graph segment (FERRET_GRAPH_SEGMENT_NODES overrides; tests use small values)
+    size_t seg_nodes = std::getenv("FERRET_GRAPH_SEGMENT_NODES")
+                           ? static_cast<size_t>(std::atoll(std::getenv("FERRET_GRAPH_SEGMENT_NODES")))
+                           : static_cast<size_t>(65536);
     bool graph_timing = false;
     bool graph_seen_any = false;  // reservoir non-empty at chunk start when captured
     PassResult graph_shape;
@@ -539,6 +558,7 @@ struct ferret_trainer {
         if (stream) cudaStreamSynchronize(stream);
         if (nstream) cudaStreamSynchronize(nstream);
         if (graph_exec) cudaGraphExecDestroy(graph_exec);
+        for (cudaGraphExec_t x : more_execs) cudaGraphExecDestroy(x);
         for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
         for (cudaEvent_t e : prof_events) cudaEventDestroy(e);
         for (void* p : peer_opened)
@@ -584,6 +604,8 @@ struct ferret_trainer {
             cudaStreamSynchronize(stream);
             cudaGraphExecDestroy(graph_exec);
             graph_exec = nullptr;
+            for (cudaGraphExec_t x : more_execs) cudaGraphExecDestroy(x);
+            more_execs.clear();
         }
     }
 
@@ -1077,6 +1099,7 @@ struct ferret_trainer {
         cuda_check(cudaMemcpyAsync(d_labc, src_lab, n_samples * sizeof(int), cudaMemcpyDeviceToDevice, stream),
                    "D2D labels");
         cuda_check(cudaGraphLaunch(graph_exec, stream), "cudaGraphLaunch");
+        for (cudaGraphExec_t x : more_execs) cuda_check(cudaGraphLaunch(x, stream), "cudaGraphLaunch");
         cuda_check(cudaMemcpyAsync(dst_pred, d_predc, n_samples * sizeof(int), cudaMemcpyDeviceToDevice, stream),
                    "D2D predictions");
         hs.norm_count += n_samples;
@@ -1112,7 +1135,18 @@ struct ferret_trainer {
             throw;
         }
         gb = nullptr;
-        cuda_check(cudaGraphInstantiate(&graph_exec, builder.g, 0), "cudaGraphInstantiate");
+        if (builder.done_segments.empty()) {
+            cuda_check(cudaGraphInstantiate(&graph_exec, builder.g, 0), "cudaGraphInstantiate");
+        } else {
+            builder.done_segments.push_back(builder.g);
+            builder.g = nullptr;
+            for (size_t i = 0; i < builder.done_segments.size(); ++i) {
+                cudaGraphExec_t x = nullptr;
+                cuda_check(cudaGraphInstantiate(&x, builder.done_segments[i], 0), "cudaGraphInstantiate");
+                if (i == 0) graph_exec = x;
+                else more_execs.push_back(x);
+            }
+        }
         launches = builder.kernels;
         prof_ldeps = std::move(builder.ldeps);
         prof_cat = std::move(builder.category);
@@ -1239,6 +1273,7 @@ struct ferret_trainer {
         }
 
         for (size_t idx = 0; idx < sched.events.size(); ++idx) {
+            if (!DRY && !gb->prof_events && gb->nodes_in_segment() >= seg_nodes) gb->new_segment();
             const ferret_event& e = sched.events[idx];
             const size_t u = static_cast<size_t>(e.item);
             const int j = e.stage;

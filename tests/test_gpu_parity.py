@@ -304,3 +304,23 @@ def test_fp32_split_tensor_core_layers(gpu, fb, orc, monkeypatch, replay):
     # parameters keep the 1e-4 bar; the gradient EMAs get twice the SIMT tolerance
     _compare(fb, orc, widths, params, feats, labels, sched, "iter_fisher", micro_batch=16, replay=replay,
              state_tol=2.0)
+
+
+@pytest.mark.parametrize("replay", [False, True])
+def test_long_log_graph_segments_bitwise(gpu, fb, monkeypatch, replay):
+    """Long logs are compiled into several graph segments launched in stream order; cutting
+    the graph every 40 nodes must not change a single bit of the result."""
+    widths = [784, 256, 256, 256, 10]
+    params, feats, labels, sched = _setup(fb, widths, 80, bounds=[0, 1, 2, 3, 4], micro_batch=4)
+    out = []
+    for seg in (None, "40"):
+        if seg:
+            monkeypatch.setenv("FERRET_GRAPH_SEGMENT_NODES", seg)
+        tr = fb.PipelineTrainer(widths, params, sched.bounds,
+                                fb.PipelineTrainOptions(policy="iter_fisher", micro_batch=4, replay=replay, replay_seed=3))
+        log = tr.run(sched.events, feats, labels)
+        out.append((log, tr.params(), tr.normalizer(widths[0])))
+        tr.close()
+    (l0, p0, n0), (l1, p1, n1) = out
+    assert np.array_equal(l0, l1) and np.array_equal(p0, p1)
+    assert n0[0] == n1[0] and np.array_equal(n0[1], n1[1]) and np.array_equal(n0[2], n1[2])
