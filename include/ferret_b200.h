@@ -64,6 +64,21 @@ enum { FERRET_STEP_CORRECT = 0, FERRET_STEP_WRONG = 1, FERRET_STEP_DROPPED = 2 }
  * fp32 on the fp32 master versions. Parity bar: online accuracy within 0.5 pp. */
 enum { FERRET_PREC_FP32 = 0, FERRET_PREC_BF16 = 1, FERRET_PREC_TF32 = 2 };
 
+/* Convolutional extension (BASELINE config 3, "ResNet-18-style CNN"; the
+ * reference has no convolution): an optional geometry per layer,
+ * FERRET_GEOM_INTS int32 each = {kind, c_in, h_in, w_in, c_out, k, stride, pad, res}.
+ *   DENSE      z = W x + b (the reference's layer; c_in = in, h_in = w_in = 1)
+ *   CONV       z[co][oh][ow] = b[co] + sum W[co][ci][kh][kw] x[ci][oh*s-p+kh][ow*s-p+kw]
+ *              (zero padding, NCHW per sample); res = 1 adds the shortcut of the
+ *              input of layer l-1 (a two-conv basic block): identity, or when the
+ *              block downsamples, stride subsample + zero channels ("option A")
+ *   GAP_DENSE  z = W mean_hw(x) + b (global average pool fused into the head)
+ * then the layer's activation. Activation widths (in[l], out[l]) are c*h*w;
+ * parameters per layer: W (c_out x c_in*k*k, or c_out x c_in) then b (c_out).
+ * Partition bounds may not split a residual block (FERRET_E_CONFIG). */
+enum { FERRET_LAYER_DENSE = 0, FERRET_LAYER_CONV = 1, FERRET_LAYER_GAP_DENSE = 2 };
+#define FERRET_GEOM_INTS 9
+
 /* DenseNet, net.hpp:20-51. params in flatten() order (learner.hpp:26-34):
  * per layer W (row-major out x in) then b. */
 typedef struct {
@@ -72,6 +87,7 @@ typedef struct {
     const uint64_t* out;
     const int32_t* act;
     const double* params;
+    const int32_t* geom;  /* nullable (all dense, the reference's DenseNet): n_layers x FERRET_GEOM_INTS */
 } ferret_net_desc;
 
 /* PipelineTrainOptions, learner.hpp:319-325, plus the Compensator constants

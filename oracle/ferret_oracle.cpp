@@ -722,3 +722,5 @@ ORACLE_API int ferret_oracle_csv(const char* path, const char* label_column, dou
         }
     });
 }
+
+#include "conv_oracle.hpp"

@@ -260,3 +260,52 @@ def load_csv_stream(path: str, label_column: str):
     _ck(L.ferret_oracle_csv(path.encode(), label_column.encode(), _dp(feats), _up(labels), C.c_size_t(n.value),
                             C.byref(n), C.byref(f), C.byref(k)))
     return feats, labels, int(k.value)
+
+
+def _i32(a):
+    return a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+def train_conv(geom, acts, params, bounds, events, features, labels, policy="none", lr=1e-3, eta_lambda=1e-3,
+               replay=False, replay_seed=0, micro_batch=1, lambda0=0.2, alpha=0.99, nu=2e-6,
+               replay_capacity=5000) -> dict:
+    """Restated PipelineTrainer over a convolutional net (conv_oracle.hpp), fp64 on the CPU.
+    geom: n_layers x 9 int32 {kind, c_in, h_in, w_in, c_out, k, stride, pad, res}."""
+    g = np.ascontiguousarray(geom, dtype=np.int32).reshape(-1, 9)
+    a = np.ascontiguousarray(acts, dtype=np.int32)
+    p = np.ascontiguousarray(params, dtype=np.float64)
+    o = OOpts(POLICIES[policy], lr, eta_lambda, lambda0, alpha, nu, int(replay), replay_seed, replay_capacity, 0,
+              micro_batch, 0, 0)
+    b = np.ascontiguousarray(bounds, dtype=np.uint64)
+    ev = np.ascontiguousarray(events, dtype=EVENT_DTYPE)
+    f = np.ascontiguousarray(features, dtype=np.float64)
+    lab = np.ascontiguousarray(labels, dtype=np.uint64)
+    n, F = f.shape
+    log = np.zeros(n, dtype=RECORD_DTYPE)
+    out = {k: np.zeros(p.size, dtype=np.float64) for k in ("params", "lambda", "v_r", "v_a")}
+    cap = 1 << 20
+    rids = np.zeros(cap, dtype=np.int64)
+    nrep = C.c_size_t()
+    _ck(lib().ferret_oracle_train_conv(C.c_int32(len(g)), _i32(g), _i32(a), _dp(p), _up(b), C.c_int32(len(b)),
+                                       C.byref(o), C.c_void_p(ev.ctypes.data), C.c_size_t(len(ev)), _dp(f), _up(lab),
+                                       C.c_size_t(n), C.c_size_t(F), C.c_void_p(log.ctypes.data), _dp(out["params"]),
+                                       _dp(out["lambda"]), _dp(out["v_r"]), _dp(out["v_a"]),
+                                       C.c_void_p(rids.ctypes.data), C.c_size_t(cap), C.byref(nrep)))
+    out.update(log=log, replay_ids=rids[: nrep.value].copy())
+    return out
+
+
+def conv_grad(geom, acts, params, x, labels):
+    """Mean-CE gradient (generalised forward_backward, net.hpp:157-200) and logits of a conv net."""
+    g = np.ascontiguousarray(geom, dtype=np.int32).reshape(-1, 9)
+    a = np.ascontiguousarray(acts, dtype=np.int32)
+    p = np.ascontiguousarray(params, dtype=np.float64)
+    xs = np.ascontiguousarray(x, dtype=np.float64)
+    lab = np.ascontiguousarray(labels, dtype=np.uint64)
+    n = xs.shape[0]
+    n_out = int(g[-1, 4])  # the head: dense, gap_dense or a conv on a 1x1 map
+    grad = np.zeros(p.size, dtype=np.float64)
+    logits = np.zeros((n, n_out), dtype=np.float64)
+    _ck(lib().ferret_oracle_conv_grad(C.c_int32(len(g)), _i32(g), _i32(a), _dp(p), _dp(xs), _up(lab), C.c_size_t(n),
+                                      _dp(grad), _dp(logits)))
+    return grad, logits

@@ -12,3 +12,4 @@ from .ferret import (  # noqa: F401
     compensate, dense_layer, device_available, lib, make_dense_net, online_accuracy, param_count,
     measure_profile, profile_from_widths, synth_drift_stream, train_pipeline,
 )
+from . import convnet  # noqa: F401,E402  (convolutional extension, BASELINE config 3)

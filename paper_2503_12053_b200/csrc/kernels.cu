@@ -549,13 +549,13 @@ __global__ void __launch_bounds__(kThreads) update_tile_kernel(const UpdArgs a) 
     const int last = a.nv - 1;
     const bool learn = a.eta > 0.f && a.v_r != nullptr;
     const bool cached = POLICY == 4 && last <= kRegChain;
-    if (!sg.bias) {
+    if (!sg.bias && sg.g_off < 0) {
         for (int i = tid; i < K * B * R; i += kThreads) {
             const int k = i / (B * R), rem = i - k * B * R, b = rem / R, rr = rem - b * R;
             sdel[i] = __ldg(a.pend[k].stash + sg.dlt_off + (size_t)b * sg.out + t.r0 + rr);
         }
-        __syncthreads();
     }
+    __syncthreads();
     // the element's new value, compensator state and write-back
     auto apply = [&](size_t e, int row_in_tile, int c) {
         const float th = __ldg(a.vers[last] + e);
@@ -577,7 +577,10 @@ __global__ void __launch_bounds__(kThreads) update_tile_kernel(const UpdArgs a) 
         float mean = 0.f;
         for (int k = 0; k < K; ++k) {
             float g = 0.f;
-            if (sg.bias) {
+            if (sg.g_off >= 0) {  // materialised gradient (convolutions: conv_wgrad / conv_bgrad)
+                g = __ldg(a.pend[k].stash + sg.g_off +
+                          (sg.bias ? (size_t)row_in_tile : (size_t)(t.r0 + row_in_tile) * sg.in + c));
+            } else if (sg.bias) {
                 const float* dl = a.pend[k].stash + sg.dlt_off + row_in_tile;  // row_in_tile = absolute row here
 #pragma unroll
                 for (int b = 0; b < BT; ++b)
@@ -1281,6 +1284,12 @@ void spec_update(const UpdArgs& a, KernelSpec& k) {
     const long long blocks = a.n_tiles;
     // FERRET_STREAM_MIN_CHAIN (test / experiment knob): chain length above which
     // the smem-staged kernel takes over from the register-resident one
+    if (a.gmat) {  // materialised gradients (conv stages): the generic tile kernel
+        const void* f = a.policy == 0 ? update_func<0>(a.B) : a.policy == 1 ? update_func<1>(a.B)
+                      : a.policy == 2 ? update_func<2>(a.B) : a.policy == 3 ? update_func<3>(a.B) : update_func<4>(a.B);
+        fill(k, f, dim3((unsigned)blocks), dim3(kThreads), a);
+        return;
+    }
     const char* env = std::getenv("FERRET_STREAM_MIN_CHAIN");
     const int min_chain = env ? std::atoi(env) : kStreamMinChain;
     if (a.policy == 4 && a.K == 1 && a.nv > min_chain && a.lam_d != nullptr) {

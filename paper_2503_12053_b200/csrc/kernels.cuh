@@ -84,6 +84,8 @@ struct UpdSeg {
     int in, out;
     long long xin_off;    // stash offset of the layer input (activation of layer l-1); -1 = net input
     long long dlt_off;    // stash offset of the layer's delta
+    long long g_off;      // >= 0: the segment's gradient is materialised in the stash at this offset
+                          // (convolutions: conv_wgrad writes it), element (r, c) at g_off + r * in + c
 };
 
 // One CTA of the update kernel: `nrows` rows x 256 columns of a layer's
@@ -120,6 +122,7 @@ struct UpdPending {
 // then theta_new = theta_cur - step * sum_k out_k, written to `dst`.
 struct UpdArgs {
     int n_segs, B, K, policy;
+    int gmat;                // some segment reads a materialised gradient (UpdSeg::g_off): generic kernel
     long long n_items;
     const UpdSeg* segs;      // device array
     const UpdTile* tiles;    // device array, one per CTA
@@ -270,6 +273,51 @@ void spec_pool(const PoolArgs& a, KernelSpec& k);
 void spec_send(const SendArgs& a, KernelSpec& k);
 void spec_recv(const RecvArgs& a, KernelSpec& k);
 cudaError_t launch_spec(KernelSpec& k, cudaStream_t s);
+
+// ---------------------------------------------------------------------------
+// Convolutional layers (conv.cu; BASELINE config 3 — the reference has no
+// convolution; the CPU checker lives with the tests). Activations are
+// NCHW per sample, rows of B samples as everywhere else. Each op is an implicit
+// GEMM C[M x N] = A[M x K] B[K x N] on 64x64 CTA tiles (fp32 SIMT, 4x4 outputs
+// per thread), optionally split over K into `partial` with an ordered
+// reduction + epilogue kernel (deterministic):
+//   fwd    M = c_out, N = B*h_out*w_out, K = c_in*k*k   Y = act(A B + b + shortcut)
+//   dgrad  M = c_in,  N = B*h_in*w_in,   K = c_out*k*k  Y = mask * (A B + skip)
+//   wgrad  M = c_out, N = c_in*k*k,      K = B*h_out*w_out   Y = gW (then gb, conv_bgrad)
+struct ConvArgs {
+    const float* W;      // c_out x c_in x k x k
+    const float* bias;   // fwd
+    const float* X;      // fwd / wgrad: the layer input rows (B x c_in*h_in*w_in)
+    const int* xidx;     // nullable: input row b at X + xidx[b] * in_w (replay gather)
+    const float* D;      // dgrad / wgrad: delta at the layer output (masked), B x c_out*h_out*w_out
+    float* Y;
+    const float* res;    // fwd: block input rows (shortcut); dgrad: delta of the residual layer above (skip)
+    int rc, rh, rw;      // fwd: block input c/h/w; dgrad: the residual layer's output c/h/w
+    const float* mask;   // dgrad: output of the layer below (ReLU mask), nullable
+    int relu;
+    int B, ci, hi, wi, co, ho, wo, k, s, p;
+    int M, N, K, splits, kchunk;
+    float* partial;      // splits x M x N (splits > 1)
+};
+enum { kConvFwd = 0, kConvDgrad = 1, kConvWgrad = 2 };
+// fills M, N, K, splits, kchunk for the op; returns the partial floats needed
+size_t conv_plan(ConvArgs& a, int mode, size_t max_partial);
+// one or two kernels (GEMM, then the ordered split reduction + epilogue)
+int spec_conv(const ConvArgs& a, int mode, KernelSpec& gemm, KernelSpec& reduce);
+// gb[co] = sum over samples and pixels of D (wgrad's bias part), written at Y
+void spec_conv_bgrad(const ConvArgs& a, float* gb, KernelSpec& k);
+// global average pool (GAP_DENSE input): pooled[b][c] = mean_p x[b][c][p]
+struct PoolMeanArgs {
+    const float* X;
+    const int* xidx;
+    float* Y;            // B x C
+    float* dX;           // unpool: d_in[b][c][p] = mask * dY[b][c] / HW
+    const float* dY;
+    const float* mask;
+    int B, C, HW;
+};
+void spec_gap(const PoolMeanArgs& a, KernelSpec& k);
+void spec_ungap(const PoolMeanArgs& a, KernelSpec& k);
 // grid geometry of the bwd launcher (for scratch sizing)
 int bwd_col_tiles(int in);
 int bwd_row_splits(int in, int out);

@@ -144,10 +144,20 @@ struct Head {
 };
 
 struct LayerDev {
-    int in = 0, out = 0, act = 0, stage = 0;
+    int in = 0, out = 0, act = 0, stage = 0;  // in / out: activation widths (c*h*w for convolutions)
     long long woff = 0, boff = 0;        // inside the stage slot
     long long host_off = 0;              // in flatten() order of the whole net
     long long act_off = 0, dlt_off = 0;  // inside a stash slot
+    // convolutional extension (ferret_b200.h FERRET_LAYER_*); dense layers: kind 0,
+    // rows = out, cols = in
+    int kind = FERRET_LAYER_DENSE;
+    int ci = 0, hi = 1, wi = 1, co = 0, ho = 1, wo = 1, k = 1, st = 1, pad = 0, res = 0;
+    int rows = 0, cols = 0;              // parameter matrix: rows x cols, then rows biases
+    long long g_off = -1;                // conv: materialised gradient (rows x cols, then rows) in a stash slot
+    long long pool_off = -1, pdl_off = -1;  // gap_dense: pooled input and its delta (B x ci) in a stash slot
+    long long nw() const { return static_cast<long long>(rows) * cols; }
+    bool conv() const { return kind == FERRET_LAYER_CONV; }
+    bool gap() const { return kind == FERRET_LAYER_GAP_DENSE; }
 };
 
 struct StageDev {
@@ -162,6 +172,7 @@ struct StageDev {
     float* gap = nullptr;
     fb200::UpdSeg* segs_dev = nullptr;
     int n_segs = 0;
+    bool gmat = false;  // holds a convolution: its update reads materialised gradients
     fb200::UpdTile* tiles_dev = nullptr;
     fb200::UpdWork* works_dev = nullptr;
     fb200::UpdWork* works4_dev = nullptr;  // float4 tiles (nullptr when a weight row is not 16-byte aligned)
@@ -385,6 +396,49 @@ struct ferret_trainer {
     std::vector<LayerDev> layers;
     std::vector<StageDev> stages;
     std::vector<double> init_params;
+    std::vector<int32_t> geom;  // conv nets: the descriptor's geometry (empty: all dense)
+
+    // FERRET_LAYER_* geometry of layer l (ferret_b200.h), checked against the widths
+    void set_geometry(LayerDev& ld, int l, const int32_t* q) {
+        const std::string at = "layer " + std::to_string(l) + ": ";
+        ld.kind = q[0];
+        const long long in_w = static_cast<long long>(q[1]) * q[2] * q[3];
+        if (q[1] < 1 || q[2] < 1 || q[3] < 1 || q[4] < 1) fail(FERRET_E_CONFIG, at + "geometry sizes must be positive");
+        if (in_w != ld.in) fail(FERRET_E_CONFIG, at + "c_in*h_in*w_in differs from the input width");
+        ld.ci = q[1];
+        ld.hi = q[2];
+        ld.wi = q[3];
+        ld.co = q[4];
+        ld.res = q[8];
+        if (ld.kind == FERRET_LAYER_CONV) {
+            ld.k = q[5];
+            ld.st = q[6];
+            ld.pad = q[7];
+            if (ld.k < 1 || ld.st < 1 || ld.pad < 0) fail(FERRET_E_CONFIG, at + "bad convolution geometry");
+            ld.ho = (ld.hi + 2 * ld.pad - ld.k) / ld.st + 1;
+            ld.wo = (ld.wi + 2 * ld.pad - ld.k) / ld.st + 1;
+            if (ld.ho < 1 || ld.wo < 1) fail(FERRET_E_CONFIG, at + "empty convolution output");
+            if (static_cast<long long>(ld.co) * ld.ho * ld.wo != ld.out)
+                fail(FERRET_E_CONFIG, at + "c_out*h_out*w_out differs from the output width");
+            ld.rows = ld.co;
+            ld.cols = ld.ci * ld.k * ld.k;
+        } else if (ld.kind == FERRET_LAYER_DENSE || ld.kind == FERRET_LAYER_GAP_DENSE) {
+            if (ld.co != ld.out) fail(FERRET_E_CONFIG, at + "c_out differs from the output width");
+            if (ld.kind == FERRET_LAYER_DENSE && (ld.hi != 1 || ld.wi != 1))
+                fail(FERRET_E_CONFIG, at + "a dense layer has h_in = w_in = 1");
+            ld.rows = ld.co;
+            ld.cols = ld.ci;
+        } else {
+            fail(FERRET_E_CONFIG, at + "unknown layer kind");
+        }
+        if (ld.res) {
+            if (!ld.conv() || l < 2 || !layers[static_cast<size_t>(l - 1)].conv())
+                fail(FERRET_E_CONFIG, at + "a residual layer is the second convolution of a block after layer 1");
+            const LayerDev& a = layers[static_cast<size_t>(l - 1)];
+            if (a.ci > ld.co || a.hi % ld.ho != 0 || a.wi % ld.wo != 0 || a.hi / ld.ho != a.wi / ld.wo)
+                fail(FERRET_E_CONFIG, at + "residual shortcut shape");
+        }
+    }
     cudaStream_t stream = nullptr;
     cudaStream_t nstream = nullptr;  // side stream: the normalizer runs ahead of training
     static constexpr size_t kNormGroup = 16;
@@ -635,8 +689,19 @@ struct ferret_trainer {
             ld.act = net.act[l];
             if (l > 0 && net.in[l] != net.out[l - 1])
                 fail(FERRET_E_CONFIG, "layer " + std::to_string(l) + ": input width mismatch");
+            ld.rows = ld.out;
+            ld.cols = ld.in;
+            ld.co = ld.out;
+            ld.ci = ld.in;
+            if (net.geom) set_geometry(ld, l, net.geom + static_cast<size_t>(l) * FERRET_GEOM_INTS);
             ld.host_off = host_off;
-            host_off += static_cast<long long>(ld.in) * ld.out + ld.out;
+            host_off += ld.nw() + ld.rows;
+        }
+        if (net.geom) {
+            geom.assign(net.geom, net.geom + static_cast<size_t>(L) * FERRET_GEOM_INTS);
+            for (int32_t i = 1; i + 1 < n_bounds; ++i)
+                if (layers[static_cast<size_t>(bounds[i])].res)
+                    fail(FERRET_E_CONFIG, "partition bound " + std::to_string(bounds[i]) + " splits a residual block");
         }
         F = layers.front().in;
         n_out = layers.back().out;
@@ -649,10 +714,22 @@ struct ferret_trainer {
             ld.dlt_off = align_up(cursor, 32);
             cursor = ld.dlt_off + static_cast<long long>(B) * ld.out;
             max_width = std::max(max_width, ld.out);
+            if (ld.conv()) {
+                ld.g_off = align_up(cursor, 32);
+                cursor = ld.g_off + ld.nw() + ld.rows;
+            }
+            if (ld.gap()) {
+                ld.pool_off = align_up(cursor, 32);
+                cursor = ld.pool_off + static_cast<long long>(B) * ld.ci;
+                ld.pdl_off = align_up(cursor, 32);
+                cursor = ld.pdl_off + static_cast<long long>(B) * ld.ci;
+            }
         }
+        // predict scratch: three rotating buffers (a residual layer reads the input of
+        // the layer below while writing its own output)
         pred_stride = align_up(static_cast<long long>(B) * max_width, 64);
         pred_off = align_up(cursor, 64);
-        stash_stride = align_up(pred_off + 2 * pred_stride, 64);
+        stash_stride = align_up(pred_off + 3 * pred_stride, 64);
         stages.resize(static_cast<size_t>(P));
         hs.current.assign(static_cast<size_t>(P), 0);
         owner.assign(static_cast<size_t>(P), 0);
@@ -670,38 +747,43 @@ struct ferret_trainer {
                 LayerDev& ld = layers[static_cast<size_t>(l)];
                 ld.stage = j;
                 ld.woff = align_up(c, 32);
-                c = ld.woff + static_cast<long long>(ld.in) * ld.out;
+                c = ld.woff + ld.nw();
                 ld.boff = align_up(c, 32);
-                c = ld.boff + ld.out;
-                s.n_params += static_cast<long long>(ld.in) * ld.out + ld.out;
+                c = ld.boff + ld.rows;
+                s.n_params += ld.nw() + ld.rows;
                 // float4 items need 16-byte aligned weight rows and input rows
                 // (stash rows are B x in; x rows are F wide with F == in at layer 0)
-                const int vec = (ld.in % 4 == 0) ? 4 : 1;
+                const int vec = (ld.cols % 4 == 0) ? 4 : 1;
                 fb200::UpdSeg w{};
                 w.layer = l - s.lo;
                 w.bias = 0;
                 w.vec = vec;
-                w.per_row = ld.in / vec;
+                w.per_row = ld.cols / vec;
                 w.item0 = s.n_items;
                 w.elem0 = ld.woff;
-                w.in = ld.in;
-                w.out = ld.out;
-                w.xin_off = l == 0 ? -1 : layers[static_cast<size_t>(l - 1)].act_off;
+                w.in = ld.cols;
+                w.out = ld.rows;
+                // gW = delta (x) input, recomputed by the update from the stash; a
+                // convolution's gradient is materialised there by conv_wgrad instead
+                w.xin_off = ld.gap() ? ld.pool_off : l == 0 ? -1 : layers[static_cast<size_t>(l - 1)].act_off;
                 w.dlt_off = ld.dlt_off;
+                w.g_off = ld.conv() ? ld.g_off : -1;
+                s.gmat = s.gmat || ld.conv();
                 tab.push_back(w);
-                s.n_items += static_cast<long long>(ld.out) * w.per_row;
+                s.n_items += static_cast<long long>(ld.rows) * w.per_row;
                 fb200::UpdSeg bs = w;
                 bs.bias = 1;
                 bs.vec = 1;
                 bs.per_row = 1;
                 bs.item0 = s.n_items;
                 bs.elem0 = ld.boff;
+                bs.g_off = ld.conv() ? ld.g_off + ld.nw() : -1;
                 tab.push_back(bs);
-                s.n_items += ld.out;
-                if (l > 0) {
-                    max_partial = std::max(max_partial, static_cast<size_t>(fb200::bwd_row_splits(ld.in, ld.out)) *
-                                                            static_cast<size_t>(B) * static_cast<size_t>(ld.in));
-                    max_tiles = std::max(max_tiles, static_cast<size_t>(fb200::bwd_col_tiles(ld.in)));
+                s.n_items += ld.rows;
+                if (l > 0 && !ld.conv()) {
+                    max_partial = std::max(max_partial, static_cast<size_t>(fb200::bwd_row_splits(ld.cols, ld.rows)) *
+                                                            static_cast<size_t>(B) * static_cast<size_t>(ld.cols));
+                    max_tiles = std::max(max_tiles, static_cast<size_t>(fb200::bwd_col_tiles(ld.cols)));
                 }
             }
             s.slot_floats = align_up(c, 64);
@@ -818,9 +900,9 @@ struct ferret_trainer {
             for (int l = s.lo; l < s.hi; ++l) {
                 const LayerDev& ld = layers[static_cast<size_t>(l)];
                 const double* src = init_params.data() + ld.host_off;
-                const long long nw = static_cast<long long>(ld.in) * ld.out;
+                const long long nw = ld.nw();
                 for (long long i = 0; i < nw; ++i) slot[static_cast<size_t>(ld.woff + i)] = static_cast<float>(src[i]);
-                for (int r = 0; r < ld.out; ++r)
+                for (int r = 0; r < ld.rows; ++r)
                     slot[static_cast<size_t>(ld.boff + r)] = static_cast<float>(src[nw + r]);
             }
             cuda_check(cudaMemcpy(s.slot(0), slot.data(), slot.size() * sizeof(float), cudaMemcpyHostToDevice),
@@ -1327,8 +1409,8 @@ struct ferret_trainer {
                     const bool cross = j > 0 && owner[static_cast<size_t>(j - 1)] != owner[static_cast<size_t>(j)];
                     if (!DRY && mine(j))
                         launch_stage_backward(j, stages[static_cast<size_t>(j)].slot(r), stash(u),
-                                              d_labc + u * static_cast<size_t>(B), slot_of[u], {vslot(j, r)}, ustash(u),
-                                              cross);
+                                              d_labc + u * static_cast<size_t>(B), slot_of[u], {vslot(j, r), ngroup(u)},
+                                              ustash(u), cross, xrows(u));
                     if (cross && sched.has_bwd[u * static_cast<size_t>(P) + static_cast<size_t>(j - 1)]) {
                         const LayerDev& below = layers[static_cast<size_t>(stages[static_cast<size_t>(j)].lo - 1)];
                         const long long doff = below.dlt_off, aoff = below.act_off;
@@ -1443,6 +1525,7 @@ struct ferret_trainer {
         const StageDev& s = stages[static_cast<size_t>(j)];
         fb200::UpdArgs a{};
         a.n_segs = s.n_segs;
+        a.gmat = s.gmat ? 1 : 0;
         a.n_items = s.n_items;
         a.B = B;
         a.segs = s.segs_dev;
@@ -1485,6 +1568,7 @@ struct ferret_trainer {
             const bool bf16 = opt.precision == FERRET_PREC_BF16;
             for (const LayerDev& ld : layers)
                 for (bool bwd : {false, true}) {
+                    if (ld.kind != FERRET_LAYER_DENSE) continue;
                     const fb200::MmaGeom g =
                         fb200::mma_geom(bf16, bwd, ld.in, ld.out, opt.precision == FERRET_PREC_FP32);
                     mma_partial_floats = std::max(mma_partial_floats, g.partial_floats);
@@ -1509,12 +1593,12 @@ struct ferret_trainer {
     long long split_min_params =
         std::getenv("FERRET_SPLIT_MIN_PARAMS") ? std::atoll(std::getenv("FERRET_SPLIT_MIN_PARAMS")) : (1LL << 20);
     bool use_split(const LayerDev& ld) const {
-        return opt.precision == FERRET_PREC_FP32 && split_min_params >= 0 &&
+        return ld.kind == FERRET_LAYER_DENSE && opt.precision == FERRET_PREC_FP32 && split_min_params >= 0 &&
                static_cast<long long>(ld.in) * ld.out >= split_min_params && fb200::mma_supported(false, ld.in, ld.out);
     }
     bool use_mma(const LayerDev& ld) const {
         if (opt.precision == FERRET_PREC_FP32) return use_split(ld);
-        return static_cast<long long>(ld.in) * ld.out >= mma_min_params &&
+        return ld.kind == FERRET_LAYER_DENSE && static_cast<long long>(ld.in) * ld.out >= mma_min_params &&
                fb200::mma_supported(opt.precision == FERRET_PREC_BF16, ld.in, ld.out);
     }
     void emit_mma(const LayerDev& ld, const float* stage_slot, bool bwd, const float* X, const int* xidx,
@@ -1546,12 +1630,41 @@ struct ferret_trainer {
 
     bool can_fuse_head() const {
         const LayerDev& last = layers.back();
-        return !use_mma(last) && fb200::fwd_single_cta(last.in, last.out, B, last.in % 4 == 0);
+        return !use_mma(last) && !last.conv() && fb200::fwd_single_cta(last.cols, last.rows, B, last.cols % 4 == 0);
     }
 
+    // `blk`: the block input (input of layer l-1) of a residual convolution;
+    // `pooled`: B x c_in scratch of a gap_dense layer
     void emit_layer(const LayerDev& ld, const float* stage_slot, const float* X, const int* xidx, float* Y,
                     const std::vector<uint64_t>& reads, const std::vector<uint64_t>& writes,
-                    const Head& head = Head{}) {
+                    const Head& head = Head{}, const float* blk = nullptr, float* pooled = nullptr) {
+        if (ld.conv()) {
+            fb200::ConvArgs c = conv_args(ld);
+            c.W = stage_slot + ld.woff;
+            c.bias = stage_slot + ld.boff;
+            c.X = X;
+            c.xidx = xidx;
+            c.Y = Y;
+            c.relu = ld.act == FERRET_ACT_RELU;
+            if (ld.res) {
+                const LayerDev& a = layers[static_cast<size_t>(&ld - layers.data() - 1)];
+                c.res = blk;
+                c.rc = a.ci;
+                c.rh = a.hi;
+                c.rw = a.wi;
+            }
+            return emit_conv(c, fb200::kConvFwd, reads, writes,
+                             4.0 * (ld.nw() + ld.rows) + 4.0 * B * (ld.in + ld.out) + (ld.res ? 4.0 * B * ld.out : 0.0));
+        }
+        if (ld.gap()) {
+            fb200::PoolMeanArgs g{X, xidx, pooled, nullptr, nullptr, nullptr, B, ld.ci, ld.hi * ld.wi};
+            fb200::KernelSpec kg;
+            fb200::spec_gap(g, kg);
+            gb->cur_bytes = 4.0 * B * (ld.in + ld.ci);
+            gb->kernel(kg, reads, writes);
+            X = pooled;
+            xidx = nullptr;
+        }
         if (use_mma(ld)) return emit_mma(ld, stage_slot, false, X, xidx, nullptr, Y, reads, writes);
         fb200::FwdArgs a{};
         a.head_mode = head.mode;
@@ -1564,14 +1677,66 @@ struct ferret_trainer {
         a.X = X;
         a.xidx = xidx;
         a.Y = Y;
-        a.in = ld.in;
-        a.out = ld.out;
+        a.in = ld.cols;
+        a.out = ld.rows;
         a.B = B;
         a.relu = ld.act == FERRET_ACT_RELU;
         fb200::KernelSpec k;
         fb200::spec_fwd(a, k);
-        gb->cur_bytes = 4.0 * ld.in * ld.out + 4.0 * ld.out + 4.0 * B * (ld.in + ld.out);  // W, b, X, Y
+        gb->cur_bytes = 4.0 * ld.cols * ld.rows + 4.0 * ld.rows + 4.0 * B * (ld.cols + ld.rows);  // W, b, X, Y
         gb->kernel(k, reads, writes);
+    }
+
+    // ------------------------------------------------ convolutions (conv.cu)
+    static constexpr size_t kConvPartialCap = size_t{1} << 22;  // split-K partial floats per scratch region
+    std::map<uint64_t, float*> conv_scratch;
+    fb200::ConvArgs conv_args(const LayerDev& ld) const {
+        fb200::ConvArgs c{};
+        c.B = B;
+        c.ci = ld.ci;
+        c.hi = ld.hi;
+        c.wi = ld.wi;
+        c.co = ld.co;
+        c.ho = ld.ho;
+        c.wo = ld.wo;
+        c.k = ld.k;
+        c.s = ld.st;
+        c.p = ld.pad;
+        return c;
+    }
+    // split-K scratch, one region per written resource (nodes writing the same
+    // resource are serialised by the DAG)
+    float* conv_scratch_for(uint64_t key) {
+        auto it = conv_scratch.find(key);
+        if (it != conv_scratch.end()) return it->second;
+        return conv_scratch[key] = dalloc<float>(kConvPartialCap, device_bytes);
+    }
+    void emit_conv(fb200::ConvArgs& c, int mode, const std::vector<uint64_t>& reads, const std::vector<uint64_t>& writes,
+                   double bytes) {
+        fb200::conv_plan(c, mode, kConvPartialCap);
+        if (c.splits > 1) c.partial = conv_scratch_for(writes.at(0));
+        fb200::KernelSpec g, r;
+        const int n = fb200::spec_conv(c, mode, g, r);
+        gb->cur_bytes = bytes;
+        gb->kernel(g, reads, writes);
+        if (n == 2) {
+            gb->cur_bytes = 8.0 * c.splits * static_cast<double>(c.M) * c.N;
+            gb->kernel(r, reads, writes);
+        }
+    }
+    // the weight and bias gradient of convolution `ld` into its stash region
+    void emit_conv_wgrad(const LayerDev& ld, float* stash_u, const float* X, const int* xidx,
+                         const std::vector<uint64_t>& reads, uint64_t stash_key) {
+        fb200::ConvArgs c = conv_args(ld);
+        c.X = X;
+        c.xidx = xidx;
+        c.D = stash_u + ld.dlt_off;
+        c.Y = stash_u + ld.g_off;
+        emit_conv(c, fb200::kConvWgrad, reads, {stash_key}, 4.0 * ld.nw() + 4.0 * B * (ld.in + ld.out));
+        fb200::KernelSpec kb;
+        fb200::spec_conv_bgrad(c, stash_u + ld.g_off + ld.nw(), kb);
+        gb->cur_bytes = 4.0 * B * ld.out + 4.0 * ld.rows;
+        gb->kernel(kb, reads, {stash_key});
     }
 
     // predict_class(net_, x) at the arrival (learner.hpp:398-399): full net at
@@ -1591,7 +1756,7 @@ struct ferret_trainer {
             const StageDev& s = stages[static_cast<size_t>(j)];
             if (j > 0) {
                 const int l = s.lo - 1;
-                float* buf = scratch + (l & 1) * pred_stride;
+                float* buf = scratch + (l % 3) * pred_stride;
                 xfer(owner[static_cast<size_t>(j - 1)], owner[static_cast<size_t>(j)], [&] { return buf; },
                      [&] { return buf; }, static_cast<size_t>(B) * layers[static_cast<size_t>(l)].out, nullptr, sk);
             }
@@ -1600,19 +1765,23 @@ struct ferret_trainer {
             gb->cur_stage = -1;
             const std::vector<uint64_t> reads{vslot(j, rel[static_cast<size_t>(j)]), ngroup(u)};
             for (int l = s.lo; l < s.hi; ++l) {
-                const float* X = l == 0 ? x0 : scratch + ((l - 1) & 1) * pred_stride;
+                const float* X = l == 0 ? x0 : scratch + ((l - 1) % 3) * pred_stride;
                 Head h;
                 if (l == L - 1 && can_fuse_head()) {
                     h.mode = 0;
                     h.pred = d_predc + u * static_cast<size_t>(B);
                 }
-                emit_layer(layers[static_cast<size_t>(l)], s.slot(rel[static_cast<size_t>(j)]), X, nullptr,
-                           scratch + (l & 1) * pred_stride, reads, {sk}, h);
+                const LayerDev& ld = layers[static_cast<size_t>(l)];
+                // the block input of a residual layer is the input of layer l-1: buffer (l-2) % 3,
+                // which a gap_dense layer (never residual) uses as its pooled scratch
+                float* third = scratch + ((l + 1) % 3) * pred_stride;
+                emit_layer(ld, s.slot(rel[static_cast<size_t>(j)]), X, nullptr, scratch + (l % 3) * pred_stride, reads,
+                           {sk}, h, ld.res ? third : nullptr, ld.gap() ? third : nullptr);
             }
         }
         if (DRY || !mine(P - 1) || can_fuse_head()) return;
         fb200::HeadArgs h{};
-        h.logits = scratch + ((L - 1) & 1) * pred_stride;
+        h.logits = scratch + ((L - 1) % 3) * pred_stride;
         h.n_out = n_out;
         h.B = B;
         h.mode = 0;
@@ -1640,7 +1809,9 @@ struct ferret_trainer {
                 h.delta = stash_u + ld.dlt_off;
                 h.scale = 1.0f / static_cast<float>(B);
             }
-            emit_layer(ld, slot, X, nullptr, stash_u + ld.act_off, reads, {stash_key}, h);
+            emit_layer(ld, slot, X, nullptr, stash_u + ld.act_off, reads, {stash_key}, h,
+                       ld.res ? stash_u + layers[static_cast<size_t>(l - 2)].act_off : nullptr,
+                       ld.gap() ? stash_u + ld.pool_off : nullptr);
         }
     }
 
@@ -1648,12 +1819,17 @@ struct ferret_trainer {
     // ReLU mask of the layer below applied on write (learner.hpp:443-476);
     // `cross`: the stage below is on another rank, which applies the mask.
     void launch_stage_backward(int j, const float* slot, float* stash_u, const int* lab, int scratch,
-                               const std::vector<uint64_t>& reads, uint64_t stash_key, bool cross) {
+                               const std::vector<uint64_t>& reads, uint64_t stash_key, bool cross,
+                               const float* x0 = nullptr, const int* x0idx = nullptr) {
         gb->cur_category = kCatBackward;
         gb->cur_stage = j;
         const StageDev& s = stages[static_cast<size_t>(j)];
         if (j == P - 1 && !can_fuse_head()) emit_delta_head(stash_u, lab, nullptr, 1.0f / static_cast<float>(B), {}, stash_key);
         for (int l = s.hi - 1; l >= s.lo; --l) {
+            const LayerDev& ld = layers[static_cast<size_t>(l)];
+            if (ld.conv())  // a convolution's weight gradient is materialised for the update
+                emit_conv_wgrad(ld, stash_u, l == 0 ? x0 : stash_u + layers[static_cast<size_t>(l - 1)].act_off,
+                                l == 0 ? x0idx : nullptr, reads, stash_key);
             if (l == 0) break;  // no input gradient for the first layer
             emit_layer_backward(l, slot, stash_u, scratch, reads, stash_key, !(cross && l == s.lo));
         }
@@ -1681,6 +1857,46 @@ struct ferret_trainer {
                              uint64_t stash_key, bool mask_on_write = true) {
         const LayerDev& ld = layers[static_cast<size_t>(l)];
         const LayerDev& below = layers[static_cast<size_t>(l - 1)];
+        const float* mask = mask_on_write && below.act == FERRET_ACT_RELU ? stash_u + below.act_off : nullptr;
+        if (ld.conv()) {  // transposed convolution, plus the shortcut's gradient when a residual layer sits above
+            fb200::ConvArgs c = conv_args(ld);
+            c.W = slot + ld.woff;
+            c.D = stash_u + ld.dlt_off;
+            c.Y = stash_u + below.dlt_off;
+            c.mask = mask;
+            if (l + 1 < L && layers[static_cast<size_t>(l + 1)].res) {
+                const LayerDev& r = layers[static_cast<size_t>(l + 1)];
+                c.res = stash_u + r.dlt_off;
+                c.rc = r.co;
+                c.rh = r.ho;
+                c.rw = r.wo;
+            }
+            return emit_conv(c, fb200::kConvDgrad, reads, {stash_key},
+                             4.0 * ld.nw() + 4.0 * B * (ld.out + 2.0 * ld.in));
+        }
+        if (ld.gap()) {  // W^T delta into the pooled delta, then spread over the pixels (/HW, ReLU mask)
+            fb200::BwdArgs a{};
+            a.W = slot + ld.woff;
+            a.d_out = stash_u + ld.dlt_off;
+            a.d_in = stash_u + ld.pdl_off;
+            a.in = ld.cols;
+            a.out = ld.rows;
+            a.B = B;
+            a.row_splits = fb200::bwd_row_splits(ld.cols, ld.rows);
+            a.partial = d_partial + static_cast<size_t>(scratch) * max_partial;
+            a.counters = d_counters + static_cast<size_t>(scratch) * max_tiles;
+            fb200::KernelSpec k;
+            fb200::spec_bwd(a, k);
+            gb->cur_bytes = 4.0 * ld.nw() + 4.0 * B * (ld.rows + ld.cols);
+            gb->kernel(k, reads, {stash_key});
+            fb200::PoolMeanArgs g{nullptr, nullptr, nullptr, stash_u + below.dlt_off, stash_u + ld.pdl_off, mask,
+                                  B, ld.ci, ld.hi * ld.wi};
+            fb200::KernelSpec ku;
+            fb200::spec_ungap(g, ku);
+            gb->cur_bytes = 4.0 * B * (ld.ci + 2.0 * ld.in);
+            gb->kernel(ku, reads, {stash_key});
+            return;
+        }
         if (use_mma(ld))
             return emit_mma(ld, slot, true, stash_u + ld.dlt_off,  nullptr,
                             mask_on_write && below.act == FERRET_ACT_RELU ? stash_u + below.act_off : nullptr,
@@ -1734,6 +1950,7 @@ struct ferret_trainer {
         std::ostringstream h;
         h << "ferret-state v1\n" << "layers";
         for (const LayerDev& ld : layers) h << ' ' << ld.in << 'x' << ld.out << ':' << ld.act;
+        for (size_t i = 0; i < geom.size(); ++i) h << (i ? "," : "\ngeometry ") << geom[i];
         h << "\nbounds";
         for (const StageDev& st : stages) h << ' ' << st.lo;
         h << ' ' << L << "\noptions policy " << opt.policy << " replay " << opt.replay << " capacity "
@@ -1760,12 +1977,14 @@ struct ferret_trainer {
             std::ostringstream l, b, o;
             l << "layers";
             for (const LayerDev& ld : layers) l << ' ' << ld.in << 'x' << ld.out << ':' << ld.act;
+            for (size_t i = 0; i < geom.size(); ++i) l << (i ? "," : "\ngeometry ") << geom[i];
             b << "bounds";
             for (const StageDev& st : stages) b << ' ' << st.lo;
             b << ' ' << L;
             o << "options policy " << opt.policy << " replay " << opt.replay << " capacity " << opt.replay_capacity
               << " precision " << opt.precision << " micro_batch " << B;
-            expect(l.str());
+            std::istringstream ls(l.str());  // "layers" and, for conv nets, "geometry"
+            for (std::string want; std::getline(ls, want);) expect(want);
             expect(b.str());
             expect(o.str());
         }
@@ -2145,7 +2364,9 @@ struct ferret_trainer {
                 const LayerDev& ld = layers[static_cast<size_t>(l)];
                 const float* X = l == 0 ? d_pool_x : d_replay + layers[static_cast<size_t>(l - 1)].act_off;
                 emit_layer(ld, s.slot(rel[static_cast<size_t>(j)]), X, l == 0 ? ids : nullptr, d_replay + ld.act_off,
-                           {vslot(j, rel[static_cast<size_t>(j)]), pk}, {rk});
+                           {vslot(j, rel[static_cast<size_t>(j)]), pk}, {rk}, Head{},
+                           ld.res ? d_replay + layers[static_cast<size_t>(l - 2)].act_off : nullptr,
+                           ld.gap() ? d_replay + ld.pool_off : nullptr);
             }
         }
         if (!DRY && mine(P - 1)) {
@@ -2158,9 +2379,15 @@ struct ferret_trainer {
             const bool cross = j > 0 && owner_of(j - 1) != owner_of(j);
             if (!DRY && mine(j)) {
                 gb->cur_category = kCatReplay;
-                for (int l = s.hi - 1; l >= std::max(s.lo, 1); --l)
+                for (int l = s.hi - 1; l >= s.lo; --l) {
+                    const LayerDev& ld = layers[static_cast<size_t>(l)];
+                    if (ld.conv())
+                        emit_conv_wgrad(ld, d_replay, l == 0 ? d_pool_x : d_replay + layers[static_cast<size_t>(l - 1)].act_off,
+                                        l == 0 ? ids : nullptr, {vslot(j, rel[static_cast<size_t>(j)]), pk}, rk);
+                    if (l == 0) break;
                     emit_layer_backward(l, s.slot(rel[static_cast<size_t>(j)]), d_replay, stash_slots,
                                         {vslot(j, rel[static_cast<size_t>(j)])}, rk, !(cross && l == s.lo));
+                }
             }
             if (cross) {
                 const LayerDev& below = layers[static_cast<size_t>(s.lo - 1)];
@@ -2228,8 +2455,10 @@ struct ferret_trainer {
             default: per = 8.0;
         }
         double side = 0.0;
-        for (int l = s.lo; l < s.hi; ++l)
-            side += 4.0 * B * (layers[static_cast<size_t>(l)].in + layers[static_cast<size_t>(l)].out);
+        for (int l = s.lo; l < s.hi; ++l) {
+            const LayerDev& ld = layers[static_cast<size_t>(l)];
+            side += ld.conv() ? 4.0 * static_cast<double>(ld.nw() + ld.rows) : 4.0 * B * (ld.cols + ld.rows);
+        }
         return per * static_cast<double>(s.n_params) + side * static_cast<double>(reads.size());
     }
 
@@ -2387,9 +2616,9 @@ struct ferret_trainer {
         for (int l = s.lo; l < s.hi; ++l) {
             const LayerDev& ld = layers[static_cast<size_t>(l)];
             double* dst = out + ld.host_off;
-            const long long nw = static_cast<long long>(ld.in) * ld.out;
+            const long long nw = ld.nw();
             for (long long i = 0; i < nw; ++i) dst[i] = offset + static_cast<double>(slot[static_cast<size_t>(ld.woff + i)]);
-            for (int r = 0; r < ld.out; ++r) dst[nw + r] = offset + static_cast<double>(slot[static_cast<size_t>(ld.boff + r)]);
+            for (int r = 0; r < ld.rows; ++r) dst[nw + r] = offset + static_cast<double>(slot[static_cast<size_t>(ld.boff + r)]);
         }
     }
 
@@ -2474,6 +2703,7 @@ ferret_status ferret_seq_create(const ferret_net_desc* net, const ferret_seq_opt
         if (!net || !o || !out) fail(FERRET_E_INVALID_ARG, "seq_create: null argument");
         if (net->n_layers <= 0) fail(FERRET_E_CONFIG, "net needs at least one layer");
         if (net->n_layers > fb200::kMaxStageLayers) fail(FERRET_E_CONFIG, "at most 16 layers per sequential learner");
+        if (net->geom) fail(FERRET_E_CONFIG, "sequential learners take dense nets (convolutions: the pipeline trainer)");
         require_device(o->device);
         ferret_train_opts t_o{};
         ferret_train_opts_default(&t_o);

@@ -71,7 +71,7 @@ class TrainOpts(C.Structure):
 
 class NetDesc(C.Structure):
     _fields_ = [("n_layers", C.c_int32), ("in_", C.POINTER(C.c_uint64)), ("out", C.POINTER(C.c_uint64)),
-                ("act", C.POINTER(C.c_int32)), ("params", C.POINTER(C.c_double))]
+                ("act", C.POINTER(C.c_int32)), ("params", C.POINTER(C.c_double)), ("geom", C.POINTER(C.c_int32))]
 
 
 class SeqOpts(C.Structure):
@@ -360,15 +360,29 @@ def widths_layers(widths: Sequence[int]):
 class PipelineTrainer:
     """PipelineTrainer (learner.hpp:330-520) on one B200; state lives in HBM."""
 
-    def __init__(self, widths: Sequence[int], params: np.ndarray, bounds: Sequence[int],
+    def __init__(self, widths, params: np.ndarray, bounds: Sequence[int],
                  opt: PipelineTrainOptions = PipelineTrainOptions()):
+        """`widths`: the MLP's layer widths (the reference's DenseNet), or a
+        convnet.ConvNetSpec (the convolutional extension, BASELINE config 3)."""
+        geom = None
+        if hasattr(widths, "geom"):  # ConvNetSpec
+            spec = widths
+            geom = np.ascontiguousarray(spec.geom, dtype=np.int32)
+            widths = spec.widths
+            acts = np.ascontiguousarray(spec.acts, dtype=np.int32)
+            ins, outs, _ = widths_layers(widths)
+            self.n_params = spec.n_params
+        else:
+            ins, outs, acts = widths_layers(widths)
+            self.n_params = param_count(widths)
         self.widths = list(widths)
         self.bounds = list(bounds)
         self.opt = opt
-        self.n_params = param_count(widths)
-        ins, outs, acts = widths_layers(widths)
-        self._keep = (ins, outs, acts, np.ascontiguousarray(params, dtype=np.float64))
-        desc = NetDesc(len(ins), _up(ins), _up(outs), acts.ctypes.data_as(C.POINTER(C.c_int32)), _dp(self._keep[3]))
+        self._keep = (ins, outs, acts, np.ascontiguousarray(params, dtype=np.float64), geom)
+        if self._keep[3].size != self.n_params:
+            raise ConfigError(f"params: expected {self.n_params} values, got {self._keep[3].size}")
+        desc = NetDesc(len(ins), _up(ins), _up(outs), acts.ctypes.data_as(C.POINTER(C.c_int32)), _dp(self._keep[3]),
+                       geom.ctypes.data_as(C.POINTER(C.c_int32)) if geom is not None else None)
         b = np.ascontiguousarray(bounds, dtype=np.uint64)
         h = C.c_void_p()
         _check(lib().ferret_trainer_create(C.byref(desc), _up(b), len(b), C.byref(opt.c()), C.byref(h)))

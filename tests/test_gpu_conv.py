@@ -1,0 +1,89 @@
+"""GPU parity of the convolutional extension (BASELINE config 3: ResNet-18-style CNN,
+CIFAR-shaped stream, ER replay, 4 stages) against the conv CPU oracle
+(oracle/conv_oracle.hpp, pinned in tests/test_conv_oracle.py).
+
+Same bar as the MLP parity tests: fp32 parameters within 1e-4 relative per stage
+of the fp64 oracle, online accuracy within 0.5 pp, schedule facts exact; plus
+bitwise determinism of the split-K convolution kernels.
+"""
+import numpy as np
+import pytest
+
+from paper_2503_12053_b200 import convnet as cn
+
+pytestmark = pytest.mark.gpu
+
+PARAM_RTOL = 1e-4
+OACC_TOL = 0.5
+
+
+def _setup(fb, width, blocks, n_units, B, n_stages=4, in_chw=(3, 32, 32)):
+    spec = cn.resnet_cifar(width=width, blocks=blocks, in_chw=in_chw)
+    params = cn.make_conv_net(spec, 1)
+    feats, labels = fb.synth_drift_stream(n_units * B, spec.in_width(0), 10, "split_tasks", 7)
+    prof = cn.profile(spec)
+    bounds = cn.balanced_bounds(spec, n_stages)
+    t_d = cn.stage_t_d(prof, bounds)
+    sched = fb.Schedule.forced(prof, t_d, fb.StreamSpec(t_d=t_d, horizon=n_units * t_d), bounds, n_units)
+    return spec, params, feats, labels, sched
+
+
+def _slices(spec, bounds):
+    offs = np.concatenate([[0], np.cumsum([spec.layer_params(l) for l in range(spec.n_layers)])])
+    return [(int(offs[bounds[j]]), int(offs[bounds[j + 1]])) for j in range(len(bounds) - 1)]
+
+
+def _compare(fb, orc, spec, params, feats, labels, sched, policy="iter_fisher", B=1, replay=False, precision="fp32"):
+    opt = fb.PipelineTrainOptions(policy=policy, replay=replay, replay_seed=3, micro_batch=B, precision=precision)
+    tr = fb.PipelineTrainer(spec, params, sched.bounds, opt)
+    log = tr.run(sched.events, feats, labels)
+    got = tr.params()
+    tr.close()
+    ref = orc.train_conv(spec.geom, spec.acts, params, sched.bounds, sched.events, feats, labels, policy=policy,
+                         replay=replay, replay_seed=3, micro_batch=B)
+    assert np.linalg.norm(ref["params"] - params) / np.linalg.norm(params) > 1e-4  # training moved them
+    if precision == "fp32":
+        for j, (lo, hi) in enumerate(_slices(spec, sched.bounds)):
+            rel = np.linalg.norm(got[lo:hi] - ref["params"][lo:hi]) / np.linalg.norm(ref["params"][lo:hi])
+            assert rel < PARAM_RTOL, f"stage {j}: param rel err {rel:.3e}"
+        flips = np.count_nonzero(log["predicted"] != ref["log"]["predicted"])
+        assert flips <= max(2, 0.005 * len(log)), f"{flips} prediction flips"
+    else:
+        assert np.all(np.isfinite(got))
+    assert abs(fb.online_accuracy(log) - fb.online_accuracy(ref["log"])) <= OACC_TOL
+    assert np.array_equal(log["outcome"] == 2, ref["log"]["outcome"] == 2)
+    assert np.array_equal(log["label"], ref["log"]["label"])
+    return got, ref
+
+
+def test_resnet_four_stages_replay(gpu, fb, orc):
+    """ResNet-18 layout (2+2+2+2 basic blocks, option-A shortcuts) at width 8, 4 stages cut
+    between blocks, iter_fisher, ER replay, micro-batch 1 (the reference's unit)."""
+    spec, params, feats, labels, sched = _setup(fb, 8, (2, 2, 2, 2), 100, 1)
+    assert len(sched.bounds) == 5
+    _compare(fb, orc, spec, params, feats, labels, sched, replay=True)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_resnet_micro_batch(gpu, fb, orc, precision):
+    spec, params, feats, labels, sched = _setup(fb, 8, (1, 1, 1, 1), 50, 4)
+    _compare(fb, orc, spec, params, feats, labels, sched, B=4, replay=True, precision=precision)
+
+
+@pytest.mark.parametrize("policy", ["none", "gap", "fisher"])
+def test_resnet_policies_two_stages(gpu, fb, orc, policy):
+    spec, params, feats, labels, sched = _setup(fb, 4, (1, 1), 80, 2, n_stages=2, in_chw=(3, 16, 16))
+    _compare(fb, orc, spec, params, feats, labels, sched, policy=policy, B=2)
+
+
+def test_conv_kernels_bitwise_deterministic(gpu, fb):
+    """Split-K partials are reduced in split order: two runs give identical bits."""
+    spec, params, feats, labels, sched = _setup(fb, 16, (1, 1, 1, 1), 24, 8)
+    outs = []
+    for _ in range(2):
+        tr = fb.PipelineTrainer(spec, params, sched.bounds,
+                                fb.PipelineTrainOptions(policy="iter_fisher", replay=True, micro_batch=8))
+        log = tr.run(sched.events, feats, labels)
+        outs.append((tr.params(), log["predicted"].copy()))
+        tr.close()
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
