@@ -1,0 +1,4 @@
+timeout 600 python -m pytest tests/test_gpu_conv.py -x -q > gpurun_out/conv_tests.log 2>&1; echo exit=$? >> gpurun_out/conv_tests.log
+for p in fp32 tf32 bf16; do timeout 300 python profiles/c3_resnet.py --prec $p --out gpurun_out/c3_$p.json > gpurun_out/c3_$p.log 2>&1; done
+tail -3 gpurun_out/conv_tests.log
+for f in fp32 tf32 bf16; do python -c "import json;r=json.load(open(\"gpurun_out/c3_$f.json\"));print(\"$f\", round(r[\"samples_per_s\"]), round(r[\"tflops\"],1), r[\"oacc_last_chunk\"], {k:round(v[\"ms\"],1) for k,v in r[\"classes\"].items()}, r[\"critical_ms\"])"; done

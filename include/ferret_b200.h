@@ -411,6 +411,17 @@ FERRET_API ferret_status ferret_dense_layer(int32_t precision, int32_t direction
                                             const float* X, const float* mask, int32_t B, int32_t in, int32_t out,
                                             int32_t relu, float* Y);
 
+/* One convolution (FERRET_LAYER_CONV geometry, 9 ints) on B samples, host
+ * buffers in and out (unit checks of the conv kernels). tc: 0 SIMT fp32,
+ * 1 tcgen05 tf32, 2 tcgen05 bf16, 3 tcgen05 3xTF32. mode 0 forward
+ * Y = act(W * X + b + shortcut(res: B x rc x rh x rw)); mode 1 input gradient
+ * Y = mask * (W^T * D + skip(res: the residual layer's delta, B x rc x rh x rw));
+ * mode 2 weight gradient Y = D (x) im2col(X) (c_out x c_in*k*k). */
+FERRET_API ferret_status ferret_conv_layer(int32_t tc, int32_t mode, const int32_t* geom, int32_t B, const float* W,
+                                           const float* bias, const float* X, const float* D, const float* res,
+                                           int32_t rc, int32_t rh, int32_t rw, const float* mask, int32_t relu,
+                                           float* Y);
+
 #ifdef __cplusplus
 }
 #endif

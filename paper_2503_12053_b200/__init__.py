@@ -9,7 +9,7 @@ from .ferret import (  # noqa: F401
     BoundError, ConfigError, DeviceError, LogicError, SchemaError,
     PipelineTrainOptions, PipelineTrainer, Schedule, StreamSpec,
     PRECISIONS, StaleHarness, apply_skip_policy, load_csv_stream, train_sequential,
-    compensate, dense_layer, device_available, lib, make_dense_net, online_accuracy, param_count,
+    compensate, conv_layer, dense_layer, device_available, lib, make_dense_net, online_accuracy, param_count,
     measure_profile, profile_from_widths, synth_drift_stream, train_pipeline,
 )
 from . import convnet  # noqa: F401,E402  (convolutional extension, BASELINE config 3)

@@ -14,6 +14,9 @@
 // order by a second kernel that also runs the epilogue, so results do not depend
 // on scheduling (bitwise reproducible).
 #include "kernels.cuh"
+#include "umma.cuh"
+
+#include <cuda_bf16.h>
 
 #include <algorithm>
 #include <cstring>
@@ -262,6 +265,312 @@ __global__ void __launch_bounds__(NT) ungap_kernel(const PoolMeanArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Tensor-core implicit GEMM (tcgen05): 128 x 128 output tile per CTA, fp32
+// accumulator in 128 TMEM columns. 8 producer warps gather the A and B operands
+// of each 128-byte K atom straight from the activations / weights (the same
+// loaders as the SIMT kernel: the im2col matrix is never written to memory),
+// convert them to the MMA type and store them K-major with the 128-byte swizzle
+// into a 3-stage smem ring; one thread issues the MMAs (M 128, N 128, 4 per atom
+// in tf32 / bf16) and frees each stage with tcgen05.commit. 3xTF32 (the fp32
+// parity mode) splits both operands into tf32 hi + lo parts and issues
+// hi*hi + hi*lo + lo*hi. The epilogue reads TMEM (tcgen05.ld), transposes the
+// tile through smem so that global stores are coalesced along pixels, then runs
+// the SIMT kernel's epilogue (bias / shortcut / ReLU, skip / mask) or writes the
+// split-K partial (reduced in split order by conv_reduce_kernel).
+// ---------------------------------------------------------------------------
+constexpr int kCT = 288;       // warp 0: TMEM + MMA issue; warps 1-8: producers, epilogue
+constexpr int kCP = 256;
+constexpr int kCNst = 3;
+constexpr int kCTile = 16384;  // 128 rows x 128 bytes
+
+template <int ES, bool SPLIT>
+__device__ __forceinline__ void put_chunk(unsigned char* dst, unsigned char* dst_lo, const float* v) {
+    if constexpr (ES == 4) {
+        if constexpr (SPLIT) {
+            const float4 hi = make_float4(tf32_hi(v[0]), tf32_hi(v[1]), tf32_hi(v[2]), tf32_hi(v[3]));
+            *reinterpret_cast<float4*>(dst) = hi;
+            *reinterpret_cast<float4*>(dst_lo) = make_float4(v[0] - hi.x, v[1] - hi.y, v[2] - hi.z, v[3] - hi.w);
+        } else {
+            *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+        }
+    } else {
+        __nv_bfloat162 h[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(h);
+    }
+}
+
+// Operand gathers of the tensor-core kernel: NE consecutive K elements of one
+// operand row, with the (channel, tap) / (sample, pixel) decomposition done once
+// per atom and advanced incrementally (no per-element integer division).
+template <int MODE, int NE>
+__device__ __forceinline__ void gather_a(const ConvArgs& a, int m, bool ok, int k0, float (&v)[NE]) {
+    if (!ok) {
+#pragma unroll
+        for (int e = 0; e < NE; ++e) v[e] = 0.f;
+        return;
+    }
+    if (MODE == kConvFwd) {  // W row m, contiguous in k
+        const float* w = a.W + (size_t)m * a.K;
+#pragma unroll
+        for (int e = 0; e < NE; ++e) v[e] = k0 + e < a.K ? __ldg(w + k0 + e) : 0.f;
+    } else if (MODE == kConvDgrad) {  // W[co][m][tap], k = co * kk + tap
+        const int kk = a.k * a.k;
+        const int co = k0 / kk;
+        int r = k0 - co * kk;
+        const float* w = a.W + ((size_t)co * a.ci + m) * kk;
+        const size_t jump = (size_t)a.ci * kk;
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+            v[e] = k0 + e < a.K ? __ldg(w + r) : 0.f;
+            if (++r == kk) {
+                r = 0;
+                w += jump;
+            }
+        }
+    } else {  // delta[b][m][pix], k = b * HWo + pix
+        const int hw = a.ho * a.wo;
+        const int b = k0 / hw;
+        int pix = k0 - b * hw;
+        const float* d = a.D + ((size_t)b * a.co + m) * hw;
+        const size_t jump = (size_t)a.co * hw;
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+            v[e] = k0 + e < a.K ? __ldg(d + pix) : 0.f;
+            if (++pix == hw) {
+                pix = 0;
+                d += jump;
+            }
+        }
+    }
+}
+
+template <int MODE, int NE>
+__device__ __forceinline__ void gather_b(const ConvArgs& a, const Col& c, int k0, float (&v)[NE]) {
+    if (!c.ok) {
+#pragma unroll
+        for (int e = 0; e < NE; ++e) v[e] = 0.f;
+        return;
+    }
+    if (MODE == kConvFwd || MODE == kConvDgrad) {
+        // k = ch * kk + kh * k + kw (fwd: ch = c_in of x; dgrad: ch = c_out of delta)
+        const int kk = a.k * a.k;
+        int ch = k0 / kk;
+        const int r = k0 - ch * kk;
+        int kh = r / a.k, kw = r - kh * a.k;
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+            float x = 0.f;
+            if (k0 + e < a.K) {
+                if (MODE == kConvFwd) {
+                    const int ih = c.y * a.s - a.p + kh, iw = c.x * a.s - a.p + kw;
+                    if ((unsigned)ih < (unsigned)a.hi && (unsigned)iw < (unsigned)a.wi)
+                        x = __ldg(c.row + ((size_t)ch * a.hi + ih) * a.wi + iw);
+                } else {
+                    int th = c.y + a.p - kh, tw = c.x + a.p - kw;
+                    bool in = th >= 0 && tw >= 0;
+                    if (a.s == 2) {
+                        in = in && !((th | tw) & 1);
+                        th >>= 1;
+                        tw >>= 1;
+                    } else if (a.s != 1) {
+                        in = in && th % a.s == 0 && tw % a.s == 0;
+                        th /= a.s;
+                        tw /= a.s;
+                    }
+                    if (in && th < a.ho && tw < a.wo) x = __ldg(c.row + ((size_t)ch * a.ho + th) * a.wo + tw);
+                }
+            }
+            v[e] = x;
+            if (++kw == a.k) {
+                kw = 0;
+                if (++kh == a.k) {
+                    kh = 0;
+                    ++ch;
+                }
+            }
+        }
+    } else {  // wgrad: column (ci, kh, kw) fixed; k = b * HWo + oh * wo + ow
+        const int hw = a.ho * a.wo;
+        int b = k0 / hw;
+        const int pix = k0 - b * hw;
+        int oh = pix / a.wo, ow = pix - oh * a.wo;
+        const size_t in_w = (size_t)a.ci * a.hi * a.wi;
+        const size_t coff = (size_t)c.ci * a.hi * a.wi;
+        auto rowp = [&](int bb) {
+            return a.X + (a.xidx ? (size_t)__ldg(a.xidx + bb) : (size_t)bb) * in_w + coff;
+        };
+        const float* row = b < a.B ? rowp(b) : a.X;
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+            float x = 0.f;
+            if (k0 + e < a.K) {
+                const int ih = oh * a.s - a.p + c.kh, iw = ow * a.s - a.p + c.kw;
+                if ((unsigned)ih < (unsigned)a.hi && (unsigned)iw < (unsigned)a.wi) x = __ldg(row + (size_t)ih * a.wi + iw);
+            }
+            v[e] = x;
+            if (++ow == a.wo) {
+                ow = 0;
+                if (++oh == a.ho) {
+                    oh = 0;
+                    if (++b < a.B) row = rowp(b);
+                }
+            }
+        }
+    }
+}
+
+template <int MODE, int ES, bool SPLIT>
+__global__ void __launch_bounds__(kCT, SPLIT ? 1 : 2) conv_mma_kernel(const __grid_constant__ ConvArgs a) {
+    constexpr int KA = 128 / ES;  // K elements per atom
+    constexpr int UK = 32 / ES;   // K per MMA
+    constexpr int CE = 16 / ES;   // elements per 16-byte chunk
+    constexpr bool TF32 = ES == 4;
+    constexpr int STAGE = kCTile * 2 * (SPLIT ? 2 : 1);  // A, B (then A lo, B lo)
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(base + kCNst * STAGE);
+    uint64_t* empty = full + kCNst;
+    uint64_t* done = empty + kCNst;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m0 = blockIdx.y * 128, n0 = blockIdx.x * 128;
+    const int katoms = (a.K + KA - 1) / KA;
+    const int a_lo = blockIdx.z * a.apc;
+    const int na = max(0, min(katoms, a_lo + a.apc) - a_lo);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kCNst; ++s) {
+            mbar_init(full + s, kCP);
+            mbar_init(empty + s, 1);
+        }
+        mbar_init(done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0 && na > 0) {
+            // instruction descriptor: D f32, A/B tf32 (2) or bf16 (1), both K-major, N >> 3, M >> 4
+            const uint32_t fmt = TF32 ? 2u : 1u;
+            const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+            for (int i = 0; i < na; ++i) {
+                const int s = i % kCNst;
+                mbar_wait(full + s, (i / kCNst) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t abase = smem_u32(base + s * STAGE);
+                const uint32_t bbase = abase + kCTile;
+#pragma unroll
+                for (int k = 0; k < KA / UK; ++k) {
+                    const uint64_t ad = smem_desc(abase + k * 32, 16, 1024);
+                    const uint64_t bd = smem_desc(bbase + k * 32, 16, 1024);
+                    umma(tmem, ad, bd, idesc, (i > 0 || k > 0) ? 1u : 0u, TF32);
+                    if constexpr (SPLIT) {  // + hi_A lo_B + lo_A hi_B
+                        umma(tmem, ad, smem_desc(bbase + 2 * kCTile + k * 32, 16, 1024), idesc, 1u, TF32);
+                        umma(tmem, smem_desc(abase + 2 * kCTile + k * 32, 16, 1024), bd, idesc, 1u, TF32);
+                    }
+                }
+                umma_commit(empty + s);
+            }
+            umma_commit(done);
+        }
+    } else {
+        // ---- producers: thread t owns operand row r (A: output row m0 + r; B: GEMM
+        // column n0 + r) and 16-byte chunks jh .. jh + 3 of every atom
+        const int t = threadIdx.x - 32, r = t >> 1, jh = (t & 1) * 4;
+        const bool arow = m0 + r < a.M;
+        const Col col = make_col<MODE>(a, n0 + r);
+        const int sw = r & 7;
+        const int rbase = (r >> 3) * 1024 + (r & 7) * 128;
+        for (int i = 0; i < na; ++i) {
+            const int s = i % kCNst;
+            if (i >= kCNst) mbar_wait(empty + s, ((i / kCNst) - 1) & 1);
+            unsigned char* sa = base + s * STAGE;
+            unsigned char* sb = sa + kCTile;
+            const int k0 = (a_lo + i) * KA + jh * CE;  // the thread's 4 chunks are 4 * CE consecutive k
+            float v[4 * CE];
+            gather_a<MODE, 4 * CE>(a, m0 + r, arow, k0, v);
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                const int off = rbase + (((jh + jj) ^ sw) << 4);
+                put_chunk<ES, SPLIT>(sa + off, sa + 2 * kCTile + off, v + jj * CE);
+            }
+            gather_b<MODE, 4 * CE>(a, col, k0, v);
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                const int off = rbase + (((jh + jj) ^ sw) << 4);
+                put_chunk<ES, SPLIT>(sb + off, sb + 2 * kCTile + off, v + jj * CE);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(full + s)) : "memory");
+        }
+        // ---- epilogue: warps 1-4 move the accumulator (TMEM lane quadrant warp % 4)
+        // into a padded smem tile; then all producers store it along pixels
+        float* T = reinterpret_cast<float*>(base);  // 128 x 129 floats, over the drained ring
+        if (warp <= 4) {
+            const int q = warp & 3, row = q * 32 + lane;
+            if (na > 0) {
+                mbar_wait(done, 0);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    float v[16];
+                    tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + c * 16, v);
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) T[row * 129 + c * 16 + e] = v[e];
+                }
+            } else {
+                for (int c = 0; c < 128; ++c) T[row * 129 + c] = 0.f;
+            }
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        for (int idx = t; idx < 128 * 128; idx += kCP) {
+            const int mm = idx >> 7, nn = idx & 127;
+            const int m = m0 + mm, n = n0 + nn;
+            if (m >= a.M || n >= a.N) continue;
+            const float v = T[mm * 129 + nn];
+            if (a.splits > 1)
+                a.partial[((size_t)blockIdx.z * a.M + m) * a.N + n] = v;
+            else
+                epilogue<MODE>(a, m, n, v);
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+    }
+}
+
+template <int MODE, int ES, bool SPLIT>
+const void* conv_mma_func(size_t& smem) {
+    smem = (size_t)kCNst * kCTile * 2 * (SPLIT ? 2 : 1) + 1024 + 128;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(reinterpret_cast<const void*>(&conv_mma_kernel<MODE, ES, SPLIT>),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    return reinterpret_cast<const void*>(&conv_mma_kernel<MODE, ES, SPLIT>);
+}
+
+template <int MODE>
+const void* conv_mma_pick(int tc, size_t& smem) {
+    return tc == 1 ? conv_mma_func<MODE, 4, false>(smem) : tc == 2 ? conv_mma_func<MODE, 2, false>(smem)
+                                                              : conv_mma_func<MODE, 4, true>(smem);
+}
+
 }  // namespace
 
 size_t conv_plan(ConvArgs& a, int mode, size_t max_partial) {
@@ -279,6 +588,20 @@ size_t conv_plan(ConvArgs& a, int mode, size_t max_partial) {
         a.N = a.ci * kk;
         a.K = a.B * a.ho * a.wo;
     }
+    if (a.tc) {  // tensor cores: 128 x 128 tiles, K in 128-byte atoms, about one wave of CTAs
+        const int KA = a.tc == 2 ? 64 : 32;
+        const long long katoms = (a.K + KA - 1) / KA;
+        const long long mt = (long long)((a.M + 127) / 128) * ((a.N + 127) / 128);
+        const long long wave = a.tc == 3 ? 148 : 296;  // CTAs resident at once (smem: 1 or 2 per SM)
+        long long sp = std::max<long long>(1, (wave + mt - 1) / mt);
+        sp = std::min<long long>(sp, std::max<long long>(1, katoms / 2));
+        const long long mn2 = (long long)a.M * a.N;
+        if (max_partial) sp = std::min<long long>(sp, std::max<long long>(1, (long long)max_partial / mn2));
+        a.apc = (int)((katoms + sp - 1) / sp);
+        a.splits = (int)((katoms + a.apc - 1) / a.apc);
+        a.kchunk = a.apc * KA;
+        return a.splits > 1 ? (size_t)a.splits * (size_t)mn2 : 0;
+    }
     const long long tiles = (long long)((a.M + TM - 1) / TM) * ((a.N + TN - 1) / TN);
     // about two waves of CTAs over the 148 SMs, each split at least 4 k-tiles deep
     long long splits = std::max<long long>(1, (296 + tiles - 1) / tiles);
@@ -292,11 +615,20 @@ size_t conv_plan(ConvArgs& a, int mode, size_t max_partial) {
 }
 
 int spec_conv(const ConvArgs& a, int mode, KernelSpec& gemm, KernelSpec& reduce) {
-    const dim3 grid((a.N + TN - 1) / TN, (a.M + TM - 1) / TM, a.splits);
-    const void* g = mode == kConvFwd     ? reinterpret_cast<const void*>(&conv_gemm_kernel<kConvFwd>)
-                    : mode == kConvDgrad ? reinterpret_cast<const void*>(&conv_gemm_kernel<kConvDgrad>)
-                                         : reinterpret_cast<const void*>(&conv_gemm_kernel<kConvWgrad>);
-    fill_spec(gemm, g, grid, dim3(NT), a);
+    if (a.tc) {
+        size_t smem = 0;
+        const void* g = mode == kConvFwd     ? conv_mma_pick<kConvFwd>(a.tc, smem)
+                        : mode == kConvDgrad ? conv_mma_pick<kConvDgrad>(a.tc, smem)
+                                             : conv_mma_pick<kConvWgrad>(a.tc, smem);
+        fill_spec(gemm, g, dim3((a.N + 127) / 128, (a.M + 127) / 128, a.splits), dim3(kCT), a);
+        gemm.smem = smem;
+    } else {
+        const dim3 grid((a.N + TN - 1) / TN, (a.M + TM - 1) / TM, a.splits);
+        const void* g = mode == kConvFwd     ? reinterpret_cast<const void*>(&conv_gemm_kernel<kConvFwd>)
+                        : mode == kConvDgrad ? reinterpret_cast<const void*>(&conv_gemm_kernel<kConvDgrad>)
+                                             : reinterpret_cast<const void*>(&conv_gemm_kernel<kConvWgrad>);
+        fill_spec(gemm, g, grid, dim3(NT), a);
+    }
     if (a.splits <= 1) return 1;
     const void* r = mode == kConvFwd     ? reinterpret_cast<const void*>(&conv_reduce_kernel<kConvFwd>)
                     : mode == kConvDgrad ? reinterpret_cast<const void*>(&conv_reduce_kernel<kConvDgrad>)

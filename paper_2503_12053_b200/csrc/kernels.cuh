@@ -298,6 +298,10 @@ struct ConvArgs {
     int B, ci, hi, wi, co, ho, wo, k, s, p;
     int M, N, K, splits, kchunk;
     float* partial;      // splits x M x N (splits > 1)
+    // tensor cores (conv_mma_kernel): 0 = SIMT FFMA; 1 = tcgen05 kind::tf32; 2 = kind::f16
+    // on bf16 operands; 3 = 3xTF32 (fp32-accurate: the fp32 parity mode)
+    int tc;
+    int apc;             // tensor-core path: 128-byte K atoms per split
 };
 enum { kConvFwd = 0, kConvDgrad = 1, kConvWgrad = 2 };
 // fills M, N, K, splits, kchunk for the op; returns the partial floats needed

@@ -1690,8 +1690,13 @@ struct ferret_trainer {
     // ------------------------------------------------ convolutions (conv.cu)
     static constexpr size_t kConvPartialCap = size_t{1} << 22;  // split-K partial floats per scratch region
     std::map<uint64_t, float*> conv_scratch;
+    // convolutions on the tensor cores: fp32 parity mode 3xTF32, fast modes tf32 / bf16;
+    // FERRET_CONV_TC overrides (0 = the SIMT kernels)
+    int conv_tc = std::getenv("FERRET_CONV_TC") ? std::atoi(std::getenv("FERRET_CONV_TC")) : -1;
     fb200::ConvArgs conv_args(const LayerDev& ld) const {
         fb200::ConvArgs c{};
+        c.tc = conv_tc >= 0 ? conv_tc
+               : opt.precision == FERRET_PREC_BF16 ? 2 : opt.precision == FERRET_PREC_TF32 ? 1 : 3;
         c.B = B;
         c.ci = ld.ci;
         c.hi = ld.hi;
@@ -3124,6 +3129,69 @@ ferret_status ferret_dense_layer(int32_t precision, int32_t direction, const flo
             }
         }
         cuda_check(cudaMemcpy(Y, L.Y, ny * 4, cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
+ferret_status ferret_conv_layer(int32_t tc, int32_t mode, const int32_t* geom, int32_t B, const float* W,
+                                const float* bias, const float* X, const float* D, const float* res, int32_t rc,
+                                int32_t rh, int32_t rw, const float* mask, int32_t relu, float* Y) {
+    return guarded([&] {
+        if (tc < 0 || tc > 3) fail(FERRET_E_CONFIG, "conv_layer: tc must lie in [0, 3]");
+        if (mode < 0 || mode > 2) fail(FERRET_E_INVALID_ARG, "conv_layer: mode must be 0 (fwd), 1 (dgrad) or 2 (wgrad)");
+        if (!geom || !W || !Y || B < 1) fail(FERRET_E_INVALID_ARG, "conv_layer: null buffer or empty batch");
+        if (geom[0] != FERRET_LAYER_CONV) fail(FERRET_E_CONFIG, "conv_layer: geometry kind must be FERRET_LAYER_CONV");
+        require_device(0);
+        fb200::ConvArgs c{};
+        c.B = B;
+        c.ci = geom[1];
+        c.hi = geom[2];
+        c.wi = geom[3];
+        c.co = geom[4];
+        c.k = geom[5];
+        c.s = geom[6];
+        c.p = geom[7];
+        c.ho = (c.hi + 2 * c.p - c.k) / c.s + 1;
+        c.wo = (c.wi + 2 * c.p - c.k) / c.s + 1;
+        if (c.ci < 1 || c.co < 1 || c.k < 1 || c.s < 1 || c.p < 0 || c.ho < 1 || c.wo < 1)
+            fail(FERRET_E_CONFIG, "conv_layer: bad geometry");
+        c.tc = tc;
+        c.relu = relu;
+        c.rc = rc;
+        c.rh = rh;
+        c.rw = rw;
+        const size_t nw = static_cast<size_t>(c.co) * c.ci * c.k * c.k;
+        const size_t nin = static_cast<size_t>(B) * c.ci * c.hi * c.wi, nout = static_cast<size_t>(B) * c.co * c.ho * c.wo;
+        const size_t nres = static_cast<size_t>(B) * rc * rh * rw;
+        const size_t ny = mode == fb200::kConvFwd ? nout : mode == fb200::kConvDgrad ? nin : nw;
+        size_t bytes = 0;
+        std::vector<void*> bufs;
+        struct Cleanup {
+            std::vector<void*>& b;
+            ~Cleanup() {
+                for (void* p : b) cudaFree(p);
+            }
+        } cleanup{bufs};
+        auto up = [&](const void* src, size_t n) -> float* {
+            float* d = dalloc<float>(std::max<size_t>(n, 1), bytes);
+            bufs.push_back(d);
+            if (src) cuda_check(cudaMemcpy(d, src, n * 4, cudaMemcpyHostToDevice), "H2D");
+            return d;
+        };
+        c.W = up(W, nw);
+        if (mode == fb200::kConvFwd) c.bias = up(bias, static_cast<size_t>(c.co));
+        if (mode != fb200::kConvDgrad) c.X = up(X, nin);
+        if (mode != fb200::kConvFwd) c.D = up(D, nout);
+        if (res && mode != fb200::kConvWgrad) c.res = up(res, nres);
+        if (mask && mode == fb200::kConvDgrad) c.mask = up(mask, nin);
+        c.Y = up(nullptr, ny);
+        const size_t part = fb200::conv_plan(c, mode, 0);
+        if (part) c.partial = up(nullptr, part);
+        fb200::KernelSpec g, r;
+        const int n = fb200::spec_conv(c, mode, g, r);
+        cuda_check(fb200::launch_spec(g, nullptr), "conv_layer launch");
+        if (n == 2) cuda_check(fb200::launch_spec(r, nullptr), "conv_layer reduce");
+        cuda_check(cudaDeviceSynchronize(), "conv_layer");
+        cuda_check(cudaMemcpy(Y, c.Y, ny * 4, cudaMemcpyDeviceToHost), "D2H");
     });
 }
 

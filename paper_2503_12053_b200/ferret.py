@@ -163,6 +163,8 @@ def lib() -> C.CDLL:
         "ferret_csv_destroy": (None, [C.c_void_p]),
         "ferret_apply_skip_policy": (C.c_int, [C.c_size_t, D, C.c_int32, C.c_uint64, C.c_uint64, C.c_uint64, D,
                                                P(C.c_int64), P(D), P(C.c_size_t)]),
+        "ferret_conv_layer": (C.c_int, [C.c_int32, C.c_int32, C.c_void_p, C.c_int32] + [C.c_void_p] * 5 +
+                              [C.c_int32] * 3 + [C.c_void_p, C.c_int32, C.c_void_p]),
         "ferret_dense_layer": (C.c_int, [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                          C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]),
         "ferret_trainer_save_state": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, P(C.c_size_t)]),
@@ -759,3 +761,19 @@ def measure_profile(widths: Sequence[int], micro_batch: int = 1, policy: str = "
     out["t_f"] = np.maximum(f, 1e-3) * 1e-6
     out["t_b"] = np.maximum(b + u, 1e-3) * 1e-6
     return out
+
+
+def conv_layer(tc: int, mode: int, geom, B: int, W, bias=None, X=None, D=None, res=None, res_chw=(0, 0, 0),
+               mask=None, relu: int = 0) -> np.ndarray:
+    """One convolution on the device (ferret_conv_layer): mode 0 forward, 1 input gradient,
+    2 weight gradient; tc 0 SIMT, 1 tf32, 2 bf16, 3 3xTF32 tensor cores. Host fp32 arrays."""
+    g = np.ascontiguousarray(geom, dtype=np.int32)
+    _, ci, hi, wi, co, k, st, p, _ = (int(v) for v in g)
+    ho, wo = (hi + 2 * p - k) // st + 1, (wi + 2 * p - k) // st + 1
+    n = {0: B * co * ho * wo, 1: B * ci * hi * wi, 2: co * ci * k * k}[mode]
+    Y = np.empty(n, dtype=np.float32)
+    keep = [np.ascontiguousarray(a, dtype=np.float32) if a is not None else None for a in (W, bias, X, D, res, mask)]
+    ptr = [a.ctypes.data if a is not None else None for a in keep]
+    _check(lib().ferret_conv_layer(tc, mode, g.ctypes.data, B, ptr[0], ptr[1], ptr[2], ptr[3], ptr[4],
+                                   int(res_chw[0]), int(res_chw[1]), int(res_chw[2]), ptr[5], relu, Y.ctypes.data))
+    return Y

@@ -25,7 +25,7 @@ sys.path.insert(0, ROOT)
 
 
 def measure(fb, torch, units=32, steps=3, warmup=2, width=64, micro_batch=16, replay=True, device=0,
-            profile=True) -> dict:
+            profile=True, precision="fp32") -> dict:
     cn = fb.convnet
     spec = cn.resnet_cifar(width=width)
     bounds = cn.balanced_bounds(spec, 4)
@@ -37,7 +37,7 @@ def measure(fb, torch, units=32, steps=3, warmup=2, width=64, micro_batch=16, re
     feats, labels = fb.synth_drift_stream(n_chunks * chunk, spec.in_width(0), 10, "split_tasks", 7)
     tr = fb.PipelineTrainer(spec, cn.make_conv_net(spec, 1), bounds,
                             fb.PipelineTrainOptions(policy="iter_fisher", micro_batch=micro_batch, device=device,
-                                                    replay=replay, replay_seed=3))
+                                                    replay=replay, replay_seed=3, precision=precision))
     tr.load_stream(feats, labels)
     tr.set_schedule(sched.events, chunk)
     for c in range(warmup):
@@ -58,7 +58,8 @@ def measure(fb, torch, units=32, steps=3, warmup=2, width=64, micro_batch=16, re
         ms += a.elapsed_time(b)
     st = tr.stats()
     out = {"workload": f"C3: ResNet-18-style CNN (width {width}, {spec.n_params / 1e6:.2f} M params) on 3x32x32, "
-                       f"4 stages {bounds}, iter_fisher, ER replay, micro-batch {micro_batch}, fp32",
+                       f"4 stages {bounds}, iter_fisher, ER replay, micro-batch {micro_batch}, {precision}"
+                       f" (conv path {os.environ.get('FERRET_CONV_TC', 'default')})",
            "samples_per_s": chunk * steps / (ms / 1e3), "ms_per_chunk": ms / steps, "samples_per_chunk": chunk,
            "bounds": bounds, "n_params": spec.n_params, "macs_per_sample": spec.macs,
            "replays_per_chunk": st["replays"], "device_gb": st["device_bytes"] / 1e9}
@@ -85,12 +86,14 @@ def main():
     ap.add_argument("--width", type=int, default=64)
     ap.add_argument("--micro-batch", type=int, default=16)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--prec", default="fp32")
     args = ap.parse_args()
     import torch
 
     import paper_2503_12053_b200 as fb
 
-    r = measure(fb, torch, units=args.units, steps=args.steps, width=args.width, micro_batch=args.micro_batch)
+    r = measure(fb, torch, units=args.units, steps=args.steps, width=args.width, micro_batch=args.micro_batch,
+                precision=args.prec)
     print(json.dumps(r))
     if args.out:
         with open(args.out, "w") as f:

@@ -87,3 +87,82 @@ def test_conv_kernels_bitwise_deterministic(gpu, fb):
         outs.append((tr.params(), log["predicted"].copy()))
         tr.close()
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+# ---------------------------------------------------------------- kernel units
+def _im2col(x, k, s, p, ho, wo):
+    B, c, h, w = x.shape
+    xp = np.zeros((B, c, h + 2 * p, w + 2 * p))
+    xp[:, :, p:p + h, p:p + w] = x
+    cols = np.empty((B, c, k, k, ho, wo))
+    for kh in range(k):
+        for kw in range(k):
+            cols[:, :, kh, kw] = xp[:, :, kh:kh + s * ho:s, kw:kw + s * wo:s]
+    return cols.reshape(B, c * k * k, ho * wo)
+
+
+def _col2im(cols, shape, k, s, p, ho, wo):
+    B, c, h, w = shape
+    xp = np.zeros((B, c, h + 2 * p, w + 2 * p))
+    cols = cols.reshape(B, c, k, k, ho, wo)
+    for kh in range(k):
+        for kw in range(k):
+            xp[:, :, kh:kh + s * ho:s, kw:kw + s * wo:s] += cols[:, :, kh, kw]
+    return xp[:, :, p:p + h, p:p + w]
+
+
+TOL = {0: 2e-6, 3: 2e-6, 1: 3e-3, 2: 1.5e-2}
+
+
+@pytest.mark.parametrize("tc", [0, 1, 2, 3])
+@pytest.mark.parametrize("shape", [(16, 9, 9, 24, 3, 2, 1), (40, 8, 8, 40, 3, 1, 1), (3, 12, 12, 20, 3, 1, 1)])
+def test_conv_layer_kernels(gpu, fb, tc, shape):
+    """fwd (bias, option-A / identity shortcut, ReLU), input gradient (skip + ReLU mask) and
+    weight gradient of one convolution on each kernel path against numpy fp64."""
+    ci, hi, wi, co, k, s, p = shape
+    B = 3
+    ho, wo = (hi + 2 * p - k) // s + 1, (wi + 2 * p - k) // s + 1
+    geom = [cn.CONV, ci, hi, wi, co, k, s, p, 0]
+    rng = np.random.default_rng(5)
+    W = rng.standard_normal((co, ci * k * k)).astype(np.float32)
+    b = rng.standard_normal(co).astype(np.float32)
+    X = rng.standard_normal((B, ci, hi, wi)).astype(np.float32)
+    D = rng.standard_normal((B, co, ho, wo)).astype(np.float32)
+    cols = _im2col(X.astype(np.float64), k, s, p, ho, wo)
+    W64 = W.astype(np.float64)
+    # forward with a shortcut from a block input (B, rc <= co, ho*st, wo*st)
+    st = 2
+    rc = min(ci, co)
+    R = rng.standard_normal((B, rc, ho * st, wo * st)).astype(np.float32)
+    ref = np.einsum("ok,bkp->bop", W64, cols).reshape(B, co, ho, wo) + b[None, :, None, None]
+    ref[:, :rc] += R[:, :, ::st, ::st]
+    ref = np.maximum(ref, 0)
+    got = fb.conv_layer(tc, 0, geom, B, W, bias=b, X=X, res=R, res_chw=(rc, ho * st, wo * st), relu=1)
+    assert np.linalg.norm(got - ref.ravel()) / np.linalg.norm(ref) < TOL[tc]
+    # weight gradient
+    ref_g = np.einsum("bop,bkp->ok", D.reshape(B, co, -1).astype(np.float64), cols)
+    got_g = fb.conv_layer(tc, 2, geom, B, W, X=X, D=D)
+    assert np.linalg.norm(got_g - ref_g.ravel()) / np.linalg.norm(ref_g) < TOL[tc]
+    # input gradient + skip of a residual layer above (its delta on a map subsampled by 2) + mask
+    dcols = np.einsum("ok,bop->bkp", W64, D.reshape(B, co, -1).astype(np.float64))
+    ref_d = _col2im(dcols, X.shape, k, s, p, ho, wo)
+    rh, rw = (hi + 1) // 2, (wi + 1) // 2
+    if hi % 2 == 0:
+        Dr = rng.standard_normal((B, ci + 2, rh, rw)).astype(np.float32)
+        ref_d[:, :, ::2, ::2] += Dr[:, :ci]
+        res, rchw = Dr, (ci + 2, rh, rw)
+    else:
+        res, rchw = None, (0, 0, 0)
+    mask = (rng.random((B, ci, hi, wi)) > 0.3).astype(np.float32)
+    ref_d = ref_d * mask
+    got_d = fb.conv_layer(tc, 1, geom, B, W, D=D, res=res, res_chw=rchw, mask=mask)
+    assert np.linalg.norm(got_d - ref_d.ravel()) / np.linalg.norm(ref_d) < TOL[tc]
+
+
+@pytest.mark.parametrize("tc", [0, 3])
+def test_resnet_parity_each_conv_path(gpu, fb, orc, monkeypatch, tc):
+    """The same C3-shaped replay with the convolutions forced onto the SIMT kernels (0) and
+    onto the 3xTF32 tensor-core kernels (3): both within the parity bar."""
+    monkeypatch.setenv("FERRET_CONV_TC", str(tc))
+    spec, params, feats, labels, sched = _setup(fb, 8, (1, 1, 1, 1), 40, 4)
+    _compare(fb, orc, spec, params, feats, labels, sched, B=4, replay=True)
