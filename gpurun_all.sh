@@ -1,0 +1,7 @@
+timeout 300 python -m pytest tests/test_gpu_conv.py -x -q -k kernels > gpurun_out/conv_unit.log 2>&1; echo exit=$? >> gpurun_out/conv_unit.log; tail -2 gpurun_out/conv_unit.log
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:conv --csv --log-file gpurun_out/conv_probe_ncu.csv python profiles/conv_probe.py --tc 1,2,3 > gpurun_out/conv_probe.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_conv.py -x -q > gpurun_out/conv_tests.log 2>&1; echo exit=$? >> gpurun_out/conv_tests.log
+for p in fp32 tf32 bf16; do timeout 300 python profiles/c3_resnet.py --prec $p --out gpurun_out/c3_$p.json > gpurun_out/c3_$p.log 2>&1; done
+tail -3 gpurun_out/conv_tests.log
+for f in fp32 tf32 bf16; do python -c "import json;r=json.load(open(\"gpurun_out/c3_$f.json\"));print(\"$f\", round(r[\"samples_per_s\"]), round(r[\"tflops\"],1), r[\"oacc_last_chunk\"], {k:round(v[\"ms\"],1) for k,v in r[\"classes\"].items()}, r[\"critical_ms\"])"; done
+python profiles/parse_conv_probe.py gpurun_out/conv_probe_ncu.csv gpurun_out/conv_probe.log > gpurun_out/conv_probe_summary.txt

@@ -19,6 +19,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 namespace fb200 {
@@ -218,10 +219,32 @@ __global__ void __launch_bounds__(NT) conv_gemm_kernel(const ConvArgs a) {
     }
 }
 
-// ordered sum of the K-split partials, then the epilogue
+// ordered sum of the K-split partials, then the epilogue. Few splits: a thread
+// per output, splits in order. Many splits (weight gradients of small layers:
+// up to ~150 partials over few outputs): a warp per output, lane l summing splits
+// l, l+32, ... in order, then a fixed butterfly — deterministic either way.
+constexpr int kWarpReduceSplits = 16;
+constexpr long long kWarpReduceMaxOutputs = 32768;  // larger outputs: coalesced thread-per-output wins
+__host__ __device__ inline bool warp_reduce(const ConvArgs& a) {
+    return a.splits >= kWarpReduceSplits && (long long)a.M * a.N <= kWarpReduceMaxOutputs;
+}
 template <int MODE>
 __global__ void __launch_bounds__(NT) conv_reduce_kernel(const ConvArgs a) {
     const size_t mn = (size_t)a.M * a.N;
+    if (warp_reduce(a)) {
+        const int lane = threadIdx.x & 31;
+        for (size_t i = ((size_t)blockIdx.x * NT + threadIdx.x) >> 5; i < mn; i += ((size_t)gridDim.x * NT) >> 5) {
+            float v = 0.f;
+            for (int s = lane; s < a.splits; s += 32) v += __ldg(a.partial + (size_t)s * mn + i);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) {
+                const int m = (int)(i / a.N), n = (int)(i - (size_t)m * a.N);
+                epilogue<MODE>(a, m, n, v);
+            }
+        }
+        return;
+    }
     for (size_t i = (size_t)blockIdx.x * NT + threadIdx.x; i < mn; i += (size_t)gridDim.x * NT) {
         float v = 0.f;
         for (int s = 0; s < a.splits; ++s) v += __ldg(a.partial + (size_t)s * mn + i);
@@ -279,9 +302,13 @@ __global__ void __launch_bounds__(NT) ungap_kernel(const PoolMeanArgs a) {
 // the SIMT kernel's epilogue (bias / shortcut / ReLU, skip / mask) or writes the
 // split-K partial (reduced in split order by conv_reduce_kernel).
 // ---------------------------------------------------------------------------
-constexpr int kCT = 288;       // warp 0: TMEM + MMA issue; warps 1-8: producers, epilogue
-constexpr int kCP = 256;
-constexpr int kCNst = 3;
+// warp 0: TMEM + MMA issue; warps 1-16: two producer groups of 8 warps taking
+// alternate atoms (two atoms' gathers in flight: the gather is L2-latency bound)
+constexpr int kCG = 2;
+constexpr int kCP = 256;           // producer threads per group (one full atom)
+constexpr int kCT = 32 + kCG * kCP;
+// smem ring depth: 3 x 64 KB (3xTF32: hi + lo operands) or 5 x 32 KB
+__host__ __device__ constexpr int conv_stages(bool split) { return split ? 3 : 5; }
 constexpr int kCTile = 16384;  // 128 rows x 128 bytes
 
 template <int ES, bool SPLIT>
@@ -305,6 +332,66 @@ __device__ __forceinline__ void put_chunk(unsigned char* dst, unsigned char* dst
 // Operand gathers of the tensor-core kernel: NE consecutive K elements of one
 // operand row, with the (channel, tap) / (sample, pixel) decomposition done once
 // per atom and advanced incrementally (no per-element integer division).
+// Tap-major gathers (ConvArgs::kt): k = tap * C + c, C = the channel count of
+// the operand that is summed over (fwd: c_in; dgrad: c_out), C % atom == 0.
+template <int MODE, int NE>
+__device__ __forceinline__ void gather_a_tm(const ConvArgs& a, int m, bool ok, int k0, float (&v)[NE]) {
+    const int kk = a.k * a.k;
+    const int C = MODE == kConvFwd ? a.ci : a.co;
+    const int tap = k0 / C, c0 = k0 - tap * C;
+    if (!ok) {
+#pragma unroll
+        for (int e = 0; e < NE; ++e) v[e] = 0.f;
+        return;
+    }
+    // fwd: W[m][c][tap]; dgrad: W[c][m][tap]
+    const float* w = MODE == kConvFwd ? a.W + ((size_t)m * a.ci + c0) * kk + tap : a.W + ((size_t)c0 * a.ci + m) * kk + tap;
+    const size_t step = MODE == kConvFwd ? (size_t)kk : (size_t)a.ci * kk;
+#pragma unroll
+    for (int e = 0; e < NE; ++e) v[e] = __ldg(w + e * step);
+}
+
+template <int MODE, int NE>
+__device__ __forceinline__ void gather_b_tm(const ConvArgs& a, const Col& c, int k0, float (&v)[NE]) {
+    const int C = MODE == kConvFwd ? a.ci : a.co;
+    const int tap = k0 / C, c0 = k0 - tap * C;
+    const int kh = tap / a.k, kw = tap - kh * a.k;
+    const float* src = nullptr;
+    size_t step = 0;
+    if (c.ok) {
+        if (MODE == kConvFwd) {
+            const int ih = c.y * a.s - a.p + kh, iw = c.x * a.s - a.p + kw;
+            if ((unsigned)ih < (unsigned)a.hi && (unsigned)iw < (unsigned)a.wi) {
+                src = c.row + ((size_t)c0 * a.hi + ih) * a.wi + iw;
+                step = (size_t)a.hi * a.wi;
+            }
+        } else {
+            int th = c.y + a.p - kh, tw = c.x + a.p - kw;
+            bool in = th >= 0 && tw >= 0;
+            if (a.s == 2) {
+                in = in && !((th | tw) & 1);
+                th >>= 1;
+                tw >>= 1;
+            } else if (a.s != 1) {
+                in = in && th % a.s == 0 && tw % a.s == 0;
+                th /= a.s;
+                tw /= a.s;
+            }
+            if (in && th < a.ho && tw < a.wo) {
+                src = c.row + ((size_t)c0 * a.ho + th) * a.wo + tw;
+                step = (size_t)a.ho * a.wo;
+            }
+        }
+    }
+    if (!src) {
+#pragma unroll
+        for (int e = 0; e < NE; ++e) v[e] = 0.f;
+        return;
+    }
+#pragma unroll
+    for (int e = 0; e < NE; ++e) v[e] = __ldg(src + e * step);
+}
+
 template <int MODE, int NE>
 __device__ __forceinline__ void gather_a(const ConvArgs& a, int m, bool ok, int k0, float (&v)[NE]) {
     if (!ok) {
@@ -423,17 +510,18 @@ __device__ __forceinline__ void gather_b(const ConvArgs& a, const Col& c, int k0
 }
 
 template <int MODE, int ES, bool SPLIT>
-__global__ void __launch_bounds__(kCT, SPLIT ? 1 : 2) conv_mma_kernel(const __grid_constant__ ConvArgs a) {
+__global__ void __launch_bounds__(kCT, 1) conv_mma_kernel(const __grid_constant__ ConvArgs a) {
     constexpr int KA = 128 / ES;  // K elements per atom
     constexpr int UK = 32 / ES;   // K per MMA
     constexpr int CE = 16 / ES;   // elements per 16-byte chunk
     constexpr bool TF32 = ES == 4;
     constexpr int STAGE = kCTile * 2 * (SPLIT ? 2 : 1);  // A, B (then A lo, B lo)
+    constexpr int NST = conv_stages(SPLIT);
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(base + kCNst * STAGE);
-    uint64_t* empty = full + kCNst;
-    uint64_t* done = empty + kCNst;
+    uint64_t* full = reinterpret_cast<uint64_t*>(base + NST * STAGE);
+    uint64_t* empty = full + NST;
+    uint64_t* done = empty + NST;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -443,7 +531,7 @@ __global__ void __launch_bounds__(kCT, SPLIT ? 1 : 2) conv_mma_kernel(const __gr
     const int na = max(0, min(katoms, a_lo + a.apc) - a_lo);
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kCNst; ++s) {
+        for (int s = 0; s < NST; ++s) {
             mbar_init(full + s, kCP);
             mbar_init(empty + s, 1);
         }
@@ -465,8 +553,8 @@ __global__ void __launch_bounds__(kCT, SPLIT ? 1 : 2) conv_mma_kernel(const __gr
             const uint32_t fmt = TF32 ? 2u : 1u;
             const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
             for (int i = 0; i < na; ++i) {
-                const int s = i % kCNst;
-                mbar_wait(full + s, (i / kCNst) & 1);
+                const int s = i % NST;
+                mbar_wait(full + s, (i / NST) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t abase = smem_u32(base + s * STAGE);
                 const uint32_t bbase = abase + kCTile;
@@ -487,25 +575,31 @@ __global__ void __launch_bounds__(kCT, SPLIT ? 1 : 2) conv_mma_kernel(const __gr
     } else {
         // ---- producers: thread t owns operand row r (A: output row m0 + r; B: GEMM
         // column n0 + r) and 16-byte chunks jh .. jh + 3 of every atom
-        const int t = threadIdx.x - 32, r = t >> 1, jh = (t & 1) * 4;
+        const int tg = threadIdx.x - 32, grp = tg / kCP, t = tg - grp * kCP, r = t >> 1, jh = (t & 1) * 4;
         const bool arow = m0 + r < a.M;
         const Col col = make_col<MODE>(a, n0 + r);
         const int sw = r & 7;
         const int rbase = (r >> 3) * 1024 + (r & 7) * 128;
-        for (int i = 0; i < na; ++i) {
-            const int s = i % kCNst;
-            if (i >= kCNst) mbar_wait(empty + s, ((i / kCNst) - 1) & 1);
+        for (int i = grp; i < na; i += kCG) {
+            const int s = i % NST;
+            if (i >= NST) mbar_wait(empty + s, ((i / NST) - 1) & 1);
             unsigned char* sa = base + s * STAGE;
             unsigned char* sb = sa + kCTile;
             const int k0 = (a_lo + i) * KA + jh * CE;  // the thread's 4 chunks are 4 * CE consecutive k
             float v[4 * CE];
-            gather_a<MODE, 4 * CE>(a, m0 + r, arow, k0, v);
+            if (MODE != kConvWgrad && a.kt)
+                gather_a_tm<MODE, 4 * CE>(a, m0 + r, arow, k0, v);
+            else
+                gather_a<MODE, 4 * CE>(a, m0 + r, arow, k0, v);
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) {
                 const int off = rbase + (((jh + jj) ^ sw) << 4);
                 put_chunk<ES, SPLIT>(sa + off, sa + 2 * kCTile + off, v + jj * CE);
             }
-            gather_b<MODE, 4 * CE>(a, col, k0, v);
+            if (MODE != kConvWgrad && a.kt)
+                gather_b_tm<MODE, 4 * CE>(a, col, k0, v);
+            else
+                gather_b<MODE, 4 * CE>(a, col, k0, v);
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) {
                 const int off = rbase + (((jh + jj) ^ sw) << 4);
@@ -533,8 +627,8 @@ __global__ void __launch_bounds__(kCT, SPLIT ? 1 : 2) conv_mma_kernel(const __gr
                 for (int c = 0; c < 128; ++c) T[row * 129 + c] = 0.f;
             }
         }
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        for (int idx = t; idx < 128 * 128; idx += kCP) {
+        asm volatile("bar.sync 1, %0;" ::"n"(kCG * kCP) : "memory");
+        for (int idx = tg; idx < 128 * 128; idx += kCG * kCP) {
             const int mm = idx >> 7, nn = idx & 127;
             const int m = m0 + mm, n = n0 + nn;
             if (m >= a.M || n >= a.N) continue;
@@ -555,7 +649,7 @@ __global__ void __launch_bounds__(kCT, SPLIT ? 1 : 2) conv_mma_kernel(const __gr
 
 template <int MODE, int ES, bool SPLIT>
 const void* conv_mma_func(size_t& smem) {
-    smem = (size_t)kCNst * kCTile * 2 * (SPLIT ? 2 : 1) + 1024 + 128;
+    smem = (size_t)conv_stages(SPLIT) * kCTile * 2 * (SPLIT ? 2 : 1) + 1024 + 128;
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(reinterpret_cast<const void*>(&conv_mma_kernel<MODE, ES, SPLIT>),
@@ -592,11 +686,14 @@ size_t conv_plan(ConvArgs& a, int mode, size_t max_partial) {
         const int KA = a.tc == 2 ? 64 : 32;
         const long long katoms = (a.K + KA - 1) / KA;
         const long long mt = (long long)((a.M + 127) / 128) * ((a.N + 127) / 128);
-        const long long wave = a.tc == 3 ? 148 : 296;  // CTAs resident at once (smem: 1 or 2 per SM)
-        long long sp = std::max<long long>(1, (wave + mt - 1) / mt);
+        // one CTA per SM (544 threads): split K only as far as the tiles stay one wave
+        // (splitting a multi-wave grid adds the partial traffic and buys nothing)
+        long long sp = std::max<long long>(1, 148 / mt);
         sp = std::min<long long>(sp, std::max<long long>(1, katoms / 2));
         const long long mn2 = (long long)a.M * a.N;
         if (max_partial) sp = std::min<long long>(sp, std::max<long long>(1, (long long)max_partial / mn2));
+        const int C = mode == kConvFwd ? a.ci : a.co;
+        a.kt = mode != kConvWgrad && C % KA == 0 && !std::getenv("FERRET_CONV_NO_TAPMAJOR");
         a.apc = (int)((katoms + sp - 1) / sp);
         a.splits = (int)((katoms + a.apc - 1) / a.apc);
         a.kchunk = a.apc * KA;
@@ -634,7 +731,8 @@ int spec_conv(const ConvArgs& a, int mode, KernelSpec& gemm, KernelSpec& reduce)
                     : mode == kConvDgrad ? reinterpret_cast<const void*>(&conv_reduce_kernel<kConvDgrad>)
                                          : reinterpret_cast<const void*>(&conv_reduce_kernel<kConvWgrad>);
     const long long mn = (long long)a.M * a.N;
-    fill_spec(reduce, r, dim3((unsigned)std::min<long long>((mn + NT - 1) / NT, 148 * 8)), dim3(NT), a);
+    const long long threads = warp_reduce(a) ? mn * 32 : mn;
+    fill_spec(reduce, r, dim3((unsigned)std::min<long long>((threads + NT - 1) / NT, 148 * 8)), dim3(NT), a);
     return 2;
 }
 

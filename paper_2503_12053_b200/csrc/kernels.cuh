@@ -302,6 +302,9 @@ struct ConvArgs {
     // on bf16 operands; 3 = 3xTF32 (fp32-accurate: the fp32 parity mode)
     int tc;
     int apc;             // tensor-core path: 128-byte K atoms per split
+    int kt;              // tensor-core fwd / dgrad: K ordered (tap, channel) instead of (channel, tap),
+                         // when the channel count is a multiple of the atom: a thread's run of k is
+                         // one tap's consecutive channels (one bounds check, constant address step)
 };
 enum { kConvFwd = 0, kConvDgrad = 1, kConvWgrad = 2 };
 // fills M, N, K, splits, kchunk for the op; returns the partial floats needed
