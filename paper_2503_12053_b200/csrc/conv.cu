@@ -302,57 +302,35 @@ __global__ void __launch_bounds__(NT) ungap_kernel(const PoolMeanArgs a) {
 // the SIMT kernel's epilogue (bias / shortcut / ReLU, skip / mask) or writes the
 // split-K partial (reduced in split order by conv_reduce_kernel).
 // ---------------------------------------------------------------------------
-// warp 0: TMEM + MMA issue; warps 1-16: two producer groups of 8 warps taking
-// alternate atoms (two atoms' gathers in flight: the gather is L2-latency bound)
-constexpr int kCG = 2;
-constexpr int kCP = 256;           // producer threads per group (one full atom)
-constexpr int kCT = 32 + kCG * kCP;
+// warp 0: TMEM + MMA issue; warps 1-8: producers (cp.async gathers), epilogue
+constexpr int kCP = 256;
+constexpr int kCT = 32 + kCP;
 // smem ring depth: 3 x 64 KB (3xTF32: hi + lo operands) or 5 x 32 KB
 __host__ __device__ constexpr int conv_stages(bool split) { return split ? 3 : 5; }
 constexpr int kCTile = 16384;  // 128 rows x 128 bytes
 
-template <int ES, bool SPLIT>
-__device__ __forceinline__ void put_chunk(unsigned char* dst, unsigned char* dst_lo, const float* v) {
-    if constexpr (ES == 4) {
-        if constexpr (SPLIT) {
-            const float4 hi = make_float4(tf32_hi(v[0]), tf32_hi(v[1]), tf32_hi(v[2]), tf32_hi(v[3]));
-            *reinterpret_cast<float4*>(dst) = hi;
-            *reinterpret_cast<float4*>(dst_lo) = make_float4(v[0] - hi.x, v[1] - hi.y, v[2] - hi.z, v[3] - hi.w);
-        } else {
-            *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
-        }
-    } else {
-        __nv_bfloat162 h[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(h);
-    }
-}
-
-// Operand gathers of the tensor-core kernel: NE consecutive K elements of one
-// operand row, with the (channel, tap) / (sample, pixel) decomposition done once
-// per atom and advanced incrementally (no per-element integer division).
-// Tap-major gathers (ConvArgs::kt): k = tap * C + c, C = the channel count of
+// Operand element sources of the tensor-core kernel (nullptr = zero: padding,
+// out of range). Tap-major (ConvArgs::kt): k = tap * C + c, C = the channel count of
 // the operand that is summed over (fwd: c_in; dgrad: c_out), C % atom == 0.
 template <int MODE, int NE>
-__device__ __forceinline__ void gather_a_tm(const ConvArgs& a, int m, bool ok, int k0, float (&v)[NE]) {
+__device__ __forceinline__ void locate_a_tm(const ConvArgs& a, int m, bool ok, int k0, const float* (&P)[NE]) {
     const int kk = a.k * a.k;
     const int C = MODE == kConvFwd ? a.ci : a.co;
     const int tap = k0 / C, c0 = k0 - tap * C;
     if (!ok) {
 #pragma unroll
-        for (int e = 0; e < NE; ++e) v[e] = 0.f;
+        for (int e = 0; e < NE; ++e) P[e] = nullptr;
         return;
     }
     // fwd: W[m][c][tap]; dgrad: W[c][m][tap]
     const float* w = MODE == kConvFwd ? a.W + ((size_t)m * a.ci + c0) * kk + tap : a.W + ((size_t)c0 * a.ci + m) * kk + tap;
     const size_t step = MODE == kConvFwd ? (size_t)kk : (size_t)a.ci * kk;
 #pragma unroll
-    for (int e = 0; e < NE; ++e) v[e] = __ldg(w + e * step);
+    for (int e = 0; e < NE; ++e) P[e] = w + e * step;
 }
 
 template <int MODE, int NE>
-__device__ __forceinline__ void gather_b_tm(const ConvArgs& a, const Col& c, int k0, float (&v)[NE]) {
+__device__ __forceinline__ void locate_b_tm(const ConvArgs& a, const Col& c, int k0, const float* (&P)[NE]) {
     const int C = MODE == kConvFwd ? a.ci : a.co;
     const int tap = k0 / C, c0 = k0 - tap * C;
     const int kh = tap / a.k, kw = tap - kh * a.k;
@@ -385,24 +363,24 @@ __device__ __forceinline__ void gather_b_tm(const ConvArgs& a, const Col& c, int
     }
     if (!src) {
 #pragma unroll
-        for (int e = 0; e < NE; ++e) v[e] = 0.f;
+        for (int e = 0; e < NE; ++e) P[e] = nullptr;
         return;
     }
 #pragma unroll
-    for (int e = 0; e < NE; ++e) v[e] = __ldg(src + e * step);
+    for (int e = 0; e < NE; ++e) P[e] = src + e * step;
 }
 
 template <int MODE, int NE>
-__device__ __forceinline__ void gather_a(const ConvArgs& a, int m, bool ok, int k0, float (&v)[NE]) {
+__device__ __forceinline__ void locate_a(const ConvArgs& a, int m, bool ok, int k0, const float* (&P)[NE]) {
     if (!ok) {
 #pragma unroll
-        for (int e = 0; e < NE; ++e) v[e] = 0.f;
+        for (int e = 0; e < NE; ++e) P[e] = nullptr;
         return;
     }
     if (MODE == kConvFwd) {  // W row m, contiguous in k
         const float* w = a.W + (size_t)m * a.K;
 #pragma unroll
-        for (int e = 0; e < NE; ++e) v[e] = k0 + e < a.K ? __ldg(w + k0 + e) : 0.f;
+        for (int e = 0; e < NE; ++e) P[e] = k0 + e < a.K ? w + k0 + e : nullptr;
     } else if (MODE == kConvDgrad) {  // W[co][m][tap], k = co * kk + tap
         const int kk = a.k * a.k;
         const int co = k0 / kk;
@@ -411,7 +389,7 @@ __device__ __forceinline__ void gather_a(const ConvArgs& a, int m, bool ok, int 
         const size_t jump = (size_t)a.ci * kk;
 #pragma unroll
         for (int e = 0; e < NE; ++e) {
-            v[e] = k0 + e < a.K ? __ldg(w + r) : 0.f;
+            P[e] = k0 + e < a.K ? w + r : nullptr;
             if (++r == kk) {
                 r = 0;
                 w += jump;
@@ -425,7 +403,7 @@ __device__ __forceinline__ void gather_a(const ConvArgs& a, int m, bool ok, int 
         const size_t jump = (size_t)a.co * hw;
 #pragma unroll
         for (int e = 0; e < NE; ++e) {
-            v[e] = k0 + e < a.K ? __ldg(d + pix) : 0.f;
+            P[e] = k0 + e < a.K ? d + pix : nullptr;
             if (++pix == hw) {
                 pix = 0;
                 d += jump;
@@ -435,10 +413,10 @@ __device__ __forceinline__ void gather_a(const ConvArgs& a, int m, bool ok, int 
 }
 
 template <int MODE, int NE>
-__device__ __forceinline__ void gather_b(const ConvArgs& a, const Col& c, int k0, float (&v)[NE]) {
+__device__ __forceinline__ void locate_b(const ConvArgs& a, const Col& c, int k0, const float* (&P)[NE]) {
     if (!c.ok) {
 #pragma unroll
-        for (int e = 0; e < NE; ++e) v[e] = 0.f;
+        for (int e = 0; e < NE; ++e) P[e] = nullptr;
         return;
     }
     if (MODE == kConvFwd || MODE == kConvDgrad) {
@@ -449,12 +427,12 @@ __device__ __forceinline__ void gather_b(const ConvArgs& a, const Col& c, int k0
         int kh = r / a.k, kw = r - kh * a.k;
 #pragma unroll
         for (int e = 0; e < NE; ++e) {
-            float x = 0.f;
+            const float* x = nullptr;
             if (k0 + e < a.K) {
                 if (MODE == kConvFwd) {
                     const int ih = c.y * a.s - a.p + kh, iw = c.x * a.s - a.p + kw;
                     if ((unsigned)ih < (unsigned)a.hi && (unsigned)iw < (unsigned)a.wi)
-                        x = __ldg(c.row + ((size_t)ch * a.hi + ih) * a.wi + iw);
+                        x = c.row + ((size_t)ch * a.hi + ih) * a.wi + iw;
                 } else {
                     int th = c.y + a.p - kh, tw = c.x + a.p - kw;
                     bool in = th >= 0 && tw >= 0;
@@ -467,10 +445,10 @@ __device__ __forceinline__ void gather_b(const ConvArgs& a, const Col& c, int k0
                         th /= a.s;
                         tw /= a.s;
                     }
-                    if (in && th < a.ho && tw < a.wo) x = __ldg(c.row + ((size_t)ch * a.ho + th) * a.wo + tw);
+                    if (in && th < a.ho && tw < a.wo) x = c.row + ((size_t)ch * a.ho + th) * a.wo + tw;
                 }
             }
-            v[e] = x;
+            P[e] = x;
             if (++kw == a.k) {
                 kw = 0;
                 if (++kh == a.k) {
@@ -492,12 +470,12 @@ __device__ __forceinline__ void gather_b(const ConvArgs& a, const Col& c, int k0
         const float* row = b < a.B ? rowp(b) : a.X;
 #pragma unroll
         for (int e = 0; e < NE; ++e) {
-            float x = 0.f;
+            const float* x = nullptr;
             if (k0 + e < a.K) {
                 const int ih = oh * a.s - a.p + c.kh, iw = ow * a.s - a.p + c.kw;
-                if ((unsigned)ih < (unsigned)a.hi && (unsigned)iw < (unsigned)a.wi) x = __ldg(row + (size_t)ih * a.wi + iw);
+                if ((unsigned)ih < (unsigned)a.hi && (unsigned)iw < (unsigned)a.wi) x = row + (size_t)ih * a.wi + iw;
             }
-            v[e] = x;
+            P[e] = x;
             if (++ow == a.wo) {
                 ow = 0;
                 if (++oh == a.ho) {
@@ -529,6 +507,18 @@ __global__ void __launch_bounds__(kCT, 1) conv_mma_kernel(const __grid_constant_
     const int katoms = (a.K + KA - 1) / KA;
     const int a_lo = blockIdx.z * a.apc;
     const int na = max(0, min(katoms, a_lo + a.apc) - a_lo);
+    // phase stamps: 0 start, 1 setup done, 2 first atom published, 3 first MMA issued,
+    // 4 last MMA committed, 5 accumulator ready (epilogue), 6 stores done
+    unsigned long long* stamp =
+        a.stamps ? a.stamps + (((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 8 : nullptr;
+    auto tick = [&](int k) {
+        if (stamp) {
+            unsigned long long tt;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+            stamp[k] = tt;
+        }
+    };
+    if (threadIdx.x == 0) tick(0);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < NST; ++s) {
@@ -546,6 +536,7 @@ __global__ void __launch_bounds__(kCT, 1) conv_mma_kernel(const __grid_constant_
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) tick(1);
 
     if (warp == 0) {
         if (lane == 0 && na > 0) {
@@ -555,6 +546,7 @@ __global__ void __launch_bounds__(kCT, 1) conv_mma_kernel(const __grid_constant_
             for (int i = 0; i < na; ++i) {
                 const int s = i % NST;
                 mbar_wait(full + s, (i / NST) & 1);
+                if (i == 0) tick(3);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t abase = smem_u32(base + s * STAGE);
                 const uint32_t bbase = abase + kCTile;
@@ -571,43 +563,100 @@ __global__ void __launch_bounds__(kCT, 1) conv_mma_kernel(const __grid_constant_
                 umma_commit(empty + s);
             }
             umma_commit(done);
+            tick(4);
         }
     } else {
         // ---- producers: thread t owns operand row r (A: output row m0 + r; B: GEMM
-        // column n0 + r) and 16-byte chunks jh .. jh + 3 of every atom
-        const int tg = threadIdx.x - 32, grp = tg / kCP, t = tg - grp * kCP, r = t >> 1, jh = (t & 1) * 4;
+        // column n0 + r) and 16-byte chunks jh .. jh + 3 of every atom. Each element
+        // is one 4-byte cp.async (zero-filled where the operand is padding), so a
+        // thread keeps D = NST - 1 atoms of copies in flight instead of waiting on
+        // its loads; an atom is published (3xTF32: after the thread splits its own
+        // elements into tf32 hi / lo) once the thread's copies of it have landed.
+        constexpr int D = NST - 1;
+        const int t = threadIdx.x - 32, r = t >> 1, jh = (t & 1) * 4;
         const bool arow = m0 + r < a.M;
         const Col col = make_col<MODE>(a, n0 + r);
         const int sw = r & 7;
         const int rbase = (r >> 3) * 1024 + (r & 7) * 128;
-        for (int i = grp; i < na; i += kCG) {
-            const int s = i % NST;
-            if (i >= NST) mbar_wait(empty + s, ((i / NST) - 1) & 1);
-            unsigned char* sa = base + s * STAGE;
-            unsigned char* sb = sa + kCTile;
-            const int k0 = (a_lo + i) * KA + jh * CE;  // the thread's 4 chunks are 4 * CE consecutive k
-            float v[4 * CE];
-            if (MODE != kConvWgrad && a.kt)
-                gather_a_tm<MODE, 4 * CE>(a, m0 + r, arow, k0, v);
-            else
-                gather_a<MODE, 4 * CE>(a, m0 + r, arow, k0, v);
+        auto issue = [&](unsigned char* X, const float* const (&P)[4 * CE]) {
 #pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {
-                const int off = rbase + (((jh + jj) ^ sw) << 4);
-                put_chunk<ES, SPLIT>(sa + off, sa + 2 * kCTile + off, v + jj * CE);
+            for (int e = 0; e < 4 * CE; ++e) {
+                const uint32_t dst = smem_u32(X + rbase + (((jh + e / CE) ^ sw) << 4) + (e % CE) * 4);
+                const float* src = P[e] ? P[e] : a.W;
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(P[e] ? 4 : 0)
+                             : "memory");
             }
-            if (MODE != kConvWgrad && a.kt)
-                gather_b_tm<MODE, 4 * CE>(a, col, k0, v);
-            else
-                gather_b<MODE, 4 * CE>(a, col, k0, v);
+        };
+        auto publish = [&](int i) {
+            const int s = i % NST;
+            if constexpr (SPLIT) {
 #pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {
-                const int off = rbase + (((jh + jj) ^ sw) << 4);
-                put_chunk<ES, SPLIT>(sb + off, sb + 2 * kCTile + off, v + jj * CE);
+                for (int h = 0; h < 2; ++h) {
+                    unsigned char* X = base + s * STAGE + h * kCTile;
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) {
+                        float4* q = reinterpret_cast<float4*>(X + rbase + (((jh + jj) ^ sw) << 4));
+                        const float4 x = *q;
+                        const float4 hi = make_float4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
+                        *q = hi;
+                        *reinterpret_cast<float4*>(reinterpret_cast<unsigned char*>(q) + 2 * kCTile) =
+                            make_float4(x.x - hi.x, x.y - hi.y, x.z - hi.z, x.w - hi.w);
+                    }
+                }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(full + s)) : "memory");
+            if (i == 0 && t == 0) tick(2);
+        };
+        // A rows that are contiguous runs of 4 * CE floats: the prepared tap-major weights
+        // (fwd / dgrad) or the delta rows of a weight gradient (HWo % 16 == 0): 16-byte copies
+        const bool arun = MODE == kConvWgrad ? (a.ho * a.wo) % (4 * CE) == 0 : (a.kt && a.Wt != nullptr);
+        auto issue16 = [&](unsigned char* X, const float* src) {
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                const uint32_t dst = smem_u32(X + rbase + (((jh + jj) ^ sw) << 4));
+                const float* p = src ? src + jj * CE : a.W;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(p), "r"(src ? 16 : 0)
+                             : "memory");
+            }
+        };
+        for (int i = 0; i < na; ++i) {
+            const int s = i % NST;
+            if (i >= NST) mbar_wait(empty + s, ((i / NST) - 1) & 1);
+            unsigned char* sa = base + s * STAGE;
+            const int k0 = (a_lo + i) * KA + jh * CE;  // the thread's 4 chunks are 4 * CE consecutive k
+            const float* P[4 * CE];
+            if (arun) {
+                const float* src = nullptr;
+                if (arow && k0 < a.K) {
+                    if (MODE == kConvWgrad) {
+                        const int hw = a.ho * a.wo, b = k0 / hw;
+                        src = a.D + ((size_t)b * a.co + m0 + r) * hw + (k0 - b * hw);
+                    } else {
+                        src = a.Wt + (size_t)(m0 + r) * a.K + k0;
+                    }
+                }
+                issue16(sa, src);
+            } else {
+                if (MODE != kConvWgrad && a.kt)
+                    locate_a_tm<MODE, 4 * CE>(a, m0 + r, arow, k0, P);
+                else
+                    locate_a<MODE, 4 * CE>(a, m0 + r, arow, k0, P);
+                issue(sa, P);
+            }
+            if (MODE != kConvWgrad && a.kt)
+                locate_b_tm<MODE, 4 * CE>(a, col, k0, P);
+            else
+                locate_b<MODE, 4 * CE>(a, col, k0, P);
+            issue(sa + kCTile, P);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            if (i >= D) {
+                asm volatile("cp.async.wait_group %0;" ::"n"(D) : "memory");
+                publish(i - D);
+            }
         }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        for (int i = max(0, na - D); i < na; ++i) publish(i);
         // ---- epilogue: warps 1-4 move the accumulator (TMEM lane quadrant warp % 4)
         // into a padded smem tile; then all producers store it along pixels
         float* T = reinterpret_cast<float*>(base);  // 128 x 129 floats, over the drained ring
@@ -615,6 +664,7 @@ __global__ void __launch_bounds__(kCT, 1) conv_mma_kernel(const __grid_constant_
             const int q = warp & 3, row = q * 32 + lane;
             if (na > 0) {
                 mbar_wait(done, 0);
+                if (warp == 1 && lane == 0) tick(5);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
@@ -627,20 +677,62 @@ __global__ void __launch_bounds__(kCT, 1) conv_mma_kernel(const __grid_constant_
                 for (int c = 0; c < 128; ++c) T[row * 129 + c] = 0.f;
             }
         }
-        asm volatile("bar.sync 1, %0;" ::"n"(kCG * kCP) : "memory");
-        for (int idx = tg; idx < 128 * 128; idx += kCG * kCP) {
-            const int mm = idx >> 7, nn = idx & 127;
-            const int m = m0 + mm, n = n0 + nn;
-            if (m >= a.M || n >= a.N) continue;
-            const float v = T[mm * 129 + nn];
-            if (a.splits > 1)
-                a.partial[((size_t)blockIdx.z * a.M + m) * a.N + n] = v;
-            else
-                epilogue<MODE>(a, m, n, v);
+        asm volatile("bar.sync 1, %0;" ::"n"(kCP) : "memory");
+        // the thread's column n is fixed (stride 256 = two rows of 128): its sample /
+        // pixel decomposition is done once, each row m is then one strided step
+        const int nn = t & 127, n = n0 + nn;
+        if (n < a.N) {
+            const int mstart = t >> 7;
+            if (a.splits > 1) {
+                float* dst = a.partial + (size_t)blockIdx.z * a.M * a.N + n;
+                for (int mm = mstart; mm < 128 && m0 + mm < a.M; mm += 2)
+                    dst[(size_t)(m0 + mm) * a.N] = T[mm * 129 + nn];
+            } else if (MODE == kConvWgrad) {
+                for (int mm = mstart; mm < 128 && m0 + mm < a.M; mm += 2)
+                    a.Y[(size_t)(m0 + mm) * a.N + n] = T[mm * 129 + nn];
+            } else if (MODE == kConvFwd) {
+                const int hw = a.ho * a.wo, b = n / hw, pix = n - b * hw;
+                float* y = a.Y + (size_t)b * a.co * hw + pix;
+                const float* rs = nullptr;
+                size_t rstep = 0;
+                if (a.res) {
+                    const int oh = pix / a.wo, ow = pix - oh * a.wo, st = a.rh / a.ho;
+                    rstep = (size_t)a.rh * a.rw;
+                    rs = a.res + (size_t)b * a.rc * rstep + (size_t)(oh * st) * a.rw + ow * st;
+                }
+                for (int mm = mstart; mm < 128 && m0 + mm < a.M; mm += 2) {
+                    const int m = m0 + mm;
+                    float v = T[mm * 129 + nn] + __ldg(a.bias + m);
+                    if (rs && m < a.rc) v += __ldg(rs + (size_t)m * rstep);
+                    if (a.relu) v = v > 0.f ? v : 0.f;
+                    y[(size_t)m * hw] = v;
+                }
+            } else {  // dgrad
+                const int hw = a.hi * a.wi, b = n / hw, pix = n - b * hw;
+                const size_t o0 = (size_t)b * a.ci * hw + pix;
+                const float* rs = nullptr;
+                size_t rstep = 0;
+                if (a.res) {
+                    const int ih = pix / a.wi, iw = pix - ih * a.wi, st = a.hi / a.rh;
+                    if (ih % st == 0 && iw % st == 0) {
+                        rstep = (size_t)a.rh * a.rw;
+                        rs = a.res + (size_t)b * a.rc * rstep + (size_t)(ih / st) * a.rw + iw / st;
+                    }
+                }
+                for (int mm = mstart; mm < 128 && m0 + mm < a.M; mm += 2) {
+                    const int m = m0 + mm;
+                    const size_t o = o0 + (size_t)m * hw;
+                    float v = T[mm * 129 + nn];
+                    if (rs) v += __ldg(rs + (size_t)m * rstep);
+                    if (a.mask && !(__ldg(a.mask + o) > 0.f)) v = 0.f;
+                    a.Y[o] = v;
+                }
+            }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    if (threadIdx.x == 0) tick(6);
     if (warp == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
@@ -661,8 +753,24 @@ const void* conv_mma_func(size_t& smem) {
 
 template <int MODE>
 const void* conv_mma_pick(int tc, size_t& smem) {
-    return tc == 1 ? conv_mma_func<MODE, 4, false>(smem) : tc == 2 ? conv_mma_func<MODE, 2, false>(smem)
-                                                              : conv_mma_func<MODE, 4, true>(smem);
+    // tc 2 (bf16 fast mode): the activations are fp32 in HBM and land in smem by cp.async
+    // as they are, so the convolutions run kind::tf32 (no conversion pass)
+    return tc == 3 ? conv_mma_func<MODE, 4, true>(smem) : conv_mma_func<MODE, 4, false>(smem);
+}
+
+// Wt[m][tap * C + c] = fwd: W[m][c][tap] (C = c_in); dgrad: W[c][m][tap] (C = c_out)
+template <int MODE>
+__global__ void __launch_bounds__(NT) conv_wprep_kernel(const ConvArgs a) {
+    float* Wt = const_cast<float*>(a.Wt);
+    const int kk = a.k * a.k;
+    const int C = MODE == kConvFwd ? a.ci : a.co;
+    const size_t n = (size_t)a.M * a.K;
+    for (size_t i = (size_t)blockIdx.x * NT + threadIdx.x; i < n; i += (size_t)gridDim.x * NT) {
+        const int m = (int)(i / a.K), k = (int)(i - (size_t)m * a.K);
+        const int tap = k / C, c = k - tap * C;
+        Wt[i] = MODE == kConvFwd ? __ldg(a.W + ((size_t)m * a.ci + c) * kk + tap)
+                                 : __ldg(a.W + ((size_t)c * a.ci + m) * kk + tap);
+    }
 }
 
 }  // namespace
@@ -683,7 +791,7 @@ size_t conv_plan(ConvArgs& a, int mode, size_t max_partial) {
         a.K = a.B * a.ho * a.wo;
     }
     if (a.tc) {  // tensor cores: 128 x 128 tiles, K in 128-byte atoms, about one wave of CTAs
-        const int KA = a.tc == 2 ? 64 : 32;
+        const int KA = 32;  // tf32 atoms (tc 2 runs the tf32 kernel)
         const long long katoms = (a.K + KA - 1) / KA;
         const long long mt = (long long)((a.M + 127) / 128) * ((a.N + 127) / 128);
         // one CTA per SM (544 threads): split K only as far as the tiles stay one wave
@@ -734,6 +842,13 @@ int spec_conv(const ConvArgs& a, int mode, KernelSpec& gemm, KernelSpec& reduce)
     const long long threads = warp_reduce(a) ? mn * 32 : mn;
     fill_spec(reduce, r, dim3((unsigned)std::min<long long>((threads + NT - 1) / NT, 148 * 8)), dim3(NT), a);
     return 2;
+}
+
+void spec_conv_wprep(const ConvArgs& a, int mode, KernelSpec& k) {
+    const long long n = (long long)a.M * a.K;
+    const void* f = mode == kConvFwd ? reinterpret_cast<const void*>(&conv_wprep_kernel<kConvFwd>)
+                                     : reinterpret_cast<const void*>(&conv_wprep_kernel<kConvDgrad>);
+    fill_spec(k, f, dim3((unsigned)std::min<long long>((n + NT - 1) / NT, 148 * 8)), dim3(NT), a);
 }
 
 void spec_conv_bgrad(const ConvArgs& a, float* gb, KernelSpec& k) {

@@ -302,6 +302,10 @@ struct ConvArgs {
     // on bf16 operands; 3 = 3xTF32 (fp32-accurate: the fp32 parity mode)
     int tc;
     int apc;             // tensor-core path: 128-byte K atoms per split
+    const float* Wt;     // kt: the weights as the A operand rows in (tap, channel) order, M x K
+                         // (spec_conv_wprep writes it before the GEMM): 16-byte copies instead of a
+                         // stride-k*k gather
+    unsigned long long* stamps;  // nullable: 8 globaltimer phase stamps per CTA (measurement)
     int kt;              // tensor-core fwd / dgrad: K ordered (tap, channel) instead of (channel, tap),
                          // when the channel count is a multiple of the atom: a thread's run of k is
                          // one tap's consecutive channels (one bounds check, constant address step)
@@ -311,6 +315,8 @@ enum { kConvFwd = 0, kConvDgrad = 1, kConvWgrad = 2 };
 size_t conv_plan(ConvArgs& a, int mode, size_t max_partial);
 // one or two kernels (GEMM, then the ordered split reduction + epilogue)
 int spec_conv(const ConvArgs& a, int mode, KernelSpec& gemm, KernelSpec& reduce);
+// kt paths: Wt (M x K, tap-major) from W, one small transpose per GEMM launch
+void spec_conv_wprep(const ConvArgs& a, int mode, KernelSpec& k);  // writes a.Wt
 // gb[co] = sum over samples and pixels of D (wgrad's bias part), written at Y
 void spec_conv_bgrad(const ConvArgs& a, float* gb, KernelSpec& k);
 // global average pool (GAP_DENSE input): pooled[b][c] = mean_p x[b][c][p]

@@ -1716,10 +1716,27 @@ struct ferret_trainer {
         if (it != conv_scratch.end()) return it->second;
         return conv_scratch[key] = dalloc<float>(kConvPartialCap, device_bytes);
     }
+    // tap-major weight copies for the tensor-core A operand, one region per written resource
+    std::map<uint64_t, float*> conv_wt;
+    float* conv_wt_for(uint64_t key) {
+        auto it = conv_wt.find(key);
+        if (it != conv_wt.end()) return it->second;
+        long long mx = 1;
+        for (const LayerDev& ld : layers)
+            if (ld.conv()) mx = std::max(mx, ld.nw());
+        return conv_wt[key] = dalloc<float>(static_cast<size_t>(mx), device_bytes);
+    }
     void emit_conv(fb200::ConvArgs& c, int mode, const std::vector<uint64_t>& reads, const std::vector<uint64_t>& writes,
                    double bytes) {
         fb200::conv_plan(c, mode, kConvPartialCap);
         if (c.splits > 1) c.partial = conv_scratch_for(writes.at(0));
+        if (c.kt && mode != fb200::kConvWgrad) {
+            c.Wt = conv_wt_for(writes.at(0));
+            fb200::KernelSpec kw;
+            fb200::spec_conv_wprep(c, mode, kw);
+            gb->cur_bytes = 8.0 * static_cast<double>(c.M) * c.K;
+            gb->kernel(kw, reads, writes);
+        }
         fb200::KernelSpec g, r;
         const int n = fb200::spec_conv(c, mode, g, r);
         gb->cur_bytes = bytes;
@@ -3186,11 +3203,36 @@ ferret_status ferret_conv_layer(int32_t tc, int32_t mode, const int32_t* geom, i
         c.Y = up(nullptr, ny);
         const size_t part = fb200::conv_plan(c, mode, 0);
         if (part) c.partial = up(nullptr, part);
+        if (c.kt && mode != fb200::kConvWgrad) {
+            c.Wt = up(nullptr, nw);
+            fb200::KernelSpec kw;
+            fb200::spec_conv_wprep(c, mode, kw);
+            cuda_check(fb200::launch_spec(kw, nullptr), "conv_layer weight prep");
+        }
+        // FERRET_CONV_STAMPS=<file>: append per-CTA phase timestamps of the tensor-core kernel
+        const char* stamp_file = std::getenv("FERRET_CONV_STAMPS");
+        const size_t n_ctas = static_cast<size_t>((c.N + 127) / 128) * ((c.M + 127) / 128) * c.splits;
+        if (stamp_file && tc) {
+            c.stamps = reinterpret_cast<unsigned long long*>(up(nullptr, n_ctas * 16));
+            cuda_check(cudaMemset(c.stamps, 0, n_ctas * 64), "memset");
+        }
         fb200::KernelSpec g, r;
         const int n = fb200::spec_conv(c, mode, g, r);
         cuda_check(fb200::launch_spec(g, nullptr), "conv_layer launch");
         if (n == 2) cuda_check(fb200::launch_spec(r, nullptr), "conv_layer reduce");
         cuda_check(cudaDeviceSynchronize(), "conv_layer");
+        if (c.stamps) {
+            std::vector<unsigned long long> h(n_ctas * 8);
+            cuda_check(cudaMemcpy(h.data(), c.stamps, n_ctas * 64, cudaMemcpyDeviceToHost), "D2H");
+            if (FILE* f = std::fopen(stamp_file, "a")) {
+                std::fprintf(f, "conv tc %d mode %d geom %d %d %d %d B %d grid %d %d %d atoms/cta %d\n", tc, mode, c.ci,
+                             c.hi, c.co, c.k, B, (c.N + 127) / 128, (c.M + 127) / 128, c.splits, c.apc);
+                for (size_t i = 0; i < n_ctas; ++i)
+                    std::fprintf(f, "%llu %llu %llu %llu %llu %llu %llu\n", h[8 * i], h[8 * i + 1], h[8 * i + 2],
+                                 h[8 * i + 3], h[8 * i + 4], h[8 * i + 5], h[8 * i + 6]);
+                std::fclose(f);
+            }
+        }
         cuda_check(cudaMemcpy(Y, c.Y, ny * 4, cudaMemcpyDeviceToHost), "D2H");
     });
 }

@@ -20,13 +20,16 @@ def main(csv_path, log_path):
         m = re.match(r"shape \((.*)\) tc (\d) mode (\d) gflop ([\d.]+)", line)
         if not m:
             continue
+        # one probe call = [weight prep] + GEMM + [split reduction]
         t = 0.0
-        while i < len(data):
+        if i < len(data) and "wprep" in data[i]["Kernel Name"]:
             t += float(data[i]["Metric Value"]) * scale
             i += 1
-            if i < len(data) and "reduce" in data[i]["Kernel Name"]:
-                continue
-            break
+        t += float(data[i]["Metric Value"]) * scale
+        i += 1
+        if i < len(data) and "reduce" in data[i]["Kernel Name"]:
+            t += float(data[i]["Metric Value"]) * scale
+            i += 1
         gf = float(m.group(4))
         print(f"{m.group(1):26s} tc{m.group(2)} mode{m.group(3)} {t:8.1f} us {gf / (t * 1e-6) / 1e3:7.1f} TFLOP/s")
 
