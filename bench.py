@@ -159,6 +159,51 @@ def config5_roofline(fb, torch, device, precision="bf16"):
     return out
 
 
+def config3_resnet(fb, torch, device, no_cpu=False):
+    """BASELINE config 3 on one GPU: ResNet-18-style CNN (11.0 M params; convolutions on the
+    tcgen05 tensor cores, 3xTF32 in the fp32 parity mode) on a CIFAR-shaped stream, 4 stages
+    cut between residual blocks, iter_fisher, ER replay, micro-batch 16 (profiles/c3_resnet.py),
+    with the conv CPU oracle timed on a bounded sample of the same workload (fp64, 1 core)."""
+    from profiles.c3_resnet import measure
+
+    r = measure(fb, torch, units=32, steps=2, warmup=2, device=device, profile=False)
+    tflops = None
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            tflops = json.load(f).get("bf16_tflops")
+    out = {"workload": r["workload"], "value": r["samples_per_s"], "unit": "samples/s",
+           "ms_per_chunk": r["ms_per_chunk"], "samples_per_chunk": r["samples_per_chunk"], "dtype": "f32 (3xTF32 convs)",
+           "achieved_tflops": r["tflops"], "oacc_last_chunk": r["oacc_last_chunk"],
+           "tensor": {"achieved_tflops": r["tflops"], "peak_tflops": tflops, "peak_kind": "bf16 dense (measured)",
+                      "frac": r["tflops"] / tflops if tflops else None,
+                      "note": "whole-step algorithmic flops (8 F per sample + 6 F per replay sample) / chunk time; "
+                              "3xTF32 issues 3 tf32 MMAs per product (tf32 peak = bf16 / 2)"}}
+    if not no_cpu:
+        try:
+            from oracle import oracle as orc
+
+            cn = fb.convnet
+            spec = cn.resnet_cifar()
+            bounds = cn.balanced_bounds(spec, 4)
+            prof = cn.profile(spec)
+            t_d = cn.stage_t_d(prof, bounds)
+            n_units = 3
+            sched = fb.Schedule.forced(prof, t_d, fb.StreamSpec(t_d=t_d, horizon=n_units * t_d), bounds, n_units)
+            feats, labels = fb.synth_drift_stream(n_units, spec.in_width(0), 10, "split_tasks", 7)
+            t0 = time.perf_counter()
+            orc.train_conv(spec.geom, spec.acts, cn.make_conv_net(spec, 1), bounds, sched.events, feats, labels,
+                           policy="iter_fisher", replay=True, replay_seed=3, micro_batch=1)
+            dt = time.perf_counter() - t0
+            out["cpu_baseline"] = {"value": n_units / dt, "unit": "samples/s", "cores": 1, "kind": "port",
+                                   "sample": f"{n_units} units x 1 sample ({dt:.1f} s) of the same net and schedule "
+                                             "rule at micro-batch 1; conv oracle (reference trainer order, "
+                                             "restated layers), fp64, single-threaded"}
+        except Exception as e:
+            out["cpu_baseline"] = {"value": None, "sample": f"unavailable: {e}"}
+    return out
+
+
 def stage_shard_measure(fb, torch, dist, rank, world, local, args, units, widths=None, bounds=None,
                         precision="fp32", steps=None, warmup=None):
     """One stream pipelined with its stages sharded over min(N, P) GPUs (one stage group
@@ -391,6 +436,7 @@ def main():
     achieved = dc["gbs"]
     large = config5_roofline(fb, torch, local) if not args.no_large else None
     large32 = config5_roofline(fb, torch, local, "fp32") if not args.no_large else None
+    conv3 = config3_resnet(fb, torch, local, no_cpu=args.no_cpu or world > 1) if not args.no_large else None
     shard = stage_shard_measure(fb, torch, dist, rank, world, local, args, units) if world > 1 else None
     shard5 = None
     if world > 1 and not args.no_large:  # config 5, bf16: 8 stages over the N GPUs
@@ -458,6 +504,7 @@ def main():
                              "config5_bf16 has the HBM-bound wide net"},
         "config5_bf16": large,
         "config5_fp32": large32,
+        "config3_resnet": conv3,
         "stage_shard": shard,
         "stage_shard_config5": shard5,
         "cpu_baseline": cpu,
