@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--replay", type=int, default=1)
     ap.add_argument("--device", type=int, default=-1, help="-1: LOCAL_RANK")
     ap.add_argument("--precision", default="fp32")
+    ap.add_argument("--conv-width", type=int, default=0, help="> 0: a ResNet-style conv net (convnet.resnet_cifar)")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -34,17 +35,27 @@ def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     dev = int(os.environ.get("LOCAL_RANK", "0")) if args.device < 0 else args.device
     dist.init_process_group("gloo")
-    widths = [int(x) for x in args.widths.split(",")]
-    bounds = [int(x) for x in args.bounds.split(",")]
-    P = len(bounds) - 1
     B = args.micro_batch
-    prof = fb.profile_from_widths(widths)
-    t_d = float(prof["t_f"].max())
+    if args.conv_width:
+        cn = fb.convnet
+        net = cn.resnet_cifar(width=args.conv_width, blocks=(1, 1, 1, 1))
+        widths = net.widths
+        bounds = cn.balanced_bounds(net, 4)
+        prof = cn.profile(net)
+        t_d = cn.stage_t_d(prof, bounds)
+        params = cn.make_conv_net(net, 1)
+    else:
+        widths = [int(x) for x in args.widths.split(",")]
+        bounds = [int(x) for x in args.bounds.split(",")]
+        net = widths
+        prof = fb.profile_from_widths(widths)
+        t_d = float(prof["t_f"].max())
+        params = fb.make_dense_net(widths, 1)
+    P = len(bounds) - 1
     sched = fb.Schedule.forced(prof, t_d, fb.StreamSpec(t_d=t_d, horizon=args.units * t_d), bounds, args.units)
     chunk = args.units * B
     feats, labels = fb.synth_drift_stream(args.chunks * chunk, widths[0], widths[-1], "split_tasks", 7)
-    params = fb.make_dense_net(widths, 1)
-    tr = fb.PipelineTrainer(widths, params, bounds,
+    tr = fb.PipelineTrainer(net, params, bounds,
                             fb.PipelineTrainOptions(policy=args.policy, micro_batch=B, replay=bool(args.replay),
                                                     replay_seed=3, device=dev, precision=args.precision))
     owners = fb.ferret.stage_owners(P, world)

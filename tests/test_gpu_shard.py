@@ -79,3 +79,48 @@ def test_two_rank_stage_shard_matches_single_process(gpu, fb, tmp_path, monkeypa
     np.testing.assert_array_equal(m0, ref["normalizer"][1])
     # both ranks really did work: each launched kernels for its stages
     assert all(rk["stats"]["kernel_launches"] > 0 for rk in ranks)
+
+
+def test_two_rank_stage_shard_conv_net(gpu, fb, tmp_path):
+    """The ResNet-style conv net (config 3's layout at width 8, 4 stages cut between blocks,
+    ER replay) sharded over 2 ranks equals the single-process trainer bit for bit: the
+    hand-offs carry NCHW activation / delta rows like any other layer's."""
+    import torch
+
+    cn = fb.convnet
+    net = cn.resnet_cifar(width=8, blocks=(1, 1, 1, 1))
+    bounds = cn.balanced_bounds(net, 4)
+    prof = cn.profile(net)
+    t_d = cn.stage_t_d(prof, bounds)
+    units, chunks, B = 24, 2, 4
+    sched = fb.Schedule.forced(prof, t_d, fb.StreamSpec(t_d=t_d, horizon=units * t_d), bounds, units)
+    chunk = units * B
+    widths = net.widths
+    feats, labels = fb.synth_drift_stream(chunks * chunk, widths[0], 10, "split_tasks", 7)
+    params = cn.make_conv_net(net, 1)
+    tr = fb.PipelineTrainer(net, params, bounds, fb.PipelineTrainOptions(policy="iter_fisher", micro_batch=B,
+                                                                          replay=True, replay_seed=3))
+    tr.load_stream(feats, labels)
+    tr.set_schedule(sched.events, chunk)
+    logs = []
+    for c in range(chunks):
+        tr.execute(c)
+        logs.append(tr.fetch_log(c))
+    ref_params, ref_log = tr.params(), np.concatenate(logs)
+    tr.close()
+    dev = [] if torch.cuda.device_count() >= 2 else ["--device", "0"]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr=127.0.0.1",
+           "--master-port=29534", os.path.join(ROOT, "tests", "shard_worker.py"), "--out", str(tmp_path),
+           "--conv-width", "8", "--units", str(units), "--chunks", str(chunks), "--micro-batch", str(B),
+           "--policy", "iter_fisher", "--replay", "1"] + dev
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env={**os.environ, "PYTHONPATH": ROOT})
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    ranks = [pickle.load(open(tmp_path / f"rank{k}.pkl", "rb")) for k in range(2)]
+    owners = ranks[0]["owners"]
+    off = np.concatenate([[0], np.cumsum([net.layer_params(l) for l in range(net.n_layers)])])
+    merged = np.empty_like(ref_params)
+    for j in range(len(bounds) - 1):
+        lo, hi = off[bounds[j]], off[bounds[j + 1]]
+        merged[lo:hi] = ranks[owners[j]]["params"][lo:hi]
+    np.testing.assert_array_equal(merged, ref_params)
+    np.testing.assert_array_equal(ranks[owners[-1]]["log"]["predicted"], ref_log["predicted"])
