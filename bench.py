@@ -437,6 +437,11 @@ def main():
     large = config5_roofline(fb, torch, local) if not args.no_large else None
     large32 = config5_roofline(fb, torch, local, "fp32") if not args.no_large else None
     conv3 = config3_resnet(fb, torch, local, no_cpu=args.no_cpu or world > 1) if not args.no_large else None
+    budget4 = None
+    if not args.no_large:  # config 4: planner partitions at 100 / 50 / 25 % memory budget (profiles/c4_budget.py)
+        from profiles.c4_budget import measure as c4_measure
+
+        budget4 = c4_measure(fb, torch, device=local, steps=2)
     shard = stage_shard_measure(fb, torch, dist, rank, world, local, args, units) if world > 1 else None
     shard5 = None
     if world > 1 and not args.no_large:  # config 5, bf16: 8 stages over the N GPUs
@@ -505,6 +510,7 @@ def main():
         "config5_bf16": large,
         "config5_fp32": large32,
         "config3_resnet": conv3,
+        "config4_budget": budget4,
         "stage_shard": shard,
         "stage_shard_config5": shard5,
         "cpu_baseline": cpu,
