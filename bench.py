@@ -205,27 +205,36 @@ def config3_resnet(fb, torch, device, no_cpu=False):
 
 
 def stage_shard_measure(fb, torch, dist, rank, world, local, args, units, widths=None, bounds=None,
-                        precision="fp32", steps=None, warmup=None):
+                        precision="fp32", steps=None, warmup=None, conv=None):
     """One stream pipelined with its stages sharded over min(N, P) GPUs (one stage group
     per rank, NVLink hand-offs: peer stores into CUDA-IPC inboxes + release flags; ranks
     beyond the stage count idle). Default: the C2 stream; config 5 passes its widths and
     bounds (8 stages -> one stage per GPU on an 8xB200 box). Device time per chunk, max
     over ranks."""
-    widths = widths or WIDTHS
-    bounds = bounds or BOUNDS
     steps = steps or args.steps
     warmup = warmup if warmup is not None else args.warmup
+    if conv is not None:  # config 3: a convnet.ConvNetSpec, its 4 block-aligned stages, ER replay
+        cn = fb.convnet
+        widths = conv.widths
+        bounds = cn.balanced_bounds(conv, 4)
+        prof = cn.profile(conv)
+        t_d = cn.stage_t_d(prof, bounds)
+        net, params, replay = conv, cn.make_conv_net(conv, 1), True
+    else:
+        widths = widths or WIDTHS
+        bounds = bounds or BOUNDS
+        prof = fb.profile_from_widths(widths)
+        t_d = float(prof["t_f"].max())
+        net, params, replay = widths, fb.make_dense_net(widths, 1), False
     P = len(bounds) - 1
     used = min(world, P)
     owners = fb.ferret.stage_owners(P, used)
-    prof = fb.profile_from_widths(widths)
-    t_d = float(prof["t_f"].max())
     sched = fb.Schedule.forced(prof, t_d, fb.StreamSpec(t_d=t_d, horizon=units * t_d), bounds, units)
     chunk = units * MICRO_BATCH
     feats, labels = fb.synth_drift_stream((warmup + steps) * chunk, widths[0], widths[-1], "split_tasks", 7)
-    tr = fb.PipelineTrainer(widths, fb.make_dense_net(widths, 1), bounds,
+    tr = fb.PipelineTrainer(net, params, bounds,
                             fb.PipelineTrainOptions(policy=POLICY, micro_batch=MICRO_BATCH, device=local,
-                                                    precision=precision))
+                                                    precision=precision, replay=replay, replay_seed=3))
     tr.set_shard(rank, world, owners)
     tr.load_stream(feats, labels)
     tr.set_schedule(sched.events, chunk)
@@ -258,7 +267,8 @@ def stage_shard_measure(fb, torch, dist, rank, world, local, args, units, widths
     tr.close()
     return {"value": chunk * steps / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms / steps,
             "ranks_with_stages": used, "stage_owner": owners, "precision": precision,
-            "workload": f"MLP {widths[0]}-...-{widths[-1]} ({len(widths) - 1} layers), bounds {bounds}, "
+            "workload": (f"ResNet-18-style CNN ({conv.n_params / 1e6:.1f} M params), ER" if conv is not None else
+                         f"MLP {widths[0]}-...-{widths[-1]}") + f" ({len(widths) - 1} layers), bounds {bounds}, "
                         f"{units} units x {MICRO_BATCH} samples per chunk",
             "note": "one stream, stages sharded across GPUs (strong scaling); hand-offs are peer stores "
                     "into CUDA-IPC inboxes + release flags; ranks synchronise per chunk"}
@@ -447,6 +457,10 @@ def main():
     if world > 1 and not args.no_large:  # config 5, bf16: 8 stages over the N GPUs
         shard5 = stage_shard_measure(fb, torch, dist, rank, world, local, args, 32, widths=[4096] * 16 + [10],
                                      bounds=[0, 2, 4, 6, 8, 10, 12, 14, 16], precision="bf16", steps=2, warmup=2)
+    shard3 = None
+    if world > 1 and not args.no_large:  # config 3: the ResNet's 4 stages over min(N, 4) GPUs
+        shard3 = stage_shard_measure(fb, torch, dist, rank, world, local, args, 32, steps=2, warmup=2,
+                                     conv=fb.convnet.resnet_cifar())
 
     # ---- e2e through the public API with host buffers: PipelineTrainer ingest
     # (ferret_trainer_ingest) of the step's samples from pinned host memory, each
@@ -513,6 +527,7 @@ def main():
         "config4_budget": budget4,
         "stage_shard": shard,
         "stage_shard_config5": shard5,
+        "stage_shard_config3": shard3,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
         "gpu_launches": int(launches_per_step * args.steps),
