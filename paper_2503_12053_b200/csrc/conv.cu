@@ -587,39 +587,41 @@ __global__ void __launch_bounds__(kCT, 1) conv_mma_kernel(const __grid_constant_
                              : "memory");
             }
         };
+        // contiguous A rows (see below) are copied with 8 lanes per row: rows q * 32 + t / 8,
+        // chunk t % 8; everything else with the thread's own row r, chunks jh .. jh + 3
+        const bool arun = MODE == kConvWgrad ? (a.ho * a.wo) % CE == 0 : (a.kt && a.Wt != nullptr);
+        const int ja = t & 7;
+        auto split16 = [&](unsigned char* p) {  // tf32 hi in place, lo 2 tiles further
+            float4* q = reinterpret_cast<float4*>(p);
+            const float4 x = *q;
+            const float4 hi = make_float4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
+            *q = hi;
+            *reinterpret_cast<float4*>(p + 2 * kCTile) = make_float4(x.x - hi.x, x.y - hi.y, x.z - hi.z, x.w - hi.w);
+        };
+        // once the thread's own copies of atom i have landed: (3xTF32) split exactly the
+        // elements this thread copied, then publish its share of the atom
         auto publish = [&](int i) {
             const int s = i % NST;
             if constexpr (SPLIT) {
+                unsigned char* A = base + s * STAGE;
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    unsigned char* X = base + s * STAGE + h * kCTile;
-#pragma unroll
-                    for (int jj = 0; jj < 4; ++jj) {
-                        float4* q = reinterpret_cast<float4*>(X + rbase + (((jh + jj) ^ sw) << 4));
-                        const float4 x = *q;
-                        const float4 hi = make_float4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
-                        *q = hi;
-                        *reinterpret_cast<float4*>(reinterpret_cast<unsigned char*>(q) + 2 * kCTile) =
-                            make_float4(x.x - hi.x, x.y - hi.y, x.z - hi.z, x.w - hi.w);
+                for (int q = 0; q < 4; ++q) {
+                    if (arun) {
+                        const int ra = q * 32 + (t >> 3);
+                        split16(A + (ra >> 3) * 1024 + (ra & 7) * 128 + ((ja ^ (ra & 7)) << 4));
+                    } else {
+                        split16(A + rbase + (((jh + q) ^ sw) << 4));
                     }
+                    split16(A + kCTile + rbase + (((jh + q) ^ sw) << 4));
                 }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(full + s)) : "memory");
             if (i == 0 && t == 0) tick(2);
         };
-        // A rows that are contiguous runs of 4 * CE floats: the prepared tap-major weights
-        // (fwd / dgrad) or the delta rows of a weight gradient (HWo % 16 == 0): 16-byte copies
-        const bool arun = MODE == kConvWgrad ? (a.ho * a.wo) % (4 * CE) == 0 : (a.kt && a.Wt != nullptr);
-        auto issue16 = [&](unsigned char* X, const float* src) {
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {
-                const uint32_t dst = smem_u32(X + rbase + (((jh + jj) ^ sw) << 4));
-                const float* p = src ? src + jj * CE : a.W;
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(p), "r"(src ? 16 : 0)
-                             : "memory");
-            }
-        };
+        // A rows that are contiguous runs: the prepared tap-major weights (fwd / dgrad) or the
+        // delta rows of a weight gradient (HWo % 4 == 0) go as 16-byte copies with 8 lanes per
+        // 128-byte row, so a warp instruction touches 4 lines (one row per lane would touch 32)
         for (int i = 0; i < na; ++i) {
             const int s = i % NST;
             if (i >= NST) mbar_wait(empty + s, ((i / NST) - 1) & 1);
@@ -627,16 +629,25 @@ __global__ void __launch_bounds__(kCT, 1) conv_mma_kernel(const __grid_constant_
             const int k0 = (a_lo + i) * KA + jh * CE;  // the thread's 4 chunks are 4 * CE consecutive k
             const float* P[4 * CE];
             if (arun) {
-                const float* src = nullptr;
-                if (arow && k0 < a.K) {
-                    if (MODE == kConvWgrad) {
-                        const int hw = a.ho * a.wo, b = k0 / hw;
-                        src = a.D + ((size_t)b * a.co + m0 + r) * hw + (k0 - b * hw);
-                    } else {
-                        src = a.Wt + (size_t)(m0 + r) * a.K + k0;
+                const int ka = (a_lo + i) * KA + ja * CE;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int ra = q * 32 + (t >> 3), m = m0 + ra;
+                    const float* src = nullptr;
+                    if (m < a.M && ka < a.K) {
+                        if (MODE == kConvWgrad) {
+                            const int hw = a.ho * a.wo, b = ka / hw;
+                            src = a.D + ((size_t)b * a.co + m) * hw + (ka - b * hw);
+                        } else {
+                            src = a.Wt + (size_t)m * a.K + ka;
+                        }
                     }
+                    const uint32_t dst = smem_u32(sa + (ra >> 3) * 1024 + (ra & 7) * 128 + ((ja ^ (ra & 7)) << 4));
+                    if (!(a.dbg & 1))
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src ? src : a.W),
+                                     "r"(src ? 16 : 0)
+                                     : "memory");
                 }
-                issue16(sa, src);
             } else {
                 if (MODE != kConvWgrad && a.kt)
                     locate_a_tm<MODE, 4 * CE>(a, m0 + r, arow, k0, P);
@@ -644,11 +655,13 @@ __global__ void __launch_bounds__(kCT, 1) conv_mma_kernel(const __grid_constant_
                     locate_a<MODE, 4 * CE>(a, m0 + r, arow, k0, P);
                 issue(sa, P);
             }
-            if (MODE != kConvWgrad && a.kt)
-                locate_b_tm<MODE, 4 * CE>(a, col, k0, P);
-            else
-                locate_b<MODE, 4 * CE>(a, col, k0, P);
-            issue(sa + kCTile, P);
+            if (!(a.dbg & 2)) {
+                if (MODE != kConvWgrad && a.kt)
+                    locate_b_tm<MODE, 4 * CE>(a, col, k0, P);
+                else
+                    locate_b<MODE, 4 * CE>(a, col, k0, P);
+                issue(sa + kCTile, P);
+            }
             asm volatile("cp.async.commit_group;" ::: "memory");
             if (i >= D) {
                 asm volatile("cp.async.wait_group %0;" ::"n"(D) : "memory");
@@ -803,6 +816,7 @@ size_t conv_plan(ConvArgs& a, int mode, size_t max_partial) {
         const int C = mode == kConvFwd ? a.ci : a.co;
         a.kt = mode != kConvWgrad && C % KA == 0 && !std::getenv("FERRET_CONV_NO_TAPMAJOR");
         a.apc = (int)((katoms + sp - 1) / sp);
+        a.dbg = std::getenv("FERRET_CONV_DBG") ? std::atoi(std::getenv("FERRET_CONV_DBG")) : 0;
         a.splits = (int)((katoms + a.apc - 1) / a.apc);
         a.kchunk = a.apc * KA;
         return a.splits > 1 ? (size_t)a.splits * (size_t)mn2 : 0;

@@ -306,6 +306,7 @@ struct ConvArgs {
                          // (spec_conv_wprep writes it before the GEMM): 16-byte copies instead of a
                          // stride-k*k gather
     unsigned long long* stamps;  // nullable: 8 globaltimer phase stamps per CTA (measurement)
+    int dbg;             // measurement only (FERRET_CONV_DBG): 1 = skip the A copies, 2 = skip the B copies
     int kt;              // tensor-core fwd / dgrad: K ordered (tap, channel) instead of (channel, tap),
                          // when the channel count is a multiple of the atom: a thread's run of k is
                          // one tap's consecutive channels (one bounds check, constant address step)
