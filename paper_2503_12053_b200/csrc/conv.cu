@@ -303,6 +303,14 @@ __global__ void __launch_bounds__(NT) ungap_kernel(const PoolMeanArgs a) {
 // split-K partial (reduced in split order by conv_reduce_kernel).
 // ---------------------------------------------------------------------------
 // warp 0: TMEM + MMA issue; warps 1-8: producers (cp.async gathers), epilogue
+// Producer lag: a thread publishes atom i - LAG after issuing the copies of atom i. With
+// LAG = NST - 1 the MMA only ever had one published atom (issue of atom i waits on the MMA of
+// atom i - NST, publication of i - NST + 1 follows it): lag NST / 2 lets published atoms
+// queue for the MMA (C3 3.3-3.5k -> 3.65k samples/s; lag 1 measured the same)
+#ifndef FERRET_CONV_LAG_DIV
+#define FERRET_CONV_LAG_DIV 2
+#endif
+#define FERRET_CONV_LAG (NST / FERRET_CONV_LAG_DIV > 0 ? NST / FERRET_CONV_LAG_DIV : 1)
 constexpr int kCP = 256;
 constexpr int kCT = 32 + kCP;
 // smem ring depth: 3 x 64 KB (3xTF32: hi + lo operands) or 5 x 32 KB
@@ -572,7 +580,7 @@ __global__ void __launch_bounds__(kCT, 1) conv_mma_kernel(const __grid_constant_
         // thread keeps D = NST - 1 atoms of copies in flight instead of waiting on
         // its loads; an atom is published (3xTF32: after the thread splits its own
         // elements into tf32 hi / lo) once the thread's copies of it have landed.
-        constexpr int D = NST - 1;
+        constexpr int D = FERRET_CONV_LAG;
         const int t = threadIdx.x - 32, r = t >> 1, jh = (t & 1) * 4;
         const bool arow = m0 + r < a.M;
         const Col col = make_col<MODE>(a, n0 + r);
