@@ -166,3 +166,19 @@ def test_resnet_parity_each_conv_path(gpu, fb, orc, monkeypatch, tc):
     monkeypatch.setenv("FERRET_CONV_TC", str(tc))
     spec, params, feats, labels, sched = _setup(fb, 8, (1, 1, 1, 1), 40, 4)
     _compare(fb, orc, spec, params, feats, labels, sched, B=4, replay=True)
+
+
+def test_resnet18_full_width_parity(gpu, fb, orc):
+    """Config 3 at its full size — ResNet-18 layout at width 64 (11.0 M parameters), 4 stages,
+    iter_fisher, ER replay — for a few units at micro-batch 1 against the fp64 conv oracle
+    (~4 s of CPU per unit): parameters within 1e-4 per stage, identical predictions."""
+    spec = cn.resnet_cifar(width=64)
+    params = cn.make_conv_net(spec, 1)
+    n_units = 6
+    feats, labels = fb.synth_drift_stream(n_units, spec.in_width(0), 10, "split_tasks", 7)
+    bounds = cn.balanced_bounds(spec, 4)
+    prof = cn.profile(spec)
+    t_d = cn.stage_t_d(prof, bounds)
+    sched = fb.Schedule.forced(prof, t_d, fb.StreamSpec(t_d=t_d, horizon=n_units * t_d), bounds, n_units)
+    got, ref = _compare(fb, orc, spec, params, feats, labels, sched, B=1, replay=True)
+    assert np.isfinite(got).all()
