@@ -253,20 +253,28 @@ __global__ void __launch_bounds__(NT) conv_reduce_kernel(const ConvArgs a) {
     }
 }
 
-// gb[co] = sum_b sum_pix D[b][co][pix]: one warp per channel, fixed order
-// (gb = a.Y)
+// gb[co] = sum_b sum_pix D[b][co][pix]: one CTA per channel, thread t summing pixels
+// t, t + 256, ... of every sample in order, then a fixed butterfly + ordered warp sums
+// (deterministic). (gb = a.Y)
 __global__ void __launch_bounds__(NT) conv_bgrad_kernel(const ConvArgs a) {
-    const int warp = (blockIdx.x * NT + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (warp >= a.co) return;
+    __shared__ float part[NT / 32];
+    const int ch = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int hw = a.ho * a.wo;
     float v = 0.f;
     for (int b = 0; b < a.B; ++b) {
-        const float* d = a.D + ((size_t)b * a.co + warp) * hw;
-        for (int p = lane; p < hw; p += 32) v += __ldg(d + p);
+        const float* d = a.D + ((size_t)b * a.co + ch) * hw;
+        for (int p = threadIdx.x; p < hw; p += NT) v += __ldg(d + p);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) a.Y[warp] = v;
+    if (lane == 0) part[w] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float sum = 0.f;
+#pragma unroll
+        for (int k = 0; k < NT / 32; ++k) sum += part[k];
+        a.Y[ch] = sum;
+    }
 }
 
 __global__ void __launch_bounds__(NT) gap_kernel(const PoolMeanArgs a) {
@@ -876,7 +884,7 @@ void spec_conv_wprep(const ConvArgs& a, int mode, KernelSpec& k) {
 void spec_conv_bgrad(const ConvArgs& a, float* gb, KernelSpec& k) {
     ConvArgs b = a;
     b.Y = gb;
-    fill_spec(k, reinterpret_cast<const void*>(&conv_bgrad_kernel), dim3((a.co * 32 + NT - 1) / NT), dim3(NT), b);
+    fill_spec(k, reinterpret_cast<const void*>(&conv_bgrad_kernel), dim3(a.co), dim3(NT), b);
 }
 
 void spec_gap(const PoolMeanArgs& a, KernelSpec& k) {
