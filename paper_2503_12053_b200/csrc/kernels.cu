@@ -675,17 +675,22 @@ __global__ void __launch_bounds__(kThreads) update_iter1_kernel(const UpdArgs a)
         vr = learn ? a.v_r[e] : 0.f;
         va = learn ? a.v_a[e] : 0.f;
     };
+    const bool gm = w.g_off >= 0;  // materialised gradient (convolutions)
     if (w.bias) {
         if (tid >= R) return;
         const int r = w.r0 + tid;
         const size_t e = (size_t)w.elem0 + r;
         float cv[NV], ld, vr, va;
         load(e, cv, ld, vr, va);
-        const float* dl = pk.stash + w.dlt_off + r;
         float g = 0.f;
+        if (gm) {
+            g = __ldg(pk.stash + w.g_off + r);
+        } else {
+            const float* dl = pk.stash + w.dlt_off + r;
 #pragma unroll
-        for (int b = 0; b < BT; ++b)
-            if (b < B) g += __ldg(dl + (size_t)b * w.out);
+            for (int b = 0; b < BT; ++b)
+                if (b < B) g += __ldg(dl + (size_t)b * w.out);
+        }
         fold(e, g, cv, ld, vr, va);
         return;
     }
@@ -695,21 +700,24 @@ __global__ void __launch_bounds__(kThreads) update_iter1_kernel(const UpdArgs a)
 #pragma unroll
     for (int i = 0; i < RB; ++i)
         if (live && i < R) load((size_t)w.elem0 + (size_t)(w.r0 + i) * w.in + c, cv[i], ld[i], vr[i], va[i]);
-    for (int i = tid; i < B * R; i += kThreads) {
-        const int b = i / R, rr = i - b * R;
-        sdel[i] = __ldg(pk.stash + w.dlt_off + (size_t)b * w.out + w.r0 + rr);
-    }
     float xv[BT];
+    if (!gm) {
+        for (int i = tid; i < B * R; i += kThreads) {
+            const int b = i / R, rr = i - b * R;
+            sdel[i] = __ldg(pk.stash + w.dlt_off + (size_t)b * w.out + w.r0 + rr);
+        }
 #pragma unroll
-    for (int b = 0; b < BT; ++b) {
-        const float* xr = w.xin_off >= 0 ? pk.stash + w.xin_off + (size_t)b * w.in
-                          : a.x0idx      ? pk.x0 + (size_t)__ldg(a.x0idx + b) * a.x0_ld
-                                         : pk.x0 + (size_t)b * a.x0_ld;
-        xv[b] = (b < B && live) ? __ldg(xr + c) : 0.f;
+        for (int b = 0; b < BT; ++b) {
+            const float* xr = w.xin_off >= 0 ? pk.stash + w.xin_off + (size_t)b * w.in
+                              : a.x0idx      ? pk.x0 + (size_t)__ldg(a.x0idx + b) * a.x0_ld
+                                             : pk.x0 + (size_t)b * a.x0_ld;
+            xv[b] = (b < B && live) ? __ldg(xr + c) : 0.f;
+        }
     }
     __syncthreads();
     if (!live) return;
     auto grad = [&](int i) {
+        if (gm) return __ldg(pk.stash + w.g_off + (size_t)(w.r0 + i) * w.in + c);
         float g = 0.f;
 #pragma unroll
         for (int b = 0; b < BT; ++b) g = fmaf(sdel[b * R + i], xv[b], g);
@@ -1284,7 +1292,8 @@ void spec_update(const UpdArgs& a, KernelSpec& k) {
     const long long blocks = a.n_tiles;
     // FERRET_STREAM_MIN_CHAIN (test / experiment knob): chain length above which
     // the smem-staged kernel takes over from the register-resident one
-    if (a.gmat) {  // materialised gradients (conv stages): the generic tile kernel
+    if (a.gmat && !(a.policy == 4 && a.K == 1 && a.nv <= 16 && a.lam_d != nullptr)) {
+        // materialised gradients (conv stages) outside the iter1 kernel's case: the generic tile kernel
         const void* f = a.policy == 0 ? update_func<0>(a.B) : a.policy == 1 ? update_func<1>(a.B)
                       : a.policy == 2 ? update_func<2>(a.B) : a.policy == 3 ? update_func<3>(a.B) : update_func<4>(a.B);
         fill(k, f, dim3((unsigned)blocks), dim3(kThreads), a);
@@ -1292,7 +1301,7 @@ void spec_update(const UpdArgs& a, KernelSpec& k) {
     }
     const char* env = std::getenv("FERRET_STREAM_MIN_CHAIN");
     const int min_chain = env ? std::atoi(env) : kStreamMinChain;
-    if (a.policy == 4 && a.K == 1 && a.nv > min_chain && a.lam_d != nullptr) {
+    if (!a.gmat && a.policy == 4 && a.K == 1 && a.nv > min_chain && a.lam_d != nullptr) {
         const size_t smem = sizeof(float) * 2 * (size_t)(a.nv + 3) * kUpdTileCols;
         const void* f = a.B <= 1 ? stream_func<1>(smem) : a.B <= 2 ? stream_func<2>(smem) : a.B <= 4 ? stream_func<4>(smem)
                       : a.B <= 8 ? stream_func<8>(smem) : stream_func<16>(smem);
@@ -1302,7 +1311,7 @@ void spec_update(const UpdArgs& a, KernelSpec& k) {
     }
     // FERRET_UPDATE_V4=0 (experiment knob) keeps the scalar kernel
     static const bool v4_on = !std::getenv("FERRET_UPDATE_V4") || std::atoi(std::getenv("FERRET_UPDATE_V4")) != 0;
-    if (v4_on && a.policy == 4 && a.K == 1 && a.nv <= 16 && a.lam_d != nullptr && a.works4 != nullptr) {
+    if (v4_on && !a.gmat && a.policy == 4 && a.K == 1 && a.nv <= 16 && a.lam_d != nullptr && a.works4 != nullptr) {
         const void* f = a.B <= 1 ? iter1v4_func<1>(a.nv) : a.B <= 2 ? iter1v4_func<2>(a.nv) : a.B <= 4 ? iter1v4_func<4>(a.nv)
                       : a.B <= 8 ? iter1v4_func<8>(a.nv) : iter1v4_func<16>(a.nv);
         fill(k, f, dim3((unsigned)a.n_tiles4), dim3(a.threads4), a);

@@ -107,6 +107,7 @@ struct UpdWork {
     long long dlt_off;    // stash offset of the layer's delta
     int in, out, bias;
     int r0, nrows, c0;
+    long long g_off = -1; // >= 0: materialised gradient in the stash (UpdSeg::g_off of this tile's segment)
 };
 
 struct UpdPending {

@@ -819,7 +819,7 @@ struct ferret_trainer {
             std::vector<fb200::UpdWork> works;
             for (const fb200::UpdTile& t : tiles) {
                 const fb200::UpdSeg& sg = tab[static_cast<size_t>(t.seg)];
-                works.push_back({sg.elem0, sg.xin_off, sg.dlt_off, sg.in, sg.out, sg.bias, t.r0, t.nrows, t.c0});
+                works.push_back({sg.elem0, sg.xin_off, sg.dlt_off, sg.in, sg.out, sg.bias, t.r0, t.nrows, t.c0, sg.g_off});
             }
             // float4 tiles: a thread owns 4 consecutive columns of R4 rows; CTA =
             // threads4 threads (enough for the widest row, <= 256) covering
