@@ -825,8 +825,11 @@ size_t conv_plan(ConvArgs& a, int mode, size_t max_partial) {
         const long long mt = (long long)((a.M + 127) / 128) * ((a.N + 127) / 128);
         // one CTA per SM (544 threads): split K only as far as the tiles stay one wave
         // (splitting a multi-wave grid adds the partial traffic and buys nothing)
-        long long sp = std::max<long long>(1, 148 / mt);
+        static const long long wave = std::getenv("FERRET_CONV_WAVE") ? std::atoll(std::getenv("FERRET_CONV_WAVE")) : 148;
+        long long sp = std::max<long long>(1, wave / mt);
         sp = std::min<long long>(sp, std::max<long long>(1, katoms / 2));
+        if (const char* ms = std::getenv("FERRET_CONV_MAX_SPLITS"))  // experiment knob
+            sp = std::min<long long>(sp, std::max(1, std::atoi(ms)));
         const long long mn2 = (long long)a.M * a.N;
         if (max_partial) sp = std::min<long long>(sp, std::max<long long>(1, (long long)max_partial / mn2));
         const int C = mode == kConvFwd ? a.ci : a.co;
