@@ -348,6 +348,17 @@ struct GraphBuilder {
         p.kernelParams = k.kernel_params();
         cudaGraphNode_t n;
         cuda_check(cudaGraphAddKernelNode(&n, g, d.data(), d.size(), &p), "cudaGraphAddKernelNode");
+        // FERRET_NODE_PRIORITY=<class digits>: those node classes (1 predict, 2 forward,
+        // 3 backward, 4 update) run at the device's highest kernel priority, so the
+        // per-stage version chain (the DAG's critical path) is not queued behind others
+        static const char* prio = std::getenv("FERRET_NODE_PRIORITY");
+        if (prio && std::strchr(prio, '0' + cur_category)) {
+            int lo = 0, hi = 0;
+            cudaDeviceGetStreamPriorityRange(&lo, &hi);
+            cudaKernelNodeAttrValue v{};
+            v.priority = hi;
+            cuda_check(cudaGraphKernelNodeSetAttribute(n, cudaKernelNodeAttributePriority, &v), "node priority");
+        }
         commit(n, ld, reads, writes);
         ++kernels;
         return n;
