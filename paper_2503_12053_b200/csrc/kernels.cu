@@ -723,6 +723,31 @@ __global__ void __launch_bounds__(kThreads) update_iter1_kernel(const UpdArgs a)
         for (int b = 0; b < BT; ++b) g = fmaf(sdel[b * R + i], xv[b], g);
         return g;
     };
+    // rows in batches of RB, double-buffered: the loads of batch g + 1 are issued before the
+    // folds of batch g, so each batch costs one L2 round trip overlapped with the previous fold
+    // (not one per row); FERRET_UPDATE_PIPELINE=0 keeps the row-serial tail (experiment knob)
+    if (a.pipe) {
+        float nv_[RB][NV], nl[RB], nr[RB], na[RB];
+        for (int g0 = 0; g0 < R; g0 += RB) {
+            const int g1 = g0 + RB;
+#pragma unroll
+            for (int i = 0; i < RB; ++i)
+                if (g1 + i < R) load((size_t)w.elem0 + (size_t)(w.r0 + g1 + i) * w.in + c, nv_[i], nl[i], nr[i], na[i]);
+#pragma unroll
+            for (int i = 0; i < RB; ++i)
+                if (g0 + i < R)
+                    fold((size_t)w.elem0 + (size_t)(w.r0 + g0 + i) * w.in + c, grad(g0 + i), cv[i], ld[i], vr[i], va[i]);
+#pragma unroll
+            for (int i = 0; i < RB; ++i) {
+#pragma unroll
+                for (int q = 0; q < NV; ++q) cv[i][q] = nv_[i][q];
+                ld[i] = nl[i];
+                vr[i] = nr[i];
+                va[i] = na[i];
+            }
+        }
+        return;
+    }
 #pragma unroll
     for (int i = 0; i < RB; ++i)
         if (i < R) fold((size_t)w.elem0 + (size_t)(w.r0 + i) * w.in + c, grad(i), cv[i], ld[i], vr[i], va[i]);
@@ -1318,9 +1343,12 @@ void spec_update(const UpdArgs& a, KernelSpec& k) {
         return;
     }
     if (a.policy == 4 && a.K == 1 && a.nv <= 16 && a.lam_d != nullptr) {
+        static const bool pipe = !std::getenv("FERRET_UPDATE_PIPELINE") || std::atoi(std::getenv("FERRET_UPDATE_PIPELINE")) != 0;
+        UpdArgs b = a;
+        b.pipe = pipe ? 1 : 0;
         const void* f = a.B <= 1 ? iter1_func<1>(a.nv) : a.B <= 2 ? iter1_func<2>(a.nv) : a.B <= 4 ? iter1_func<4>(a.nv)
                       : a.B <= 8 ? iter1_func<8>(a.nv) : iter1_func<16>(a.nv);
-        fill(k, f, dim3((unsigned)blocks), dim3(kThreads), a);
+        fill(k, f, dim3((unsigned)blocks), dim3(kThreads), b);
         return;
     }
     const void* f = a.policy == 0 ? update_func<0>(a.B) : a.policy == 1 ? update_func<1>(a.B)

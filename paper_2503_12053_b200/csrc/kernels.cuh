@@ -123,7 +123,8 @@ struct UpdPending {
 // then theta_new = theta_cur - step * sum_k out_k, written to `dst`.
 struct UpdArgs {
     int n_segs, B, K, policy;
-    int gmat;                // some segment reads a materialised gradient (UpdSeg::g_off): generic kernel
+    int gmat;                // some segment reads a materialised gradient (UpdSeg::g_off)
+    int pipe;                // update_iter1_kernel: double-buffered row batches (set by spec_update)
     long long n_items;
     const UpdSeg* segs;      // device array
     const UpdTile* tiles;    // device array, one per CTA
