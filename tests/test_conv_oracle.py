@@ -94,3 +94,43 @@ def test_resnet18_layout():
     assert 10_900_000 < spec.n_params < 11_300_000, spec.n_params
     b = cn.balanced_bounds(spec, 4)
     assert len(b) == 5 and all(spec.valid_bound(x) for x in b[1:-1])
+
+
+def test_convnet_helpers():
+    """Host-side conv net description: widths chain, parameter / MAC counts, block-respecting
+    balanced partitions, the stage-rate inter-arrival time."""
+    spec = cn.resnet_cifar(width=16, blocks=(2, 2, 2, 2))
+    w = spec.widths
+    assert len(w) == spec.n_layers + 1
+    for l in range(spec.n_layers):
+        assert spec.in_width(l) == w[l] and spec.out_width(l) == w[l + 1]
+    assert spec.n_params == sum(spec.layer_params(l) for l in range(spec.n_layers))
+    assert spec.macs == sum(spec.layer_macs(l) for l in range(spec.n_layers))
+    for P in (2, 3, 4):
+        b = cn.balanced_bounds(spec, P)
+        assert b[0] == 0 and b[-1] == spec.n_layers and len(b) == P + 1
+        assert all(b[i] < b[i + 1] for i in range(P)) and all(spec.valid_bound(x) for x in b[1:-1])
+    prof = cn.profile(spec)
+    b = cn.balanced_bounds(spec, 4)
+    assert cn.stage_t_d(prof, b) == max(prof["t_f"][b[j]:b[j + 1]].sum() for j in range(4))
+    p1, p2 = cn.make_conv_net(spec, 1), cn.make_conv_net(spec, 1)
+    assert np.array_equal(p1, p2) and p1.size == spec.n_params
+
+
+def test_conv_geometry_validation(fb):
+    """The device trainer (plan-only, no GPU) rejects inconsistent geometry with FERRET_E_CONFIG."""
+    spec = cn.resnet_cifar(width=4, blocks=(1, 1), in_chw=(3, 8, 8))
+    params = cn.make_conv_net(spec, 1)
+    bounds = [0, spec.n_layers]
+    opt = fb.PipelineTrainOptions(device=-1)
+    fb.PipelineTrainer(spec, params, bounds, opt).close()
+    bad = cn.ConvNetSpec(spec.geom.copy(), spec.acts.copy())
+    bad.geom[1, 4] += 1  # c_out of layer 1 no longer matches its declared output width chain
+    with pytest.raises(fb.ConfigError):
+        fb.PipelineTrainer(bad, cn.make_conv_net(bad, 1), bounds, opt)
+    bad = cn.ConvNetSpec(spec.geom.copy(), spec.acts.copy())
+    bad.geom[1, 8] = 1  # a residual flag on the first conv of a block (layer 1: no block input)
+    with pytest.raises(fb.ConfigError):
+        fb.PipelineTrainer(bad, params, bounds, opt)
+    with pytest.raises(fb.ConfigError):
+        fb.PipelineTrainer(spec, params[:-1], bounds, opt)  # wrong parameter count
