@@ -246,9 +246,9 @@ __global__ void __launch_bounds__(kMmaThreads, 1) mma_layer_kernel(const __grid_
                 float4* A4 = reinterpret_cast<float4*>(sA + s * kTileBytes);
                 float4* L4 = reinterpret_cast<float4*>(sAlo + s * kTileBytes);
                 for (int e = t; e < kTileBytes / 16; e += kStagers) {
+                    // hi stays implicit (kind::tf32 drops the low 13 mantissa bits of the raw operand)
                     const float4 x = A4[e];
                     const float4 hi = make_float4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
-                    A4[e] = hi;
                     L4[e] = make_float4(x.x - hi.x, x.y - hi.y, x.z - hi.z, x.w - hi.w);
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
