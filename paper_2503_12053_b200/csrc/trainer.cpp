@@ -38,6 +38,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <set>
 #include <tuple>
 #include <memory>
 #include <sstream>
@@ -211,7 +212,7 @@ struct ChunkPlan {
 // concurrently, which is the pipeline parallelism of the 1F1B schedule
 // realised on one GPU. `serial` chains every node instead (timing mode).
 struct GraphBuilder {
-    enum : uint64_t { kVSlot = 1, kState, kStash, kPred, kNorm, kNormState, kPool, kReplay, kNormScratch };
+    enum : uint64_t { kVSlot = 1, kState, kStash, kPred, kNorm, kNormState, kPool, kReplay, kNormScratch, kWt };
     static uint64_t key(uint64_t kind, uint64_t a, uint64_t b = 0) { return (kind << 56) | (a << 32) | b; }
 
     cudaGraph_t g = nullptr;
@@ -1217,6 +1218,7 @@ struct ferret_trainer {
         cuda_check(cudaStreamSynchronize(stream), "sync");
         // timing / profile modes serialise the graph so events bracket one node each
         GraphBuilder builder(timing || profiling);
+        wt_valid.clear();  // tap-major weight copies are (re)prepared inside each graph
         if (profiling) builder.prof_events = &prof_events;
         gb = &builder;
         PassResult got;
@@ -1470,6 +1472,7 @@ struct ferret_trainer {
                         time_begin();
                         gb->cur_category = kCatUpdate; gb->cur_stage = j;
                         gb->kernel(k, rk, {vslot(j, cur + 1), GB::key(GB::kState, static_cast<uint64_t>(j))});
+                        wt_invalidate(stages[static_cast<size_t>(j)], a.dst);
                         time_end(update_bytes(j, opt.policy, reads, cur));
                     }
                     rel[static_cast<size_t>(j)] += 1;
@@ -1507,6 +1510,7 @@ struct ferret_trainer {
                     gb->cur_bytes = 8.0 * static_cast<double>(s.slot_floats);
                     gb->copy(s.ring, s.slot(fin), static_cast<size_t>(s.slot_floats) * sizeof(float), {vslot(j, fin)},
                              {vslot(j, 0)});
+                    wt_invalidate(s, s.ring);
                     if (s.ring16)
                         gb->copy(s.ring16, s.shadow(s.slot(fin)), static_cast<size_t>(s.slot_floats) * sizeof(uint16_t),
                                  {vslot(j, fin)}, {vslot(j, 0)});
@@ -1727,34 +1731,47 @@ struct ferret_trainer {
         if (it != conv_scratch.end()) return it->second;
         return conv_scratch[key] = dalloc<float>(kConvPartialCap, device_bytes);
     }
-    // tap-major weight copies for the tensor-core A operand, one region per written resource
-    std::map<uint64_t, float*> conv_wt;
-    float* conv_wt_for(uint64_t key) {
-        auto it = conv_wt.find(key);
-        if (it != conv_wt.end()) return it->second;
-        long long mx = 1;
-        for (const LayerDev& ld : layers)
-            if (ld.conv()) mx = std::max(mx, ld.nw());
-        return conv_wt[key] = dalloc<float>(static_cast<size_t>(mx), device_bytes);
+    // tap-major weight copies for the tensor-core A operand: one buffer per (weight version
+    // slot + layer, direction), valid from its prep node until the slot is rewritten
+    std::map<std::pair<const float*, int>, std::pair<float*, uint32_t>> wt_buf;
+    std::set<std::pair<const float*, int>> wt_valid;
+    void wt_invalidate(const StageDev& s, const float* slot) {
+        for (auto it = wt_valid.begin(); it != wt_valid.end();)
+            it = (it->first >= slot && it->first < slot + s.slot_floats) ? wt_valid.erase(it) : std::next(it);
     }
     void emit_conv(fb200::ConvArgs& c, int mode, const std::vector<uint64_t>& reads, const std::vector<uint64_t>& writes,
                    double bytes) {
         fb200::conv_plan(c, mode, kConvPartialCap);
         if (c.splits > 1) c.partial = conv_scratch_for(writes.at(0));
+        std::vector<uint64_t> rd = reads;
         if (c.kt && mode != fb200::kConvWgrad) {
-            c.Wt = conv_wt_for(writes.at(0));
-            fb200::KernelSpec kw;
-            fb200::spec_conv_wprep(c, mode, kw);
-            gb->cur_bytes = 8.0 * static_cast<double>(c.M) * c.K;
-            gb->kernel(kw, reads, writes);
+            // the tap-major copy of this weight version, prepared once per version inside the
+            // graph and reused by every launch that reads the version (predict, forward, input
+            // gradient, replay); the update writing the slot invalidates it (wt_invalidate)
+            const std::pair<const float*, int> k{c.W, mode};
+            auto it = wt_buf.find(k);
+            if (it == wt_buf.end()) {
+                float* buf = dalloc<float>(static_cast<size_t>(c.M) * c.K, device_bytes);
+                it = wt_buf.emplace(k, std::make_pair(buf, static_cast<uint32_t>(wt_buf.size()))).first;
+            }
+            c.Wt = it->second.first;
+            const uint64_t wk = GraphBuilder::key(GraphBuilder::kWt, it->second.second);
+            if (!wt_valid.count(k)) {
+                fb200::KernelSpec kw;
+                fb200::spec_conv_wprep(c, mode, kw);
+                gb->cur_bytes = 8.0 * static_cast<double>(c.M) * c.K;
+                gb->kernel(kw, reads, {wk});
+                wt_valid.insert(k);
+            }
+            rd.push_back(wk);
         }
         fb200::KernelSpec g, r;
         const int n = fb200::spec_conv(c, mode, g, r);
         gb->cur_bytes = bytes;
-        gb->kernel(g, reads, writes);
+        gb->kernel(g, rd, writes);
         if (n == 2) {
             gb->cur_bytes = 8.0 * c.splits * static_cast<double>(c.M) * c.N;
-            gb->kernel(r, reads, writes);
+            gb->kernel(r, rd, writes);
         }
     }
     // the weight and bias gradient of convolution `ld` into its stash region
@@ -2445,6 +2462,7 @@ struct ferret_trainer {
                 fb200::spec_update(a, k);
                 gb->cur_bytes = update_bytes(j, FERRET_POLICY_NONE, {cur}, cur);
                 gb->kernel(k, {rk, pk, vslot(j, cur)}, {vslot(j, cur + 1)});
+                wt_invalidate(stages[static_cast<size_t>(j)], a.dst);
             }
         }
         for (int j = 0; j < P; ++j) rel[static_cast<size_t>(j)] += 1;
