@@ -260,11 +260,17 @@ __global__ void __launch_bounds__(NT) conv_bgrad_kernel(const ConvArgs a) {
     __shared__ float part[NT / 32];
     const int ch = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int hw = a.ho * a.wo;
-    float v = 0.f;
-    for (int b = 0; b < a.B; ++b) {
-        const float* d = a.D + ((size_t)b * a.co + ch) * hw;
-        for (int p = threadIdx.x; p < hw; p += NT) v += __ldg(d + p);
+    // four independent accumulators (samples b mod 4) so the loads pipeline; combined in order
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int b0 = 0; b0 < a.B; b0 += 4) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (b0 + q >= a.B) break;
+            const float* d = a.D + ((size_t)(b0 + q) * a.co + ch) * hw;
+            for (int p = threadIdx.x; p < hw; p += NT) acc[q] += __ldg(d + p);
+        }
     }
+    float v = (acc[0] + acc[1]) + (acc[2] + acc[3]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if (lane == 0) part[w] = v;
