@@ -8,11 +8,13 @@
 //   fwd    C[c_out x B*HWo]   = W[c_out x c_in*k*k] . im2col(x)
 //   dgrad  C[c_in  x B*HWi]   = W^T (per tap) . scatter(delta)        (transposed conv)
 //   wgrad  C[c_out x c_in*k*k] = delta[c_out x B*HWo] . im2col(x)^T
-// 64 x 64 CTA tiles, K in steps of 16 through shared memory, 4 x 4 fp32
-// accumulators per thread (SIMT FFMA: the fp32 parity mode's arithmetic). Grids
-// with few tiles split K over blockIdx.z into a partial buffer, reduced in split
-// order by a second kernel that also runs the epilogue, so results do not depend
-// on scheduling (bitwise reproducible).
+// Two implementations: conv_mma_kernel (tcgen05 tensor cores, the default: 3xTF32
+// in the fp32 parity mode, tf32 in the fast modes) and conv_gemm_kernel (SIMT
+// FFMA, 64 x 64 CTA tiles, K in steps of 16 through shared memory, 4 x 4 fp32
+// accumulators per thread; FERRET_CONV_TC=0). Grids with few tiles split K over
+// blockIdx.z into a partial buffer, reduced in split order by a second kernel
+// that also runs the epilogue, so results do not depend on scheduling (bitwise
+// reproducible).
 #include "kernels.cuh"
 #include "umma.cuh"
 
@@ -305,16 +307,17 @@ __global__ void __launch_bounds__(NT) ungap_kernel(const PoolMeanArgs a) {
 // ---------------------------------------------------------------------------
 // Tensor-core implicit GEMM (tcgen05): 128 x 128 output tile per CTA, fp32
 // accumulator in 128 TMEM columns. 8 producer warps gather the A and B operands
-// of each 128-byte K atom straight from the activations / weights (the same
-// loaders as the SIMT kernel: the im2col matrix is never written to memory),
-// convert them to the MMA type and store them K-major with the 128-byte swizzle
-// into a 3-stage smem ring; one thread issues the MMAs (M 128, N 128, 4 per atom
-// in tf32 / bf16) and frees each stage with tcgen05.commit. 3xTF32 (the fp32
-// parity mode) splits both operands into tf32 hi + lo parts and issues
-// hi*hi + hi*lo + lo*hi. The epilogue reads TMEM (tcgen05.ld), transposes the
-// tile through smem so that global stores are coalesced along pixels, then runs
-// the SIMT kernel's epilogue (bias / shortcut / ReLU, skip / mask) or writes the
-// split-K partial (reduced in split order by conv_reduce_kernel).
+// of each 128-byte K atom straight from the activations / weights with cp.async
+// (4-byte element copies with zero fill for padding; 16-byte copies for the
+// contiguous rows of the tap-major prepared weights and of weight-gradient deltas)
+// into a 3-5 stage smem ring, K-major with the 128-byte swizzle; one thread issues
+// the MMAs (M 128, N 128, 4 per atom) and frees each stage with tcgen05.commit.
+// 3xTF32 (the fp32 parity mode) adds a tf32 lo tile per operand (lo = x - hi,
+// written by the thread that copied x; hi is the raw operand, which kind::tf32
+// truncates) and issues hi*hi + hi*lo + lo*hi. The epilogue reads TMEM
+// (tcgen05.ld), stages the tile through smem so global stores are coalesced along
+// pixels, then runs the SIMT kernel's epilogue (bias / shortcut / ReLU, skip /
+// mask) or writes the split-K partial (reduced in split order by conv_reduce_kernel).
 // ---------------------------------------------------------------------------
 // warp 0: TMEM + MMA issue; warps 1-8: producers (cp.async gathers), epilogue
 // Producer lag: a thread publishes atom i - LAG after issuing the copies of atom i. With
