@@ -182,3 +182,39 @@ def test_resnet18_full_width_parity(gpu, fb, orc):
     sched = fb.Schedule.forced(prof, t_d, fb.StreamSpec(t_d=t_d, horizon=n_units * t_d), bounds, n_units)
     got, ref = _compare(fb, orc, spec, params, feats, labels, sched, B=1, replay=True)
     assert np.isfinite(got).all()
+
+
+def test_conv_graph_segments_and_chunks_bitwise(gpu, fb, monkeypatch):
+    """The conv chunk graph cut every 40 nodes (long-log segments) and the stream replayed in
+    several chunks through one compiled graph give the same bits as one uncut graph: the
+    cached tap-major weight copies are re-prepared inside every segment / chunk as needed."""
+    spec, params, feats, labels, sched = _setup(fb, 8, (1, 1, 1, 1), 24, 4)
+    opt = fb.PipelineTrainOptions(policy="iter_fisher", micro_batch=4, replay=True, replay_seed=3)
+    out = []
+    for seg in (None, "40"):
+        if seg:
+            monkeypatch.setenv("FERRET_GRAPH_SEGMENT_NODES", seg)
+        tr = fb.PipelineTrainer(spec, params, sched.bounds, opt)
+        log = tr.run(sched.events, feats, labels)
+        out.append((log["predicted"].copy(), tr.params()))
+        tr.close()
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+    # the same 24-unit schedule replayed as 3 chunks of 8 units through one compiled graph
+    monkeypatch.delenv("FERRET_GRAPH_SEGMENT_NODES", raising=False)
+    feats3, labels3 = fb.synth_drift_stream(3 * 24 * 4, spec.in_width(0), 10, "split_tasks", 7)
+    a = fb.PipelineTrainer(spec, params, sched.bounds, opt)
+    a.load_stream(feats3, labels3)
+    a.set_schedule(sched.events, 24 * 4)
+    for c in range(3):
+        a.execute(c)
+    pa = a.params()
+    a.close()
+    b = fb.PipelineTrainer(spec, params, sched.bounds, opt)
+    b.load_stream(feats3, labels3)
+    b.set_schedule(sched.events, 24 * 4)
+    for c in range(3):
+        b.execute(c)
+    pb = b.params()
+    b.close()
+    assert np.array_equal(pa, pb) and np.isfinite(pa).all()
+    assert np.linalg.norm(pa - params) > 0
