@@ -218,3 +218,39 @@ def test_conv_graph_segments_and_chunks_bitwise(gpu, fb, monkeypatch):
     b.close()
     assert np.array_equal(pa, pb) and np.isfinite(pa).all()
     assert np.linalg.norm(pa - params) > 0
+
+
+def test_conv_multi_chunk_replay_vs_oracle(gpu, fb, orc):
+    """One compiled chunk graph replayed over consecutive stream chunks (state carried in HBM:
+    version rings, compensator, normalizer, replay reservoir) equals the oracle on the
+    concatenated log (items offset per chunk)."""
+    spec = cn.resnet_cifar(width=8, blocks=(1, 1, 1, 1))
+    params = cn.make_conv_net(spec, 1)
+    bounds = cn.balanced_bounds(spec, 4)
+    prof = cn.profile(spec)
+    t_d = cn.stage_t_d(prof, bounds)
+    units, chunks, B = 16, 3, 2
+    sched = fb.Schedule.forced(prof, t_d, fb.StreamSpec(t_d=t_d, horizon=units * t_d), bounds, units)
+    feats, labels = fb.synth_drift_stream(chunks * units * B, spec.in_width(0), 10, "split_tasks", 7)
+    opt = fb.PipelineTrainOptions(policy="iter_fisher", micro_batch=B, replay=True, replay_seed=3)
+    tr = fb.PipelineTrainer(spec, params, bounds, opt)
+    tr.load_stream(feats, labels)
+    tr.set_schedule(sched.events, units * B)
+    logs = []
+    for c in range(chunks):
+        tr.execute(c)
+        logs.append(tr.fetch_log(c))
+    got = tr.params()
+    tr.close()
+    ev = []
+    for c in range(chunks):
+        e = sched.events.copy()
+        e["item"] += c * units
+        ev.append(e)
+    ref = orc.train_conv(spec.geom, spec.acts, params, bounds, np.concatenate(ev), feats, labels, policy="iter_fisher",
+                         replay=True, replay_seed=3, micro_batch=B)
+    for j, (lo, hi) in enumerate(_slices(spec, bounds)):
+        rel = np.linalg.norm(got[lo:hi] - ref["params"][lo:hi]) / np.linalg.norm(ref["params"][lo:hi])
+        assert rel < PARAM_RTOL, f"stage {j}: param rel err {rel:.3e}"
+    log = np.concatenate(logs)
+    assert np.count_nonzero(log["predicted"] != ref["log"]["predicted"]) <= 2
