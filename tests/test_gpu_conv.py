@@ -254,3 +254,49 @@ def test_conv_multi_chunk_replay_vs_oracle(gpu, fb, orc):
         assert rel < PARAM_RTOL, f"stage {j}: param rel err {rel:.3e}"
     log = np.concatenate(logs)
     assert np.count_nonzero(log["predicted"] != ref["log"]["predicted"]) <= 2
+
+
+def test_conv_exact_resume(gpu, fb):
+    """ferret-state v1 for a conv net (the header carries the geometry): 3 chunks straight vs
+    1 chunk, save, a fresh trainer loads and runs 2 more — identical bits; a state saved by a
+    net of another geometry is refused (SchemaError)."""
+    spec = cn.resnet_cifar(width=8, blocks=(1, 1, 1, 1))
+    params = cn.make_conv_net(spec, 1)
+    bounds = cn.balanced_bounds(spec, 4)
+    prof = cn.profile(spec)
+    t_d = cn.stage_t_d(prof, bounds)
+    units, chunks, B = 16, 3, 2
+    sched = fb.Schedule.forced(prof, t_d, fb.StreamSpec(t_d=t_d, horizon=units * t_d), bounds, units)
+    feats, labels = fb.synth_drift_stream(chunks * units * B, spec.in_width(0), 10, "split_tasks", 7)
+    opt = fb.PipelineTrainOptions(policy="iter_fisher", micro_batch=B, replay=True, replay_seed=3)
+
+    def trainer(s=spec, p=params):
+        t = fb.PipelineTrainer(s, p, bounds, opt)
+        t.load_stream(feats, labels)
+        t.set_schedule(sched.events, units * B)
+        return t
+
+    a = trainer()
+    for c in range(chunks):
+        a.execute(c)
+    pa, la = a.params(), a.fetch_log(chunks - 1)
+    a.close()
+    b = trainer()
+    b.execute(0)
+    state = b.save_state()
+    b.close()
+    assert state.startswith(b"ferret-state v1\n") and b"geometry " in state[:4096]
+    c = trainer()
+    c.load_state(state)
+    for k in range(1, chunks):
+        c.execute(k)
+    pc, lc = c.params(), c.fetch_log(chunks - 1)
+    c.close()
+    assert np.array_equal(pa, pc) and np.array_equal(la, lc)
+    other = cn.ConvNetSpec(spec.geom.copy(), spec.acts.copy())
+    other.geom[1, 7] = 0  # padding 0 instead of 1: a different net with the same widths chain?
+    other.geom[1, 5] = 1  # 1x1 kernel keeps the map size, changes the parameter count
+    d = fb.PipelineTrainer(other, cn.make_conv_net(other, 1), bounds, opt)
+    with pytest.raises(fb.SchemaError):
+        d.load_state(state)
+    d.close()
