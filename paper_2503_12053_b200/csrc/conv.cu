@@ -330,8 +330,11 @@ __global__ void __launch_bounds__(NT) ungap_kernel(const PoolMeanArgs a) {
 #define FERRET_CONV_LAG (NST / FERRET_CONV_LAG_DIV > 0 ? NST / FERRET_CONV_LAG_DIV : 1)
 constexpr int kCP = 256;
 constexpr int kCT = 32 + kCP;
-// smem ring depth: 3 x 64 KB (3xTF32: hi + lo operands) or 5 x 32 KB
-__host__ __device__ constexpr int conv_stages(bool split) { return split ? 3 : 5; }
+// smem ring depth: 3 x 64 KB (3xTF32: raw + lo operands) or 3 x 32 KB (tf32)
+// (3 x 32 KB for tf32 keeps two CTAs per SM resident — 2 x 97 KB smem, 2 x 288 x <= 107
+// registers — so one CTA's producer / MMA handshake overlaps the other's: +4 % over 5 stages
+// at one CTA per SM)
+__host__ __device__ constexpr int conv_stages(bool split) { return 3; }
 constexpr int kCTile = 16384;  // 128 rows x 128 bytes
 
 // Operand element sources of the tensor-core kernel (nullptr = zero: padding,
@@ -513,7 +516,7 @@ __device__ __forceinline__ void locate_b(const ConvArgs& a, const Col& c, int k0
 }
 
 template <int MODE, int ES, bool SPLIT>
-__global__ void __launch_bounds__(kCT, 1) conv_mma_kernel(const __grid_constant__ ConvArgs a) {
+__global__ void __launch_bounds__(kCT, SPLIT ? 1 : 2) conv_mma_kernel(const __grid_constant__ ConvArgs a) {
     constexpr int KA = 128 / ES;  // K elements per atom
     constexpr int UK = 32 / ES;   // K per MMA
     constexpr int CE = 16 / ES;   // elements per 16-byte chunk
@@ -835,7 +838,8 @@ size_t conv_plan(ConvArgs& a, int mode, size_t max_partial) {
         const long long mt = (long long)((a.M + 127) / 128) * ((a.N + 127) / 128);
         // one CTA per SM (544 threads): split K only as far as the tiles stay one wave
         // (splitting a multi-wave grid adds the partial traffic and buys nothing)
-        static const long long wave = std::getenv("FERRET_CONV_WAVE") ? std::atoll(std::getenv("FERRET_CONV_WAVE")) : 148;
+        static const char* wave_env = std::getenv("FERRET_CONV_WAVE");
+        const long long wave = wave_env ? std::atoll(wave_env) : (a.tc == 3 ? 148 : 296);
         long long sp = std::max<long long>(1, wave / mt);
         sp = std::min<long long>(sp, std::max<long long>(1, katoms / 2));
         if (const char* ms = std::getenv("FERRET_CONV_MAX_SPLITS"))  // experiment knob
