@@ -221,7 +221,7 @@ class PipelineTrainer {
     ferret_trainer* handle() { return handle_.get(); }
 
     /// Exact resume (no reference counterpart; extends ferret-ckpt v1, net.hpp:210-259,
-    /// with the trainer state): "ferret-state v1" between run() calls.
+    /// with the trainer state): "ferret-state v2" between run() calls.
     void save_state(const std::string& path) {
         std::size_t n = 0;
         b200_check(ferret_trainer_save_state(handle_.get(), nullptr, 0, &n));

@@ -270,6 +270,13 @@ FERRET_API ferret_status ferret_trainer_comp_state(ferret_trainer* t, int32_t st
 /* TrainOutcome::normalizer (learner.hpp:180): count, mean[f], m2[f] */
 FERRET_API ferret_status ferret_trainer_normalizer(ferret_trainer* t, uint64_t* count, double* mean, double* m2,
                                         size_t n_features);
+/* The replay draws made so far (ReplayBuffer::sample, learner.hpp:75-78, called by
+ * replay_step :513-519): the stream sample index of every drawn sample, in draw order,
+ * across every run/execute/ingest call of this trainer (B draws per replay step at
+ * micro-batch B). Writes min(cap, total) indices to `out` (may be NULL) and the total
+ * to *n. The reservoir arithmetic is the reference's (same mt19937_64 draws), so these
+ * equal the reference trainer's replay indices element for element. */
+FERRET_API ferret_status ferret_trainer_replay_draws(ferret_trainer* t, int64_t* out, size_t cap, size_t* n);
 /* counters of the last execute/run: kernel launches, ring depth per stage, ... */
 typedef struct {
     uint64_t kernel_launches;
@@ -314,7 +321,7 @@ FERRET_API ferret_status ferret_trainer_update_timing(ferret_trainer* t, double*
                                                       double* alg_bytes);
 
 /* Exact resume (ferret-ckpt v1, net.hpp:210-259, extended with the
- * trainer state): "ferret-state v1" = text header (net shape, bounds, options,
+ * trainer state): "ferret-state v2" = text header (net shape, bounds, options,
  * normalizer count, version counters, replay reservoir RNG state and labels)
  * + raw arrays (live parameters per stage in the device slot layout,
  * compensator state, normalizer mean/M2, replay pool rows). Valid between

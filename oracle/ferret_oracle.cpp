@@ -26,11 +26,16 @@
 //   ferret::train_pipeline unchanged instead.
 //
 // Parity status: the host tiers are the reference itself; the trainer
-// restatement is pinned by (a) equality with the reference's train_pipeline
-// whenever the reference trains at all (as-shipped path, predictions only),
-// (b) the SPEC worked examples in tests/test_oracle_kats.py, and (c) the
-// replay-index cross-check below (restated index reservoir vs the reference
-// ReplayBuffer's returned sample, asserted on every draw).
+// restatement is pinned by (a) bit-for-bit equality (log and parameters, every
+// policy, with and without replay, micro-batch 1) with the reference's own
+// train_pipeline built from learner.hpp with only the in-flight key patched
+// (keyed_ref.cpp; tests/test_abi_and_oracle.py::
+// test_restatement_equals_key_patched_reference), (b) equality with the
+// as-shipped reference where it trains at all (predictions before the first
+// update; tests/test_abi_and_oracle.py), (c) the SPEC worked examples
+// (tests/cpp/host_kats.cpp -> tests/golden/host_kats.txt, tests/test_host_parity.py),
+// and (d) the replay-index cross-check below (restated index reservoir vs the
+// reference ReplayBuffer's returned sample, asserted on every draw).
 #include <cstdint>
 #include <cstring>
 #include <map>
@@ -70,7 +75,7 @@ int guard(F&& f) {
 }
 
 // layout mirrors of the product's C structs (ferret_b200.h); kept in sync by
-// tests/test_abi.py which checks sizes against ctypes.
+// tests/test_abi_and_oracle.py, which checks their sizes against ctypes.
 struct OEvent {
     double time;
     int32_t kind, worker, stage, staleness;

@@ -177,6 +177,39 @@ def train(widths, params, bounds, events, features, labels, policy="none", lr=1e
     return out
 
 
+KEYED_PATH = os.path.join(HERE, "_ref", "libferret_keyed.so")
+_keyed: Optional[C.CDLL] = None
+
+
+def keyed_train(widths, params, bounds, events, features, labels, policy="none", lr=1e-3, eta_lambda=1e-3,
+                replay=False, replay_seed=0) -> dict:
+    """The reference's own train_pipeline with only its in-flight key patched to the item
+    (learner.hpp:408,413,436,483; oracle/keyed_ref.cpp), fp64, micro-batch 1."""
+    global _keyed
+    if _keyed is None:
+        if not os.path.exists(KEYED_PATH):
+            raise FileNotFoundError(f"{KEYED_PATH} missing: build it with `make -C oracle`")
+        _keyed = C.CDLL(KEYED_PATH)
+        _keyed.ferret_keyed_last_error.restype = C.c_char_p
+    w = np.ascontiguousarray(widths, dtype=np.uint64)
+    p = np.ascontiguousarray(params, dtype=np.float64)
+    b = np.ascontiguousarray(bounds, dtype=np.uint64)
+    ev = np.ascontiguousarray(events, dtype=EVENT_DTYPE)
+    f = np.ascontiguousarray(features, dtype=np.float64)
+    lab = np.ascontiguousarray(labels, dtype=np.uint64)
+    n, F = f.shape
+    log = np.zeros(n, dtype=RECORD_DTYPE)
+    out = np.zeros(p.size, dtype=np.float64)
+    rc = _keyed.ferret_keyed_train(_up(w), C.c_int32(len(w)), _dp(p), _up(b), C.c_int32(len(b)),
+                                   C.c_int32(POLICIES[policy]), C.c_double(lr), C.c_double(eta_lambda),
+                                   C.c_int32(int(replay)), C.c_uint64(replay_seed), C.c_void_p(ev.ctypes.data),
+                                   C.c_size_t(len(ev)), _dp(f), _up(lab), C.c_size_t(n), C.c_size_t(F),
+                                   C.c_void_p(log.ctypes.data), _dp(out))
+    if rc != 0:
+        raise RuntimeError("keyed reference: " + _keyed.ferret_keyed_last_error().decode())
+    return {"params": out, "log": log}
+
+
 def compensate(policy, g, chain, lam=None, v_r=None, v_a=None, mean_gap=None, alpha=0.99, eta=0.0, nu=2e-6):
     g = np.ascontiguousarray(g, dtype=np.float64)
     n = g.size

@@ -109,9 +109,11 @@ struct Reservoir {
     Reservoir() = default;
     Reservoir(uint64_t capacity, uint64_t seed) : cap(capacity), rng(seed ^ 0xbf58476d1ce4e5b9ULL) {}
 
-    std::vector<int> label_at;  // label of the sample held at each pool position
+    std::vector<int> label_at;      // label of the sample held at each pool position
+    std::vector<int64_t> id_at;     // stream sample index held at each pool position
+    std::vector<int64_t> draws;     // stream sample index of every replay draw, in draw order
 
-    int add(int label) {  // pool position the new sample is written to, or -1
+    int add(int label, int64_t id) {  // pool position the new sample is written to, or -1
         ++seen;
         int pos = -1;
         if (size < cap) {
@@ -123,10 +125,16 @@ struct Reservoir {
         if (pos >= 0) {
             if (label_at.size() <= static_cast<size_t>(pos)) label_at.resize(static_cast<size_t>(pos) + 1);
             label_at[static_cast<size_t>(pos)] = label;
+            if (id_at.size() <= static_cast<size_t>(pos)) id_at.resize(static_cast<size_t>(pos) + 1, -1);
+            id_at[static_cast<size_t>(pos)] = id;
         }
         return pos;
     }
-    int sample() { return static_cast<int>(rng.below(size)); }
+    int sample() {
+        const int pos = static_cast<int>(rng.below(size));
+        draws.push_back(static_cast<size_t>(pos) < id_at.size() ? id_at[static_cast<size_t>(pos)] : -1);
+        return pos;
+    }
 };
 
 struct HostState {
@@ -329,13 +337,6 @@ struct GraphBuilder {
         if (eager) {
             cuda_check(fb200::launch_spec(k, eager), "kernel launch");
             ++kernels;
-            cur_bytes = 0.0;
-            return nullptr;
-        }
-        // FERRET_EXPERIMENT_SKIP_CLASS=<class digits> (timing ablation only, results invalid):
-        // node classes 1 predict, 2 forward, 3 backward, 4 update are left out of the graph
-        static const char* skip = std::getenv("FERRET_EXPERIMENT_SKIP_CLASS");
-        if (skip && std::strchr(skip, '0' + cur_category)) {
             cur_bytes = 0.0;
             return nullptr;
         }
@@ -552,17 +553,21 @@ struct ferret_trainer {
         inbox_data_bytes = plan.inbox_bytes;
         const size_t data = (inbox_data_bytes[static_cast<size_t>(rank)] + 255) / 256 * 256;
         const size_t need = data + plan.inbox_flags[static_cast<size_t>(rank)] * sizeof(unsigned) + 256;
+        cuda_check(cudaStreamSynchronize(stream), "sync");
         if (need > inbox_alloc) {
-            cuda_check(cudaStreamSynchronize(stream), "sync");
             dfree(d_inbox);
             d_inbox = dalloc<unsigned char>(need, device_bytes);
             inbox_alloc = need;
-            for (size_t p = 0; p < peer_opened.size(); ++p)
-                if (peer_opened[p]) cudaIpcCloseMemHandle(peer_opened[p]);
-            peer_opened.assign(static_cast<size_t>(world), nullptr);
-            std::fill(peer_data.begin(), peer_data.end(), nullptr);
-            std::fill(peer_flags.begin(), peer_flags.end(), nullptr);
         }
+        // every schedule change re-opens the peers: a peer may have reallocated its inbox, and
+        // the flag offsets inside it follow the new plan's data size (stale mappings would
+        // publish flags at the old plan's positions)
+        for (size_t p = 0; p < peer_opened.size(); ++p)
+            if (peer_opened[p]) cudaIpcCloseMemHandle(peer_opened[p]);
+        peer_opened.assign(static_cast<size_t>(world), nullptr);
+        std::fill(peer_data.begin(), peer_data.end(), nullptr);
+        std::fill(peer_flags.begin(), peer_flags.end(), nullptr);
+        invalidate_graph();
         cuda_check(cudaMemset(d_inbox, 0, inbox_alloc), "memset inbox");  // flags start below every epoch
         peer_data[static_cast<size_t>(rank)] = reinterpret_cast<float*>(d_inbox);
         peer_flags[static_cast<size_t>(rank)] = reinterpret_cast<unsigned*>(d_inbox + data);
@@ -650,6 +655,8 @@ struct ferret_trainer {
             dfree(kv.second.first);
             dfree(kv.second.second);
         }
+        wt_reset();
+        for (auto& kv : conv_scratch) dfree(kv.second);
         for (void* p : {static_cast<void*>(d_raw), static_cast<void*>(d_lab), static_cast<void*>(d_pred),
                         static_cast<void*>(d_norm_mean), static_cast<void*>(d_norm_m2), static_cast<void*>(d_rawc),
                         static_cast<void*>(d_norm_mu), static_cast<void*>(d_norm_m2i),
@@ -1123,7 +1130,7 @@ struct ferret_trainer {
     // Walks the log exactly like the reference trainer's buffer_ calls
     // (learner.hpp:409 add at every non-dropped arrival, :509/:514 sample at
     // every firing stage-0 update while non-empty).
-    ChunkPlan plan_chunk(Reservoir& res, const int* chunk_labels) const {
+    ChunkPlan plan_chunk(Reservoir& res, const int* chunk_labels, int64_t sample_base) const {
         ChunkPlan cp;
         cp.pool_dst.assign(sched.chunk_items, -1);
         if (!opt.replay || opt.as_shipped) return cp;
@@ -1132,7 +1139,7 @@ struct ferret_trainer {
             if (e.kind == FERRET_EV_ARRIVAL && !sched.dropped[static_cast<size_t>(e.item)]) {
                 for (int b = 0; b < B; ++b) {
                     const size_t s = static_cast<size_t>(e.item) * static_cast<size_t>(B) + static_cast<size_t>(b);
-                    cp.pool_dst[s] = res.add(chunk_labels[s]);
+                    cp.pool_dst[s] = res.add(chunk_labels[s], sample_base + static_cast<int64_t>(s));
                 }
             } else if (e.kind == FERRET_EV_UPDATE && e.stage == 0 && sched.update_fires[i] && res.size > 0) {
                 for (int b = 0; b < B; ++b) {
@@ -1165,7 +1172,7 @@ struct ferret_trainer {
             invalidate_graph();
         if (!graph_exec) build_graph(seen_any);
         // host decisions for this chunk
-        const ChunkPlan cp = plan_chunk(hs.replay, chunk_labels);
+        const ChunkPlan cp = plan_chunk(hs.replay, chunk_labels, static_cast<int64_t>(hs.norm_count));
         if (cp.n_replays != graph_shape.n_replays)
             fail(FERRET_E_LOGIC, "replay pattern of this chunk differs from the compiled graph");
         // control block -> device (double-buffered pinned staging)
@@ -1218,7 +1225,7 @@ struct ferret_trainer {
         cuda_check(cudaStreamSynchronize(stream), "sync");
         // timing / profile modes serialise the graph so events bracket one node each
         GraphBuilder builder(timing || profiling);
-        wt_valid.clear();  // tap-major weight copies are (re)prepared inside each graph
+        wt_reset();  // tap-major weight copies are (re)allocated and (re)prepared inside each graph
         if (profiling) builder.prof_events = &prof_events;
         gb = &builder;
         PassResult got;
@@ -1735,6 +1742,17 @@ struct ferret_trainer {
     // slot + layer, direction), valid from its prep node until the slot is rewritten
     std::map<std::pair<const float*, int>, std::pair<float*, uint32_t>> wt_buf;
     std::set<std::pair<const float*, int>> wt_valid;
+    size_t wt_bytes = 0;
+    // Called before every graph build (the previous graph is already destroyed): ring
+    // reallocation (grow_ring) may hand a freed slot's address to another stage or layer,
+    // so a pointer-keyed buffer must never outlive the graph it was sized for.
+    void wt_reset() {
+        for (auto& kv : wt_buf) dfree(kv.second.first);
+        device_bytes -= wt_bytes;
+        wt_bytes = 0;
+        wt_buf.clear();
+        wt_valid.clear();
+    }
     void wt_invalidate(const StageDev& s, const float* slot) {
         for (auto it = wt_valid.begin(); it != wt_valid.end();)
             it = (it->first >= slot && it->first < slot + s.slot_floats) ? wt_valid.erase(it) : std::next(it);
@@ -1752,6 +1770,7 @@ struct ferret_trainer {
             auto it = wt_buf.find(k);
             if (it == wt_buf.end()) {
                 float* buf = dalloc<float>(static_cast<size_t>(c.M) * c.K, device_bytes);
+                wt_bytes += static_cast<size_t>(c.M) * c.K * sizeof(float);
                 it = wt_buf.emplace(k, std::make_pair(buf, static_cast<uint32_t>(wt_buf.size()))).first;
             }
             c.Wt = it->second.first;
@@ -1797,8 +1816,6 @@ struct ferret_trainer {
     template <bool DRY, class Xfer, class VSlot, class NGroup>
     void emit_predict(size_t u, const std::vector<long long>& rel, int slot, Xfer& xfer, VSlot& vslot, NGroup& ngroup) {
         using GB = GraphBuilder;
-        static const bool skip = std::getenv("FERRET_EXPERIMENT_SKIP_PREDICT") != nullptr;  // timing experiment only
-        if (skip && !DRY) return;
         float* scratch = (slot >= 0 ? d_stash + static_cast<long long>(slot) * stash_stride : d_replay) + pred_off;
         const uint64_t sk = slot >= 0 ? GB::key(GB::kPred, static_cast<uint64_t>(slot)) : GB::key(GB::kReplay, 0);
         const float* x0 = d_xc + u * static_cast<size_t>(B) * static_cast<size_t>(F);
@@ -1969,13 +1986,25 @@ struct ferret_trainer {
     }
 
     // ------------------------------------------------ exact resume
-    // "ferret-state v1": everything a pipeline trainer carries from one chunk to
+    // "ferret-state v2": everything a pipeline trainer carries from one chunk to
     // the next — the live parameters of every stage (ring slot 0 between chunks),
     // the compensator state, the RunningNormalizer, the version counters and the
     // replay reservoir (host RNG state, positions' labels, pool rows). A text
     // header (shape and options, checked on load) followed by raw little-endian
     // arrays in the device slot layout. Loading it into a trainer built with the
     // same net, bounds and options continues training bit for bit.
+    // the options a saved state depends on; the compensator constants and lr are written as
+    // exact hex floats (lambda is stored as an offset from lambda0, so a state is only valid
+    // for the lambda0 it was saved with)
+    std::string options_line() const {
+        std::ostringstream o;
+        o << "options policy " << opt.policy << " replay " << opt.replay << " capacity " << opt.replay_capacity
+          << " precision " << opt.precision << " micro_batch " << B << std::hexfloat << " lr " << opt.lr
+          << " lambda0 " << opt.lambda0 << " eta_lambda " << opt.eta_lambda << " alpha " << opt.alpha << " nu "
+          << opt.nu;
+        return o.str();
+    }
+
     std::string save_state() {
         if (sq.on) fail(FERRET_E_CONFIG, "save_state: sequential learners carry no pipeline state");
         cuda_check(cudaStreamSynchronize(stream), "sync");
@@ -1998,18 +2027,20 @@ struct ferret_trainer {
             put_dev(d_pool_lab, static_cast<size_t>(hs.replay.size) * sizeof(int));
         }
         std::ostringstream h;
-        h << "ferret-state v1\n" << "layers";
+        h << "ferret-state v2\n" << "layers";
         for (const LayerDev& ld : layers) h << ' ' << ld.in << 'x' << ld.out << ':' << ld.act;
         for (size_t i = 0; i < geom.size(); ++i) h << (i ? "," : "\ngeometry ") << geom[i];
         h << "\nbounds";
         for (const StageDev& st : stages) h << ' ' << st.lo;
-        h << ' ' << L << "\noptions policy " << opt.policy << " replay " << opt.replay << " capacity "
-          << opt.replay_capacity << " precision " << opt.precision << " micro_batch " << B << "\n"
+        h << ' ' << L << "\n" << options_line() << "\n"
           << "norm_count " << hs.norm_count << "\nversions";
         for (long long v : hs.current) h << ' ' << v;
         h << "\nreservoir " << hs.replay.seen << ' ' << hs.replay.size << "\nrng " << hs.replay.rng.state()
           << "\nlabels";
         for (uint64_t i = 0; i < hs.replay.size; ++i) h << ' ' << hs.replay.label_at[static_cast<size_t>(i)];
+        h << "\nids";
+        for (uint64_t i = 0; i < hs.replay.size; ++i)
+            h << ' ' << (i < hs.replay.id_at.size() ? hs.replay.id_at[static_cast<size_t>(i)] : -1);
         h << "\nbinary " << bin.size() << "\n";
         return h.str() + bin;
     }
@@ -2022,7 +2053,7 @@ struct ferret_trainer {
         auto expect = [&](const std::string& want) {
             if (!std::getline(in, line) || line != want) fail(FERRET_E_SCHEMA, "state: expected '" + want + "'");
         };
-        expect("ferret-state v1");
+        expect("ferret-state v2");
         {
             std::ostringstream l, b, o;
             l << "layers";
@@ -2031,8 +2062,7 @@ struct ferret_trainer {
             b << "bounds";
             for (const StageDev& st : stages) b << ' ' << st.lo;
             b << ' ' << L;
-            o << "options policy " << opt.policy << " replay " << opt.replay << " capacity " << opt.replay_capacity
-              << " precision " << opt.precision << " micro_batch " << B;
+            o << options_line();
             std::istringstream ls(l.str());  // "layers" and, for conv nets, "geometry"
             for (std::string want; std::getline(ls, want);) expect(want);
             expect(b.str());
@@ -2070,10 +2100,28 @@ struct ferret_trainer {
             for (int& x : labels)
                 if (!(f >> x)) fail(FERRET_E_SCHEMA, "state: bad labels");
         }
+        std::vector<int64_t> ids(static_cast<size_t>(size));
+        {
+            auto f = record("ids");
+            for (int64_t& x : ids)
+                if (!(f >> x)) fail(FERRET_E_SCHEMA, "state: bad ids");
+        }
         size_t nbin = 0;
         if (!(record("binary") >> nbin)) fail(FERRET_E_SCHEMA, "state: bad binary size");
         const size_t off = static_cast<size_t>(in.tellg());
         if (off + nbin != len) fail(FERRET_E_SCHEMA, "state: binary section size mismatch");
+        {  // the expected binary layout, checked before any device slot is overwritten
+            size_t want = 0;
+            for (const StageDev& st : stages) {
+                size_t arrays = 1;
+                for (const float* a : {st.lam_d, st.v_r, st.v_a, st.gap})
+                    if (a) ++arrays;
+                want += arrays * static_cast<size_t>(st.slot_floats) * sizeof(float);
+            }
+            want += 2 * static_cast<size_t>(F) * sizeof(double);
+            if (opt.replay && size) want += static_cast<size_t>(size) * (static_cast<size_t>(F) * sizeof(float) + sizeof(int));
+            if (nbin != want) fail(FERRET_E_SCHEMA, "state: binary section does not match this trainer's layout");
+        }
         const char* p = data + off;
         size_t left = nbin;
         auto take_dev = [&](void* dev, size_t bytes) {
@@ -2112,6 +2160,8 @@ struct ferret_trainer {
         hs.replay.size = size;
         hs.replay.rng.restore(rng_state);
         hs.replay.label_at = labels;
+        hs.replay.id_at = ids;
+        hs.replay.draws.clear();
     }
 
     // ------------------------------------------------ sequential learners
@@ -2362,7 +2412,7 @@ struct ferret_trainer {
                 seq_labels[2 * k + 1] = hs.replay.label_at[static_cast<size_t>(src[k])];
                 rows[k] = 2;
             }
-            if (opt.replay) dst[k] = hs.replay.add(seq_labels[2 * k]);
+            if (opt.replay) dst[k] = hs.replay.add(seq_labels[2 * k], kept[k]);
         }
         cuda_check(cudaMemcpyAsync(sq.d_lab, seq_labels.data(), 2 * n_kept * sizeof(int), cudaMemcpyHostToDevice, stream),
                    "H2D labels");
@@ -2584,6 +2634,9 @@ struct ferret_trainer {
 
     void ingest(const double* features, const uint64_t* lab, size_t n, size_t f, ferret_step_record* log) {
         if (!have_schedule) fail(FERRET_E_LOGIC, "ingest: no schedule set");
+        // stage-sharded trainers reuse their inboxes every chunk and need a barrier between
+        // chunks, which a multi-chunk call cannot insert
+        if (world > 1) fail(FERRET_E_CONFIG, "ingest: not available on a stage-sharded trainer (world > 1)");
         if (static_cast<int>(f) != F) fail(FERRET_E_INVALID_ARG, "stream feature width does not match the net input");
         const size_t chunk = sched.chunk_items;
         if (n % chunk) fail(FERRET_E_INVALID_ARG, "ingest: sample count must be a whole number of chunks");
@@ -2923,6 +2976,16 @@ ferret_status ferret_trainer_comp_state(ferret_trainer* t, int32_t stage, double
         if (v_r) t->read_state(stage, s.v_r, v_r, n, 0.0);
         if (v_a) t->read_state(stage, s.v_a, v_a, n, 0.0);
         if (mean_gap) t->read_state(stage, s.gap, mean_gap, n, 0.0);
+    });
+}
+
+ferret_status ferret_trainer_replay_draws(ferret_trainer* t, int64_t* out, size_t cap, size_t* n) {
+    return guarded([&] {
+        if (!t) fail(FERRET_E_INVALID_ARG, "replay_draws: null trainer");
+        const std::vector<int64_t>& d = t->hs.replay.draws;
+        if (out)
+            for (size_t i = 0; i < d.size() && i < cap; ++i) out[i] = d[i];
+        if (n) *n = d.size();
     });
 }
 

@@ -138,6 +138,7 @@ def lib() -> C.CDLL:
         "ferret_trainer_params": (C.c_int, [C.c_void_p, P(D), C.c_size_t]),
         "ferret_trainer_comp_state": (C.c_int, [C.c_void_p, C.c_int32, P(D), P(D), P(D), P(D), C.c_size_t]),
         "ferret_trainer_normalizer": (C.c_int, [C.c_void_p, P(C.c_uint64), P(D), P(D), C.c_size_t]),
+        "ferret_trainer_replay_draws": (C.c_int, [C.c_void_p, P(C.c_int64), C.c_size_t, P(C.c_size_t)]),
         "ferret_trainer_get_stats": (C.c_int, [C.c_void_p, P(TrainerStats)]),
         "ferret_trainer_destroy": (None, [C.c_void_p]),
         "ferret_trainer_set_timing": (C.c_int, [C.c_void_p, C.c_int32]),
@@ -445,7 +446,7 @@ class PipelineTrainer:
         return out
 
     def save_state(self) -> bytes:
-        """ferret-state v1 (exact resume between execute()/run() calls)."""
+        """ferret-state v2 (exact resume between execute()/run() calls)."""
         n = C.c_size_t()
         _check(lib().ferret_trainer_save_state(self._h, None, 0, C.byref(n)))
         buf = C.create_string_buffer(n.value)
@@ -466,6 +467,17 @@ class PipelineTrainer:
         m2 = np.empty(n_features, dtype=np.float64)
         _check(lib().ferret_trainer_normalizer(self._h, C.byref(cnt), _dp(mean), _dp(m2), n_features))
         return int(cnt.value), mean, m2
+
+    def replay_draws(self) -> np.ndarray:
+        """Stream sample index of every replay draw so far, in draw order
+        (ferret_trainer_replay_draws; the reference trainer's replay indices)."""
+        n = C.c_size_t()
+        _check(lib().ferret_trainer_replay_draws(self._h, None, 0, C.byref(n)))
+        out = np.zeros(n.value, dtype=np.int64)
+        if n.value:
+            _check(lib().ferret_trainer_replay_draws(self._h, out.ctypes.data_as(C.POINTER(C.c_int64)), n.value,
+                                                     C.byref(n)))
+        return out
 
     def stats(self) -> dict:
         s = TrainerStats()

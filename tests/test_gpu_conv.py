@@ -38,9 +38,12 @@ def _compare(fb, orc, spec, params, feats, labels, sched, policy="iter_fisher", 
     tr = fb.PipelineTrainer(spec, params, sched.bounds, opt)
     log = tr.run(sched.events, feats, labels)
     got = tr.params()
+    draws = tr.replay_draws()
     tr.close()
     ref = orc.train_conv(spec.geom, spec.acts, params, sched.bounds, sched.events, feats, labels, policy=policy,
                          replay=replay, replay_seed=3, micro_batch=B)
+    if replay:  # replay indices: bit-exact with the conv oracle's reference ReplayBuffer draws
+        assert len(ref["replay_ids"]) > 0 and np.array_equal(draws, ref["replay_ids"])
     assert np.linalg.norm(ref["params"] - params) / np.linalg.norm(params) > 1e-4  # training moved them
     if precision == "fp32":
         for j, (lo, hi) in enumerate(_slices(spec, sched.bounds)):
@@ -257,7 +260,7 @@ def test_conv_multi_chunk_replay_vs_oracle(gpu, fb, orc):
 
 
 def test_conv_exact_resume(gpu, fb):
-    """ferret-state v1 for a conv net (the header carries the geometry): 3 chunks straight vs
+    """ferret-state v2 for a conv net (the header carries the geometry): 3 chunks straight vs
     1 chunk, save, a fresh trainer loads and runs 2 more — identical bits; a state saved by a
     net of another geometry is refused (SchemaError)."""
     spec = cn.resnet_cifar(width=8, blocks=(1, 1, 1, 1))
@@ -285,7 +288,7 @@ def test_conv_exact_resume(gpu, fb):
     b.execute(0)
     state = b.save_state()
     b.close()
-    assert state.startswith(b"ferret-state v1\n") and b"geometry " in state[:4096]
+    assert state.startswith(b"ferret-state v2\n") and b"geometry " in state[:4096]
     c = trainer()
     c.load_state(state)
     for k in range(1, chunks):

@@ -57,6 +57,10 @@ def _compare(fb, orc, widths, params, feats, labels, sched, policy, micro_batch=
     assert np.array_equal(log["item"], ref["log"]["item"])
     flips = np.count_nonzero(log["predicted"] != ref["log"]["predicted"])
     assert flips <= max(2, 0.005 * len(log)), f"{flips} prediction flips"
+    if replay:  # replay indices: bit-exact with the reference ReplayBuffer's draws
+        draws = tr.replay_draws()
+        assert len(ref["replay_ids"]) > 0
+        assert np.array_equal(draws, ref["replay_ids"]), "replay draws differ from the oracle's"
     # normalizer: bit-exact
     cnt, mean, m2 = tr.normalizer(widths[0])
     assert cnt == ref["norm_count"]
@@ -161,11 +165,50 @@ def test_as_shipped_is_noop(gpu, fb, orc):
 
 
 def test_replay_indices_bit_exact(gpu, fb, orc):
-    """Replay indices: the device run's sampled items (reflected in the params) match the
-    oracle's restated reservoir, which itself is asserted against the reference buffer."""
+    """Replay indices: the trainer's draws (ferret_trainer_replay_draws, the stream sample
+    index of every ReplayBuffer::sample) equal the oracle's element for element; the oracle's
+    restated index reservoir is itself asserted against the reference ReplayBuffer's returned
+    sample on every draw (oracle/ferret_oracle.cpp replay_step)."""
     widths = [64, 96, 10]
     params, feats, labels, sched = _setup(fb, widths, 200, bounds=[0, 1, 2])
     _compare(fb, orc, widths, params, feats, labels, sched, "none", replay=True)
+
+
+@pytest.mark.parametrize("micro_batch", [1, 4])
+def test_replay_draws_across_chunks_bit_exact(gpu, fb, orc, micro_batch):
+    """Replay draws past the reservoir capacity (the random-replacement branch of
+    learner.hpp:65-69) and across chunk boundaries: the same stream replayed as 3 chunks of
+    one compiled schedule draws exactly the oracle's indices for the concatenated log."""
+    widths = [32, 48, 10]
+    units = 40
+    prof = fb.profile_from_widths(widths)
+    t_d = float(prof["t_f"].max())
+    sched = fb.Schedule.forced(prof, t_d, fb.StreamSpec(t_d=t_d, horizon=units * t_d), [0, 1, 2], units)
+    chunks = 3
+    n = units * micro_batch
+    feats, labels = fb.synth_drift_stream(chunks * n, widths[0], widths[-1], "split_tasks", 7)
+    params = fb.make_dense_net(widths, 1)
+    cap = 24  # smaller than the stream: draws come from a reservoir that replaces entries
+    tr = fb.PipelineTrainer(widths, params, sched.bounds,
+                            fb.PipelineTrainOptions(policy="iter_fisher", replay=True, replay_seed=5,
+                                                    replay_capacity=cap, micro_batch=micro_batch))
+    tr.load_stream(feats, labels)
+    tr.set_schedule(sched.events, n)
+    for c in range(chunks):
+        tr.execute(c)
+    tr.sync()
+    draws = tr.replay_draws()
+    tr.close()
+    # the oracle over the concatenated log: chunk c's events shifted by c * units items
+    evs = []
+    for c in range(chunks):
+        e = sched.events.copy()
+        e["item"] += c * units
+        evs.append(e)
+    ref = orc.train(widths, params, sched.bounds, np.concatenate(evs), feats, labels, policy="iter_fisher",
+                    replay=True, replay_seed=5, replay_capacity=cap, micro_batch=micro_batch)
+    assert len(draws) == len(ref["replay_ids"]) > cap
+    assert np.array_equal(draws, ref["replay_ids"])
 
 
 @pytest.mark.parametrize("policy", ["none", "step", "gap", "fisher", "iter_fisher"])

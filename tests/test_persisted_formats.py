@@ -122,7 +122,7 @@ def test_exact_resume(gpu, fb, prec):
     for c in range(2):
         b.execute(c)
     state = b.save_state()
-    assert state.startswith(b"ferret-state v1\n")
+    assert state.startswith(b"ferret-state v2\n")
     b.close()
     c_ = trainer()
     c_.load_state(state)
