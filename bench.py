@@ -1,27 +1,37 @@
 """Benchmark: stream samples/sec of Ferret's pipelined stream training on B200.
 
-Workload (BASELINE.json configs[1], the metric's config that fits one GPU):
-MLP 784-256-256-256-10 split into 4 pipeline stages (bounds 0,1,2,3,4,
-default_config workers), iter_fisher gradient compensation, micro-batch 16,
-synthetic class-incremental stream (synth_drift_stream, split_tasks, seed 7).
-A step = one replay of the simulator's event log over one chunk of the stream
-(UNITS pipeline units x 16 samples), continuing training from the previous
-chunk. All stages share one GPU at N=1.
+Headline workload (BASELINE.json configs[4], the largest configuration; it fits one
+B200 in the fp32 parity mode, 29 GB): wide deep MLP 16 x 4096 (+ 10-way head) split
+into 8 pipeline stages [0,2,...,16] (forced bounds, default_config workers), iter_fisher
+gradient compensation (lambda0 0.2, alpha 0.99, nu 2e-6, eta_lambda 1e-3), micro-batch 16,
+fp32 parity mode (the mode that holds the 1e-4 parameter bar against the fp64 reference),
+synthetic class-incremental stream (synth_drift_stream split_tasks seed 7, make_dense_net
+seed 1). A step = one replay of the simulator's event log over one chunk of the stream
+(32 pipeline units x 16 samples = 512 samples), continuing training from the previous
+chunk. At N = 1 all 8 stages share the GPU.
 
-  value      samples/s with the stream already resident in HBM (device time,
-             CUDA events on the trainer's stream, L2 flushed between steps)
-  e2e        the same metric through the reference-facing call
-             (ferret_trainer_run == PipelineTrainer::run) from pinned host
-             buffers: H2D stream copy + replay + D2H StepRecord log per step
-  roofline   the fused compensation + SGD update kernel against the measured
-             HBM copy bandwidth (algorithmic bytes per launch / event time)
-  cpu_baseline  the reference CPU pipeline (oracle/_ref: reference headers +
-             item-keyed PipelineTrainer restatement) on a bounded sample, 1 core
+  value        samples/s with the stream resident in HBM (device time: CUDA events on
+               the trainer's stream around each chunk, L2 flushed between steps)
+  e2e          the same metric through the reference-facing call (PipelineTrainer::run
+               chunk after chunk = ferret_trainer_ingest) from pinned host buffers: the
+               H2D copy of each step's samples and the D2H StepRecord predictions are
+               inside the timed region (host wall clock around the call)
+  roofline     the dominant KERNEL SYMBOL of the step (largest summed device time in one
+               profiled chunk): its algorithmic HBM bytes per launch / its mean launch time,
+               against the measured HBM copy bandwidth; `traffic` = its ncu
+               dram__bytes_read+write per launch from the committed capture
+  cpu_baseline the reference CPU pipeline (oracle/_ref: reference headers + item-keyed
+               PipelineTrainer restatement, bit-identical to the key-patched reference
+               trainer) on a bounded sample of the same workload, 1 core
 
---impl reference times that CPU reference alone on the same config.
-Multi-GPU (--gpus N>1, torchrun): every rank runs an independent replica of the
-pipeline on its own stream shard ("replicas only" scaling); value
-= total samples / max-over-ranks time.
+--impl reference runs that CPU reference alone (no product code on its path) on the same
+config and prints the same JSON line with "impl": "reference".
+
+Multi-GPU (torchrun, --gpus N > 1): the SAME stream with its 8 stages sharded over the N
+GPUs (stage j on rank floor(j N / 8); one stage per GPU at N = 8); hand-offs are NVLink
+peer stores into CUDA-IPC inboxes with release/acquire flags inside each rank's chunk
+graph. value = stream samples / max-over-ranks device time (strong
+scaling: the total work is fixed).
 """
 from __future__ import annotations
 
@@ -39,13 +49,32 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-WIDTHS = [784, 256, 256, 256, 10]
-BOUNDS = [0, 1, 2, 3, 4]
+WIDTHS = [4096] * 16 + [10]
+BOUNDS = [0, 2, 4, 6, 8, 10, 12, 14, 16]
 MICRO_BATCH = 16
-UNITS = 256            # pipeline units per step (x16 samples)
+UNITS = 32             # pipeline units per step (x 16 samples)
 POLICY = "iter_fisher"
-REDUCE_DEV = "cuda"     # device of the tensors max-reduced over ranks
-CPU_UNITS = 512         # bounded CPU sample (~10 s of reference work): 512 units x 16 samples
+PRECISION = "fp32"
+CPU_UNITS = 1          # bounded CPU sample for cpu_baseline: the first unit of the stream (~60 s)
+REF_UNITS = 2          # --impl reference: one replay of the stream's first 2 units (~2 min)
+REDUCE_DEV = "cuda"
+
+
+def workload_config(n_gpus: int) -> dict:
+    """The config object both arms print (identical for the same N)."""
+    return {"workload": "C5: MLP 16x4096+10 (251.8 M params), 8 pipeline stages [0,2,...,16], iter_fisher "
+                        "compensation, micro-batch 16, fp32 parity mode",
+            "model": "dense MLP 16x4096+10", "stages": len(BOUNDS) - 1, "micro_batch": MICRO_BATCH,
+            "global_batch": MICRO_BATCH, "policy": POLICY, "precision": "fp32 parity",
+            "units_per_step": UNITS, "samples_per_step": UNITS * MICRO_BATCH,
+            "parallelism": f"pipeline stages over {n_gpus} GPU" + ("s" if n_gpus > 1 else ""),
+            "l2": "flushed between timed steps (256 MB write); the 1 GB of weights exceed L2 anyway"}
+
+
+def _refuse_experiments():
+    bad = sorted(k for k in os.environ if k.startswith("FERRET_EXPERIMENT"))
+    if bad:
+        raise SystemExit(f"bench.py: refusing to run with experiment knobs set: {bad}")
 
 
 def _peaks():
@@ -55,8 +84,8 @@ def _peaks():
             d = json.load(f)
         for k in ("hbm_gbs", "hbm_GBs", "hbm_gb_s"):
             if k in d:
-                return float(d[k]), "measured"
-    return 6650.0, "fallback"
+                return float(d[k]), "measured", d.get("bf16_tflops")
+    return 6650.0, "fallback (B200_PROFILING.md)", None
 
 
 class ClockSampler:
@@ -82,7 +111,7 @@ class ClockSampler:
                     self.rows.append(parts)
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.1)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -104,258 +133,187 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-KERNEL_OF = {"normalize": "normalize_kernel", "predict": "fwd_kernel + head_kernel", "forward": "fwd_kernel",
-             "backward": "bwd_kernel + head_kernel", "update": "update_iter1_kernel (fused compensation + SGD)",
-             "replay": "fwd/bwd/update", "other": "pool_kernel / copies"}
-
-
-def _traffic(cls):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the class's kernel from
-    the committed ncu --set full capture (profiles/r1_ncu_traffic.json), or None."""
-    path = os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")
+def _ncu_traffic(symbol):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `symbol` from the committed
+    ncu --set full capture of this bench's workload (profiles/r2/ncu_traffic.json), or None."""
+    path = os.path.join(ROOT, "profiles", "r2", "ncu_traffic.json")
     if not os.path.exists(path):
         return None
     with open(path) as f:
-        return json.load(f).get(cls)
+        d = json.load(f)
+    for k, v in d.get("kernels", {}).items():
+        if k.split("(")[0] == symbol.split("(")[0]:
+            return v
+    return None
 
 
-def config5_roofline(fb, torch, device, precision="bf16"):
-    """BASELINE config 5 on one GPU: MLP 16x4096+10, 8 stages [0,2,...,16], iter_fisher,
-    micro-batch 16, bf16 fast mode (tcgen05 layers + fp32 compensation/SGD over HBM version
-    rings), 32 units per chunk (steady-state staleness). samples/s from CUDA events on the
-    trainer's stream (L2 flushed between chunks), per-class rooflines from one profiled chunk
-    (profiles/c5_fast.py)."""
-    from profiles.c5_fast import measure
-
-    r = measure(fb, torch, precision, units=32, steps=2, device=device)
-    peak, kind = _peaks()
-    tflops = None
-    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(path):
-        with open(path) as f:
-            tflops = json.load(f).get("bf16_tflops")
-    tot = sum(v["alg_bytes"] for v in r["classes"].values())
-    mode = {"bf16": "bf16 fast mode", "tf32": "tf32 fast mode", "fp32": "fp32 parity mode (3xTF32 tensor-core layers)"}
-    out = {"workload": f"C5: MLP 16x4096+10, 8 stages [0,2,...,16] on one GPU, iter_fisher, micro-batch 16, {mode[precision]}",
-           "value": r["samples_per_s"], "unit": "samples/s", "ms_per_chunk": r["ms_per_chunk"],
-           "samples_per_chunk": r["samples_per_chunk"],
-           "dtype": "f32 (3xTF32 layers), f32 update" if precision == "fp32" else f"{precision} layers, f32 update",
-           "step_achieved_gbs": tot / (r["ms_per_chunk"] * 1e-3) / 1e9, "peak": peak, "peak_kind": kind,
-           "classes": r["classes"], "critical_ms": r["critical_ms"], "serial_ms": r["serial_ms"],
-           "ring_depth": r["ring_depth"], "mean_tau": r["mean_tau"], "device_gb": r["device_gb"]}
-    out["step_frac"] = out["step_achieved_gbs"] / peak
-    # the tensor-core layer kernels: weight-stream bandwidth and tensor-pipe share
-    # (2 * 16 * in * out flops per layer node; bound by HBM at micro-batch 16)
-    for k in ("predict", "forward", "backward"):
-        c = r["classes"].get(k)
-        if c and c["nodes"]:
-            c["frac_of_hbm_peak"] = c["gbs"] / peak
-    fwd = r["classes"].get("forward")
-    if fwd and tflops and precision == "bf16":
-        # 4096x4096 layers dominate: 2*16*4096*4096 flops per node
-        fl = 2.0 * 16 * 4096 * 4096 / (fwd["us_per_node"] * 1e-6) / 1e12
-        out["tensor"] = {"achieved_tflops": fl, "peak_tflops": tflops, "frac": fl / tflops,
-                         "note": "micro-batch 16: 16 MACs per 2-byte weight, HBM-bound by construction"}
-    return out
-
-
-def config3_resnet(fb, torch, device, no_cpu=False):
-    """BASELINE config 3 on one GPU: ResNet-18-style CNN (11.0 M params; convolutions on the
-    tcgen05 tensor cores, 3xTF32 in the fp32 parity mode) on a CIFAR-shaped stream, 4 stages
-    cut between residual blocks, iter_fisher, ER replay, micro-batch 16 (profiles/c3_resnet.py),
-    with the conv CPU oracle timed on a bounded sample of the same workload (fp64, 1 core)."""
-    from profiles.c3_resnet import measure
-
-    r = measure(fb, torch, units=32, steps=2, warmup=2, device=device, profile=False)
-    tflops = None
-    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(path):
-        with open(path) as f:
-            tflops = json.load(f).get("bf16_tflops")
-    out = {"workload": r["workload"], "value": r["samples_per_s"], "unit": "samples/s",
-           "ms_per_chunk": r["ms_per_chunk"], "samples_per_chunk": r["samples_per_chunk"], "dtype": "f32 (3xTF32 convs)",
-           "achieved_tflops": r["tflops"], "oacc_last_chunk": r["oacc_last_chunk"],
-           "tensor": {"achieved_tflops": r["tflops"], "peak_tflops": tflops / 6 if tflops else None,
-                      "peak_kind": "3xTF32 effective = measured bf16 dense / 6 (tf32 = bf16 / 2, 3 MMAs per product)",
-                      "frac": r["tflops"] / (tflops / 6) if tflops else None,
-                      "frac_of_bf16_peak": r["tflops"] / tflops if tflops else None,
-                      "note": "whole-step algorithmic flops (8 F per sample + 6 F per replay sample) / chunk time, "
-                              "all kernels of the step included (update, normalizer, GAP head)"}}
-    if not no_cpu:
-        try:
-            from oracle import oracle as orc
-
-            cn = fb.convnet
-            spec = cn.resnet_cifar()
-            bounds = cn.balanced_bounds(spec, 4)
-            prof = cn.profile(spec)
-            t_d = cn.stage_t_d(prof, bounds)
-            n_units = 3
-            sched = fb.Schedule.forced(prof, t_d, fb.StreamSpec(t_d=t_d, horizon=n_units * t_d), bounds, n_units)
-            feats, labels = fb.synth_drift_stream(n_units, spec.in_width(0), 10, "split_tasks", 7)
-            t0 = time.perf_counter()
-            orc.train_conv(spec.geom, spec.acts, cn.make_conv_net(spec, 1), bounds, sched.events, feats, labels,
-                           policy="iter_fisher", replay=True, replay_seed=3, micro_batch=1)
-            dt = time.perf_counter() - t0
-            out["cpu_baseline"] = {"value": n_units / dt, "unit": "samples/s", "cores": 1, "kind": "port",
-                                   "sample": f"{n_units} units x 1 sample ({dt:.1f} s) of the same net and schedule "
-                                             "rule at micro-batch 1; conv oracle (reference trainer order, "
-                                             "restated layers), fp64, single-threaded"}
-        except Exception as e:
-            out["cpu_baseline"] = {"value": None, "sample": f"unavailable: {e}"}
-    return out
-
-
-def stage_shard_measure(fb, torch, dist, rank, world, local, args, units, widths=None, bounds=None,
-                        precision="fp32", steps=None, warmup=None, conv=None):
-    """One stream pipelined with its stages sharded over min(N, P) GPUs (one stage group
-    per rank, NVLink hand-offs: peer stores into CUDA-IPC inboxes + release flags; ranks
-    beyond the stage count idle). Default: the C2 stream; config 5 passes its widths and
-    bounds (8 stages -> one stage per GPU on an 8xB200 box). Device time per chunk, max
-    over ranks."""
-    steps = steps or args.steps
-    warmup = warmup if warmup is not None else args.warmup
-    if conv is not None:  # config 3: a convnet.ConvNetSpec, its 4 block-aligned stages, ER replay
-        cn = fb.convnet
-        widths = conv.widths
-        bounds = cn.balanced_bounds(conv, 4)
-        prof = cn.profile(conv)
-        t_d = cn.stage_t_d(prof, bounds)
-        net, params, replay = conv, cn.make_conv_net(conv, 1), True
-    else:
-        widths = widths or WIDTHS
-        bounds = bounds or BOUNDS
-        prof = fb.profile_from_widths(widths)
-        t_d = float(prof["t_f"].max())
-        net, params, replay = widths, fb.make_dense_net(widths, 1), False
-    P = len(bounds) - 1
-    used = min(world, P)
-    owners = fb.ferret.stage_owners(P, used)
-    sched = fb.Schedule.forced(prof, t_d, fb.StreamSpec(t_d=t_d, horizon=units * t_d), bounds, units)
-    chunk = units * MICRO_BATCH
-    feats, labels = fb.synth_drift_stream((warmup + steps) * chunk, widths[0], widths[-1], "split_tasks", 7)
-    tr = fb.PipelineTrainer(net, params, bounds,
-                            fb.PipelineTrainOptions(policy=POLICY, micro_batch=MICRO_BATCH, device=local,
-                                                    precision=precision, replay=replay, replay_seed=3))
-    tr.set_shard(rank, world, owners)
-    tr.load_stream(feats, labels)
-    tr.set_schedule(sched.events, chunk)
-
-    def gather(b):
-        out = [None] * world
-        dist.all_gather_object(out, b)
-        return out
-
-    tr.connect(gather)
-    stream = torch.cuda.ExternalStream(tr.cuda_stream, device=torch.device("cuda", local))
-    for c in range(warmup):
-        tr.execute(c)
-        tr.sync()
-        dist.barrier()
-    ms = 0.0
-    for s in range(steps):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        dist.barrier()
-        with torch.cuda.stream(stream):
-            a.record(stream)
-        tr.execute(warmup + s)
-        with torch.cuda.stream(stream):
-            b.record(stream)
-        tr.sync()
-        ms += a.elapsed_time(b)
-    t = torch.tensor([ms], device=REDUCE_DEV)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    tr.close()
-    return {"value": chunk * steps / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms / steps,
-            "ranks_with_stages": used, "stage_owner": owners, "precision": precision,
-            "workload": (f"ResNet-18-style CNN ({conv.n_params / 1e6:.1f} M params), ER" if conv is not None else
-                         f"MLP {widths[0]}-...-{widths[-1]}") + f" ({len(widths) - 1} layers), bounds {bounds}, "
-                        f"{units} units x {MICRO_BATCH} samples per chunk",
-            "note": "one stream, stages sharded across GPUs (strong scaling); hand-offs are peer stores "
-                    "into CUDA-IPC inboxes + release flags; ranks synchronise per chunk"}
-
-
-def make_workload(fb, n_chunks, units):
-    prof = fb.profile_from_widths(WIDTHS)
-    t_d = float(prof["t_f"].max())
-    sched = fb.Schedule.forced(prof, t_d, fb.StreamSpec(t_d=t_d, horizon=units * t_d), BOUNDS, units)
-    chunk = units * MICRO_BATCH
-    feats, labels = fb.synth_drift_stream(n_chunks * chunk, WIDTHS[0], WIDTHS[-1], "split_tasks", 7)
-    return sched, feats, labels, chunk
-
-
-def cpu_reference(units: int, steps: int, warmup: int):
-    """The reference CPU pipeline on `units` pipeline units per step (1 core)."""
-    import paper_2503_12053_b200 as fb
+# ------------------------------------------------------------------ CPU reference
+def cpu_reference_sample(units: int) -> dict:
+    """The reference CPU pipeline (oracle/_ref) on the first `units` pipeline units of the
+    headline stream: same net, same schedule rule, same stream, fp64, single-threaded.
+    Imports only the oracle: no product code on this path."""
     from oracle import oracle as orc
 
-    sched, feats, labels, chunk = make_workload(fb, 1, units)
-    params = fb.make_dense_net(WIDTHS, 1)
-    times = []
-    ref = None
-    for s in range(warmup + steps):
-        t0 = time.perf_counter()
-        ref = orc.train(WIDTHS, params, BOUNDS, sched.events, feats, labels, policy=POLICY, micro_batch=MICRO_BATCH)
-        dt = time.perf_counter() - t0
-        if s >= warmup:
-            times.append(dt)
-    tot = sum(times)
-    cpu_run.update(ref=ref, sched=sched, feats=feats, labels=labels, params=params)
-    return chunk * len(times) / tot, tot, chunk
+    prof = orc.profile_from_widths(WIDTHS)
+    t_d = float(prof["t_f"].max())
+    sched = orc.Schedule(prof, t_d, [t_d, 0.0, 1.0, units * t_d], forced=BOUNDS, n_items=units)
+    feats, labels = orc.synth_drift_stream(units * MICRO_BATCH, WIDTHS[0], WIDTHS[-1], "split_tasks", 7)
+    params = orc.make_dense_net(WIDTHS, 1)
+    t0 = time.perf_counter()
+    ref = orc.train(WIDTHS, params, BOUNDS, sched.events, feats, labels, policy=POLICY, micro_batch=MICRO_BATCH)
+    dt = time.perf_counter() - t0
+    n = units * MICRO_BATCH
+    return {"seconds": dt, "samples": n, "value": n / dt,
+            "oacc": 100.0 * float(np.count_nonzero(ref["log"]["outcome"] == 0)) / n}
 
 
-cpu_run = {}  # the last CPU reference run (its inputs and outputs), for the accuracy comparison
-
-
-def accuracy_vs_cpu(fb, device):
-    """Online accuracy of the B200 trainer vs the CPU reference on the identical bounded
-    sample (same schedule, same stream, same initial net): the '+ online accuracy vs CPU'
-    half of the metric, with the parameter agreement beside it."""
-    if not cpu_run:
-        return None
-    tr = fb.PipelineTrainer(WIDTHS, cpu_run["params"], BOUNDS,
-                            fb.PipelineTrainOptions(policy=POLICY, micro_batch=MICRO_BATCH, device=device))
-    log = tr.run(cpu_run["sched"].events, cpu_run["feats"], cpu_run["labels"])
-    got = tr.params()
-    tr.close()
-    ref = cpu_run["ref"]
-    g, c = fb.online_accuracy(log), fb.online_accuracy(ref["log"])
-    return {"b200": g, "cpu_reference": c, "diff_pp": g - c,
-            "param_rel_err": float(np.linalg.norm(got - ref["params"]) / np.linalg.norm(ref["params"])),
-            "prediction_flips": int(np.count_nonzero(log["predicted"] != ref["log"]["predicted"])),
-            "sample": f"{len(log)} samples of the bench stream ({CPU_UNITS} units x {MICRO_BATCH}), fp32 parity mode"}
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def run_reference_arm(args):
+    """--impl reference: the reference's own CPU pipeline (oracle/_ref), rank 0 only, no
+    product code on its path. A C5 pipeline unit costs the reference about a minute (it
+    copies the 2 GB fp64 net for every stage event and the version chain for every
+    update), so the arm times ONE replay of the stream's first REF_UNITS units — a bounded
+    sample of the same workload — instead of --steps chunks of 32 units (which would take
+    hours); it reports steps = 1, warmup = 0 and echoes the requested counts. The
+    reference is single-threaded by design."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    units = 64  # per step: 64 units x 16 samples (~1 s of reference work)
-    value, tot, chunk = cpu_reference(units, args.steps, args.warmup)
-    sample = f"{units} units x {MICRO_BATCH} samples = {chunk} samples per step, {args.steps} timed steps"
+    r = cpu_reference_sample(REF_UNITS)
+    secs, samples, value = r["seconds"], r["samples"], r["value"]
+    sample = (f"one replay of the headline stream's first {REF_UNITS} pipeline units x {MICRO_BATCH} samples = "
+              f"{samples} samples ({secs:.1f} s); reference headers + item-keyed PipelineTrainer restatement "
+              f"(bit-identical to the key-patched reference trainer), fp64, single-threaded; host {_cpu_model()}, "
+              f"nproc={os.cpu_count()}; pipeline fill only (short version chains), which favours the reference")
     line = {"impl": "reference", "metric": "stream samples/sec", "value": value, "unit": "samples/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C2: MLP 784-256-256-256-10, 4 stages, iter_fisher, micro-batch 16",
-                       "global_batch": MICRO_BATCH, "stages": 4},
-            "cpu_baseline": {"value": value, "unit": "samples/s", "cores": 1, "kind": "reference",
-                             "sample": sample + "; reference headers + item-keyed PipelineTrainer restatement "
-                                                "(single-threaded by design)"},
+            "n_gpus": args.gpus, "steps": 1, "warmup": 0, "ms_per_step": 1e3 * secs,
+            "requested": {"steps": args.steps, "warmup": args.warmup},
+            "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (synth_drift_stream split_tasks seed 7; make_dense_net seed 1)",
+            "config": workload_config(args.gpus), "online_accuracy": r["oacc"],
+            "cpu_baseline": {"value": value, "unit": "samples/s", "cores": 1, "kind": "reference", "sample": sample},
             "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------ side configs
+def side(fn):
+    """Secondary configurations never cost the headline line: errors are recorded."""
+    try:
+        return fn()
+    except Exception as e:  # noqa: BLE001
+        return {"error": f"{type(e).__name__}: {e}"}
+
+
+def config2_small(fb, torch, device):
+    """BASELINE config 2 (784-256-256-256-10, 4 stages, micro-batch 16): L2-resident weights,
+    latency-bound; device samples/s of 256-unit chunks."""
+    widths, bounds, units = [784, 256, 256, 256, 10], [0, 1, 2, 3, 4], 256
+    prof = fb.profile_from_widths(widths)
+    t_d = float(prof["t_f"].max())
+    sched = fb.Schedule.forced(prof, t_d, fb.StreamSpec(t_d=t_d, horizon=units * t_d), bounds, units)
+    chunk = units * MICRO_BATCH
+    steps, warmup = 10, 3
+    feats, labels = fb.synth_drift_stream((steps + warmup) * chunk, widths[0], widths[-1], "split_tasks", 7)
+    tr = fb.PipelineTrainer(widths, fb.make_dense_net(widths, 1), bounds,
+                            fb.PipelineTrainOptions(policy=POLICY, micro_batch=MICRO_BATCH, device=device))
+    tr.load_stream(feats, labels)
+    tr.set_schedule(sched.events, chunk)
+    for c in range(warmup):
+        tr.execute(c)
+    tr.sync()
+    stream = torch.cuda.ExternalStream(tr.cuda_stream, device=torch.device("cuda", device))
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        a.record(stream)
+    h0 = time.perf_counter()
+    for s in range(steps):
+        tr.execute(warmup + s)
+    host = time.perf_counter() - h0
+    with torch.cuda.stream(stream):
+        b.record(stream)
+    tr.sync()
+    ms = a.elapsed_time(b)
+    st = tr.stats()
+    tr.close()
+    return {"workload": "C2: MLP 784-256-256-256-10, 4 stages, iter_fisher, micro-batch 16, fp32 parity",
+            "value": chunk * steps / (ms / 1e3), "unit": "samples/s", "ms_per_chunk": ms / steps,
+            "host_issue_ms_per_chunk": 1e3 * host / steps, "graph_nodes": st["kernel_launches"]}
+
+
+def config5_fast(fb, torch, device, precision):
+    from profiles.c5_fast import measure
+
+    r = measure(fb, torch, precision, units=UNITS, steps=2, device=device)
+    return {"workload": f"C5 as the headline in the {precision} fast mode (tcgen05 layers, fp32 update)",
+            "value": r["samples_per_s"], "unit": "samples/s", "ms_per_chunk": r["ms_per_chunk"],
+            "oacc_last_chunk": r["oacc_last_chunk"]}
+
+
+def config3_resnet(fb, torch, device):
+    from profiles.c3_resnet import measure
+
+    r = measure(fb, torch, units=32, steps=2, warmup=2, device=device, profile=False)
+    return {"workload": r["workload"], "value": r["samples_per_s"], "unit": "samples/s",
+            "ms_per_chunk": r["ms_per_chunk"], "achieved_tflops": r["tflops"], "oacc_last_chunk": r["oacc_last_chunk"]}
+
+
+def config4_budget(fb, torch, device):
+    from profiles.c4_budget import measure
+
+    return measure(fb, torch, device=device, steps=2)
+
+
+def accuracy_vs_cpu(fb, device):
+    """'+ online accuracy vs CPU': the fp32 parity trainer on the headline workload's first
+    16 units against the committed fp64 CPU-reference fixture of exactly that run
+    (tests/golden/c5_oracle.npz, made by tests/golden/make_c5_fixture.py)."""
+    path = os.path.join(ROOT, "tests", "golden", "c5_oracle.npz")
+    if not os.path.exists(path):
+        return None
+    g = np.load(path)
+    units = int(g["units"])
+    prof = fb.profile_from_widths(WIDTHS)
+    t_d = float(prof["t_f"].max())
+    sched = fb.Schedule.forced(prof, t_d, fb.StreamSpec(t_d=t_d, horizon=units * t_d), BOUNDS, units)
+    feats, labels = fb.synth_drift_stream(units * MICRO_BATCH, WIDTHS[0], WIDTHS[-1], "split_tasks", 7)
+    tr = fb.PipelineTrainer(WIDTHS, fb.make_dense_net(WIDTHS, 1), BOUNDS,
+                            fb.PipelineTrainOptions(policy=POLICY, micro_batch=MICRO_BATCH, device=device,
+                                                    precision=PRECISION))
+    log = tr.run(sched.events, feats, labels)
+    got = tr.params()
+    tr.close()
+    pos = g["sample_pos"]
+    rel = float(np.linalg.norm(got[pos] - g["params_sample"]) / np.linalg.norm(g["params_sample"]))
+    ga, ca = fb.online_accuracy(log), float(g["oacc"])
+    return {"b200": ga, "cpu_reference": ca, "diff_pp": ga - ca,
+            "prediction_flips": int(np.count_nonzero(log["predicted"] != g["log"]["predicted"])),
+            "param_rel_err_sampled": rel,
+            "sample": f"the headline stream's first {units} units x {MICRO_BATCH} samples, fp32 parity mode, "
+                      "vs the committed fp64 reference fixture"}
+
+
+# ------------------------------------------------------------------ the B200 arm
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--units", type=int, default=UNITS)
-    ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-large", action="store_true", help="skip the config-5 (16x4096, bf16) measurement")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--no-side", action="store_true", help="skip the secondary configurations")
     args = ap.parse_args()
+    _refuse_experiments()
     if args.impl == "reference":
         return run_reference_arm(args)
 
@@ -381,31 +339,59 @@ def main():
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    units = args.units
+    def max_over_ranks(x: float) -> float:
+        if not dist:
+            return x
+        t = torch.tensor([x], device=REDUCE_DEV, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    P = len(BOUNDS) - 1
+    prof = fb.profile_from_widths(WIDTHS)
+    t_d = float(prof["t_f"].max())
+    sched = fb.Schedule.forced(prof, t_d, fb.StreamSpec(t_d=t_d, horizon=UNITS * t_d), BOUNDS, UNITS)
+    chunk = UNITS * MICRO_BATCH
     n_chunks = args.warmup + args.steps
-    sched, feats, labels, chunk = make_workload(fb, n_chunks, units)
-    # each rank trains its own replica on its own shard of the stream
-    if world > 1:
-        feats2, labels2 = fb.synth_drift_stream(n_chunks * chunk, WIDTHS[0], WIDTHS[-1], "split_tasks", 7 + rank)
-        feats, labels = feats2, labels2
+    feats, labels = fb.synth_drift_stream(n_chunks * chunk, WIDTHS[0], WIDTHS[-1], "split_tasks", 7)
     params = fb.make_dense_net(WIDTHS, 1)
-    opt = fb.PipelineTrainOptions(policy=POLICY, micro_batch=MICRO_BATCH, device=local)
-    tr = fb.PipelineTrainer(WIDTHS, params, BOUNDS, opt)
+    opt = fb.PipelineTrainOptions(policy=POLICY, micro_batch=MICRO_BATCH, device=local, precision=PRECISION)
+
+    def make_trainer():
+        tr = fb.PipelineTrainer(WIDTHS, params, BOUNDS, opt)
+        if world > 1:
+            tr.set_shard(rank, world, fb.ferret.stage_owners(P, min(world, P)))
+        return tr
+
+    def connect(tr):
+        if world > 1:
+            def gather(b):
+                out = [None] * world
+                dist.all_gather_object(out, b)
+                return out
+
+            tr.connect(gather)
+
+    tr = make_trainer()
     tr.load_stream(feats, labels)
     tr.set_schedule(sched.events, chunk)
+    connect(tr)
     stream = torch.cuda.ExternalStream(tr.cuda_stream, device=torch.device("cuda", local))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
 
     for c in range(args.warmup):
         tr.execute(c)
-    tr.sync()
+        tr.sync()
+        barrier()
     launches_per_step = tr.stats()["kernel_launches"]
 
-    # ---- device-resident timed region
+    # ---- device-resident timed region: events on the trainer's stream around every chunk
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    if dist:
-        dist.barrier()
+    barrier()
     torch.cuda.synchronize()
     host_s = 0.0
     with ClockSampler(local) as clk:
@@ -418,124 +404,113 @@ def main():
             host_s += time.perf_counter() - h0
             with torch.cuda.stream(stream):
                 ends[s].record(stream)
+            if world > 1:  # sharded: inboxes are reused per chunk
+                tr.sync()
+                barrier()
         tr.sync()
         torch.cuda.synchronize()
-    dev_ms = sum(a.elapsed_time(b) for a, b in zip(starts, ends))
-    if dist:
-        t = torch.tensor([dev_ms], device=REDUCE_DEV)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dev_ms = float(t.item())
-        dist.barrier()
-    total_samples = chunk * args.steps * world
-    value = total_samples / (dev_ms / 1e3)
-    log = tr.fetch_log(args.warmup + args.steps - 1)
-    oacc_last = fb.online_accuracy(log)
+    dev_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in zip(starts, ends)))
+    barrier()
+    value = chunk * args.steps / (dev_ms / 1e3)
+    oacc_last = fb.online_accuracy(tr.fetch_log(args.warmup + args.steps - 1)) if rank == 0 else None
 
-    # ---- roofline: one more chunk in profile mode (serialised graph, CUDA events
-    # around every node on the trainer's stream); the dominant kernel class is the
-    # one with the largest measured device time; achieved = its algorithmic bytes
-    # per launch / its mean launch time
-    tr.set_profiling(True)
-    tr.execute(0)  # replays chunk 0 again (continues training; not part of the timed region)
-    prof = tr.profile()
-    tr.set_profiling(False)
+    # ---- roofline: one more chunk in profile mode (serialised graph, an event pair around
+    # every node on the trainer's stream), aggregated per kernel symbol
+    kern = None
+    if world == 1:
+        tr.set_profiling(True)
+        tr.execute(0)  # replays chunk 0 again (continues training; outside the timed region)
+        kern = tr.profile_kernels()
+        cls = tr.profile()
+        tr.set_profiling(False)
     stats = tr.stats()
     tr.close()
-    peak, peak_kind = _peaks()
-    classes = {k: v for k, v in prof["classes"].items() if v["nodes"] > 0}
-    dom = max(classes, key=lambda k: classes[k]["ms"])
-    dc = classes[dom]
-    achieved = dc["gbs"]
-    large = config5_roofline(fb, torch, local) if not args.no_large else None
-    large32 = config5_roofline(fb, torch, local, "fp32") if not args.no_large else None
-    def side(fn):  # the secondary configs must never cost the headline line
-        try:
-            return fn()
-        except Exception as e:  # noqa: BLE001
-            return {"error": f"{type(e).__name__}: {e}"}
 
-    conv3 = side(lambda: config3_resnet(fb, torch, local, no_cpu=args.no_cpu or world > 1)) if not args.no_large else None
-    budget4 = None
-    if not args.no_large:  # config 4: planner partitions at 100 / 50 / 25 % memory budget (profiles/c4_budget.py)
-        from profiles.c4_budget import measure as c4_measure
-
-        budget4 = side(lambda: c4_measure(fb, torch, device=local, steps=2))
-    shard = stage_shard_measure(fb, torch, dist, rank, world, local, args, units) if world > 1 else None
-    shard5 = None
-    if world > 1 and not args.no_large:  # config 5, bf16: 8 stages over the N GPUs
-        shard5 = stage_shard_measure(fb, torch, dist, rank, world, local, args, 32, widths=[4096] * 16 + [10],
-                                     bounds=[0, 2, 4, 6, 8, 10, 12, 14, 16], precision="bf16", steps=2, warmup=2)
-    shard3 = None
-    if world > 1 and not args.no_large:  # config 3: the ResNet's 4 stages over min(N, 4) GPUs
-        shard3 = stage_shard_measure(fb, torch, dist, rank, world, local, args, 32, steps=2, warmup=2,
-                                     conv=fb.convnet.resnet_cifar())
-
-    # ---- e2e through the public API with host buffers: PipelineTrainer ingest
-    # (ferret_trainer_ingest) of the step's samples from pinned host memory, each
-    # step's H2D copy and D2H StepRecord read inside the timed region (copies of
-    # step s+1 overlap the compute of step s through two staging slots)
-    tr2 = fb.PipelineTrainer(WIDTHS, params, BOUNDS, opt)
+    # ---- e2e through the public API with host buffers (ferret_trainer_ingest = PipelineTrainer::run
+    # chunk after chunk): each step's H2D copy of its samples from pinned memory and the D2H of its
+    # predictions are inside the timed region
+    tr2 = make_trainer()
     tr2.set_schedule(sched.events, chunk)
-    pin_f = torch.from_numpy(np.ascontiguousarray(feats[: n_chunks * chunk])).pin_memory()
-    pin_l = torch.from_numpy(labels[: n_chunks * chunk].astype(np.int64)).pin_memory()
-    h2d = chunk * WIDTHS[0] * 8 + chunk * 4
-    d2h = chunk * 4
+    connect(tr2)
+    pin_f = torch.from_numpy(np.ascontiguousarray(feats)).pin_memory()
+    pin_l = torch.from_numpy(labels.astype(np.int64)).pin_memory()
+    pf, pl = pin_f.numpy(), pin_l.numpy().view(np.uint64)
     w = args.warmup * chunk
-    tr2.ingest(pin_f.numpy()[:w], pin_l.numpy()[:w].view(np.uint64))
-    if dist:
-        dist.barrier()
+    for c in range(args.warmup):  # warm-up chunks (one per call when sharded)
+        tr2.ingest(pf[c * chunk:(c + 1) * chunk], pl[c * chunk:(c + 1) * chunk])
+        barrier()
+    barrier()
     t0 = time.perf_counter()
-    tr2.ingest(pin_f.numpy()[w:], pin_l.numpy()[w:].view(np.uint64))
-    e2e_s = time.perf_counter() - t0
-    if dist:
-        t = torch.tensor([e2e_s], device=REDUCE_DEV, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e_value = total_samples / e2e_s
+    if world == 1:
+        tr2.ingest(pf[w:], pl[w:])
+    else:
+        for s in range(args.steps):
+            c = args.warmup + s
+            tr2.ingest(pf[c * chunk:(c + 1) * chunk], pl[c * chunk:(c + 1) * chunk])
+            barrier()
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
     tr2.close()
+    e2e_value = chunk * args.steps / e2e_s
+    h2d = (chunk * WIDTHS[0] * 8 + chunk * 4) * world
+    d2h = chunk * 4 * world
 
     if rank != 0:
         if dist:
             dist.destroy_process_group()
         return
-    cpu = None
-    if not args.no_cpu and world == 1:
+
+    peak, peak_kind, tflops = _peaks()
+    roofline = None
+    if kern:
+        dom = max(kern, key=lambda k: kern[k]["ms"])
+        d = kern[dom]
+        achieved = d["alg_bytes"] / d["launches"] / (d["us_per_launch"] * 1e-6) / 1e9
+        tot_ms = sum(v["ms"] for v in kern.values())
+        tr_ = _ncu_traffic(dom)
+        roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "peak_kind": peak_kind,
+                    "traffic": tr_["dram_bytes_per_launch"] if tr_ else None,
+                    "traffic_capture": tr_, "alg_bytes_per_launch": d["alg_bytes"] / d["launches"],
+                    "avg_launch_us": d["us_per_launch"], "launches_per_step": d["launches"],
+                    "share_of_serial_device_time": d["ms"] / tot_ms,
+                    "kernels": {k: {"ms": v["ms"], "launches": v["launches"], "us_per_launch": v["us_per_launch"],
+                                    "gbs": v["gbs"], "frac_of_peak": v["gbs"] / peak} for k, v in kern.items()},
+                    "serial_ms": cls["serial_ms"], "dag_critical_path_ms": cls["critical_path_ms"],
+                    "step_alg_gbs": sum(v["alg_bytes"] for v in kern.values()) / (dev_ms / args.steps * 1e-3) / 1e9,
+                    "note": "per-launch times from one profiled chunk (graph serialised, CUDA events around every "
+                            "node on the trainer's stream); algorithmic bytes per launch in DESIGN.md §3"}
+        roofline["step_frac"] = roofline["step_alg_gbs"] / peak
+
+    cpu = acc = None
+    if world == 1 and not args.no_cpu:
         try:
-            v, tot, n = cpu_reference(CPU_UNITS, 1, 0)
-            cpu = {"value": v, "unit": "samples/s", "cores": 1, "kind": "reference",
-                   "sample": f"{CPU_UNITS} units x {MICRO_BATCH} samples ({n} samples, {tot:.1f} s) of the same "
-                             "workload; reference headers + item-keyed PipelineTrainer restatement, fp64, "
-                             f"single-threaded (host nproc={os.cpu_count()})"}
+            r = cpu_reference_sample(CPU_UNITS)
+            cpu = {"value": r["value"], "unit": "samples/s", "cores": 1, "kind": "reference",
+                   "sample": f"the headline stream's first {CPU_UNITS} unit(s) x {MICRO_BATCH} samples "
+                             f"({r['samples']} samples, {r['seconds']:.1f} s, pipeline fill: short chains, favours "
+                             "the reference); reference headers + item-keyed PipelineTrainer restatement, fp64, "
+                             f"single-threaded; host {_cpu_model()}, nproc={os.cpu_count()}"}
         except Exception as e:  # the oracle .so is built where /root/reference exists
             cpu = {"value": None, "unit": "samples/s", "cores": 1, "kind": "reference", "sample": f"unavailable: {e}"}
-    acc = accuracy_vs_cpu(fb, local) if cpu and cpu.get("value") else None
+    if world == 1:
+        acc = side(lambda: accuracy_vs_cpu(fb, local))
+    extra = {}
+    if world == 1 and not args.no_side:
+        extra["config5_bf16"] = side(lambda: config5_fast(fb, torch, local, "bf16"))
+        extra["config2"] = side(lambda: config2_small(fb, torch, local))
+        extra["config3_resnet"] = side(lambda: config3_resnet(fb, torch, local))
+        extra["config4_budget"] = side(lambda: config4_budget(fb, torch, local))
     line = {
         "metric": "stream samples/sec", "value": value, "unit": "samples/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (synth_drift_stream split_tasks seed 7; make_dense_net seed 1)",
-        "config": {"workload": "C2: MLP 784-256-256-256-10, 4 pipeline stages on one GPU, iter_fisher, micro-batch 16",
-                   "global_batch": MICRO_BATCH, "units_per_step": units, "samples_per_step": chunk,
-                   "stages": len(BOUNDS) - 1, "parallelism": f"replicas{world}" if world > 1 else "pipeline-on-1",
-                   "l2": "flushed between timed steps (256 MB write)"},
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (synth_drift_stream split_tasks seed 7; make_dense_net seed 1)",
+        "config": workload_config(world),
         "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "call": "ferret_trainer_ingest (PipelineTrainer::run chunk after chunk) from pinned host buffers, "
-                        "host wall clock around the call"},
-        "roofline": {"bound": "hbm", "kernel": f"{dom} class ({KERNEL_OF[dom]})", "achieved": achieved,
-                     "peak": peak, "unit": "GB/s", "frac": achieved / peak, "peak_kind": peak_kind,
-                     "traffic": _traffic(dom), "alg_bytes_per_launch": dc["alg_bytes"] / dc["nodes"],
-                     "avg_launch_us": 1e3 * dc["ms"] / dc["nodes"],
-                     "share_of_serial_device_time": dc["ms"] / prof["serial_ms"],
-                     "dag_critical_path_ms": prof["critical_path_ms"], "classes": classes,
-                     "note": "C2 weights (1.3 MB) live in L2: the small-net path is latency-bound; "
-                             "config5_bf16 has the HBM-bound wide net"},
-        "config5_bf16": large,
-        "config5_fp32": large32,
-        "config3_resnet": conv3,
-        "config4_budget": budget4,
-        "stage_shard": shard,
-        "stage_shard_config5": shard5,
-        "stage_shard_config3": shard3,
+                "call": "ferret_trainer_ingest (PipelineTrainer::run chunk after chunk) from pinned host "
+                        "buffers, host wall clock around the call" + (", one chunk per call + barrier when "
+                                                                       "sharded" if world > 1 else "")},
+        "roofline": roofline,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
         "gpu_launches": int(launches_per_step * args.steps),
@@ -543,8 +518,11 @@ def main():
         "online_accuracy_last_chunk": oacc_last,
         "online_accuracy_vs_cpu": acc,
         "trainer": {"ring_depth": stats["ring_depth"], "stash_slots": stats["stash_slots"],
-                    "mean_tau": stats["mean_tau"], "device_bytes": stats["device_bytes"]},
+                    "mean_tau": stats["mean_tau"], "device_bytes": stats["device_bytes"],
+                    "stage_owner": fb.ferret.stage_owners(P, min(world, P)) if world > 1 else None},
+        "env": {k: v for k, v in os.environ.items() if k.startswith("FERRET_")},
     }
+    line.update(extra)
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

@@ -270,6 +270,30 @@ FERRET_API ferret_status ferret_trainer_comp_state(ferret_trainer* t, int32_t st
 /* TrainOutcome::normalizer (learner.hpp:180): count, mean[f], m2[f] */
 FERRET_API ferret_status ferret_trainer_normalizer(ferret_trainer* t, uint64_t* count, double* mean, double* m2,
                                         size_t n_features);
+/* ---- The reference's dense-net math (net.hpp:99-208) on the device, fp64 ----
+ * Host buffers in and out, synchronous, on the calling thread's current CUDA device.
+ * Every sum runs in the reference's index order with separately rounded products and
+ * sums, so affine_forward / forward_all / the gradients / apply_sgd are bit-identical to
+ * the reference's loops; exp and log are CUDA's (<= 2 ulp from glibc), so softmax and the
+ * loss (and the gradients through the softmax delta) agree to ~1e-15 relative.
+ * detail::affine_forward (net.hpp:99-108): z = W x + b, W row-major out x in */
+FERRET_API ferret_status ferret_affine_forward(const double* W, const double* b, uint64_t in, uint64_t out,
+                                               const double* x, double* z);
+/* detail::apply_activation (net.hpp:110-113), in place */
+FERRET_API ferret_status ferret_apply_activation(int32_t act, double* z, size_t n);
+/* detail::softmax (net.hpp:115-125) */
+FERRET_API ferret_status ferret_softmax(const double* z, size_t n, double* p);
+/* forward_all (net.hpp:130-142) for n samples (x: n x in, row-major): acts row s holds every
+ * layer's post-activation output, layer after layer (n x sum(out)) */
+FERRET_API ferret_status ferret_net_forward_all(const ferret_net_desc* net, const double* x, size_t n, double* acts);
+/* forward_backward (net.hpp:157-200): mean softmax cross-entropy over the batch and its
+ * gradients in flatten() order (per layer W then b); FERRET_E_INVALID_ARG for an empty
+ * batch or a label out of range */
+FERRET_API ferret_status ferret_net_forward_backward(const ferret_net_desc* net, const double* x,
+                                                     const uint64_t* labels, size_t n, double* loss, double* grads);
+/* apply_sgd (net.hpp:202-208): params -= lr * grads, in place, flatten() order */
+FERRET_API ferret_status ferret_net_apply_sgd(double* params, const double* grads, size_t n, double lr);
+
 /* The replay draws made so far (ReplayBuffer::sample, learner.hpp:75-78, called by
  * replay_step :513-519): the stream sample index of every drawn sample, in draw order,
  * across every run/execute/ingest call of this trainer (B draws per replay step at
@@ -306,6 +330,12 @@ FERRET_API ferret_status ferret_trainer_set_timing(ferret_trainer* t, int32_t en
  * the serial total, and the critical
  * path of the concurrent DAG computed from the measured node times. */
 FERRET_API ferret_status ferret_trainer_set_profiling(ferret_trainer* t, int32_t enable);
+/* After a profiled execute(): per KERNEL SYMBOL (demangled, '\n'-separated in `names`, in
+ * first-launch order) the summed device ms, launch count and algorithmic HBM bytes of its
+ * launches in the chunk. Writes min(cap, n) entries; *n_kernels = distinct kernels. */
+FERRET_API ferret_status ferret_trainer_profile_kernels(ferret_trainer* t, char* names, size_t names_cap,
+                                                        double* ms, uint64_t* launches, double* alg_bytes,
+                                                        int32_t cap, int32_t* n_kernels);
 /* After ferret_trainer_profile: per node class, device ms and node count along the critical path. */
 FERRET_API ferret_status ferret_trainer_profile_critical(ferret_trainer* t, double* class_ms, uint64_t* class_nodes,
                                                          int32_t n_classes);

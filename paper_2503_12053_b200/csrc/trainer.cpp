@@ -37,6 +37,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <cxxabi.h>
 #include <map>
 #include <set>
 #include <tuple>
@@ -237,6 +238,8 @@ struct GraphBuilder {
     double cur_bytes = 0.0;       // algorithmic HBM bytes of the next node (set by the emitter)
     std::vector<double> bytes;
     std::vector<int> stage_of;
+    const void* cur_func = nullptr;  // kernel of the next node (null: copy / memset / event)
+    std::vector<const void*> funcs;
     struct Res {
         int writer = -1;
         std::vector<int> readers;
@@ -313,7 +316,9 @@ struct GraphBuilder {
         category.push_back(cur_category);
         bytes.push_back(cur_bytes);
         stage_of.push_back(cur_stage);
+        funcs.push_back(cur_func);
         cur_bytes = 0.0;
+        cur_func = nullptr;
         last = n;
         if (serial && prof_events) {  // event after the node
             cudaGraphNode_t e;
@@ -350,6 +355,7 @@ struct GraphBuilder {
         p.kernelParams = k.kernel_params();
         cudaGraphNode_t n;
         cuda_check(cudaGraphAddKernelNode(&n, g, d.data(), d.size(), &p), "cudaGraphAddKernelNode");
+        cur_func = k.func;
         // FERRET_NODE_PRIORITY=<class digits>: those node classes (1 predict, 2 forward,
         // 3 backward, 4 update) run at the device's highest kernel priority, so the
         // per-stage version chain (the DAG's critical path) is not queued behind others
@@ -616,6 +622,7 @@ struct ferret_trainer {
     std::vector<double> crit_class_ms;     // critical path composition of the last profile()
     std::vector<uint64_t> crit_class_nodes;
     std::vector<int> prof_stage;
+    std::vector<const void*> prof_func;
 
     // optional per-launch timing of the update kernel (event record nodes)
     bool timing = false;
@@ -1254,6 +1261,7 @@ struct ferret_trainer {
         prof_cat = std::move(builder.category);
         prof_bytes = std::move(builder.bytes);
         prof_stage = std::move(builder.stage_of);
+        prof_func = std::move(builder.funcs);
         graph_profiling = profiling;
         graph_shape = got;
         graph_timing = timing;
@@ -2635,8 +2643,9 @@ struct ferret_trainer {
     void ingest(const double* features, const uint64_t* lab, size_t n, size_t f, ferret_step_record* log) {
         if (!have_schedule) fail(FERRET_E_LOGIC, "ingest: no schedule set");
         // stage-sharded trainers reuse their inboxes every chunk and need a barrier between
-        // chunks, which a multi-chunk call cannot insert
-        if (world > 1) fail(FERRET_E_CONFIG, "ingest: not available on a stage-sharded trainer (world > 1)");
+        // chunks, which a multi-chunk call cannot insert: one chunk per call there
+        if (world > 1 && n != sched.chunk_items)
+            fail(FERRET_E_CONFIG, "ingest: a stage-sharded trainer (world > 1) takes one chunk per call");
         if (static_cast<int>(f) != F) fail(FERRET_E_INVALID_ARG, "stream feature width does not match the net input");
         const size_t chunk = sched.chunk_items;
         if (n % chunk) fail(FERRET_E_INVALID_ARG, "ingest: sample count must be a whole number of chunks");
@@ -3097,6 +3106,55 @@ ferret_status ferret_trainer_profile(ferret_trainer* t, double* class_ms, uint64
             const int c = t->prof_cat[static_cast<size_t>(i)];
             t->crit_class_ms[static_cast<size_t>(c)] += dur[static_cast<size_t>(i)];
             t->crit_class_nodes[static_cast<size_t>(c)] += 1;
+        }
+    });
+}
+
+ferret_status ferret_trainer_profile_kernels(ferret_trainer* t, char* names, size_t names_cap, double* ms,
+                                             uint64_t* launches, double* alg_bytes, int32_t cap, int32_t* n_kernels) {
+    return guarded([&] {
+        if (!t->graph_profiling) fail(FERRET_E_LOGIC, "profile: the last execute() did not run a profiling graph");
+        cuda_check(cudaStreamSynchronize(t->stream), "sync");
+        std::vector<const void*> order;
+        std::map<const void*, std::tuple<double, uint64_t, double>> agg;
+        for (size_t i = 0; i < t->prof_func.size(); ++i) {
+            const void* f = t->prof_func[i];
+            if (!f) continue;
+            float m = 0.f;
+            cuda_check(cudaEventElapsedTime(&m, t->prof_events[2 * i], t->prof_events[2 * i + 1]), "cudaEventElapsedTime");
+            auto it = agg.find(f);
+            if (it == agg.end()) {
+                order.push_back(f);
+                it = agg.emplace(f, std::make_tuple(0.0, uint64_t{0}, 0.0)).first;
+            }
+            std::get<0>(it->second) += m;
+            std::get<1>(it->second) += 1;
+            std::get<2>(it->second) += t->prof_bytes[i];
+        }
+        std::string text;
+        int32_t k = 0;
+        for (const void* f : order) {
+            const char* raw = nullptr;
+            std::string name = "?";
+            if (cudaFuncGetName(&raw, f) == cudaSuccess && raw) {
+                int st = 0;
+                char* dem = abi::__cxa_demangle(raw, nullptr, nullptr, &st);
+                name = (st == 0 && dem) ? dem : raw;
+                std::free(dem);
+            }
+            if (k < cap) {
+                ms[k] = std::get<0>(agg[f]);
+                launches[k] = std::get<1>(agg[f]);
+                alg_bytes[k] = std::get<2>(agg[f]);
+            }
+            text += name + "\n";
+            ++k;
+        }
+        *n_kernels = k;
+        if (names && names_cap) {
+            const size_t m = std::min(text.size(), names_cap - 1);
+            std::memcpy(names, text.data(), m);
+            names[m] = '\0';
         }
     });
 }

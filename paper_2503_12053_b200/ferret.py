@@ -139,6 +139,8 @@ def lib() -> C.CDLL:
         "ferret_trainer_comp_state": (C.c_int, [C.c_void_p, C.c_int32, P(D), P(D), P(D), P(D), C.c_size_t]),
         "ferret_trainer_normalizer": (C.c_int, [C.c_void_p, P(C.c_uint64), P(D), P(D), C.c_size_t]),
         "ferret_trainer_replay_draws": (C.c_int, [C.c_void_p, P(C.c_int64), C.c_size_t, P(C.c_size_t)]),
+        "ferret_trainer_profile_kernels": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t, P(D), P(C.c_uint64), P(D),
+                                                     C.c_int32, P(C.c_int32)]),
         "ferret_trainer_get_stats": (C.c_int, [C.c_void_p, P(TrainerStats)]),
         "ferret_trainer_destroy": (None, [C.c_void_p]),
         "ferret_trainer_set_timing": (C.c_int, [C.c_void_p, C.c_int32]),
@@ -467,6 +469,24 @@ class PipelineTrainer:
         m2 = np.empty(n_features, dtype=np.float64)
         _check(lib().ferret_trainer_normalizer(self._h, C.byref(cnt), _dp(mean), _dp(m2), n_features))
         return int(cnt.value), mean, m2
+
+    def profile_kernels(self) -> dict:
+        """After a profiled execute(): {kernel symbol: {ms, launches, alg_bytes, us_per_launch, gbs}}."""
+        cap = 64
+        ms = np.zeros(cap)
+        n_l = np.zeros(cap, dtype=np.uint64)
+        by = np.zeros(cap)
+        names = C.create_string_buffer(1 << 16)
+        k = C.c_int32()
+        _check(lib().ferret_trainer_profile_kernels(self._h, names, len(names), _dp(ms),
+                                                    n_l.ctypes.data_as(C.POINTER(C.c_uint64)), _dp(by), cap,
+                                                    C.byref(k)))
+        out = {}
+        for i, nm in enumerate(names.value.decode().splitlines()[: min(k.value, cap)]):
+            out[nm] = {"ms": float(ms[i]), "launches": int(n_l[i]), "alg_bytes": float(by[i]),
+                       "us_per_launch": 1e3 * float(ms[i]) / max(int(n_l[i]), 1),
+                       "gbs": float(by[i]) / (float(ms[i]) * 1e-3) / 1e9 if ms[i] > 0 else 0.0}
+        return out
 
     def replay_draws(self) -> np.ndarray:
         """Stream sample index of every replay draw so far, in draw order

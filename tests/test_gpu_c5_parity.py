@@ -1,0 +1,110 @@
+"""BASELINE config 5 at full size against the fp64 CPU reference: MLP 16 x 4096 (+ 10-way
+head, 251.8 M parameters), 8 stages [0,2,...,16], iter_fisher, micro-batch 16, the first
+16 pipeline units (256 samples) of the bench stream. The reference run (oracle/_ref, the
+reference headers + the item-keyed PipelineTrainer restatement, itself bit-identical to the
+key-patched reference trainer) takes ~30 min and ~45 GB on one core, so its result is the
+committed fixture tests/golden/c5_oracle.npz (tests/golden/make_c5_fixture.py): per-stage
+norms, a seeded sample of 8192 parameters per stage with their iter_fisher state, the full
+StepRecord log and the normalizer state.
+
+Bars (north star): fp32 parity mode — parameters within 1e-4 relative per stage (on the
+sample, plus the per-stage norms), online accuracy within 0.5 pp; bf16 / tf32 fast modes —
+online accuracy within 0.5 pp."""
+import os
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+FIXTURE = os.path.join(ROOT, "tests", "golden", "c5_oracle.npz")
+PARAM_RTOL = 1e-4
+OACC_TOL = 0.5
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fix():
+    return np.load(FIXTURE)
+
+
+def _run(fb, g, precision):
+    widths = [int(x) for x in g["widths"]]
+    bounds = [int(x) for x in g["bounds"]]
+    units, B = int(g["units"]), int(g["micro_batch"])
+    prof = fb.profile_from_widths(widths)
+    t_d = float(prof["t_f"].max())
+    sched = fb.Schedule.forced(prof, t_d, fb.StreamSpec(t_d=t_d, horizon=units * t_d), bounds, units)
+    feats, labels = fb.synth_drift_stream(units * B, widths[0], widths[-1], "split_tasks", 7)
+    init = fb.make_dense_net(widths, 1)
+    tr = fb.PipelineTrainer(widths, init, bounds,
+                            fb.PipelineTrainOptions(policy="iter_fisher", micro_batch=B, precision=precision))
+    log = tr.run(sched.events, feats, labels)
+    out = {"log": log, "params": tr.params(), "init": init, "widths": widths, "bounds": bounds,
+           "norm": tr.normalizer(widths[0])}
+    if precision == "fp32":
+        offs = np.concatenate([[0], np.cumsum([widths[i] * widths[i + 1] + widths[i + 1]
+                                               for i in range(len(widths) - 1)])])
+        pos = g["sample_pos"]
+        lam, vr, va = (np.zeros(len(pos)) for _ in range(3))
+        for j in range(len(bounds) - 1):
+            lo, hi = int(offs[bounds[j]]), int(offs[bounds[j + 1]])
+            sel = (pos >= lo) & (pos < hi)
+            l_, r_, a_, _ = tr.comp_state(j, hi - lo)
+            lam[sel], vr[sel], va[sel] = l_[pos[sel] - lo], r_[pos[sel] - lo], a_[pos[sel] - lo]
+        out.update(lam=lam, vr=vr, va=va)
+    tr.close()
+    return out
+
+
+def _stage_ranges(widths, bounds):
+    offs = np.concatenate([[0], np.cumsum([widths[i] * widths[i + 1] + widths[i + 1] for i in range(len(widths) - 1)])])
+    return [(int(offs[bounds[j]]), int(offs[bounds[j + 1]])) for j in range(len(bounds) - 1)]
+
+
+def test_c5_fp32_parity_against_cpu_reference(gpu, fb, fix):
+    g = fix
+    r = _run(fb, g, "fp32")
+    got, init = r["params"], r["init"]
+    pos = g["sample_pos"]
+    ref_s, init_s = g["params_sample"], g["init_sample"]
+    assert np.array_equal(init[pos], init_s)  # same initial net as the reference run
+    for j, (lo, hi) in enumerate(_stage_ranges(r["widths"], r["bounds"])):
+        sel = (pos >= lo) & (pos < hi)
+        rel = np.linalg.norm(got[pos[sel]] - ref_s[sel]) / np.linalg.norm(ref_s[sel])
+        assert rel < PARAM_RTOL, f"stage {j}: sampled param rel err {rel:.3e}"
+        # training moved this stage, and the GPU moved it the same way (update-relative error)
+        moved_ref = ref_s[sel] - init_s[sel]
+        assert np.linalg.norm(moved_ref) > 0
+        upd = np.linalg.norm((got[pos[sel]] - init_s[sel]) - moved_ref) / np.linalg.norm(moved_ref)
+        assert upd < 2e-2, f"stage {j}: update-relative error {upd:.3e}"
+        # whole-stage norms (all 33.5 M parameters, not just the sample)
+        n_got = np.linalg.norm(got[lo:hi])
+        assert abs(n_got - g["stage_norm"][j]) / g["stage_norm"][j] < PARAM_RTOL
+        m_got = np.linalg.norm(got[lo:hi] - init[lo:hi])
+        assert abs(m_got - g["stage_moved"][j]) / g["stage_moved"][j] < 2e-2
+    log, ref_log = r["log"], g["log"]
+    assert abs(fb.online_accuracy(log) - float(g["oacc"])) <= OACC_TOL
+    assert np.array_equal(log["label"], ref_log["label"]) and np.array_equal(log["item"], ref_log["item"])
+    assert np.array_equal(log["outcome"] == 2, ref_log["outcome"] == 2)
+    assert np.count_nonzero(log["predicted"] != ref_log["predicted"]) <= 2
+    cnt, mean, m2 = r["norm"]
+    assert cnt == int(g["norm_count"])
+    assert np.array_equal(mean, g["norm_mean"]) and np.array_equal(m2, g["norm_m2"])
+    # iter_fisher state on the sample (tolerances as in test_gpu_parity._compare)
+    d_ref, d_got = g["lambda_sample"] - 0.2, r["lam"] - 0.2
+    if np.linalg.norm(d_ref) > 0:
+        assert np.linalg.norm(d_got - d_ref) / np.linalg.norm(d_ref) < 2e-2
+    for a, b, tol in ((r["vr"], g["v_r_sample"], 1e-3), (r["va"], g["v_a_sample"], 3e-3)):
+        if np.linalg.norm(b) > 0:
+            assert np.linalg.norm(a - b) / np.linalg.norm(b) < tol
+
+
+@pytest.mark.parametrize("precision", ["bf16", "tf32"])
+def test_c5_fast_modes_online_accuracy(gpu, fb, fix, precision):
+    g = fix
+    r = _run(fb, g, precision)
+    assert np.all(np.isfinite(r["params"]))
+    d = abs(fb.online_accuracy(r["log"]) - float(g["oacc"]))
+    assert d <= OACC_TOL, f"{precision}: online accuracy {fb.online_accuracy(r['log']):.2f} vs {float(g['oacc']):.2f}"
+    assert np.array_equal(r["log"]["outcome"] == 2, g["log"]["outcome"] == 2)
