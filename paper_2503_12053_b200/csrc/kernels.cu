@@ -1054,6 +1054,156 @@ __global__ void __launch_bounds__(kThreads) update_stream_kernel(const UpdArgs a
     }
 }
 
+// ---------------------------------------------------------------------------
+// update_group_kernel: G consecutive iter_fisher updates of one stage in one launch
+// (GroupArgs, kernels.cuh). A CTA owns <= kGroupRows rows x 256 columns of one weight
+// matrix (a thread: one column, the tile's rows) or 256 bias elements (a thread: one).
+// Per element the chain is held as its successive DIFFERENCES d[s] = v[s+1] - v[s] (the
+// fold only ever uses differences, and d[s] is the same fp32 value update_iter1_kernel
+// recomputes from the stored versions) plus the live value; update k folds over
+// d[first_k .. n-2], writes version n and appends its difference. The unit deltas of every
+// update and tile row are staged in smem once; the unit inputs x_k[b][c] of the thread's
+// column are loaded per update (L2-resident activations) and reused across the rows.
+// CM = difference capacity (chain span - 1), BT = micro-batch bound.
+// ---------------------------------------------------------------------------
+template <int CM, int BT>
+__global__ void __launch_bounds__(kThreads, 1) update_group_kernel(const GroupArgs a) {
+    __shared__ float sdel[kGroupMax * kMaxBatch * kGroupRows];
+    const UpdWork w = a.works[blockIdx.x];
+    const int tid = threadIdx.x, B = a.B, G = a.G;
+    const bool bias = w.bias != 0;
+    const bool gm = w.g_off >= 0;  // materialised gradients (convolutions)
+    const int R = bias ? 1 : w.nrows;
+    const int c = w.c0 + tid;
+    const bool live = bias ? tid < w.nrows : c < w.in;
+    if (!bias && !gm) {  // deltas of every update and tile row: sdel[(k * BT + b) * 4 + i]
+        for (int q = tid; q < G * BT * kGroupRows; q += kThreads) {
+            const int i = q % kGroupRows, b = (q / kGroupRows) % BT, k = q / (kGroupRows * BT);
+            sdel[q] = (b < B && i < R) ? __ldg(a.pend[k].stash + w.dlt_off + (size_t)b * w.out + w.r0 + i) : 0.f;
+        }
+    }
+    __syncthreads();
+    if (!live) return;
+    size_t e[kGroupRows];
+#pragma unroll
+    for (int i = 0; i < kGroupRows; ++i)
+        e[i] = bias ? (size_t)w.elem0 + w.r0 + tid : (size_t)w.elem0 + (size_t)(w.r0 + (i < R ? i : 0)) * w.in + c;
+    // the HBM chain -> differences + live value; the compensator state
+    float d[kGroupRows][CM], cur[kGroupRows], ld[kGroupRows], vr[kGroupRows], va[kGroupRows];
+#pragma unroll
+    for (int i = 0; i < kGroupRows; ++i) {
+        if (i >= R) break;
+        float prev = __ldg(a.vers[0] + e[i]);
+#pragma unroll
+        for (int s = 0; s < CM; ++s) {
+            if (s + 1 < a.n0) {
+                const float nxt = __ldg(a.vers[s + 1] + e[i]);
+                d[i][s] = nxt - prev;
+                prev = nxt;
+            }
+        }
+        cur[i] = prev;
+        ld[i] = a.lam_d[e[i]];
+        vr[i] = a.learn ? a.v_r[e[i]] : 0.f;
+        va[i] = a.learn ? a.v_a[e[i]] : 0.f;
+    }
+    const float one_m_a = 1.f - a.alpha;
+    int n = a.n0;  // chain length so far (versions 0 .. n-1; cur = version n-1)
+    for (int k = 0; k < G; ++k) {
+        const UpdPending& pk = a.pend[k];
+        const int first = pk.first;
+        // the unit's inputs of this column (weights) — reused by the tile's rows
+        float xv[BT];
+        if (!bias && !gm) {
+            const float* xr0 = w.xin_off >= 0 ? pk.stash + w.xin_off : nullptr;
+#pragma unroll
+            for (int b = 0; b < BT; ++b) {
+                const float* xr = xr0 ? xr0 + (size_t)b * w.in
+                                  : a.x0idx ? pk.x0 + (size_t)__ldg(a.x0idx + b) * a.x0_ld
+                                            : pk.x0 + (size_t)b * a.x0_ld;
+                xv[b] = b < B ? __ldg(xr + c) : 0.f;
+            }
+        }
+        float o[kGroupRows], g[kGroupRows], lam[kGroupRows];
+#pragma unroll
+        for (int i = 0; i < kGroupRows; ++i) {
+            if (i >= R) break;
+            float gi = 0.f;
+            if (gm) {
+                gi = bias ? __ldg(pk.stash + w.g_off + w.r0 + tid) : __ldg(pk.stash + w.g_off + (size_t)(w.r0 + i) * w.in + c);
+            } else if (bias) {
+                const float* dl = pk.stash + w.dlt_off + w.r0 + tid;
+#pragma unroll
+                for (int b = 0; b < BT; ++b)
+                    if (b < B) gi += __ldg(dl + (size_t)b * w.out);
+            } else {
+#pragma unroll
+                for (int b = 0; b < BT; ++b)
+                    if (b < B) gi = fmaf(sdel[(k * BT + b) * kGroupRows + i], xv[b], gi);
+            }
+            g[i] = gi;
+            // iter_fisher state step (compensate.hpp:87-95) when the chain has >= 2 versions
+            float l = a.lambda0 + ld[i];
+            if (a.learn && n - first >= 2) {
+                float d0 = 0.f;
+#pragma unroll
+                for (int s = 0; s < CM; ++s)
+                    if (s == first) d0 = d[i][s];
+                const float dv = one_m_a * (gi - vr[i]);
+                const float resid = dv - l * va[i];
+                const float grad_l = -2.f * resid * va[i] + 2.f * a.nu * l;
+                ld[i] -= a.eta * grad_l;
+                l = a.lambda0 + ld[i];
+                vr[i] = a.alpha * vr[i] + one_m_a * gi;
+                va[i] = a.alpha * va[i] + one_m_a * gi * gi * d0;
+            }
+            lam[i] = l;
+            o[i] = gi;
+        }
+        // the fold over the chain (compensate.hpp:97-102), rows interleaved
+#pragma unroll
+        for (int s = 0; s < CM; ++s) {
+            if (s >= n - 1) break;
+            if (s >= first) {
+#pragma unroll
+                for (int i = 0; i < kGroupRows; ++i)
+                    if (i < R) o[i] += lam[i] * o[i] * o[i] * d[i][s];
+            }
+        }
+        // theta_new = theta_cur - lr * out (learner.hpp:497-502); append its difference
+#pragma unroll
+        for (int i = 0; i < kGroupRows; ++i) {
+            if (i >= R) break;
+            const float nv = cur[i] - a.step * o[i];
+#pragma unroll
+            for (int s = 0; s < CM; ++s)
+                if (s == n - 1) d[i][s] = nv - cur[i];
+            cur[i] = nv;
+            a.dst[k][e[i]] = nv;
+            if (a.dst16[k]) reinterpret_cast<__nv_bfloat16*>(a.dst16[k])[e[i]] = __float2bfloat16_rn(nv);
+        }
+        ++n;
+    }
+#pragma unroll
+    for (int i = 0; i < kGroupRows; ++i) {
+        if (i >= R) break;
+        a.lam_d[e[i]] = ld[i];
+        if (a.learn) {
+            a.v_r[e[i]] = vr[i];
+            a.v_a[e[i]] = va[i];
+        }
+    }
+}
+
+template <int BT>
+const void* group_func(int span) {
+    if (span <= 8) return reinterpret_cast<const void*>(&update_group_kernel<7, BT>);
+    if (span <= 16) return reinterpret_cast<const void*>(&update_group_kernel<15, BT>);
+    if (span <= 24) return reinterpret_cast<const void*>(&update_group_kernel<23, BT>);
+    if (span <= 32) return reinterpret_cast<const void*>(&update_group_kernel<31, BT>);
+    return reinterpret_cast<const void*>(&update_group_kernel<kGroupChainMax - 1, BT>);
+}
+
 template <int BT>
 const void* stream_func(size_t smem) {
     static size_t configured = 0;  // (static smem counts against the 48 KB default too)
@@ -1354,6 +1504,13 @@ void spec_update(const UpdArgs& a, KernelSpec& k) {
     const void* f = a.policy == 0 ? update_func<0>(a.B) : a.policy == 1 ? update_func<1>(a.B)
                   : a.policy == 2 ? update_func<2>(a.B) : a.policy == 3 ? update_func<3>(a.B) : update_func<4>(a.B);
     fill(k, f, dim3((unsigned)blocks), dim3(kThreads), a);
+}
+
+void spec_update_group(const GroupArgs& a, KernelSpec& k) {
+    const int span = a.n0 + a.G;  // versions spanned: the HBM chain + the group's outputs
+    const void* f = a.B <= 1 ? group_func<1>(span) : a.B <= 2 ? group_func<2>(span) : a.B <= 4 ? group_func<4>(span)
+                  : a.B <= 8 ? group_func<8>(span) : group_func<16>(span);
+    fill(k, f, dim3((unsigned)a.n_tiles), dim3(kThreads), a);
 }
 
 void spec_normalize(const NormArgs& a, KernelSpec& k) {

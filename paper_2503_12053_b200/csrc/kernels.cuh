@@ -147,6 +147,35 @@ struct UpdArgs {
     float step;     // lr / K
 };
 
+// A GROUP of consecutive iter_fisher updates of one stage (one pending gradient each),
+// fused into one launch: update k of the group is learner.hpp:491-510 with the chain
+// [vers[first_k] .. version cur0 + k]; the versions after cur0 are the group's own outputs,
+// kept in registers, so the chain is read from HBM once for the whole group and the
+// compensator state is read and written once. Per element the arithmetic is exactly
+// update_iter1_kernel's, update after update (bit-identical results). The trainer forms
+// groups while compiling the log (trainer.cpp: pending update groups): a group is emitted
+// as late as the first later node that touches one of its resources, so deferring its
+// members past the nodes in between never changes what any node reads.
+constexpr int kGroupMax = 32;        // updates per group
+constexpr int kGroupChainMax = 40;   // versions a group spans: HBM chain + its own outputs
+constexpr int kGroupRows = 4;        // weight rows per thread (a CTA: 4 rows x 256 columns)
+struct GroupArgs {
+    const UpdWork* works;            // the stage's group tiles (weights: <= 4 rows x 256 columns)
+    int n_tiles;
+    int B, G, n0;                    // micro-batch, updates, chain versions read from HBM
+    int learn;                       // eta_lambda > 0 (v_r / v_a tracked)
+    const float* vers[kGroupChainMax];  // vers[0] = oldest read version ... vers[n0 - 1] = cur0
+    UpdPending pend[kGroupMax];      // update k: its unit's stash, net-input rows, first chain index
+    float* dst[kGroupMax];           // slot of version cur0 + 1 + k
+    unsigned short* dst16[kGroupMax];  // its bf16 copy (bf16 fast mode) or null
+    const int* x0idx;
+    int x0_ld;
+    float* lam_d;
+    float* v_r;
+    float* v_a;
+    float lambda0, alpha, eta, nu, step;
+};
+
 // RunningNormalizer over a run of arrivals (reference stream.hpp:307-334):
 // fp64, one thread per feature, sequential over items; bit-exact with the host.
 struct NormArgs {
@@ -268,6 +297,7 @@ bool fwd_single_cta(int in, int out, int B, bool vec);
 void spec_head(const HeadArgs& a, KernelSpec& k);
 void spec_bwd(const BwdArgs& a, KernelSpec& k);
 void spec_update(const UpdArgs& a, KernelSpec& k);
+void spec_update_group(const GroupArgs& a, KernelSpec& k);
 void spec_normalize(const NormArgs& a, KernelSpec& k);
 void spec_welford(const NormArgs& a, KernelSpec& k);
 void spec_standardize(const NormArgs& a, KernelSpec& k);

@@ -38,6 +38,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <cxxabi.h>
+#include <functional>
 #include <map>
 #include <set>
 #include <tuple>
@@ -188,6 +189,8 @@ struct StageDev {
     fb200::UpdWork* works4_dev = nullptr;  // float4 tiles (nullptr when a weight row is not 16-byte aligned)
     int n_tiles4 = 0, threads4 = 0;
     int n_tiles = 0;
+    fb200::UpdWork* works_g_dev = nullptr;  // update-group tiles (weights: <= 4 rows x 256 columns)
+    int n_tiles_g = 0;
     long long n_items = 0;
     // slot of a version counted from the chunk start (the live version is in slot 0 between chunks)
     float* slot(long long rel) const { return ring + (rel % depth) * slot_floats; }
@@ -338,6 +341,23 @@ struct GraphBuilder {
     // graph nodes (the caller may be capturing the stream into a graph)
     cudaStream_t eager = nullptr;
 
+    // Called before a node is added with the resources it will read and write (the
+    // trainer's pending update groups flush themselves here on a conflict). The
+    // emitter's next-node fields are preserved across the call.
+    std::function<void(const std::vector<uint64_t>&, const std::vector<uint64_t>&)> before;
+    bool in_before = false;
+    void check_before(const std::vector<uint64_t>& reads, const std::vector<uint64_t>& writes) {
+        if (!before || in_before) return;
+        in_before = true;
+        const int cc = cur_category, cs = cur_stage;
+        const double cb = cur_bytes;
+        before(reads, writes);
+        cur_category = cc;
+        cur_stage = cs;
+        cur_bytes = cb;
+        in_before = false;
+    }
+
     cudaGraphNode_t kernel(fb200::KernelSpec& k, const std::vector<uint64_t>& reads, const std::vector<uint64_t>& writes) {
         if (eager) {
             cuda_check(fb200::launch_spec(k, eager), "kernel launch");
@@ -345,6 +365,7 @@ struct GraphBuilder {
             cur_bytes = 0.0;
             return nullptr;
         }
+        check_before(reads, writes);
         const std::vector<int> ld = logical(reads, writes);
         const std::vector<cudaGraphNode_t> d = deps(ld);
         cudaKernelNodeParams p{};
@@ -378,6 +399,7 @@ struct GraphBuilder {
             cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, eager), "cudaMemcpyAsync");
             return nullptr;
         }
+        check_before(reads, writes);
         const std::vector<int> ld = logical(reads, writes);
         const std::vector<cudaGraphNode_t> d = deps(ld);
         cudaGraphNode_t n;
@@ -656,6 +678,7 @@ struct ferret_trainer {
             dfree(s.tiles_dev);
             dfree(s.works_dev);
             dfree(s.works4_dev);
+            dfree(s.works_g_dev);
             dfree(s.ring16);
         }
         for (auto& kv : mma_scratch) {
@@ -887,6 +910,25 @@ struct ferret_trainer {
             s.works_dev = dalloc<fb200::UpdWork>(works.size(), device_bytes);
             cuda_check(cudaMemcpy(s.works_dev, works.data(), works.size() * sizeof(fb200::UpdWork), cudaMemcpyHostToDevice),
                        "upload work table");
+            {  // update-group tiles: kGroupRows rows x 256 columns, bias runs of 256
+                std::vector<fb200::UpdWork> wg;
+                for (const fb200::UpdSeg& sg : tab) {
+                    if (sg.bias) {
+                        for (int r0 = 0; r0 < sg.out; r0 += fb200::kUpdTileCols)
+                            wg.push_back({sg.elem0, sg.xin_off, sg.dlt_off, sg.in, sg.out, 1, r0,
+                                          std::min(fb200::kUpdTileCols, sg.out - r0), 0, sg.g_off});
+                    } else {
+                        for (int r0 = 0; r0 < sg.out; r0 += fb200::kGroupRows)
+                            for (int c0 = 0; c0 < sg.in; c0 += fb200::kUpdTileCols)
+                                wg.push_back({sg.elem0, sg.xin_off, sg.dlt_off, sg.in, sg.out, 0, r0,
+                                              std::min(fb200::kGroupRows, sg.out - r0), c0, sg.g_off});
+                    }
+                }
+                s.n_tiles_g = static_cast<int>(wg.size());
+                s.works_g_dev = dalloc<fb200::UpdWork>(wg.size(), device_bytes);
+                cuda_check(cudaMemcpy(s.works_g_dev, wg.data(), wg.size() * sizeof(fb200::UpdWork), cudaMemcpyHostToDevice),
+                           "upload group work table");
+            }
             s.tiles_dev = dalloc<fb200::UpdTile>(tiles.size(), device_bytes);
             cuda_check(cudaMemcpy(s.tiles_dev, tiles.data(), tiles.size() * sizeof(fb200::UpdTile), cudaMemcpyHostToDevice),
                        "upload tile table");
@@ -1382,6 +1424,88 @@ struct ferret_trainer {
             }
         }
 
+        // ---- pending update groups (kernels.cuh GroupArgs): consecutive iter_fisher updates of
+        // a stage (one pending gradient each) are collected instead of emitted; the group is
+        // emitted as ONE node as soon as a later node would read what it writes (a version it
+        // produces, the compensator state) or write what it reads (a member's stash slot, a
+        // chain version), when it is full, and at the end of the log. Every node emitted in
+        // between touches none of the group's resources, so deferring the members past them
+        // is exactly equivalent; the DAG the builder derives is the same one with the
+        // members' nodes merged.
+        struct PGroup {
+            long long cur0 = 0, oldest = 0;
+            std::vector<Pend> members;
+            std::vector<const float*> stash_of, x0_of;  // captured at join (a unit's slot is freed after its update)
+            std::vector<uint64_t> reads, writes;  // sorted, unique
+        };
+        std::vector<PGroup> groups(static_cast<size_t>(P));
+        const bool grouping = !DRY && group_updates && !timing && !as_shipped && opt.policy == FERRET_POLICY_ITER_FISHER;
+        auto add_keys = [](std::vector<uint64_t>& v, std::initializer_list<uint64_t> ks) {
+            v.insert(v.end(), ks.begin(), ks.end());
+        };
+        auto tidy = [](std::vector<uint64_t>& v) {
+            std::sort(v.begin(), v.end());
+            v.erase(std::unique(v.begin(), v.end()), v.end());
+        };
+        auto flush_group = [&](int j) {
+            PGroup g = std::move(groups[static_cast<size_t>(j)]);
+            groups[static_cast<size_t>(j)] = PGroup{};
+            if (g.members.empty()) return;
+            const StageDev& sd = stages[static_cast<size_t>(j)];
+            fb200::GroupArgs a{};
+            a.works = sd.works_g_dev;
+            a.n_tiles = sd.n_tiles_g;
+            a.B = B;
+            a.G = static_cast<int>(g.members.size());
+            a.n0 = static_cast<int>(g.cur0 - g.oldest + 1);
+            a.learn = (opt.eta_lambda > 0.0 && sd.v_r) ? 1 : 0;
+            for (long long v = g.oldest; v <= g.cur0; ++v) a.vers[v - g.oldest] = sd.slot(v);
+            for (size_t k = 0; k < g.members.size(); ++k) {
+                const Pend& m = g.members[k];
+                a.pend[k] = {g.stash_of[k], g.x0_of[k], static_cast<int>(m.read - g.oldest)};
+                a.dst[k] = sd.slot(g.cur0 + 1 + static_cast<long long>(k));
+                a.dst16[k] = sd.ring16 ? const_cast<uint16_t*>(sd.shadow(a.dst[k])) : nullptr;
+            }
+            a.x0idx = nullptr;
+            a.x0_ld = F;
+            a.lam_d = sd.lam_d;
+            a.v_r = sd.v_r;
+            a.v_a = sd.v_a;
+            a.lambda0 = static_cast<float>(opt.lambda0);
+            a.alpha = static_cast<float>(opt.alpha);
+            a.eta = static_cast<float>(opt.eta_lambda);
+            a.nu = static_cast<float>(opt.nu);
+            a.step = static_cast<float>(opt.lr * (1.0 / 1.0));
+            fb200::KernelSpec k;
+            fb200::spec_update_group(a, k);
+            gb->cur_bytes = group_bytes(j, a.n0, a.G);
+            gb->cur_category = kCatUpdate;
+            gb->cur_stage = j;
+            gb->kernel(k, g.reads, g.writes);
+            for (int q = 0; q < a.G; ++q) wt_invalidate(sd, a.dst[q]);
+            ++n_group_nodes;
+        };
+        auto hits = [](const std::vector<uint64_t>& sorted, const std::vector<uint64_t>& keys) {
+            for (uint64_t x : keys)
+                if (std::binary_search(sorted.begin(), sorted.end(), x)) return true;
+            return false;
+        };
+        struct HookReset {
+            GraphBuilder* b;
+            ~HookReset() {
+                if (b) b->before = nullptr;
+            }
+        } hook_reset{grouping ? gb : nullptr};
+        if (grouping)
+            gb->before = [&](const std::vector<uint64_t>& r, const std::vector<uint64_t>& w) {
+                for (int q = 0; q < P; ++q) {
+                    const PGroup& g = groups[static_cast<size_t>(q)];
+                    if (g.members.empty()) continue;
+                    if (hits(g.writes, r) || hits(g.writes, w) || hits(g.reads, w)) flush_group(q);
+                }
+            };
+        if (!DRY) n_group_nodes = 0;
+
         for (size_t idx = 0; idx < sched.events.size(); ++idx) {
             if (!DRY && !gb->prof_events && gb->nodes_in_segment() >= seg_nodes) gb->new_segment();
             const ferret_event& e = sched.events[idx];
@@ -1467,7 +1591,34 @@ struct ferret_trainer {
                     }
                     ++n_upd;
                     if (timing && mine(j)) ++res.n_updates_timed;
-                    if (!DRY && mine(j)) {
+                    const bool join = grouping && mine(j) && pl.size() == 1 && stages[static_cast<size_t>(j)].lam_d &&
+                                      (cur - pl[0].read + 2) <= fb200::kGroupChainMax;
+                    if (join) {
+                        PGroup& g = groups[static_cast<size_t>(j)];
+                        const long long rd = pl[0].read;
+                        if (!g.members.empty()) {
+                            const long long span = (g.cur0 - std::min(g.oldest, rd) + 1) +
+                                                   static_cast<long long>(g.members.size()) + 1;
+                            if (static_cast<int>(g.members.size()) >= fb200::kGroupMax || span > fb200::kGroupChainMax)
+                                flush_group(j);
+                        }
+                        if (g.members.empty()) {
+                            g.cur0 = cur;
+                            g.oldest = rd;
+                        } else if (cur != g.cur0 + static_cast<long long>(g.members.size()) || rd > g.cur0) {
+                            fail(FERRET_E_LOGIC, "update group: a stage version advanced outside its pending group");
+                        }
+                        g.oldest = std::min(g.oldest, rd);
+                        g.members.push_back(pl[0]);
+                        g.stash_of.push_back(stash(pl[0].u));
+                        g.x0_of.push_back(xrows(pl[0].u));
+                        add_keys(g.reads, {ustash(pl[0].u), ngroup(pl[0].u)});
+                        for (long long v = rd; v <= g.cur0; ++v) g.reads.push_back(vslot(j, v));
+                        add_keys(g.writes, {vslot(j, cur + 1), GB::key(GB::kState, static_cast<uint64_t>(j))});
+                        tidy(g.reads);
+                        tidy(g.writes);
+                    }
+                    if (!DRY && mine(j) && !join) {
                         fb200::UpdArgs a = update_args(j, cur, oldest);
                         a.policy = opt.policy;
                         a.K = static_cast<int>(pl.size());
@@ -1514,6 +1665,7 @@ struct ferret_trainer {
                         slot_of[fu] = -1;
                     }
         }
+        for (int q = 0; q < P; ++q) flush_group(q);
         if (!DRY) {
             // leave every stage's live version in slot 0 for the next chunk
             for (int j = 0; j < P; ++j) {
@@ -2543,6 +2695,24 @@ struct ferret_trainer {
     // Algorithmic bytes of one update launch: every parameter element reads the
     // versions it needs + its compensator state and writes the new version +
     // state; plus the deltas and layer inputs of each pending gradient.
+    // FERRET_UPDATE_GROUPS=0 (A/B knob, same results): every update is its own node
+    bool group_updates = !std::getenv("FERRET_UPDATE_GROUPS") || std::atoi(std::getenv("FERRET_UPDATE_GROUPS")) != 0;
+    size_t n_group_nodes = 0;
+    // algorithmic HBM bytes of one update group of stage j: the n0 chain versions read once,
+    // lambda / v_r / v_a read and written once, G new versions written (+ their bf16 copies),
+    // plus every member's unit activations and deltas
+    double group_bytes(int j, int n0, int G) const {
+        const StageDev& s = stages[static_cast<size_t>(j)];
+        const double state = s.v_r ? 24.0 : 8.0;
+        const double per = 4.0 * n0 + state + (4.0 + (s.ring16 ? 2.0 : 0.0)) * G;
+        double side = 0.0;
+        for (int l = s.lo; l < s.hi; ++l) {
+            const LayerDev& ld = layers[static_cast<size_t>(l)];
+            side += ld.conv() ? 4.0 * static_cast<double>(ld.nw() + ld.rows) : 4.0 * B * (ld.cols + ld.rows);
+        }
+        return per * static_cast<double>(s.n_params) + side * G;
+    }
+
     double update_bytes(int j, int policy, const std::vector<long long>& reads, long long cur) const {
         const StageDev& s = stages[static_cast<size_t>(j)];
         long long lo = cur;
