@@ -445,6 +445,32 @@ struct ElemState {
     float ld, vr, va, gp;
 };
 
+// ---------------------------------------------------------------------------
+// iter_fisher arithmetic (compensate.hpp:82-104) with every rounding spelled out (explicit
+// fma / mul / add, no compiler-chosen contraction), shared by every update kernel — single,
+// tiled, float4, smem-streamed and grouped — so they all produce the same bits.
+// ---------------------------------------------------------------------------
+// the lambda / v_r / v_a step (compensate.hpp:87-95); d0 = theta_1 - theta_0; returns lambda
+__device__ __forceinline__ float iter_learn(float g, float d0, float& ld, float& vr, float& va, float lam_base,
+                                            float alpha, float eta, float nu) {
+    const float one_m_a = __fsub_rn(1.f, alpha);
+    float lam = __fadd_rn(lam_base, ld);
+    const float dv = __fmul_rn(one_m_a, __fsub_rn(g, vr));
+    const float resid = __fmaf_rn(-lam, va, dv);
+    const float grad_l = __fmaf_rn(__fmul_rn(-2.f, resid), va, __fmul_rn(__fmul_rn(2.f, nu), lam));
+    ld = __fmaf_rn(-eta, grad_l, ld);
+    lam = __fadd_rn(lam_base, ld);
+    vr = __fmaf_rn(alpha, vr, __fmul_rn(one_m_a, g));
+    va = __fmaf_rn(alpha, va, __fmul_rn(__fmul_rn(__fmul_rn(one_m_a, g), g), d0));
+    return lam;
+}
+// one step of the fold: out += lambda * out^2 * (theta_{s+1} - theta_s)   compensate.hpp:99-102
+__device__ __forceinline__ float iter_fold(float o, float lam, float d) {
+    return __fmaf_rn(__fmul_rn(__fmul_rn(lam, o), o), d, o);
+}
+// theta_new = theta_cur - step * out   learner.hpp:497-502
+__device__ __forceinline__ float sgd_new(float cur, float step, float o) { return __fmaf_rn(-step, o, cur); }
+
 template <int POLICY>
 __device__ __forceinline__ float compensate_elem(float g, const float* const* vers, int first, int last, size_t e,
                                                  float th_cur, ElemState& st, float lam_base, float alpha,
@@ -468,21 +494,13 @@ __device__ __forceinline__ float compensate_elem(float g, const float* const* ve
         float lam = lam_base + st.ld;
         float prev = tau >= 1 ? __ldg(vers[first] + e) : th_cur;
         if (learn && tau >= 1) {
-            const float one_m_a = 1.f - alpha;
-            const float dv = one_m_a * (g - st.vr);
-            const float resid = dv - lam * st.va;
-            const float grad_l = -2.f * resid * st.va + 2.f * nu * lam;
-            st.ld -= eta * grad_l;
-            lam = lam_base + st.ld;
             const float nxt = tau == 1 ? th_cur : __ldg(vers[first + 1] + e);
-            const float d0 = nxt - prev;
-            st.vr = alpha * st.vr + one_m_a * g;
-            st.va = alpha * st.va + one_m_a * g * g * d0;
+            lam = iter_learn(g, nxt - prev, st.ld, st.vr, st.va, lam_base, alpha, eta, nu);
         }
         float o = g;
         for (int s = first; s < last; ++s) {
             const float nxt = (s + 1 == last) ? th_cur : __ldg(vers[s + 1] + e);
-            o += lam * o * o * (nxt - prev);
+            o = iter_fold(o, lam, nxt - prev);
             prev = nxt;
         }
         return o;
@@ -513,21 +531,14 @@ __device__ __forceinline__ float fold_iter_cached(float g, const float (&cv)[kRe
                 v0 = cv[i][v];
                 v1 = (i + 1 < last) ? cv[i + 1][v] : th;
             }
-        const float one_m_a = 1.f - alpha;
-        const float dv = one_m_a * (g - st.vr);
-        const float resid = dv - lam * st.va;
-        const float grad_l = -2.f * resid * st.va + 2.f * nu * lam;
-        st.ld -= eta * grad_l;
-        lam = lam_base + st.ld;
-        st.vr = alpha * st.vr + one_m_a * g;
-        st.va = alpha * st.va + one_m_a * g * g * (v1 - v0);
+        lam = iter_learn(g, v1 - v0, st.ld, st.vr, st.va, lam_base, alpha, eta, nu);
     }
     float o = g;
 #pragma unroll
     for (int i = 0; i < kRegChain; ++i)
         if (i >= first && i < last) {
             const float nxt = (i + 1 < last) ? cv[i + 1][v] : th;
-            o += lam * o * o * (nxt - cv[i][v]);
+            o = iter_fold(o, lam, nxt - cv[i][v]);
         }
     return o;
 }
@@ -604,7 +615,7 @@ __global__ void __launch_bounds__(kThreads) update_tile_kernel(const UpdArgs a) 
                 mean += compensate_elem<POLICY>(g, a.vers, a.pend[k].first, last, e, th, st, a.lambda0, a.alpha, a.eta,
                                                 a.nu, learn);
         }
-        const float nv = th - a.step * mean;
+        const float nv = sgd_new(th, a.step, mean);
         a.dst[e] = nv;
         if (a.dst16) reinterpret_cast<__nv_bfloat16*>(a.dst16)[e] = __float2bfloat16_rn(nv);
         if (POLICY == 4) {
@@ -645,26 +656,19 @@ __global__ void __launch_bounds__(kThreads) update_iter1_kernel(const UpdArgs a)
     const int B = a.B, R = w.nrows, tid = threadIdx.x;
     const bool learn = a.eta > 0.f && a.v_r != nullptr;
     const UpdPending& pk = a.pend[0];
-    const float one_m_a = 1.f - a.alpha;
     // the fold of one element (compensate.hpp:87-102) from values in registers
     auto fold = [&](size_t e, float g, const float (&cv)[NV], float ld, float vr, float va) {
         float lam = a.lambda0 + ld;
         if (NV >= 2 && learn) {
-            const float dv = one_m_a * (g - vr);
-            const float resid = dv - lam * va;
-            const float grad_l = -2.f * resid * va + 2.f * a.nu * lam;
-            ld -= a.eta * grad_l;
-            lam = a.lambda0 + ld;
-            vr = a.alpha * vr + one_m_a * g;
-            va = a.alpha * va + one_m_a * g * g * (cv[NV >= 2 ? 1 : 0] - cv[0]);
+            lam = iter_learn(g, cv[NV >= 2 ? 1 : 0] - cv[0], ld, vr, va, a.lambda0, a.alpha, a.eta, a.nu);
             a.v_r[e] = vr;
             a.v_a[e] = va;
             a.lam_d[e] = ld;
         }
         float o = g;
 #pragma unroll
-        for (int s = 0; s + 1 < NV; ++s) o += lam * o * o * (cv[s + 1] - cv[s]);
-        const float nv = cv[NV - 1] - a.step * o;
+        for (int s = 0; s + 1 < NV; ++s) o = iter_fold(o, lam, cv[s + 1] - cv[s]);
+        const float nv = sgd_new(cv[NV - 1], a.step, o);
         a.dst[e] = nv;
         if (a.dst16) reinterpret_cast<__nv_bfloat16*>(a.dst16)[e] = __float2bfloat16_rn(nv);
     };
@@ -775,22 +779,15 @@ __global__ void __launch_bounds__(kThreads) update_iter1v4_kernel(const UpdArgs 
     const int B = a.B, R = w.nrows, tid = threadIdx.x;
     const bool learn = a.eta > 0.f && a.v_r != nullptr;
     const UpdPending& pk = a.pend[0];
-    const float one_m_a = 1.f - a.alpha;
     auto fold1 = [&](float g, const float* cv, float& ld, float& vr, float& va) {  // one element
         float lam = a.lambda0 + ld;
         if (NV >= 2 && learn) {
-            const float dv = one_m_a * (g - vr);
-            const float resid = dv - lam * va;
-            const float grad_l = -2.f * resid * va + 2.f * a.nu * lam;
-            ld -= a.eta * grad_l;
-            lam = a.lambda0 + ld;
-            vr = a.alpha * vr + one_m_a * g;
-            va = a.alpha * va + one_m_a * g * g * (cv[NV >= 2 ? 1 : 0] - cv[0]);
+            lam = iter_learn(g, cv[NV >= 2 ? 1 : 0] - cv[0], ld, vr, va, a.lambda0, a.alpha, a.eta, a.nu);
         }
         float o = g;
 #pragma unroll
-        for (int s = 0; s + 1 < NV; ++s) o += lam * o * o * (cv[s + 1] - cv[s]);
-        return cv[NV - 1] - a.step * o;
+        for (int s = 0; s + 1 < NV; ++s) o = iter_fold(o, lam, cv[s + 1] - cv[s]);
+        return sgd_new(cv[NV - 1], a.step, o);
     };
     if (w.bias) {  // one element per thread
         if (tid >= R) return;
@@ -924,18 +921,11 @@ __global__ void __launch_bounds__(kThreads) update_stream_kernel(const UpdArgs a
     const int B = a.B, R = t.nrows, tid = threadIdx.x, nv = a.nv;
     const bool learn = a.eta > 0.f && a.v_r != nullptr;
     const UpdPending& pk = a.pend[0];
-    const float one_m_a = 1.f - a.alpha;
     // fold of one element given accessors for chain version i and the state
     auto fold = [&](size_t e, float g, auto ver, float ld, float vr, float va) {
         float lam = a.lambda0 + ld;
         if (nv >= 2 && learn) {  // compensate.hpp:87-98
-            const float dv = one_m_a * (g - vr);
-            const float resid = dv - lam * va;
-            const float grad_l = -2.f * resid * va + 2.f * a.nu * lam;
-            ld -= a.eta * grad_l;
-            lam = a.lambda0 + ld;
-            vr = a.alpha * vr + one_m_a * g;
-            va = a.alpha * va + one_m_a * g * g * (ver(1) - ver(0));
+            lam = iter_learn(g, ver(1) - ver(0), ld, vr, va, a.lambda0, a.alpha, a.eta, a.nu);
             a.v_r[e] = vr;
             a.v_a[e] = va;
             a.lam_d[e] = ld;
@@ -944,10 +934,10 @@ __global__ void __launch_bounds__(kThreads) update_stream_kernel(const UpdArgs a
         float prev = ver(0);
         for (int s = 1; s < nv; ++s) {
             const float nxt = ver(s);
-            o += lam * o * o * (nxt - prev);
+            o = iter_fold(o, lam, nxt - prev);
             prev = nxt;
         }
-        const float nvv = prev - a.step * o;
+        const float nvv = sgd_new(prev, a.step, o);
         a.dst[e] = nvv;
         if (a.dst16) reinterpret_cast<__nv_bfloat16*>(a.dst16)[e] = __float2bfloat16_rn(nvv);
     };
@@ -1107,7 +1097,6 @@ __global__ void __launch_bounds__(kThreads, 1) update_group_kernel(const GroupAr
         vr[i] = a.learn ? a.v_r[e[i]] : 0.f;
         va[i] = a.learn ? a.v_a[e[i]] : 0.f;
     }
-    const float one_m_a = 1.f - a.alpha;
     int n = a.n0;  // chain length so far (versions 0 .. n-1; cur = version n-1)
     for (int k = 0; k < G; ++k) {
         const UpdPending& pk = a.pend[k];
@@ -1149,13 +1138,7 @@ __global__ void __launch_bounds__(kThreads, 1) update_group_kernel(const GroupAr
 #pragma unroll
                 for (int s = 0; s < CM; ++s)
                     if (s == first) d0 = d[i][s];
-                const float dv = one_m_a * (gi - vr[i]);
-                const float resid = dv - l * va[i];
-                const float grad_l = -2.f * resid * va[i] + 2.f * a.nu * l;
-                ld[i] -= a.eta * grad_l;
-                l = a.lambda0 + ld[i];
-                vr[i] = a.alpha * vr[i] + one_m_a * gi;
-                va[i] = a.alpha * va[i] + one_m_a * gi * gi * d0;
+                l = iter_learn(gi, d0, ld[i], vr[i], va[i], a.lambda0, a.alpha, a.eta, a.nu);
             }
             lam[i] = l;
             o[i] = gi;
@@ -1167,14 +1150,14 @@ __global__ void __launch_bounds__(kThreads, 1) update_group_kernel(const GroupAr
             if (s >= first) {
 #pragma unroll
                 for (int i = 0; i < kGroupRows; ++i)
-                    if (i < R) o[i] += lam[i] * o[i] * o[i] * d[i][s];
+                    if (i < R) o[i] = iter_fold(o[i], lam[i], d[i][s]);
             }
         }
         // theta_new = theta_cur - lr * out (learner.hpp:497-502); append its difference
 #pragma unroll
         for (int i = 0; i < kGroupRows; ++i) {
             if (i >= R) break;
-            const float nv = cur[i] - a.step * o[i];
+            const float nv = sgd_new(cur[i], a.step, o[i]);
 #pragma unroll
             for (int s = 0; s < CM; ++s)
                 if (s == n - 1) d[i][s] = nv - cur[i];

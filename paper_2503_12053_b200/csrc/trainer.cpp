@@ -224,7 +224,10 @@ struct ChunkPlan {
 // concurrently, which is the pipeline parallelism of the 1F1B schedule
 // realised on one GPU. `serial` chains every node instead (timing mode).
 struct GraphBuilder {
-    enum : uint64_t { kVSlot = 1, kState, kStash, kPred, kNorm, kNormState, kPool, kReplay, kNormScratch, kWt };
+    // kAct / kDlt: one unit stash slot's activations / deltas of one stage's layers
+    // (key(kind, slot, stage)): a stage's update reads its own deltas and activations while
+    // the backward of the stage below writes only that stage's deltas
+    enum : uint64_t { kVSlot = 1, kState, kStash, kPred, kNorm, kNormState, kPool, kReplay, kNormScratch, kWt, kAct, kDlt };
     static uint64_t key(uint64_t kind, uint64_t a, uint64_t b = 0) { return (kind << 56) | (a << 32) | b; }
 
     cudaGraph_t g = nullptr;
@@ -1362,8 +1365,17 @@ struct ferret_trainer {
         auto vslot = [&](int j, long long v) {  // resource key of the ring slot holding version v of stage j
             return GB::key(GB::kVSlot, static_cast<uint64_t>(j), static_cast<uint64_t>(v % stages[static_cast<size_t>(j)].depth));
         };
-        auto ustash = [&](size_t u) { return GB::key(GB::kStash, static_cast<uint64_t>(slot_of[u])); };
+        // a unit's stash regions: activations / deltas of stage r's layers
+        auto uact = [&](size_t u, int r) {
+            return GB::key(GB::kAct, static_cast<uint64_t>(slot_of[u]), static_cast<uint64_t>(r));
+        };
+        auto udlt = [&](size_t u, int r) {
+            return GB::key(GB::kDlt, static_cast<uint64_t>(slot_of[u]), static_cast<uint64_t>(r));
+        };
         auto ngroup = [&](size_t u) { return GB::key(GB::kNorm, u / kNormGroup); };
+        // what stage j's work on unit u reads of the stage below: its output activation, or
+        // the unit's normalised rows for stage 0
+        auto uin = [&](size_t u, int j) { return j > 0 ? uact(u, j - 1) : ngroup(u); };
 
         // Cross-rank hand-off: every rank numbers every message identically (same
         // log, same pass), so the sender knows where the receiver's inbox slot and
@@ -1543,12 +1555,15 @@ struct ferret_trainer {
                     if (sched.has_bwd[u * static_cast<size_t>(P) + static_cast<size_t>(j)]) live[static_cast<size_t>(j)][v] += 1;
                     if (!DRY && mine(j))
                         launch_stage_forward(j, stages[static_cast<size_t>(j)].slot(v), stash(u), xrows(u),
-                                             {vslot(j, v), ngroup(u)}, ustash(u), d_labc + u * static_cast<size_t>(B));
+                                             {vslot(j, v), ngroup(u), uin(u, j)},
+                                             j == P - 1 ? std::vector<uint64_t>{uact(u, j), udlt(u, j)}
+                                                        : std::vector<uint64_t>{uact(u, j)},
+                                             d_labc + u * static_cast<size_t>(B));
                     if (j + 1 < P) {  // hand the stage output to the next stage's rank
                         const LayerDev& top = layers[static_cast<size_t>(stages[static_cast<size_t>(j)].hi - 1)];
                         const long long off = top.act_off;
                         xfer(owner[static_cast<size_t>(j)], owner[static_cast<size_t>(j + 1)], [&] { return stash(u) + off; },
-                             [&] { return stash(u) + off; }, static_cast<size_t>(B) * top.out, nullptr, ustash(u));
+                             [&] { return stash(u) + off; }, static_cast<size_t>(B) * top.out, nullptr, uact(u, j));
                     }
                     break;
                 }
@@ -1561,15 +1576,18 @@ struct ferret_trainer {
                     const bool cross = j > 0 && owner[static_cast<size_t>(j - 1)] != owner[static_cast<size_t>(j)];
                     if (!DRY && mine(j))
                         launch_stage_backward(j, stages[static_cast<size_t>(j)].slot(r), stash(u),
-                                              d_labc + u * static_cast<size_t>(B), slot_of[u], {vslot(j, r), ngroup(u)},
-                                              ustash(u), cross, xrows(u));
+                                              d_labc + u * static_cast<size_t>(B), slot_of[u],
+                                              {vslot(j, r), ngroup(u), uin(u, j), uact(u, j)},
+                                              j > 0 ? std::vector<uint64_t>{udlt(u, j), udlt(u, j - 1)}
+                                                    : std::vector<uint64_t>{udlt(u, j)},
+                                              cross, xrows(u));
                     if (cross && sched.has_bwd[u * static_cast<size_t>(P) + static_cast<size_t>(j - 1)]) {
                         const LayerDev& below = layers[static_cast<size_t>(stages[static_cast<size_t>(j)].lo - 1)];
                         const long long doff = below.dlt_off, aoff = below.act_off;
                         const bool relu = below.act == FERRET_ACT_RELU;
                         xfer(owner[static_cast<size_t>(j)], owner[static_cast<size_t>(j - 1)], [&] { return stash(u) + doff; },
                              [&] { return stash(u) + doff; }, static_cast<size_t>(B) * below.out,
-                             relu ? stash(u) + aoff : nullptr, ustash(u));
+                             relu ? stash(u) + aoff : nullptr, udlt(u, j - 1));
                     }
                     pending[{e.worker, j}].push_back({u, r});
                     break;
@@ -1612,7 +1630,7 @@ struct ferret_trainer {
                         g.members.push_back(pl[0]);
                         g.stash_of.push_back(stash(pl[0].u));
                         g.x0_of.push_back(xrows(pl[0].u));
-                        add_keys(g.reads, {ustash(pl[0].u), ngroup(pl[0].u)});
+                        add_keys(g.reads, {uin(pl[0].u, j), uact(pl[0].u, j), udlt(pl[0].u, j), ngroup(pl[0].u)});
                         for (long long v = rd; v <= g.cur0; ++v) g.reads.push_back(vslot(j, v));
                         add_keys(g.writes, {vslot(j, cur + 1), GB::key(GB::kState, static_cast<uint64_t>(j))});
                         tidy(g.reads);
@@ -1627,7 +1645,9 @@ struct ferret_trainer {
                         for (size_t k = 0; k < pl.size(); ++k) {
                             a.pend[k] = {stash(pl[k].u), xrows(pl[k].u), static_cast<int>(pl[k].read - oldest)};
                             reads.push_back(pl[k].read);
-                            rk.push_back(ustash(pl[k].u));
+                            rk.push_back(uin(pl[k].u, j));
+                            rk.push_back(uact(pl[k].u, j));
+                            rk.push_back(udlt(pl[k].u, j));
                             rk.push_back(ngroup(pl[k].u));
                         }
                         for (long long v = oldest; v <= cur; ++v) rk.push_back(vslot(j, v));
@@ -1955,17 +1975,17 @@ struct ferret_trainer {
     }
     // the weight and bias gradient of convolution `ld` into its stash region
     void emit_conv_wgrad(const LayerDev& ld, float* stash_u, const float* X, const int* xidx,
-                         const std::vector<uint64_t>& reads, uint64_t stash_key) {
+                         const std::vector<uint64_t>& reads, const std::vector<uint64_t>& writes) {
         fb200::ConvArgs c = conv_args(ld);
         c.X = X;
         c.xidx = xidx;
         c.D = stash_u + ld.dlt_off;
         c.Y = stash_u + ld.g_off;
-        emit_conv(c, fb200::kConvWgrad, reads, {stash_key}, 4.0 * ld.nw() + 4.0 * B * (ld.in + ld.out));
+        emit_conv(c, fb200::kConvWgrad, reads, writes, 4.0 * ld.nw() + 4.0 * B * (ld.in + ld.out));
         fb200::KernelSpec kb;
         fb200::spec_conv_bgrad(c, stash_u + ld.g_off + ld.nw(), kb);
         gb->cur_bytes = 4.0 * B * ld.out + 4.0 * ld.rows;
-        gb->kernel(kb, reads, {stash_key});
+        gb->kernel(kb, reads, writes);
     }
 
     // predict_class(net_, x) at the arrival (learner.hpp:398-399): full net at
@@ -2020,7 +2040,7 @@ struct ferret_trainer {
     }
 
     void launch_stage_forward(int j, const float* slot, float* stash_u, const float* x0, const std::vector<uint64_t>& reads,
-                              uint64_t stash_key, const int* lab) {
+                              const std::vector<uint64_t>& writes, const int* lab) {
         gb->cur_category = kCatForward;
         gb->cur_stage = j;
         const StageDev& s = stages[static_cast<size_t>(j)];
@@ -2036,7 +2056,7 @@ struct ferret_trainer {
                 h.delta = stash_u + ld.dlt_off;
                 h.scale = 1.0f / static_cast<float>(B);
             }
-            emit_layer(ld, slot, X, nullptr, stash_u + ld.act_off, reads, {stash_key}, h,
+            emit_layer(ld, slot, X, nullptr, stash_u + ld.act_off, reads, writes, h,
                        ld.res ? stash_u + layers[static_cast<size_t>(l - 2)].act_off : nullptr,
                        ld.gap() ? stash_u + ld.pool_off : nullptr);
         }
@@ -2046,24 +2066,24 @@ struct ferret_trainer {
     // ReLU mask of the layer below applied on write (learner.hpp:443-476);
     // `cross`: the stage below is on another rank, which applies the mask.
     void launch_stage_backward(int j, const float* slot, float* stash_u, const int* lab, int scratch,
-                               const std::vector<uint64_t>& reads, uint64_t stash_key, bool cross,
+                               const std::vector<uint64_t>& reads, const std::vector<uint64_t>& writes, bool cross,
                                const float* x0 = nullptr, const int* x0idx = nullptr) {
         gb->cur_category = kCatBackward;
         gb->cur_stage = j;
         const StageDev& s = stages[static_cast<size_t>(j)];
-        if (j == P - 1 && !can_fuse_head()) emit_delta_head(stash_u, lab, nullptr, 1.0f / static_cast<float>(B), {}, stash_key);
+        if (j == P - 1 && !can_fuse_head()) emit_delta_head(stash_u, lab, nullptr, 1.0f / static_cast<float>(B), reads, writes);
         for (int l = s.hi - 1; l >= s.lo; --l) {
             const LayerDev& ld = layers[static_cast<size_t>(l)];
             if (ld.conv())  // a convolution's weight gradient is materialised for the update
                 emit_conv_wgrad(ld, stash_u, l == 0 ? x0 : stash_u + layers[static_cast<size_t>(l - 1)].act_off,
-                                l == 0 ? x0idx : nullptr, reads, stash_key);
+                                l == 0 ? x0idx : nullptr, reads, writes);
             if (l == 0) break;  // no input gradient for the first layer
-            emit_layer_backward(l, slot, stash_u, scratch, reads, stash_key, !(cross && l == s.lo));
+            emit_layer_backward(l, slot, stash_u, scratch, reads, writes, !(cross && l == s.lo));
         }
     }
 
     void emit_delta_head(float* stash_u, const int* lab, const int* lidx, float scale, const std::vector<uint64_t>& reads,
-                         uint64_t stash_key) {
+                         const std::vector<uint64_t>& writes) {
         const LayerDev& last = layers.back();
         fb200::HeadArgs h{};
         h.logits = stash_u + last.act_off;
@@ -2077,11 +2097,11 @@ struct ferret_trainer {
         fb200::KernelSpec k;
         fb200::spec_head(h, k);
         gb->cur_bytes = 8.0 * B * n_out;
-        gb->kernel(k, reads, {stash_key});
+        gb->kernel(k, reads, writes);
     }
 
     void emit_layer_backward(int l, const float* slot, float* stash_u, int scratch, const std::vector<uint64_t>& reads,
-                             uint64_t stash_key, bool mask_on_write = true) {
+                             const std::vector<uint64_t>& writes, bool mask_on_write = true) {
         const LayerDev& ld = layers[static_cast<size_t>(l)];
         const LayerDev& below = layers[static_cast<size_t>(l - 1)];
         const float* mask = mask_on_write && below.act == FERRET_ACT_RELU ? stash_u + below.act_off : nullptr;
@@ -2098,7 +2118,7 @@ struct ferret_trainer {
                 c.rh = r.ho;
                 c.rw = r.wo;
             }
-            return emit_conv(c, fb200::kConvDgrad, reads, {stash_key},
+            return emit_conv(c, fb200::kConvDgrad, reads, writes,
                              4.0 * ld.nw() + 4.0 * B * (ld.out + 2.0 * ld.in));
         }
         if (ld.gap()) {  // W^T delta into the pooled delta, then spread over the pixels (/HW, ReLU mask)
@@ -2115,19 +2135,19 @@ struct ferret_trainer {
             fb200::KernelSpec k;
             fb200::spec_bwd(a, k);
             gb->cur_bytes = 4.0 * ld.nw() + 4.0 * B * (ld.rows + ld.cols);
-            gb->kernel(k, reads, {stash_key});
+            gb->kernel(k, reads, writes);
             fb200::PoolMeanArgs g{nullptr, nullptr, nullptr, stash_u + below.dlt_off, stash_u + ld.pdl_off, mask,
                                   B, ld.ci, ld.hi * ld.wi};
             fb200::KernelSpec ku;
             fb200::spec_ungap(g, ku);
             gb->cur_bytes = 4.0 * B * (ld.ci + 2.0 * ld.in);
-            gb->kernel(ku, reads, {stash_key});
+            gb->kernel(ku, reads, writes);
             return;
         }
         if (use_mma(ld))
             return emit_mma(ld, slot, true, stash_u + ld.dlt_off,  nullptr,
                             mask_on_write && below.act == FERRET_ACT_RELU ? stash_u + below.act_off : nullptr,
-                            stash_u + below.dlt_off, reads, {stash_key});
+                            stash_u + below.dlt_off, reads, writes);
         fb200::BwdArgs a{};
         a.W = slot + ld.woff;
         a.d_out = stash_u + ld.dlt_off;
@@ -2142,7 +2162,7 @@ struct ferret_trainer {
         fb200::KernelSpec k;
         fb200::spec_bwd(a, k);
         gb->cur_bytes = 4.0 * ld.in * ld.out + 4.0 * B * (ld.out + 2.0 * ld.in);  // W, delta_out, mask, delta_in
-        gb->kernel(k, reads, {stash_key});
+        gb->kernel(k, reads, writes);
     }
 
     // ------------------------------------------------ exact resume
@@ -2426,8 +2446,8 @@ struct ferret_trainer {
             const float* X = l == 0 ? sq.d_ux : su + layers[static_cast<size_t>(l - 1)].act_off;
             emit_layer(ld, s.slot(read), X, nullptr, su + ld.act_off, {}, {GB::key(GB::kStash, 0)});
         }
-        emit_delta_head(su, sq.d_lab + 2 * i, nullptr, 1.0f / static_cast<float>(rows), {}, GB::key(GB::kStash, 0));
-        for (int l = L - 1; l >= 1; --l) emit_layer_backward(l, s.slot(read), su, 0, {}, GB::key(GB::kStash, 0), true);
+        emit_delta_head(su, sq.d_lab + 2 * i, nullptr, 1.0f / static_cast<float>(rows), {}, {GB::key(GB::kStash, 0)});
+        for (int l = L - 1; l >= 1; --l) emit_layer_backward(l, s.slot(read), su, 0, {}, {GB::key(GB::kStash, 0)}, true);
         fb200::UpdArgs a = update_args(0, sq.version, read);
         a.policy = policy;
         a.K = 1;
@@ -2632,7 +2652,7 @@ struct ferret_trainer {
         if (!DRY && mine(P - 1)) {
             gb->cur_category = kCatReplay;
             emit_delta_head(d_replay, ctl_rep_labels() + r * static_cast<size_t>(B), nullptr,
-                            1.0f / static_cast<float>(B), {}, rk);
+                            1.0f / static_cast<float>(B), {}, {rk});
         }
         for (int j = P - 1; j >= 0; --j) {  // backward sweep
             const StageDev& s = stages[static_cast<size_t>(j)];
@@ -2643,10 +2663,10 @@ struct ferret_trainer {
                     const LayerDev& ld = layers[static_cast<size_t>(l)];
                     if (ld.conv())
                         emit_conv_wgrad(ld, d_replay, l == 0 ? d_pool_x : d_replay + layers[static_cast<size_t>(l - 1)].act_off,
-                                        l == 0 ? ids : nullptr, {vslot(j, rel[static_cast<size_t>(j)]), pk}, rk);
+                                        l == 0 ? ids : nullptr, {vslot(j, rel[static_cast<size_t>(j)]), pk}, {rk});
                     if (l == 0) break;
                     emit_layer_backward(l, s.slot(rel[static_cast<size_t>(j)]), d_replay, stash_slots,
-                                        {vslot(j, rel[static_cast<size_t>(j)])}, rk, !(cross && l == s.lo));
+                                        {vslot(j, rel[static_cast<size_t>(j)])}, {rk}, !(cross && l == s.lo));
                 }
             }
             if (cross) {
