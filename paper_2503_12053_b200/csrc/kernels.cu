@@ -1053,27 +1053,62 @@ __global__ void __launch_bounds__(kThreads) update_stream_kernel(const UpdArgs a
 // recomputes from the stored versions) plus the live value; update k folds over
 // d[first_k .. n-2], writes version n and appends its difference. The unit deltas of every
 // update and tile row are staged in smem once; the unit inputs x_k[b][c] of the thread's
-// column are loaded per update (L2-resident activations) and reused across the rows.
+// column are prefetched kGroupXBuf updates ahead with cp.async into a per-thread smem ring
+// (each thread copies and reads only its own column: no barrier), so the L2 latency of the
+// activations overlaps the folds of the updates before.
 // CM = difference capacity (chain span - 1), BT = micro-batch bound.
 // ---------------------------------------------------------------------------
+constexpr int kGroupXBuf = 6;
+
+__device__ __forceinline__ void cp_async4(float* dst_smem, const float* src, bool valid) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst_smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(valid ? 4 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 template <int CM, int BT>
 __global__ void __launch_bounds__(kThreads, 1) update_group_kernel(const GroupArgs a) {
     __shared__ float sdel[kGroupMax * kMaxBatch * kGroupRows];
+    extern __shared__ float xs[];  // [kGroupXBuf][BT][kThreads]: the unit inputs, column tid per thread
     const UpdWork w = a.works[blockIdx.x];
     const int tid = threadIdx.x, B = a.B, G = a.G;
     const bool bias = w.bias != 0;
     const bool gm = w.g_off >= 0;  // materialised gradients (convolutions)
+    const bool use_x = !bias && !gm;
     const int R = bias ? 1 : w.nrows;
     const int c = w.c0 + tid;
     const bool live = bias ? tid < w.nrows : c < w.in;
-    if (!bias && !gm) {  // deltas of every update and tile row: sdel[(k * BT + b) * 4 + i]
+    // x_k[b][c] -> xs[k % kGroupXBuf][b][tid] (zero-filled past the micro-batch / the row end)
+    auto issue_x = [&](int k) {
+        if (use_x && k < G) {
+            const UpdPending& pk = a.pend[k];
+            float* dst = xs + (size_t)(k % kGroupXBuf) * BT * kThreads + tid;
+#pragma unroll
+            for (int b = 0; b < BT; ++b) {
+                const float* xr = w.xin_off >= 0 ? pk.stash + w.xin_off + (size_t)b * w.in
+                                  : a.x0idx      ? pk.x0 + (size_t)__ldg(a.x0idx + (b < B ? b : 0)) * a.x0_ld
+                                                 : pk.x0 + (size_t)b * a.x0_ld;
+                const bool ok = b < B && live;
+                cp_async4(dst + b * kThreads, ok ? xr + c : pk.x0 ? pk.x0 : pk.stash, ok);
+            }
+        }
+        cp_async_commit();  // (an empty group past the end keeps the wait count uniform)
+    };
+#pragma unroll
+    for (int k = 0; k < kGroupXBuf - 1; ++k) issue_x(k);
+    if (use_x) {  // deltas of every update and tile row: sdel[(k * BT + b) * 4 + i]
         for (int q = tid; q < G * BT * kGroupRows; q += kThreads) {
             const int i = q % kGroupRows, b = (q / kGroupRows) % BT, k = q / (kGroupRows * BT);
             sdel[q] = (b < B && i < R) ? __ldg(a.pend[k].stash + w.dlt_off + (size_t)b * w.out + w.r0 + i) : 0.f;
         }
     }
     __syncthreads();
-    if (!live) return;
+    if (!live) {
+        cp_async_wait<0>();
+        return;
+    }
     size_t e[kGroupRows];
 #pragma unroll
     for (int i = 0; i < kGroupRows; ++i)
@@ -1101,19 +1136,10 @@ __global__ void __launch_bounds__(kThreads, 1) update_group_kernel(const GroupAr
     for (int k = 0; k < G; ++k) {
         const UpdPending& pk = a.pend[k];
         const int first = pk.first;
-        // the unit's inputs of this column (weights) — reused by the tile's rows
-        float xv[BT];
-        if (!bias && !gm) {
-            const float* xr0 = w.xin_off >= 0 ? pk.stash + w.xin_off : nullptr;
-#pragma unroll
-            for (int b = 0; b < BT; ++b) {
-                const float* xr = xr0 ? xr0 + (size_t)b * w.in
-                                  : a.x0idx ? pk.x0 + (size_t)__ldg(a.x0idx + b) * a.x0_ld
-                                            : pk.x0 + (size_t)b * a.x0_ld;
-                xv[b] = b < B ? __ldg(xr + c) : 0.f;
-            }
-        }
-        float o[kGroupRows], g[kGroupRows], lam[kGroupRows];
+        issue_x(k + kGroupXBuf - 1);
+        cp_async_wait<kGroupXBuf - 1>();  // this thread's copies of update k have landed
+        const float* xk = xs + (size_t)(k % kGroupXBuf) * BT * kThreads + tid;
+        float o[kGroupRows], lam[kGroupRows];
 #pragma unroll
         for (int i = 0; i < kGroupRows; ++i) {
             if (i >= R) break;
@@ -1128,9 +1154,8 @@ __global__ void __launch_bounds__(kThreads, 1) update_group_kernel(const GroupAr
             } else {
 #pragma unroll
                 for (int b = 0; b < BT; ++b)
-                    if (b < B) gi = fmaf(sdel[(k * BT + b) * kGroupRows + i], xv[b], gi);
+                    if (b < B) gi = fmaf(sdel[(k * BT + b) * kGroupRows + i], xk[b * kThreads], gi);
             }
-            g[i] = gi;
             // iter_fisher state step (compensate.hpp:87-95) when the chain has >= 2 versions
             float l = a.lambda0 + ld[i];
             if (a.learn && n - first >= 2) {
@@ -1154,6 +1179,8 @@ __global__ void __launch_bounds__(kThreads, 1) update_group_kernel(const GroupAr
             }
         }
         // theta_new = theta_cur - lr * out (learner.hpp:497-502); append its difference
+        float* dk = a.dst[k];
+        unsigned short* dk16 = a.dst16[k];
 #pragma unroll
         for (int i = 0; i < kGroupRows; ++i) {
             if (i >= R) break;
@@ -1162,8 +1189,8 @@ __global__ void __launch_bounds__(kThreads, 1) update_group_kernel(const GroupAr
             for (int s = 0; s < CM; ++s)
                 if (s == n - 1) d[i][s] = nv - cur[i];
             cur[i] = nv;
-            a.dst[k][e[i]] = nv;
-            if (a.dst16[k]) reinterpret_cast<__nv_bfloat16*>(a.dst16[k])[e[i]] = __float2bfloat16_rn(nv);
+            dk[e[i]] = nv;
+            if (dk16) reinterpret_cast<__nv_bfloat16*>(dk16)[e[i]] = __float2bfloat16_rn(nv);
         }
         ++n;
     }
@@ -1179,12 +1206,25 @@ __global__ void __launch_bounds__(kThreads, 1) update_group_kernel(const GroupAr
 }
 
 template <int BT>
+constexpr size_t group_smem() { return sizeof(float) * (size_t)kGroupXBuf * BT * kThreads; }
+
+template <int CM, int BT>
+const void* group_fn() {
+    static const void* f = [] {
+        const void* p = reinterpret_cast<const void*>(&update_group_kernel<CM, BT>);
+        cudaFuncSetAttribute(p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)group_smem<BT>());
+        return p;
+    }();
+    return f;
+}
+
+template <int BT>
 const void* group_func(int span) {
-    if (span <= 8) return reinterpret_cast<const void*>(&update_group_kernel<7, BT>);
-    if (span <= 16) return reinterpret_cast<const void*>(&update_group_kernel<15, BT>);
-    if (span <= 24) return reinterpret_cast<const void*>(&update_group_kernel<23, BT>);
-    if (span <= 32) return reinterpret_cast<const void*>(&update_group_kernel<31, BT>);
-    return reinterpret_cast<const void*>(&update_group_kernel<kGroupChainMax - 1, BT>);
+    if (span <= 8) return group_fn<7, BT>();
+    if (span <= 16) return group_fn<15, BT>();
+    if (span <= 24) return group_fn<23, BT>();
+    if (span <= 32) return group_fn<31, BT>();
+    return group_fn<kGroupChainMax - 1, BT>();
 }
 
 template <int BT>
@@ -1494,6 +1534,8 @@ void spec_update_group(const GroupArgs& a, KernelSpec& k) {
     const void* f = a.B <= 1 ? group_func<1>(span) : a.B <= 2 ? group_func<2>(span) : a.B <= 4 ? group_func<4>(span)
                   : a.B <= 8 ? group_func<8>(span) : group_func<16>(span);
     fill(k, f, dim3((unsigned)a.n_tiles), dim3(kThreads), a);
+    k.smem = a.B <= 1 ? group_smem<1>() : a.B <= 2 ? group_smem<2>() : a.B <= 4 ? group_smem<4>()
+           : a.B <= 8 ? group_smem<8>() : group_smem<16>();
 }
 
 void spec_normalize(const NormArgs& a, KernelSpec& k) {
