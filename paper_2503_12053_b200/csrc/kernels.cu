@@ -1069,7 +1069,7 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 template <int CM, int BT>
-__global__ void __launch_bounds__(kThreads, 1) update_group_kernel(const GroupArgs a) {
+__global__ void __launch_bounds__(kThreads, CM <= 7 ? 2 : 1) update_group_kernel(const GroupArgs a) {
     __shared__ float sdel[kGroupMax * kMaxBatch * kGroupRows];
     extern __shared__ float xs[];  // [kGroupXBuf][BT][kThreads]: the unit inputs, column tid per thread
     const UpdWork w = a.works[blockIdx.x];
@@ -1077,7 +1077,7 @@ __global__ void __launch_bounds__(kThreads, 1) update_group_kernel(const GroupAr
     const bool bias = w.bias != 0;
     const bool gm = w.g_off >= 0;  // materialised gradients (convolutions)
     const bool use_x = !bias && !gm;
-    const int R = bias ? 1 : w.nrows;
+    const int R = bias ? 1 : w.nrows;  // rows i >= R of the thread are computed on a copy of row 0, never stored
     const int c = w.c0 + tid;
     const bool live = bias ? tid < w.nrows : c < w.in;
     // x_k[b][c] -> xs[k % kGroupXBuf][b][tid] (zero-filled past the micro-batch / the row end)
@@ -1117,7 +1117,6 @@ __global__ void __launch_bounds__(kThreads, 1) update_group_kernel(const GroupAr
     float d[kGroupRows][CM], cur[kGroupRows], ld[kGroupRows], vr[kGroupRows], va[kGroupRows];
 #pragma unroll
     for (int i = 0; i < kGroupRows; ++i) {
-        if (i >= R) break;
         float prev = __ldg(a.vers[0] + e[i]);
 #pragma unroll
         for (int s = 0; s < CM; ++s) {
@@ -1132,20 +1131,20 @@ __global__ void __launch_bounds__(kThreads, 1) update_group_kernel(const GroupAr
         vr[i] = a.learn ? a.v_r[e[i]] : 0.f;
         va[i] = a.learn ? a.v_a[e[i]] : 0.f;
     }
-    int n = a.n0;  // chain length so far (versions 0 .. n-1; cur = version n-1)
+    const bool learn = a.learn != 0;
+    int n = a.n0;  // chain length so far (versions 0 .. n-1; cur = version n-1); n - 1 < CM by the span check
     for (int k = 0; k < G; ++k) {
         const UpdPending& pk = a.pend[k];
         const int first = pk.first;
         issue_x(k + kGroupXBuf - 1);
         cp_async_wait<kGroupXBuf - 1>();  // this thread's copies of update k have landed
         const float* xk = xs + (size_t)(k % kGroupXBuf) * BT * kThreads + tid;
-        float o[kGroupRows], lam[kGroupRows];
+        float g[kGroupRows], o[kGroupRows], lam[kGroupRows];
 #pragma unroll
         for (int i = 0; i < kGroupRows; ++i) {
-            if (i >= R) break;
             float gi = 0.f;
             if (gm) {
-                gi = bias ? __ldg(pk.stash + w.g_off + w.r0 + tid) : __ldg(pk.stash + w.g_off + (size_t)(w.r0 + i) * w.in + c);
+                gi = bias ? __ldg(pk.stash + w.g_off + w.r0 + tid) : __ldg(pk.stash + w.g_off + (e[i] - (size_t)w.elem0));
             } else if (bias) {
                 const float* dl = pk.stash + w.dlt_off + w.r0 + tid;
 #pragma unroll
@@ -1156,41 +1155,38 @@ __global__ void __launch_bounds__(kThreads, 1) update_group_kernel(const GroupAr
                 for (int b = 0; b < BT; ++b)
                     if (b < B) gi = fmaf(sdel[(k * BT + b) * kGroupRows + i], xk[b * kThreads], gi);
             }
-            // iter_fisher state step (compensate.hpp:87-95) when the chain has >= 2 versions
-            float l = a.lambda0 + ld[i];
-            if (a.learn && n - first >= 2) {
-                float d0 = 0.f;
-#pragma unroll
-                for (int s = 0; s < CM; ++s)
-                    if (s == first) d0 = d[i][s];
-                l = iter_learn(gi, d0, ld[i], vr[i], va[i], a.lambda0, a.alpha, a.eta, a.nu);
-            }
-            lam[i] = l;
+            g[i] = gi;
             o[i] = gi;
+            lam[i] = a.lambda0 + ld[i];
         }
-        // the fold over the chain (compensate.hpp:97-102), rows interleaved
-#pragma unroll
-        for (int s = 0; s < CM; ++s) {
-            if (s >= n - 1) break;
-            if (s >= first) {
-#pragma unroll
-                for (int i = 0; i < kGroupRows; ++i)
-                    if (i < R) o[i] = iter_fold(o[i], lam[i], d[i][s]);
-            }
-        }
-        // theta_new = theta_cur - lr * out (learner.hpp:497-502); append its difference
         float* dk = a.dst[k];
         unsigned short* dk16 = a.dst16[k];
+        // one pass over the chain with static indices: the lambda / v_r / v_a step at the read
+        // version (compensate.hpp:87-95), the fold (:97-102), then at the live version the SGD
+        // step (learner.hpp:497-502) and the new version's difference appended
 #pragma unroll
-        for (int i = 0; i < kGroupRows; ++i) {
-            if (i >= R) break;
-            const float nv = sgd_new(cur[i], a.step, o[i]);
+        for (int s = 0; s < CM; ++s) {
+            if (s == n - 1) {
 #pragma unroll
-            for (int s = 0; s < CM; ++s)
-                if (s == n - 1) d[i][s] = nv - cur[i];
-            cur[i] = nv;
-            dk[e[i]] = nv;
-            if (dk16) reinterpret_cast<__nv_bfloat16*>(dk16)[e[i]] = __float2bfloat16_rn(nv);
+                for (int i = 0; i < kGroupRows; ++i) {
+                    const float nv = sgd_new(cur[i], a.step, o[i]);
+                    d[i][s] = nv - cur[i];
+                    cur[i] = nv;
+                    if (i < R) {
+                        dk[e[i]] = nv;
+                        if (dk16) reinterpret_cast<__nv_bfloat16*>(dk16)[e[i]] = __float2bfloat16_rn(nv);
+                    }
+                }
+            }
+            if (s >= first && s < n - 1) {
+                if (s == first && learn) {
+#pragma unroll
+                    for (int i = 0; i < kGroupRows; ++i)
+                        lam[i] = iter_learn(g[i], d[i][s], ld[i], vr[i], va[i], a.lambda0, a.alpha, a.eta, a.nu);
+                }
+#pragma unroll
+                for (int i = 0; i < kGroupRows; ++i) o[i] = iter_fold(o[i], lam[i], d[i][s]);
+            }
         }
         ++n;
     }
@@ -1198,7 +1194,7 @@ __global__ void __launch_bounds__(kThreads, 1) update_group_kernel(const GroupAr
     for (int i = 0; i < kGroupRows; ++i) {
         if (i >= R) break;
         a.lam_d[e[i]] = ld[i];
-        if (a.learn) {
+        if (learn) {
             a.v_r[e[i]] = vr[i];
             a.v_a[e[i]] = va[i];
         }
