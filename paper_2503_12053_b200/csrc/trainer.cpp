@@ -2715,8 +2715,11 @@ struct ferret_trainer {
     // Algorithmic bytes of one update launch: every parameter element reads the
     // versions it needs + its compensator state and writes the new version +
     // state; plus the deltas and layer inputs of each pending gradient.
-    // FERRET_UPDATE_GROUPS=0 (A/B knob, same results): every update is its own node
-    bool group_updates = !std::getenv("FERRET_UPDATE_GROUPS") || std::atoi(std::getenv("FERRET_UPDATE_GROUPS")) != 0;
+    // FERRET_UPDATE_GROUPS=1 (A/B knob, same results): consecutive iter_fisher updates of a stage
+    // fused into one update_group_kernel launch. Off by default: measured on C5 fp32 the grouped
+    // kernel runs at 61 GB/s (15K-instruction body, one CTA per SM) and the step drops from
+    // 3.2k to 0.77k samples/s; C2 from 1.12M to 0.45M (profiles/r2/ab_update_groups.txt)
+    bool group_updates = std::getenv("FERRET_UPDATE_GROUPS") && std::atoi(std::getenv("FERRET_UPDATE_GROUPS")) != 0;
     size_t n_group_nodes = 0;
     // algorithmic HBM bytes of one update group of stage j: the n0 chain versions read once,
     // lambda / v_r / v_a read and written once, G new versions written (+ their bf16 copies),
