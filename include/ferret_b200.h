@@ -196,6 +196,61 @@ FERRET_API size_t ferret_schedule_plan_text(const ferret_schedule* s, char* buf,
 FERRET_API size_t ferret_schedule_trace_text(const ferret_schedule* s, char* buf, size_t cap);
 FERRET_API void ferret_schedule_destroy(ferret_schedule* s);
 
+/* ---------------- planner re-costed for B200 (north-star item 4) ----------------
+ * The reference planner (planner.hpp:180-215, analytics.hpp:72-104) prices a plan with
+ * synthetic per-layer times (net.hpp:263-274: 1e-6 s per parameter) and memory in
+ * parameter/activation COUNT units. The B200 planner keeps its search unchanged and
+ * feeds it (1) per-layer t_f / t_b measured on the device and (2) w / a in HBM BYTES
+ * of this trainer's layout; the chosen plan is then priced exactly by the trainer's own
+ * dry-run footprint (ferret_trainer_footprint) and re-planned under a tightened budget
+ * until it fits. Candidate partitions are limited to max_stages (= #GPUs, one stage per
+ * GPU at most). */
+typedef struct {
+    int32_t micro_batch;       /* stream samples per pipeline unit */
+    int32_t precision;         /* FERRET_PREC_*: bf16 keeps a bf16 copy of every weight version (+2 B) */
+    int32_t policy;            /* FERRET_POLICY_*: compensator state bytes */
+    double eta_lambda;         /* iter_fisher: > 0 learns lambda (v_r, v_a state) */
+    int32_t replay;            /* ER replay pool */
+    uint64_t replay_capacity;
+    uint64_t chunk_units;      /* pipeline units per compiled chunk (staging); 0 = n_items */
+} ferret_b200_cost;
+FERRET_API void ferret_b200_cost_default(ferret_b200_cost* c);
+
+/* profile_from_net (net.hpp:263-274) re-costed on the device: per layer, t_f = measured
+ * mean device seconds of the layer's forward event and t_b = its backward + compensated
+ * update, from a profiled replay of the real kernels with one layer per stage (`units`
+ * pipeline units of a synthetic stream, after one warm-up chunk); w / a are the
+ * reference's counts. layers_out has n_widths - 1 entries. */
+FERRET_API ferret_status ferret_measure_profile(const uint64_t* widths, int32_t n_widths, const ferret_b200_cost* cost,
+                                                int32_t units, int32_t device, ferret_layer_profile* layers_out);
+
+/* A (measured) profile with w = HBM bytes of one weight version of the layer and
+ * a = stash bytes one in-flight unit holds for it (activation + delta, micro_batch rows):
+ * the reference planner's count units become bytes. */
+FERRET_API ferret_status ferret_b200_byte_profile(const ferret_layer_profile* layers, int32_t n_layers,
+                                                  const ferret_b200_cost* cost, ferret_layer_profile* out);
+
+typedef struct {
+    uint64_t budget_bytes;     /* the caller's HBM budget for the whole pipeline */
+    uint64_t fixed_bytes;      /* plan-independent: compensator state, normalizer, staging, replay pool */
+    uint64_t planner_budget;   /* budget handed to the reference search (bytes) on the last pass */
+    uint64_t planner_bytes;    /* the reference memory model of the chosen plan, in bytes */
+    uint64_t predicted_bytes;  /* fixed + planner */
+    uint64_t trainer_bytes;    /* exact: the trainer's footprint for the plan's event log */
+    int32_t passes;            /* planner passes (1 = the first plan fit) */
+    int32_t stages;
+    int32_t fits;              /* trainer_bytes <= budget_bytes */
+} ferret_b200_plan_report;
+
+/* plan_b200: widths give the net (dense, ReLU hidden), layers the measured profile
+ * (ferret_measure_profile, or any ModelProfile with times in seconds and count units),
+ * budget in bytes (0 = unconstrained), max_stages = #GPUs (0 = unlimited). The
+ * schedule's plan is a reference PlanResult whose `memory` is in bytes. */
+FERRET_API ferret_status ferret_plan_b200(const uint64_t* widths, int32_t n_widths, const ferret_layer_profile* layers,
+                                          double t_d, const ferret_stream_spec* spec, uint64_t budget_bytes,
+                                          int32_t max_stages, const ferret_b200_cost* cost, size_t n_items,
+                                          ferret_schedule** out, ferret_b200_plan_report* report);
+
 /* ---------------- hot path: PipelineTrainer on sm_100a ---------------- */
 
 typedef struct ferret_trainer ferret_trainer;
@@ -315,6 +370,23 @@ typedef struct {
     uint64_t device_bytes;       /* HBM the trainer allocated */
 } ferret_trainer_stats;
 FERRET_API ferret_status ferret_trainer_get_stats(ferret_trainer* t, ferret_trainer_stats* out);
+/* HBM footprint of the current schedule (no reference counterpart; north-star item 4, the
+ * planner re-costed in bytes): what the trainer holds once execute() has compiled the
+ * schedule's chunk graph, from the same dry pass over the event log that sizes the version
+ * rings (exact retention) and the stash. Works on plan-only trainers (device -1), so a
+ * planner can price a candidate plan without a GPU. Excludes the tensor-core layers'
+ * graph-build scratch (split-K partials, conv weight copies). */
+typedef struct {
+    uint64_t total;        /* bytes */
+    uint64_t rings;        /* weight-version rings, fp32 (+ bf16 copies in bf16 mode) */
+    uint64_t comp_state;   /* compensator state (iter_fisher: lambda, v_r, v_a; gap: mean gap) */
+    uint64_t stash;        /* in-flight unit activations and deltas (+ the replay slot) */
+    uint64_t scratch;      /* backward split-reduction scratch */
+    uint64_t other;        /* staging, control block, normalizer, replay pool, resident stream, tables */
+    int32_t ring_depth[16];
+    int32_t stash_slots;
+} ferret_footprint;
+FERRET_API ferret_status ferret_trainer_footprint(ferret_trainer* t, ferret_footprint* out);
 FERRET_API void ferret_trainer_destroy(ferret_trainer* t);
 
 /* Measurement hook (no reference counterpart): when enabled, every update

@@ -11,5 +11,6 @@ from .ferret import (  # noqa: F401
     PRECISIONS, StaleHarness, apply_skip_policy, load_csv_stream, train_sequential,
     compensate, conv_layer, dense_layer, device_available, lib, make_dense_net, online_accuracy, param_count,
     measure_profile, profile_from_widths, synth_drift_stream, train_pipeline,
+    b200_cost, b200_byte_profile, plan_b200,
 )
 from . import convnet  # noqa: F401,E402  (convolutional extension, BASELINE config 3)

@@ -14,6 +14,7 @@
 #include "ferret/profile.hpp"
 #include "ferret/sim.hpp"
 #include "ferret/stream.hpp"
+#include "schedule.hpp"
 
 namespace fb200 {
 
@@ -28,11 +29,6 @@ void set_last_error(const std::string& msg) { g_last_error = msg; }
 using fb200::fail;
 using fb200::guarded;
 
-struct ferret_schedule {
-    ferret::PlanResult plan;  // partition + config (+ planner trace when planned)
-    ferret::StreamSpec spec;
-    ferret::SimTrace trace;
-};
 
 namespace {
 

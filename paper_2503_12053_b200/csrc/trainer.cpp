@@ -85,13 +85,14 @@ uint16_t bf16_bits(float f) {
     return static_cast<uint16_t>(u >> 16);
 }
 
+// Plan-only trainers count what they would allocate (ferret_trainer_footprint) and get null.
 template <class T>
 T* dalloc(size_t n, size_t& counter) {
     void* p = nullptr;
-    if (t_plan_only) return nullptr;
     if (n == 0) n = 1;
-    cuda_check(cudaMalloc(&p, n * sizeof(T)), "cudaMalloc");
     counter += n * sizeof(T);
+    if (t_plan_only) return nullptr;
+    cuda_check(cudaMalloc(&p, n * sizeof(T)), "cudaMalloc");
     return static_cast<T*>(p);
 }
 
@@ -501,6 +502,7 @@ struct ferret_trainer {
 
     // per-chunk staging (fixed addresses baked into the graph)
     size_t chunk_cap = 0;
+    size_t stream_cap = 0;  // samples the resident-stream buffers hold
     double* d_rawc = nullptr;
     double* d_norm_mu = nullptr;   // per chunk sample x feature: mean / M2 after observing it (two-phase normalizer)
     double* d_norm_m2i = nullptr;
@@ -757,7 +759,8 @@ struct ferret_trainer {
         }
         F = layers.front().in;
         n_out = layers.back().out;
-        init_params.assign(net.params, net.params + host_off);
+        if (net.params) init_params.assign(net.params, net.params + host_off);
+        else if (!t_plan_only) fail(FERRET_E_INVALID_ARG, "net params: null (allowed for plan-only trainers only)");
         long long cursor = 0;
         int max_width = F;
         for (LayerDev& ld : layers) {
@@ -951,7 +954,7 @@ struct ferret_trainer {
             }
             grow_ring(s, 2);
         }
-        upload_initial_params();
+        if (!t_plan_only) upload_initial_params();
         d_replay = dalloc<float>(static_cast<size_t>(stash_stride), device_bytes);
         d_norm_mean = dalloc<double>(static_cast<size_t>(F), device_bytes);
         d_norm_m2 = dalloc<double>(static_cast<size_t>(F), device_bytes);
@@ -991,23 +994,27 @@ struct ferret_trainer {
     void grow_ring(StageDev& s, int depth) {
         if (depth <= s.depth) return;
         float* fresh = dalloc<float>(static_cast<size_t>(depth) * static_cast<size_t>(s.slot_floats), device_bytes);
-        if (s.ring) {
-            cuda_check(cudaStreamSynchronize(stream), "sync");
-            cuda_check(cudaMemcpy(fresh, s.ring, static_cast<size_t>(s.slot_floats) * sizeof(float),
-                                  cudaMemcpyDeviceToDevice),
-                       "ring copy");
-            cudaFree(s.ring);
+        if (s.depth > 0) {  // (plan-only trainers count the old ring without holding it)
+            if (s.ring) {
+                cuda_check(cudaStreamSynchronize(stream), "sync");
+                cuda_check(cudaMemcpy(fresh, s.ring, static_cast<size_t>(s.slot_floats) * sizeof(float),
+                                      cudaMemcpyDeviceToDevice),
+                           "ring copy");
+                cudaFree(s.ring);
+            }
             device_bytes -= static_cast<size_t>(s.depth) * static_cast<size_t>(s.slot_floats) * sizeof(float);
         }
         s.ring = fresh;
         if (opt.precision == FERRET_PREC_BF16) {
             uint16_t* fresh16 =
                 dalloc<uint16_t>(static_cast<size_t>(depth) * static_cast<size_t>(s.slot_floats), device_bytes);
-            if (s.ring16) {
-                cuda_check(cudaMemcpy(fresh16, s.ring16, static_cast<size_t>(s.slot_floats) * sizeof(uint16_t),
-                                      cudaMemcpyDeviceToDevice),
-                           "ring copy");
-                cudaFree(s.ring16);
+            if (s.depth > 0) {
+                if (s.ring16) {
+                    cuda_check(cudaMemcpy(fresh16, s.ring16, static_cast<size_t>(s.slot_floats) * sizeof(uint16_t),
+                                          cudaMemcpyDeviceToDevice),
+                               "ring copy");
+                    cudaFree(s.ring16);
+                }
                 device_bytes -= static_cast<size_t>(s.depth) * static_cast<size_t>(s.slot_floats) * sizeof(uint16_t);
             }
             s.ring16 = fresh16;
@@ -1021,6 +1028,7 @@ struct ferret_trainer {
         cuda_check(cudaStreamSynchronize(stream), "sync");
         dfree(d_partial);
         dfree(d_counters);
+        device_bytes -= static_cast<size_t>(scratch_slots) * (max_partial * sizeof(float) + max_tiles * sizeof(unsigned));
         d_partial = dalloc<float>(static_cast<size_t>(slots) * max_partial, device_bytes);
         d_counters = dalloc<unsigned>(static_cast<size_t>(slots) * max_tiles, device_bytes);
         cuda_check(cudaMemset(d_counters, 0, static_cast<size_t>(slots) * max_tiles * sizeof(unsigned)), "memset");
@@ -1030,10 +1038,8 @@ struct ferret_trainer {
     void ensure_stash(int slots) {
         if (slots <= stash_slots) return;
         cuda_check(cudaStreamSynchronize(stream), "sync");
-        if (d_stash) {
-            cudaFree(d_stash);
-            device_bytes -= static_cast<size_t>(stash_slots) * static_cast<size_t>(stash_stride) * sizeof(float);
-        }
+        if (d_stash) cudaFree(d_stash);
+        device_bytes -= static_cast<size_t>(stash_slots) * static_cast<size_t>(stash_stride) * sizeof(float);
         d_stash = dalloc<float>(static_cast<size_t>(slots) * static_cast<size_t>(stash_stride), device_bytes);
         stash_slots = slots;
     }
@@ -1051,6 +1057,8 @@ struct ferret_trainer {
             dfree(d_raw);
             dfree(d_lab);
             dfree(d_pred);
+            if (d_raw) device_bytes -= stream_cap * (f * sizeof(double) + 2 * sizeof(int));
+            stream_cap = n;
             d_raw = dalloc<double>(n * f, device_bytes);
             d_lab = dalloc<int>(n, device_bytes);
             d_pred = dalloc<int>(n, device_bytes);
@@ -1138,6 +1146,7 @@ struct ferret_trainer {
             for (void* p : {static_cast<void*>(d_rawc), static_cast<void*>(d_xc), static_cast<void*>(d_labc),
                             static_cast<void*>(d_predc), static_cast<void*>(d_norm_mu), static_cast<void*>(d_norm_m2i)})
                 dfree(p);
+            device_bytes -= chunk_cap * (static_cast<size_t>(F) * (3 * sizeof(double) + sizeof(float)) + 3 * sizeof(int));
             d_rawc = dalloc<double>(cap * static_cast<size_t>(F), device_bytes);
             d_norm_mu = dalloc<double>(cap * static_cast<size_t>(F), device_bytes);
             d_norm_m2i = dalloc<double>(cap * static_cast<size_t>(F), device_bytes);
@@ -1149,6 +1158,7 @@ struct ferret_trainer {
         if (need_ctl > ctl_bytes) {
             cuda_check(cudaStreamSynchronize(stream), "sync");
             dfree(d_ctl);
+            device_bytes -= ctl_bytes;
             for (unsigned char* p : h_ctl) cudaFreeHost(p);
             h_ctl.clear();
             d_ctl = dalloc<unsigned char>(need_ctl, device_bytes);
@@ -1260,6 +1270,46 @@ struct ferret_trainer {
         stats.kernel_launches = launches;
         stats.stash_slots = stash_slots;
         for (int j = 0; j < P && j < 16; ++j) stats.ring_depth[j] = stages[static_cast<size_t>(j)].depth;
+    }
+
+    // HBM the trainer holds once the current schedule's chunk graph is built (north-star item 4:
+    // the planner's memory in bytes): the dry pass that build_graph() runs sizes the version
+    // rings and the stash; everything else is already allocated (or, for a plan-only trainer,
+    // counted). Graph-build scratch of the tensor-core layers (split-K partials, conv weight
+    // copies) is not included.
+    ferret_footprint footprint() {
+        if (!have_schedule) fail(FERRET_E_LOGIC, "footprint: set_schedule first");
+        HostState probe = hs;
+        const PassResult need = [&] {
+            PlanOnlyScope scope(true);
+            return run_pass<true>(probe, hs.replay.seen > 0);
+        }();
+        ferret_footprint f{};
+        const size_t per_float = sizeof(float) + (opt.precision == FERRET_PREC_BF16 ? sizeof(uint16_t) : 0);
+        size_t total = device_bytes;
+        for (int j = 0; j < P; ++j) {
+            const StageDev& sd = stages[static_cast<size_t>(j)];
+            const int d = std::max(sd.depth, need.need_depth[static_cast<size_t>(j)]);
+            total += static_cast<size_t>(d - sd.depth) * static_cast<size_t>(sd.slot_floats) * per_float;
+            f.rings += static_cast<size_t>(d) * static_cast<size_t>(sd.slot_floats) * per_float;
+            const size_t nstate = (sd.lam_d ? 1 : 0) + (sd.v_r ? 2 : 0) + (sd.gap ? 1 : 0);
+            const size_t plan_state = plan_only ? (opt.policy == FERRET_POLICY_ITER_FISHER ? (opt.eta_lambda > 0.0 ? 3 : 1)
+                                                   : opt.policy == FERRET_POLICY_GAP ? 1 : 0)
+                                                : nstate;
+            f.comp_state += plan_state * static_cast<size_t>(sd.slot_floats) * sizeof(float);
+            if (j < 16) f.ring_depth[j] = d;
+        }
+        const int slots = std::max({need.need_slots, 1, stash_slots});
+        total += static_cast<size_t>(slots - stash_slots) * static_cast<size_t>(stash_stride) * sizeof(float);
+        f.stash = static_cast<size_t>(slots + 1) * static_cast<size_t>(stash_stride) * sizeof(float);  // + replay slot
+        const int ss = std::max(slots + 1, scratch_slots);
+        const size_t per_scratch = max_partial * sizeof(float) + max_tiles * sizeof(unsigned);
+        total += static_cast<size_t>(ss - scratch_slots) * per_scratch;
+        f.scratch = static_cast<size_t>(ss) * per_scratch;
+        f.stash_slots = slots;
+        f.total = total;
+        f.other = total - f.rings - f.comp_state - f.stash - f.scratch;
+        return f;
     }
 
     void build_graph(bool seen_any) {
@@ -2830,6 +2880,7 @@ struct ferret_trainer {
             ing.d_lab[s] = ing.d_pred[s] = ing.h_lab[s] = ing.h_pred[s] = nullptr;
             ing.in[s] = ing.freed[s] = ing.out[s] = nullptr;
         }
+        device_bytes -= 2 * ing.cap * (static_cast<size_t>(F) * sizeof(double) + 2 * sizeof(int));
         ing.cap = 0;
     }
 
@@ -3206,6 +3257,13 @@ ferret_status ferret_trainer_get_stats(ferret_trainer* t, ferret_trainer_stats* 
     return guarded([&] {
         *out = t->stats;
         out->device_bytes = t->device_bytes;
+    });
+}
+
+ferret_status ferret_trainer_footprint(ferret_trainer* t, ferret_footprint* out) {
+    return guarded([&] {
+        if (!out) fail(FERRET_E_INVALID_ARG, "footprint: null output");
+        *out = t->footprint();
     });
 }
 

@@ -84,6 +84,24 @@ class StreamSpecC(C.Structure):
     _fields_ = [("t_d", C.c_double), ("decay_c", C.c_double), ("value", C.c_double), ("horizon", C.c_double)]
 
 
+class Footprint(C.Structure):
+    _fields_ = [("total", C.c_uint64), ("rings", C.c_uint64), ("comp_state", C.c_uint64), ("stash", C.c_uint64),
+                ("scratch", C.c_uint64), ("other", C.c_uint64), ("ring_depth", C.c_int32 * 16),
+                ("stash_slots", C.c_int32)]
+
+
+class B200Cost(C.Structure):
+    _fields_ = [("micro_batch", C.c_int32), ("precision", C.c_int32), ("policy", C.c_int32),
+                ("eta_lambda", C.c_double), ("replay", C.c_int32), ("replay_capacity", C.c_uint64),
+                ("chunk_units", C.c_uint64)]
+
+
+class B200PlanReport(C.Structure):
+    _fields_ = [("budget_bytes", C.c_uint64), ("fixed_bytes", C.c_uint64), ("planner_budget", C.c_uint64),
+                ("planner_bytes", C.c_uint64), ("predicted_bytes", C.c_uint64), ("trainer_bytes", C.c_uint64),
+                ("passes", C.c_int32), ("stages", C.c_int32), ("fits", C.c_int32)]
+
+
 class TrainerStats(C.Structure):
     _fields_ = [("kernel_launches", C.c_uint64), ("events", C.c_uint64), ("updates", C.c_uint64),
                 ("replays", C.c_uint64), ("predicts", C.c_uint64), ("ring_depth", C.c_int32 * 16),
@@ -142,6 +160,13 @@ def lib() -> C.CDLL:
         "ferret_trainer_profile_kernels": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t, P(D), P(C.c_uint64), P(D),
                                                      C.c_int32, P(C.c_int32)]),
         "ferret_trainer_get_stats": (C.c_int, [C.c_void_p, P(TrainerStats)]),
+        "ferret_trainer_footprint": (C.c_int, [C.c_void_p, P(Footprint)]),
+        "ferret_b200_cost_default": (None, [P(B200Cost)]),
+        "ferret_measure_profile": (C.c_int, [P(C.c_uint64), C.c_int32, P(B200Cost), C.c_int32, C.c_int32,
+                                             C.c_void_p]),
+        "ferret_b200_byte_profile": (C.c_int, [C.c_void_p, C.c_int32, P(B200Cost), C.c_void_p]),
+        "ferret_plan_b200": (C.c_int, [P(C.c_uint64), C.c_int32, C.c_void_p, D, P(StreamSpecC), C.c_uint64,
+                                       C.c_int32, P(B200Cost), C.c_size_t, P(C.c_void_p), P(B200PlanReport)]),
         "ferret_trainer_destroy": (None, [C.c_void_p]),
         "ferret_trainer_set_timing": (C.c_int, [C.c_void_p, C.c_int32]),
         "ferret_trainer_update_timing": (C.c_int, [C.c_void_p, P(D), P(C.c_uint64), P(D)]),
@@ -383,10 +408,12 @@ class PipelineTrainer:
         self.widths = list(widths)
         self.bounds = list(bounds)
         self.opt = opt
-        self._keep = (ins, outs, acts, np.ascontiguousarray(params, dtype=np.float64), geom)
-        if self._keep[3].size != self.n_params:
+        # params may be None for a plan-only trainer (opt.device = -1: host passes and footprints only)
+        self._keep = (ins, outs, acts, None if params is None else np.ascontiguousarray(params, dtype=np.float64), geom)
+        if self._keep[3] is not None and self._keep[3].size != self.n_params:
             raise ConfigError(f"params: expected {self.n_params} values, got {self._keep[3].size}")
-        desc = NetDesc(len(ins), _up(ins), _up(outs), acts.ctypes.data_as(C.POINTER(C.c_int32)), _dp(self._keep[3]),
+        desc = NetDesc(len(ins), _up(ins), _up(outs), acts.ctypes.data_as(C.POINTER(C.c_int32)),
+                       _dp(self._keep[3]) if self._keep[3] is not None else None,
                        geom.ctypes.data_as(C.POINTER(C.c_int32)) if geom is not None else None)
         b = np.ascontiguousarray(bounds, dtype=np.uint64)
         h = C.c_void_p()
@@ -554,6 +581,15 @@ class PipelineTrainer:
 
     def open_peer(self, peer: int, handle: bytes) -> None:
         _check(lib().ferret_trainer_open_peer(self._h, peer, C.c_char_p(handle)))
+
+    def footprint(self) -> dict:
+        """ferret_trainer_footprint: HBM bytes once the current schedule's graph is built (works plan-only)."""
+        f = Footprint()
+        _check(lib().ferret_trainer_footprint(self._h, C.byref(f)))
+        P = len(self.bounds) - 1
+        d = {k: getattr(f, k) for k in ("total", "rings", "comp_state", "stash", "scratch", "other", "stash_slots")}
+        d["ring_depth"] = list(f.ring_depth[:P])
+        return d
 
     def handoff_plan(self):
         """(bytes, messages) per destination rank per chunk for the current schedule."""
@@ -765,34 +801,50 @@ def stage_owners(n_stages: int, world: int) -> list:
     return [min(world - 1, (j * world) // n_stages) for j in range(n_stages)]
 
 
+def b200_cost(micro_batch: int = 1, precision: str = "fp32", policy: str = "iter_fisher", eta_lambda: float = 1e-3,
+              replay: bool = False, replay_capacity: int = 5000, chunk_units: int = 0) -> B200Cost:
+    """ferret_b200_cost: what the B200 planner prices (bytes per weight version, stash per unit, state)."""
+    c = B200Cost()
+    lib().ferret_b200_cost_default(C.byref(c))
+    c.micro_batch, c.precision, c.policy = micro_batch, PRECISIONS[precision], POLICIES[policy]
+    c.eta_lambda, c.replay, c.replay_capacity, c.chunk_units = eta_lambda, int(replay), replay_capacity, chunk_units
+    return c
+
+
 def measure_profile(widths: Sequence[int], micro_batch: int = 1, policy: str = "iter_fisher", units: int = 48,
-                    device: int = 0) -> np.ndarray:
-    """B200 re-costing of profile_from_net (net.hpp:263-274): per layer, t_f = measured
-    device seconds of its forward and t_b = its backward + compensated update, from a
-    profiled one-layer-per-stage run of the actual kernels at this micro-batch. w and a
-    are the reference's counts. Feed the result to Schedule.plan(..., max_stages=#GPUs)."""
-    L = len(widths) - 1
-    prof = profile_from_widths(widths)
-    bounds = list(range(L + 1))
-    t_d = float(prof["t_f"].max())
-    sched = Schedule.forced(prof, t_d, StreamSpec(t_d=t_d, horizon=units * t_d), bounds, units)
-    chunk = units * micro_batch
-    feats, labels = synth_drift_stream(2 * chunk, widths[0], widths[-1], "split_tasks", 7)
-    tr = PipelineTrainer(widths, make_dense_net(widths, 1), bounds,
-                         PipelineTrainOptions(policy=policy, micro_batch=micro_batch, device=device))
-    try:
-        tr.load_stream(feats, labels)
-        tr.set_schedule(sched.events, chunk)
-        tr.execute(0)
-        tr.set_profiling(True)
-        tr.execute(1)
-        f, b, u = tr.profile_stages()
-    finally:
-        tr.close()
-    out = prof.copy()
-    out["t_f"] = np.maximum(f, 1e-3) * 1e-6
-    out["t_b"] = np.maximum(b + u, 1e-3) * 1e-6
+                    device: int = 0, precision: str = "fp32") -> np.ndarray:
+    """B200 re-costing of profile_from_net (net.hpp:263-274), ferret_measure_profile: per layer,
+    t_f = measured device seconds of its forward event and t_b = its backward + compensated
+    update, from a profiled one-layer-per-stage replay of the real kernels at this micro-batch.
+    w and a are the reference's counts. Feed the result to plan_b200()."""
+    w = np.ascontiguousarray(widths, dtype=np.uint64)
+    out = np.zeros(len(widths) - 1, dtype=PROFILE_DTYPE)
+    cost = b200_cost(micro_batch, precision, policy)
+    _check(lib().ferret_measure_profile(_up(w), len(w), C.byref(cost), units, device, out.ctypes.data))
     return out
+
+
+def b200_byte_profile(profile: np.ndarray, cost: B200Cost) -> np.ndarray:
+    """ferret_b200_byte_profile: w -> bytes of one weight version, a -> stash bytes per in-flight unit."""
+    prof = np.ascontiguousarray(profile, dtype=PROFILE_DTYPE)
+    out = np.zeros_like(prof)
+    _check(lib().ferret_b200_byte_profile(prof.ctypes.data, len(prof), C.byref(cost), out.ctypes.data))
+    return out
+
+
+def plan_b200(widths: Sequence[int], profile: np.ndarray, t_d: float, spec: StreamSpec, budget_bytes: int = 0,
+              max_stages: int = 0, cost: Optional[B200Cost] = None, n_items: int = 0):
+    """ferret_plan_b200: the reference planner fed measured times and HBM bytes, the chosen plan
+    priced exactly by the trainer's dry-run footprint (re-planned until it fits), partitions
+    limited to max_stages = #GPUs. Returns (Schedule, report dict)."""
+    w = np.ascontiguousarray(widths, dtype=np.uint64)
+    prof = np.ascontiguousarray(profile, dtype=PROFILE_DTYPE)
+    cost = cost if cost is not None else b200_cost()
+    h = C.c_void_p()
+    rep = B200PlanReport()
+    _check(lib().ferret_plan_b200(_up(w), len(w), prof.ctypes.data, t_d, C.byref(spec.c()), budget_bytes, max_stages,
+                                  C.byref(cost), n_items, C.byref(h), C.byref(rep)))
+    return Schedule(h.value), {k: getattr(rep, k) for k, _ in B200PlanReport._fields_}
 
 
 def conv_layer(tc: int, mode: int, geom, B: int, W, bias=None, X=None, D=None, res=None, res_chw=(0, 0, 0),
