@@ -301,8 +301,11 @@ FERRET_API void* ferret_trainer_stream(ferret_trainer* t);
  * Each rank replays the whole log but launches only its stages' kernels; stage
  * outputs, input gradients (sent unmasked, masked by the receiver) and the
  * predict / replay sweeps cross ranks as direct stores into the peer's inbox
- * followed by a release flag (NVLink P2P on an 8xB200 box). Ranks must finish
- * chunk c before any rank starts chunk c+1 (the caller's barrier). Only the
+ * followed by a release flag (NVLink P2P on an 8xB200 box). Flow control is
+ * on the device: the receiver acknowledges every consumed message by storing
+ * the chunk's epoch into the sender's ack slot, and the sender of the next
+ * chunk's message in that slot waits for it, so ranks run chunk after chunk
+ * (and ingest() many chunks per call) with no host barrier. Only the
  * rank owning the last stage produces predictions (fetch_log); only rank 0
  * holds the normalizer; params/comp_state are valid for the stages a rank owns. */
 FERRET_API ferret_status ferret_trainer_set_shard(ferret_trainer* t, int32_t rank, int32_t world,

@@ -1355,7 +1355,32 @@ __global__ void pool_kernel(const PoolArgs a) {
 }
 
 // Hand-off between ranks. One CTA each: messages are B x width floats (<= 256 KB).
+// Flow control without host barriers: a message slot of chunk e may be overwritten
+// only once its receiver consumed it in chunk e - 1, which the receiver reports by
+// storing e - 1 into the sender's ack slot (recv_kernel); the sender waits for it.
+__device__ __forceinline__ bool wait_epoch(const unsigned* word, unsigned want, bool exact, unsigned* error) {
+    unsigned v;
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(word) : "memory");
+        if (exact ? v == want : static_cast<int>(v - want) >= 0) return true;
+        __nanosleep(64);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 10000000000ull) {  // a peer rank is not progressing: fail the chunk, never hang
+            if (error) atomicExch(error, 1u);
+            return false;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(512) send_kernel(const SendArgs a) {
+    if (a.ack) {
+        __shared__ unsigned go;
+        if (threadIdx.x == 0) go = wait_epoch(a.ack, *a.epoch - 1u, false, a.error);
+        __syncthreads();
+        (void)go;
+    }
     const bool vec = ((reinterpret_cast<uintptr_t>(a.src) | reinterpret_cast<uintptr_t>(a.dst)) & 15u) == 0 && (a.n & 3) == 0;
     if (vec) {
         const float4* s = reinterpret_cast<const float4*>(a.src);
@@ -1374,29 +1399,21 @@ __global__ void __launch_bounds__(512) send_kernel(const SendArgs a) {
 
 __global__ void __launch_bounds__(512) recv_kernel(const RecvArgs a) {
     __shared__ unsigned ready;
-    if (threadIdx.x == 0) {
-        const unsigned e = *a.epoch;
-        unsigned v;
-        unsigned long long t0, t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-        for (;;) {
-            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a.flag) : "memory");
-            if (v == e) break;
-            __nanosleep(64);
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            if (t - t0 > 10000000000ull) {  // a peer rank is not progressing: fail the chunk, never hang
-                if (a.error) atomicExch(a.error, 1u);
-                break;
-            }
-        }
-        ready = 1;
-    }
+    const unsigned e = *a.epoch;
+    if (threadIdx.x == 0) ready = wait_epoch(a.flag, e, true, a.error);
     __syncthreads();
     (void)ready;
     for (int i = threadIdx.x; i < a.n; i += blockDim.x) {
         float v = __ldcv(a.src + i);  // bypass L1: the peer wrote it
         if (a.mask && !(a.mask[i] > 0.f)) v = 0.f;
         a.dst[i] = v;
+    }
+    if (a.ack) {  // every read of the slot is done: the sender may reuse it next chunk
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence_system();
+            asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.ack), "r"(e) : "memory");
+        }
     }
 }
 

@@ -218,6 +218,8 @@ struct SendArgs {
     unsigned* flag;            // peer flag
     const unsigned* epoch;     // control block (this chunk's epoch)
     int n;
+    const unsigned* ack;       // own memory: the receiver's last consumed epoch of this inbox slot
+    unsigned* error;           // own hand-off error word
 };
 struct RecvArgs {
     const float* src;          // own inbox
@@ -227,6 +229,7 @@ struct RecvArgs {
     const unsigned* epoch;
     int n;
     unsigned* error;           // set to 1 when the flag did not arrive within 10 s (the chunk's results are invalid)
+    unsigned* ack;             // the sender's ack slot of this message (peer memory)
 };
 
 // A fully resolved kernel launch: the trainer either launches it on a stream

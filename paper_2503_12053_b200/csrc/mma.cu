@@ -58,6 +58,75 @@ constexpr int kBAtomBytes = 16 * 128;  // B operand per 128-byte K atom: 16 rows
 constexpr size_t kMaxSmem = 225 * 1024;  // opt-in dynamic shared memory per CTA (227 KB less static)
 
 
+// Epilogue of the dense-layer kernels, warps 2-5: TMEM -> registers (warp w reads TMEM
+// lanes of quadrant w % 4: thread = accumulator row m0 + row, 16 columns n), then bias +
+// ReLU (forward) or the ReLU mask (backward); with S > 1 K splits the partial tile goes
+// to L2 scratch and the last CTA of the M tile sums the S partials in split order.
+template <bool BWD>
+__device__ __forceinline__ void mma_epilogue(const MmaArgs& a, uint32_t tmem, uint64_t* done, bool any, int warp,
+                                             int lane, int m0, int q, int S) {
+    const int row = (warp & 3) * 32 + lane;
+    float acc[16];
+    if (any) {
+        mbar_wait(done, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        tmem_ld16(tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16), acc);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+    }
+    auto finish = [&](int m, int nn, float v) {
+        if (m >= a.M || nn >= a.N) return;
+        const size_t o = static_cast<size_t>(nn) * a.ldy + m;
+        if (!BWD) {
+            v += __ldg(a.bias + m);
+            if (a.relu) v = v > 0.f ? v : 0.f;
+        } else if (a.mask) {
+            v = __ldg(a.mask + o) > 0.f ? v : 0.f;
+        }
+        a.Y[o] = v;
+    };
+    if (S == 1) {
+#pragma unroll
+        for (int nn = 0; nn < 16; ++nn) finish(m0 + row, nn, acc[nn]);
+        return;
+    }
+    // split-K: partial tile to global scratch ([n][128], coalesced); the last CTA of the
+    // M tile to arrive sums the S partials in split order (deterministic) and runs the
+    // epilogue
+    float* part = a.partial + (static_cast<size_t>(blockIdx.y) * S + q) * 128 * 16;
+#pragma unroll
+    for (int nn = 0; nn < 16; ++nn) part[nn * 128 + row] = acc[nn];
+    __threadfence();
+    asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps
+    __shared__ unsigned last;
+    if (warp == 2 && lane == 0) last = atomicAdd(a.counters + blockIdx.y, 1u) == static_cast<unsigned>(S - 1);
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (!last) return;
+    __threadfence();
+    // sum in split order; this CTA's own partial is still in registers, the others'
+    // 16 values per split are loaded together
+    const float* base = a.partial + static_cast<size_t>(blockIdx.y) * S * 128 * 16 + row;
+    float v[16];
+#pragma unroll
+    for (int nn = 0; nn < 16; ++nn) v[nn] = 0.f;
+    for (int p = 0; p < S; ++p) {
+        float tv[16];
+        if (p == q) {
+#pragma unroll
+            for (int nn = 0; nn < 16; ++nn) tv[nn] = acc[nn];
+        } else {
+#pragma unroll
+            for (int nn = 0; nn < 16; ++nn) tv[nn] = __ldcg(base + (static_cast<size_t>(p) * 16 + nn) * 128);
+        }
+#pragma unroll
+        for (int nn = 0; nn < 16; ++nn) v[nn] += tv[nn];
+    }
+#pragma unroll
+    for (int nn = 0; nn < 16; ++nn) finish(m0 + row, nn, v[nn]);
+    if (warp == 2 && lane == 0) a.counters[blockIdx.y] = 0u;  // self-resetting (graph replays)
+}
+
 template <int ES, bool BWD, bool SPLIT = false>
 __global__ void __launch_bounds__(kMmaThreads, 1) mma_layer_kernel(const __grid_constant__ MmaArgs a) {
     constexpr int KA = 128 / ES;       // K elements per 128-byte atom
@@ -258,74 +327,168 @@ __global__ void __launch_bounds__(kMmaThreads, 1) mma_layer_kernel(const __grid_
     }
     __syncwarp();
 
-    // ---- epilogue, warps 2-5: TMEM -> registers (warp w reads TMEM lanes of
-    // quadrant w % 4: thread = accumulator row m0 + row, 16 columns n)
+    // ---- epilogue, warps 2-5
     if (warp >= 2 && warp < 6) {
-        const int row = (warp & 3) * 32 + lane;
-        float acc[16];
-        if (na > 0) {
+        if (warp == 2 && lane == 0 && na > 0) {
             mbar_wait(done, 0);
-            if (warp == 2 && lane == 0) tick(4);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            tmem_ld16(tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16), acc);
-        } else {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+            tick(4);
         }
-        auto finish = [&](int m, int nn, float v) {
-            if (m >= a.M || nn >= a.N) return;
-            const size_t o = static_cast<size_t>(nn) * a.ldy + m;
-            if (!BWD) {
-                v += __ldg(a.bias + m);
-                if (a.relu) v = v > 0.f ? v : 0.f;
-            } else if (a.mask) {
-                v = __ldg(a.mask + o) > 0.f ? v : 0.f;
-            }
-            a.Y[o] = v;
-        };
-        if (S == 1) {
-#pragma unroll
-            for (int nn = 0; nn < 16; ++nn) finish(m0 + row, nn, acc[nn]);
-        } else {
-            // split-K: partial tile to global scratch ([n][128], coalesced); the last
-            // CTA of the M tile to arrive sums the S partials in split order
-            // (deterministic) and runs the epilogue
-            float* part = a.partial + (static_cast<size_t>(blockIdx.y) * S + q) * 128 * 16;
-#pragma unroll
-            for (int nn = 0; nn < 16; ++nn) part[nn * 128 + row] = acc[nn];
-            __threadfence();
-            asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps
-            __shared__ unsigned last;
-            if (warp == 2 && lane == 0) last = atomicAdd(a.counters + blockIdx.y, 1u) == static_cast<unsigned>(S - 1);
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            if (last) {
-                __threadfence();
-                // sum in split order; this CTA's own partial is still in registers,
-                // the others' 16 values per split are loaded together
-                const float* base = a.partial + static_cast<size_t>(blockIdx.y) * S * 128 * 16 + row;
-                float v[16];
-#pragma unroll
-                for (int nn = 0; nn < 16; ++nn) v[nn] = 0.f;
-                for (int p = 0; p < S; ++p) {
-                    float tv[16];
-                    if (p == q) {
-#pragma unroll
-                        for (int nn = 0; nn < 16; ++nn) tv[nn] = acc[nn];
-                    } else {
-#pragma unroll
-                        for (int nn = 0; nn < 16; ++nn) tv[nn] = __ldcg(base + (static_cast<size_t>(p) * 16 + nn) * 128);
-                    }
-#pragma unroll
-                    for (int nn = 0; nn < 16; ++nn) v[nn] += tv[nn];
-                }
-#pragma unroll
-                for (int nn = 0; nn < 16; ++nn) finish(m0 + row, nn, v[nn]);
-                if (warp == 2 && lane == 0) a.counters[blockIdx.y] = 0u;  // self-resetting (graph replays)
-            }
-        }
+        mma_epilogue<BWD>(a, tmem, done, na > 0, warp, lane, m0, q, S);
     }
 
     if (warp == 2 && lane == 0) tick(5);
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// mma_split_kernel: the fp32 parity mode's dense layer (3xTF32, see tf32_hi) with
+// the B operand staged per ring stage instead of for the CTA's whole K range up
+// front. A ring stage holds the TMA'd A tile (16 KB, hi implicit: kind::tf32 drops
+// the low mantissa bits), its lo part (16 KB) and the unit's B atom as hi + lo
+// (2 + 2 KB): 36 KB, so two CTAs per SM keep 3 stages each in flight (the
+// whole-K B staging of mma_layer_kernel<4, *, true> left room for 2 stages of one
+// CTA: 1.5 TB/s on config 5's 4096 x 4096 layers). Roles:
+//   warp 0 / lane 0  TMA producer: A tile of stage s once the MMA freed it (empty[s])
+//   warp 1 / lane 0  MMA issuer: 4 k-steps x 3 MMAs (hi.hi, hi.lo, lo.hi) per stage,
+//                    tcgen05.commit -> empty[s]
+//   warps 2-9        stagers: load the unit's B atom i (L2) before waiting for the
+//                    A tile, then split A (lo) and B (hi, lo) into the stage and
+//                    publish it on lready[s]; warps 2-5 then run the epilogue
+// ---------------------------------------------------------------------------
+constexpr int kSplitStageBytes = 2 * kTileBytes + 2 * kBAtomBytes;
+
+template <bool BWD>
+__global__ void __launch_bounds__(kMmaThreads, 2) mma_split_kernel(const __grid_constant__ MmaArgs a) {
+    constexpr int KA = 32, UK = 8;  // fp32: 32 K elements per 128-byte atom, 8 per tcgen05.mma (kind::tf32)
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int nst = a.stages;
+    auto stage = [&](int s) { return base + static_cast<size_t>(s) * kSplitStageBytes; };
+    uint64_t* full = reinterpret_cast<uint64_t*>(stage(nst));
+    uint64_t* empty = full + nst;
+    uint64_t* lready = empty + nst;
+    uint64_t* done = lready + nst;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int S = a.splits, q = blockIdx.x;
+    const int m0 = blockIdx.y * 128;
+    const int a_lo = q * a.atoms_per_cta;
+    const int a_hi = min(a.katoms, a_lo + a.atoms_per_cta);
+    const int na = max(0, a_hi - a_lo);
+
+    if (threadIdx.x == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.tmap)) : "memory");
+        for (int s = 0; s < nst; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 1);
+            mbar_init(lready + s, kStagers);
+        }
+        mbar_init(done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0 && lane == 0 && na > 0) {
+        for (int i = 0; i < na; ++i) {
+            const int s = i % nst;
+            if (i >= nst) mbar_wait(empty + s, ((i / nst) - 1) & 1);
+            mbar_expect_tx(full + s, kTileBytes);
+            unsigned char* dst = stage(s);
+            const int kk = (a_lo + i) * KA;
+            if (!BWD) {
+                tma_load_2d(dst, &a.tmap, full + s, kk, m0);
+            } else {
+#pragma unroll
+                for (int c = 0; c < 128 / KA; ++c) tma_load_2d(dst + c * KA * 128, &a.tmap, full + s, m0 + c * KA, kk);
+            }
+        }
+    } else if (warp == 1 && lane == 0 && na > 0) {
+        // D f32, A/B tf32, A K-major (forward) or MN-major (backward), N = 16, M = 128
+        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((BWD ? 1u : 0u) << 15) | ((16u >> 3) << 17) |
+                               ((128u >> 4) << 24);
+        for (int i = 0; i < na; ++i) {
+            const int s = i % nst;
+            mbar_wait(lready + s, (i / nst) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t ah = smem_u32(stage(s)), al = ah + kTileBytes;
+            const uint32_t bh = al + kTileBytes, bl = bh + kBAtomBytes;
+#pragma unroll
+            for (int k = 0; k < KA / UK; ++k) {
+                const uint64_t adh = BWD ? smem_desc(ah + k * UK * 128, KA * 128, 512, 1) : smem_desc(ah + k * 32, 16, 1024);
+                const uint64_t adl = BWD ? smem_desc(al + k * UK * 128, KA * 128, 512, 1) : smem_desc(al + k * 32, 16, 1024);
+                const uint64_t bdh = smem_desc(bh + k * 32, 16, 1024);
+                const uint64_t bdl = smem_desc(bl + k * 32, 16, 1024);
+                umma(tmem, adh, bdh, idesc, (i > 0 || k > 0) ? 1u : 0u, true);
+                umma(tmem, adh, bdl, idesc, 1u, true);
+                umma(tmem, adl, bdh, idesc, 1u, true);
+            }
+            umma_commit(empty + s);
+        }
+        umma_commit(done);
+    } else if (warp >= 2) {
+        // B atom: 16 rows x 32 floats; thread t < 128 owns 16-byte chunk j = t % 8 of row
+        // n = t / 8 (swizzled to (n/8)*1024 + (n%8)*128 + ((j ^ n%8) * 16)); the A tile's
+        // 1024 float4 are split by all 256 stagers
+        const int t = threadIdx.x - 64, j = t & 7, n = t >> 3;
+        const bool bthr = t < 128, rowv = bthr && n < a.N;
+        const float* rowp = rowv ? a.X + static_cast<size_t>(a.xidx ? __ldg(a.xidx + n) : n) * a.ldx : a.X;
+        const int boff = (n >> 3) * 1024 + (n & 7) * 128 + ((j ^ (n & 7)) << 4);
+        auto load_b = [&](int i) {
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            const int k0 = (a_lo + i) * KA + j * 4;
+            if (rowv && i < na) {
+                const float* src = rowp + k0;
+                if (a.vec && k0 + 4 <= a.K) {
+                    v = __ldg(reinterpret_cast<const float4*>(src));
+                } else {
+                    v.x = k0 < a.K ? __ldg(src) : 0.f;
+                    v.y = k0 + 1 < a.K ? __ldg(src + 1) : 0.f;
+                    v.z = k0 + 2 < a.K ? __ldg(src + 2) : 0.f;
+                    v.w = k0 + 3 < a.K ? __ldg(src + 3) : 0.f;
+                }
+            }
+            return v;
+        };
+        float4 bnext = load_b(0);
+        for (int i = 0; i < na; ++i) {
+            const int s = i % nst;
+            const float4 bv = bnext;
+            bnext = load_b(i + 1);  // next atom's B in flight while this stage is split
+            mbar_wait(full + s, (i / nst) & 1);
+            unsigned char* st = stage(s);
+            const float4* A4 = reinterpret_cast<const float4*>(st);
+            float4* L4 = reinterpret_cast<float4*>(st + kTileBytes);
+#pragma unroll
+            for (int e = t; e < kTileBytes / 16; e += kStagers) {
+                const float4 x = A4[e];
+                L4[e] = make_float4(x.x - tf32_hi(x.x), x.y - tf32_hi(x.y), x.z - tf32_hi(x.z), x.w - tf32_hi(x.w));
+            }
+            if (bthr) {  // rows n >= N stay stale: D column n reads B row n only, never stored
+                const float4 hi = make_float4(tf32_hi(bv.x), tf32_hi(bv.y), tf32_hi(bv.z), tf32_hi(bv.w));
+                *reinterpret_cast<float4*>(st + 2 * kTileBytes + boff) = hi;
+                *reinterpret_cast<float4*>(st + 2 * kTileBytes + kBAtomBytes + boff) =
+                    make_float4(bv.x - hi.x, bv.y - hi.y, bv.z - hi.z, bv.w - hi.w);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(lready + s)) : "memory");
+        }
+    }
+    __syncwarp();
+    if (warp >= 2 && warp < 6) mma_epilogue<BWD>(a, tmem, done, na > 0, warp, lane, m0, q, S);
+
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 1) {
@@ -358,6 +521,17 @@ const void* mma_func(size_t smem) {
     return f;
 }
 
+template <bool BWD>
+const void* split_func(size_t smem) {
+    static size_t configured = 0;
+    const void* f = reinterpret_cast<const void*>(&mma_split_kernel<BWD>);
+    if (smem > configured) {
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        configured = smem;
+    }
+    return f;
+}
+
 }  // namespace
 
 bool mma_supported(bool bf16, int in, int out) {
@@ -368,6 +542,27 @@ bool mma_supported(bool bf16, int in, int out) {
 
 MmaGeom mma_geom(bool bf16, bool bwd, int in, int out, bool split) {
     const int es = bf16 ? 2 : 4;
+    if (split && !bf16 && !std::getenv("FERRET_MMA_SPLIT_WHOLE_B")) {
+        // mma_split_kernel: two CTAs per SM, 36 KB ring stages (A hi, A lo, B hi, B lo)
+        MmaGeom g{};
+        const int M = bwd ? in : out, K = bwd ? out : in;
+        g.mtiles = (M + 127) / 128;
+        g.katoms = static_cast<int>((static_cast<long long>(K) * 4 + 127) / 128);
+        int S = 2 * 148 / g.mtiles;
+        if (S > 16) S = 16;
+        if (S > g.katoms) S = g.katoms;
+        if (S < 1) S = 1;
+        if (const char* env = std::getenv("FERRET_MMA_SPLIT")) S = std::atoi(env);  // experiment knob
+        g.apc = (g.katoms + S - 1) / S;
+        g.S = (g.katoms + g.apc - 1) / g.apc;
+        constexpr size_t kPerCta = 113 * 1024;  // two CTAs per SM (228 KB less the per-CTA reserve)
+        const size_t fixed = 1024 + 4 * 16 * 8 + 16;
+        g.stages = static_cast<int>((kPerCta - fixed) / kSplitStageBytes);
+        if (g.stages > g.apc) g.stages = g.apc;
+        g.smem = fixed + static_cast<size_t>(g.stages) * kSplitStageBytes;
+        g.partial_floats = g.S > 1 ? static_cast<size_t>(g.mtiles) * g.S * 128 * 16 : 0;
+        return g;
+    }
     const int mult = split ? 2 : 1;  // 3xTF32: hi + lo copies of the A ring and of B
     MmaGeom g{};
     const int M = bwd ? in : out, K = bwd ? out : in;
@@ -435,7 +630,9 @@ void spec_mma(const MmaLayer& L, KernelSpec& k) {
         std::abort();
     }
     a.vec = (a.ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(L.X) & 15u) == 0);
+    const bool ring_b = split && !std::getenv("FERRET_MMA_SPLIT_WHOLE_B");
     const void* f = es == 2 ? (L.bwd ? mma_func<2, true>(g.smem) : mma_func<2, false>(g.smem))
+                  : ring_b  ? (L.bwd ? split_func<true>(g.smem) : split_func<false>(g.smem))
                   : split   ? (L.bwd ? mma_func<4, true, true>(g.smem) : mma_func<4, false, true>(g.smem))
                             : (L.bwd ? mma_func<4, true>(g.smem) : mma_func<4, false>(g.smem));
     static_assert(sizeof(MmaArgs) <= sizeof(k.arg0), "kernel argument too large");

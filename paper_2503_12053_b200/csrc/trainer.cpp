@@ -549,6 +549,9 @@ struct ferret_trainer {
     std::vector<float*> peer_data;          // per rank: inbox data base (own included)
     std::vector<unsigned*> peer_flags;
     std::vector<void*> peer_opened;         // IPC mappings to close
+    std::vector<unsigned*> peer_acks;       // per rank: its ack region (own rank: this rank's)
+    std::vector<size_t> inbox_flag_counts;  // per rank: incoming messages per chunk
+    std::vector<size_t> ack_off;            // per destination: first ack slot of messages to it
     unsigned epoch_counter = 0;
 
     void set_shard(int r, int w, const int32_t* own) {
@@ -563,6 +566,7 @@ struct ferret_trainer {
         owner.assign(own, own + P);
         peer_data.assign(static_cast<size_t>(w), nullptr);
         peer_flags.assign(static_cast<size_t>(w), nullptr);
+        peer_acks.assign(static_cast<size_t>(w), nullptr);
         have_schedule = false;
         invalidate_graph();
     }
@@ -584,8 +588,17 @@ struct ferret_trainer {
         HostState probe = hs;
         const PassResult plan = run_pass<true>(probe, false);
         inbox_data_bytes = plan.inbox_bytes;
+        inbox_flag_counts = plan.inbox_flags;
+        // layout: [incoming message data][incoming flags][acks of this rank's outgoing
+        // messages, per destination d: inbox_flags[d] slots][pad; last word: error]
+        ack_off.assign(static_cast<size_t>(world), 0);
+        size_t n_acks = 0;
+        for (int d = 0; d < world; ++d) {
+            ack_off[static_cast<size_t>(d)] = n_acks;
+            n_acks += inbox_flag_counts[static_cast<size_t>(d)];
+        }
         const size_t data = (inbox_data_bytes[static_cast<size_t>(rank)] + 255) / 256 * 256;
-        const size_t need = data + plan.inbox_flags[static_cast<size_t>(rank)] * sizeof(unsigned) + 256;
+        const size_t need = data + (plan.inbox_flags[static_cast<size_t>(rank)] + n_acks) * sizeof(unsigned) + 256;
         cuda_check(cudaStreamSynchronize(stream), "sync");
         if (need > inbox_alloc) {
             dfree(d_inbox);
@@ -600,10 +613,13 @@ struct ferret_trainer {
         peer_opened.assign(static_cast<size_t>(world), nullptr);
         std::fill(peer_data.begin(), peer_data.end(), nullptr);
         std::fill(peer_flags.begin(), peer_flags.end(), nullptr);
+        peer_acks.assign(static_cast<size_t>(world), nullptr);
         invalidate_graph();
-        cuda_check(cudaMemset(d_inbox, 0, inbox_alloc), "memset inbox");  // flags start below every epoch
+        cuda_check(cudaMemset(d_inbox, 0, inbox_alloc), "memset inbox");  // flags and acks start at epoch 0
+        epoch_counter = 0;  // every rank re-sets its schedule together: epochs restart in step
         peer_data[static_cast<size_t>(rank)] = reinterpret_cast<float*>(d_inbox);
         peer_flags[static_cast<size_t>(rank)] = reinterpret_cast<unsigned*>(d_inbox + data);
+        peer_acks[static_cast<size_t>(rank)] = peer_flags[static_cast<size_t>(rank)] + plan.inbox_flags[static_cast<size_t>(rank)];
     }
 
     void open_peer(int p, const void* handle) {
@@ -619,6 +635,7 @@ struct ferret_trainer {
         const size_t data = (inbox_data_bytes[static_cast<size_t>(p)] + 255) / 256 * 256;
         peer_data[static_cast<size_t>(p)] = static_cast<float*>(ptr);
         peer_flags[static_cast<size_t>(p)] = reinterpret_cast<unsigned*>(static_cast<unsigned char*>(ptr) + data);
+        peer_acks[static_cast<size_t>(p)] = peer_flags[static_cast<size_t>(p)] + inbox_flag_counts[static_cast<size_t>(p)];
         invalidate_graph();
     }
 
@@ -790,6 +807,7 @@ struct ferret_trainer {
         owner.assign(static_cast<size_t>(P), 0);
         peer_data.assign(1, nullptr);
         peer_flags.assign(1, nullptr);
+        peer_acks.assign(1, nullptr);
         for (int j = 0; j < P; ++j) {
             StageDev& s = stages[static_cast<size_t>(j)];
             s.lo = static_cast<int>(bounds[j]);
@@ -1442,7 +1460,9 @@ struct ferret_trainer {
                 fail(FERRET_E_LOGIC, "hand-off to rank " + std::to_string(dst) + ": peer inbox not opened");
             if (rank == src) {
                 fb200::SendArgs a{src_ptr(), peer_data[static_cast<size_t>(dst)] + off / sizeof(float),
-                                  peer_flags[static_cast<size_t>(dst)] + fl, ctl_epoch(), static_cast<int>(n)};
+                                  peer_flags[static_cast<size_t>(dst)] + fl, ctl_epoch(), static_cast<int>(n),
+                                  peer_acks[static_cast<size_t>(rank)] + ack_off[static_cast<size_t>(dst)] + fl,
+                                  handoff_error()};
                 fb200::KernelSpec k;
                 fb200::spec_send(a, k);
                 gb->cur_category = kCatOther;
@@ -1450,9 +1470,12 @@ struct ferret_trainer {
                 gb->kernel(k, {key}, {});
             }
             if (rank == dst) {
+                if (!peer_acks[static_cast<size_t>(src)])
+                    fail(FERRET_E_LOGIC, "hand-off from rank " + std::to_string(src) + ": peer inbox not opened");
                 fb200::RecvArgs a{peer_data[static_cast<size_t>(rank)] + off / sizeof(float), dst_ptr(), mask,
                                   peer_flags[static_cast<size_t>(rank)] + fl, ctl_epoch(), static_cast<int>(n),
-                                  handoff_error()};
+                                  handoff_error(),
+                                  peer_acks[static_cast<size_t>(src)] + ack_off[static_cast<size_t>(rank)] + fl};
                 fb200::KernelSpec k;
                 fb200::spec_recv(a, k);
                 gb->cur_category = kCatOther;
@@ -2886,10 +2909,8 @@ struct ferret_trainer {
 
     void ingest(const double* features, const uint64_t* lab, size_t n, size_t f, ferret_step_record* log) {
         if (!have_schedule) fail(FERRET_E_LOGIC, "ingest: no schedule set");
-        // stage-sharded trainers reuse their inboxes every chunk and need a barrier between
-        // chunks, which a multi-chunk call cannot insert: one chunk per call there
-        if (world > 1 && n != sched.chunk_items)
-            fail(FERRET_E_CONFIG, "ingest: a stage-sharded trainer (world > 1) takes one chunk per call");
+        // (stage-sharded trainers reuse their inboxes every chunk: the per-message acks of
+        // send_kernel / recv_kernel keep a chunk's sends behind the previous chunk's reads)
         if (static_cast<int>(f) != F) fail(FERRET_E_INVALID_ARG, "stream feature width does not match the net input");
         const size_t chunk = sched.chunk_items;
         if (n % chunk) fail(FERRET_E_INVALID_ARG, "ingest: sample count must be a whole number of chunks");

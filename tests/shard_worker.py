@@ -26,6 +26,9 @@ def main():
     ap.add_argument("--device", type=int, default=-1, help="-1: LOCAL_RANK")
     ap.add_argument("--precision", default="fp32")
     ap.add_argument("--conv-width", type=int, default=0, help="> 0: a ResNet-style conv net (convnet.resnet_cifar)")
+    ap.add_argument("--mode", default="free", choices=["free", "barrier", "ingest"],
+                    help="free: execute() chunk after chunk with no host sync (device acks only); barrier: sync + "
+                         "dist.barrier between chunks; ingest: one ingest() call over every chunk from host memory")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -60,7 +63,8 @@ def main():
                                                     replay_seed=3, device=dev, precision=args.precision))
     owners = fb.ferret.stage_owners(P, world)
     tr.set_shard(rank, world, owners)
-    tr.load_stream(feats, labels)
+    if args.mode != "ingest":
+        tr.load_stream(feats, labels)
     tr.set_schedule(sched.events, chunk)
 
     def gather(b):
@@ -69,14 +73,18 @@ def main():
         return out
 
     tr.connect(gather)
-    logs = []
-    for c in range(args.chunks):
-        tr.execute(c)
+    if args.mode == "ingest":
+        log = tr.ingest(feats, labels)
+        logs = [log]
+    else:
+        for c in range(args.chunks):
+            tr.execute(c)
+            if args.mode == "barrier":
+                tr.sync()
+                dist.barrier()
         tr.sync()
-        dist.barrier()  # no rank starts chunk c+1 before every rank finished chunk c
-        if owners[-1] == rank:
-            logs.append(tr.fetch_log(c))
-    res = {"params": tr.params(), "owners": owners, "stats": tr.stats()}
+        logs = [tr.fetch_log(c) for c in range(args.chunks)] if owners[-1] == rank else []
+    res = {"params": tr.params(), "owners": owners, "stats": tr.stats(), "mode": args.mode}
     if owners[-1] == rank:
         res["log"] = np.concatenate(logs)
     if rank == 0:

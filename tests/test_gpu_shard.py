@@ -45,25 +45,32 @@ def _offsets(widths):
     return o
 
 
-@pytest.mark.parametrize("bounds,replay,precision", [("0,1,2,3,4", 1, "fp32"), ("0,2,4", 0, "fp32"),
-                                                     ("0,1,2,3,4", 1, "bf16")])
-def test_two_rank_stage_shard_matches_single_process(gpu, fb, tmp_path, monkeypatch, bounds, replay, precision):
+# mode: barrier = host sync + dist.barrier between chunks; free = execute() chunk after chunk with
+# no host synchronisation (the device acks of send_kernel / recv_kernel are the only flow
+# control); ingest = one ingest() call over every chunk from host memory
+@pytest.mark.parametrize("bounds,replay,precision,mode,world",
+                         [("0,1,2,3,4", 1, "fp32", "barrier", 2), ("0,2,4", 0, "fp32", "free", 2),
+                          ("0,1,2,3,4", 1, "bf16", "free", 2), ("0,1,2,3,4", 1, "fp32", "ingest", 2),
+                          ("0,1,2,3,4", 1, "fp32", "free", 4)])
+def test_stage_shard_matches_single_process(gpu, fb, tmp_path, monkeypatch, bounds, replay, precision, mode, world):
     import torch
 
     monkeypatch.setenv("FERRET_MMA_MIN_PARAMS", "0")  # bf16: every layer on the tensor cores
-    widths, units, chunks, B, policy = [96, 128, 64, 48, 10], 40, 2, 4, "iter_fisher"
+    widths, units, B, policy = [96, 128, 64, 48, 10], 40, 4, "iter_fisher"
+    chunks = 2 if mode == "barrier" else 4
     if precision == "bf16":
         widths = [512, 256, 256, 128, 16]  # 16-byte rows in bf16 for every layer
     b = [int(x) for x in bounds.split(",")]
     ref = _single(fb, widths, b, units, chunks, B, policy, bool(replay), precision)
-    dev = [] if torch.cuda.device_count() >= 2 else ["--device", "0"]
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr=127.0.0.1",
-           "--master-port=29533", os.path.join(ROOT, "tests", "shard_worker.py"), "--out", str(tmp_path),
-           "--widths", ",".join(map(str, widths)), "--bounds", bounds, "--units", str(units), "--chunks", str(chunks),
-           "--micro-batch", str(B), "--policy", policy, "--replay", str(replay), "--precision", precision] + dev
+    dev = [] if torch.cuda.device_count() >= world else ["--device", "0"]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "tests", "shard_worker.py"),
+           "--out", str(tmp_path), "--widths", ",".join(map(str, widths)), "--bounds", bounds, "--units", str(units),
+           "--chunks", str(chunks), "--micro-batch", str(B), "--policy", policy, "--replay", str(replay),
+           "--precision", precision, "--mode", mode] + dev
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env={**os.environ, "PYTHONPATH": ROOT})
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
-    ranks = [pickle.load(open(tmp_path / f"rank{k}.pkl", "rb")) for k in range(2)]
+    ranks = [pickle.load(open(tmp_path / f"rank{k}.pkl", "rb")) for k in range(world)]
     owners = ranks[0]["owners"]
     off = _offsets(widths)
     merged = np.empty_like(ref["params"])
@@ -77,8 +84,9 @@ def test_two_rank_stage_shard_matches_single_process(gpu, fb, tmp_path, monkeypa
     c0, m0, s0 = ranks[0]["normalizer"]
     assert c0 == ref["normalizer"][0]
     np.testing.assert_array_equal(m0, ref["normalizer"][1])
-    # both ranks really did work: each launched kernels for its stages
+    # every rank really did work: each launched kernels for its stages
     assert all(rk["stats"]["kernel_launches"] > 0 for rk in ranks)
+    assert all(rk["mode"] == mode for rk in ranks)
 
 
 def test_two_rank_stage_shard_conv_net(gpu, fb, tmp_path):

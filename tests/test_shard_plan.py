@@ -109,3 +109,85 @@ def test_plan_only_trainer_refuses_device_work(fb):
     with pytest.raises(fb.DeviceError):
         tr.load_stream(np.zeros((4, WIDTHS[0])), np.zeros(4, dtype=np.uint64))
     tr.close()
+
+
+# ---- world sizes 4 and 8 (one stage per rank at 8): C4's deep MLP, 8 one-layer stages
+DEEP = [784] + [256] * 7 + [10]
+DEEP_BOUNDS = list(range(9))
+
+
+def _deep_worker(rank, world, port, owners, out):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2503_12053_b200 as fb
+
+    prof = fb.profile_from_widths(DEEP)
+    t_d = float(prof["t_f"].max())
+    sched = fb.Schedule.forced(prof, t_d, fb.StreamSpec(t_d=t_d, horizon=UNITS * t_d), DEEP_BOUNDS, UNITS)
+    tr = fb.PipelineTrainer(DEEP, None, DEEP_BOUNDS,
+                            fb.PipelineTrainOptions(policy="iter_fisher", micro_batch=B, replay=True, device=-1))
+    tr.set_shard(rank, world, owners)
+    tr.set_schedule(sched.events, UNITS * B)
+    plan = tr.handoff_plan()
+    mine = [int(x) for x in plan[0]] + [int(x) for x in plan[1]]
+    allp = [None] * world
+    dist.all_gather_object(allp, mine)
+    out[rank] = allp
+    tr.close()
+    dist.destroy_process_group()
+
+
+def _expected_general(fb, owners, world):
+    """Messages per destination rank per chunk, counted from the event log: across every
+    rank boundary j | j+1, one per predict sweep, stage-j forward and replay forward sweep
+    (to owner[j+1]); one per stage-(j+1) backward whose unit runs stage j's backward and
+    per replay backward sweep (to owner[j])."""
+    prof = fb.profile_from_widths(DEEP)
+    t_d = float(prof["t_f"].max())
+    ev = fb.Schedule.forced(prof, t_d, fb.StreamSpec(t_d=t_d, horizon=UNITS * t_d), DEEP_BOUNDS, UNITS).events
+    dropped = set(ev["item"][ev["kind"] == 1].tolist())
+    has_bwd = {(int(e["item"]), int(e["stage"])) for e in ev if e["kind"] == 4}
+    P = len(owners)
+    cuts = [j for j in range(P - 1) if owners[j] != owners[j + 1]]
+    to = [0] * world
+    pending = {}
+    for e in ev:
+        k, u, j = int(e["kind"]), int(e["item"]), int(e["stage"])
+        if k == 0 and u not in dropped:
+            for c in cuts:
+                to[owners[c + 1]] += 1
+        elif k == 2 and j in cuts:
+            to[owners[j + 1]] += 1
+        elif k == 4:
+            pending.setdefault((int(e["worker"]), j), []).append(u)
+            if j - 1 in cuts and (u, j - 1) in has_bwd:
+                to[owners[j - 1]] += 1
+        elif k == 5 and pending.get((int(e["worker"]), j)):
+            pending[(int(e["worker"]), j)] = []
+            if j == 0:
+                for c in cuts:
+                    to[owners[c + 1]] += 1
+                    to[owners[c]] += 1
+    return to
+
+
+@pytest.mark.parametrize("world", [4, 8])
+def test_ranks_agree_on_handoff_plan_wide(fb, world):
+    """World sizes 4 and 8 over gloo: every rank computes every rank's message plan
+    identically (senders address receivers' inboxes and acks from it), and the per-rank
+    message counts equal the independent count from the event log."""
+    owners = fb.ferret.stage_owners(len(DEEP_BOUNDS) - 1, world)
+    assert sorted(set(owners)) == list(range(world))
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.start_processes(_deep_worker, args=(world, _free_port(), owners, out), nprocs=world, join=True,
+                       start_method="spawn")
+    plans = [out[r] for r in range(world)]
+    for r in range(1, world):
+        assert plans[r] == plans[0]
+    msgs_to = plans[0][0][world:]
+    assert msgs_to == _expected_general(fb, owners, world)
+    assert all(m > 0 for m in msgs_to)
