@@ -346,29 +346,36 @@ __global__ void __launch_bounds__(kMmaThreads, 1) mma_layer_kernel(const __grid_
 }
 
 // ---------------------------------------------------------------------------
-// mma_split_kernel: the fp32 parity mode's dense layer (3xTF32, see tf32_hi) with
-// the B operand staged per ring stage instead of for the CTA's whole K range up
-// front. A ring stage holds the TMA'd A tile (16 KB, hi implicit: kind::tf32 drops
-// the low mantissa bits), its lo part (16 KB) and the unit's B atom as hi + lo
-// (2 + 2 KB): 36 KB, so two CTAs per SM keep 3 stages each in flight (the
-// whole-K B staging of mma_layer_kernel<4, *, true> left room for 2 stages of one
-// CTA: 1.5 TB/s on config 5's 4096 x 4096 layers). Roles:
+// mma_ring_kernel: the dense layer with the B operand staged per ring stage
+// instead of for the CTA's whole K range up front (mma_layer_kernel), so the
+// first MMA waits for one A tile, not for the whole B slice, and the ring is as
+// deep as the A stream needs. A ring stage holds the TMA'd A tile (16 KB) and the
+// unit's B atom (2 KB); in the fp32 parity mode (SPLIT, 3xTF32, see tf32_hi) also
+// the A tile's lo part (16 KB, hi stays implicit: kind::tf32 drops the low
+// mantissa bits) and B as hi + lo: 36 KB. Two CTAs per SM. Roles:
 //   warp 0 / lane 0  TMA producer: A tile of stage s once the MMA freed it (empty[s])
-//   warp 1 / lane 0  MMA issuer: 4 k-steps x 3 MMAs (hi.hi, hi.lo, lo.hi) per stage,
-//                    tcgen05.commit -> empty[s]
+//   warp 1 / lane 0  MMA issuer: per stage KA/UK k-steps x (1, or 3 for SPLIT:
+//                    hi.hi, hi.lo, lo.hi) MMAs, tcgen05.commit -> empty[s]
 //   warps 2-9        stagers: load the unit's B atom i (L2) before waiting for the
-//                    A tile, then split A (lo) and B (hi, lo) into the stage and
-//                    publish it on lready[s]; warps 2-5 then run the epilogue
+//                    A tile, convert / split it into the stage (and split A for
+//                    SPLIT), publish the stage on lready[s]; warps 2-5 then run the
+//                    epilogue
+// (the whole-K B staging left the fp32 parity mode room for 2 stages of one CTA:
+// 1.5 TB/s on config 5's 4096 x 4096 layers; this kernel: 2.5 TB/s forward)
 // ---------------------------------------------------------------------------
-constexpr int kSplitStageBytes = 2 * kTileBytes + 2 * kBAtomBytes;
+template <int ES, bool SPLIT>
+__host__ __device__ constexpr int ring_stage_bytes() { return (SPLIT ? 2 : 1) * (kTileBytes + kBAtomBytes); }
 
-template <bool BWD>
-__global__ void __launch_bounds__(kMmaThreads, 2) mma_split_kernel(const __grid_constant__ MmaArgs a) {
-    constexpr int KA = 32, UK = 8;  // fp32: 32 K elements per 128-byte atom, 8 per tcgen05.mma (kind::tf32)
+template <int ES, bool BWD, bool SPLIT>
+__global__ void __launch_bounds__(kMmaThreads, 2) mma_ring_kernel(const __grid_constant__ MmaArgs a) {
+    constexpr int KA = 128 / ES, UK = 32 / ES;  // K elements per 128-byte atom / per tcgen05.mma
+    constexpr bool TF32 = ES == 4;
+    constexpr int SB = ring_stage_bytes<ES, SPLIT>();
+    constexpr int BOFF = (SPLIT ? 2 : 1) * kTileBytes;  // B hi inside a stage (B lo follows)
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int nst = a.stages;
-    auto stage = [&](int s) { return base + static_cast<size_t>(s) * kSplitStageBytes; };
+    auto stage = [&](int s) { return base + static_cast<size_t>(s) * SB; };
     uint64_t* full = reinterpret_cast<uint64_t*>(stage(nst));
     uint64_t* empty = full + nst;
     uint64_t* lready = empty + nst;
@@ -409,78 +416,114 @@ __global__ void __launch_bounds__(kMmaThreads, 2) mma_split_kernel(const __grid_
             unsigned char* dst = stage(s);
             const int kk = (a_lo + i) * KA;
             if (!BWD) {
-                tma_load_2d(dst, &a.tmap, full + s, kk, m0);
+                tma_load_2d(dst, &a.tmap, full + s, kk, m0);  // {K inner, M rows}: 128 rows x 128 bytes
             } else {
 #pragma unroll
-                for (int c = 0; c < 128 / KA; ++c) tma_load_2d(dst + c * KA * 128, &a.tmap, full + s, m0 + c * KA, kk);
+                for (int c = 0; c < 128 / KA; ++c)  // {M inner, K rows}: (128/KA) boxes of KA rows x 128 bytes
+                    tma_load_2d(dst + c * KA * 128, &a.tmap, full + s, m0 + c * KA, kk);
             }
         }
     } else if (warp == 1 && lane == 0 && na > 0) {
-        // D f32, A/B tf32, A K-major (forward) or MN-major (backward), N = 16, M = 128
-        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((BWD ? 1u : 0u) << 15) | ((16u >> 3) << 17) |
+        // D f32, A/B tf32 (2) or bf16 (1), A K-major (forward) or MN-major (backward), N = 16, M = 128
+        const uint32_t fmt = TF32 ? 2u : 1u;
+        const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((BWD ? 1u : 0u) << 15) | ((16u >> 3) << 17) |
                                ((128u >> 4) << 24);
         for (int i = 0; i < na; ++i) {
             const int s = i % nst;
             mbar_wait(lready + s, (i / nst) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t ah = smem_u32(stage(s)), al = ah + kTileBytes;
-            const uint32_t bh = al + kTileBytes, bl = bh + kBAtomBytes;
+            const uint32_t ah = smem_u32(stage(s)), bh = ah + BOFF;
 #pragma unroll
             for (int k = 0; k < KA / UK; ++k) {
-                const uint64_t adh = BWD ? smem_desc(ah + k * UK * 128, KA * 128, 512, 1) : smem_desc(ah + k * 32, 16, 1024);
-                const uint64_t adl = BWD ? smem_desc(al + k * UK * 128, KA * 128, 512, 1) : smem_desc(al + k * 32, 16, 1024);
+                // K-major A: advance 32 bytes inside the swizzled row; SBO = 8 rows x 128 B.
+                // MN-major A: K step = UK rows of 128 B; LBO = the next 128-byte column of M
+                // (KA rows down); SBO = the next group of 8 K rows (bf16, 16-byte swizzle
+                // atoms) or of 4 K rows (tf32, 32-byte swizzle atoms).
+                auto adesc = [&](uint32_t at) {
+                    return BWD ? (TF32 ? smem_desc(at + k * UK * 128, KA * 128, 512, 1)
+                                       : smem_desc(at + k * UK * 128, KA * 128, 1024))
+                               : smem_desc(at + k * 32, 16, 1024);
+                };
                 const uint64_t bdh = smem_desc(bh + k * 32, 16, 1024);
-                const uint64_t bdl = smem_desc(bl + k * 32, 16, 1024);
-                umma(tmem, adh, bdh, idesc, (i > 0 || k > 0) ? 1u : 0u, true);
-                umma(tmem, adh, bdl, idesc, 1u, true);
-                umma(tmem, adl, bdh, idesc, 1u, true);
+                umma(tmem, adesc(ah), bdh, idesc, (i > 0 || k > 0) ? 1u : 0u, TF32);
+                if constexpr (SPLIT) {
+                    const uint64_t bdl = smem_desc(bh + kBAtomBytes + k * 32, 16, 1024);
+                    umma(tmem, adesc(ah), bdl, idesc, 1u, true);
+                    umma(tmem, adesc(ah + kTileBytes), bdh, idesc, 1u, true);
+                }
             }
             umma_commit(empty + s);
         }
         umma_commit(done);
     } else if (warp >= 2) {
-        // B atom: 16 rows x 32 floats; thread t < 128 owns 16-byte chunk j = t % 8 of row
-        // n = t / 8 (swizzled to (n/8)*1024 + (n%8)*128 + ((j ^ n%8) * 16)); the A tile's
-        // 1024 float4 are split by all 256 stagers
+        // B atom: 16 rows x 128 bytes; thread t < 128 owns 16-byte chunk j = t % 8 of row
+        // n = t / 8 (swizzled to (n/8)*1024 + (n%8)*128 + ((j ^ n%8) * 16)), i.e. CE = 16/ES
+        // consecutive K elements; for SPLIT the A tile's 1024 float4 are split by all 256
+        constexpr int CE = 16 / ES;
         const int t = threadIdx.x - 64, j = t & 7, n = t >> 3;
         const bool bthr = t < 128, rowv = bthr && n < a.N;
         const float* rowp = rowv ? a.X + static_cast<size_t>(a.xidx ? __ldg(a.xidx + n) : n) * a.ldx : a.X;
         const int boff = (n >> 3) * 1024 + (n & 7) * 128 + ((j ^ (n & 7)) << 4);
+        struct BV {
+            float v[CE];
+        };
         auto load_b = [&](int i) {
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            const int k0 = (a_lo + i) * KA + j * 4;
+            BV r;
+#pragma unroll
+            for (int e = 0; e < CE; ++e) r.v[e] = 0.f;
+            const int k0 = (a_lo + i) * KA + j * CE;
             if (rowv && i < na) {
                 const float* src = rowp + k0;
-                if (a.vec && k0 + 4 <= a.K) {
-                    v = __ldg(reinterpret_cast<const float4*>(src));
+                if (a.vec && k0 + CE <= a.K) {
+#pragma unroll
+                    for (int c = 0; c < CE / 4; ++c) {
+                        const float4 x4 = __ldg(reinterpret_cast<const float4*>(src) + c);
+                        r.v[4 * c] = x4.x; r.v[4 * c + 1] = x4.y; r.v[4 * c + 2] = x4.z; r.v[4 * c + 3] = x4.w;
+                    }
                 } else {
-                    v.x = k0 < a.K ? __ldg(src) : 0.f;
-                    v.y = k0 + 1 < a.K ? __ldg(src + 1) : 0.f;
-                    v.z = k0 + 2 < a.K ? __ldg(src + 2) : 0.f;
-                    v.w = k0 + 3 < a.K ? __ldg(src + 3) : 0.f;
+#pragma unroll
+                    for (int e = 0; e < CE; ++e) r.v[e] = k0 + e < a.K ? __ldg(src + e) : 0.f;
                 }
             }
-            return v;
+            return r;
         };
-        float4 bnext = load_b(0);
+        BV bnext = load_b(0);
         for (int i = 0; i < na; ++i) {
             const int s = i % nst;
-            const float4 bv = bnext;
-            bnext = load_b(i + 1);  // next atom's B in flight while this stage is split
+            const BV bv = bnext;
+            bnext = load_b(i + 1);  // the next atom's B is in flight while this stage is prepared
             mbar_wait(full + s, (i / nst) & 1);
             unsigned char* st = stage(s);
-            const float4* A4 = reinterpret_cast<const float4*>(st);
-            float4* L4 = reinterpret_cast<float4*>(st + kTileBytes);
+            if constexpr (SPLIT) {
+                const float4* A4 = reinterpret_cast<const float4*>(st);
+                float4* L4 = reinterpret_cast<float4*>(st + kTileBytes);
 #pragma unroll
-            for (int e = t; e < kTileBytes / 16; e += kStagers) {
-                const float4 x = A4[e];
-                L4[e] = make_float4(x.x - tf32_hi(x.x), x.y - tf32_hi(x.y), x.z - tf32_hi(x.z), x.w - tf32_hi(x.w));
+                for (int e = t; e < kTileBytes / 16; e += kStagers) {
+                    const float4 x = A4[e];
+                    L4[e] = make_float4(x.x - tf32_hi(x.x), x.y - tf32_hi(x.y), x.z - tf32_hi(x.z), x.w - tf32_hi(x.w));
+                }
             }
             if (bthr) {  // rows n >= N stay stale: D column n reads B row n only, never stored
-                const float4 hi = make_float4(tf32_hi(bv.x), tf32_hi(bv.y), tf32_hi(bv.z), tf32_hi(bv.w));
-                *reinterpret_cast<float4*>(st + 2 * kTileBytes + boff) = hi;
-                *reinterpret_cast<float4*>(st + 2 * kTileBytes + kBAtomBytes + boff) =
-                    make_float4(bv.x - hi.x, bv.y - hi.y, bv.z - hi.z, bv.w - hi.w);
+                unsigned char* dst = st + BOFF + boff;
+                if constexpr (ES == 4) {
+                    if constexpr (SPLIT) {
+                        const float4 hi = make_float4(tf32_hi(bv.v[0]), tf32_hi(bv.v[1]), tf32_hi(bv.v[2]), tf32_hi(bv.v[3]));
+                        *reinterpret_cast<float4*>(dst) = hi;
+                        *reinterpret_cast<float4*>(dst + kBAtomBytes) =
+                            make_float4(bv.v[0] - hi.x, bv.v[1] - hi.y, bv.v[2] - hi.z, bv.v[3] - hi.w);
+                    } else {
+                        *reinterpret_cast<float4*>(dst) = make_float4(bv.v[0], bv.v[1], bv.v[2], bv.v[3]);
+                    }
+                } else {
+                    uint4 p;
+                    __nv_bfloat162 h0 = __floats2bfloat162_rn(bv.v[0], bv.v[1]), h1 = __floats2bfloat162_rn(bv.v[2], bv.v[3]);
+                    __nv_bfloat162 h2 = __floats2bfloat162_rn(bv.v[4], bv.v[5]), h3 = __floats2bfloat162_rn(bv.v[6], bv.v[7]);
+                    p.x = *reinterpret_cast<uint32_t*>(&h0);
+                    p.y = *reinterpret_cast<uint32_t*>(&h1);
+                    p.z = *reinterpret_cast<uint32_t*>(&h2);
+                    p.w = *reinterpret_cast<uint32_t*>(&h3);
+                    *reinterpret_cast<uint4*>(dst) = p;
+                }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(lready + s)) : "memory");
@@ -521,15 +564,21 @@ const void* mma_func(size_t smem) {
     return f;
 }
 
-template <bool BWD>
-const void* split_func(size_t smem) {
+template <int ES, bool BWD, bool SPLIT>
+const void* ring_func(size_t smem) {
     static size_t configured = 0;
-    const void* f = reinterpret_cast<const void*>(&mma_split_kernel<BWD>);
+    const void* f = reinterpret_cast<const void*>(&mma_ring_kernel<ES, BWD, SPLIT>);
     if (smem > configured) {
         cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         configured = smem;
     }
     return f;
+}
+
+// mma_ring_kernel unless FERRET_MMA_WHOLE_B=1 (A/B knob: mma_layer_kernel, B staged for the whole K range)
+bool ring_b() {
+    static const bool on = !std::getenv("FERRET_MMA_WHOLE_B") || std::atoi(std::getenv("FERRET_MMA_WHOLE_B")) == 0;
+    return on;
 }
 
 }  // namespace
@@ -542,12 +591,13 @@ bool mma_supported(bool bf16, int in, int out) {
 
 MmaGeom mma_geom(bool bf16, bool bwd, int in, int out, bool split) {
     const int es = bf16 ? 2 : 4;
-    if (split && !bf16 && !std::getenv("FERRET_MMA_SPLIT_WHOLE_B")) {
-        // mma_split_kernel: two CTAs per SM, 36 KB ring stages (A hi, A lo, B hi, B lo)
+    if (ring_b()) {
+        // mma_ring_kernel: two CTAs per SM, ring stages of A (+ A lo) and one B atom (hi, lo)
+        const int sb = split ? ring_stage_bytes<4, true>() : ring_stage_bytes<4, false>();
         MmaGeom g{};
         const int M = bwd ? in : out, K = bwd ? out : in;
         g.mtiles = (M + 127) / 128;
-        g.katoms = static_cast<int>((static_cast<long long>(K) * 4 + 127) / 128);
+        g.katoms = static_cast<int>((static_cast<long long>(K) * es + 127) / 128);
         int S = 2 * 148 / g.mtiles;
         if (S > 16) S = 16;
         if (S > g.katoms) S = g.katoms;
@@ -557,9 +607,10 @@ MmaGeom mma_geom(bool bf16, bool bwd, int in, int out, bool split) {
         g.S = (g.katoms + g.apc - 1) / g.apc;
         constexpr size_t kPerCta = 113 * 1024;  // two CTAs per SM (228 KB less the per-CTA reserve)
         const size_t fixed = 1024 + 4 * 16 * 8 + 16;
-        g.stages = static_cast<int>((kPerCta - fixed) / kSplitStageBytes);
+        g.stages = static_cast<int>((kPerCta - fixed) / static_cast<size_t>(sb));
         if (g.stages > g.apc) g.stages = g.apc;
-        g.smem = fixed + static_cast<size_t>(g.stages) * kSplitStageBytes;
+        if (g.stages > 16) g.stages = 16;
+        g.smem = fixed + static_cast<size_t>(g.stages) * static_cast<size_t>(sb);
         g.partial_floats = g.S > 1 ? static_cast<size_t>(g.mtiles) * g.S * 128 * 16 : 0;
         return g;
     }
@@ -630,11 +681,15 @@ void spec_mma(const MmaLayer& L, KernelSpec& k) {
         std::abort();
     }
     a.vec = (a.ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(L.X) & 15u) == 0);
-    const bool ring_b = split && !std::getenv("FERRET_MMA_SPLIT_WHOLE_B");
-    const void* f = es == 2 ? (L.bwd ? mma_func<2, true>(g.smem) : mma_func<2, false>(g.smem))
-                  : ring_b  ? (L.bwd ? split_func<true>(g.smem) : split_func<false>(g.smem))
-                  : split   ? (L.bwd ? mma_func<4, true, true>(g.smem) : mma_func<4, false, true>(g.smem))
-                            : (L.bwd ? mma_func<4, true>(g.smem) : mma_func<4, false>(g.smem));
+    const void* f;
+    if (ring_b())
+        f = es == 2 ? (L.bwd ? ring_func<2, true, false>(g.smem) : ring_func<2, false, false>(g.smem))
+          : split   ? (L.bwd ? ring_func<4, true, true>(g.smem) : ring_func<4, false, true>(g.smem))
+                    : (L.bwd ? ring_func<4, true, false>(g.smem) : ring_func<4, false, false>(g.smem));
+    else
+        f = es == 2 ? (L.bwd ? mma_func<2, true>(g.smem) : mma_func<2, false>(g.smem))
+          : split   ? (L.bwd ? mma_func<4, true, true>(g.smem) : mma_func<4, false, true>(g.smem))
+                    : (L.bwd ? mma_func<4, true>(g.smem) : mma_func<4, false>(g.smem));
     static_assert(sizeof(MmaArgs) <= sizeof(k.arg0), "kernel argument too large");
     k.func = f;
     k.grid = dim3(g.S, g.mtiles);
