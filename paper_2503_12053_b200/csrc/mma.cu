@@ -62,7 +62,9 @@ constexpr size_t kMaxSmem = 225 * 1024;  // opt-in dynamic shared memory per CTA
 // lanes of quadrant w % 4: thread = accumulator row m0 + row, 16 columns n), then bias +
 // ReLU (forward) or the ReLU mask (backward); with S > 1 K splits the partial tile goes
 // to L2 scratch and the last CTA of the M tile sums the S partials in split order.
-template <bool BWD>
+// STACK: the accumulator is two 16-column halves to add (3xTF32 with B hi / lo stacked as
+// one N = 32 operand: columns 0-15 = hi.hi + lo.hi, columns 16-31 = hi.lo).
+template <bool BWD, bool STACK = false>
 __device__ __forceinline__ void mma_epilogue(const MmaArgs& a, uint32_t tmem, uint64_t* done, bool any, int warp,
                                              int lane, int m0, int q, int S) {
     const int row = (warp & 3) * 32 + lane;
@@ -70,7 +72,14 @@ __device__ __forceinline__ void mma_epilogue(const MmaArgs& a, uint32_t tmem, ui
     if (any) {
         mbar_wait(done, 0);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        tmem_ld16(tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16), acc);
+        const uint32_t taddr = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+        tmem_ld16(taddr, acc);
+        if constexpr (STACK) {
+            float hl[16];
+            tmem_ld16(taddr + 16, hl);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc[i] += hl[i];
+        }
     } else {
 #pragma unroll
         for (int i = 0; i < 16; ++i) acc[i] = 0.f;
@@ -354,8 +363,8 @@ __global__ void __launch_bounds__(kMmaThreads, 1) mma_layer_kernel(const __grid_
 // the A tile's lo part (16 KB, hi stays implicit: kind::tf32 drops the low
 // mantissa bits) and B as hi + lo: 36 KB. Two CTAs per SM. Roles:
 //   warp 0 / lane 0  TMA producer: A tile of stage s once the MMA freed it (empty[s])
-//   warp 1 / lane 0  MMA issuer: per stage KA/UK k-steps x (1, or 3 for SPLIT:
-//                    hi.hi, hi.lo, lo.hi) MMAs, tcgen05.commit -> empty[s]
+//   warp 1 / lane 0  MMA issuer: per stage KA/UK k-steps x 1 MMA (SPLIT: 2, hi_A x
+//                    [B hi; B lo] as one N = 32 operand, then lo_A x B hi), commit -> empty[s]
 //   warps 2-9        stagers: load the unit's B atom i (L2) before waiting for the
 //                    A tile, convert / split it into the stage (and split A for
 //                    SPLIT), publish the stage on lready[s]; warps 2-5 then run the
@@ -388,6 +397,18 @@ __global__ void __launch_bounds__(kMmaThreads, 2) mma_ring_kernel(const __grid_c
     const int a_lo = q * a.atoms_per_cta;
     const int a_hi = min(a.katoms, a_lo + a.atoms_per_cta);
     const int na = max(0, a_hi - a_lo);
+    // optional phase timestamps (globaltimer ns) per CTA: 0 start, 1 setup done, 2 first A
+    // tile landed, 3 first MMA issued, 4 accumulator done, 5 exit, 6 last TMA issued,
+    // 7 epilogue done
+    unsigned long long* stamp = a.stamps ? a.stamps + (static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * 8 : nullptr;
+    auto tick = [&](int idx) {
+        if (stamp) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            stamp[idx] = t;
+        }
+    };
+    if (threadIdx.x == 0) tick(0);
 
     if (threadIdx.x == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.tmap)) : "memory");
@@ -407,6 +428,7 @@ __global__ void __launch_bounds__(kMmaThreads, 2) mma_ring_kernel(const __grid_c
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) tick(1);
 
     if (warp == 0 && lane == 0 && na > 0) {
         for (int i = 0; i < na; ++i) {
@@ -423,15 +445,20 @@ __global__ void __launch_bounds__(kMmaThreads, 2) mma_ring_kernel(const __grid_c
                     tma_load_2d(dst + c * KA * 128, &a.tmap, full + s, m0 + c * KA, kk);
             }
         }
+        tick(6);
     } else if (warp == 1 && lane == 0 && na > 0) {
         // D f32, A/B tf32 (2) or bf16 (1), A K-major (forward) or MN-major (backward), N = 16, M = 128
         const uint32_t fmt = TF32 ? 2u : 1u;
         const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((BWD ? 1u : 0u) << 15) | ((16u >> 3) << 17) |
                                ((128u >> 4) << 24);
+        // SPLIT: B hi (rows 0-15) and B lo (rows 16-31) are one N = 32 operand, so hi_A meets
+        // both in one MMA (A read once for hi.hi + hi.lo); lo.hi is an N = 16 MMA into columns 0-15
+        const uint32_t idesc32 = (idesc & ~(0x3Fu << 17)) | ((32u >> 3) << 17);
         for (int i = 0; i < na; ++i) {
             const int s = i % nst;
             mbar_wait(lready + s, (i / nst) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            if (i == 0) tick(3);
             const uint32_t ah = smem_u32(stage(s)), bh = ah + BOFF;
 #pragma unroll
             for (int k = 0; k < KA / UK; ++k) {
@@ -445,11 +472,11 @@ __global__ void __launch_bounds__(kMmaThreads, 2) mma_ring_kernel(const __grid_c
                                : smem_desc(at + k * 32, 16, 1024);
                 };
                 const uint64_t bdh = smem_desc(bh + k * 32, 16, 1024);
-                umma(tmem, adesc(ah), bdh, idesc, (i > 0 || k > 0) ? 1u : 0u, TF32);
                 if constexpr (SPLIT) {
-                    const uint64_t bdl = smem_desc(bh + kBAtomBytes + k * 32, 16, 1024);
-                    umma(tmem, adesc(ah), bdl, idesc, 1u, true);
+                    umma(tmem, adesc(ah), bdh, idesc32, (i > 0 || k > 0) ? 1u : 0u, true);
                     umma(tmem, adesc(ah + kTileBytes), bdh, idesc, 1u, true);
+                } else {
+                    umma(tmem, adesc(ah), bdh, idesc, (i > 0 || k > 0) ? 1u : 0u, TF32);
                 }
             }
             umma_commit(empty + s);
@@ -493,6 +520,7 @@ __global__ void __launch_bounds__(kMmaThreads, 2) mma_ring_kernel(const __grid_c
             const BV bv = bnext;
             bnext = load_b(i + 1);  // the next atom's B is in flight while this stage is prepared
             mbar_wait(full + s, (i / nst) & 1);
+            if (i == 0 && t == 0) tick(2);
             unsigned char* st = stage(s);
             if constexpr (SPLIT) {
                 const float4* A4 = reinterpret_cast<const float4*>(st);
@@ -530,10 +558,18 @@ __global__ void __launch_bounds__(kMmaThreads, 2) mma_ring_kernel(const __grid_c
         }
     }
     __syncwarp();
-    if (warp >= 2 && warp < 6) mma_epilogue<BWD>(a, tmem, done, na > 0, warp, lane, m0, q, S);
+    if (warp >= 2 && warp < 6) {
+        if (warp == 2 && lane == 0 && na > 0) {
+            mbar_wait(done, 0);
+            tick(4);
+        }
+        mma_epilogue<BWD, SPLIT>(a, tmem, done, na > 0, warp, lane, m0, q, S);
+        if (warp == 2 && lane == 0) tick(7);
+    }
 
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    if (threadIdx.x == 0) tick(5);
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem));

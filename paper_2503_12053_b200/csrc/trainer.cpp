@@ -3554,6 +3554,10 @@ ferret_status ferret_dense_layer(int32_t precision, int32_t direction, const flo
         }
         fb200::KernelSpec k;
         fb200::spec_mma(L, k);
+        if (stamp_file) {  // measurement: W cold in HBM like inside a chunk (the upload left it in L2)
+            void* flush = up(nullptr, 256u << 20);
+            cuda_check(cudaMemset(flush, 1, 256u << 20), "L2 flush");
+        }
         cuda_check(fb200::launch_spec(k, nullptr), "dense_layer launch");
         cuda_check(cudaDeviceSynchronize(), "dense_layer");
         if (stamp_file) {
@@ -3562,8 +3566,8 @@ ferret_status ferret_dense_layer(int32_t precision, int32_t direction, const flo
             if (FILE* f = std::fopen(stamp_file, "a")) {
                 std::fprintf(f, "layer %d %d %d %d %d\n", precision, direction, in, out, g.S * g.mtiles);
                 for (size_t i = 0; i < n_stamps; i += 8)
-                    std::fprintf(f, "%llu %llu %llu %llu %llu %llu\n", h[i], h[i + 1], h[i + 2], h[i + 3], h[i + 4],
-                                 h[i + 5]);
+                    std::fprintf(f, "%llu %llu %llu %llu %llu %llu %llu %llu\n", h[i], h[i + 1], h[i + 2], h[i + 3],
+                                 h[i + 4], h[i + 5], h[i + 6], h[i + 7]);
                 std::fclose(f);
             }
         }

@@ -14,7 +14,7 @@ rng = np.random.default_rng(0)
 W = rng.standard_normal((4096, 4096)).astype(np.float32)
 X = rng.standard_normal((16, 4096)).astype(np.float32)
 b = np.zeros(4096, np.float32)
-for prec in ("bf16", "tf32"):
+for prec in ("fp32", "bf16", "tf32"):
     for _ in range(reps):
         fb.dense_layer(prec, 0, W, X, bias=b, relu=True)
         fb.dense_layer(prec, 1, W, X)
