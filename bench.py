@@ -284,7 +284,8 @@ def config3_resnet(fb, torch, device):
 def config4_budget(fb, torch, device):
     from profiles.c4_budget import measure
 
-    return measure(fb, torch, device=device, steps=2)
+    return {"reference_planner": measure(fb, torch, device=device, steps=2),
+            "b200_planner": measure(fb, torch, device=device, steps=2, planner="b200")}
 
 
 def accuracy_vs_cpu(fb, device):

@@ -155,6 +155,7 @@ __device__ __forceinline__ void epilogue(const ConvArgs& a, int m, int n, float 
 
 template <int MODE>
 __global__ void __launch_bounds__(NT) conv_gemm_kernel(const ConvArgs a) {
+    FB_PDL_ENTRY();
     __shared__ __align__(16) float As[TK][TM];
     __shared__ __align__(16) float Bs[TK][TN];
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
@@ -232,6 +233,7 @@ __host__ __device__ inline bool warp_reduce(const ConvArgs& a) {
 }
 template <int MODE>
 __global__ void __launch_bounds__(NT) conv_reduce_kernel(const ConvArgs a) {
+    FB_PDL_ENTRY();
     const size_t mn = (size_t)a.M * a.N;
     if (warp_reduce(a)) {
         const int lane = threadIdx.x & 31;
@@ -259,6 +261,7 @@ __global__ void __launch_bounds__(NT) conv_reduce_kernel(const ConvArgs a) {
 // t, t + 256, ... of every sample in order, then a fixed butterfly + ordered warp sums
 // (deterministic). (gb = a.Y)
 __global__ void __launch_bounds__(NT) conv_bgrad_kernel(const ConvArgs a) {
+    FB_PDL_ENTRY();
     __shared__ float part[NT / 32];
     const int ch = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int hw = a.ho * a.wo;
@@ -286,6 +289,7 @@ __global__ void __launch_bounds__(NT) conv_bgrad_kernel(const ConvArgs a) {
 }
 
 __global__ void __launch_bounds__(NT) gap_kernel(const PoolMeanArgs a) {
+    FB_PDL_ENTRY();
     const int i = blockIdx.x * NT + threadIdx.x;
     if (i >= a.B * a.C) return;
     const int b = i / a.C, c = i - b * a.C;
@@ -296,6 +300,7 @@ __global__ void __launch_bounds__(NT) gap_kernel(const PoolMeanArgs a) {
 }
 
 __global__ void __launch_bounds__(NT) ungap_kernel(const PoolMeanArgs a) {
+    FB_PDL_ENTRY();
     const size_t n = (size_t)a.B * a.C * a.HW;
     for (size_t i = (size_t)blockIdx.x * NT + threadIdx.x; i < n; i += (size_t)gridDim.x * NT) {
         float v = __ldg(a.dY + i / a.HW) / (float)a.HW;
@@ -517,6 +522,7 @@ __device__ __forceinline__ void locate_b(const ConvArgs& a, const Col& c, int k0
 
 template <int MODE, int ES, bool SPLIT>
 __global__ void __launch_bounds__(kCT, SPLIT ? 1 : 2) conv_mma_kernel(const __grid_constant__ ConvArgs a) {
+    FB_PDL_ENTRY();
     constexpr int KA = 128 / ES;  // K elements per atom
     constexpr int UK = 32 / ES;   // K per MMA
     constexpr int CE = 16 / ES;   // elements per 16-byte chunk
@@ -803,6 +809,7 @@ const void* conv_mma_pick(int tc, size_t& smem) {
 // Wt[m][tap * C + c] = fwd: W[m][c][tap] (C = c_in); dgrad: W[c][m][tap] (C = c_out)
 template <int MODE>
 __global__ void __launch_bounds__(NT) conv_wprep_kernel(const ConvArgs a) {
+    FB_PDL_ENTRY();
     float* Wt = const_cast<float*>(a.Wt);
     const int kk = a.k * a.k;
     const int C = MODE == kConvFwd ? a.ci : a.co;

@@ -100,6 +100,7 @@ __device__ __forceinline__ void head_sample(const float* z, int n_out, int mode,
 // ---------------------------------------------------------------------------
 template <int BT, int RW, bool VEC>
 __global__ void __launch_bounds__(kThreads) fwd_kernel(const FwdArgs a, int nwk) {
+    FB_PDL_ENTRY();
     constexpr int NV = RW * BT;
     __shared__ float part[kWarps][NV];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -227,6 +228,7 @@ void fwd_spec(const FwdArgs& a, bool vec, KernelSpec& k) {
 // softmax head: one warp per sample.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads) head_kernel(const HeadArgs a) {
+    FB_PDL_ENTRY();
     const int lane = threadIdx.x & 31;
     const int b = blockIdx.x * kWarps + (threadIdx.x >> 5);
     if (b >= a.B) return;
@@ -252,6 +254,7 @@ constexpr int kBwdSmallRows = 256;
 
 template <int BT>
 __global__ void __launch_bounds__(kThreads) bwd_small_kernel(const BwdArgs a) {
+    FB_PDL_ENTRY();
     __shared__ __align__(16) float sd[kBwdSmallRows][BT];
     __shared__ float part[kWarps][BT][33];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -305,6 +308,7 @@ __global__ void __launch_bounds__(kThreads) bwd_small_kernel(const BwdArgs a) {
 
 template <int BT, int V>
 __global__ void __launch_bounds__(kThreads) bwd_kernel(const BwdArgs a) {
+    FB_PDL_ENTRY();
     // deltas as [row][sample]: one row's B values are read as float4s
     __shared__ __align__(16) float sd[kBwdMaxRows][BT];
     extern __shared__ float wpart[];  // [kWarps][BT][32 * V] per-warp partials (dynamic)
@@ -552,6 +556,7 @@ __device__ __forceinline__ float fold_iter_cached(float g, const float (&cv)[kRe
 // ---------------------------------------------------------------------------
 template <int POLICY, int BT>
 __global__ void __launch_bounds__(kThreads) update_tile_kernel(const UpdArgs a) {
+    FB_PDL_ENTRY();
     __shared__ float sdel[kMaxPending * kMaxBatch * kUpdMaxTileRows];
     const UpdTile t = a.tiles[blockIdx.x];
     const UpdSeg sg = a.segs[t.seg];
@@ -645,6 +650,7 @@ __global__ void __launch_bounds__(kThreads) update_tile_kernel(const UpdArgs a) 
 // ---------------------------------------------------------------------------
 template <int BT, int NV>
 __global__ void __launch_bounds__(kThreads) update_iter1_kernel(const UpdArgs a) {
+    FB_PDL_ENTRY();
     // Latency-shaped: after the one dependent load of the CTA's work record,
     // every load of the launch — the unit's deltas (to smem), its input values
     // of the thread's column, and the version chain + compensator state of the
@@ -773,6 +779,7 @@ __global__ void __launch_bounds__(kThreads) update_iter1_kernel(const UpdArgs a)
 // ---------------------------------------------------------------------------
 template <int BT, int NV>
 __global__ void __launch_bounds__(kThreads) update_iter1v4_kernel(const UpdArgs a) {
+    FB_PDL_ENTRY();
     constexpr int RB = NV <= 6 ? 2 : 1;  // rows whose chains are loaded before any arithmetic
     __shared__ float sdel[kMaxBatch * kUpdMaxTileRows];
     const UpdWork w = a.works4[blockIdx.x];
@@ -913,6 +920,7 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
 
 template <int BT>
 __global__ void __launch_bounds__(kThreads) update_stream_kernel(const UpdArgs a) {
+    FB_PDL_ENTRY();
     extern __shared__ __align__(128) float sbuf[];  // 2 buffers x (nv + 3) x 256 floats
     __shared__ float sdel[kMaxBatch * kUpdMaxTileRows];
     __shared__ __align__(8) uint64_t full[2];
@@ -1070,6 +1078,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 template <int CM, int BT>
 __global__ void __launch_bounds__(kThreads, CM <= 7 ? 2 : 1) update_group_kernel(const GroupArgs a) {
+    FB_PDL_ENTRY();
     __shared__ float sdel[kGroupMax * kMaxBatch * kGroupRows];
     extern __shared__ float xs[];  // [kGroupXBuf][BT][kThreads]: the unit inputs, column tid per thread
     const UpdWork w = a.works[blockIdx.x];
@@ -1259,6 +1268,7 @@ const void* update_func(int B) {
 // ---------------------------------------------------------------------------
 template <int POLICY>
 __global__ void __launch_bounds__(kThreads) compensate_kernel(const CompArgs a) {
+    FB_PDL_ENTRY();
     const long long stride = (long long)gridDim.x * blockDim.x;
     const bool learn = a.eta > 0.f && a.v_r != nullptr;
     const int last = a.chain_len - 1;
@@ -1286,6 +1296,7 @@ __global__ void __launch_bounds__(kThreads) compensate_kernel(const CompArgs a) 
 // separately rounded multiply/add (x86-64 SSE2, no FMA) bit for bit.
 // ---------------------------------------------------------------------------
 __global__ void normalize_kernel(const NormArgs a) {
+    FB_PDL_ENTRY();
     const int f = blockIdx.x * blockDim.x + threadIdx.x;
     if (f >= a.F) return;
     double mu = a.mean[f], m2 = a.m2[f];
@@ -1314,6 +1325,7 @@ __global__ void normalize_kernel(const NormArgs a) {
 // (mean_i, M2_i) alone. Phase 1 walks the recurrence per feature and records
 // (mean_i, M2_i); phase 2 standardises every (sample, feature) in parallel.
 __global__ void welford_kernel(const NormArgs a) {
+    FB_PDL_ENTRY();
     const int f = blockIdx.x * blockDim.x + threadIdx.x;
     if (f >= a.F) return;
     double mu = a.mean[f], m2 = a.m2[f];
@@ -1333,6 +1345,7 @@ __global__ void welford_kernel(const NormArgs a) {
 }
 
 __global__ void standardize_kernel(const NormArgs a) {
+    FB_PDL_ENTRY();
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= a.n * a.F) return;
     const long long i = t / a.F;
@@ -1345,6 +1358,7 @@ __global__ void standardize_kernel(const NormArgs a) {
 
 // Replay-pool insertion: one CTA per sample of the unit.
 __global__ void pool_kernel(const PoolArgs a) {
+    FB_PDL_ENTRY();
     const int b = blockIdx.x;
     const int dst = a.dst[b];
     if (dst < 0) return;
@@ -1375,6 +1389,7 @@ __device__ __forceinline__ bool wait_epoch(const unsigned* word, unsigned want, 
 }
 
 __global__ void __launch_bounds__(512) send_kernel(const SendArgs a) {
+    FB_PDL_ENTRY();
     if (a.ack) {
         __shared__ unsigned go;
         if (threadIdx.x == 0) go = wait_epoch(a.ack, *a.epoch - 1u, false, a.error);
@@ -1398,6 +1413,7 @@ __global__ void __launch_bounds__(512) send_kernel(const SendArgs a) {
 }
 
 __global__ void __launch_bounds__(512) recv_kernel(const RecvArgs a) {
+    FB_PDL_ENTRY();
     __shared__ unsigned ready;
     const unsigned e = *a.epoch;
     if (threadIdx.x == 0) ready = wait_epoch(a.flag, e, true, a.error);

@@ -212,6 +212,17 @@ struct PoolArgs {
 // system-scope release; the receiver spins on its flag with acquire loads and
 // copies the message into its stash (applying the ReLU mask of its own layer,
 // which the sender does not hold).
+// Programmatic dependent launch (graph edges of type Programmatic, trainer.cpp GraphBuilder):
+// every graph kernel first waits for its upstream kernels' completion and memory flush
+// (a no-op without a programmatic upstream), then lets its own dependents launch, so a
+// dependent's CTAs are resident and waiting when this kernel drains instead of paying the
+// launch latency after it.
+#define FB_PDL_ENTRY()                                                  \
+    do {                                                                \
+        asm volatile("griddepcontrol.wait;" ::: "memory");              \
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); \
+    } while (0)
+
 struct SendArgs {
     const float* src;
     float* dst;                // peer inbox

@@ -138,6 +138,7 @@ __device__ __forceinline__ void mma_epilogue(const MmaArgs& a, uint32_t tmem, ui
 
 template <int ES, bool BWD, bool SPLIT = false>
 __global__ void __launch_bounds__(kMmaThreads, 1) mma_layer_kernel(const __grid_constant__ MmaArgs a) {
+    FB_PDL_ENTRY();
     constexpr int KA = 128 / ES;       // K elements per 128-byte atom
     constexpr int UK = 32 / ES;        // K per tcgen05.mma (32 bytes of operand)
     constexpr bool TF32 = ES == 4;
@@ -377,6 +378,7 @@ __host__ __device__ constexpr int ring_stage_bytes() { return (SPLIT ? 2 : 1) * 
 
 template <int ES, bool BWD, bool SPLIT>
 __global__ void __launch_bounds__(kMmaThreads, 2) mma_ring_kernel(const __grid_constant__ MmaArgs a) {
+    FB_PDL_ENTRY();
     constexpr int KA = 128 / ES, UK = 32 / ES;  // K elements per 128-byte atom / per tcgen05.mma
     constexpr bool TF32 = ES == 4;
     constexpr int SB = ring_stage_bytes<ES, SPLIT>();

@@ -233,6 +233,10 @@ struct GraphBuilder {
 
     cudaGraph_t g = nullptr;
     bool serial = false;
+    // FERRET_PDL=1: kernel -> kernel edges programmatic (A/B knob). Off: measured C2 1.12M ->
+    // 0.85M samples/s (graph launch dearer, early-resident CTAs crowd the concurrent DAG),
+    // C5 and C3 neutral (profiles/r2/pdl_ab.txt)
+    bool pdl = std::getenv("FERRET_PDL") && std::atoi(std::getenv("FERRET_PDL")) != 0;
     cudaGraphNode_t last = nullptr;
     uint64_t kernels = 0;
     // Logical DAG (node index = creation order), kept in both modes: the
@@ -371,7 +375,12 @@ struct GraphBuilder {
         }
         check_before(reads, writes);
         const std::vector<int> ld = logical(reads, writes);
-        const std::vector<cudaGraphNode_t> d = deps(ld);
+        // kernel -> kernel edges are programmatic (every kernel starts with FB_PDL_ENTRY:
+        // griddepcontrol.wait, then launch_dependents), so this node's CTAs launch while its
+        // upstream kernels drain; edges from copies / events stay full dependencies
+        std::vector<int> normal, prog;
+        for (int x : ld) (pdl && !serial && funcs[static_cast<size_t>(x)] ? prog : normal).push_back(x);
+        const std::vector<cudaGraphNode_t> d = deps(normal);
         cudaKernelNodeParams p{};
         p.func = const_cast<void*>(k.func);
         p.gridDim = k.grid;
@@ -380,6 +389,12 @@ struct GraphBuilder {
         p.kernelParams = k.kernel_params();
         cudaGraphNode_t n;
         cuda_check(cudaGraphAddKernelNode(&n, g, d.data(), d.size(), &p), "cudaGraphAddKernelNode");
+        for (int x : prog) {
+            cudaGraphEdgeData e{};
+            e.from_port = cudaGraphKernelNodePortProgrammatic;
+            e.type = cudaGraphDependencyTypeProgrammatic;
+            cuda_check(cudaGraphAddDependencies_v2(g, &nodes[static_cast<size_t>(x)], &n, &e, 1), "programmatic edge");
+        }
         cur_func = k.func;
         // FERRET_NODE_PRIORITY=<class digits>: those node classes (1 predict, 2 forward,
         // 3 backward, 4 update) run at the device's highest kernel priority, so the
