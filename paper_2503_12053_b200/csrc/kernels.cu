@@ -518,6 +518,7 @@ __device__ __forceinline__ float compensate_elem(float g, const float* const* ve
 constexpr int kRegChain = 12;  // chain versions the iter_fisher fold keeps in registers
 // iter_fisher K = 1 chains longer than this take the smem-staged update_stream_kernel
 constexpr int kStreamMinChain = 16;
+constexpr int kStreamMinChainLarge = 4;  // the same for stages of >= 8 M parameters (HBM-bound)
 
 // iter_fisher (compensate.hpp:82-104) for one element with the chain values
 // already in registers: cv[i] = version i (i < last), th = version `last`.
@@ -1526,8 +1527,12 @@ void spec_update(const UpdArgs& a, KernelSpec& k) {
         fill(k, f, dim3((unsigned)blocks), dim3(kThreads), a);
         return;
     }
+    // Stages of >= 8 M parameters (chains of 32 MB versions, far beyond L2) stream every chain
+    // longer than 4 versions through smem: C5 fp32 3.51k -> 3.74k samples/s against the
+    // register-resident kernel up to 16 (profiles/r2/stream_chain_ab.txt); small L2-resident
+    // stages keep the latency-shaped register kernel up to 16 versions
     const char* env = std::getenv("FERRET_STREAM_MIN_CHAIN");
-    const int min_chain = env ? std::atoi(env) : kStreamMinChain;
+    const int min_chain = env ? std::atoi(env) : a.n_elems >= (8ll << 20) ? kStreamMinChainLarge : kStreamMinChain;
     if (!a.gmat && a.policy == 4 && a.K == 1 && a.nv > min_chain && a.lam_d != nullptr) {
         const size_t smem = sizeof(float) * 2 * (size_t)(a.nv + 3) * kUpdTileCols;
         const void* f = a.B <= 1 ? stream_func<1>(smem) : a.B <= 2 ? stream_func<2>(smem) : a.B <= 4 ? stream_func<4>(smem)

@@ -126,6 +126,7 @@ struct UpdArgs {
     int gmat;                // some segment reads a materialised gradient (UpdSeg::g_off)
     int pipe;                // update_iter1_kernel: double-buffered row batches (set by spec_update)
     long long n_items;
+    long long n_elems;       // parameters of the stage (chooses the HBM- or latency-shaped kernel)
     const UpdSeg* segs;      // device array
     const UpdTile* tiles;    // device array, one per CTA
     const UpdWork* works;    // the same tiles with their segment fields (one per CTA)

@@ -1817,6 +1817,7 @@ struct ferret_trainer {
         a.n_segs = s.n_segs;
         a.gmat = s.gmat ? 1 : 0;
         a.n_items = s.n_items;
+        a.n_elems = s.slot_floats;
         a.B = B;
         a.segs = s.segs_dev;
         a.tiles = s.tiles_dev;
