@@ -498,8 +498,10 @@ FERRET_API ferret_status ferret_apply_skip_policy(size_t n_items, double t_d, in
 
 /* ---------------- unit entry: the fused compensation kernel ---------------- */
 
-/* One Compensator::apply (learner.hpp:97-120) on the device, fp32:
- * chain = chain_len parameter versions oldest first (chain_len = tau + 1),
+/* One Compensator::apply (learner.hpp:97-120) on the device in fp64 with the reference's
+ * operation order (bit-identical to the reference's host arithmetic; the trainer's own fused
+ * update kernels compute in fp32): chain = chain_len parameter versions oldest first
+ * (chain_len = tau + 1, any length),
  * state arrays updated in place (lambda/v_r/v_a for iter_fisher, mean_gap for gap;
  * NULL where the policy has none). lambda0 is the fisher policy's fixed lambda. */
 FERRET_API ferret_status ferret_compensate(int32_t policy, const double* g, const double* const* chain,

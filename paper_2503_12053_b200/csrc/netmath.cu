@@ -173,4 +173,64 @@ cudaError_t nm_sgd(double* p, const double* g, size_t n, double lr, cudaStream_t
     return cudaGetLastError();
 }
 
+
+namespace {
+// Compensator::apply per element, the reference's fp64 expressions evaluated left to right
+// with separately rounded operations (bit-identical to the host build, which has no FMA):
+//   step   g * (1 / (1 + tau))                                    compensate.hpp:107-113
+//   gap    g / (1 + |now - read| / max(m, 1e-12)); m = 0.99 m + 0.01 |now - read|
+//                                                                 compensate.hpp:117-130, learner.hpp:104-111
+//   fisher g + lambda0 g g (now - read)                           compensate.hpp:42-51
+//   iter_fisher: the lambda / v_r / v_a step (eta > 0, >= 2 versions), then
+//          out += lambda out out (theta_{s+1} - theta_s) over the chain   compensate.hpp:82-104
+__global__ void compensate_f64_kernel(int policy, const double* __restrict__ g, const double* const* __restrict__ chain,
+                                      int chain_len, double* lambda, double* v_r, double* v_a, double* mean_gap,
+                                      size_t n, double lambda0, double alpha, double eta, double nu, double* out) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const double gi = g[i];
+    const double now = chain[chain_len - 1][i], read = chain[0][i];
+    const int tau = chain_len - 1;
+    double o = gi;
+    if (policy == 1) {
+        o = __dmul_rn(gi, __ddiv_rn(1.0, __dadd_rn(1.0, static_cast<double>(tau))));
+    } else if (policy == 2) {
+        const double m = mean_gap[i];
+        const double gap = fabs(__dsub_rn(now, read));
+        o = __ddiv_rn(gi, __dadd_rn(1.0, __ddiv_rn(gap, fmax(m, 1e-12))));
+        mean_gap[i] = __dadd_rn(__dmul_rn(0.99, m), __dmul_rn(0.01, gap));
+    } else if (policy == 3) {
+        o = __dadd_rn(gi, __dmul_rn(__dmul_rn(__dmul_rn(lambda0, gi), gi), __dsub_rn(now, read)));
+    } else if (policy == 4) {
+        double lam = lambda[i];
+        if (eta > 0.0 && chain_len >= 2 && v_r && v_a) {
+            const double one_m_a = __dsub_rn(1.0, alpha);
+            double vr = v_r[i], va = v_a[i];
+            const double dv_r = __dmul_rn(one_m_a, __dsub_rn(gi, vr));
+            const double resid = __dsub_rn(dv_r, __dmul_rn(lam, va));
+            const double grad_l = __dadd_rn(__dmul_rn(__dmul_rn(-2.0, resid), va), __dmul_rn(__dmul_rn(2.0, nu), lam));
+            lam = __dsub_rn(lam, __dmul_rn(eta, grad_l));
+            const double dtheta = __dsub_rn(chain[1][i], chain[0][i]);
+            vr = __dadd_rn(__dmul_rn(alpha, vr), __dmul_rn(one_m_a, gi));
+            va = __dadd_rn(__dmul_rn(alpha, va), __dmul_rn(__dmul_rn(__dmul_rn(one_m_a, gi), gi), dtheta));
+            lambda[i] = lam;
+            v_r[i] = vr;
+            v_a[i] = va;
+        }
+        for (int s = 0; s + 1 < chain_len; ++s)
+            o = __dadd_rn(o, __dmul_rn(__dmul_rn(__dmul_rn(lam, o), o), __dsub_rn(chain[s + 1][i], chain[s][i])));
+    }
+    out[i] = o;
+}
+}  // namespace
+
+cudaError_t nm_compensate(int policy, const double* g, const double* const* chain, int chain_len, double* lambda,
+                          double* v_r, double* v_a, double* mean_gap, size_t n, double lambda0, double alpha,
+                          double eta, double nu, double* out, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    compensate_f64_kernel<<<blocks(n), kT, 0, st>>>(policy, g, chain, chain_len, lambda, v_r, v_a, mean_gap, n,
+                                                     lambda0, alpha, eta, nu, out);
+    return cudaGetLastError();
+}
+
 }  // namespace fb200

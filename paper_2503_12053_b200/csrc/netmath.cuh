@@ -19,5 +19,10 @@ cudaError_t nm_wgrad(const double* delta, const double* X, long long ldx, double
                      int n, cudaStream_t st);
 cudaError_t nm_dgrad(const double* delta, const double* W, double* prev, int in, int out, int n, cudaStream_t st);
 cudaError_t nm_sgd(double* p, const double* g, size_t n, double lr, cudaStream_t st);
+// Compensator::apply (learner.hpp:97-120) in fp64: chain = chain_len device pointers (any
+// length), oldest first; state arrays updated in place (NULL where the policy has none)
+cudaError_t nm_compensate(int policy, const double* g, const double* const* chain, int chain_len, double* lambda,
+                          double* v_r, double* v_a, double* mean_gap, size_t n, double lambda0, double alpha,
+                          double eta, double nu, double* out, cudaStream_t st);
 
 }  // namespace fb200

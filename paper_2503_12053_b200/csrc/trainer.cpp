@@ -52,6 +52,7 @@
 #include "common.hpp"
 #include "ferret/rng.hpp"
 #include "kernels.cuh"
+#include "netmath.cuh"
 
 using fb200::fail;
 using fb200::guarded;
@@ -3684,58 +3685,51 @@ ferret_status ferret_compensate(int32_t policy, const double* g, const double* c
                                 double alpha, double eta_lambda, double nu, double* out) {
     return guarded([&] {
         if (chain_len < 1) fail(FERRET_E_INVALID_ARG, "compensate_iterative: empty version chain");
-        if (chain_len > fb200::kMaxVersions) fail(FERRET_E_INVALID_ARG, "compensate: chain longer than 64 versions");
         if (policy < 0 || policy > 4) fail(FERRET_E_CONFIG, "unknown compensation policy");
         if (policy == FERRET_POLICY_ITER_FISHER && !lambda) fail(FERRET_E_INVALID_ARG, "compensate: lambda required");
         if (policy == FERRET_POLICY_GAP && !mean_gap) fail(FERRET_E_INVALID_ARG, "compensate: mean_gap required");
         require_device(0);
+        // fp64 end to end (the reference's arithmetic): the state round-trips without
+        // rounding, and the chain is a device pointer table of any length
         size_t bytes = 0;
         const size_t nn = n ? n : 1;
-        std::vector<float*> bufs;
+        std::vector<void*> bufs;
         struct Cleanup {
-            std::vector<float*>& b;
+            std::vector<void*>& b;
             ~Cleanup() {
-                for (float* p : b) cudaFree(p);
+                for (void* p : b) cudaFree(p);
             }
         } cleanup{bufs};
         auto up = [&](const double* src) {
-            float* d = dalloc<float>(nn, bytes);
+            double* d = dalloc<double>(nn, bytes);
             bufs.push_back(d);
-            if (src) {
-                std::vector<float> h(src, src + n);
-                cuda_check(cudaMemcpy(d, h.data(), n * sizeof(float), cudaMemcpyHostToDevice), "H2D");
-            }
+            if (src && n) cuda_check(cudaMemcpy(d, src, n * sizeof(double), cudaMemcpyHostToDevice), "H2D");
             return d;
         };
-        auto down = [&](float* d, double* dst) {
-            std::vector<float> h(n);
-            cuda_check(cudaMemcpy(h.data(), d, n * sizeof(float), cudaMemcpyDeviceToHost), "D2H");
-            for (size_t i = 0; i < n; ++i) dst[i] = h[i];
+        auto down = [&](const double* d, double* dst) {
+            if (n) cuda_check(cudaMemcpy(dst, d, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
         };
-        fb200::CompArgs a{};
-        a.policy = policy;
-        a.g = up(g);
-        for (int32_t i = 0; i < chain_len; ++i) a.chain[i] = up(chain[i]);
-        a.chain_len = chain_len;
+        const double* dg = up(g);
+        std::vector<const double*> links(static_cast<size_t>(chain_len));
+        for (int32_t i = 0; i < chain_len; ++i) links[static_cast<size_t>(i)] = up(chain[i]);
+        const double** dchain = dalloc<const double*>(links.size(), bytes);
+        bufs.push_back(const_cast<double**>(dchain));
+        cuda_check(cudaMemcpy(dchain, links.data(), links.size() * sizeof(double*), cudaMemcpyHostToDevice), "H2D chain");
         const bool learn = policy == FERRET_POLICY_ITER_FISHER && v_r && v_a && eta_lambda > 0.0;
-        a.lambda = policy == FERRET_POLICY_ITER_FISHER ? up(lambda) : nullptr;
-        a.v_r = learn ? up(v_r) : nullptr;
-        a.v_a = learn ? up(v_a) : nullptr;
-        a.gap = policy == FERRET_POLICY_GAP ? up(mean_gap) : nullptr;
-        a.n = static_cast<long long>(n);
-        a.lambda0 = static_cast<float>(lambda0);
-        a.alpha = static_cast<float>(alpha);
-        a.eta = learn ? static_cast<float>(eta_lambda) : 0.f;
-        a.nu = static_cast<float>(nu);
-        a.out = up(nullptr);
-        if (n > 0) fb200::launch_compensate(a, nullptr);
-        cuda_check(cudaGetLastError(), "compensate launch");
+        double* dl = policy == FERRET_POLICY_ITER_FISHER ? up(lambda) : nullptr;
+        double* dvr = learn ? up(v_r) : nullptr;
+        double* dva = learn ? up(v_a) : nullptr;
+        double* dgap = policy == FERRET_POLICY_GAP ? up(mean_gap) : nullptr;
+        double* dout = up(nullptr);
+        cuda_check(fb200::nm_compensate(policy, dg, dchain, chain_len, dl, dvr, dva, dgap, n, lambda0, alpha,
+                                        learn ? eta_lambda : 0.0, nu, dout, nullptr),
+                   "compensate launch");
         cuda_check(cudaDeviceSynchronize(), "compensate");
-        down(a.out, out);
-        if (a.lambda) down(a.lambda, lambda);
-        if (a.v_r) down(a.v_r, v_r);
-        if (a.v_a) down(a.v_a, v_a);
-        if (a.gap) down(a.gap, mean_gap);
+        down(dout, out);
+        if (dl) down(dl, lambda);
+        if (dvr) down(dvr, v_r);
+        if (dva) down(dva, v_a);
+        if (dgap) down(dgap, mean_gap);
     });
 }
 

@@ -225,13 +225,33 @@ def test_compensate_unit(gpu, fb, orc, policy):
     ref = orc.compensate(policy, g, chain, **kw_ref)
     kw = dict(lam=lam.copy(), v_r=vr.copy(), v_a=va.copy(), mean_gap=gap.copy(), eta_lambda=1e-3)
     got = fb.compensate(policy, g, chain, **kw)
-    np.testing.assert_allclose(got, ref, rtol=2e-5, atol=1e-7)
+    # the unit entry computes in fp64 with the reference's operation order (no FMA): bit for bit
+    np.testing.assert_array_equal(got, ref)
     if policy == "gap":
-        np.testing.assert_allclose(kw["mean_gap"], kw_ref["mean_gap"], rtol=1e-5)
+        np.testing.assert_array_equal(kw["mean_gap"], kw_ref["mean_gap"])
     if policy == "iter_fisher":
-        # fp32 EMAs: a few ulp of the largest term (|v_r| ~ 1e-3, |v_a| ~ 1e-4)
-        np.testing.assert_allclose(kw["v_r"], kw_ref["v_r"], rtol=1e-4, atol=1e-8)
-        np.testing.assert_allclose(kw["v_a"], kw_ref["v_a"], rtol=1e-4, atol=1e-9)
+        for k in ("lam", "v_r", "v_a"):
+            np.testing.assert_array_equal(kw[k], kw_ref[k])
+
+
+@pytest.mark.parametrize("policy", ["gap", "iter_fisher"])
+def test_compensate_unit_repeated_long_chains(gpu, fb, orc, policy):
+    """The state carried across 20 calls (the drop-in Compensator::apply, learner.hpp:97-120)
+    does not drift from the reference's fp64 state, and chains far beyond the trainer's ring
+    (100 versions) are accepted like the reference accepts any tau."""
+    rng = np.random.default_rng(1)
+    n = 1031
+    kw = dict(lam=np.full(n, 0.2), v_r=np.zeros(n), v_a=np.zeros(n), mean_gap=np.zeros(n))
+    kw_ref = {k: v.copy() for k, v in kw.items()}
+    for call in range(20):
+        tau = 99 if call == 7 else int(rng.integers(0, 6))
+        g = rng.normal(size=n) * 0.1
+        chain = [rng.normal(size=n) * 0.05 for _ in range(tau + 1)]
+        ref = orc.compensate(policy, g, chain, eta=1e-3, **kw_ref)
+        got = fb.compensate(policy, g, chain, eta_lambda=1e-3, **kw)
+        np.testing.assert_array_equal(got, ref)
+    for k in kw:
+        np.testing.assert_array_equal(kw[k], kw_ref[k])
 
 
 def test_spec_kats_on_device(gpu, fb):
