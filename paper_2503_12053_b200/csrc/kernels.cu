@@ -651,7 +651,12 @@ __global__ void __launch_bounds__(kThreads) update_tile_kernel(const UpdArgs a) 
 // ---------------------------------------------------------------------------
 template <int BT, int NV>
 __global__ void __launch_bounds__(kThreads) update_iter1_kernel(const UpdArgs a) {
-    FB_PDL_ENTRY();
+    // Programmatic chain (trainer.cpp, FERRET_UPDATE_PDL): this launch may start while the
+    // previous update of the stage still runs. Everything that update does not write — the work
+    // record, the unit's deltas and inputs, versions 0 .. NV-2 of the chain — is loaded before
+    // griddepcontrol.wait; the newest version and the compensator state (its outputs) after it.
+    // launch_dependents follows the wait, so the next update of the stage launches only once
+    // this one's own predecessor has completed (its pre-wait reads then see finished versions).
     // Latency-shaped: after the one dependent load of the CTA's work record,
     // every load of the launch — the unit's deltas (to smem), its input values
     // of the thread's column, and the version chain + compensator state of the
@@ -686,13 +691,33 @@ __global__ void __launch_bounds__(kThreads) update_iter1_kernel(const UpdArgs a)
         vr = learn ? a.v_r[e] : 0.f;
         va = learn ? a.v_a[e] : 0.f;
     };
+    // the first batch: older versions before the dependency wait, the newest + state after it
+    auto load_old = [&](size_t e, float (&cv)[NV]) {
+#pragma unroll
+        for (int i = 0; i + 1 < NV; ++i) cv[i] = __ldg(a.vers[i] + e);
+    };
+    auto load_new = [&](size_t e, float (&cv)[NV], float& ld, float& vr, float& va) {
+        cv[NV - 1] = a.vers[NV - 1][e];  // (not __ldg: written by the upstream update)
+        ld = a.lam_d[e];
+        vr = learn ? a.v_r[e] : 0.f;
+        va = learn ? a.v_a[e] : 0.f;
+    };
+    auto dep_wait = [] {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    };
     const bool gm = w.g_off >= 0;  // materialised gradient (convolutions)
     if (w.bias) {
-        if (tid >= R) return;
+        if (tid >= R) {
+            dep_wait();
+            return;
+        }
         const int r = w.r0 + tid;
         const size_t e = (size_t)w.elem0 + r;
         float cv[NV], ld, vr, va;
-        load(e, cv, ld, vr, va);
+        load_old(e, cv);
+        dep_wait();
+        load_new(e, cv, ld, vr, va);
         float g = 0.f;
         if (gm) {
             g = __ldg(pk.stash + w.g_off + r);
@@ -710,7 +735,7 @@ __global__ void __launch_bounds__(kThreads) update_iter1_kernel(const UpdArgs a)
     float cv[RB][NV], ld[RB], vr[RB], va[RB];
 #pragma unroll
     for (int i = 0; i < RB; ++i)
-        if (live && i < R) load((size_t)w.elem0 + (size_t)(w.r0 + i) * w.in + c, cv[i], ld[i], vr[i], va[i]);
+        if (live && i < R) load_old((size_t)w.elem0 + (size_t)(w.r0 + i) * w.in + c, cv[i]);
     float xv[BT];
     if (!gm) {
         for (int i = tid; i < B * R; i += kThreads) {
@@ -725,6 +750,10 @@ __global__ void __launch_bounds__(kThreads) update_iter1_kernel(const UpdArgs a)
             xv[b] = (b < B && live) ? __ldg(xr + c) : 0.f;
         }
     }
+    dep_wait();
+#pragma unroll
+    for (int i = 0; i < RB; ++i)
+        if (live && i < R) load_new((size_t)w.elem0 + (size_t)(w.r0 + i) * w.in + c, cv[i], ld[i], vr[i], va[i]);
     __syncthreads();
     if (!live) return;
     auto grad = [&](int i) {
@@ -1556,6 +1585,7 @@ void spec_update(const UpdArgs& a, KernelSpec& k) {
         const void* f = a.B <= 1 ? iter1_func<1>(a.nv) : a.B <= 2 ? iter1_func<2>(a.nv) : a.B <= 4 ? iter1_func<4>(a.nv)
                       : a.B <= 8 ? iter1_func<8>(a.nv) : iter1_func<16>(a.nv);
         fill(k, f, dim3((unsigned)blocks), dim3(kThreads), b);
+        k.chain_pdl = true;
         return;
     }
     const void* f = a.policy == 0 ? update_func<0>(a.B) : a.policy == 1 ? update_func<1>(a.B)

@@ -253,6 +253,9 @@ struct KernelSpec {
     alignas(64) unsigned char arg0[2048];  // the kernel's struct argument
     int arg1 = 0;                         // optional trailing int argument
     int nargs = 1;
+    // the kernel splits its prologue around griddepcontrol.wait (update_iter1_kernel): it may
+    // be the programmatic dependent of the previous update of its stage (trainer.cpp)
+    bool chain_pdl = false;
     void* params[2];
     KernelSpec() = default;
     KernelSpec(const KernelSpec&) = delete;

@@ -238,6 +238,9 @@ struct GraphBuilder {
     // 0.85M samples/s (graph launch dearer, early-resident CTAs crowd the concurrent DAG),
     // C5 and C3 neutral (profiles/r2/pdl_ab.txt)
     bool pdl = std::getenv("FERRET_PDL") && std::atoi(std::getenv("FERRET_PDL")) != 0;
+    // the next kernel node's programmatic upstream when the kernel supports it (KernelSpec::chain_pdl):
+    // the previous update of the same stage (set by the trainer, consumed by kernel())
+    int pdl_pred = -1;
     cudaGraphNode_t last = nullptr;
     uint64_t kernels = 0;
     // Logical DAG (node index = creation order), kept in both modes: the
@@ -380,7 +383,10 @@ struct GraphBuilder {
         // griddepcontrol.wait, then launch_dependents), so this node's CTAs launch while its
         // upstream kernels drain; edges from copies / events stay full dependencies
         std::vector<int> normal, prog;
-        for (int x : ld) (pdl && !serial && funcs[static_cast<size_t>(x)] ? prog : normal).push_back(x);
+        const int chain_pred = k.chain_pdl && !serial ? pdl_pred : -1;
+        pdl_pred = -1;
+        for (int x : ld)
+            ((pdl && !serial && funcs[static_cast<size_t>(x)]) || x == chain_pred ? prog : normal).push_back(x);
         const std::vector<cudaGraphNode_t> d = deps(normal);
         cudaKernelNodeParams p{};
         p.func = const_cast<void*>(k.func);
@@ -1540,6 +1546,7 @@ struct ferret_trainer {
             std::vector<uint64_t> reads, writes;  // sorted, unique
         };
         std::vector<PGroup> groups(static_cast<size_t>(P));
+        std::vector<int> last_update_node(static_cast<size_t>(P), -1);  // graph node of stage j's last update
         const bool grouping = !DRY && group_updates && !timing && !as_shipped && opt.policy == FERRET_POLICY_ITER_FISHER;
         auto add_keys = [](std::vector<uint64_t>& v, std::initializer_list<uint64_t> ks) {
             v.insert(v.end(), ks.begin(), ks.end());
@@ -1746,7 +1753,9 @@ struct ferret_trainer {
                         gb->cur_bytes = update_bytes(j, opt.policy, reads, cur);
                         time_begin();
                         gb->cur_category = kCatUpdate; gb->cur_stage = j;
+                        if (update_pdl && !timing) gb->pdl_pred = last_update_node[static_cast<size_t>(j)];
                         gb->kernel(k, rk, {vslot(j, cur + 1), GB::key(GB::kState, static_cast<uint64_t>(j))});
+                        last_update_node[static_cast<size_t>(j)] = static_cast<int>(gb->nodes.size()) - 1;
                         wt_invalidate(stages[static_cast<size_t>(j)], a.dst);
                         time_end(update_bytes(j, opt.policy, reads, cur));
                     }
@@ -2810,6 +2819,11 @@ struct ferret_trainer {
     // kernel runs at 61 GB/s (15K-instruction body, one CTA per SM) and the step drops from
     // 3.2k to 0.77k samples/s; C2 from 1.12M to 0.45M (profiles/r2/ab_update_groups.txt)
     bool group_updates = std::getenv("FERRET_UPDATE_GROUPS") && std::atoi(std::getenv("FERRET_UPDATE_GROUPS")) != 0;
+    // Consecutive updates of a stage joined by programmatic edges (KernelSpec::chain_pdl kernels:
+    // the next update launches and loads its unit's inputs and older versions while the previous
+    // one drains): C2 1.10M -> 1.23M samples/s, its critical path being the stage-0 update chain
+    // (profiles/r2/update_pdl_ab.txt). FERRET_UPDATE_PDL=0: full dependencies (A/B knob)
+    bool update_pdl = !std::getenv("FERRET_UPDATE_PDL") || std::atoi(std::getenv("FERRET_UPDATE_PDL")) != 0;
     size_t n_group_nodes = 0;
     // algorithmic HBM bytes of one update group of stage j: the n0 chain versions read once,
     // lambda / v_r / v_a read and written once, G new versions written (+ their bf16 copies),
