@@ -662,7 +662,9 @@ __global__ void __launch_bounds__(kThreads) update_iter1_kernel(const UpdArgs a)
     // of the thread's column, and the version chain + compensator state of the
     // first RB rows — is issued before any arithmetic, so the kernel costs ~two
     // L2 round trips rather than one per row and stage of the address chain.
-    constexpr int RB = NV <= 8 ? 4 : 2;  // rows whose chains are held in registers at once
+    // rows whose chains are held in registers at once (4 rows up to 12 versions measured 20 %
+    // slower on C2: register pressure against the concurrent DAG, profiles/r2/update_rb_ab.txt)
+    constexpr int RB = NV <= 8 ? 4 : 2;
     __shared__ float sdel[kMaxBatch * kUpdMaxTileRows];
     const UpdWork w = a.works[blockIdx.x];
     const int B = a.B, R = w.nrows, tid = threadIdx.x;
