@@ -91,7 +91,7 @@ struct UpdSeg {
 // One CTA of the update kernel: `nrows` rows x 256 columns of a layer's
 // weights starting at (r0, c0), or 256 consecutive bias elements from r0.
 constexpr int kUpdTileCols = 256;
-constexpr int kUpdMaxTileRows = 8;
+constexpr int kUpdMaxTileRows = 16;
 struct UpdTile {
     int seg;    // index into the stage's segment table
     int r0;     // first row (weights) or first bias element
