@@ -319,7 +319,8 @@ __global__ void __launch_bounds__(NT) ungap_kernel(const PoolMeanArgs a) {
 // the MMAs (M 128, N 128, 4 per atom) and frees each stage with tcgen05.commit.
 // 3xTF32 (the fp32 parity mode) adds a tf32 lo tile per operand (lo = x - hi,
 // written by the thread that copied x; hi is the raw operand, which kind::tf32
-// truncates) and issues hi*hi + hi*lo + lo*hi. The epilogue reads TMEM
+// truncates; stage layout A, B, B lo, A lo) and issues hi_A x [hi_B; lo_B] as one
+// N = 256 MMA into 256 TMEM columns (halves summed in the epilogue) plus lo_A x hi_B. The epilogue reads TMEM
 // (tcgen05.ld), stages the tile through smem so global stores are coalesced along
 // pixels, then runs the SIMT kernel's epilogue (bias / shortcut / ReLU, skip /
 // mask) or writes the split-K partial (reduced in split order by conv_reduce_kernel).
@@ -563,7 +564,8 @@ __global__ void __launch_bounds__(kCT, SPLIT ? 1 : 2) conv_mma_kernel(const __gr
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(SPLIT ? 256 : 128));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -588,10 +590,15 @@ __global__ void __launch_bounds__(kCT, SPLIT ? 1 : 2) conv_mma_kernel(const __gr
                 for (int k = 0; k < KA / UK; ++k) {
                     const uint64_t ad = smem_desc(abase + k * 32, 16, 1024);
                     const uint64_t bd = smem_desc(bbase + k * 32, 16, 1024);
-                    umma(tmem, ad, bd, idesc, (i > 0 || k > 0) ? 1u : 0u, TF32);
-                    if constexpr (SPLIT) {  // + hi_A lo_B + lo_A hi_B
-                        umma(tmem, ad, smem_desc(bbase + 2 * kCTile + k * 32, 16, 1024), idesc, 1u, TF32);
-                        umma(tmem, smem_desc(abase + 2 * kCTile + k * 32, 16, 1024), bd, idesc, 1u, TF32);
+                    if constexpr (SPLIT) {
+                        // hi_A x [hi_B; lo_B]: B hi and B lo are one N = 256 operand (stage layout A, B,
+                        // B lo, A lo), accumulator columns 0-127 and 128-255 summed in the epilogue;
+                        // then + lo_A hi_B (N = 128): 8 MMAs per atom instead of 12
+                        const uint32_t idesc256 = (idesc & ~(0x3Fu << 17)) | ((256u >> 3) << 17);
+                        umma(tmem, ad, bd, idesc256, (i > 0 || k > 0) ? 1u : 0u, TF32);
+                        umma(tmem, smem_desc(abase + 3 * kCTile + k * 32, 16, 1024), bd, idesc, 1u, TF32);
+                    } else {
+                        umma(tmem, ad, bd, idesc, (i > 0 || k > 0) ? 1u : 0u, TF32);
                     }
                 }
                 umma_commit(empty + s);
@@ -628,10 +635,10 @@ __global__ void __launch_bounds__(kCT, SPLIT ? 1 : 2) conv_mma_kernel(const __gr
         // lo = x - hi goes 2 tiles further; hi stays implicit: kind::tf32 reads the raw fp32
         // operand and drops its low 13 mantissa bits, i.e. multiplies exactly tf32_hi(x)
         // (checked by the 3xTF32 unit tests at 2e-6; writing hi back cost 2.7 % of C3)
-        auto split16 = [&](unsigned char* p) {
+        auto split16 = [&](unsigned char* p, int lo_off) {
             const float4 x = *reinterpret_cast<const float4*>(p);
             const float4 hi = make_float4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
-            *reinterpret_cast<float4*>(p + 2 * kCTile) = make_float4(x.x - hi.x, x.y - hi.y, x.z - hi.z, x.w - hi.w);
+            *reinterpret_cast<float4*>(p + lo_off) = make_float4(x.x - hi.x, x.y - hi.y, x.z - hi.z, x.w - hi.w);
         };
         // once the thread's own copies of atom i have landed: (3xTF32) split exactly the
         // elements this thread copied, then publish its share of the atom
@@ -643,11 +650,11 @@ __global__ void __launch_bounds__(kCT, SPLIT ? 1 : 2) conv_mma_kernel(const __gr
                 for (int q = 0; q < 4; ++q) {
                     if (arun) {
                         const int ra = q * 32 + (t >> 3);
-                        split16(A + (ra >> 3) * 1024 + (ra & 7) * 128 + ((ja ^ (ra & 7)) << 4));
+                        split16(A + (ra >> 3) * 1024 + (ra & 7) * 128 + ((ja ^ (ra & 7)) << 4), 3 * kCTile);
                     } else {
-                        split16(A + rbase + (((jh + q) ^ sw) << 4));
+                        split16(A + rbase + (((jh + q) ^ sw) << 4), 3 * kCTile);
                     }
-                    split16(A + kCTile + rbase + (((jh + q) ^ sw) << 4));
+                    split16(A + kCTile + rbase + (((jh + q) ^ sw) << 4), kCTile);
                 }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -718,6 +725,12 @@ __global__ void __launch_bounds__(kCT, SPLIT ? 1 : 2) conv_mma_kernel(const __gr
                 for (int c = 0; c < 8; ++c) {
                     float v[16];
                     tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + c * 16, v);
+                    if constexpr (SPLIT) {  // + hi_A lo_B (accumulator columns 128-255)
+                        float w[16];
+                        tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + 128 + c * 16, w);
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) v[e] += w[e];
+                    }
 #pragma unroll
                     for (int e = 0; e < 16; ++e) T[row * 129 + c * 16 + e] = v[e];
                 }
@@ -783,7 +796,7 @@ __global__ void __launch_bounds__(kCT, SPLIT ? 1 : 2) conv_mma_kernel(const __gr
     if (threadIdx.x == 0) tick(6);
     if (warp == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(SPLIT ? 256 : 128));
     }
 }
 
