@@ -2725,7 +2725,14 @@ struct ferret_trainer {
     void replay_step(size_t r, std::vector<long long>& rel, NotePush& note_push, VSlot& vslot, Xfer& xfer) {
         using GB = GraphBuilder;
         for (int j = 0; j < P; ++j) note_push(j);
-        const uint64_t rk = GB::key(GB::kReplay, 0), pk = GB::key(GB::kPool, 0);
+        // replay stash resources per layer: its activation (act), the delta at its output (dlt)
+        // and its materialised conv weight gradient (grd), so a layer's weight gradient runs
+        // beside its input gradient and a stage's SGD step starts once its own layers are done
+        // (one key for the whole replay stash chained every replay node after the previous)
+        auto ract = [](int l) { return GB::key(GB::kReplay, 1, static_cast<uint64_t>(l)); };
+        auto rdlt = [](int l) { return GB::key(GB::kReplay, 2, static_cast<uint64_t>(l)); };
+        auto rgrd = [](int l) { return GB::key(GB::kReplay, 3, static_cast<uint64_t>(l)); };
+        const uint64_t pk = GB::key(GB::kPool, 0);
         const int* ids = ctl_rep_ids() + r * static_cast<size_t>(B);
         auto owner_of = [&](int j) { return owner[static_cast<size_t>(j)]; };
         for (int j = 0; j < P; ++j) {  // forward sweep
@@ -2734,7 +2741,7 @@ struct ferret_trainer {
                 const LayerDev& in_l = layers[static_cast<size_t>(s.lo - 1)];
                 float* buf = d_replay + in_l.act_off;
                 xfer(owner_of(j - 1), owner_of(j), [&] { return buf; }, [&] { return buf; },
-                     static_cast<size_t>(B) * in_l.out, nullptr, rk);
+                     static_cast<size_t>(B) * in_l.out, nullptr, ract(s.lo - 1));
             }
             if (DRY || !mine(j)) continue;
             gb->cur_category = kCatReplay;
@@ -2742,16 +2749,17 @@ struct ferret_trainer {
             for (int l = s.lo; l < s.hi; ++l) {
                 const LayerDev& ld = layers[static_cast<size_t>(l)];
                 const float* X = l == 0 ? d_pool_x : d_replay + layers[static_cast<size_t>(l - 1)].act_off;
-                emit_layer(ld, s.slot(rel[static_cast<size_t>(j)]), X, l == 0 ? ids : nullptr, d_replay + ld.act_off,
-                           {vslot(j, rel[static_cast<size_t>(j)]), pk}, {rk}, Head{},
-                           ld.res ? d_replay + layers[static_cast<size_t>(l - 2)].act_off : nullptr,
+                std::vector<uint64_t> rd{vslot(j, rel[static_cast<size_t>(j)]), l == 0 ? pk : ract(l - 1)};
+                if (ld.res) rd.push_back(ract(l - 2));
+                emit_layer(ld, s.slot(rel[static_cast<size_t>(j)]), X, l == 0 ? ids : nullptr, d_replay + ld.act_off, rd,
+                           {ract(l)}, Head{}, ld.res ? d_replay + layers[static_cast<size_t>(l - 2)].act_off : nullptr,
                            ld.gap() ? d_replay + ld.pool_off : nullptr);
             }
         }
         if (!DRY && mine(P - 1)) {
             gb->cur_category = kCatReplay;
             emit_delta_head(d_replay, ctl_rep_labels() + r * static_cast<size_t>(B), nullptr,
-                            1.0f / static_cast<float>(B), {}, {rk});
+                            1.0f / static_cast<float>(B), {ract(L - 1)}, {rdlt(L - 1)});
         }
         for (int j = P - 1; j >= 0; --j) {  // backward sweep
             const StageDev& s = stages[static_cast<size_t>(j)];
@@ -2762,10 +2770,14 @@ struct ferret_trainer {
                     const LayerDev& ld = layers[static_cast<size_t>(l)];
                     if (ld.conv())
                         emit_conv_wgrad(ld, d_replay, l == 0 ? d_pool_x : d_replay + layers[static_cast<size_t>(l - 1)].act_off,
-                                        l == 0 ? ids : nullptr, {vslot(j, rel[static_cast<size_t>(j)]), pk}, {rk});
+                                        l == 0 ? ids : nullptr,
+                                        {vslot(j, rel[static_cast<size_t>(j)]), l == 0 ? pk : ract(l - 1), rdlt(l)},
+                                        {rgrd(l)});
                     if (l == 0) break;
-                    emit_layer_backward(l, s.slot(rel[static_cast<size_t>(j)]), d_replay, stash_slots,
-                                        {vslot(j, rel[static_cast<size_t>(j)])}, {rk}, !(cross && l == s.lo));
+                    std::vector<uint64_t> rd{vslot(j, rel[static_cast<size_t>(j)]), rdlt(l), ract(l - 1)};
+                    if (l + 1 < L && layers[static_cast<size_t>(l + 1)].res) rd.push_back(rdlt(l + 1));
+                    emit_layer_backward(l, s.slot(rel[static_cast<size_t>(j)]), d_replay, stash_slots, rd, {rdlt(l - 1)},
+                                        !(cross && l == s.lo));
                 }
             }
             if (cross) {
@@ -2773,13 +2785,14 @@ struct ferret_trainer {
                 float* buf = d_replay + below.dlt_off;
                 xfer(owner_of(j), owner_of(j - 1), [&] { return buf; }, [&] { return buf; },
                      static_cast<size_t>(B) * below.out, below.act == FERRET_ACT_RELU ? d_replay + below.act_off : nullptr,
-                     rk);
+                     rdlt(s.lo - 1));
             }
         }
         if (!DRY) {
             for (int j = 0; j < P; ++j) {
                 if (!mine(j)) continue;
                 gb->cur_category = kCatReplay;
+                const StageDev& s = stages[static_cast<size_t>(j)];
                 const long long cur = rel[static_cast<size_t>(j)];
                 fb200::UpdArgs a = update_args(j, cur, cur);
                 a.policy = FERRET_POLICY_NONE;
@@ -2789,8 +2802,15 @@ struct ferret_trainer {
                 a.step = static_cast<float>(opt.lr);
                 fb200::KernelSpec k;
                 fb200::spec_update(a, k);
+                std::vector<uint64_t> rd{pk, vslot(j, cur)};
+                for (int l = s.lo; l < s.hi; ++l) {
+                    rd.push_back(rdlt(l));
+                    if (l > 0) rd.push_back(ract(l - 1));
+                    if (layers[static_cast<size_t>(l)].conv()) rd.push_back(rgrd(l));
+                    if (layers[static_cast<size_t>(l)].gap()) rd.push_back(ract(l));  // the pooled input
+                }
                 gb->cur_bytes = update_bytes(j, FERRET_POLICY_NONE, {cur}, cur);
-                gb->kernel(k, {rk, pk, vslot(j, cur)}, {vslot(j, cur + 1)});
+                gb->kernel(k, rd, {vslot(j, cur + 1)});
                 wt_invalidate(stages[static_cast<size_t>(j)], a.dst);
             }
         }

@@ -74,6 +74,8 @@ def measure(fb, torch, units=32, steps=3, warmup=2, width=64, micro_batch=16, re
         out["classes"] = {k: v for k, v in p["classes"].items() if v["nodes"] > 0}
         out["serial_ms"] = p["serial_ms"]
         out["critical_ms"] = p["critical_path_ms"]
+        out["critical_by_class"] = p["critical_path"]
+        out["kernels"] = tr.profile_kernels()
     out["oacc_last_chunk"] = fb.online_accuracy(tr.fetch_log(warmup + steps - 1))
     tr.close()
     return out
