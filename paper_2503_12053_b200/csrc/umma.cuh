@@ -1,5 +1,5 @@
 // tcgen05 / TMEM / TMA / mbarrier primitives shared by the tensor-core kernels
-// (mma.cu: dense layers; conv_mma.cu: implicit-GEMM convolutions). sm_100a only.
+// (mma.cu: dense layers; conv.cu: implicit-GEMM convolutions). sm_100a only.
 #pragma once
 
 #include <cuda.h>
