@@ -393,6 +393,7 @@ def main():
     tr.load_stream(feats, labels)
     tr.set_schedule(sched.events, chunk)
     connect(tr)
+    footprint = tr.footprint()  # HBM the trainer will hold for this schedule (dry run, before the graph build)
     stream = torch.cuda.ExternalStream(tr.cuda_stream, device=torch.device("cuda", local))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
 
@@ -521,6 +522,11 @@ def main():
         "host_issue_ms_per_step": 1e3 * host_s / args.steps,
         "online_accuracy_last_chunk": oacc_last,
         "online_accuracy_vs_cpu": acc,
+        "memory": {"device_bytes": stats["device_bytes"], "predicted_bytes": footprint["total"],
+                   "rings_bytes": footprint["rings"], "comp_state_bytes": footprint["comp_state"],
+                   "stash_bytes": footprint["stash"], "note": "the fixed memory of the metric: HBM the trainer holds "
+                   "on rank 0 (predicted by the dry-run footprint before the graph build; includes the resident "
+                   "stream of all chunks)"},
         "trainer": {"ring_depth": stats["ring_depth"], "stash_slots": stats["stash_slots"],
                     "mean_tau": stats["mean_tau"], "device_bytes": stats["device_bytes"],
                     "stage_owner": fb.ferret.stage_owners(P, min(world, P)) if world > 1 else None},
