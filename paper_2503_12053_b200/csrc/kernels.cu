@@ -1086,154 +1086,175 @@ __global__ void __launch_bounds__(kThreads) update_stream_kernel(const UpdArgs a
 
 // ---------------------------------------------------------------------------
 // update_group_kernel: G consecutive iter_fisher updates of one stage in one launch
-// (GroupArgs, kernels.cuh). A CTA owns <= kGroupRows rows x 256 columns of one weight
-// matrix (a thread: one column, the tile's rows) or 256 bias elements (a thread: one).
-// Per element the chain is held as its successive DIFFERENCES d[s] = v[s+1] - v[s] (the
-// fold only ever uses differences, and d[s] is the same fp32 value update_iter1_kernel
-// recomputes from the stored versions) plus the live value; update k folds over
-// d[first_k .. n-2], writes version n and appends its difference. The unit deltas of every
-// update and tile row are staged in smem once; the unit inputs x_k[b][c] of the thread's
-// column are prefetched kGroupXBuf updates ahead with cp.async into a per-thread smem ring
-// (each thread copies and reads only its own column: no barrier), so the L2 latency of the
-// activations overlaps the folds of the updates before.
-// CM = difference capacity (chain span - 1), BT = micro-batch bound.
+// (GroupArgs, kernels.cuh): the version chain and the compensator state cross HBM once for
+// the whole group instead of once per update. A CTA owns <= kGroupRows rows x 256 columns of
+// one weight matrix (a thread: one column, the tile's rows) or 256 bias elements (a thread:
+// one). The chain lives in shared memory as its successive DIFFERENCES
+// D[s][row][column] = v[s+1] - v[s] (the fold only ever uses differences, and D[s] is the same
+// fp32 value update_iter1_kernel computes from the stored versions), the live value in a
+// register; update k runs the lambda step on D[first_k] and the fold over D[first_k .. n-2]
+// with a dynamic loop (exact trip counts, no predicated padding), writes version n and appends
+// its difference. The deltas of every member and tile row are staged in smem once; the unit
+// inputs x_k[b][c] of the thread's column are loaded one member ahead into registers.
+// Per element the arithmetic is update_iter1_kernel's, update after update (bit-identical).
 // ---------------------------------------------------------------------------
-constexpr int kGroupXBuf = 6;
-
-__device__ __forceinline__ void cp_async4(float* dst_smem, const float* src, bool valid) {
-    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst_smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(valid ? 4 : 0) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-template <int CM, int BT>
-__global__ void __launch_bounds__(kThreads, CM <= 7 ? 2 : 1) update_group_kernel(const GroupArgs a) {
+template <int BT>
+__global__ void __launch_bounds__(kThreads, 2) update_group_kernel(const GroupArgs a) {
+    static_assert(kGroupRows == 2, "the group kernel packs its two rows into float2 lanes");
     FB_PDL_ENTRY();
-    __shared__ float sdel[kGroupMax * kMaxBatch * kGroupRows];
-    extern __shared__ float xs[];  // [kGroupXBuf][BT][kThreads]: the unit inputs, column tid per thread
+    // [span - 1][2 rows][kThreads] floats: first the HBM chain's versions (one 1 KB bulk copy per
+    // version and row: every load in flight at once), then, in place, their differences
+    extern __shared__ __align__(128) float dsm[];
+    __shared__ float2 sdel[kGroupMax * kMaxBatch];  // member k, sample b: (delta of row 0, row 1)
+    __shared__ __align__(8) uint64_t bar;
     const UpdWork w = a.works[blockIdx.x];
     const int tid = threadIdx.x, B = a.B, G = a.G;
     const bool bias = w.bias != 0;
     const bool gm = w.g_off >= 0;  // materialised gradients (convolutions)
     const bool use_x = !bias && !gm;
-    const int R = bias ? 1 : w.nrows;  // rows i >= R of the thread are computed on a copy of row 0, never stored
+    const int R = bias ? 1 : w.nrows;  // row 1 of a 1-row tile is computed on a copy of row 0, never stored
     const int c = w.c0 + tid;
     const bool live = bias ? tid < w.nrows : c < w.in;
-    // x_k[b][c] -> xs[k % kGroupXBuf][b][tid] (zero-filled past the micro-batch / the row end)
-    auto issue_x = [&](int k) {
-        if (use_x && k < G) {
-            const UpdPending& pk = a.pend[k];
-            float* dst = xs + (size_t)(k % kGroupXBuf) * BT * kThreads + tid;
-#pragma unroll
-            for (int b = 0; b < BT; ++b) {
-                const float* xr = w.xin_off >= 0 ? pk.stash + w.xin_off + (size_t)b * w.in
-                                  : a.x0idx      ? pk.x0 + (size_t)__ldg(a.x0idx + (b < B ? b : 0)) * a.x0_ld
-                                                 : pk.x0 + (size_t)b * a.x0_ld;
-                const bool ok = b < B && live;
-                cp_async4(dst + b * kThreads, ok ? xr + c : pk.x0 ? pk.x0 : pk.stash, ok);
-            }
-        }
-        cp_async_commit();  // (an empty group past the end keeps the wait count uniform)
-    };
-#pragma unroll
-    for (int k = 0; k < kGroupXBuf - 1; ++k) issue_x(k);
-    if (use_x) {  // deltas of every update and tile row: sdel[(k * BT + b) * 4 + i]
-        for (int q = tid; q < G * BT * kGroupRows; q += kThreads) {
-            const int i = q % kGroupRows, b = (q / kGroupRows) % BT, k = q / (kGroupRows * BT);
-            sdel[q] = (b < B && i < R) ? __ldg(a.pend[k].stash + w.dlt_off + (size_t)b * w.out + w.r0 + i) : 0.f;
-        }
+    // bulk-staged chain: weight tiles whose rows are 16-byte aligned; bias tiles load directly
+    const int ncols = bias ? 0 : min(kThreads, w.in - w.c0);
+    const bool staged = !bias && (w.in & 3) == 0 && a.n0 > 1;
+    auto V = [&](int sv, int i) -> float& { return dsm[((size_t)sv * 2 + i) * kThreads + tid]; };
+    if (tid == 0 && staged) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (!live) {
-        cp_async_wait<0>();
-        return;
-    }
-    size_t e[kGroupRows];
-#pragma unroll
-    for (int i = 0; i < kGroupRows; ++i)
-        e[i] = bias ? (size_t)w.elem0 + w.r0 + tid : (size_t)w.elem0 + (size_t)(w.r0 + (i < R ? i : 0)) * w.in + c;
-    // the HBM chain -> differences + live value; the compensator state
-    float d[kGroupRows][CM], cur[kGroupRows], ld[kGroupRows], vr[kGroupRows], va[kGroupRows];
-#pragma unroll
-    for (int i = 0; i < kGroupRows; ++i) {
-        float prev = __ldg(a.vers[0] + e[i]);
-#pragma unroll
-        for (int s = 0; s < CM; ++s) {
-            if (s + 1 < a.n0) {
-                const float nxt = __ldg(a.vers[s + 1] + e[i]);
-                d[i][s] = nxt - prev;
-                prev = nxt;
-            }
+    if (staged && tid < 32) {
+        const uint32_t row_bytes = static_cast<uint32_t>(ncols) * 4u;
+        if (tid == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&bar)),
+                         "r"(row_bytes * (uint32_t)(a.n0 * R))
+                         : "memory");
+        __syncwarp();
+        for (int q = tid; q < a.n0 * R; q += 32) {
+            const int sv = q / R, i = q - sv * R;
+            const float* src = a.vers[sv] + (size_t)w.elem0 + (size_t)(w.r0 + i) * w.in + w.c0;
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                             smem_addr(dsm + ((size_t)sv * 2 + i) * kThreads)),
+                         "l"(src), "r"(row_bytes), "r"(smem_addr(&bar))
+                         : "memory");
         }
-        cur[i] = prev;
-        ld[i] = a.lam_d[e[i]];
-        vr[i] = a.learn ? a.v_r[e[i]] : 0.f;
-        va[i] = a.learn ? a.v_a[e[i]] : 0.f;
     }
+    if (use_x) {
+        for (int q = tid; q < G * BT; q += kThreads) {
+            const int b = q % BT, k = q / BT;
+            const float* dl = a.pend[k].stash + w.dlt_off + (size_t)b * w.out + w.r0;
+            sdel[q] = b < B ? make_float2(__ldg(dl), __ldg(dl + (R > 1 ? 1 : 0))) : make_float2(0.f, 0.f);
+        }
+    }
+    size_t e[2];
+    e[0] = bias ? (size_t)w.elem0 + w.r0 + tid : (size_t)w.elem0 + (size_t)w.r0 * w.in + c;
+    e[1] = bias ? e[0] : (size_t)w.elem0 + (size_t)(w.r0 + (R > 1 ? 1 : 0)) * w.in + c;
     const bool learn = a.learn != 0;
-    int n = a.n0;  // chain length so far (versions 0 .. n-1; cur = version n-1); n - 1 < CM by the span check
+    float ld[2], vr[2], va[2];
+    if (live) {
+        ld[0] = a.lam_d[e[0]];
+        ld[1] = a.lam_d[e[1]];
+        vr[0] = learn ? a.v_r[e[0]] : 0.f;
+        vr[1] = learn ? a.v_r[e[1]] : 0.f;
+        va[0] = learn ? a.v_a[e[0]] : 0.f;
+        va[1] = learn ? a.v_a[e[1]] : 0.f;
+    }
+    auto load_x = [&](int k, float (&xv)[BT]) {
+#pragma unroll
+        for (int b = 0; b < BT; ++b) {
+            const UpdPending& pk = a.pend[k];
+            const float* xr = w.xin_off >= 0 ? pk.stash + w.xin_off + (size_t)b * w.in
+                              : a.x0idx      ? pk.x0 + (size_t)__ldg(a.x0idx + b) * a.x0_ld
+                                             : pk.x0 + (size_t)b * a.x0_ld;
+            xv[b] = (b < B && live) ? __ldg(xr + c) : 0.f;
+        }
+    };
+    float xnext[BT];
+    if (use_x) load_x(0, xnext);
+    __syncthreads();  // sdel
+    if (staged) {
+        uint32_t done = 0;
+        while (!done)
+            asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\t"
+                         "selp.u32 %0, 1, 0, p;\n\t}"
+                         : "=r"(done)
+                         : "r"(smem_addr(&bar))
+                         : "memory");
+    }
+    if (!live) return;
+    // the chain -> differences (in place, ascending: V[s + 1] is read before it is overwritten)
+    float2 cur;
+    if (staged) {
+        if (R < 2)
+            for (int sv = 0; sv < a.n0; ++sv) V(sv, 1) = V(sv, 0);
+        float2 prev = make_float2(V(0, 0), V(0, 1));
+        for (int sv = 0; sv + 1 < a.n0; ++sv) {
+            const float2 nxt = make_float2(V(sv + 1, 0), V(sv + 1, 1));
+            V(sv, 0) = nxt.x - prev.x;
+            V(sv, 1) = nxt.y - prev.y;
+            prev = nxt;
+        }
+        cur = prev;
+    } else {
+        float2 prev = make_float2(__ldg(a.vers[0] + e[0]), __ldg(a.vers[0] + e[1]));
+        for (int sv = 0; sv + 1 < a.n0; ++sv) {
+            const float2 nxt = make_float2(__ldg(a.vers[sv + 1] + e[0]), __ldg(a.vers[sv + 1] + e[1]));
+            V(sv, 0) = nxt.x - prev.x;
+            V(sv, 1) = nxt.y - prev.y;
+            prev = nxt;
+        }
+        cur = prev;
+    }
+    int n = a.n0;  // chain length so far (versions 0 .. n-1; cur = version n-1)
     for (int k = 0; k < G; ++k) {
         const UpdPending& pk = a.pend[k];
         const int first = pk.first;
-        issue_x(k + kGroupXBuf - 1);
-        cp_async_wait<kGroupXBuf - 1>();  // this thread's copies of update k have landed
-        const float* xk = xs + (size_t)(k % kGroupXBuf) * BT * kThreads + tid;
-        float g[kGroupRows], o[kGroupRows], lam[kGroupRows];
+        float xv[BT];
 #pragma unroll
-        for (int i = 0; i < kGroupRows; ++i) {
-            float gi = 0.f;
-            if (gm) {
-                gi = bias ? __ldg(pk.stash + w.g_off + w.r0 + tid) : __ldg(pk.stash + w.g_off + (e[i] - (size_t)w.elem0));
-            } else if (bias) {
-                const float* dl = pk.stash + w.dlt_off + w.r0 + tid;
+        for (int b = 0; b < BT; ++b) xv[b] = xnext[b];
+        if (use_x && k + 1 < G) load_x(k + 1, xnext);  // the next member's inputs in flight
+        float2 g = make_float2(0.f, 0.f);
+        if (gm) {
+            g = bias ? make_float2(__ldg(pk.stash + w.g_off + w.r0 + tid), 0.f)
+                     : make_float2(__ldg(pk.stash + w.g_off + (e[0] - (size_t)w.elem0)),
+                                   __ldg(pk.stash + w.g_off + (e[1] - (size_t)w.elem0)));
+        } else if (bias) {
+            const float* dl = pk.stash + w.dlt_off + w.r0 + tid;
 #pragma unroll
-                for (int b = 0; b < BT; ++b)
-                    if (b < B) gi += __ldg(dl + (size_t)b * w.out);
-            } else {
+            for (int b = 0; b < BT; ++b)
+                if (b < B) g.x += __ldg(dl + (size_t)b * w.out);
+            g.y = g.x;
+        } else {
 #pragma unroll
-                for (int b = 0; b < BT; ++b)
-                    if (b < B) gi = fmaf(sdel[(k * BT + b) * kGroupRows + i], xk[b * kThreads], gi);
-            }
-            g[i] = gi;
-            o[i] = gi;
-            lam[i] = a.lambda0 + ld[i];
+            for (int b = 0; b < BT; ++b)
+                if (b < B) g = __ffma2_rn(sdel[k * BT + b], make_float2(xv[b], xv[b]), g);
         }
+        float2 lam = make_float2(a.lambda0 + ld[0], a.lambda0 + ld[1]);
+        if (learn && first + 1 < n) {  // the lambda / v_r / v_a step on the read version's difference
+            lam.x = iter_learn(g.x, V(first, 0), ld[0], vr[0], va[0], a.lambda0, a.alpha, a.eta, a.nu);
+            lam.y = iter_learn(g.y, V(first, 1), ld[1], vr[1], va[1], a.lambda0, a.alpha, a.eta, a.nu);
+        }
+        // the fold, both rows in the two lanes of f32x2 ops: o += lam o o d (iter_fold's order)
+        float2 o = g;
+#pragma unroll 4
+        for (int sv = first; sv + 1 < n; ++sv)
+            o = __ffma2_rn(__fmul2_rn(__fmul2_rn(lam, o), o), make_float2(V(sv, 0), V(sv, 1)), o);
+        const float2 nv = make_float2(sgd_new(cur.x, a.step, o.x), sgd_new(cur.y, a.step, o.y));
+        V(n - 1, 0) = nv.x - cur.x;
+        V(n - 1, 1) = nv.y - cur.y;
+        cur = nv;
         float* dk = a.dst[k];
         unsigned short* dk16 = a.dst16[k];
-        // one pass over the chain with static indices: the lambda / v_r / v_a step at the read
-        // version (compensate.hpp:87-95), the fold (:97-102), then at the live version the SGD
-        // step (learner.hpp:497-502) and the new version's difference appended
-#pragma unroll
-        for (int s = 0; s < CM; ++s) {
-            if (s == n - 1) {
-#pragma unroll
-                for (int i = 0; i < kGroupRows; ++i) {
-                    const float nv = sgd_new(cur[i], a.step, o[i]);
-                    d[i][s] = nv - cur[i];
-                    cur[i] = nv;
-                    if (i < R) {
-                        dk[e[i]] = nv;
-                        if (dk16) reinterpret_cast<__nv_bfloat16*>(dk16)[e[i]] = __float2bfloat16_rn(nv);
-                    }
-                }
-            }
-            if (s >= first && s < n - 1) {
-                if (s == first && learn) {
-#pragma unroll
-                    for (int i = 0; i < kGroupRows; ++i)
-                        lam[i] = iter_learn(g[i], d[i][s], ld[i], vr[i], va[i], a.lambda0, a.alpha, a.eta, a.nu);
-                }
-#pragma unroll
-                for (int i = 0; i < kGroupRows; ++i) o[i] = iter_fold(o[i], lam[i], d[i][s]);
-            }
+        dk[e[0]] = nv.x;
+        if (dk16) reinterpret_cast<__nv_bfloat16*>(dk16)[e[0]] = __float2bfloat16_rn(nv.x);
+        if (R > 1) {
+            dk[e[1]] = nv.y;
+            if (dk16) reinterpret_cast<__nv_bfloat16*>(dk16)[e[1]] = __float2bfloat16_rn(nv.y);
         }
         ++n;
     }
-#pragma unroll
-    for (int i = 0; i < kGroupRows; ++i) {
-        if (i >= R) break;
+    for (int i = 0; i < R && i < 2; ++i) {
         a.lam_d[e[i]] = ld[i];
         if (learn) {
             a.v_r[e[i]] = vr[i];
@@ -1242,26 +1263,16 @@ __global__ void __launch_bounds__(kThreads, CM <= 7 ? 2 : 1) update_group_kernel
     }
 }
 
-template <int BT>
-constexpr size_t group_smem() { return sizeof(float) * (size_t)kGroupXBuf * BT * kThreads; }
+size_t group_smem(int span) { return sizeof(float) * 2 * (size_t)(span > 1 ? span - 1 : 1) * kThreads; }
 
-template <int CM, int BT>
-const void* group_fn() {
+template <int BT>
+const void* group_func() {
     static const void* f = [] {
-        const void* p = reinterpret_cast<const void*>(&update_group_kernel<CM, BT>);
-        cudaFuncSetAttribute(p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)group_smem<BT>());
+        const void* p = reinterpret_cast<const void*>(&update_group_kernel<BT>);
+        cudaFuncSetAttribute(p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)group_smem(kGroupChainMax));
         return p;
     }();
     return f;
-}
-
-template <int BT>
-const void* group_func(int span) {
-    if (span <= 8) return group_fn<7, BT>();
-    if (span <= 16) return group_fn<15, BT>();
-    if (span <= 24) return group_fn<23, BT>();
-    if (span <= 32) return group_fn<31, BT>();
-    return group_fn<kGroupChainMax - 1, BT>();
 }
 
 template <int BT>
@@ -1597,11 +1608,10 @@ void spec_update(const UpdArgs& a, KernelSpec& k) {
 
 void spec_update_group(const GroupArgs& a, KernelSpec& k) {
     const int span = a.n0 + a.G;  // versions spanned: the HBM chain + the group's outputs
-    const void* f = a.B <= 1 ? group_func<1>(span) : a.B <= 2 ? group_func<2>(span) : a.B <= 4 ? group_func<4>(span)
-                  : a.B <= 8 ? group_func<8>(span) : group_func<16>(span);
+    const void* f = a.B <= 1 ? group_func<1>() : a.B <= 2 ? group_func<2>() : a.B <= 4 ? group_func<4>()
+                  : a.B <= 8 ? group_func<8>() : group_func<16>();
     fill(k, f, dim3((unsigned)a.n_tiles), dim3(kThreads), a);
-    k.smem = a.B <= 1 ? group_smem<1>() : a.B <= 2 ? group_smem<2>() : a.B <= 4 ? group_smem<4>()
-           : a.B <= 8 ? group_smem<8>() : group_smem<16>();
+    k.smem = group_smem(span);
 }
 
 void spec_normalize(const NormArgs& a, KernelSpec& k) {

@@ -159,7 +159,7 @@ struct UpdArgs {
 // members past the nodes in between never changes what any node reads.
 constexpr int kGroupMax = 32;        // updates per group
 constexpr int kGroupChainMax = 40;   // versions a group spans: HBM chain + its own outputs
-constexpr int kGroupRows = 4;        // weight rows per thread (a CTA: 4 rows x 256 columns)
+constexpr int kGroupRows = 2;        // weight rows per thread (a CTA: 2 rows x 256 columns)
 struct GroupArgs {
     const UpdWork* works;            // the stage's group tiles (weights: <= 4 rows x 256 columns)
     int n_tiles;
