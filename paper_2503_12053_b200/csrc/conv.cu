@@ -29,6 +29,7 @@ namespace fb200 {
 namespace {
 
 constexpr int TM = 64, TN = 64, TK = 16, NT = 256;
+__device__ const float kConvOne = 1.0f;  // the B operand of the wgrad bias column (ConvArgs::bcol)
 
 template <class Args>
 void fill_spec(KernelSpec& k, const void* func, dim3 grid, dim3 block, const Args& a) {
@@ -126,7 +127,8 @@ __device__ __forceinline__ float load_b(const ConvArgs& a, const Col& c, int k) 
 template <int MODE>
 __device__ __forceinline__ void epilogue(const ConvArgs& a, int m, int n, float v) {
     if (MODE == kConvWgrad) {
-        a.Y[(size_t)m * a.N + n] = v;
+        if (a.bcol) a.Y[n == a.N - 1 ? (size_t)a.M * (a.N - 1) + m : (size_t)m * (a.N - 1) + n] = v;
+        else a.Y[(size_t)m * a.N + n] = v;
         return;
     }
     if (MODE == kConvFwd) {
@@ -492,6 +494,11 @@ __device__ __forceinline__ void locate_b(const ConvArgs& a, const Col& c, int k0
             }
         }
     } else {  // wgrad: column (ci, kh, kw) fixed; k = b * HWo + oh * wo + ow
+        if (a.bcol && c.ci >= a.ci) {  // the bias column: B = 1 for every k (the bias gradient)
+#pragma unroll
+            for (int e = 0; e < NE; ++e) P[e] = k0 + e < a.K ? &kConvOne : nullptr;
+            return;
+        }
         const int hw = a.ho * a.wo;
         int b = k0 / hw;
         const int pix = k0 - b * hw;
@@ -749,8 +756,11 @@ __global__ void __launch_bounds__(kCT, SPLIT ? 1 : 2) conv_mma_kernel(const __gr
                 for (int mm = mstart; mm < 128 && m0 + mm < a.M; mm += 2)
                     dst[(size_t)(m0 + mm) * a.N] = T[mm * 129 + nn];
             } else if (MODE == kConvWgrad) {
+                // with the bias column (bcol) the weights are M x (N - 1) and the bias follows them
+                const size_t ldw = a.bcol ? (size_t)(a.N - 1) : (size_t)a.N;
+                const bool bias_col = a.bcol && n == a.N - 1;
                 for (int mm = mstart; mm < 128 && m0 + mm < a.M; mm += 2)
-                    a.Y[(size_t)(m0 + mm) * a.N + n] = T[mm * 129 + nn];
+                    a.Y[bias_col ? (size_t)a.M * ldw + m0 + mm : (size_t)(m0 + mm) * ldw + n] = T[mm * 129 + nn];
             } else if (MODE == kConvFwd) {
                 const int hw = a.ho * a.wo, b = n / hw, pix = n - b * hw;
                 float* y = a.Y + (size_t)b * a.co * hw + pix;
@@ -849,7 +859,8 @@ size_t conv_plan(ConvArgs& a, int mode, size_t max_partial) {
         a.K = a.co * kk;
     } else {
         a.M = a.co;
-        a.N = a.ci * kk;
+        a.bcol = a.tc && a.bcol ? 1 : 0;  // the fused bias column needs the tensor-core path
+        a.N = a.ci * kk + a.bcol;
         a.K = a.B * a.ho * a.wo;
     }
     if (a.tc) {  // tensor cores: 128 x 128 tiles, K in 128-byte atoms, about one wave of CTAs

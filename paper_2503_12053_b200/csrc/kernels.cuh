@@ -357,6 +357,8 @@ struct ConvArgs {
                          // stride-k*k gather
     unsigned long long* stamps;  // nullable: 8 globaltimer phase stamps per CTA (measurement)
     int dbg;             // measurement only (FERRET_CONV_DBG): 1 = skip the A copies, 2 = skip the B copies
+    int bcol;            // tensor-core wgrad: GEMM column N-1 is the bias gradient (a ones column of B),
+                         // written at Y + M * (N - 1) + m (after the M x (N-1) weight gradient)
     int kt;              // tensor-core fwd / dgrad: K ordered (tap, channel) instead of (channel, tap),
                          // when the channel count is a multiple of the atom: a thread's run of k is
                          // one tap's consecutive channels (one bounds check, constant address step)

@@ -2080,7 +2080,11 @@ struct ferret_trainer {
         c.xidx = xidx;
         c.D = stash_u + ld.dlt_off;
         c.Y = stash_u + ld.g_off;
+        // tensor cores: the bias gradient is the GEMM's extra ones column (one launch less per weight
+        // gradient; FERRET_CONV_BIAS_COL=0: the separate conv_bgrad_kernel)
+        c.bcol = c.tc && !(std::getenv("FERRET_CONV_BIAS_COL") && std::atoi(std::getenv("FERRET_CONV_BIAS_COL")) == 0);
         emit_conv(c, fb200::kConvWgrad, reads, writes, 4.0 * ld.nw() + 4.0 * B * (ld.in + ld.out));
+        if (c.bcol) return;
         fb200::KernelSpec kb;
         fb200::spec_conv_bgrad(c, stash_u + ld.g_off + ld.nw(), kb);
         gb->cur_bytes = 4.0 * B * ld.out + 4.0 * ld.rows;
