@@ -1085,191 +1085,320 @@ __global__ void __launch_bounds__(kThreads) update_stream_kernel(const UpdArgs a
 }
 
 // ---------------------------------------------------------------------------
-// update_group_kernel: G consecutive iter_fisher updates of one stage in one launch
-// (GroupArgs, kernels.cuh): the version chain and the compensator state cross HBM once for
-// the whole group instead of once per update. A CTA owns <= kGroupRows rows x 256 columns of
-// one weight matrix (a thread: one column, the tile's rows) or 256 bias elements (a thread:
-// one). The chain lives in shared memory as its successive DIFFERENCES
-// D[s][row][column] = v[s+1] - v[s] (the fold only ever uses differences, and D[s] is the same
-// fp32 value update_iter1_kernel computes from the stored versions), the live value in a
-// register; update k runs the lambda step on D[first_k] and the fold over D[first_k .. n-2]
-// with a dynamic loop (exact trip counts, no predicated padding), writes version n and appends
-// its difference. The deltas of every member and tile row are staged in smem once; the unit
-// inputs x_k[b][c] of the thread's column are loaded one member ahead into registers.
+// update_group_kernel: G <= kGroupMax consecutive iter_fisher updates of one large dense stage
+// in one launch (GroupArgs, kernels.cuh): the version chain and the compensator state cross
+// HBM once for the whole group instead of once per update. Persistent and warp-specialised:
+// one CTA per SM walks a contiguous range of 2-row x 256-column tiles (column-block major: a
+// thread keeps its column's unit inputs of all members in registers while the block lasts).
+// A producer warp keeps as many tiles in flight as fit in smem (a stage: the tile's chain and
+// compensator state rows, landed by 1 KB bulk copies on the stage's full barrier, plus its
+// descriptor and the members' deltas of its two rows); the 8 consumer warps turn the stage's
+// chain into successive DIFFERENCES (D[s] = v[s+1] - v[s], the same fp32 values
+// update_iter1_kernel computes from the stored versions) in a per-thread float2 array, form the
+// members' gradients, and hand the stage back (empty barrier) before folding: the learning
+// steps run member after member (they chain the compensator state), then the members' folds
+// over the HBM part of the chain run interleaved (one difference load feeds every member whose
+// fold covers it; each member's operations stay in its own order), then member k folds the
+// k differences its predecessors appended, writes version n0 + k and appends its own. Launches
+// where a member's learning step reads an appended difference (it read the live version) fold
+// member after member instead. Bias runs (a thread: one element) follow with direct loads.
 // Per element the arithmetic is update_iter1_kernel's, update after update (bit-identical).
 // ---------------------------------------------------------------------------
+constexpr int kGroupChainRows = kGroupChainMax - 1;  // differences of the HBM chain (n0 <= kGroupChainMax - 1)
+constexpr int kGrpMaxStages = 8;
+constexpr int kGrpThreads = kThreads + 32;  // 8 consumer warps + the producer warp
+constexpr size_t kGrpDiffBytes = sizeof(float2) * (kGroupChainRows - 1) * kThreads;
+constexpr size_t kGrpSmem = 220 * 1024;     // differences + the stage ring
+
 template <int BT>
-__global__ void __launch_bounds__(kThreads, 2) update_group_kernel(const GroupArgs a) {
+__global__ void __launch_bounds__(kGrpThreads, 1) update_group_kernel(const GroupArgs a) {
     static_assert(kGroupRows == 2, "the group kernel packs its two rows into float2 lanes");
+    static_assert(kGroupMax * BT <= 64, "a producer lane stages at most two deltas per tile");
     FB_PDL_ENTRY();
-    // [span - 1][2 rows][kThreads] floats: first the HBM chain's versions (one 1 KB bulk copy per
-    // version and row: every load in flight at once), then, in place, their differences
-    extern __shared__ __align__(128) float dsm[];
-    __shared__ float2 sdel[kGroupMax * kMaxBatch];  // member k, sample b: (delta of row 0, row 1)
-    __shared__ __align__(8) uint64_t bar;
-    const UpdWork w = a.works[blockIdx.x];
-    const int tid = threadIdx.x, B = a.B, G = a.G;
-    const bool bias = w.bias != 0;
-    const bool gm = w.g_off >= 0;  // materialised gradients (convolutions)
-    const bool use_x = !bias && !gm;
-    const int R = bias ? 1 : w.nrows;  // row 1 of a 1-row tile is computed on a copy of row 0, never stored
-    const int c = w.c0 + tid;
-    const bool live = bias ? tid < w.nrows : c < w.in;
-    // bulk-staged chain: weight tiles whose rows are 16-byte aligned; bias tiles load directly
-    const int ncols = bias ? 0 : min(kThreads, w.in - w.c0);
-    const bool staged = !bias && (w.in & 3) == 0 && a.n0 > 1;
-    auto V = [&](int sv, int i) -> float& { return dsm[((size_t)sv * 2 + i) * kThreads + tid]; };
-    if (tid == 0 && staged) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar)) : "memory");
+    extern __shared__ __align__(128) float gsm[];
+    float2* dsm = reinterpret_cast<float2*>(gsm);                                  // [n0 - 1][kThreads]
+    float* ring = gsm + kGrpDiffBytes / sizeof(float);                             // [S][n_rows][2][kThreads]
+    __shared__ float2 sdel[kGrpMaxStages][kGroupMax * BT];  // per stage: member k, sample b (rows r0, r0 + 1)
+    __shared__ UpdWork wsm[kGrpMaxStages];
+    __shared__ __align__(8) uint64_t full[kGrpMaxStages], empty[kGrpMaxStages];
+    const int tid = threadIdx.x, B = a.B, G = a.G, n0 = a.n0;
+    const bool learn = a.learn != 0;
+    const int n_rows = n0 + (learn ? 3 : 1);  // bulk-copied rows per tile row: the chain, then the state
+    const size_t stage_floats = (size_t)n_rows * 2 * kThreads;
+    const int S = min(kGrpMaxStages, (int)((kGrpSmem - kGrpDiffBytes) / (stage_floats * sizeof(float))));
+    // this CTA's contiguous range of weight tiles
+    const int per = (a.n_wtiles + gridDim.x - 1) / gridDim.x;
+    const int t0 = min(a.n_wtiles, (int)blockIdx.x * per), t1 = min(a.n_wtiles, t0 + per);
+    if (tid == 0) {
+        for (int q = 0; q < S; ++q) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&full[q])) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(&empty[q])), "r"(kThreads / 32) : "memory");
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (staged && tid < 32) {
-        const uint32_t row_bytes = static_cast<uint32_t>(ncols) * 4u;
-        if (tid == 0)
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&bar)),
-                         "r"(row_bytes * (uint32_t)(a.n0 * R))
-                         : "memory");
-        __syncwarp();
-        for (int q = tid; q < a.n0 * R; q += 32) {
-            const int sv = q / R, i = q - sv * R;
-            const float* src = a.vers[sv] + (size_t)w.elem0 + (size_t)(w.r0 + i) * w.in + w.c0;
-            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                             smem_addr(dsm + ((size_t)sv * 2 + i) * kThreads)),
-                         "l"(src), "r"(row_bytes), "r"(smem_addr(&bar))
-                         : "memory");
-        }
-    }
-    if (use_x) {
-        for (int q = tid; q < G * BT; q += kThreads) {
-            const int b = q % BT, k = q / BT;
-            const float* dl = a.pend[k].stash + w.dlt_off + (size_t)b * w.out + w.r0;
-            sdel[q] = b < B ? make_float2(__ldg(dl), __ldg(dl + (R > 1 ? 1 : 0))) : make_float2(0.f, 0.f);
-        }
-    }
-    size_t e[2];
-    e[0] = bias ? (size_t)w.elem0 + w.r0 + tid : (size_t)w.elem0 + (size_t)w.r0 * w.in + c;
-    e[1] = bias ? e[0] : (size_t)w.elem0 + (size_t)(w.r0 + (R > 1 ? 1 : 0)) * w.in + c;
-    const bool learn = a.learn != 0;
-    float ld[2], vr[2], va[2];
-    if (live) {
-        ld[0] = a.lam_d[e[0]];
-        ld[1] = a.lam_d[e[1]];
-        vr[0] = learn ? a.v_r[e[0]] : 0.f;
-        vr[1] = learn ? a.v_r[e[1]] : 0.f;
-        va[0] = learn ? a.v_a[e[0]] : 0.f;
-        va[1] = learn ? a.v_a[e[1]] : 0.f;
-    }
-    auto load_x = [&](int k, float (&xv)[BT]) {
-#pragma unroll
-        for (int b = 0; b < BT; ++b) {
-            const UpdPending& pk = a.pend[k];
-            const float* xr = w.xin_off >= 0 ? pk.stash + w.xin_off + (size_t)b * w.in
-                              : a.x0idx      ? pk.x0 + (size_t)__ldg(a.x0idx + b) * a.x0_ld
-                                             : pk.x0 + (size_t)b * a.x0_ld;
-            xv[b] = (b < B && live) ? __ldg(xr + c) : 0.f;
-        }
-    };
-    float xnext[BT];
-    if (use_x) load_x(0, xnext);
-    __syncthreads();  // sdel
-    if (staged) {
+    auto wait_bar = [](uint64_t* b, uint32_t parity) {
         uint32_t done = 0;
         while (!done)
-            asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\t"
+            asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
                          "selp.u32 %0, 1, 0, p;\n\t}"
                          : "=r"(done)
-                         : "r"(smem_addr(&bar))
+                         : "r"(smem_addr(b)), "r"(parity)
                          : "memory");
-    }
-    if (!live) return;
-    // the chain -> differences (in place, ascending: V[s + 1] is read before it is overwritten)
-    float2 cur;
-    if (staged) {
-        if (R < 2)
-            for (int sv = 0; sv < a.n0; ++sv) V(sv, 1) = V(sv, 0);
-        float2 prev = make_float2(V(0, 0), V(0, 1));
-        for (int sv = 0; sv + 1 < a.n0; ++sv) {
-            const float2 nxt = make_float2(V(sv + 1, 0), V(sv + 1, 1));
-            V(sv, 0) = nxt.x - prev.x;
-            V(sv, 1) = nxt.y - prev.y;
-            prev = nxt;
+    };
+    if (tid >= kThreads) {  // ---- producer warp: descriptors and deltas loaded a tile ahead
+        const int lane = tid - kThreads;
+        auto load_w = [&](int t) {
+            UpdWork w{};
+            if (t < t1) w = a.works[t];
+            return w;
+        };
+        auto load_d = [&](const UpdWork& w, int t, float2* d) {
+            for (int h = 0; h < 2; ++h) {
+                const int q = lane + 32 * h, b = q % BT, k = q / BT;
+                d[h] = make_float2(0.f, 0.f);
+                if (t < t1 && k < G && b < B) {
+                    const float* dl = a.pend[k].stash + w.dlt_off + (size_t)b * w.out + w.r0;
+                    d[h] = make_float2(__ldg(dl), __ldg(dl + (w.nrows > 1 ? 1 : 0)));
+                }
+            }
+        };
+        UpdWork w_cur = load_w(t0), w_nxt = load_w(t0 + 1);
+        float2 d_cur[2], d_nxt[2];
+        load_d(w_cur, t0, d_cur);
+        for (int t = t0, it = 0; t < t1; ++t, ++it) {
+            const int st = it % S;
+            const UpdWork w_nn = load_w(t + 2);
+            load_d(w_nxt, t + 1, d_nxt);
+            if (it >= S) wait_bar(&empty[st], ((it / S) - 1) & 1);
+            const UpdWork& w = w_cur;
+            const int R = w.nrows, ncols = min(kThreads, w.in - w.c0);
+            if (lane == 0) wsm[st] = w;
+            for (int h = 0; h < 2; ++h)
+                if (lane + 32 * h < G * BT) sdel[st][lane + 32 * h] = d_cur[h];
+            __syncwarp();
+            const uint32_t row_bytes = static_cast<uint32_t>(ncols) * 4u;
+            if (lane == 0)  // release: the descriptor and deltas above, then the copies' bytes
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&full[st])),
+                             "r"(row_bytes * (uint32_t)(n_rows * R))
+                             : "memory");
+            __syncwarp();
+            float* stage = ring + st * stage_floats;
+            for (int q = lane; q < n_rows * R; q += 32) {
+                const int sv = q / R, i = q - sv * R;
+                const size_t off = (size_t)w.elem0 + (size_t)(w.r0 + i) * w.in + w.c0;
+                const int state = sv - n0;  // >= 0: lam_d, v_r, v_a
+                const float* src = state < 0 ? a.vers[sv] + off : (state == 0 ? a.lam_d : state == 1 ? a.v_r : a.v_a) + off;
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                 smem_addr(stage + (size_t)(sv * 2 + i) * kThreads)),
+                             "l"(src), "r"(row_bytes), "r"(smem_addr(&full[st]))
+                             : "memory");
+            }
+            w_cur = w_nxt;
+            w_nxt = w_nn;
+            d_cur[0] = d_nxt[0];
+            d_cur[1] = d_nxt[1];
         }
-        cur = prev;
-    } else {
-        float2 prev = make_float2(__ldg(a.vers[0] + e[0]), __ldg(a.vers[0] + e[1]));
-        for (int sv = 0; sv + 1 < a.n0; ++sv) {
-            const float2 nxt = make_float2(__ldg(a.vers[sv + 1] + e[0]), __ldg(a.vers[sv + 1] + e[1]));
-            V(sv, 0) = nxt.x - prev.x;
-            V(sv, 1) = nxt.y - prev.y;
-            prev = nxt;
+    } else {  // ---- consumer warps: thread tid owns column c0 + tid of every tile
+        // the members' learning steps read only HBM differences: fold them interleaved
+        bool interleave = true;
+        for (int k = 0; k < G; ++k) {
+            const int first = a.pend[k].first;
+            if (learn && first + 1 < n0 + k && first >= n0 - 1) interleave = false;
         }
-        cur = prev;
-    }
-    int n = a.n0;  // chain length so far (versions 0 .. n-1; cur = version n-1)
-    for (int k = 0; k < G; ++k) {
-        const UpdPending& pk = a.pend[k];
-        const int first = pk.first;
-        float xv[BT];
+        float xr[kGroupMax][BT];  // unit inputs x_k[b][c] of the current column block
+        long long x_key = -1;
+        for (int t = t0, it = 0; t < t1; ++t, ++it) {
+            const int st = it % S;
+            wait_bar(&full[st], (it / S) & 1);
+            const UpdWork w = wsm[st];
+            const int R = w.nrows, c = w.c0 + tid;
+            const bool live = c < w.in;
+            const float* stage = ring + st * stage_floats;
+            auto row = [&](int sv) {  // chain / state row sv of both tile rows
+                return make_float2(stage[(size_t)(sv * 2) * kThreads + tid],
+                                   stage[(size_t)(sv * 2 + (R > 1 ? 1 : 0)) * kThreads + tid]);
+            };
+            float2 g[kGroupMax], cur = make_float2(0.f, 0.f), ld = cur, vr = cur, va = cur;
+            if (live) {
+                const long long key = w.elem0 * 65536 + w.c0;
+                if (key != x_key) {
 #pragma unroll
-        for (int b = 0; b < BT; ++b) xv[b] = xnext[b];
-        if (use_x && k + 1 < G) load_x(k + 1, xnext);  // the next member's inputs in flight
-        float2 g = make_float2(0.f, 0.f);
-        if (gm) {
-            g = bias ? make_float2(__ldg(pk.stash + w.g_off + w.r0 + tid), 0.f)
-                     : make_float2(__ldg(pk.stash + w.g_off + (e[0] - (size_t)w.elem0)),
-                                   __ldg(pk.stash + w.g_off + (e[1] - (size_t)w.elem0)));
-        } else if (bias) {
+                    for (int k = 0; k < kGroupMax; ++k)
+                        if (k < G) {
+                            const UpdPending& pk = a.pend[k];
+#pragma unroll
+                            for (int b = 0; b < BT; ++b) {
+                                const float* xr_p = w.xin_off >= 0 ? pk.stash + w.xin_off + (size_t)b * w.in
+                                                    : a.x0idx      ? pk.x0 + (size_t)__ldg(a.x0idx + b) * a.x0_ld
+                                                                   : pk.x0 + (size_t)b * a.x0_ld;
+                                xr[k][b] = b < B ? __ldg(xr_p + c) : 0.f;
+                            }
+                        }
+                    x_key = key;
+                }
+                ld = row(n0);
+                if (learn) {
+                    vr = row(n0 + 1);
+                    va = row(n0 + 2);
+                }
+                float2 prev = row(0);
+                for (int sv = 1; sv < n0; ++sv) {
+                    const float2 nxt = row(sv);
+                    dsm[(size_t)(sv - 1) * kThreads + tid] = make_float2(nxt.x - prev.x, nxt.y - prev.y);
+                    prev = nxt;
+                }
+                cur = prev;
+#pragma unroll
+                for (int k = 0; k < kGroupMax; ++k) {
+                    g[k] = make_float2(0.f, 0.f);
+                    if (k < G) {
+#pragma unroll
+                        for (int b = 0; b < BT; ++b)
+                            if (b < B) g[k] = __ffma2_rn(sdel[st][k * BT + b], make_float2(xr[k][b], xr[k][b]), g[k]);
+                    }
+                }
+            }
+            // hand the stage back: our generic smem accesses ordered before the producer's bulk copies
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if ((tid & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[st])) : "memory");
+            if (!live) continue;
+            auto D = [&](int sv) { return dsm[(size_t)sv * kThreads + tid]; };
+            auto fold2 = [](float2 o, float2 lam, float2 d) { return __ffma2_rn(__fmul2_rn(__fmul2_rn(lam, o), o), d, o); };
+            auto learn2 = [&](float2 gk, float2 d0) {
+                float2 lam;
+                lam.x = iter_learn(gk.x, d0.x, ld.x, vr.x, va.x, a.lambda0, a.alpha, a.eta, a.nu);
+                lam.y = iter_learn(gk.y, d0.y, ld.y, vr.y, va.y, a.lambda0, a.alpha, a.eta, a.nu);
+                return lam;
+            };
+            float2 dt[kGroupMax];  // differences appended by the members
+            float2 nv[kGroupMax];
+            if (interleave) {
+                float2 lam[kGroupMax], o[kGroupMax];
+                int fmin = n0 - 1, fk[kGroupMax];
+#pragma unroll
+                for (int k = 0; k < kGroupMax; ++k) {
+                    o[k] = g[k];
+                    lam[k] = make_float2(0.f, 0.f);
+                    fk[k] = k < G ? a.pend[k].first : n0;  // absent members fold nothing
+                    if (k < G) {
+                        const int first = fk[k];
+                        fmin = min(fmin, first);
+                        lam[k] = make_float2(a.lambda0 + ld.x, a.lambda0 + ld.y);
+                        if (learn && first + 1 < n0 + k) lam[k] = learn2(g[k], D(first));
+                    }
+                }
+                for (int sv = fmin; sv + 1 < n0; ++sv) {
+                    const float2 d = D(sv);
+#pragma unroll
+                    for (int k = 0; k < kGroupMax; ++k)
+                        if (sv >= fk[k]) o[k] = fold2(o[k], lam[k], d);
+                }
+#pragma unroll
+                for (int k = 0; k < kGroupMax; ++k)
+                    if (k < G) {
+#pragma unroll
+                        for (int j = 0; j < k; ++j) o[k] = fold2(o[k], lam[k], dt[j]);
+                        nv[k] = make_float2(sgd_new(cur.x, a.step, o[k].x), sgd_new(cur.y, a.step, o[k].y));
+                        dt[k] = make_float2(nv[k].x - cur.x, nv[k].y - cur.y);
+                        cur = nv[k];
+                    }
+            } else {
+#pragma unroll
+                for (int k = 0; k < kGroupMax; ++k)
+                    if (k < G) {
+                        const int first = a.pend[k].first;
+                        float2 lam = make_float2(a.lambda0 + ld.x, a.lambda0 + ld.y);
+                        if (learn && first + 1 < n0 + k) {
+                            float2 d0 = first < n0 - 1 ? D(first) : dt[0];
+#pragma unroll
+                            for (int j = 1; j < k; ++j)
+                                if (first == n0 - 1 + j) d0 = dt[j];
+                            lam = learn2(g[k], d0);
+                        }
+                        float2 o = g[k];
+                        for (int sv = first; sv + 1 < n0; ++sv) o = fold2(o, lam, D(sv));
+#pragma unroll
+                        for (int j = 0; j < k; ++j)
+                            if (n0 - 1 + j >= first) o = fold2(o, lam, dt[j]);
+                        nv[k] = make_float2(sgd_new(cur.x, a.step, o.x), sgd_new(cur.y, a.step, o.y));
+                        dt[k] = make_float2(nv[k].x - cur.x, nv[k].y - cur.y);
+                        cur = nv[k];
+                    }
+            }
+            const size_t e0 = (size_t)w.elem0 + (size_t)w.r0 * w.in + c, e1 = e0 + (size_t)w.in;
+#pragma unroll
+            for (int k = 0; k < kGroupMax; ++k)
+                if (k < G) {
+                    float* dk = a.dst[k];
+                    unsigned short* dk16 = a.dst16[k];
+                    dk[e0] = nv[k].x;
+                    if (dk16) reinterpret_cast<__nv_bfloat16*>(dk16)[e0] = __float2bfloat16_rn(nv[k].x);
+                    if (R > 1) {
+                        dk[e1] = nv[k].y;
+                        if (dk16) reinterpret_cast<__nv_bfloat16*>(dk16)[e1] = __float2bfloat16_rn(nv[k].y);
+                    }
+                }
+            a.lam_d[e0] = ld.x;
+            if (learn) {
+                a.v_r[e0] = vr.x;
+                a.v_a[e0] = va.x;
+            }
+            if (R > 1) {
+                a.lam_d[e1] = ld.y;
+                if (learn) {
+                    a.v_r[e1] = vr.y;
+                    a.v_a[e1] = va.y;
+                }
+            }
+        }
+    }
+    // bias runs (after the weight tiles): a thread per element, direct loads
+    for (int t = a.n_wtiles + blockIdx.x; t < a.n_tiles; t += gridDim.x) {
+        const UpdWork w = a.works[t];
+        if (tid >= w.nrows || tid >= kThreads) continue;
+        const size_t e = (size_t)w.elem0 + w.r0 + tid;
+        float prev = __ldg(a.vers[0] + e);
+        float d[kGroupChainRows];
+        int n = a.n0;
+        for (int sv = 0; sv + 1 < n; ++sv) {
+            const float nxt = __ldg(a.vers[sv + 1] + e);
+            d[sv] = nxt - prev;
+            prev = nxt;
+        }
+        float cur = prev, ld = a.lam_d[e], vr = learn ? a.v_r[e] : 0.f, va = learn ? a.v_a[e] : 0.f;
+        for (int k = 0; k < G; ++k) {
+            const UpdPending& pk = a.pend[k];
+            const int first = pk.first;
+            float g = 0.f;
             const float* dl = pk.stash + w.dlt_off + w.r0 + tid;
-#pragma unroll
             for (int b = 0; b < BT; ++b)
-                if (b < B) g.x += __ldg(dl + (size_t)b * w.out);
-            g.y = g.x;
-        } else {
-#pragma unroll
-            for (int b = 0; b < BT; ++b)
-                if (b < B) g = __ffma2_rn(sdel[k * BT + b], make_float2(xv[b], xv[b]), g);
+                if (b < B) g += __ldg(dl + (size_t)b * w.out);
+            float lam = a.lambda0 + ld;
+            if (learn && first + 1 < n) lam = iter_learn(g, d[first], ld, vr, va, a.lambda0, a.alpha, a.eta, a.nu);
+            float o = g;
+            for (int sv = first; sv + 1 < n; ++sv) o = iter_fold(o, lam, d[sv]);
+            const float nv = sgd_new(cur, a.step, o);
+            d[n - 1] = nv - cur;
+            cur = nv;
+            a.dst[k][e] = nv;
+            if (a.dst16[k]) reinterpret_cast<__nv_bfloat16*>(a.dst16[k])[e] = __float2bfloat16_rn(nv);
+            ++n;
         }
-        float2 lam = make_float2(a.lambda0 + ld[0], a.lambda0 + ld[1]);
-        if (learn && first + 1 < n) {  // the lambda / v_r / v_a step on the read version's difference
-            lam.x = iter_learn(g.x, V(first, 0), ld[0], vr[0], va[0], a.lambda0, a.alpha, a.eta, a.nu);
-            lam.y = iter_learn(g.y, V(first, 1), ld[1], vr[1], va[1], a.lambda0, a.alpha, a.eta, a.nu);
-        }
-        // the fold, both rows in the two lanes of f32x2 ops: o += lam o o d (iter_fold's order)
-        float2 o = g;
-#pragma unroll 4
-        for (int sv = first; sv + 1 < n; ++sv)
-            o = __ffma2_rn(__fmul2_rn(__fmul2_rn(lam, o), o), make_float2(V(sv, 0), V(sv, 1)), o);
-        const float2 nv = make_float2(sgd_new(cur.x, a.step, o.x), sgd_new(cur.y, a.step, o.y));
-        V(n - 1, 0) = nv.x - cur.x;
-        V(n - 1, 1) = nv.y - cur.y;
-        cur = nv;
-        float* dk = a.dst[k];
-        unsigned short* dk16 = a.dst16[k];
-        dk[e[0]] = nv.x;
-        if (dk16) reinterpret_cast<__nv_bfloat16*>(dk16)[e[0]] = __float2bfloat16_rn(nv.x);
-        if (R > 1) {
-            dk[e[1]] = nv.y;
-            if (dk16) reinterpret_cast<__nv_bfloat16*>(dk16)[e[1]] = __float2bfloat16_rn(nv.y);
-        }
-        ++n;
-    }
-    for (int i = 0; i < R && i < 2; ++i) {
-        a.lam_d[e[i]] = ld[i];
+        a.lam_d[e] = ld;
         if (learn) {
-            a.v_r[e[i]] = vr[i];
-            a.v_a[e[i]] = va[i];
+            a.v_r[e] = vr;
+            a.v_a[e] = va;
         }
     }
 }
-
-size_t group_smem(int span) { return sizeof(float) * 2 * (size_t)(span > 1 ? span - 1 : 1) * kThreads; }
 
 template <int BT>
 const void* group_func() {
     static const void* f = [] {
         const void* p = reinterpret_cast<const void*>(&update_group_kernel<BT>);
-        cudaFuncSetAttribute(p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)group_smem(kGroupChainMax));
+        cudaFuncSetAttribute(p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGrpSmem);
         return p;
     }();
     return f;
@@ -1607,11 +1736,11 @@ void spec_update(const UpdArgs& a, KernelSpec& k) {
 }
 
 void spec_update_group(const GroupArgs& a, KernelSpec& k) {
-    const int span = a.n0 + a.G;  // versions spanned: the HBM chain + the group's outputs
     const void* f = a.B <= 1 ? group_func<1>() : a.B <= 2 ? group_func<2>() : a.B <= 4 ? group_func<4>()
                   : a.B <= 8 ? group_func<8>() : group_func<16>();
-    fill(k, f, dim3((unsigned)a.n_tiles), dim3(kThreads), a);
-    k.smem = group_smem(span);
+    // persistent: one CTA per SM (at most one per tile)
+    fill(k, f, dim3((unsigned)std::max(1, std::min(a.n_tiles, 148))), dim3(kGrpThreads), a);
+    k.smem = kGrpSmem;
 }
 
 void spec_normalize(const NormArgs& a, KernelSpec& k) {

@@ -157,12 +157,13 @@ struct UpdArgs {
 // groups while compiling the log (trainer.cpp: pending update groups): a group is emitted
 // as late as the first later node that touches one of its resources, so deferring its
 // members past the nodes in between never changes what any node reads.
-constexpr int kGroupMax = 32;        // updates per group
-constexpr int kGroupChainMax = 40;   // versions a group spans: HBM chain + its own outputs
-constexpr int kGroupRows = 2;        // weight rows per thread (a CTA: 2 rows x 256 columns)
+constexpr int kGroupMax = 4;         // updates per group (their unit inputs are staged in smem)
+constexpr int kGroupChainMax = 24;   // versions a group spans: HBM chain + its own outputs
+constexpr int kGroupRows = 2;        // weight rows per tile (a tile: 2 rows x 256 columns, a thread: one column)
 struct GroupArgs {
-    const UpdWork* works;            // the stage's group tiles (weights: <= 4 rows x 256 columns)
-    int n_tiles;
+    const UpdWork* works;            // the stage's group tiles: weights (<= 2 rows x 256 columns, column
+                                     // block major) first, then bias runs of 256
+    int n_tiles, n_wtiles;           // all tiles / weight tiles
     int B, G, n0;                    // micro-batch, updates, chain versions read from HBM
     int learn;                       // eta_lambda > 0 (v_r / v_a tracked)
     const float* vers[kGroupChainMax];  // vers[0] = oldest read version ... vers[n0 - 1] = cur0

@@ -191,8 +191,9 @@ struct StageDev {
     fb200::UpdWork* works4_dev = nullptr;  // float4 tiles (nullptr when a weight row is not 16-byte aligned)
     int n_tiles4 = 0, threads4 = 0;
     int n_tiles = 0;
-    fb200::UpdWork* works_g_dev = nullptr;  // update-group tiles (weights: <= 4 rows x 256 columns)
-    int n_tiles_g = 0;
+    fb200::UpdWork* works_g_dev = nullptr;  // update-group tiles (kernels.cuh GroupArgs::works)
+    int n_tiles_g = 0, n_wtiles_g = 0;
+    bool group_ok = false;  // update groups apply: a large dense stage with 16-byte aligned weight rows
     long long n_items = 0;
     // slot of a version counted from the chunk start (the live version is in slot 0 between chunks)
     float* slot(long long rel) const { return ring + (rel % depth) * slot_floats; }
@@ -956,20 +957,28 @@ struct ferret_trainer {
             s.works_dev = dalloc<fb200::UpdWork>(works.size(), device_bytes);
             cuda_check(cudaMemcpy(s.works_dev, works.data(), works.size() * sizeof(fb200::UpdWork), cudaMemcpyHostToDevice),
                        "upload work table");
-            {  // update-group tiles: kGroupRows rows x 256 columns, bias runs of 256
+            // update groups (kernels.cuh GroupArgs) pay off only where a stage's chain is far larger
+            // than its unit inputs: dense stages of at least FERRET_UPDATE_GROUPS_MIN parameters
+            // (default 8M), weight rows 16-byte aligned for the kernel's bulk copies
+            s.group_ok = group_updates && !s.gmat && opt.policy == FERRET_POLICY_ITER_FISHER &&
+                         s.slot_floats >= group_min_params;
+            for (const fb200::UpdSeg& sg : tab)
+                if (!sg.bias && sg.in % 4 != 0) s.group_ok = false;
+            if (s.group_ok) {  // tiles: kGroupRows rows x 256 columns, column-block major (a CTA's
+                               // range shares its column block's unit inputs), then bias runs of 256
                 std::vector<fb200::UpdWork> wg;
-                for (const fb200::UpdSeg& sg : tab) {
-                    if (sg.bias) {
+                for (const fb200::UpdSeg& sg : tab)
+                    if (!sg.bias)
+                        for (int c0 = 0; c0 < sg.in; c0 += fb200::kUpdTileCols)
+                            for (int r0 = 0; r0 < sg.out; r0 += fb200::kGroupRows)
+                                wg.push_back({sg.elem0, sg.xin_off, sg.dlt_off, sg.in, sg.out, 0, r0,
+                                              std::min(fb200::kGroupRows, sg.out - r0), c0, sg.g_off});
+                s.n_wtiles_g = static_cast<int>(wg.size());
+                for (const fb200::UpdSeg& sg : tab)
+                    if (sg.bias)
                         for (int r0 = 0; r0 < sg.out; r0 += fb200::kUpdTileCols)
                             wg.push_back({sg.elem0, sg.xin_off, sg.dlt_off, sg.in, sg.out, 1, r0,
                                           std::min(fb200::kUpdTileCols, sg.out - r0), 0, sg.g_off});
-                    } else {
-                        for (int r0 = 0; r0 < sg.out; r0 += fb200::kGroupRows)
-                            for (int c0 = 0; c0 < sg.in; c0 += fb200::kUpdTileCols)
-                                wg.push_back({sg.elem0, sg.xin_off, sg.dlt_off, sg.in, sg.out, 0, r0,
-                                              std::min(fb200::kGroupRows, sg.out - r0), c0, sg.g_off});
-                    }
-                }
                 s.n_tiles_g = static_cast<int>(wg.size());
                 s.works_g_dev = dalloc<fb200::UpdWork>(wg.size(), device_bytes);
                 cuda_check(cudaMemcpy(s.works_g_dev, wg.data(), wg.size() * sizeof(fb200::UpdWork), cudaMemcpyHostToDevice),
@@ -1563,6 +1572,7 @@ struct ferret_trainer {
             fb200::GroupArgs a{};
             a.works = sd.works_g_dev;
             a.n_tiles = sd.n_tiles_g;
+            a.n_wtiles = sd.n_wtiles_g;
             a.B = B;
             a.G = static_cast<int>(g.members.size());
             a.n0 = static_cast<int>(g.cur0 - g.oldest + 1);
@@ -1705,7 +1715,8 @@ struct ferret_trainer {
                     }
                     ++n_upd;
                     if (timing && mine(j)) ++res.n_updates_timed;
-                    const bool join = grouping && mine(j) && pl.size() == 1 && stages[static_cast<size_t>(j)].lam_d &&
+                    const bool join = grouping && mine(j) && pl.size() == 1 && stages[static_cast<size_t>(j)].group_ok &&
+                                      stages[static_cast<size_t>(j)].lam_d &&
                                       (cur - pl[0].read + 2) <= fb200::kGroupChainMax;
                     if (join) {
                         PGroup& g = groups[static_cast<size_t>(j)];
@@ -2838,11 +2849,13 @@ struct ferret_trainer {
     // Algorithmic bytes of one update launch: every parameter element reads the
     // versions it needs + its compensator state and writes the new version +
     // state; plus the deltas and layer inputs of each pending gradient.
-    // FERRET_UPDATE_GROUPS=1 (A/B knob, same results): consecutive iter_fisher updates of a stage
-    // fused into one update_group_kernel launch. Off by default: measured on C5 fp32 the grouped
-    // kernel runs at 61 GB/s (15K-instruction body, one CTA per SM) and the step drops from
-    // 3.2k to 0.77k samples/s; C2 from 1.12M to 0.45M (profiles/r2/ab_update_groups.txt)
+    // FERRET_UPDATE_GROUPS=1 (A/B knob, same results): consecutive iter_fisher updates of a large stage
+    // fused into one update_group_kernel launch. Off by default: on C5 fp32 the groups cut the
+    // update bytes 3x but the kernel runs at 2.6 TB/s (consumer-bound), so the step is a wash
+    // (3.84k vs 3.87k samples/s, profiles/r2/ab_update_groups_ws.txt)
     bool group_updates = std::getenv("FERRET_UPDATE_GROUPS") && std::atoi(std::getenv("FERRET_UPDATE_GROUPS")) != 0;
+    long long group_min_params = std::getenv("FERRET_UPDATE_GROUPS_MIN") ? std::atoll(std::getenv("FERRET_UPDATE_GROUPS_MIN"))
+                                                                          : 8ll << 20;
     // Consecutive updates of a stage joined by programmatic edges (KernelSpec::chain_pdl kernels:
     // the next update launches and loads its unit's inputs and older versions while the previous
     // one drains): C2 1.10M -> 1.23M samples/s, its critical path being the stage-0 update chain
