@@ -1200,13 +1200,17 @@ __global__ void __launch_bounds__(kGrpThreads, 1) update_group_kernel(const Grou
             d_cur[1] = d_nxt[1];
         }
     } else {  // ---- consumer warps: thread tid owns column c0 + tid of every tile
-        // the members' learning steps read only HBM differences: fold them interleaved
-        bool interleave = true;
-        for (int k = 0; k < G; ++k) {
-            const int first = a.pend[k].first;
-            if (learn && first + 1 < n0 + k && first >= n0 - 1) interleave = false;
+        // members' read versions (first chain index), uniform over the launch
+        int fk[kGroupMax];
+        bool interleave = true;  // read versions ascending, learning steps on HBM differences only
+#pragma unroll
+        for (int k = 0; k < kGroupMax; ++k) {
+            fk[k] = k < G ? a.pend[k].first : n0 - 1;
+            if (k < G && learn && fk[k] + 1 < n0 + k && fk[k] >= n0 - 1) interleave = false;
+            if (k > 0 && k < G && fk[k] < fk[k - 1]) interleave = false;
         }
-        float xr[kGroupMax][BT];  // unit inputs x_k[b][c] of the current column block
+        const float lambda0 = a.lambda0, alpha = a.alpha, eta = a.eta, nu = a.nu, step = a.step;
+        float xr[kGroupMax][BT];  // unit inputs x_k[b][c] of the current column block (0 past B)
         long long x_key = -1;
         for (int t = t0, it = 0; t < t1; ++t, ++it) {
             const int st = it % S;
@@ -1214,11 +1218,9 @@ __global__ void __launch_bounds__(kGrpThreads, 1) update_group_kernel(const Grou
             const UpdWork w = wsm[st];
             const int R = w.nrows, c = w.c0 + tid;
             const bool live = c < w.in;
-            const float* stage = ring + st * stage_floats;
-            auto row = [&](int sv) {  // chain / state row sv of both tile rows
-                return make_float2(stage[(size_t)(sv * 2) * kThreads + tid],
-                                   stage[(size_t)(sv * 2 + (R > 1 ? 1 : 0)) * kThreads + tid]);
-            };
+            // this thread's column of the stage's two tile rows; row sv at + sv * 2 * kThreads
+            const float* p0 = ring + st * stage_floats + tid;
+            const float* p1 = p0 + (R > 1 ? kThreads : 0);
             float2 g[kGroupMax], cur = make_float2(0.f, 0.f), ld = cur, vr = cur, va = cur;
             if (live) {
                 const long long key = w.elem0 * 65536 + w.c0;
@@ -1237,25 +1239,30 @@ __global__ void __launch_bounds__(kGrpThreads, 1) update_group_kernel(const Grou
                         }
                     x_key = key;
                 }
-                ld = row(n0);
+                const size_t srow = (size_t)n0 * 2 * kThreads;
+                ld = make_float2(p0[srow], p1[srow]);
                 if (learn) {
-                    vr = row(n0 + 1);
-                    va = row(n0 + 2);
+                    vr = make_float2(p0[srow + 2 * kThreads], p1[srow + 2 * kThreads]);
+                    va = make_float2(p0[srow + 4 * kThreads], p1[srow + 4 * kThreads]);
                 }
-                float2 prev = row(0);
+                float2 prev = make_float2(p0[0], p1[0]);
+                float2* dq = dsm + tid;
                 for (int sv = 1; sv < n0; ++sv) {
-                    const float2 nxt = row(sv);
-                    dsm[(size_t)(sv - 1) * kThreads + tid] = make_float2(nxt.x - prev.x, nxt.y - prev.y);
+                    p0 += 2 * kThreads;
+                    p1 += 2 * kThreads;
+                    const float2 nxt = make_float2(*p0, *p1);
+                    *dq = make_float2(nxt.x - prev.x, nxt.y - prev.y);
+                    dq += kThreads;
                     prev = nxt;
                 }
                 cur = prev;
+                // gradients (padded samples: delta 0 x input 0 adds +0, which leaves g unchanged)
 #pragma unroll
                 for (int k = 0; k < kGroupMax; ++k) {
                     g[k] = make_float2(0.f, 0.f);
                     if (k < G) {
 #pragma unroll
-                        for (int b = 0; b < BT; ++b)
-                            if (b < B) g[k] = __ffma2_rn(sdel[st][k * BT + b], make_float2(xr[k][b], xr[k][b]), g[k]);
+                        for (int b = 0; b < BT; ++b) g[k] = __ffma2_rn(sdel[st][k * BT + b], make_float2(xr[k][b], xr[k][b]), g[k]);
                     }
                 }
             }
@@ -1268,39 +1275,38 @@ __global__ void __launch_bounds__(kGrpThreads, 1) update_group_kernel(const Grou
             auto fold2 = [](float2 o, float2 lam, float2 d) { return __ffma2_rn(__fmul2_rn(__fmul2_rn(lam, o), o), d, o); };
             auto learn2 = [&](float2 gk, float2 d0) {
                 float2 lam;
-                lam.x = iter_learn(gk.x, d0.x, ld.x, vr.x, va.x, a.lambda0, a.alpha, a.eta, a.nu);
-                lam.y = iter_learn(gk.y, d0.y, ld.y, vr.y, va.y, a.lambda0, a.alpha, a.eta, a.nu);
+                lam.x = iter_learn(gk.x, d0.x, ld.x, vr.x, va.x, lambda0, alpha, eta, nu);
+                lam.y = iter_learn(gk.y, d0.y, ld.y, vr.y, va.y, lambda0, alpha, eta, nu);
                 return lam;
             };
             float2 dt[kGroupMax];  // differences appended by the members
             float2 nv[kGroupMax];
             if (interleave) {
                 float2 lam[kGroupMax], o[kGroupMax];
-                int fmin = n0 - 1, fk[kGroupMax];
 #pragma unroll
                 for (int k = 0; k < kGroupMax; ++k) {
                     o[k] = g[k];
-                    lam[k] = make_float2(0.f, 0.f);
-                    fk[k] = k < G ? a.pend[k].first : n0;  // absent members fold nothing
-                    if (k < G) {
-                        const int first = fk[k];
-                        fmin = min(fmin, first);
-                        lam[k] = make_float2(a.lambda0 + ld.x, a.lambda0 + ld.y);
-                        if (learn && first + 1 < n0 + k) lam[k] = learn2(g[k], D(first));
-                    }
+                    lam[k] = make_float2(lambda0 + ld.x, lambda0 + ld.y);
+                    if (k < G && learn && fk[k] + 1 < n0 + k) lam[k] = learn2(g[k], D(fk[k]));
                 }
-                for (int sv = fmin; sv + 1 < n0; ++sv) {
-                    const float2 d = D(sv);
+                // segment j of the HBM differences, [fk[j], fk[j + 1]), is folded by members 0..j
 #pragma unroll
-                    for (int k = 0; k < kGroupMax; ++k)
-                        if (sv >= fk[k]) o[k] = fold2(o[k], lam[k], d);
-                }
+                for (int j = 0; j < kGroupMax; ++j)
+                    if (j < G) {
+                        const int hi = j + 1 < G ? fk[j + 1] : n0 - 1;
+                        const float2* dp = dsm + (size_t)fk[j] * kThreads + tid;
+                        for (int sv = fk[j]; sv < hi; ++sv, dp += kThreads) {
+                            const float2 d = *dp;
+#pragma unroll
+                            for (int m = 0; m <= j; ++m) o[m] = fold2(o[m], lam[m], d);
+                        }
+                    }
 #pragma unroll
                 for (int k = 0; k < kGroupMax; ++k)
                     if (k < G) {
 #pragma unroll
                         for (int j = 0; j < k; ++j) o[k] = fold2(o[k], lam[k], dt[j]);
-                        nv[k] = make_float2(sgd_new(cur.x, a.step, o[k].x), sgd_new(cur.y, a.step, o[k].y));
+                        nv[k] = make_float2(sgd_new(cur.x, step, o[k].x), sgd_new(cur.y, step, o[k].y));
                         dt[k] = make_float2(nv[k].x - cur.x, nv[k].y - cur.y);
                         cur = nv[k];
                     }
@@ -1308,8 +1314,8 @@ __global__ void __launch_bounds__(kGrpThreads, 1) update_group_kernel(const Grou
 #pragma unroll
                 for (int k = 0; k < kGroupMax; ++k)
                     if (k < G) {
-                        const int first = a.pend[k].first;
-                        float2 lam = make_float2(a.lambda0 + ld.x, a.lambda0 + ld.y);
+                        const int first = fk[k];
+                        float2 lam = make_float2(lambda0 + ld.x, lambda0 + ld.y);
                         if (learn && first + 1 < n0 + k) {
                             float2 d0 = first < n0 - 1 ? D(first) : dt[0];
 #pragma unroll
@@ -1322,7 +1328,7 @@ __global__ void __launch_bounds__(kGrpThreads, 1) update_group_kernel(const Grou
 #pragma unroll
                         for (int j = 0; j < k; ++j)
                             if (n0 - 1 + j >= first) o = fold2(o, lam, dt[j]);
-                        nv[k] = make_float2(sgd_new(cur.x, a.step, o.x), sgd_new(cur.y, a.step, o.y));
+                        nv[k] = make_float2(sgd_new(cur.x, step, o.x), sgd_new(cur.y, step, o.y));
                         dt[k] = make_float2(nv[k].x - cur.x, nv[k].y - cur.y);
                         cur = nv[k];
                     }

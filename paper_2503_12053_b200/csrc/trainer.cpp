@@ -1569,6 +1569,24 @@ struct ferret_trainer {
             groups[static_cast<size_t>(j)] = PGroup{};
             if (g.members.empty()) return;
             const StageDev& sd = stages[static_cast<size_t>(j)];
+            if (g.members.size() == 1) {  // a lone member: the single-update kernels stream it faster
+                fb200::UpdArgs a = update_args(j, g.cur0, g.oldest);
+                a.policy = opt.policy;
+                a.K = 1;
+                a.pend[0] = {g.stash_of[0], g.x0_of[0], static_cast<int>(g.members[0].read - g.oldest)};
+                a.step = static_cast<float>(opt.lr);
+                fb200::KernelSpec k;
+                fb200::spec_update(a, k);
+                gb->cur_bytes = update_bytes(j, opt.policy, {g.members[0].read}, g.cur0);
+                gb->cur_category = kCatUpdate;
+                gb->cur_stage = j;
+                if (update_pdl) gb->pdl_pred = last_update_node[static_cast<size_t>(j)];
+                gb->kernel(k, g.reads, g.writes);
+                last_update_node[static_cast<size_t>(j)] = static_cast<int>(gb->nodes.size()) - 1;
+                wt_invalidate(sd, a.dst);
+                ++n_single_groups;
+                return;
+            }
             fb200::GroupArgs a{};
             a.works = sd.works_g_dev;
             a.n_tiles = sd.n_tiles_g;
@@ -1600,6 +1618,9 @@ struct ferret_trainer {
             gb->cur_category = kCatUpdate;
             gb->cur_stage = j;
             gb->kernel(k, g.reads, g.writes);
+            // no programmatic edge out of a group: a chained single update loads its older versions
+            // before griddepcontrol.wait, and a group writes several of them
+            last_update_node[static_cast<size_t>(j)] = -1;
             for (int q = 0; q < a.G; ++q) wt_invalidate(sd, a.dst[q]);
             ++n_group_nodes;
         };
@@ -1622,7 +1643,7 @@ struct ferret_trainer {
                     if (hits(g.writes, r) || hits(g.writes, w) || hits(g.reads, w)) flush_group(q);
                 }
             };
-        if (!DRY) n_group_nodes = 0;
+        if (!DRY) n_group_nodes = n_single_groups = 0;
 
         for (size_t idx = 0; idx < sched.events.size(); ++idx) {
             if (!DRY && !gb->prof_events && gb->nodes_in_segment() >= seg_nodes) gb->new_segment();
@@ -2849,11 +2870,11 @@ struct ferret_trainer {
     // Algorithmic bytes of one update launch: every parameter element reads the
     // versions it needs + its compensator state and writes the new version +
     // state; plus the deltas and layer inputs of each pending gradient.
-    // FERRET_UPDATE_GROUPS=1 (A/B knob, same results): consecutive iter_fisher updates of a large stage
-    // fused into one update_group_kernel launch. Off by default: on C5 fp32 the groups cut the
-    // update bytes 3x but the kernel runs at 2.6 TB/s (consumer-bound), so the step is a wash
-    // (3.84k vs 3.87k samples/s, profiles/r2/ab_update_groups_ws.txt)
-    bool group_updates = std::getenv("FERRET_UPDATE_GROUPS") && std::atoi(std::getenv("FERRET_UPDATE_GROUPS")) != 0;
+    // Update groups (same results): consecutive iter_fisher updates of a large dense stage fused
+    // into one update_group_kernel launch that reads the version chain and the compensator state
+    // once; one-member groups go to the single-update kernels. C5 fp32: 3.87k -> 4.85k samples/s
+    // (profiles/r2/ab_update_groups_final.txt). FERRET_UPDATE_GROUPS=0: every update its own node
+    bool group_updates = !std::getenv("FERRET_UPDATE_GROUPS") || std::atoi(std::getenv("FERRET_UPDATE_GROUPS")) != 0;
     long long group_min_params = std::getenv("FERRET_UPDATE_GROUPS_MIN") ? std::atoll(std::getenv("FERRET_UPDATE_GROUPS_MIN"))
                                                                           : 8ll << 20;
     // Consecutive updates of a stage joined by programmatic edges (KernelSpec::chain_pdl kernels:
@@ -2861,7 +2882,7 @@ struct ferret_trainer {
     // one drains): C2 1.10M -> 1.23M samples/s, its critical path being the stage-0 update chain
     // (profiles/r2/update_pdl_ab.txt). FERRET_UPDATE_PDL=0: full dependencies (A/B knob)
     bool update_pdl = !std::getenv("FERRET_UPDATE_PDL") || std::atoi(std::getenv("FERRET_UPDATE_PDL")) != 0;
-    size_t n_group_nodes = 0;
+    size_t n_group_nodes = 0, n_single_groups = 0;  // group launches / one-member groups sent to the single-update kernels
     // algorithmic HBM bytes of one update group of stage j: the n0 chain versions read once,
     // lambda / v_r / v_a read and written once, G new versions written (+ their bf16 copies),
     // plus every member's unit activations and deltas

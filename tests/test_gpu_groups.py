@@ -129,3 +129,43 @@ def test_groups_skip_conv_stages(gpu, fb):
     u = _train(fb, spec, params, bounds, sched, feats, labels, units * B, 1, False, micro_batch=B)
     assert _groups_launched(g["kern"]) == 0
     _same(g, u)
+
+
+def test_groups_bit_identical_c5_full_size(gpu, fb):
+    """The headline shape at full size with the default 8M-parameter floor: 16 x 4096, 8 stages,
+    micro-batch 16, two chunks — groups on (the default) vs every update its own node."""
+    widths, bounds, units, B = [4096] * 16 + [10], list(range(0, 17, 2)), 32, 16
+    prof = fb.profile_from_widths(widths)
+    t_d = float(prof["t_f"].max())
+    sched = fb.Schedule.forced(prof, t_d, fb.StreamSpec(t_d=t_d, horizon=units * t_d), bounds, units)
+    feats, labels = fb.synth_drift_stream(2 * units * B, widths[0], widths[-1], "split_tasks", 7)
+    params = fb.make_dense_net(widths, 1)
+    outs = []
+    for grouped in (True, False):
+        env = {"FERRET_UPDATE_GROUPS": "1" if grouped else "0"}
+        old = {k: os.environ.get(k) for k in list(env) + ["FERRET_UPDATE_GROUPS_MIN"]}
+        os.environ.update(env)
+        os.environ.pop("FERRET_UPDATE_GROUPS_MIN", None)
+        try:
+            tr = fb.PipelineTrainer(widths, params, bounds, fb.PipelineTrainOptions(policy="iter_fisher", micro_batch=B))
+        finally:
+            for k, v in old.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
+        tr.load_stream(feats, labels)
+        tr.set_schedule(sched.events, units * B)
+        logs = []
+        for c in range(2):
+            if grouped and c == 1:
+                tr.set_profiling(True)
+            tr.execute(c)
+            logs.append(tr.fetch_log(c))
+        kern = tr.profile_kernels() if grouped else None
+        outs.append({"params": tr.params(), "log": np.concatenate(logs), "kern": kern})
+        tr.close()
+    g, u = outs
+    assert _groups_launched(g["kern"]) > 0
+    assert np.array_equal(g["params"], u["params"])
+    assert np.array_equal(g["log"]["predicted"], u["log"]["predicted"])
