@@ -1107,8 +1107,7 @@ __global__ void __launch_bounds__(kThreads) update_stream_kernel(const UpdArgs a
 constexpr int kGroupChainRows = kGroupChainMax - 1;  // differences of the HBM chain (n0 <= kGroupChainMax - 1)
 constexpr int kGrpMaxStages = 8;
 constexpr int kGrpThreads = kThreads + 32;  // 8 consumer warps + the producer warp
-constexpr size_t kGrpDiffBytes = sizeof(float2) * (kGroupChainRows - 1) * kThreads;
-constexpr size_t kGrpSmem = 220 * 1024;     // differences + the stage ring
+constexpr size_t kGrpSmem = 220 * 1024;     // the stage ring
 
 template <int BT>
 __global__ void __launch_bounds__(kGrpThreads, 1) update_group_kernel(const GroupArgs a) {
@@ -1116,8 +1115,7 @@ __global__ void __launch_bounds__(kGrpThreads, 1) update_group_kernel(const Grou
     static_assert(kGroupMax * BT <= 64, "a producer lane stages at most two deltas per tile");
     FB_PDL_ENTRY();
     extern __shared__ __align__(128) float gsm[];
-    float2* dsm = reinterpret_cast<float2*>(gsm);                                  // [n0 - 1][kThreads]
-    float* ring = gsm + kGrpDiffBytes / sizeof(float);                             // [S][n_rows][2][kThreads]
+    float* ring = gsm;  // [S][n_rows][2][kThreads]
     __shared__ float2 sdel[kGrpMaxStages][kGroupMax * BT];  // per stage: member k, sample b (rows r0, r0 + 1)
     __shared__ UpdWork wsm[kGrpMaxStages];
     __shared__ __align__(8) uint64_t full[kGrpMaxStages], empty[kGrpMaxStages];
@@ -1125,7 +1123,7 @@ __global__ void __launch_bounds__(kGrpThreads, 1) update_group_kernel(const Grou
     const bool learn = a.learn != 0;
     const int n_rows = n0 + (learn ? 3 : 1);  // bulk-copied rows per tile row: the chain, then the state
     const size_t stage_floats = (size_t)n_rows * 2 * kThreads;
-    const int S = min(kGrpMaxStages, (int)((kGrpSmem - kGrpDiffBytes) / (stage_floats * sizeof(float))));
+    const int S = min(kGrpMaxStages, (int)(kGrpSmem / (stage_floats * sizeof(float))));
     // this CTA's contiguous range of weight tiles
     const int per = (a.n_wtiles + gridDim.x - 1) / gridDim.x;
     const int t0 = min(a.n_wtiles, (int)blockIdx.x * per), t1 = min(a.n_wtiles, t0 + per);
@@ -1221,118 +1219,138 @@ __global__ void __launch_bounds__(kGrpThreads, 1) update_group_kernel(const Grou
             // this thread's column of the stage's two tile rows; row sv at + sv * 2 * kThreads
             const float* p0 = ring + st * stage_floats + tid;
             const float* p1 = p0 + (R > 1 ? kThreads : 0);
-            float2 g[kGroupMax], cur = make_float2(0.f, 0.f), ld = cur, vr = cur, va = cur;
-            if (live) {
-                const long long key = w.elem0 * 65536 + w.c0;
-                if (key != x_key) {
+            if (!live) {  // past the segment's last column: nothing to fold, hand the stage back
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if ((tid & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[st])) : "memory");
+                continue;
+            }
+            const long long key = w.elem0 * 65536 + w.c0;
+            if (key != x_key) {
 #pragma unroll
-                    for (int k = 0; k < kGroupMax; ++k)
-                        if (k < G) {
-                            const UpdPending& pk = a.pend[k];
-#pragma unroll
-                            for (int b = 0; b < BT; ++b) {
-                                const float* xr_p = w.xin_off >= 0 ? pk.stash + w.xin_off + (size_t)b * w.in
-                                                    : a.x0idx      ? pk.x0 + (size_t)__ldg(a.x0idx + b) * a.x0_ld
-                                                                   : pk.x0 + (size_t)b * a.x0_ld;
-                                xr[k][b] = b < B ? __ldg(xr_p + c) : 0.f;
-                            }
-                        }
-                    x_key = key;
-                }
-                const size_t srow = (size_t)n0 * 2 * kThreads;
-                ld = make_float2(p0[srow], p1[srow]);
-                if (learn) {
-                    vr = make_float2(p0[srow + 2 * kThreads], p1[srow + 2 * kThreads]);
-                    va = make_float2(p0[srow + 4 * kThreads], p1[srow + 4 * kThreads]);
-                }
-                float2 prev = make_float2(p0[0], p1[0]);
-                float2* dq = dsm + tid;
-                for (int sv = 1; sv < n0; ++sv) {
-                    p0 += 2 * kThreads;
-                    p1 += 2 * kThreads;
-                    const float2 nxt = make_float2(*p0, *p1);
-                    *dq = make_float2(nxt.x - prev.x, nxt.y - prev.y);
-                    dq += kThreads;
-                    prev = nxt;
-                }
-                cur = prev;
-                // gradients (padded samples: delta 0 x input 0 adds +0, which leaves g unchanged)
-#pragma unroll
-                for (int k = 0; k < kGroupMax; ++k) {
-                    g[k] = make_float2(0.f, 0.f);
+                for (int k = 0; k < kGroupMax; ++k)
                     if (k < G) {
+                        const UpdPending& pk = a.pend[k];
 #pragma unroll
-                        for (int b = 0; b < BT; ++b) g[k] = __ffma2_rn(sdel[st][k * BT + b], make_float2(xr[k][b], xr[k][b]), g[k]);
+                        for (int b = 0; b < BT; ++b) {
+                            const float* xr_p = w.xin_off >= 0 ? pk.stash + w.xin_off + (size_t)b * w.in
+                                                : a.x0idx      ? pk.x0 + (size_t)__ldg(a.x0idx + b) * a.x0_ld
+                                                               : pk.x0 + (size_t)b * a.x0_ld;
+                            xr[k][b] = b < B ? __ldg(xr_p + c) : 0.f;
+                        }
                     }
+                x_key = key;
+            }
+            constexpr int kRow = 2 * kThreads;  // floats between a row's versions sv and sv + 1
+            auto V = [&](int sv) { return make_float2(p0[(size_t)sv * kRow], p1[(size_t)sv * kRow]); };
+            auto sub2 = [](float2 x, float2 y) { return __fadd2_rn(x, make_float2(-y.x, -y.y)); };  // x - y, exact negation
+            float2 ld = V(n0), vr = make_float2(0.f, 0.f), va = vr;
+            if (learn) {
+                vr = V(n0 + 1);
+                va = V(n0 + 2);
+            }
+            // gradients (padded samples: delta 0 x input 0 adds +0, which leaves g unchanged)
+            float2 g[kGroupMax];
+#pragma unroll
+            for (int k = 0; k < kGroupMax; ++k) {
+                g[k] = make_float2(0.f, 0.f);
+                if (k < G) {
+#pragma unroll
+                    for (int b = 0; b < BT; ++b) g[k] = __ffma2_rn(sdel[st][k * BT + b], make_float2(xr[k][b], xr[k][b]), g[k]);
                 }
             }
-            // hand the stage back: our generic smem accesses ordered before the producer's bulk copies
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if ((tid & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[st])) : "memory");
-            if (!live) continue;
-            auto D = [&](int sv) { return dsm[(size_t)sv * kThreads + tid]; };
             auto fold2 = [](float2 o, float2 lam, float2 d) { return __ffma2_rn(__fmul2_rn(__fmul2_rn(lam, o), o), d, o); };
+            // iter_learn on both rows in f32x2 lanes (the same rounded operations, lane by lane)
+            const float2 lb2 = make_float2(lambda0, lambda0), oma = make_float2(__fsub_rn(1.f, alpha), __fsub_rn(1.f, alpha));
+            const float2 al2 = make_float2(alpha, alpha), neta = make_float2(-eta, -eta), m2 = make_float2(-2.f, -2.f);
+            const float2 nu2 = make_float2(__fmul_rn(2.f, nu), __fmul_rn(2.f, nu));
             auto learn2 = [&](float2 gk, float2 d0) {
-                float2 lam;
-                lam.x = iter_learn(gk.x, d0.x, ld.x, vr.x, va.x, lambda0, alpha, eta, nu);
-                lam.y = iter_learn(gk.y, d0.y, ld.y, vr.y, va.y, lambda0, alpha, eta, nu);
+                float2 lam = __fadd2_rn(lb2, ld);
+                const float2 dv = __fmul2_rn(oma, sub2(gk, vr));
+                const float2 resid = __ffma2_rn(make_float2(-lam.x, -lam.y), va, dv);
+                const float2 grad_l = __ffma2_rn(__fmul2_rn(m2, resid), va, __fmul2_rn(nu2, lam));
+                ld = __ffma2_rn(neta, grad_l, ld);
+                lam = __fadd2_rn(lb2, ld);
+                const float2 og = __fmul2_rn(oma, gk);
+                vr = __ffma2_rn(al2, vr, og);
+                va = __ffma2_rn(al2, va, __fmul2_rn(__fmul2_rn(og, gk), d0));
                 return lam;
             };
             float2 dt[kGroupMax];  // differences appended by the members
             float2 nv[kGroupMax];
+            float2 cur;
             if (interleave) {
                 float2 lam[kGroupMax], o[kGroupMax];
 #pragma unroll
                 for (int k = 0; k < kGroupMax; ++k) {
                     o[k] = g[k];
-                    lam[k] = make_float2(lambda0 + ld.x, lambda0 + ld.y);
-                    if (k < G && learn && fk[k] + 1 < n0 + k) lam[k] = learn2(g[k], D(fk[k]));
+                    lam[k] = __fadd2_rn(lb2, ld);
+                    if (k < G && learn && fk[k] + 1 < n0 + k) lam[k] = learn2(g[k], sub2(V(fk[k] + 1), V(fk[k])));
                 }
-                // segment j of the HBM differences, [fk[j], fk[j + 1]), is folded by members 0..j
+                // the HBM chain's differences in one ascending pass: segment j, [fk[j], fk[j + 1]),
+                // is folded by members 0..j
+                const float* q0 = p0 + (size_t)fk[0] * kRow;
+                const float* q1 = p1 + (size_t)fk[0] * kRow;
+                float2 vp = make_float2(*q0, *q1);
 #pragma unroll
                 for (int j = 0; j < kGroupMax; ++j)
                     if (j < G) {
                         const int hi = j + 1 < G ? fk[j + 1] : n0 - 1;
-                        const float2* dp = dsm + (size_t)fk[j] * kThreads + tid;
-                        for (int sv = fk[j]; sv < hi; ++sv, dp += kThreads) {
-                            const float2 d = *dp;
+                        for (int sv = fk[j]; sv < hi; ++sv) {
+                            q0 += kRow;
+                            q1 += kRow;
+                            const float2 vn = make_float2(*q0, *q1);
+                            const float2 d = sub2(vn, vp);
+                            vp = vn;
 #pragma unroll
                             for (int m = 0; m <= j; ++m) o[m] = fold2(o[m], lam[m], d);
                         }
                     }
+                cur = vp;  // version n0 - 1
 #pragma unroll
                 for (int k = 0; k < kGroupMax; ++k)
                     if (k < G) {
 #pragma unroll
                         for (int j = 0; j < k; ++j) o[k] = fold2(o[k], lam[k], dt[j]);
                         nv[k] = make_float2(sgd_new(cur.x, step, o[k].x), sgd_new(cur.y, step, o[k].y));
-                        dt[k] = make_float2(nv[k].x - cur.x, nv[k].y - cur.y);
+                        dt[k] = sub2(nv[k], cur);
                         cur = nv[k];
                     }
             } else {
+                cur = V(n0 - 1);
 #pragma unroll
                 for (int k = 0; k < kGroupMax; ++k)
                     if (k < G) {
                         const int first = fk[k];
-                        float2 lam = make_float2(lambda0 + ld.x, lambda0 + ld.y);
+                        float2 lam = __fadd2_rn(lb2, ld);
                         if (learn && first + 1 < n0 + k) {
-                            float2 d0 = first < n0 - 1 ? D(first) : dt[0];
+                            float2 d0 = first < n0 - 1 ? sub2(V(first + 1), V(first)) : dt[0];
 #pragma unroll
                             for (int j = 1; j < k; ++j)
                                 if (first == n0 - 1 + j) d0 = dt[j];
                             lam = learn2(g[k], d0);
                         }
                         float2 o = g[k];
-                        for (int sv = first; sv + 1 < n0; ++sv) o = fold2(o, lam, D(sv));
+                        if (first + 1 < n0) {
+                            float2 vp = V(first);
+                            for (int sv = first; sv + 1 < n0; ++sv) {
+                                const float2 vn = V(sv + 1);
+                                o = fold2(o, lam, sub2(vn, vp));
+                                vp = vn;
+                            }
+                        }
 #pragma unroll
                         for (int j = 0; j < k; ++j)
                             if (n0 - 1 + j >= first) o = fold2(o, lam, dt[j]);
                         nv[k] = make_float2(sgd_new(cur.x, step, o.x), sgd_new(cur.y, step, o.y));
-                        dt[k] = make_float2(nv[k].x - cur.x, nv[k].y - cur.y);
+                        dt[k] = sub2(nv[k], cur);
                         cur = nv[k];
                     }
             }
+            // hand the stage back: our smem reads ordered before the producer's next bulk copies
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if ((tid & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[st])) : "memory");
             const size_t e0 = (size_t)w.elem0 + (size_t)w.r0 * w.in + c, e1 = e0 + (size_t)w.in;
 #pragma unroll
             for (int k = 0; k < kGroupMax; ++k)
