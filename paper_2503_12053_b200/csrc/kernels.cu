@@ -1088,49 +1088,53 @@ __global__ void __launch_bounds__(kThreads) update_stream_kernel(const UpdArgs a
 // update_group_kernel: G <= kGroupMax consecutive iter_fisher updates of one large dense stage
 // in one launch (GroupArgs, kernels.cuh): the version chain and the compensator state cross
 // HBM once for the whole group instead of once per update. Persistent and warp-specialised:
-// one CTA per SM walks a contiguous range of 2-row x 256-column tiles (column-block major: a
+// one CTA per SM walks a contiguous range of 4-row x 128-column tiles (column-block major: a
 // thread keeps its column's unit inputs of all members in registers while the block lasts).
 // A producer warp keeps as many tiles in flight as fit in smem (a stage: the tile's chain and
-// compensator state rows, landed by 1 KB bulk copies on the stage's full barrier, plus its
-// descriptor and the members' deltas of its two rows); the 8 consumer warps turn the stage's
-// chain into successive DIFFERENCES (D[s] = v[s+1] - v[s], the same fp32 values
-// update_iter1_kernel computes from the stored versions) in a per-thread float2 array, form the
-// members' gradients, and hand the stage back (empty barrier) before folding: the learning
-// steps run member after member (they chain the compensator state), then the members' folds
-// over the HBM part of the chain run interleaved (one difference load feeds every member whose
-// fold covers it; each member's operations stay in its own order), then member k folds the
-// k differences its predecessors appended, writes version n0 + k and appends its own. Launches
-// where a member's learning step reads an appended difference (it read the live version) fold
-// member after member instead. Bias runs (a thread: one element) follow with direct loads.
-// Per element the arithmetic is update_iter1_kernel's, update after update (bit-identical).
+// compensator state rows, landed by 512-byte bulk copies on the stage's full barrier, plus its
+// descriptor and the members' deltas of its four rows). Two consumer teams of 4 warps take
+// alternate tiles, so two tiles fold at once; a thread owns one column of its tile and all
+// four rows, as two f32x2 lane pairs (rows 0-1, rows 2-3): two independent dependency chains
+// per thread next to the other team's. A thread forms the members' gradients, runs the
+// learning steps member after member (they chain the compensator state), folds the members
+// over the HBM part of the chain interleaved (segment j of the chain, between members j and
+// j+1's read versions, is folded by members 0..j: one difference feeds each), hands the stage
+// back (empty barrier), then member k folds the k differences its predecessors appended,
+// writes version n0 + k and appends its own. Launches where a member's learning step reads an
+// appended difference (it read the live version) fold member after member instead. Bias runs
+// (a thread: one element) follow with direct loads. Per element the arithmetic is
+// update_iter1_kernel's, update after update (bit-identical).
 // ---------------------------------------------------------------------------
 constexpr int kGroupChainRows = kGroupChainMax - 1;  // differences of the HBM chain (n0 <= kGroupChainMax - 1)
 constexpr int kGrpMaxStages = 8;
-constexpr int kGrpThreads = kThreads + 32;  // 8 consumer warps + the producer warp
-constexpr size_t kGrpSmem = 220 * 1024;     // the stage ring
+constexpr int kGrpTeam = kGroupCols;        // consumer threads per team (a thread: one column)
+constexpr int kGrpThreads = 3 * kGrpTeam;  // two consumer warpgroups + the producer warpgroup (one warp working)
+constexpr size_t kGrpSmem = 212 * 1024;     // the stage ring
 
 template <int BT>
-__global__ void __launch_bounds__(kGrpThreads, 1) update_group_kernel(const GroupArgs a) {
-    static_assert(kGroupRows == 2, "the group kernel packs its two rows into float2 lanes");
+__global__ void __launch_bounds__(kGrpThreads, 1) update_group_kernel(const __grid_constant__ GroupArgs a) {
+    static_assert(kGroupRows == 4, "a consumer thread packs its four rows into two f32x2 lane pairs");
     static_assert(kGroupMax * BT <= 64, "a producer lane stages at most two deltas per tile");
     FB_PDL_ENTRY();
     extern __shared__ __align__(128) float gsm[];
-    float* ring = gsm;  // [S][n_rows][2][kThreads]
-    __shared__ float2 sdel[kGrpMaxStages][kGroupMax * BT];  // per stage: member k, sample b (rows r0, r0 + 1)
+    float* ring = gsm;  // [S][n_rows][4][kGroupCols]
+    __shared__ float4 sdel[kGrpMaxStages][kGroupMax * BT];  // per stage: member k, sample b (rows r0 .. r0 + 3)
     __shared__ UpdWork wsm[kGrpMaxStages];
     __shared__ __align__(8) uint64_t full[kGrpMaxStages], empty[kGrpMaxStages];
     const int tid = threadIdx.x, B = a.B, G = a.G, n0 = a.n0;
     const bool learn = a.learn != 0;
     const int n_rows = n0 + (learn ? 3 : 1);  // bulk-copied rows per tile row: the chain, then the state
-    const size_t stage_floats = (size_t)n_rows * 2 * kThreads;
+    constexpr int kRow = kGroupRows * kGroupCols;  // floats between a row's versions sv and sv + 1
+    const size_t stage_floats = (size_t)n_rows * kRow;
     const int S = min(kGrpMaxStages, (int)(kGrpSmem / (stage_floats * sizeof(float))));
     // this CTA's contiguous range of weight tiles
     const int per = (a.n_wtiles + gridDim.x - 1) / gridDim.x;
     const int t0 = min(a.n_wtiles, (int)blockIdx.x * per), t1 = min(a.n_wtiles, t0 + per);
     if (tid == 0) {
         for (int q = 0; q < S; ++q) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&full[q])) : "memory");
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(&empty[q])), "r"(kThreads / 32) : "memory");
+            // full: an expect_tx arrival per producer warp + one cp.async (deltas) arrival per lane of warp 0
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 36;" ::"r"(smem_addr(&full[q])) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(&empty[q])), "r"(kGrpTeam / 32) : "memory");
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -1144,60 +1148,79 @@ __global__ void __launch_bounds__(kGrpThreads, 1) update_group_kernel(const Grou
                          : "r"(smem_addr(b)), "r"(parity)
                          : "memory");
     };
-    if (tid >= kThreads) {  // ---- producer warp: descriptors and deltas loaded a tile ahead
-        const int lane = tid - kThreads;
-        auto load_w = [&](int t) {
+    // 12 warps = 3 per SM sub-partition at launch (<= 168 registers each); the producer
+    // warpgroup hands registers to the consumer warpgroups (setmaxnreg), which need ~190
+    if (tid >= 2 * kGrpTeam) {  // ---- producer warp: descriptors and deltas loaded a tile ahead
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+        // the warpgroup's four warps share a tile's bulk copies (each copy is issued lane after lane
+        // on the uniform datapath: one warp alone cannot issue them as fast as HBM delivers); warp 0
+        // also writes the descriptor and stages the deltas
+        const int pw = (tid - 2 * kGrpTeam) >> 5, lane = tid & 31;
+        // no global loads on this warp's path: a tile's position is decoded from the segment table
+        // (kernel parameters) and its deltas land by cp.async on the stage's full barrier
+        auto decode = [&](int t) {
+            int s = 0;
+            while (s + 1 < a.n_gsegs && t >= a.gseg[s + 1].tile0) ++s;
+            const GroupSeg& gs = a.gseg[s];
+            const int local = t - gs.tile0, cb = local / gs.nrt, rt = local - cb * gs.nrt;
             UpdWork w{};
-            if (t < t1) w = a.works[t];
+            w.elem0 = gs.elem0;
+            w.xin_off = gs.xin_off;
+            w.dlt_off = gs.dlt_off;
+            w.in = gs.in;
+            w.out = gs.out;
+            w.r0 = rt * kGroupRows;
+            w.nrows = min(kGroupRows, gs.out - w.r0);
+            w.c0 = cb * kGroupCols;
             return w;
         };
-        auto load_d = [&](const UpdWork& w, int t, float2* d) {
-            for (int h = 0; h < 2; ++h) {
-                const int q = lane + 32 * h, b = q % BT, k = q / BT;
-                d[h] = make_float2(0.f, 0.f);
-                if (t < t1 && k < G && b < B) {
-                    const float* dl = a.pend[k].stash + w.dlt_off + (size_t)b * w.out + w.r0;
-                    d[h] = make_float2(__ldg(dl), __ldg(dl + (w.nrows > 1 ? 1 : 0)));
-                }
-            }
-        };
-        UpdWork w_cur = load_w(t0), w_nxt = load_w(t0 + 1);
-        float2 d_cur[2], d_nxt[2];
-        load_d(w_cur, t0, d_cur);
         for (int t = t0, it = 0; t < t1; ++t, ++it) {
             const int st = it % S;
-            const UpdWork w_nn = load_w(t + 2);
-            load_d(w_nxt, t + 1, d_nxt);
+            const UpdWork w = decode(t);
             if (it >= S) wait_bar(&empty[st], ((it / S) - 1) & 1);
-            const UpdWork& w = w_cur;
-            const int R = w.nrows, ncols = min(kThreads, w.in - w.c0);
-            if (lane == 0) wsm[st] = w;
-            for (int h = 0; h < 2; ++h)
-                if (lane + 32 * h < G * BT) sdel[st][lane + 32 * h] = d_cur[h];
+            const int R = w.nrows, ncols = min(kGroupCols, w.in - w.c0);
+            if (pw == 0 && lane == 0) wsm[st] = w;
+            // deltas of member k, sample b, rows r0 .. r0 + 3 (rows past the tile's last alias it,
+            // padded members / samples are zero-filled); each lane's copies arrive on full[st]
+            for (int h = 0; h < 2 && pw == 0; ++h) {
+                const int q = lane + 32 * h, b = q % BT, k = q / BT;
+                if (q >= kGroupMax * BT) break;
+                const bool ok = k < G && b < B;
+                const float* dl = ok ? a.pend[k].stash + w.dlt_off + (size_t)b * w.out + w.r0 : a.vers[0];
+                const uint32_t dst = smem_addr(&sdel[st][q]);
+#pragma unroll
+                for (int i = 0; i < kGroupRows; ++i)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst + 4 * i), "l"(dl + (ok ? min(i, R - 1) : 0)),
+                                 "r"(ok ? 4 : 0)
+                                 : "memory");
+            }
+            if (pw == 0) asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(&full[st])) : "memory");
             __syncwarp();
             const uint32_t row_bytes = static_cast<uint32_t>(ncols) * 4u;
-            if (lane == 0)  // release: the descriptor and deltas above, then the copies' bytes
+            const int n_copy = n_rows * R;
+            int mine = 0;  // copies q = pw * 32 + lane + 128 j < n_copy
+            for (int q = pw * 32; q < n_copy; q += 128) mine += min(32, n_copy - q);
+            // (warp 0) release: the descriptor above; every warp: the bytes of its copies
+            if (lane == 0)
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&full[st])),
-                             "r"(row_bytes * (uint32_t)(n_rows * R))
+                             "r"(row_bytes * (uint32_t)mine)
                              : "memory");
             __syncwarp();
             float* stage = ring + st * stage_floats;
-            for (int q = lane; q < n_rows * R; q += 32) {
+            for (int q = pw * 32 + lane; q < n_copy; q += 128) {
                 const int sv = q / R, i = q - sv * R;
                 const size_t off = (size_t)w.elem0 + (size_t)(w.r0 + i) * w.in + w.c0;
                 const int state = sv - n0;  // >= 0: lam_d, v_r, v_a
                 const float* src = state < 0 ? a.vers[sv] + off : (state == 0 ? a.lam_d : state == 1 ? a.v_r : a.v_a) + off;
                 asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                                 smem_addr(stage + (size_t)(sv * 2 + i) * kThreads)),
+                                 smem_addr(stage + (size_t)(sv * kGroupRows + i) * kGroupCols)),
                              "l"(src), "r"(row_bytes), "r"(smem_addr(&full[st]))
                              : "memory");
             }
-            w_cur = w_nxt;
-            w_nxt = w_nn;
-            d_cur[0] = d_nxt[0];
-            d_cur[1] = d_nxt[1];
         }
-    } else {  // ---- consumer warps: thread tid owns column c0 + tid of every tile
+    } else {  // ---- consumer teams: team tm takes tiles it = tm, tm + 2, ...; thread lc owns column c0 + lc
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
+        const int tm = tid / kGrpTeam, lc = tid - tm * kGrpTeam;
         // members' read versions (first chain index), uniform over the launch
         int fk[kGroupMax];
         bool interleave = true;  // read versions ascending, learning steps on HBM differences only
@@ -1210,19 +1233,23 @@ __global__ void __launch_bounds__(kGrpThreads, 1) update_group_kernel(const Grou
         const float lambda0 = a.lambda0, alpha = a.alpha, eta = a.eta, nu = a.nu, step = a.step;
         float xr[kGroupMax][BT];  // unit inputs x_k[b][c] of the current column block (0 past B)
         long long x_key = -1;
-        for (int t = t0, it = 0; t < t1; ++t, ++it) {
+        const float2 lb2 = make_float2(lambda0, lambda0), oma = make_float2(__fsub_rn(1.f, alpha), __fsub_rn(1.f, alpha));
+        const float2 al2 = make_float2(alpha, alpha), neta = make_float2(-eta, -eta), m2 = make_float2(-2.f, -2.f);
+        const float2 nu2 = make_float2(__fmul_rn(2.f, nu), __fmul_rn(2.f, nu));
+        auto sub2 = [](float2 x, float2 y) { return __fadd2_rn(x, make_float2(-y.x, -y.y)); };  // x - y, exact negation
+        auto fold2 = [](float2 o, float2 lam, float2 d) { return __ffma2_rn(__fmul2_rn(__fmul2_rn(lam, o), o), d, o); };
+        for (int t = t0 + tm, it = tm; t < t1; t += 2, it += 2) {
             const int st = it % S;
             wait_bar(&full[st], (it / S) & 1);
             const UpdWork w = wsm[st];
-            const int R = w.nrows, c = w.c0 + tid;
-            const bool live = c < w.in;
-            // this thread's column of the stage's two tile rows; row sv at + sv * 2 * kThreads
-            const float* p0 = ring + st * stage_floats + tid;
-            const float* p1 = p0 + (R > 1 ? kThreads : 0);
-            if (!live) {  // past the segment's last column: nothing to fold, hand the stage back
+            const int R = w.nrows, c = w.c0 + lc;
+            auto release = [&] {  // our smem reads ordered before the producer's next bulk copies
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
                 if ((tid & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[st])) : "memory");
+            };
+            if (c >= w.in) {  // past the segment's last column: nothing to fold, hand the stage back
+                release();
                 continue;
             }
             const long long key = w.elem0 * 65536 + w.c0;
@@ -1241,139 +1268,147 @@ __global__ void __launch_bounds__(kGrpThreads, 1) update_group_kernel(const Grou
                     }
                 x_key = key;
             }
-            constexpr int kRow = 2 * kThreads;  // floats between a row's versions sv and sv + 1
-            auto V = [&](int sv) { return make_float2(p0[(size_t)sv * kRow], p1[(size_t)sv * kRow]); };
-            auto sub2 = [](float2 x, float2 y) { return __fadd2_rn(x, make_float2(-y.x, -y.y)); };  // x - y, exact negation
-            float2 ld = V(n0), vr = make_float2(0.f, 0.f), va = vr;
-            if (learn) {
-                vr = V(n0 + 1);
-                va = V(n0 + 2);
+            // this thread's column of the stage's four tile rows (rows past R alias row R - 1)
+            const float* pr[kGroupRows];
+#pragma unroll
+            for (int i = 0; i < kGroupRows; ++i) pr[i] = ring + st * stage_floats + (size_t)min(i, R - 1) * kGroupCols + lc;
+            auto V = [&](int p, int sv) { return make_float2(pr[2 * p][(size_t)sv * kRow], pr[2 * p + 1][(size_t)sv * kRow]); };
+            float2 ld[2], vr[2], va[2];
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                ld[p] = V(p, n0);
+                vr[p] = learn ? V(p, n0 + 1) : make_float2(0.f, 0.f);
+                va[p] = learn ? V(p, n0 + 2) : make_float2(0.f, 0.f);
             }
             // gradients (padded samples: delta 0 x input 0 adds +0, which leaves g unchanged)
-            float2 g[kGroupMax];
+            float2 g[kGroupMax][2];
 #pragma unroll
             for (int k = 0; k < kGroupMax; ++k) {
-                g[k] = make_float2(0.f, 0.f);
+                g[k][0] = g[k][1] = make_float2(0.f, 0.f);
                 if (k < G) {
 #pragma unroll
-                    for (int b = 0; b < BT; ++b) g[k] = __ffma2_rn(sdel[st][k * BT + b], make_float2(xr[k][b], xr[k][b]), g[k]);
+                    for (int b = 0; b < BT; ++b) {
+                        const float4 dd = sdel[st][k * BT + b];
+                        const float2 xx = make_float2(xr[k][b], xr[k][b]);
+                        g[k][0] = __ffma2_rn(make_float2(dd.x, dd.y), xx, g[k][0]);
+                        g[k][1] = __ffma2_rn(make_float2(dd.z, dd.w), xx, g[k][1]);
+                    }
                 }
             }
-            auto fold2 = [](float2 o, float2 lam, float2 d) { return __ffma2_rn(__fmul2_rn(__fmul2_rn(lam, o), o), d, o); };
-            // iter_learn on both rows in f32x2 lanes (the same rounded operations, lane by lane)
-            const float2 lb2 = make_float2(lambda0, lambda0), oma = make_float2(__fsub_rn(1.f, alpha), __fsub_rn(1.f, alpha));
-            const float2 al2 = make_float2(alpha, alpha), neta = make_float2(-eta, -eta), m2 = make_float2(-2.f, -2.f);
-            const float2 nu2 = make_float2(__fmul_rn(2.f, nu), __fmul_rn(2.f, nu));
-            auto learn2 = [&](float2 gk, float2 d0) {
-                float2 lam = __fadd2_rn(lb2, ld);
-                const float2 dv = __fmul2_rn(oma, sub2(gk, vr));
-                const float2 resid = __ffma2_rn(make_float2(-lam.x, -lam.y), va, dv);
-                const float2 grad_l = __ffma2_rn(__fmul2_rn(m2, resid), va, __fmul2_rn(nu2, lam));
-                ld = __ffma2_rn(neta, grad_l, ld);
-                lam = __fadd2_rn(lb2, ld);
+            // iter_learn in f32x2 lanes (the same rounded operations, lane by lane)
+            auto learn2 = [&](int p, float2 gk, float2 d0) {
+                float2 lam = __fadd2_rn(lb2, ld[p]);
+                const float2 dv = __fmul2_rn(oma, sub2(gk, vr[p]));
+                const float2 resid = __ffma2_rn(make_float2(-lam.x, -lam.y), va[p], dv);
+                const float2 grad_l = __ffma2_rn(__fmul2_rn(m2, resid), va[p], __fmul2_rn(nu2, lam));
+                ld[p] = __ffma2_rn(neta, grad_l, ld[p]);
+                lam = __fadd2_rn(lb2, ld[p]);
                 const float2 og = __fmul2_rn(oma, gk);
-                vr = __ffma2_rn(al2, vr, og);
-                va = __ffma2_rn(al2, va, __fmul2_rn(__fmul2_rn(og, gk), d0));
+                vr[p] = __ffma2_rn(al2, vr[p], og);
+                va[p] = __ffma2_rn(al2, va[p], __fmul2_rn(__fmul2_rn(og, gk), d0));
                 return lam;
             };
-            float2 dt[kGroupMax];  // differences appended by the members
-            float2 nv[kGroupMax];
-            float2 cur;
-            if (interleave) {
-                float2 lam[kGroupMax], o[kGroupMax];
-#pragma unroll
-                for (int k = 0; k < kGroupMax; ++k) {
-                    o[k] = g[k];
-                    lam[k] = __fadd2_rn(lb2, ld);
-                    if (k < G && learn && fk[k] + 1 < n0 + k) lam[k] = learn2(g[k], sub2(V(fk[k] + 1), V(fk[k])));
+            const size_t e0 = (size_t)w.elem0 + (size_t)w.r0 * w.in + c;
+            auto store = [&](float* dk, unsigned short* dk16, int p, float2 v) {  // rows 2p, 2p + 1 if inside the tile
+                const size_t ea = e0 + (size_t)(2 * p) * w.in, eb = ea + (size_t)w.in;
+                if (2 * p < R) {
+                    dk[ea] = v.x;
+                    if (dk16) reinterpret_cast<__nv_bfloat16*>(dk16)[ea] = __float2bfloat16_rn(v.x);
                 }
+                if (2 * p + 1 < R) {
+                    dk[eb] = v.y;
+                    if (dk16) reinterpret_cast<__nv_bfloat16*>(dk16)[eb] = __float2bfloat16_rn(v.y);
+                }
+            };
+            float2 dt[kGroupMax][2];  // differences appended by the members
+            float2 cur[2];
+            if (interleave) {
+                float2 lam[kGroupMax][2], o[kGroupMax][2];
+#pragma unroll
+                for (int k = 0; k < kGroupMax; ++k)
+#pragma unroll
+                    for (int p = 0; p < 2; ++p) {
+                        o[k][p] = g[k][p];
+                        lam[k][p] = __fadd2_rn(lb2, ld[p]);
+                        if (k < G && learn && fk[k] + 1 < n0 + k) lam[k][p] = learn2(p, g[k][p], sub2(V(p, fk[k] + 1), V(p, fk[k])));
+                    }
                 // the HBM chain's differences in one ascending pass: segment j, [fk[j], fk[j + 1]),
                 // is folded by members 0..j
-                const float* q0 = p0 + (size_t)fk[0] * kRow;
-                const float* q1 = p1 + (size_t)fk[0] * kRow;
-                float2 vp = make_float2(*q0, *q1);
+                float2 vp[2] = {V(0, fk[0]), V(1, fk[0])};
 #pragma unroll
                 for (int j = 0; j < kGroupMax; ++j)
                     if (j < G) {
                         const int hi = j + 1 < G ? fk[j + 1] : n0 - 1;
                         for (int sv = fk[j]; sv < hi; ++sv) {
-                            q0 += kRow;
-                            q1 += kRow;
-                            const float2 vn = make_float2(*q0, *q1);
-                            const float2 d = sub2(vn, vp);
-                            vp = vn;
 #pragma unroll
-                            for (int m = 0; m <= j; ++m) o[m] = fold2(o[m], lam[m], d);
+                            for (int p = 0; p < 2; ++p) {
+                                const float2 vn = V(p, sv + 1);
+                                const float2 d = sub2(vn, vp[p]);
+                                vp[p] = vn;
+#pragma unroll
+                                for (int m = 0; m <= j; ++m) o[m][p] = fold2(o[m][p], lam[m][p], d);
+                            }
                         }
                     }
-                cur = vp;  // version n0 - 1
+                release();
+                cur[0] = vp[0];  // version n0 - 1
+                cur[1] = vp[1];
 #pragma unroll
                 for (int k = 0; k < kGroupMax; ++k)
-                    if (k < G) {
+                    if (k < G)
 #pragma unroll
-                        for (int j = 0; j < k; ++j) o[k] = fold2(o[k], lam[k], dt[j]);
-                        nv[k] = make_float2(sgd_new(cur.x, step, o[k].x), sgd_new(cur.y, step, o[k].y));
-                        dt[k] = sub2(nv[k], cur);
-                        cur = nv[k];
-                    }
+                        for (int p = 0; p < 2; ++p) {
+                            float2 ok = o[k][p];
+#pragma unroll
+                            for (int j = 0; j < k; ++j) ok = fold2(ok, lam[k][p], dt[j][p]);
+                            const float2 nv = make_float2(sgd_new(cur[p].x, step, ok.x), sgd_new(cur[p].y, step, ok.y));
+                            dt[k][p] = sub2(nv, cur[p]);
+                            cur[p] = nv;
+                            store(a.dst[k], a.dst16[k], p, nv);
+                        }
             } else {
-                cur = V(n0 - 1);
+                cur[0] = V(0, n0 - 1);
+                cur[1] = V(1, n0 - 1);
 #pragma unroll
                 for (int k = 0; k < kGroupMax; ++k)
                     if (k < G) {
                         const int first = fk[k];
-                        float2 lam = __fadd2_rn(lb2, ld);
-                        if (learn && first + 1 < n0 + k) {
-                            float2 d0 = first < n0 - 1 ? sub2(V(first + 1), V(first)) : dt[0];
 #pragma unroll
-                            for (int j = 1; j < k; ++j)
-                                if (first == n0 - 1 + j) d0 = dt[j];
-                            lam = learn2(g[k], d0);
-                        }
-                        float2 o = g[k];
-                        if (first + 1 < n0) {
-                            float2 vp = V(first);
-                            for (int sv = first; sv + 1 < n0; ++sv) {
-                                const float2 vn = V(sv + 1);
-                                o = fold2(o, lam, sub2(vn, vp));
-                                vp = vn;
+                        for (int p = 0; p < 2; ++p) {
+                            float2 lam = __fadd2_rn(lb2, ld[p]);
+                            if (learn && first + 1 < n0 + k) {
+                                float2 d0 = first < n0 - 1 ? sub2(V(p, first + 1), V(p, first)) : dt[0][p];
+#pragma unroll
+                                for (int j = 1; j < k; ++j)
+                                    if (first == n0 - 1 + j) d0 = dt[j][p];
+                                lam = learn2(p, g[k][p], d0);
                             }
+                            float2 o = g[k][p];
+                            if (first + 1 < n0) {
+                                float2 vp = V(p, first);
+                                for (int sv = first; sv + 1 < n0; ++sv) {
+                                    const float2 vn = V(p, sv + 1);
+                                    o = fold2(o, lam, sub2(vn, vp));
+                                    vp = vn;
+                                }
+                            }
+#pragma unroll
+                            for (int j = 0; j < k; ++j)
+                                if (n0 - 1 + j >= first) o = fold2(o, lam, dt[j][p]);
+                            const float2 nv = make_float2(sgd_new(cur[p].x, step, o.x), sgd_new(cur[p].y, step, o.y));
+                            dt[k][p] = sub2(nv, cur[p]);
+                            cur[p] = nv;
+                            store(a.dst[k], a.dst16[k], p, nv);
                         }
-#pragma unroll
-                        for (int j = 0; j < k; ++j)
-                            if (n0 - 1 + j >= first) o = fold2(o, lam, dt[j]);
-                        nv[k] = make_float2(sgd_new(cur.x, step, o.x), sgd_new(cur.y, step, o.y));
-                        dt[k] = sub2(nv[k], cur);
-                        cur = nv[k];
                     }
+                release();
             }
-            // hand the stage back: our smem reads ordered before the producer's next bulk copies
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if ((tid & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[st])) : "memory");
-            const size_t e0 = (size_t)w.elem0 + (size_t)w.r0 * w.in + c, e1 = e0 + (size_t)w.in;
 #pragma unroll
-            for (int k = 0; k < kGroupMax; ++k)
-                if (k < G) {
-                    float* dk = a.dst[k];
-                    unsigned short* dk16 = a.dst16[k];
-                    dk[e0] = nv[k].x;
-                    if (dk16) reinterpret_cast<__nv_bfloat16*>(dk16)[e0] = __float2bfloat16_rn(nv[k].x);
-                    if (R > 1) {
-                        dk[e1] = nv[k].y;
-                        if (dk16) reinterpret_cast<__nv_bfloat16*>(dk16)[e1] = __float2bfloat16_rn(nv[k].y);
-                    }
-                }
-            a.lam_d[e0] = ld.x;
-            if (learn) {
-                a.v_r[e0] = vr.x;
-                a.v_a[e0] = va.x;
-            }
-            if (R > 1) {
-                a.lam_d[e1] = ld.y;
+            for (int p = 0; p < 2; ++p) {
+                store(a.lam_d, nullptr, p, ld[p]);
                 if (learn) {
-                    a.v_r[e1] = vr.y;
-                    a.v_a[e1] = va.y;
+                    store(a.v_r, nullptr, p, vr[p]);
+                    store(a.v_a, nullptr, p, va[p]);
                 }
             }
         }
@@ -1381,7 +1416,7 @@ __global__ void __launch_bounds__(kGrpThreads, 1) update_group_kernel(const Grou
     // bias runs (after the weight tiles): a thread per element, direct loads
     for (int t = a.n_wtiles + blockIdx.x; t < a.n_tiles; t += gridDim.x) {
         const UpdWork w = a.works[t];
-        if (tid >= w.nrows || tid >= kThreads) continue;
+        if (tid >= w.nrows || tid >= 2 * kGrpTeam) continue;
         const size_t e = (size_t)w.elem0 + w.r0 + tid;
         float prev = __ldg(a.vers[0] + e);
         float d[kGroupChainRows];

@@ -159,9 +159,20 @@ struct UpdArgs {
 // members past the nodes in between never changes what any node reads.
 constexpr int kGroupMax = 4;         // updates per group (their unit inputs are staged in smem)
 constexpr int kGroupChainMax = 24;   // versions a group spans: HBM chain + its own outputs
-constexpr int kGroupRows = 2;        // weight rows per tile (a tile: 2 rows x 256 columns, a thread: one column)
+constexpr int kGroupRows = 4;        // weight rows per tile (a tile: 4 rows x 128 columns, a thread: one column)
+constexpr int kGroupCols = 128;      // weight columns per tile
+// A weight segment of a group stage: its tiles are tile0 .. tile0 + ceil(in / kGroupCols) * nrt - 1,
+// column block after column block, nrt = ceil(out / kGroupRows) row tiles each (the producer decodes a
+// tile's position arithmetically instead of loading its UpdWork)
+constexpr int kGroupMaxSegs = 8;
+struct GroupSeg {
+    long long elem0, xin_off, dlt_off;
+    int in, out, tile0, nrt;
+};
 struct GroupArgs {
-    const UpdWork* works;            // the stage's group tiles: weights (<= 2 rows x 256 columns, column
+    int n_gsegs;
+    GroupSeg gseg[kGroupMaxSegs];
+    const UpdWork* works;            // the stage's group tiles: weights (<= 4 rows x 128 columns, column
                                      // block major) first, then bias runs of 256
     int n_tiles, n_wtiles;           // all tiles / weight tiles
     int B, G, n0;                    // micro-batch, updates, chain versions read from HBM

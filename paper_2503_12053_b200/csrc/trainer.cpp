@@ -193,6 +193,7 @@ struct StageDev {
     int n_tiles = 0;
     fb200::UpdWork* works_g_dev = nullptr;  // update-group tiles (kernels.cuh GroupArgs::works)
     int n_tiles_g = 0, n_wtiles_g = 0;
+    std::vector<fb200::GroupSeg> gsegs;  // the weight segments' tile ranges (GroupArgs::gseg)
     bool group_ok = false;  // update groups apply: a large dense stage with 16-byte aligned weight rows
     long long n_items = 0;
     // slot of a version counted from the chunk start (the live version is in slot 0 between chunks)
@@ -962,17 +963,25 @@ struct ferret_trainer {
             // (default 8M), weight rows 16-byte aligned for the kernel's bulk copies
             s.group_ok = group_updates && !s.gmat && opt.policy == FERRET_POLICY_ITER_FISHER &&
                          s.slot_floats >= group_min_params;
-            for (const fb200::UpdSeg& sg : tab)
+            int n_wsegs = 0;
+            for (const fb200::UpdSeg& sg : tab) {
                 if (!sg.bias && sg.in % 4 != 0) s.group_ok = false;
-            if (s.group_ok) {  // tiles: kGroupRows rows x 256 columns, column-block major (a CTA's
+                n_wsegs += sg.bias ? 0 : 1;
+            }
+            if (n_wsegs > fb200::kGroupMaxSegs) s.group_ok = false;
+            s.gsegs.clear();
+            if (s.group_ok) {  // tiles: kGroupRows rows x kGroupCols columns, column-block major (a CTA's
                                // range shares its column block's unit inputs), then bias runs of 256
                 std::vector<fb200::UpdWork> wg;
                 for (const fb200::UpdSeg& sg : tab)
-                    if (!sg.bias)
-                        for (int c0 = 0; c0 < sg.in; c0 += fb200::kUpdTileCols)
+                    if (!sg.bias) {
+                        s.gsegs.push_back({sg.elem0, sg.xin_off, sg.dlt_off, sg.in, sg.out, static_cast<int>(wg.size()),
+                                           (sg.out + fb200::kGroupRows - 1) / fb200::kGroupRows});
+                        for (int c0 = 0; c0 < sg.in; c0 += fb200::kGroupCols)
                             for (int r0 = 0; r0 < sg.out; r0 += fb200::kGroupRows)
                                 wg.push_back({sg.elem0, sg.xin_off, sg.dlt_off, sg.in, sg.out, 0, r0,
                                               std::min(fb200::kGroupRows, sg.out - r0), c0, sg.g_off});
+                    }
                 s.n_wtiles_g = static_cast<int>(wg.size());
                 for (const fb200::UpdSeg& sg : tab)
                     if (sg.bias)
@@ -1589,6 +1598,8 @@ struct ferret_trainer {
             }
             fb200::GroupArgs a{};
             a.works = sd.works_g_dev;
+            a.n_gsegs = static_cast<int>(sd.gsegs.size());
+            for (size_t q = 0; q < sd.gsegs.size(); ++q) a.gseg[q] = sd.gsegs[q];
             a.n_tiles = sd.n_tiles_g;
             a.n_wtiles = sd.n_wtiles_g;
             a.B = B;
