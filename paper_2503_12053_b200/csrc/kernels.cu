@@ -1268,11 +1268,13 @@ __global__ void __launch_bounds__(kGrpThreads, 1) update_group_kernel(const __gr
                     }
                 x_key = key;
             }
-            // this thread's column of the stage's four tile rows (rows past R alias row R - 1)
-            const float* pr[kGroupRows];
-#pragma unroll
-            for (int i = 0; i < kGroupRows; ++i) pr[i] = ring + st * stage_floats + (size_t)min(i, R - 1) * kGroupCols + lc;
-            auto V = [&](int p, int sv) { return make_float2(pr[2 * p][(size_t)sv * kRow], pr[2 * p + 1][(size_t)sv * kRow]); };
+            // this thread's column of the stage's four tile rows: one base, the rows at immediate
+            // offsets (rows past R hold an earlier tile's values: folded, never stored)
+            const float* pb = ring + st * stage_floats + lc;
+            auto V = [&](int p, int sv) {
+                const float* q = pb + sv * kRow + 2 * p * kGroupCols;
+                return make_float2(q[0], q[kGroupCols]);
+            };
             float2 ld[2], vr[2], va[2];
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
