@@ -8,4 +8,5 @@ python bench.py > gpurun_out/bench.log 2>&1
 timeout 600 python profiles/c2_tc.py > gpurun_out/c2_tc.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches.csv \
   python bench.py --steps 1 --warmup 1 --no-cpu --no-side > gpurun_out/ncu_bench.log 2>&1
+timeout 600 python profiles/timeline.py c5 gpurun_out/timeline_c5 > gpurun_out/timeline_c5.log 2>&1
 tail -3 gpurun_out/gpu_tests.log; tail -2 gpurun_out/smoke.log; tail -1 gpurun_out/bench.log | cut -c1-600; cat gpurun_out/c2_tc.log
