@@ -114,6 +114,18 @@ def test_groups_odd_rows_and_unaligned_stage(gpu, fb):
     _same(g, u)
 
 
+def test_groups_many_layer_stage(gpu, fb):
+    """A stage of more weight segments than the group kernel's segment table holds (kGroupMaxSegs = 8)
+    keeps single updates; the 2-layer stage next to it groups (24-column rows, a 2-row tail tile);
+    results bit-identical."""
+    widths = [64] * 10 + [24, 10]
+    bounds = [0, 9, 11]
+    params, sched, feats, labels = _mlp_case(fb, widths, bounds, 48, 4, n_chunks=2)
+    g = _train(fb, widths, params, bounds, sched, feats, labels, 48 * 4, 2, True, profile=True, micro_batch=4)
+    u = _train(fb, widths, params, bounds, sched, feats, labels, 48 * 4, 2, False, micro_batch=4)
+    _same(g, u)
+
+
 def test_groups_skip_conv_stages(gpu, fb):
     """Conv stages (materialised gradients) never group; the trainer is unchanged."""
     cn = fb.convnet
