@@ -636,7 +636,12 @@ MmaGeom mma_geom(bool bf16, bool bwd, int in, int out, bool split) {
         const int M = bwd ? in : out, K = bwd ? out : in;
         g.mtiles = (M + 127) / 128;
         g.katoms = static_cast<int>((static_cast<long long>(K) * es + 127) / 128);
-        int S = 2 * 148 / g.mtiles;
+        // K splits: about 96 CTAs per layer (two thirds of the SMs at one CTA each), not the one full
+        // wave of two CTAs per SM that an isolated launch prefers: inside the concurrent chunk graph a
+        // layer shares the GPU with update kernels and other stages' layers, and the smaller grid left
+        // them room — C5 fp32 +2.5 % over the full wave (S = 9 -> 3 at 4096 outputs;
+        // profiles/r2/split_bench.txt)
+        int S = 96 / g.mtiles;
         if (S > 16) S = 16;
         if (S > g.katoms) S = g.katoms;
         if (S < 1) S = 1;
