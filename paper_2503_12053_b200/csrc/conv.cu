@@ -869,11 +869,12 @@ size_t conv_plan(ConvArgs& a, int mode, size_t max_partial) {
         const long long mt = (long long)((a.M + 127) / 128) * ((a.N + 127) / 128);
         // one CTA per SM (544 threads): split K only as far as the tiles stay one wave
         // (splitting a multi-wave grid adds the partial traffic and buys nothing)
-        // 3xTF32: half a wave of one CTA per SM — inside the concurrent chunk graph the other stages'
-        // convolutions run beside it (C3 4,155 -> 4,310 samples/s against a full wave of 148;
-        // profiles/r2/c3_wave.txt)
+        // half a wave of the resident CTAs (3xTF32: one per SM -> 74; tf32 / bf16 modes: two per SM
+        // -> 148): inside the concurrent chunk graph the other stages' convolutions run beside it
+        // (C3 fp32 4,155 -> 4,310, tf32 5,204 -> 6,087 samples/s against a full wave;
+        // profiles/r2/c3_wave.txt, profiles/r2/c3_wave_tf32.txt)
         static const char* wave_env = std::getenv("FERRET_CONV_WAVE");
-        const long long wave = wave_env ? std::atoll(wave_env) : (a.tc == 3 ? 74 : 296);
+        const long long wave = wave_env ? std::atoll(wave_env) : (a.tc == 3 ? 74 : 148);
         long long sp = std::max<long long>(1, wave / mt);
         sp = std::min<long long>(sp, std::max<long long>(1, katoms / 2));
         if (const char* ms = std::getenv("FERRET_CONV_MAX_SPLITS"))  // experiment knob
